@@ -1,0 +1,793 @@
+// gbmw_host.cpp — C ABI, validation, host-side problem set-up and chunk scheduling
+// of the Galvatron-BMW stage search (see include/gbmw.h and DESIGN.md).
+//
+// The host does the O(L + S) per-problem bookkeeping the reference does in Python
+// before its tables (dpsearch.py:103-125: argument checks, usable-strategy filter,
+// unit fusion) plus the (data, tp) class map the device formulation needs, lays
+// problems out in a chunk workspace, and issues the K1..K4 launches on the
+// context's stream.  All fp64 cost arithmetic lives in costmodel.cuh.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/gbmw.h"
+#include "costmodel.cuh"
+#include "gbmw_internal.h"
+
+using namespace gbmw;
+
+namespace {
+
+thread_local std::string g_err;
+
+constexpr double kTwo53 = 9007199254740992.0;
+constexpr int64_t kTwo53i = 9007199254740992LL;
+
+bool is_pow2(int64_t n) { return n >= 1 && (n & (n - 1)) == 0; }
+
+int set_err(std::string *dst, int code, const std::string &msg) {
+    if (dst) *dst = msg;
+    g_err = msg;
+    return code;
+}
+
+size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+// |a*b| < 2^53 with no overflow in the test itself
+bool prod_exact(int64_t a, int64_t b) {
+    if (a < 0 || b < 0) return false;
+    if (a == 0 || b == 0) return true;
+    return (double)a * (double)b < kTwo53 * 0.5;   // margin for rounding of the test
+}
+
+struct HostProb {
+    int status = GBMW_OK;
+    bool gpu = false;              // has device work
+    std::vector<int32_t> cand, cand_cls, cls_d, cls_t, unit_first, unit_count;
+    int U = 0, S = 0, K = 0;
+    int64_t n_b = 0;
+    int64_t plan_off = 0, frontier_off = -1;
+    // workspace footprint (elements)
+    int64_t n_cells = 0, n_r = 0, n_bcells = 0, n_par = 0, n_tiles = 0, n_step_tiles = 0;
+    size_t ws_bytes = 0;
+};
+
+struct Chunk {
+    std::vector<int> probs;        // host problem indices, sorted by U descending
+    std::vector<int64_t> step_prefix;
+    std::vector<int> n_active;     // per u (index u), problems with U > u
+    int Umax = 0, max_k = 1;
+    int64_t n_cells = 0, n_r = 0, n_bcells = 0, n_par = 0, n_tiles = 0;
+    size_t small_off = 0;          // byte offset of this chunk's descriptor block in the arena
+    // offsets inside the descriptor block
+    size_t o_probs, o_cellp, o_rp, o_stepp, o_sweepp, o_cand, o_ccls, o_clsd, o_clst, o_uf, o_uc;
+    size_t small_bytes = 0;
+    size_t ws_bytes = 0;
+    cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    int launches = 0;
+};
+
+}  // namespace
+
+struct gbmw_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    uint64_t workspace_limit = 0;
+    void *ws = nullptr;
+    size_t ws_size = 0;
+    std::string err;
+};
+
+struct gbmw_batch {
+    std::vector<gbmw_layer> layers;
+    std::vector<gbmw_strategy> strats;
+    std::vector<gbmw_env> envs;
+    std::vector<gbmw_problem> problems;
+    std::vector<HostProb> hp;
+    std::vector<Chunk> chunks;
+    int64_t total_plan = 0, total_frontier = 0;
+    // device arena: inputs | chunk descriptor blocks | outputs
+    void *arena = nullptr;
+    size_t arena_size = 0;
+    size_t o_layers = 0, o_strats = 0, o_envs = 0, o_results = 0, o_plans = 0, o_frontier = 0;
+    size_t max_ws = 0;
+    gbmw_timing timing{};
+    bool ran = false;
+};
+
+// ----------------------------------------------------------------------------- misc
+extern "C" const char *gbmw_version(void) { return "gbmw 0.1.0 (sm_100a)"; }
+extern "C" int gbmw_abi_version(void) { return GBMW_ABI_VERSION; }
+extern "C" void gbmw_limits(int32_t *max_units, int32_t *max_classes, int32_t *max_strategies) {
+    if (max_units) *max_units = kMaxUnits;
+    if (max_classes) *max_classes = kMaxClasses;
+    if (max_strategies) *max_strategies = kMaxStrats;
+}
+extern "C" const char *gbmw_last_error(const gbmw_ctx *ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
+extern "C" const char *gbmw_last_error_global(void) { return g_err.c_str(); }
+extern "C" void *gbmw_ctx_stream(const gbmw_ctx *ctx) { return ctx ? (void *)ctx->stream : nullptr; }
+
+// ----------------------------------------------------------------------------- enumeration
+// strategies.py:149-200 — ordered power-of-two factorisations of G = N/P into <= 3
+// levels, injective paradigm labels in itertools.permutations order, x {ckpt off, on},
+// sorted by (n_levels, paradigm names, degrees, ckpt); prune drops dp>1 and sdp>1.
+namespace {
+void factor_seqs(int64_t rem, std::vector<int32_t> &prefix, std::vector<std::vector<int32_t>> &out) {
+    if (rem == 1) { out.push_back(prefix); return; }
+    if (prefix.size() >= 3) return;
+    for (int64_t f = 2; f <= rem; f *= 2) {
+        if (rem % f == 0) {
+            prefix.push_back((int32_t)f);
+            factor_seqs(rem / f, prefix, out);
+            prefix.pop_back();
+        }
+    }
+}
+
+const int kPerm1[3][1] = {{0}, {1}, {2}};
+const int kPerm2[6][2] = {{0, 1}, {0, 2}, {1, 0}, {1, 2}, {2, 0}, {2, 1}};
+const int kPerm3[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+
+bool sort_key_less(const gbmw_strategy &a, const gbmw_strategy &b) {
+    if (a.n_levels != b.n_levels) return a.n_levels < b.n_levels;
+    for (int l = 0; l < a.n_levels; ++l)   // "dp" < "sdp" < "tp" as strings == index order
+        if (a.paradigm[l] != b.paradigm[l]) return a.paradigm[l] < b.paradigm[l];
+    for (int l = 0; l < a.n_levels; ++l)
+        if (a.degree[l] != b.degree[l]) return a.degree[l] < b.degree[l];
+    return a.ckpt < b.ckpt;
+}
+}  // namespace
+
+extern "C" int gbmw_enumerate(int64_t n_devices, int64_t pp_degree, int32_t prune, gbmw_strategy *out,
+                              int32_t capacity, int32_t *count) {
+    if (!is_pow2(n_devices))
+        return set_err(nullptr, GBMW_EINVAL, "device count must be a power of two, got " + std::to_string(n_devices));
+    if (!is_pow2(pp_degree))
+        return set_err(nullptr, GBMW_EINVAL, "pipeline degree must be a power of two, got " + std::to_string(pp_degree));
+    if (pp_degree > n_devices || n_devices % pp_degree != 0)
+        return set_err(nullptr, GBMW_EINVAL, "pipeline degree " + std::to_string(pp_degree) +
+                                                 " does not divide device count " + std::to_string(n_devices));
+    const int64_t group = n_devices / pp_degree;
+    std::vector<std::vector<int32_t>> seqs;
+    std::vector<int32_t> prefix;
+    if (group == 1) seqs.push_back({});
+    else factor_seqs(group, prefix, seqs);
+    std::vector<gbmw_strategy> all;
+    for (const auto &f : seqs) {
+        const int k = (int)f.size();
+        const int nperm = (k == 0) ? 1 : (k == 1 ? 3 : 6);
+        for (int pi = 0; pi < nperm; ++pi) {
+            for (int ck = 0; ck < 2; ++ck) {
+                gbmw_strategy s;
+                std::memset(&s, 0, sizeof(s));
+                s.pp_degree = (int32_t)pp_degree;
+                s.n_levels = k;
+                for (int l = 0; l < k; ++l) {
+                    s.paradigm[l] = (k == 1) ? kPerm1[pi][l] : (k == 2 ? kPerm2[pi][l] : kPerm3[pi][l]);
+                    s.degree[l] = f[l];
+                }
+                s.ckpt = ck;
+                all.push_back(s);
+            }
+        }
+    }
+    std::stable_sort(all.begin(), all.end(), sort_key_less);
+    std::vector<gbmw_strategy> keep;
+    for (const auto &s : all) {
+        if (prune) {
+            const StratDeg d = strat_degrees(s);
+            if (d.dp > 1 && d.sdp > 1) continue;
+        }
+        keep.push_back(s);
+    }
+    if (count) *count = (int32_t)keep.size();
+    if (out) {
+        if ((int64_t)keep.size() > capacity) return set_err(nullptr, GBMW_EINVAL, "enumerate: output capacity too small");
+        std::memcpy(out, keep.data(), keep.size() * sizeof(gbmw_strategy));
+    }
+    return GBMW_OK;
+}
+
+// ----------------------------------------------------------------------------- scalar costs
+namespace {
+int check_strategy(const gbmw_strategy &s, std::string *err) {
+    if (s.n_levels < 0 || s.n_levels > 3) return set_err(err, GBMW_EINVAL, "strategy has more than 3 levels");
+    if (s.pp_degree < 1) return set_err(err, GBMW_EINVAL, "strategy pipeline degree must be >= 1");
+    for (int l = 0; l < s.n_levels; ++l) {
+        if (s.paradigm[l] < 0 || s.paradigm[l] > 2) return set_err(err, GBMW_EINVAL, "strategy has an unknown paradigm");
+        if (s.degree[l] < 1) return set_err(err, GBMW_EINVAL, "strategy level degree must be >= 1");
+    }
+    return GBMW_OK;
+}
+int check_layer(const gbmw_layer &L, std::string *err) {
+    if (L.param_bytes < 0 || L.param_bytes >= kTwo53i || L.bnd_bytes_per_sample < 0 ||
+        L.bnd_bytes_per_sample >= kTwo53i || L.int_bytes_per_sample < 0 || L.int_bytes_per_sample >= kTwo53i)
+        return set_err(err, GBMW_ERANGE, "layer byte counts must lie in [0, 2^53)");
+    return GBMW_OK;
+}
+}  // namespace
+
+extern "C" int gbmw_layer_cost(const gbmw_layer *layer, const gbmw_strategy *s, const gbmw_env *env,
+                               int64_t micro_batch, int32_t stage_index, int32_t n_micro, double *out) {
+    if (!layer || !s || !env || !out) return set_err(nullptr, GBMW_EINVAL, "null argument");
+    int rc = check_strategy(*s, nullptr);
+    if (rc) return rc;
+    if ((rc = check_layer(*layer, nullptr))) return rc;
+    const StratDeg d = strat_degrees(*s);
+    if (micro_batch % d.data != 0)
+        return set_err(nullptr, GBMW_EMICRO, "micro-batch " + std::to_string(micro_batch) +
+                                                 " is not divisible by the DP*SDP degree " + std::to_string(d.data));
+    if (stage_index < 1 || stage_index > s->pp_degree)
+        return set_err(nullptr, GBMW_ESTAGE, "stage_index " + std::to_string(stage_index) + " out of range 1.." +
+                                                 std::to_string(s->pp_degree));
+    if (n_micro < 1) return set_err(nullptr, GBMW_ESTAGE, "n_micro must be >= 1, got " + std::to_string(n_micro));
+    double t, t_ns;
+    layer_times(*layer, *s, d, micro_batch, *env, &t, &t_ns);
+    const Mem m = layer_memory(*layer, d, micro_batch, stage_index, n_micro, env->ms_bytes_per_param_byte);
+    out[0] = t; out[1] = t_ns; out[2] = m.o_f; out[3] = m.o_b; out[4] = m.o_ms;
+    return GBMW_OK;
+}
+
+extern "C" int gbmw_comm_breakdown(const gbmw_layer *layer, const gbmw_strategy *s, const gbmw_env *env,
+                                   int64_t micro_batch, double *out) {
+    if (!layer || !s || !env || !out) return set_err(nullptr, GBMW_EINVAL, "null argument");
+    int rc = check_strategy(*s, nullptr);
+    if (rc) return rc;
+    const StratDeg d = strat_degrees(*s);
+    const Comm c = comm_breakdown(*layer, *s, d, micro_batch, *env);
+    out[0] = c.grad; out[1] = c.fwd_act; out[2] = c.bwd_act; out[3] = c.ckpt_act;
+    return GBMW_OK;
+}
+
+extern "C" int gbmw_transform_cost(const gbmw_layer *layer, const gbmw_strategy *prev, const gbmw_strategy *cur,
+                                   int64_t micro_batch, const gbmw_env *env, double *out) {
+    if (!layer || !cur || !env || !out) return set_err(nullptr, GBMW_EINVAL, "null argument");
+    if (!prev) { *out = 0.0; return GBMW_OK; }
+    const StratDeg a = strat_degrees(*prev), b = strat_degrees(*cur);
+    *out = transform_cost(layer->bnd_bytes_per_sample, a.data, a.tp, b.data, b.tp, micro_batch, env->intra_island_bw);
+    return GBMW_OK;
+}
+
+// ----------------------------------------------------------------------------- ctx
+extern "C" int gbmw_ctx_create(int32_t device, uint64_t workspace_bytes, gbmw_ctx **out) {
+    if (!out) return set_err(nullptr, GBMW_EINVAL, "null out");
+    *out = nullptr;
+    int dev = device;
+    cudaError_t ce;
+    if (dev < 0) {
+        ce = cudaGetDevice(&dev);
+        if (ce != cudaSuccess) return set_err(nullptr, GBMW_ECUDA, std::string("cudaGetDevice: ") + cudaGetErrorString(ce));
+    }
+    ce = cudaSetDevice(dev);
+    if (ce != cudaSuccess) return set_err(nullptr, GBMW_ECUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(ce));
+    gbmw_ctx *c = new gbmw_ctx();
+    c->device = dev;
+    ce = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (ce != cudaSuccess) {
+        delete c;
+        return set_err(nullptr, GBMW_ECUDA, std::string("cudaStreamCreate: ") + cudaGetErrorString(ce));
+    }
+    if (workspace_bytes == 0) {
+        size_t fr = 0, tot = 0;
+        cudaMemGetInfo(&fr, &tot);
+        workspace_bytes = std::min<uint64_t>((uint64_t)(fr * 0.4), 32ull << 30);
+        if (workspace_bytes < (64ull << 20)) workspace_bytes = 64ull << 20;
+    }
+    c->workspace_limit = workspace_bytes;
+    *out = c;
+    return GBMW_OK;
+}
+
+extern "C" int gbmw_ctx_destroy(gbmw_ctx *ctx) {
+    if (!ctx) return GBMW_OK;
+    cudaSetDevice(ctx->device);
+    if (ctx->ws) cudaFree(ctx->ws);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+    return GBMW_OK;
+}
+
+// ----------------------------------------------------------------------------- batch set-up
+namespace {
+
+// dp_search argument checks and host bookkeeping (dpsearch.py:103-125, :42-43, :71-86)
+void prepare_problem(gbmw_batch &b, int pi, std::string *err) {
+    const gbmw_problem &P = b.problems[pi];
+    HostProb &h = b.hp[pi];
+    auto fail = [&](int code, const std::string &msg) { h.status = code; set_err(err, code, msg); };
+    if (P.granularity_bytes <= 0) return fail(GBMW_EINVAL_GRAN, "granularity_bytes must be positive, got " + std::to_string(P.granularity_bytes));
+    if (!(P.budget_bytes >= 0.0)) return fail(GBMW_EINVAL_BUDGET, "budget_bytes must be non-negative");
+    if (P.n_layers <= 0) return fail(GBMW_EEMPTY, "stage must contain at least one layer");
+    if (P.micro_batch < 1) return fail(GBMW_EMICRO, "micro-batch must be >= 1, got " + std::to_string(P.micro_batch));
+    if (P.n_buckets < 0) return fail(GBMW_EINVAL, "n_buckets must be non-negative");
+    if (P.n_buckets > GBMW_MAX_BUCKETS)
+        return fail(GBMW_EBUCKETS, "budget/granularity yields " + std::to_string(P.n_buckets) + " buckets (> " +
+                                       std::to_string(GBMW_MAX_BUCKETS) + "); increase the memory granularity");
+    if (P.layer_begin < 0 || (int64_t)P.layer_begin + P.n_layers > (int64_t)b.layers.size())
+        return fail(GBMW_EINVAL, "problem layer range out of bounds");
+    if (P.strat_begin < 0 || P.n_strats < 0 || (int64_t)P.strat_begin + P.n_strats > (int64_t)b.strats.size())
+        return fail(GBMW_EINVAL, "problem strategy range out of bounds");
+    if (P.env_index < 0 || P.env_index >= (int)b.envs.size()) return fail(GBMW_EINVAL, "problem env index out of bounds");
+    if (P.budget_bytes >= kTwo53) return fail(GBMW_ERANGE, "budget_bytes must be < 2^53");
+    h.n_b = P.n_buckets;
+    for (int i = 0; i < P.n_strats; ++i) {
+        const gbmw_strategy &s = b.strats[P.strat_begin + i];
+        int rc = check_strategy(s, err);
+        if (rc) { h.status = rc; return; }
+        const StratDeg d = strat_degrees(s);
+        if (P.micro_batch % d.data == 0) h.cand.push_back(P.strat_begin + i);
+    }
+    h.S = (int)h.cand.size();
+    if (h.S == 0 || h.n_b == 0) return;    // infeasible, dpsearch.py:119-121
+    for (int i = 0; i < P.n_layers; ++i) {
+        int rc = check_layer(b.layers[P.layer_begin + i], err);
+        if (rc) { h.status = rc; return; }
+    }
+    // layer_memory range checks (costs.py:207-210), raised on the first table cell
+    for (int32_t gi : h.cand) {
+        const gbmw_strategy &s = b.strats[gi];
+        if (P.stage_index < 1 || P.stage_index > s.pp_degree)
+            return fail(GBMW_ESTAGE, "stage_index " + std::to_string(P.stage_index) + " out of range 1.." + std::to_string(s.pp_degree));
+        if (P.n_micro < 1) return fail(GBMW_ESTAGE, "n_micro must be >= 1, got " + std::to_string(P.n_micro));
+    }
+    // exactness of Python int arithmetic in fp64
+    int64_t max_stash = 1;
+    for (int32_t gi : h.cand) max_stash = std::max<int64_t>(max_stash, (int64_t)b.strats[gi].pp_degree);
+    max_stash = std::min<int64_t>(max_stash, std::max<int32_t>(1, P.n_micro));
+    for (int i = 0; i < P.n_layers; ++i) {
+        const gbmw_layer &L = b.layers[P.layer_begin + i];
+        if (!prod_exact(L.bnd_bytes_per_sample, P.micro_batch) ||
+            !prod_exact(L.bnd_bytes_per_sample * (P.micro_batch), max_stash) ||
+            !prod_exact(L.int_bytes_per_sample, P.micro_batch))
+            return fail(GBMW_ERANGE, "byte products of layer " + std::to_string(i) + " reach 2^53; fp64 would not be exact");
+    }
+    if (h.S > kMaxStrats || h.S > 65535) return fail(GBMW_ENOTSUP, "more than " + std::to_string(kMaxStrats) + " usable strategies");
+    // (data, tp) classes in first-appearance order
+    for (int32_t gi : h.cand) {
+        const StratDeg d = strat_degrees(b.strats[gi]);
+        int k = -1;
+        for (int c = 0; c < (int)h.cls_d.size(); ++c)
+            if (h.cls_d[c] == d.data && h.cls_t[c] == d.tp) { k = c; break; }
+        if (k < 0) { k = (int)h.cls_d.size(); h.cls_d.push_back(d.data); h.cls_t.push_back(d.tp); }
+        h.cand_cls.push_back(k);
+    }
+    h.K = (int)h.cls_d.size();
+    if (h.K > kMaxClasses) return fail(GBMW_ENOTSUP, "more than " + std::to_string(kMaxClasses) + " (data, tp) classes");
+    // units (dpsearch.py:71-86): fusion key (kind, param, bnd, int, raw fwd_time, frac)
+    const bool fuse = (P.flags & GBMW_FUSE) != 0;
+    for (int i = 0; i < P.n_layers; ++i) {
+        const int gl = P.layer_begin + i;
+        if (fuse && !h.unit_first.empty()) {
+            const gbmw_layer &A = b.layers[h.unit_first.back()];
+            const gbmw_layer &B = b.layers[gl];
+            if (A.kind_id == B.kind_id && A.param_bytes == B.param_bytes &&
+                A.bnd_bytes_per_sample == B.bnd_bytes_per_sample && A.int_bytes_per_sample == B.int_bytes_per_sample &&
+                A.fwd_time_raw == B.fwd_time_raw && A.tp_act_replication_fraction == B.tp_act_replication_fraction) {
+                h.unit_count.back() += 1;
+                continue;
+            }
+        }
+        h.unit_first.push_back(gl);
+        h.unit_count.push_back(1);
+    }
+    h.U = (int)h.unit_first.size();
+    if (h.U > kMaxUnits) return fail(GBMW_ENOTSUP, "more than " + std::to_string(kMaxUnits) + " units in one stage");
+    const int64_t n_e = h.n_b + 1;
+    h.n_cells = (int64_t)h.U * h.S;
+    h.n_r = (int64_t)h.U * h.K * h.K;
+    h.n_bcells = (h.U > 1) ? (int64_t)h.K * n_e : 0;
+    h.n_par = (int64_t)(h.U - 1) * h.K * n_e;
+    h.n_tiles = (h.n_b + kSweepThreads - 1) / kSweepThreads;
+    h.n_step_tiles = (n_e + kStepThreads - 1) / kStepThreads;
+    h.ws_bytes = (size_t)h.n_cells * (sizeof(Cell) + sizeof(CellMem)) + (size_t)h.n_r * 8 + 8 +
+                 (size_t)h.n_bcells * 32 + (size_t)h.n_par * 2 + (size_t)h.n_tiles * sizeof(SweepPartial);
+    h.gpu = true;
+}
+
+template <class T>
+size_t put(std::vector<char> &blob, const T *src, size_t n) {
+    const size_t off = align_up(blob.size(), 16);
+    blob.resize(off + n * sizeof(T));
+    if (n) std::memcpy(blob.data() + off, src, n * sizeof(T));
+    return off;
+}
+
+// chunk workspace layout (byte offsets from ws base)
+struct WsLayout {
+    size_t cells, cmem, rcls, bup, tb0, tb1, fb0, fb1, par, parts, total;
+};
+WsLayout ws_layout(const Chunk &c) {
+    WsLayout w;
+    size_t o = 0;
+    w.cells = o; o = align_up(o + c.n_cells * sizeof(Cell));
+    w.cmem = o; o = align_up(o + c.n_cells * sizeof(CellMem));
+    w.rcls = o; o = align_up(o + c.n_r * 8);
+    w.bup = o; o = align_up(o + c.probs.size() * 8);
+    w.tb0 = o; o = align_up(o + c.n_bcells * 8);
+    w.tb1 = o; o = align_up(o + c.n_bcells * 8);
+    w.fb0 = o; o = align_up(o + c.n_bcells * 8);
+    w.fb1 = o; o = align_up(o + c.n_bcells * 8);
+    w.par = o; o = align_up(o + c.n_par * 2);
+    w.parts = o; o = align_up(o + c.n_tiles * sizeof(SweepPartial));
+    w.total = o;
+    return w;
+}
+
+}  // namespace
+
+extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_t n_layers,
+                                 const gbmw_strategy *strategies, int64_t n_strategies, const gbmw_env *envs,
+                                 int64_t n_envs, const gbmw_problem *problems, int64_t n_problems, gbmw_batch **out) {
+    if (!ctx || !out) return set_err(nullptr, GBMW_EINVAL, "null ctx/out");
+    *out = nullptr;
+    if (n_problems < 0 || n_layers < 0 || n_strategies < 0 || n_envs < 0)
+        return set_err(&ctx->err, GBMW_EINVAL, "negative array length");
+    gbmw_batch *b = new gbmw_batch();
+    b->layers.assign(layers, layers + n_layers);
+    b->strats.assign(strategies, strategies + n_strategies);
+    b->envs.assign(envs, envs + n_envs);
+    b->problems.assign(problems, problems + n_problems);
+    b->hp.resize(n_problems);
+    int first_err = GBMW_OK;
+    std::string first_msg;
+    for (int64_t i = 0; i < n_problems; ++i) {
+        std::string msg;
+        prepare_problem(*b, (int)i, &msg);
+        if (b->hp[i].status != GBMW_OK && first_err == GBMW_OK) { first_err = b->hp[i].status; first_msg = msg; }
+    }
+    // output offsets
+    int64_t plan = 0, front = 0;
+    for (int64_t i = 0; i < n_problems; ++i) {
+        HostProb &h = b->hp[i];
+        h.plan_off = plan;
+        plan += std::max<int32_t>(0, b->problems[i].n_layers);
+        if (h.gpu && (b->problems[i].flags & GBMW_FRONTIER)) { h.frontier_off = front; front += h.n_b; }
+    }
+    b->total_plan = plan;
+    b->total_frontier = front;
+    // greedy chunking by workspace budget
+    const size_t limit = ctx->workspace_limit;
+    Chunk cur;
+    size_t cur_bytes = 0;
+    auto flush = [&]() {
+        if (cur.probs.empty()) return;
+        b->chunks.push_back(cur);
+        cur = Chunk();
+        cur_bytes = 0;
+    };
+    for (int64_t i = 0; i < n_problems; ++i) {
+        HostProb &h = b->hp[i];
+        if (!h.gpu) continue;
+        const size_t need = h.ws_bytes + 16 * 256;
+        if (need > limit) {
+            h.status = GBMW_ENOMEM;
+            h.gpu = false;
+            if (first_err == GBMW_OK) { first_err = GBMW_ENOMEM; first_msg = "one stage search needs more workspace than the context limit"; }
+            continue;
+        }
+        if (cur_bytes + need > limit) flush();
+        cur.probs.push_back((int)i);
+        cur_bytes += need;
+    }
+    flush();
+    // per-chunk descriptors
+    std::vector<char> blob;
+    for (Chunk &c : b->chunks) {
+        std::stable_sort(c.probs.begin(), c.probs.end(), [&](int x, int y) { return b->hp[x].U > b->hp[y].U; });
+        std::vector<DevProblem> dps;
+        std::vector<int64_t> cellp{0}, rp{0}, stepp{0}, sweepp{0};
+        std::vector<int32_t> cand, ccls, clsd, clst, uf, uc;
+        for (int pi : c.probs) {
+            const HostProb &h = b->hp[pi];
+            const gbmw_problem &P = b->problems[pi];
+            DevProblem d;
+            std::memset(&d, 0, sizeof(d));
+            d.U = h.U; d.S = h.S; d.K = h.K; d.flags = P.flags;
+            d.n_layers = P.n_layers; d.stage_index = P.stage_index; d.n_micro = P.n_micro; d.env_index = P.env_index;
+            d.n_b = h.n_b; d.micro = P.micro_batch; d.gran = P.granularity_bytes; d.budget = P.budget_bytes;
+            d.cell_off = c.n_cells; d.r_off = c.n_r; d.b_off = c.n_bcells; d.par_off = c.n_par; d.tile_off = c.n_tiles;
+            d.plan_off = h.plan_off; d.frontier_off = h.frontier_off;
+            d.cand_off = (int32_t)cand.size(); d.class_off = (int32_t)clsd.size(); d.unit_off = (int32_t)uf.size();
+            d.layer_begin = P.layer_begin; d.strat_begin = P.strat_begin; d.result_index = pi;
+            d.n_sweep_tiles = (int32_t)h.n_tiles;
+            dps.push_back(d);
+            c.n_cells += h.n_cells; c.n_r += h.n_r; c.n_bcells += h.n_bcells; c.n_par += h.n_par; c.n_tiles += h.n_tiles;
+            cellp.push_back(c.n_cells); rp.push_back(c.n_r);
+            stepp.push_back(stepp.back() + h.n_step_tiles);
+            sweepp.push_back(c.n_tiles);
+            cand.insert(cand.end(), h.cand.begin(), h.cand.end());
+            ccls.insert(ccls.end(), h.cand_cls.begin(), h.cand_cls.end());
+            clsd.insert(clsd.end(), h.cls_d.begin(), h.cls_d.end());
+            clst.insert(clst.end(), h.cls_t.begin(), h.cls_t.end());
+            uf.insert(uf.end(), h.unit_first.begin(), h.unit_first.end());
+            uc.insert(uc.end(), h.unit_count.begin(), h.unit_count.end());
+            c.Umax = std::max(c.Umax, h.U);
+            c.max_k = std::max(c.max_k, h.K);
+        }
+        c.step_prefix = stepp;
+        c.n_active.assign(c.Umax + 1, 0);
+        for (int u = 0; u <= c.Umax; ++u) {
+            int n = 0;
+            for (int pi : c.probs) if (b->hp[pi].U > u) ++n;
+            c.n_active[u] = n;
+        }
+        const size_t base = align_up(blob.size(), 256);
+        blob.resize(base);
+        c.small_off = base;
+        c.o_probs = put(blob, dps.data(), dps.size()) - base;
+        c.o_cellp = put(blob, cellp.data(), cellp.size()) - base;
+        c.o_rp = put(blob, rp.data(), rp.size()) - base;
+        c.o_stepp = put(blob, stepp.data(), stepp.size()) - base;
+        c.o_sweepp = put(blob, sweepp.data(), sweepp.size()) - base;
+        c.o_cand = put(blob, cand.data(), cand.size()) - base;
+        c.o_ccls = put(blob, ccls.data(), ccls.size()) - base;
+        c.o_clsd = put(blob, clsd.data(), clsd.size()) - base;
+        c.o_clst = put(blob, clst.data(), clst.size()) - base;
+        c.o_uf = put(blob, uf.data(), uf.size()) - base;
+        c.o_uc = put(blob, uc.data(), uc.size()) - base;
+        c.small_bytes = blob.size() - base;
+        c.ws_bytes = ws_layout(c).total;
+        b->max_ws = std::max(b->max_ws, c.ws_bytes);
+    }
+    // arena: inputs | descriptor blob | outputs
+    size_t o = 0;
+    b->o_layers = o; o = align_up(o + b->layers.size() * sizeof(gbmw_layer));
+    b->o_strats = o; o = align_up(o + b->strats.size() * sizeof(gbmw_strategy));
+    b->o_envs = o; o = align_up(o + b->envs.size() * sizeof(gbmw_env));
+    const size_t o_blob = o; o = align_up(o + blob.size());
+    b->o_results = o; o = align_up(o + b->problems.size() * sizeof(gbmw_result));
+    b->o_plans = o; o = align_up(o + (size_t)b->total_plan * sizeof(int32_t));
+    b->o_frontier = o; o = align_up(o + (size_t)b->total_frontier * sizeof(double));
+    b->arena_size = std::max<size_t>(o, 256);
+    for (Chunk &c : b->chunks) c.small_off += o_blob;
+    cudaSetDevice(ctx->device);
+    cudaError_t ce = cudaMalloc(&b->arena, b->arena_size);
+    if (ce != cudaSuccess) {
+        delete b;
+        return set_err(&ctx->err, GBMW_ENOMEM, std::string("cudaMalloc(arena): ") + cudaGetErrorString(ce));
+    }
+    // one staged upload of the input part of the arena
+    std::vector<char> host(o_blob + blob.size());
+    if (!b->layers.empty()) std::memcpy(host.data() + b->o_layers, b->layers.data(), b->layers.size() * sizeof(gbmw_layer));
+    if (!b->strats.empty()) std::memcpy(host.data() + b->o_strats, b->strats.data(), b->strats.size() * sizeof(gbmw_strategy));
+    if (!b->envs.empty()) std::memcpy(host.data() + b->o_envs, b->envs.data(), b->envs.size() * sizeof(gbmw_env));
+    if (!blob.empty()) std::memcpy(host.data() + o_blob, blob.data(), blob.size());
+    ce = cudaMemcpyAsync(b->arena, host.data(), host.size(), cudaMemcpyHostToDevice, ctx->stream);
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(ctx->stream);
+    b->timing.h2d_bytes = (double)host.size();
+    if (ce != cudaSuccess) {
+        cudaFree(b->arena);
+        delete b;
+        return set_err(&ctx->err, GBMW_ECUDA, std::string("upload: ") + cudaGetErrorString(ce));
+    }
+    // algorithmic work counters
+    for (int64_t i = 0; i < n_problems; ++i) {
+        const HostProb &h = b->hp[i];
+        if (!h.gpu) continue;
+        const double rows = (double)(h.U - 1) * (double)(h.n_b + 1);
+        b->timing.transitions += rows * h.S * h.S;
+        b->timing.row_steps += rows;
+        b->timing.dp_cells += rows * h.S * h.K;
+        // K2 compulsory bytes: B_{u-1} (T,F) read once + B_u written + argmin written
+        b->timing.dp_bytes += rows * h.K * (16.0 + 16.0 + 2.0);
+    }
+    b->timing.n_chunks = (int32_t)b->chunks.size();
+    *out = b;
+    if (first_err != GBMW_OK) set_err(&ctx->err, first_err, first_msg);
+    return first_err;
+}
+
+namespace {
+int ensure_ws(gbmw_ctx *ctx, size_t bytes) {
+    if (bytes <= ctx->ws_size) return GBMW_OK;
+    if (ctx->ws) { cudaFree(ctx->ws); ctx->ws = nullptr; ctx->ws_size = 0; }
+    cudaError_t ce = cudaMalloc(&ctx->ws, bytes);
+    if (ce != cudaSuccess) return set_err(&ctx->err, GBMW_ENOMEM, std::string("cudaMalloc(workspace): ") + cudaGetErrorString(ce));
+    ctx->ws_size = bytes;
+    return GBMW_OK;
+}
+
+ChunkArgs chunk_args(gbmw_batch *b, const Chunk &c, char *ws) {
+    char *arena = (char *)b->arena;
+    char *sm = arena + c.small_off;
+    ChunkArgs a;
+    a.layers = (const gbmw_layer *)(arena + b->o_layers);
+    a.strats = (const gbmw_strategy *)(arena + b->o_strats);
+    a.envs = (const gbmw_env *)(arena + b->o_envs);
+    a.probs = (const DevProblem *)(sm + c.o_probs);
+    a.n_probs = (int32_t)c.probs.size();
+    a.max_k = c.max_k;
+    a.cell_prefix = (const int64_t *)(sm + c.o_cellp);
+    a.r_prefix = (const int64_t *)(sm + c.o_rp);
+    a.step_tiles = (const int64_t *)(sm + c.o_stepp);
+    a.sweep_tiles = (const int64_t *)(sm + c.o_sweepp);
+    a.cand_strat = (const int32_t *)(sm + c.o_cand);
+    a.cand_cls = (const int32_t *)(sm + c.o_ccls);
+    a.class_d = (const int32_t *)(sm + c.o_clsd);
+    a.class_t = (const int32_t *)(sm + c.o_clst);
+    a.unit_first = (const int32_t *)(sm + c.o_uf);
+    a.unit_count = (const int32_t *)(sm + c.o_uc);
+    const WsLayout w = ws_layout(c);
+    a.cells = (Cell *)(ws + w.cells);
+    a.cmem = (CellMem *)(ws + w.cmem);
+    a.rcls = (double *)(ws + w.rcls);
+    a.bup = (unsigned long long *)(ws + w.bup);
+    a.Tb[0] = (double *)(ws + w.tb0);
+    a.Tb[1] = (double *)(ws + w.tb1);
+    a.Fb[0] = (double *)(ws + w.fb0);
+    a.Fb[1] = (double *)(ws + w.fb1);
+    a.par = (uint16_t *)(ws + w.par);
+    a.partials = (SweepPartial *)(ws + w.parts);
+    a.results = (gbmw_result *)(arena + b->o_results);
+    a.plans = (int32_t *)(arena + b->o_plans);
+    a.frontier = (double *)(arena + b->o_frontier);
+    return a;
+}
+
+int cuda_fail(gbmw_ctx *ctx, int rc, const char *what) {
+    return set_err(&ctx->err, GBMW_ECUDA, std::string(what) + ": " + cudaGetErrorString((cudaError_t)rc));
+}
+
+// Runs K1 for every chunk; with tables_only it stops there (gbmw_cost_tables).
+int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
+    cudaSetDevice(ctx->device);
+    int rc = ensure_ws(ctx, b->max_ws);
+    if (rc) return rc;
+    b->timing.total_ms = b->timing.dp_ms = b->timing.sweep_ms = b->timing.tables_ms = b->timing.finalize_ms = 0.f;
+    b->timing.n_launches = 0;
+    cudaStream_t st = ctx->stream;
+    for (Chunk &c : b->chunks) {
+        for (auto &e : c.ev)
+            if (!e) cudaEventCreate(&e);
+        ChunkArgs a = chunk_args(b, c, (char *)ctx->ws);
+        c.launches = 0;
+        cudaEventRecord(c.ev[0], st);
+        cudaMemsetAsync(a.bup, 0, c.probs.size() * 8, st);
+        if ((rc = launch_cost_tables(a, c.n_cells, c.n_r, st))) return cuda_fail(ctx, rc, "K1 launch");
+        c.launches += (c.n_cells > 0) + (c.n_r > 0);
+        cudaEventRecord(c.ev[1], st);
+        if (tables_only) continue;
+        for (int u = 1; u < c.Umax; ++u) {
+            const int na = c.n_active[u];
+            if ((rc = launch_dp_step(a, u, na, c.step_prefix[na], st))) return cuda_fail(ctx, rc, "K2 launch");
+            c.launches += 1;
+        }
+        cudaEventRecord(c.ev[2], st);
+        if ((rc = launch_sweep(a, c.n_tiles, st))) return cuda_fail(ctx, rc, "K3 launch");
+        cudaEventRecord(c.ev[3], st);
+        if ((rc = launch_finalize(a, st))) return cuda_fail(ctx, rc, "K4 launch");
+        c.launches += 2;
+        cudaEventRecord(c.ev[4], st);
+    }
+    cudaError_t ce = cudaStreamSynchronize(st);
+    if (ce != cudaSuccess) return cuda_fail(ctx, (int)ce, "search kernels");
+    for (Chunk &c : b->chunks) {
+        float t;
+        b->timing.n_launches += c.launches;
+        cudaEventElapsedTime(&t, c.ev[0], c.ev[1]); b->timing.tables_ms += t;
+        if (tables_only) continue;
+        cudaEventElapsedTime(&t, c.ev[1], c.ev[2]); b->timing.dp_ms += t;
+        cudaEventElapsedTime(&t, c.ev[2], c.ev[3]); b->timing.sweep_ms += t;
+        cudaEventElapsedTime(&t, c.ev[3], c.ev[4]); b->timing.finalize_ms += t;
+        cudaEventElapsedTime(&t, c.ev[0], c.ev[4]); b->timing.total_ms += t;
+    }
+    b->ran = true;
+    return GBMW_OK;
+}
+}  // namespace
+
+extern "C" int gbmw_batch_run(gbmw_ctx *ctx, gbmw_batch *b) {
+    if (!ctx || !b) return set_err(nullptr, GBMW_EINVAL, "null ctx/batch");
+    return run_chunks(ctx, b, false);
+}
+
+extern "C" int gbmw_batch_fetch(gbmw_ctx *ctx, gbmw_batch *b, gbmw_result *results, int32_t *plans, double *frontier) {
+    if (!ctx || !b) return set_err(nullptr, GBMW_EINVAL, "null ctx/batch");
+    if (!b->ran && !b->chunks.empty()) return set_err(&ctx->err, GBMW_EINVAL, "batch has not been run");
+    cudaSetDevice(ctx->device);
+    cudaStream_t st = ctx->stream;
+    const size_t np = b->problems.size();
+    std::vector<gbmw_result> dev_res(np);
+    cudaError_t ce = cudaSuccess;
+    if (np) ce = cudaMemcpyAsync(dev_res.data(), (char *)b->arena + b->o_results, np * sizeof(gbmw_result), cudaMemcpyDeviceToHost, st);
+    if (ce == cudaSuccess && plans && b->total_plan)
+        ce = cudaMemcpyAsync(plans, (char *)b->arena + b->o_plans, b->total_plan * sizeof(int32_t), cudaMemcpyDeviceToHost, st);
+    if (ce == cudaSuccess && frontier && b->total_frontier)
+        ce = cudaMemcpyAsync(frontier, (char *)b->arena + b->o_frontier, b->total_frontier * sizeof(double), cudaMemcpyDeviceToHost, st);
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
+    if (ce != cudaSuccess) return cuda_fail(ctx, (int)ce, "fetch");
+    b->timing.d2h_bytes = (double)(np * sizeof(gbmw_result)) + (plans ? (double)b->total_plan * 4.0 : 0.0) +
+                          (frontier ? (double)b->total_frontier * 8.0 : 0.0);
+    int first = GBMW_OK;
+    for (size_t i = 0; i < np; ++i) {
+        const HostProb &h = b->hp[i];
+        gbmw_result r;
+        if (h.gpu) {
+            r = dev_res[i];
+            r.frontier_offset = h.frontier_off;
+        } else {
+            std::memset(&r, 0, sizeof(r));
+            r.time_s = INFINITY;
+            r.e_fwd_used = 0.0;
+            r.feasible = 0;
+            r.status = h.status;
+            r.frontier_offset = -1;
+            if (plans)
+                for (int l = 0; l < std::max<int32_t>(0, b->problems[i].n_layers); ++l) plans[h.plan_off + l] = -1;
+        }
+        if (r.status != GBMW_OK && first == GBMW_OK) first = r.status;
+        if (results) results[i] = r;
+    }
+    if (first == GBMW_EINTERNAL) set_err(&ctx->err, first, "dp_search produced a plan exceeding the memory budget");
+    return first;
+}
+
+extern "C" int gbmw_batch_timing(const gbmw_batch *b, gbmw_timing *out) {
+    if (!b || !out) return set_err(nullptr, GBMW_EINVAL, "null batch/out");
+    *out = b->timing;
+    return GBMW_OK;
+}
+
+extern "C" int gbmw_batch_destroy(gbmw_batch *b) {
+    if (!b) return GBMW_OK;
+    for (Chunk &c : b->chunks)
+        for (auto &e : c.ev)
+            if (e) cudaEventDestroy(e);
+    if (b->arena) cudaFree(b->arena);
+    delete b;
+    return GBMW_OK;
+}
+
+extern "C" int gbmw_search_batch(gbmw_ctx *ctx, const gbmw_layer *layers, int64_t n_layers,
+                                 const gbmw_strategy *strategies, int64_t n_strategies, const gbmw_env *envs,
+                                 int64_t n_envs, const gbmw_problem *problems, int64_t n_problems,
+                                 gbmw_result *results, int32_t *plans, double *frontier) {
+    gbmw_batch *b = nullptr;
+    int rc = gbmw_batch_create(ctx, layers, n_layers, strategies, n_strategies, envs, n_envs, problems, n_problems, &b);
+    if (!b) return rc;
+    const int prep_rc = rc;
+    rc = gbmw_batch_run(ctx, b);
+    if (rc == GBMW_OK) rc = gbmw_batch_fetch(ctx, b, results, plans, frontier);
+    gbmw_batch_destroy(b);
+    if (rc == GBMW_OK) rc = prep_rc;
+    return rc;
+}
+
+extern "C" int gbmw_cost_tables(gbmw_ctx *ctx, const gbmw_layer *layers, int64_t n_layers,
+                                const gbmw_strategy *strategies, int64_t n_strategies, const gbmw_env *envs,
+                                int64_t n_envs, const gbmw_problem *problem, double *time_c, double *ef_true,
+                                double *o_b, int64_t *weight, int32_t *usable, int32_t *n_usable, int32_t *n_units) {
+    gbmw_batch *b = nullptr;
+    int rc = gbmw_batch_create(ctx, layers, n_layers, strategies, n_strategies, envs, n_envs, problem, 1, &b);
+    if (!b) return rc;
+    if (rc != GBMW_OK) { gbmw_batch_destroy(b); return rc; }
+    const HostProb &h = b->hp[0];
+    if (n_usable) *n_usable = h.S;
+    if (n_units) *n_units = h.U;
+    if (usable)
+        for (int i = 0; i < h.S; ++i) usable[i] = h.cand[i] - problem->strat_begin;
+    if (!h.gpu) { gbmw_batch_destroy(b); return GBMW_OK; }
+    rc = run_chunks(ctx, b, true);
+    if (rc == GBMW_OK) {
+        const Chunk &c = b->chunks[0];
+        const WsLayout w = ws_layout(c);
+        std::vector<Cell> cells(c.n_cells);
+        std::vector<CellMem> cm(c.n_cells);
+        cudaMemcpy(cells.data(), (char *)ctx->ws + w.cells, c.n_cells * sizeof(Cell), cudaMemcpyDeviceToHost);
+        cudaError_t ce = cudaMemcpy(cm.data(), (char *)ctx->ws + w.cmem, c.n_cells * sizeof(CellMem), cudaMemcpyDeviceToHost);
+        if (ce != cudaSuccess) rc = cuda_fail(ctx, (int)ce, "cost tables fetch");
+        for (int64_t x = 0; x < c.n_cells && rc == GBMW_OK; ++x) {
+            if (time_c) time_c[x] = cells[x].c;
+            if (ef_true) ef_true[x] = cells[x].ef;
+            if (o_b) o_b[x] = cm[x].o_b;
+            if (weight) weight[x] = cells[x].w;
+        }
+    }
+    gbmw_batch_destroy(b);
+    return rc;
+}

@@ -1,0 +1,103 @@
+// gbmw_internal.h — device-side data layout of one chunk of stage searches and the
+// launch entry points of gbmw_kernels.cu.  Not part of the C ABI.
+//
+// Layout.  For a problem with U units, S usable strategies,
+// K (data, tp) classes and n_e = n_buckets + 1 memory buckets:
+//   cells[U][S]        {time_c, ef_true, weight, class}        dpsearch.py:131-145
+//   cmem [U][S]        {O_f, O_b, O_ms} of one layer of the unit (E_all check)
+//   rcls [U][K][K]     transform cost between classes for unit u (dpsearch.py:149-160)
+//   Tb/Fb[2][K][n_e]   class-reduced frontier B_u (ping-pong), column-major by class
+//   par  [U-1][K][n_e] argmin strategy of B_u (uint16)
+// B_u[e'][k] = lexmin_i (T_{u-1}[e',i] + R_u[cls(i),k], F_{u-1}[e',i], i), from which
+// the reference table is T_u[e,j] = B_u[e-w_uj][cls j].t + time_c[u,j]  (exact
+// restatement of dpsearch.py:261-280: R depends on (i, j) only through their classes).
+#pragma once
+#include <stdint.h>
+#include "../../include/gbmw.h"
+
+namespace gbmw {
+
+constexpr int kMaxUnits = 1024;      // backtrack path held in local memory
+constexpr int kMaxClasses = 16;
+constexpr int kMaxStrats = 512;      // smem staging of per-strategy constants
+constexpr int kStepThreads = 256;    // rows per K2 tile
+constexpr int kSweepThreads = 256;   // rows per K3 tile
+
+struct Cell {
+    double c;       // time_c = t * count
+    double ef;      // ef_true = (O_f + O_ms) * count
+    int32_t w;      // weight = ceil(ef / gran), clamped to n_buckets + 1
+    int32_t k;      // class of the strategy
+};
+
+struct CellMem {
+    double o_f, o_b, o_ms;
+};
+
+struct DevProblem {
+    int32_t U, S, K, flags;
+    int32_t n_layers, stage_index, n_micro, env_index;
+    int64_t n_b;            // buckets; rows are e = 0 .. n_b
+    int64_t micro, gran;
+    double budget;
+    int64_t cell_off;       // into cells / cmem  (U*S)
+    int64_t r_off;          // into rcls (U*K*K)
+    int64_t b_off;          // into Tb/Fb buffers (K*n_e)
+    int64_t par_off;        // into par ((U-1)*K*n_e)
+    int64_t tile_off;       // into sweep partials (n_sweep_tiles)
+    int64_t plan_off;       // into plans (n_layers)
+    int64_t frontier_off;   // into frontier (n_b), -1 if not requested
+    int32_t cand_off;       // into cand_strat / cand_cls (S)
+    int32_t class_off;      // into class_d / class_t (K)
+    int32_t unit_off;       // into unit_first / unit_count (U)
+    int32_t layer_begin;    // global layer index of the first stage layer
+    int32_t strat_begin;    // global index of the problem's strategy list
+    int32_t result_index;   // slot in the batch result array
+    int32_t n_sweep_tiles;
+    int32_t pad_;
+};
+
+struct SweepPartial {
+    double t;
+    int64_t e;
+    int32_t j;
+    int32_t pad_;
+};
+
+// Everything a chunk's kernels read or write (device pointers).
+struct ChunkArgs {
+    const gbmw_layer *layers;
+    const gbmw_strategy *strats;
+    const gbmw_env *envs;
+    const DevProblem *probs;      // sorted by U descending
+    int32_t n_probs;
+    int32_t max_k;
+    const int64_t *cell_prefix;   // n_probs + 1
+    const int64_t *r_prefix;      // n_probs + 1
+    const int64_t *step_tiles;    // n_probs + 1, tiles of ceil(n_e / kStepThreads)
+    const int64_t *sweep_tiles;   // n_probs + 1
+    const int32_t *cand_strat;    // global strategy index
+    const int32_t *cand_cls;
+    const int32_t *class_d, *class_t;
+    const int32_t *unit_first;    // global layer index
+    const int32_t *unit_count;
+    Cell *cells;
+    CellMem *cmem;
+    double *rcls;
+    unsigned long long *bup;      // per problem, bits of max O_b (all >= 0)
+    double *Tb[2];
+    double *Fb[2];
+    uint16_t *par;
+    SweepPartial *partials;
+    gbmw_result *results;
+    int32_t *plans;
+    double *frontier;
+};
+
+// launchers (gbmw_kernels.cu); all asynchronous on `stream`, return cudaError_t as int
+int launch_cost_tables(const ChunkArgs &a, int64_t n_cells, int64_t n_r, void *stream);
+int launch_dp_step(const ChunkArgs &a, int u, int32_t n_active, int64_t n_tiles, void *stream);
+int launch_sweep(const ChunkArgs &a, int64_t n_tiles, void *stream);
+int launch_finalize(const ChunkArgs &a, void *stream);
+
+}  // namespace gbmw

@@ -1,0 +1,434 @@
+// gbmw_kernels.cu — sm_100a kernels of the Galvatron-BMW stage search.
+//
+//   K1 k_cost_cells / k_cost_r : batched cost-model tables      (dpsearch.py:127-163)
+//   K2 k_dp_step<KT>           : one min-plus layer step, all problems of the chunk
+//                                 that have that many units      (dpsearch.py:245-282)
+//   K3 k_sweep                 : E_fwd sweep + backward-peak validity + per-tile argmin
+//                                                                (dpsearch.py:174-208)
+//   K4 k_finalize              : cross-tile argmin, backtrack, plan expansion,
+//                                 stage_cost of the plan         (dpsearch.py:210-227,
+//                                                                 costs.py:289-352)
+// All fp64 arithmetic follows the reference's evaluation order; the file is built
+// with -fmad=false so no a*b+c is contracted (SURVEY.md §8 arithmetic contract).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "costmodel.cuh"
+#include "gbmw_internal.h"
+
+namespace gbmw {
+
+#define GBMW_INF __longlong_as_double(0x7ff0000000000000LL)
+
+// largest q in [0, n) with prefix[q] <= x; prefix is non-decreasing and prefix[0] = 0
+__device__ __forceinline__ int find_slot(const int64_t *prefix, int n, int64_t x) {
+    int lo = 0, hi = n - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (prefix[mid] <= x) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+// Python's `int <= float` is exact; e_fwd = e * gran is an int.
+__device__ __forceinline__ bool int_le_double(int64_t x, double y) {
+    if (y != y) return false;
+    if (y >= 9.2233720368547758e18) return true;
+    if (y < -9.2233720368547758e18) return false;
+    return x <= (int64_t)floor(y);
+}
+
+// ---------------------------------------------------------------- K1: cost tables
+__global__ void k_cost_cells(ChunkArgs a, int64_t n_cells) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= n_cells) return;
+    const int q = find_slot(a.cell_prefix, a.n_probs, idx);
+    const DevProblem &p = a.probs[q];
+    const int64_t local = idx - a.cell_prefix[q];
+    const int u = (int)(local / p.S);
+    const int i = (int)(local % p.S);
+    const gbmw_layer L = a.layers[a.unit_first[p.unit_off + u]];
+    const gbmw_strategy s = a.strats[a.cand_strat[p.cand_off + i]];
+    const gbmw_env env = a.envs[p.env_index];
+    const StratDeg d = strat_degrees(s);
+    double t, t_ns;
+    layer_times(L, s, d, p.micro, env, &t, &t_ns);
+    const Mem m = layer_memory(L, d, p.micro, p.stage_index, p.n_micro, env.ms_bytes_per_param_byte);
+    const int cnt = a.unit_count[p.unit_off + u];
+    Cell c;
+    c.c = t * (double)cnt;                       // dpsearch.py:141
+    c.ef = (m.o_f + m.o_ms) * (double)cnt;       // dpsearch.py:142
+    const double wq = ceil(c.ef / (double)p.gran);   // dpsearch.py:144
+    int64_t w = (wq > (double)p.n_b) ? p.n_b + 1 : (int64_t)wq;
+    if (w < 0) w = 0;                            // dpsearch.py:145
+    c.w = (int32_t)w;
+    c.k = a.cand_cls[p.cand_off + i];
+    a.cells[p.cell_off + local] = c;
+    CellMem cm;
+    cm.o_f = m.o_f; cm.o_b = m.o_b; cm.o_ms = m.o_ms;
+    a.cmem[p.cell_off + local] = cm;
+    // b_up = max O_b over (unit, strategy)  (dpsearch.py:162); O_b >= 0 so the bit
+    // pattern orders like the value
+    atomicMax(&a.bup[q], (unsigned long long)__double_as_longlong(m.o_b));
+}
+
+__global__ void k_cost_r(ChunkArgs a, int64_t n_r) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= n_r) return;
+    const int q = find_slot(a.r_prefix, a.n_probs, idx);
+    const DevProblem &p = a.probs[q];
+    const int64_t local = idx - a.r_prefix[q];
+    const int KK = p.K * p.K;
+    const int u = (int)(local / KK);
+    const int rem = (int)(local % KK);
+    const int ka = rem / p.K, kb = rem % p.K;
+    const gbmw_layer L = a.layers[a.unit_first[p.unit_off + u]];
+    const gbmw_env env = a.envs[p.env_index];
+    a.rcls[p.r_off + local] = transform_cost(
+        L.bnd_bytes_per_sample, a.class_d[p.class_off + ka], a.class_t[p.class_off + ka],
+        a.class_d[p.class_off + kb], a.class_t[p.class_off + kb], p.micro, env.intra_island_bw);
+}
+
+// ---------------------------------------------------------------- K2: min-plus layer step
+// One thread per bucket row e' of one problem.  Reads the previous unit's table row
+// T_{u-1}[e', :] (reconstructed from the class-reduced B_{u-1}, or the init row for
+// u == 1), relaxes it against every target class and writes B_u[e', k] and its argmin.
+// Tie-break T1 (dpsearch.py:271-276): lexicographic (cand, F, i), first i wins.
+template <int KT>
+__global__ void __launch_bounds__(kStepThreads) k_dp_step(ChunkArgs a, int u, int n_active) {
+    __shared__ int32_t sW[kMaxStrats];
+    __shared__ int32_t sK[kMaxStrats];
+    __shared__ double sC[kMaxStrats];
+    __shared__ double sE[kMaxStrats];
+    __shared__ double sR[kMaxClasses * kMaxClasses];
+    __shared__ int sq;
+    if (threadIdx.x == 0) sq = find_slot(a.step_tiles, n_active, blockIdx.x);
+    __syncthreads();
+    const int q = sq;
+    const DevProblem &p = a.probs[q];
+    const int S = p.S, K = p.K;
+    const int64_t n_e = p.n_b + 1;
+    const Cell *prev_cells = a.cells + p.cell_off + (int64_t)(u - 1) * S;
+    for (int i = threadIdx.x; i < S; i += blockDim.x) {
+        const Cell c = prev_cells[i];
+        sW[i] = c.w; sK[i] = c.k; sC[i] = c.c; sE[i] = c.ef;
+    }
+    const double *r_u = a.rcls + p.r_off + (int64_t)u * K * K;
+    for (int x = threadIdx.x; x < K * K; x += blockDim.x) sR[x] = r_u[x];
+    __syncthreads();
+
+    const int64_t e = (int64_t)(blockIdx.x - a.step_tiles[q]) * kStepThreads + threadIdx.x;
+    if (e >= n_e) return;
+    const double *tin = a.Tb[(u - 1) & 1] + p.b_off;
+    const double *fin = a.Fb[(u - 1) & 1] + p.b_off;
+    const bool first = (u == 1);
+
+    double bt[KT], bf[KT];
+    int bp[KT];
+#pragma unroll
+    for (int kk = 0; kk < KT; ++kk) { bt[kk] = GBMW_INF; bf[kk] = GBMW_INF; bp[kk] = 0; }
+
+    for (int i = 0; i < S; ++i) {
+        const int w = sW[i];
+        const int k = sK[i];
+        double T = GBMW_INF, F = GBMW_INF;
+        if (e >= w) {
+            if (first) {                       // init row, dpsearch.py:255-259
+                T = sC[i]; F = sE[i];
+            } else {                           // T_{u-1}[e,i] = B_{u-1}[e-w,k].t + time_c
+                const int64_t src = (int64_t)k * n_e + (e - w);
+                T = tin[src] + sC[i];
+                F = fin[src] + sE[i];
+            }
+        }
+        const double *rrow = sR + k * K;
+#pragma unroll
+        for (int kk = 0; kk < KT; ++kk) {
+            if (kk < K) {
+                const double cand = T + rrow[kk];
+                const bool better = (cand < bt[kk]) || (cand == bt[kk] && F < bf[kk]);
+                if (better) { bt[kk] = cand; bf[kk] = F; bp[kk] = i; }
+            }
+        }
+    }
+    double *tout = a.Tb[u & 1] + p.b_off;
+    double *fout = a.Fb[u & 1] + p.b_off;
+    uint16_t *pout = a.par + p.par_off + (int64_t)(u - 1) * K * n_e;
+#pragma unroll
+    for (int kk = 0; kk < KT; ++kk) {
+        if (kk < K) {
+            tout[(int64_t)kk * n_e + e] = bt[kk];
+            fout[(int64_t)kk * n_e + e] = bf[kk];
+            pout[(int64_t)kk * n_e + e] = (uint16_t)bp[kk];
+        }
+    }
+}
+
+// ---------------------------------------------------------------- shared helpers
+// reference table of the last unit at row e, strategy j
+struct RowCtx {
+    const int32_t *w; const int32_t *k; const double *c; const double *ef;
+    const double *tin; const double *fin;
+    int64_t n_e;
+    bool init;
+};
+
+__device__ __forceinline__ void row_value(const RowCtx &r, int64_t e, int j, double &T, double &F) {
+    const int w = r.w[j];
+    if (e < w) { T = GBMW_INF; F = GBMW_INF; return; }
+    if (r.init) { T = r.c[j]; F = r.ef[j]; return; }
+    const int64_t src = (int64_t)r.k[j] * r.n_e + (e - w);
+    T = r.tin[src] + r.c[j];
+    F = r.fin[src] + r.ef[j];
+}
+
+// Walk the argmin pointers back from (last unit, e, j) (dpsearch.py:292-301).
+__device__ __forceinline__ void backtrack(const ChunkArgs &a, const DevProblem &p, int64_t e, int j,
+                                          uint16_t *path) {
+    const int U = p.U, S = p.S, K = p.K;
+    const int64_t n_e = p.n_b + 1;
+    const Cell *cells = a.cells + p.cell_off;
+    const uint16_t *par = a.par + p.par_off;
+    path[U - 1] = (uint16_t)j;
+    for (int u = U - 1; u >= 1; --u) {
+        const Cell c = cells[(int64_t)u * S + j];
+        e -= c.w;
+        j = par[((int64_t)(u - 1) * K + c.k) * n_e + e];
+        path[u - 1] = (uint16_t)j;
+    }
+}
+
+// E_all of the expanded plan in layer order (costs.py:307-318).
+__device__ __forceinline__ double plan_e_all(const ChunkArgs &a, const DevProblem &p, const uint16_t *path) {
+    double total_ms = 0.0, prefix_f = 0.0, peak = 0.0;
+    const CellMem *cm = a.cmem + p.cell_off;
+    for (int u = 0; u < p.U; ++u) {
+        const CellMem m = cm[(int64_t)u * p.S + path[u]];
+        const int cnt = a.unit_count[p.unit_off + u];
+        for (int r = 0; r < cnt; ++r) {
+            total_ms = total_ms + m.o_ms;
+            prefix_f = prefix_f + m.o_f;
+            peak = py_max(peak, prefix_f + m.o_b);
+        }
+    }
+    return peak + total_ms;
+}
+
+__device__ __forceinline__ bool lex_less(double t1, double f1, int j1, double t2, double f2, int j2) {
+    if (t1 != t2) return t1 < t2;
+    if (f1 != f2) return f1 < f2;
+    return j1 < j2;
+}
+
+// candidate order across buckets: smaller t, ties -> larger e (dpsearch.py:203-207)
+__device__ __forceinline__ bool cand_better(double t1, int64_t e1, double t2, int64_t e2) {
+    return (t1 < t2) || (t1 == t2 && e1 > e2);
+}
+
+// ---------------------------------------------------------------- K3: E_fwd sweep
+// One thread per bucket e in [1, n_b].  f(e) = first strategy in (T, F, j) order that
+// is finite and fits (inside the safe zone everything fits); the tile keeps the
+// best f(e) by (t, larger e).  Equivalent to the sequential sweep.
+__global__ void __launch_bounds__(kSweepThreads) k_sweep(ChunkArgs a) {
+    __shared__ int32_t sW[kMaxStrats];
+    __shared__ int32_t sK[kMaxStrats];
+    __shared__ double sC[kMaxStrats];
+    __shared__ double sE[kMaxStrats];
+    __shared__ int sq;
+    __shared__ double red_t[kSweepThreads / 32];
+    __shared__ long long red_e[kSweepThreads / 32];
+    __shared__ int red_j[kSweepThreads / 32];
+    if (threadIdx.x == 0) sq = find_slot(a.sweep_tiles, a.n_probs, blockIdx.x);
+    __syncthreads();
+    const int q = sq;
+    const DevProblem &p = a.probs[q];
+    const int S = p.S;
+    const int last = p.U - 1;
+    const Cell *lc = a.cells + p.cell_off + (int64_t)last * S;
+    for (int i = threadIdx.x; i < S; i += blockDim.x) {
+        const Cell c = lc[i];
+        sW[i] = c.w; sK[i] = c.k; sC[i] = c.c; sE[i] = c.ef;
+    }
+    __syncthreads();
+
+    RowCtx r;
+    r.w = sW; r.k = sK; r.c = sC; r.ef = sE;
+    r.n_e = p.n_b + 1;
+    r.init = (last == 0);
+    r.tin = a.Tb[last & 1] + p.b_off;
+    r.fin = a.Fb[last & 1] + p.b_off;
+
+    const int tile = blockIdx.x - (int)a.sweep_tiles[q];
+    const int64_t e = 1 + (int64_t)tile * kSweepThreads + threadIdx.x;
+    double best_t = GBMW_INF;
+    int64_t best_e = -1;
+    int best_j = 0;
+    if (e <= p.n_b) {
+        // rank-0 candidate
+        double t0 = GBMW_INF, f0 = GBMW_INF;
+        int j0 = -1;
+        for (int j = 0; j < S; ++j) {
+            double T, F;
+            row_value(r, e, j, T, F);
+            if (T < GBMW_INF && (j0 < 0 || lex_less(T, F, j, t0, f0, j0))) { t0 = T; f0 = F; j0 = j; }
+        }
+        if (p.frontier_off >= 0) a.frontier[p.frontier_off + e - 1] = t0;
+        if (j0 >= 0) {
+            const double safe_limit = p.budget - __longlong_as_double((long long)a.bup[q]);
+            const bool safe = int_le_double(e * p.gran, safe_limit);
+            if (safe) {
+                best_t = t0; best_e = e; best_j = j0;
+            } else {
+                uint16_t path[kMaxUnits];
+                double ct = t0, cf = f0;
+                int cj = j0;
+                while (true) {
+                    backtrack(a, p, e, cj, path);
+                    if (plan_e_all(a, p, path) <= p.budget) {
+                        best_t = ct; best_e = e; best_j = cj;
+                        break;
+                    }
+                    // next candidate in (T, F, j) order
+                    double nt = GBMW_INF, nf = GBMW_INF;
+                    int nj = -1;
+                    for (int j = 0; j < S; ++j) {
+                        double T, F;
+                        row_value(r, e, j, T, F);
+                        if (!(T < GBMW_INF)) continue;
+                        if (!lex_less(ct, cf, cj, T, F, j)) continue;
+                        if (nj < 0 || lex_less(T, F, j, nt, nf, nj)) { nt = T; nf = F; nj = j; }
+                    }
+                    if (nj < 0) break;
+                    ct = nt; cf = nf; cj = nj;
+                }
+            }
+        }
+    }
+    // tile reduction: (t, larger e)
+    for (int off = 16; off > 0; off >>= 1) {
+        const double ot = __shfl_down_sync(0xffffffffu, best_t, off);
+        const long long oe = __shfl_down_sync(0xffffffffu, (long long)best_e, off);
+        const int oj = __shfl_down_sync(0xffffffffu, best_j, off);
+        if (cand_better(ot, oe, best_t, best_e)) { best_t = ot; best_e = oe; best_j = oj; }
+    }
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) { red_t[wid] = best_t; red_e[wid] = best_e; red_j[wid] = best_j; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double bt = red_t[0];
+        long long be = red_e[0];
+        int bj = red_j[0];
+        for (int w = 1; w < kSweepThreads / 32; ++w)
+            if (cand_better(red_t[w], red_e[w], bt, be)) { bt = red_t[w]; be = red_e[w]; bj = red_j[w]; }
+        SweepPartial sp;
+        sp.t = bt; sp.e = be; sp.j = bj; sp.pad_ = 0;
+        a.partials[p.tile_off + tile] = sp;
+    }
+}
+
+// ---------------------------------------------------------------- K4: finalize
+__global__ void k_finalize(ChunkArgs a) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= a.n_probs) return;
+    const DevProblem &p = a.probs[q];
+    double bt = GBMW_INF;
+    int64_t be = -1;
+    int bj = 0;
+    for (int t = 0; t < p.n_sweep_tiles; ++t) {
+        const SweepPartial sp = a.partials[p.tile_off + t];
+        if (cand_better(sp.t, sp.e, bt, be)) { bt = sp.t; be = sp.e; bj = sp.j; }
+    }
+    gbmw_result res;
+    res.frontier_offset = -1;
+    res.status = GBMW_OK;
+    res.stage_time_s = 0.0; res.stage_time_no_sync_s = 0.0; res.stage_peak_mem_bytes = 0.0;
+    int32_t *plan = a.plans + p.plan_off;
+    if (be < 0) {
+        res.time_s = GBMW_INF; res.e_fwd_used = 0.0; res.feasible = 0;
+        for (int l = 0; l < p.n_layers; ++l) plan[l] = -1;
+        a.results[p.result_index] = res;
+        return;
+    }
+    uint16_t path[kMaxUnits];
+    backtrack(a, p, be, bj, path);
+    const double e_all = plan_e_all(a, p, path);
+    res.time_s = bt;
+    res.e_fwd_used = (double)(be * p.gran);
+    res.feasible = 1;
+    if (!(e_all <= p.budget)) res.status = GBMW_EINTERNAL;   // dpsearch.py:220
+    // expand units to layers (dpsearch.py:230-234) and cost the stage (costs.py:322-352)
+    const gbmw_env env = a.envs[p.env_index];
+    double time_s = 0.0, no_sync = 0.0;
+    int l = 0;
+    int prev_d = 0, prev_t = 0;
+    int32_t first_pp = 1;
+    for (int u = 0; u < p.U; ++u) {
+        const int cand = path[u];
+        const int gs = a.cand_strat[p.cand_off + cand];
+        const gbmw_strategy s = a.strats[gs];
+        const StratDeg d = strat_degrees(s);
+        const int cnt = a.unit_count[p.unit_off + u];
+        for (int r = 0; r < cnt; ++r, ++l) {
+            plan[l] = gs - p.strat_begin;
+            if (p.flags & GBMW_STAGE_COST) {
+                const gbmw_layer L = a.layers[p.layer_begin + l];
+                double t, t_ns;
+                layer_times(L, s, d, p.micro, env, &t, &t_ns);
+                const double rc = (l == 0) ? 0.0
+                    : transform_cost(L.bnd_bytes_per_sample, prev_d, prev_t, d.data, d.tp,
+                                     p.micro, env.intra_island_bw);
+                time_s = time_s + (t + rc);
+                no_sync = no_sync + (t_ns + rc);
+            }
+            if (l == 0) first_pp = s.pp_degree;
+            prev_d = d.data; prev_t = d.tp;
+        }
+    }
+    if (p.flags & GBMW_STAGE_COST) {
+        if (p.stage_index > 1) {
+            const double p2p = stage_p2p_time(a.layers[p.layer_begin].bnd_bytes_per_sample,
+                                              p.micro, first_pp, env);
+            time_s = time_s + p2p;
+            no_sync = no_sync + p2p;
+        }
+        res.stage_time_s = time_s;
+        res.stage_time_no_sync_s = no_sync;
+        res.stage_peak_mem_bytes = e_all;
+    }
+    a.results[p.result_index] = res;
+}
+
+// ---------------------------------------------------------------- launchers
+static inline unsigned blocks_for(int64_t n, int threads) { return (unsigned)((n + threads - 1) / threads); }
+
+int launch_cost_tables(const ChunkArgs &a, int64_t n_cells, int64_t n_r, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n_cells > 0) k_cost_cells<<<blocks_for(n_cells, 128), 128, 0, st>>>(a, n_cells);
+    if (n_r > 0) k_cost_r<<<blocks_for(n_r, 128), 128, 0, st>>>(a, n_r);
+    return (int)cudaGetLastError();
+}
+
+int launch_dp_step(const ChunkArgs &a, int u, int32_t n_active, int64_t n_tiles, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n_tiles <= 0) return 0;
+    const unsigned g = (unsigned)n_tiles;
+    if (a.max_k <= 4) k_dp_step<4><<<g, kStepThreads, 0, st>>>(a, u, n_active);
+    else if (a.max_k <= 8) k_dp_step<8><<<g, kStepThreads, 0, st>>>(a, u, n_active);
+    else k_dp_step<16><<<g, kStepThreads, 0, st>>>(a, u, n_active);
+    return (int)cudaGetLastError();
+}
+
+int launch_sweep(const ChunkArgs &a, int64_t n_tiles, void *stream) {
+    if (n_tiles <= 0) return 0;
+    k_sweep<<<(unsigned)n_tiles, kSweepThreads, 0, (cudaStream_t)stream>>>(a);
+    return (int)cudaGetLastError();
+}
+
+int launch_finalize(const ChunkArgs &a, void *stream) {
+    if (a.n_probs <= 0) return 0;
+    k_finalize<<<blocks_for(a.n_probs, 64), 64, 0, (cudaStream_t)stream>>>(a);
+    return (int)cudaGetLastError();
+}
+
+}  // namespace gbmw
