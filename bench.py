@@ -316,10 +316,24 @@ def main():
         winner = best
         h2d = int(L.nbytes + S.nbytes + E.nbytes + Pm.nbytes)
         d2h = int(r.nbytes + 4 * int(Pm["n_layers"].sum()))
-    e2e_t = torch.tensor([max(e2e_ms)], dtype=torch.float64, device="cuda")
+    e2e_t = torch.tensor([max(e2e_ms) if e2e_ms else float("nan")], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     e2e_step_ms = float(e2e_t.item())
+    # where the e2e time goes (one extra, untimed, instrumented pass)
+    t0 = time.perf_counter()
+    b2 = SearchBatch(L, S, E, Pm, ctx)
+    t1 = time.perf_counter()
+    b2.run()
+    t2 = time.perf_counter()
+    b2.fetch()
+    t3 = time.perf_counter()
+    tb = b2.timing()
+    b2.close()
+    t4 = time.perf_counter()
+    breakdown = {"create_ms": (t1 - t0) * 1e3, "host_prep_ms": tb["prep_ms"], "upload_ms": tb["upload_ms"],
+                 "run_ms": (t2 - t1) * 1e3, "device_ms": tb["total_ms"], "fetch_ms": (t3 - t2) * 1e3,
+                 "destroy_ms": (t4 - t3) * 1e3}
 
     if rank == 0:
         hbm, kind = peaks()
@@ -343,7 +357,8 @@ def main():
             "clocks": clk,
             "e2e": {"value": total_T / (e2e_step_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_step_ms,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "api": "dpsearch.run_native_batch -> gbmw_search_batch (host arrays) + NCCL argmin"},
+                    "api": "dpsearch.run_native_batch -> gbmw_search_batch (host arrays) + NCCL argmin",
+                    "breakdown_rank0": breakdown},
             "winner": {"time_s": winner[0], "search": winner[1]} if winner else None,
             "transitions_per_step": total_T,
         }

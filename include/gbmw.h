@@ -141,6 +141,9 @@ typedef struct gbmw_timing {
     double  dp_cells;          /* sum over problems of (U-1) * n_e * S * K (relaxations executed) */
     double  h2d_bytes;         /* bytes uploaded by gbmw_batch_create */
     double  d2h_bytes;         /* bytes downloaded by the last gbmw_batch_fetch */
+    double  prep_ms;           /* host wall time of gbmw_batch_create before the upload */
+    double  upload_ms;         /* host wall time of the arena allocation + upload */
+    double  fetch_ms;          /* host wall time of the last gbmw_batch_fetch */
 } gbmw_timing;
 
 typedef struct gbmw_ctx gbmw_ctx;

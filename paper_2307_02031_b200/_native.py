@@ -51,7 +51,8 @@ class Timing(ctypes.Structure):
                 ("n_chunks", ctypes.c_int32), ("n_launches", ctypes.c_int32),
                 ("transitions", ctypes.c_double), ("row_steps", ctypes.c_double),
                 ("dp_bytes", ctypes.c_double), ("dp_cells", ctypes.c_double),
-                ("h2d_bytes", ctypes.c_double), ("d2h_bytes", ctypes.c_double)]
+                ("h2d_bytes", ctypes.c_double), ("d2h_bytes", ctypes.c_double),
+                ("prep_ms", ctypes.c_double), ("upload_ms", ctypes.c_double), ("fetch_ms", ctypes.c_double)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -65,7 +66,7 @@ EXPORTS = (
 )
 
 _lib = None
-_lib_lock = threading.Lock()
+_lib_lock = threading.RLock()
 
 
 def lib() -> ctypes.CDLL:

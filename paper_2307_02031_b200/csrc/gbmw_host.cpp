@@ -14,6 +14,11 @@
 #include <cstring>
 #include <string>
 #include <vector>
+#include <chrono>
+
+static double now_ms() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
 
 #include "../../include/gbmw.h"
 #include "costmodel.cuh"
@@ -58,14 +63,16 @@ struct HostProb {
 };
 
 struct Chunk {
-    std::vector<int> probs;        // host problem indices, sorted by U descending
+    std::vector<int> probs;        // host problem indices, sorted by (K group, U descending)
     std::vector<int64_t> step_prefix;
-    std::vector<int> n_active;     // per u (index u), problems with U > u
+    int group_lo[kStepGroups + 1] = {0};
+    std::vector<int> n_active[kStepGroups];   // per group, per u: problems of the group with U > u
     int Umax = 0, max_k = 1;
     int64_t n_cells = 0, n_r = 0, n_bcells = 0, n_par = 0, n_tiles = 0;
     size_t small_off = 0;          // byte offset of this chunk's descriptor block in the arena
     // offsets inside the descriptor block
     size_t o_probs, o_cellp, o_rp, o_stepp, o_sweepp, o_cand, o_ccls, o_clsd, o_clst, o_uf, o_uc;
+    size_t o_stepmap, o_sweepmap;
     size_t small_bytes = 0;
     size_t ws_bytes = 0;
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -383,7 +390,7 @@ void prepare_problem(gbmw_batch &b, int pi, std::string *err) {
     h.n_bcells = (h.U > 1) ? (int64_t)h.K * n_e : 0;
     h.n_par = (int64_t)(h.U - 1) * h.K * n_e;
     h.n_tiles = (h.n_b + kSweepThreads - 1) / kSweepThreads;
-    h.n_step_tiles = (n_e + kStepThreads - 1) / kStepThreads;
+    h.n_step_tiles = (n_e + kStepRows - 1) / kStepRows;
     h.ws_bytes = (size_t)h.n_cells * (sizeof(Cell) + sizeof(CellMem)) + (size_t)h.n_r * 8 + 8 +
                  (size_t)h.n_bcells * 32 + (size_t)h.n_par * 2 + (size_t)h.n_tiles * sizeof(SweepPartial);
     h.gpu = true;
@@ -427,6 +434,7 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
     *out = nullptr;
     if (n_problems < 0 || n_layers < 0 || n_strategies < 0 || n_envs < 0)
         return set_err(&ctx->err, GBMW_EINVAL, "negative array length");
+    const double t_start = now_ms();
     gbmw_batch *b = new gbmw_batch();
     b->layers.assign(layers, layers + n_layers);
     b->strats.assign(strategies, strategies + n_strategies);
@@ -478,7 +486,11 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
     // per-chunk descriptors
     std::vector<char> blob;
     for (Chunk &c : b->chunks) {
-        std::stable_sort(c.probs.begin(), c.probs.end(), [&](int x, int y) { return b->hp[x].U > b->hp[y].U; });
+        std::stable_sort(c.probs.begin(), c.probs.end(), [&](int x, int y) {
+            const int gx = step_group(b->hp[x].K), gy = step_group(b->hp[y].K);
+            if (gx != gy) return gx < gy;
+            return b->hp[x].U > b->hp[y].U;
+        });
         std::vector<DevProblem> dps;
         std::vector<int64_t> cellp{0}, rp{0}, stepp{0}, sweepp{0};
         std::vector<int32_t> cand, ccls, clsd, clst, uf, uc;
@@ -510,11 +522,21 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
             c.max_k = std::max(c.max_k, h.K);
         }
         c.step_prefix = stepp;
-        c.n_active.assign(c.Umax + 1, 0);
-        for (int u = 0; u <= c.Umax; ++u) {
-            int n = 0;
-            for (int pi : c.probs) if (b->hp[pi].U > u) ++n;
-            c.n_active[u] = n;
+        // groups are contiguous in sorted order; within a group U is descending, so
+        // the problems still active at unit u are a prefix of the group
+        const int np = (int)c.probs.size();
+        for (int g = 0, s = 0; g < kStepGroups; ++g) {
+            c.group_lo[g] = s;
+            while (s < np && step_group(b->hp[c.probs[s]].K) == g) ++s;
+            c.group_lo[g + 1] = s;
+            c.n_active[g].assign(c.Umax + 1, 0);
+            for (int x = c.group_lo[g]; x < s; ++x)
+                for (int u = 0; u < b->hp[c.probs[x]].U && u <= c.Umax; ++u) c.n_active[g][u]++;
+        }
+        std::vector<int32_t> stepmap(stepp.back()), sweepmap(sweepp.back());
+        for (int x = 0; x < np; ++x) {
+            for (int64_t t = stepp[x]; t < stepp[x + 1]; ++t) stepmap[t] = x;
+            for (int64_t t = sweepp[x]; t < sweepp[x + 1]; ++t) sweepmap[t] = x;
         }
         const size_t base = align_up(blob.size(), 256);
         blob.resize(base);
@@ -530,10 +552,13 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
         c.o_clst = put(blob, clst.data(), clst.size()) - base;
         c.o_uf = put(blob, uf.data(), uf.size()) - base;
         c.o_uc = put(blob, uc.data(), uc.size()) - base;
+        c.o_stepmap = put(blob, stepmap.data(), stepmap.size()) - base;
+        c.o_sweepmap = put(blob, sweepmap.data(), sweepmap.size()) - base;
         c.small_bytes = blob.size() - base;
         c.ws_bytes = ws_layout(c).total;
         b->max_ws = std::max(b->max_ws, c.ws_bytes);
     }
+    const double t_prep = now_ms();
     // arena: inputs | descriptor blob | outputs
     size_t o = 0;
     b->o_layers = o; o = align_up(o + b->layers.size() * sizeof(gbmw_layer));
@@ -560,6 +585,8 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
     ce = cudaMemcpyAsync(b->arena, host.data(), host.size(), cudaMemcpyHostToDevice, ctx->stream);
     if (ce == cudaSuccess) ce = cudaStreamSynchronize(ctx->stream);
     b->timing.h2d_bytes = (double)host.size();
+    b->timing.prep_ms = t_prep - t_start;
+    b->timing.upload_ms = now_ms() - t_prep;
     if (ce != cudaSuccess) {
         cudaFree(b->arena);
         delete b;
@@ -612,6 +639,8 @@ ChunkArgs chunk_args(gbmw_batch *b, const Chunk &c, char *ws) {
     a.class_t = (const int32_t *)(sm + c.o_clst);
     a.unit_first = (const int32_t *)(sm + c.o_uf);
     a.unit_count = (const int32_t *)(sm + c.o_uc);
+    a.step_map = (const int32_t *)(sm + c.o_stepmap);
+    a.sweep_map = (const int32_t *)(sm + c.o_sweepmap);
     const WsLayout w = ws_layout(c);
     a.cells = (Cell *)(ws + w.cells);
     a.cmem = (CellMem *)(ws + w.cmem);
@@ -653,9 +682,13 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
         cudaEventRecord(c.ev[1], st);
         if (tables_only) continue;
         for (int u = 1; u < c.Umax; ++u) {
-            const int na = c.n_active[u];
-            if ((rc = launch_dp_step(a, u, na, c.step_prefix[na], st))) return cuda_fail(ctx, rc, "K2 launch");
-            c.launches += 1;
+            for (int g = 0; g < kStepGroups; ++g) {
+                const int lo = c.group_lo[g], na = c.n_active[g][u];
+                if (na == 0) continue;
+                const int64_t base = c.step_prefix[lo], n = c.step_prefix[lo + na] - base;
+                if ((rc = launch_dp_step(a, g, u, base, n, st))) return cuda_fail(ctx, rc, "K2 launch");
+                c.launches += 1;
+            }
         }
         cudaEventRecord(c.ev[2], st);
         if ((rc = launch_sweep(a, c.n_tiles, st))) return cuda_fail(ctx, rc, "K3 launch");
@@ -689,6 +722,7 @@ extern "C" int gbmw_batch_run(gbmw_ctx *ctx, gbmw_batch *b) {
 extern "C" int gbmw_batch_fetch(gbmw_ctx *ctx, gbmw_batch *b, gbmw_result *results, int32_t *plans, double *frontier) {
     if (!ctx || !b) return set_err(nullptr, GBMW_EINVAL, "null ctx/batch");
     if (!b->ran && !b->chunks.empty()) return set_err(&ctx->err, GBMW_EINVAL, "batch has not been run");
+    const double t0 = now_ms();
     cudaSetDevice(ctx->device);
     cudaStream_t st = ctx->stream;
     const size_t np = b->problems.size();
@@ -724,6 +758,7 @@ extern "C" int gbmw_batch_fetch(gbmw_ctx *ctx, gbmw_batch *b, gbmw_result *resul
         if (results) results[i] = r;
     }
     if (first == GBMW_EINTERNAL) set_err(&ctx->err, first, "dp_search produced a plan exceeding the memory budget");
+    b->timing.fetch_ms = now_ms() - t0;
     return first;
 }
 

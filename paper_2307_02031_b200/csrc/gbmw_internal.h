@@ -20,8 +20,15 @@ namespace gbmw {
 constexpr int kMaxUnits = 1024;      // backtrack path held in local memory
 constexpr int kMaxClasses = 16;
 constexpr int kMaxStrats = 512;      // smem staging of per-strategy constants
-constexpr int kStepThreads = 256;    // rows per K2 tile
+constexpr int kStepThreads = 256;    // threads per K2 CTA
+constexpr int kStepRowsPerThread = 2;
+constexpr int kStepRows = kStepThreads * kStepRowsPerThread;   // rows per K2 tile
 constexpr int kSweepThreads = 256;   // rows per K3 tile
+
+// K2 is instantiated per class-count group so a problem with few classes does not
+// pay the register footprint of the widest one: K <= 4, 5..8, 9..kMaxClasses.
+constexpr int kStepGroups = 3;
+inline int step_group(int K) { return K <= 4 ? 0 : (K <= 8 ? 1 : 2); }
 
 struct Cell {
     double c;       // time_c = t * count
@@ -74,8 +81,10 @@ struct ChunkArgs {
     int32_t max_k;
     const int64_t *cell_prefix;   // n_probs + 1
     const int64_t *r_prefix;      // n_probs + 1
-    const int64_t *step_tiles;    // n_probs + 1, tiles of ceil(n_e / kStepThreads)
+    const int64_t *step_tiles;    // n_probs + 1, tiles of ceil(n_e / kStepRows)
     const int64_t *sweep_tiles;   // n_probs + 1
+    const int32_t *step_map;      // K2 tile -> problem (sorted position)
+    const int32_t *sweep_map;     // K3 tile -> problem
     const int32_t *cand_strat;    // global strategy index
     const int32_t *cand_cls;
     const int32_t *class_d, *class_t;
@@ -96,7 +105,7 @@ struct ChunkArgs {
 
 // launchers (gbmw_kernels.cu); all asynchronous on `stream`, return cudaError_t as int
 int launch_cost_tables(const ChunkArgs &a, int64_t n_cells, int64_t n_r, void *stream);
-int launch_dp_step(const ChunkArgs &a, int u, int32_t n_active, int64_t n_tiles, void *stream);
+int launch_dp_step(const ChunkArgs &a, int group, int u, int64_t tile_base, int64_t n_tiles, void *stream);
 int launch_sweep(const ChunkArgs &a, int64_t n_tiles, void *stream);
 int launch_finalize(const ChunkArgs &a, void *stream);
 

@@ -95,60 +95,56 @@ __global__ void k_cost_r(ChunkArgs a, int64_t n_r) {
 // T_{u-1}[e', :] (reconstructed from the class-reduced B_{u-1}, or the init row for
 // u == 1), relaxes it against every target class and writes B_u[e', k] and its argmin.
 // Tie-break T1 (dpsearch.py:271-276): lexicographic (cand, F, i), first i wins.
-template <int KT>
-__global__ void __launch_bounds__(kStepThreads) k_dp_step(ChunkArgs a, int u, int n_active) {
-    __shared__ int32_t sW[kMaxStrats];
-    __shared__ int32_t sK[kMaxStrats];
-    __shared__ double sC[kMaxStrats];
-    __shared__ double sE[kMaxStrats];
-    __shared__ double sR[kMaxClasses * kMaxClasses];
-    __shared__ int sq;
-    if (threadIdx.x == 0) sq = find_slot(a.step_tiles, n_active, blockIdx.x);
-    __syncthreads();
-    const int q = sq;
-    const DevProblem &p = a.probs[q];
-    const int S = p.S, K = p.K;
-    const int64_t n_e = p.n_b + 1;
-    const Cell *prev_cells = a.cells + p.cell_off + (int64_t)(u - 1) * S;
-    for (int i = threadIdx.x; i < S; i += blockDim.x) {
-        const Cell c = prev_cells[i];
-        sW[i] = c.w; sK[i] = c.k; sC[i] = c.c; sE[i] = c.ef;
-    }
-    const double *r_u = a.rcls + p.r_off + (int64_t)u * K * K;
-    for (int x = threadIdx.x; x < K * K; x += blockDim.x) sR[x] = r_u[x];
-    __syncthreads();
-
-    const int64_t e = (int64_t)(blockIdx.x - a.step_tiles[q]) * kStepThreads + threadIdx.x;
-    if (e >= n_e) return;
+//
+// Each thread owns kStepRowsPerThread rows (stride kStepThreads) so the per-strategy
+// constants and transform costs read from shared memory are shared by its rows.
+// KT is the exact class count (CTA-uniform dispatch) up to 8; KT = kMaxClasses with
+// a runtime guard covers larger strategy spaces.
+template <int KT, int NR, bool FIRST, bool GUARD>
+__device__ __forceinline__ void step_rows(const ChunkArgs &a, const DevProblem &p, int u, int e0,
+                                          const Cell *sCell, const double *sR) {
+    const int S = p.S, K = GUARD ? p.K : KT;
+    const int n_e = (int)(p.n_b + 1);
     const double *tin = a.Tb[(u - 1) & 1] + p.b_off;
     const double *fin = a.Fb[(u - 1) & 1] + p.b_off;
-    const bool first = (u == 1);
 
-    double bt[KT], bf[KT];
-    int bp[KT];
+    double bt[NR][KT], bf[NR][KT];
+    int bp[NR][KT];
 #pragma unroll
-    for (int kk = 0; kk < KT; ++kk) { bt[kk] = GBMW_INF; bf[kk] = GBMW_INF; bp[kk] = 0; }
+    for (int r = 0; r < NR; ++r)
+#pragma unroll
+        for (int kk = 0; kk < KT; ++kk) { bt[r][kk] = GBMW_INF; bf[r][kk] = GBMW_INF; bp[r][kk] = 0; }
 
     for (int i = 0; i < S; ++i) {
-        const int w = sW[i];
-        const int k = sK[i];
-        double T = GBMW_INF, F = GBMW_INF;
-        if (e >= w) {
-            if (first) {                       // init row, dpsearch.py:255-259
-                T = sC[i]; F = sE[i];
-            } else {                           // T_{u-1}[e,i] = B_{u-1}[e-w,k].t + time_c
-                const int64_t src = (int64_t)k * n_e + (e - w);
-                T = tin[src] + sC[i];
-                F = fin[src] + sE[i];
+        const Cell c = sCell[i];
+        double T[NR], F[NR];
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+            const int e = e0 + r * kStepThreads;
+            const int src = e - c.w;
+            T[r] = GBMW_INF; F[r] = GBMW_INF;
+            if (src >= 0 && e < n_e) {
+                if (FIRST) {                       // init row, dpsearch.py:255-259
+                    T[r] = c.c; F[r] = c.ef;
+                } else {                           // T_{u-1}[e,i] = B_{u-1}[e-w,k].t + time_c
+                    T[r] = __ldg(tin + c.k * n_e + src) + c.c;
+                    F[r] = __ldg(fin + c.k * n_e + src) + c.ef;
+                }
             }
         }
-        const double *rrow = sR + k * K;
+        const double *rrow = sR + c.k * K;
 #pragma unroll
         for (int kk = 0; kk < KT; ++kk) {
-            if (kk < K) {
-                const double cand = T + rrow[kk];
-                const bool better = (cand < bt[kk]) || (cand == bt[kk] && F < bf[kk]);
-                if (better) { bt[kk] = cand; bf[kk] = F; bp[kk] = i; }
+            if (!GUARD || kk < K) {
+                const double rv = rrow[kk];
+#pragma unroll
+                for (int r = 0; r < NR; ++r) {
+                    const double cand = T[r] + rv;
+                    const bool better = (cand < bt[r][kk]) || (cand == bt[r][kk] && F[r] < bf[r][kk]);
+                    bt[r][kk] = better ? cand : bt[r][kk];
+                    bf[r][kk] = better ? F[r] : bf[r][kk];
+                    bp[r][kk] = better ? i : bp[r][kk];
+                }
             }
         }
     }
@@ -156,12 +152,59 @@ __global__ void __launch_bounds__(kStepThreads) k_dp_step(ChunkArgs a, int u, in
     double *fout = a.Fb[u & 1] + p.b_off;
     uint16_t *pout = a.par + p.par_off + (int64_t)(u - 1) * K * n_e;
 #pragma unroll
-    for (int kk = 0; kk < KT; ++kk) {
-        if (kk < K) {
-            tout[(int64_t)kk * n_e + e] = bt[kk];
-            fout[(int64_t)kk * n_e + e] = bf[kk];
-            pout[(int64_t)kk * n_e + e] = (uint16_t)bp[kk];
+    for (int r = 0; r < NR; ++r) {
+        const int e = e0 + r * kStepThreads;
+        if (e >= n_e) continue;
+#pragma unroll
+        for (int kk = 0; kk < KT; ++kk) {
+            if (!GUARD || kk < K) {
+                tout[kk * n_e + e] = bt[r][kk];
+                fout[kk * n_e + e] = bf[r][kk];
+                pout[kk * n_e + e] = (uint16_t)bp[r][kk];
+            }
         }
+    }
+}
+
+// GROUP selects the class-count range (step_group): 0 -> K 1..4 with two rows per
+// pass, 1 -> K 5..8 one row per pass, 2 -> K 9..16 generic.  A tile is always
+// kStepRows rows; narrower passes loop.
+template <int GROUP, bool FIRST>
+__global__ void __launch_bounds__(kStepThreads) k_dp_step(ChunkArgs a, int u, int64_t tile_base) {
+    __shared__ Cell sCell[kMaxStrats];
+    __shared__ double sR[kMaxClasses * kMaxClasses];
+    const int64_t tile = tile_base + blockIdx.x;
+    const int q = a.step_map[tile];
+    const DevProblem &p = a.probs[q];
+    const int S = p.S, K = p.K;
+    const Cell *prev_cells = a.cells + p.cell_off + (int64_t)(u - 1) * S;
+    for (int i = threadIdx.x; i < S; i += blockDim.x) sCell[i] = prev_cells[i];
+    const double *r_u = a.rcls + p.r_off + (int64_t)u * K * K;
+    for (int x = threadIdx.x; x < K * K; x += blockDim.x) sR[x] = r_u[x];
+    __syncthreads();
+    const int base = (int)(tile - a.step_tiles[q]) * kStepRows + threadIdx.x;
+    if (GROUP == 0) {
+        switch (K) {
+            case 1: step_rows<1, 2, FIRST, false>(a, p, u, base, sCell, sR); break;
+            case 2: step_rows<2, 2, FIRST, false>(a, p, u, base, sCell, sR); break;
+            case 3: step_rows<3, 2, FIRST, false>(a, p, u, base, sCell, sR); break;
+            default: step_rows<4, 2, FIRST, false>(a, p, u, base, sCell, sR); break;
+        }
+    } else if (GROUP == 1) {
+#pragma unroll 1
+        for (int pass = 0; pass < 2; ++pass) {
+            const int e0 = base + pass * kStepThreads;
+            switch (K) {
+                case 5: step_rows<5, 1, FIRST, false>(a, p, u, e0, sCell, sR); break;
+                case 6: step_rows<6, 1, FIRST, false>(a, p, u, e0, sCell, sR); break;
+                case 7: step_rows<7, 1, FIRST, false>(a, p, u, e0, sCell, sR); break;
+                default: step_rows<8, 1, FIRST, false>(a, p, u, e0, sCell, sR); break;
+            }
+        }
+    } else {
+#pragma unroll 1
+        for (int pass = 0; pass < 2; ++pass)
+            step_rows<kMaxClasses, 1, FIRST, true>(a, p, u, base + pass * kStepThreads, sCell, sR);
     }
 }
 
@@ -235,13 +278,10 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(ChunkArgs a) {
     __shared__ int32_t sK[kMaxStrats];
     __shared__ double sC[kMaxStrats];
     __shared__ double sE[kMaxStrats];
-    __shared__ int sq;
     __shared__ double red_t[kSweepThreads / 32];
     __shared__ long long red_e[kSweepThreads / 32];
     __shared__ int red_j[kSweepThreads / 32];
-    if (threadIdx.x == 0) sq = find_slot(a.sweep_tiles, a.n_probs, blockIdx.x);
-    __syncthreads();
-    const int q = sq;
+    const int q = a.sweep_map[blockIdx.x];
     const DevProblem &p = a.probs[q];
     const int S = p.S;
     const int last = p.U - 1;
@@ -409,13 +449,17 @@ int launch_cost_tables(const ChunkArgs &a, int64_t n_cells, int64_t n_r, void *s
     return (int)cudaGetLastError();
 }
 
-int launch_dp_step(const ChunkArgs &a, int u, int32_t n_active, int64_t n_tiles, void *stream) {
+int launch_dp_step(const ChunkArgs &a, int group, int u, int64_t tile_base, int64_t n_tiles, void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
     if (n_tiles <= 0) return 0;
     const unsigned g = (unsigned)n_tiles;
-    if (a.max_k <= 4) k_dp_step<4><<<g, kStepThreads, 0, st>>>(a, u, n_active);
-    else if (a.max_k <= 8) k_dp_step<8><<<g, kStepThreads, 0, st>>>(a, u, n_active);
-    else k_dp_step<16><<<g, kStepThreads, 0, st>>>(a, u, n_active);
+#define GBMW_STEP(G)                                                                       \
+    if (u == 1) k_dp_step<G, true><<<g, kStepThreads, 0, st>>>(a, u, tile_base);          \
+    else k_dp_step<G, false><<<g, kStepThreads, 0, st>>>(a, u, tile_base);
+    if (group == 0) { GBMW_STEP(0) }
+    else if (group == 1) { GBMW_STEP(1) }
+    else { GBMW_STEP(2) }
+#undef GBMW_STEP
     return (int)cudaGetLastError();
 }
 
