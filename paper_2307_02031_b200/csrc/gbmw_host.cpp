@@ -87,6 +87,13 @@ struct gbmw_ctx {
     uint64_t workspace_limit = 0;
     void *ws = nullptr;
     size_t ws_size = 0;
+    // grow-only device arena lent to one batch at a time (no cudaMalloc per call)
+    void *arena = nullptr;
+    size_t arena_cap = 0;
+    bool arena_busy = false;
+    // grow-only pinned staging buffer for uploads
+    void *pinned = nullptr;
+    size_t pinned_cap = 0;
     std::string err;
 };
 
@@ -105,6 +112,8 @@ struct gbmw_batch {
     size_t max_ws = 0;
     gbmw_timing timing{};
     bool ran = false;
+    gbmw_ctx *ctx = nullptr;
+    bool ctx_arena = false;        // arena is borrowed from ctx (returned on destroy)
 };
 
 // ----------------------------------------------------------------------------- misc
@@ -294,6 +303,8 @@ extern "C" int gbmw_ctx_destroy(gbmw_ctx *ctx) {
     if (!ctx) return GBMW_OK;
     cudaSetDevice(ctx->device);
     if (ctx->ws) cudaFree(ctx->ws);
+    if (ctx->arena) cudaFree(ctx->arena);
+    if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
     return GBMW_OK;
@@ -571,25 +582,52 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
     b->arena_size = std::max<size_t>(o, 256);
     for (Chunk &c : b->chunks) c.small_off += o_blob;
     cudaSetDevice(ctx->device);
-    cudaError_t ce = cudaMalloc(&b->arena, b->arena_size);
+    b->ctx = ctx;
+    cudaError_t ce = cudaSuccess;
+    if (!ctx->arena_busy) {
+        if (ctx->arena_cap < b->arena_size) {
+            if (ctx->arena) cudaFree(ctx->arena);
+            ctx->arena = nullptr;
+            ctx->arena_cap = 0;
+            const size_t cap = std::max<size_t>(b->arena_size + b->arena_size / 4, 4u << 20);
+            ce = cudaMalloc(&ctx->arena, cap);
+            if (ce == cudaSuccess) ctx->arena_cap = cap;
+        }
+        if (ce == cudaSuccess) {
+            b->arena = ctx->arena;
+            b->ctx_arena = true;
+            ctx->arena_busy = true;
+        }
+    } else {
+        ce = cudaMalloc(&b->arena, b->arena_size);
+    }
     if (ce != cudaSuccess) {
         delete b;
         return set_err(&ctx->err, GBMW_ENOMEM, std::string("cudaMalloc(arena): ") + cudaGetErrorString(ce));
     }
-    // one staged upload of the input part of the arena
-    std::vector<char> host(o_blob + blob.size());
-    if (!b->layers.empty()) std::memcpy(host.data() + b->o_layers, b->layers.data(), b->layers.size() * sizeof(gbmw_layer));
-    if (!b->strats.empty()) std::memcpy(host.data() + b->o_strats, b->strats.data(), b->strats.size() * sizeof(gbmw_strategy));
-    if (!b->envs.empty()) std::memcpy(host.data() + b->o_envs, b->envs.data(), b->envs.size() * sizeof(gbmw_env));
-    if (!blob.empty()) std::memcpy(host.data() + o_blob, blob.data(), blob.size());
-    ce = cudaMemcpyAsync(b->arena, host.data(), host.size(), cudaMemcpyHostToDevice, ctx->stream);
+    // one staged upload of the input part of the arena, through pinned memory
+    const size_t up = o_blob + blob.size();
+    if (ctx->pinned_cap < up) {
+        if (ctx->pinned) cudaFreeHost(ctx->pinned);
+        ctx->pinned = nullptr;
+        ctx->pinned_cap = 0;
+        const size_t cap = std::max<size_t>(up + up / 4, 1u << 20);
+        if (cudaHostAlloc(&ctx->pinned, cap, cudaHostAllocDefault) == cudaSuccess) ctx->pinned_cap = cap;
+    }
+    std::vector<char> fallback;
+    char *host = (char *)ctx->pinned;
+    if (!host) { fallback.resize(up); host = fallback.data(); }
+    if (!b->layers.empty()) std::memcpy(host + b->o_layers, b->layers.data(), b->layers.size() * sizeof(gbmw_layer));
+    if (!b->strats.empty()) std::memcpy(host + b->o_strats, b->strats.data(), b->strats.size() * sizeof(gbmw_strategy));
+    if (!b->envs.empty()) std::memcpy(host + b->o_envs, b->envs.data(), b->envs.size() * sizeof(gbmw_env));
+    if (!blob.empty()) std::memcpy(host + o_blob, blob.data(), blob.size());
+    ce = cudaMemcpyAsync(b->arena, host, up, cudaMemcpyHostToDevice, ctx->stream);
     if (ce == cudaSuccess) ce = cudaStreamSynchronize(ctx->stream);
-    b->timing.h2d_bytes = (double)host.size();
+    b->timing.h2d_bytes = (double)up;
     b->timing.prep_ms = t_prep - t_start;
     b->timing.upload_ms = now_ms() - t_prep;
     if (ce != cudaSuccess) {
-        cudaFree(b->arena);
-        delete b;
+        gbmw_batch_destroy(b);
         return set_err(&ctx->err, GBMW_ECUDA, std::string("upload: ") + cudaGetErrorString(ce));
     }
     // algorithmic work counters
@@ -773,7 +811,8 @@ extern "C" int gbmw_batch_destroy(gbmw_batch *b) {
     for (Chunk &c : b->chunks)
         for (auto &e : c.ev)
             if (e) cudaEventDestroy(e);
-    if (b->arena) cudaFree(b->arena);
+    if (b->ctx_arena) b->ctx->arena_busy = false;
+    else if (b->arena) cudaFree(b->arena);
     delete b;
     return GBMW_OK;
 }

@@ -96,17 +96,27 @@ __global__ void k_cost_r(ChunkArgs a, int64_t n_r) {
 // u == 1), relaxes it against every target class and writes B_u[e', k] and its argmin.
 // Tie-break T1 (dpsearch.py:271-276): lexicographic (cand, F, i), first i wins.
 //
-// Each thread owns kStepRowsPerThread rows (stride kStepThreads) so the per-strategy
-// constants and transform costs read from shared memory are shared by its rows.
-// KT is the exact class count (CTA-uniform dispatch) up to 8; KT = kMaxClasses with
-// a runtime guard covers larger strategy spaces.
+// Each thread owns NR rows (stride kStepThreads) so the per-strategy constants and
+// transform costs read from shared memory are shared by its rows; the strategy loop
+// is processed in batches of kStepIB so 2*NR*kStepIB independent loads are in flight
+// before the first relaxation.  KT is the exact class count (CTA-uniform dispatch)
+// up to 8; KT = kMaxClasses with a runtime guard covers larger strategy spaces.
+constexpr int kStepIB = 4;
+constexpr int kStepCtasPerSm = 6;
+
+struct StepShared {
+    Cell cell[kMaxStrats];
+    double r[kMaxClasses * kMaxClasses];
+    int S, K, n_e, q;
+    int64_t b_off, par_off, tile0;
+};
+
 template <int KT, int NR, bool FIRST, bool GUARD>
-__device__ __forceinline__ void step_rows(const ChunkArgs &a, const DevProblem &p, int u, int e0,
-                                          const Cell *sCell, const double *sR) {
-    const int S = p.S, K = GUARD ? p.K : KT;
-    const int n_e = (int)(p.n_b + 1);
-    const double *tin = a.Tb[(u - 1) & 1] + p.b_off;
-    const double *fin = a.Fb[(u - 1) & 1] + p.b_off;
+__device__ __forceinline__ void step_rows(const ChunkArgs &a, const StepShared &sh, int u, int e0) {
+    const int S = sh.S, K = GUARD ? sh.K : KT;
+    const int n_e = sh.n_e;
+    const double *tin = a.Tb[(u - 1) & 1] + sh.b_off;
+    const double *fin = a.Fb[(u - 1) & 1] + sh.b_off;
 
     double bt[NR][KT], bf[NR][KT];
     int bp[NR][KT];
@@ -115,42 +125,58 @@ __device__ __forceinline__ void step_rows(const ChunkArgs &a, const DevProblem &
 #pragma unroll
         for (int kk = 0; kk < KT; ++kk) { bt[r][kk] = GBMW_INF; bf[r][kk] = GBMW_INF; bp[r][kk] = 0; }
 
-    for (int i = 0; i < S; ++i) {
-        const Cell c = sCell[i];
-        double T[NR], F[NR];
+    for (int i0 = 0; i0 < S; i0 += kStepIB) {
+        double T[kStepIB][NR], F[kStepIB][NR];
 #pragma unroll
-        for (int r = 0; r < NR; ++r) {
-            const int e = e0 + r * kStepThreads;
-            const int src = e - c.w;
-            T[r] = GBMW_INF; F[r] = GBMW_INF;
-            if (src >= 0 && e < n_e) {
-                if (FIRST) {                       // init row, dpsearch.py:255-259
-                    T[r] = c.c; F[r] = c.ef;
-                } else {                           // T_{u-1}[e,i] = B_{u-1}[e-w,k].t + time_c
-                    T[r] = __ldg(tin + c.k * n_e + src) + c.c;
-                    F[r] = __ldg(fin + c.k * n_e + src) + c.ef;
+        for (int b = 0; b < kStepIB; ++b) {
+            const int i = i0 + b;
+            const Cell c = sh.cell[i < S ? i : 0];
+#pragma unroll
+            for (int r = 0; r < NR; ++r) {
+                const int e = e0 + r * kStepThreads;
+                const int src = e - c.w;
+                T[b][r] = GBMW_INF; F[b][r] = GBMW_INF;
+                if (i < S && src >= 0 && e < n_e) {
+                    if (FIRST) {                   // init row, dpsearch.py:255-259
+                        T[b][r] = c.c; F[b][r] = c.ef;
+                    } else {                       // T_{u-1}[e,i] = B_{u-1}[e-w,k].t + time_c
+                        T[b][r] = __ldg(tin + c.k * n_e + src);
+                        F[b][r] = __ldg(fin + c.k * n_e + src);
+                    }
                 }
             }
         }
-        const double *rrow = sR + c.k * K;
 #pragma unroll
-        for (int kk = 0; kk < KT; ++kk) {
-            if (!GUARD || kk < K) {
-                const double rv = rrow[kk];
+        for (int b = 0; b < kStepIB; ++b) {
+            const int i = i0 + b;
+            if (i >= S) break;
+            const Cell c = sh.cell[i];
+            const double *rrow = sh.r + c.k * K;
+            double Tv[NR], Fv[NR];
 #pragma unroll
-                for (int r = 0; r < NR; ++r) {
-                    const double cand = T[r] + rv;
-                    const bool better = (cand < bt[r][kk]) || (cand == bt[r][kk] && F[r] < bf[r][kk]);
-                    bt[r][kk] = better ? cand : bt[r][kk];
-                    bf[r][kk] = better ? F[r] : bf[r][kk];
-                    bp[r][kk] = better ? i : bp[r][kk];
+            for (int r = 0; r < NR; ++r) {
+                Tv[r] = FIRST ? T[b][r] : T[b][r] + c.c;
+                Fv[r] = FIRST ? F[b][r] : F[b][r] + c.ef;
+            }
+#pragma unroll
+            for (int kk = 0; kk < KT; ++kk) {
+                if (!GUARD || kk < K) {
+                    const double rv = rrow[kk];
+#pragma unroll
+                    for (int r = 0; r < NR; ++r) {
+                        const double cand = Tv[r] + rv;
+                        const bool better = (cand < bt[r][kk]) || (cand == bt[r][kk] && Fv[r] < bf[r][kk]);
+                        bt[r][kk] = better ? cand : bt[r][kk];
+                        bf[r][kk] = better ? Fv[r] : bf[r][kk];
+                        bp[r][kk] = better ? i : bp[r][kk];
+                    }
                 }
             }
         }
     }
-    double *tout = a.Tb[u & 1] + p.b_off;
-    double *fout = a.Fb[u & 1] + p.b_off;
-    uint16_t *pout = a.par + p.par_off + (int64_t)(u - 1) * K * n_e;
+    double *tout = a.Tb[u & 1] + sh.b_off;
+    double *fout = a.Fb[u & 1] + sh.b_off;
+    uint16_t *pout = a.par + sh.par_off + (int64_t)(u - 1) * K * n_e;
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
         const int e = e0 + r * kStepThreads;
@@ -166,45 +192,59 @@ __device__ __forceinline__ void step_rows(const ChunkArgs &a, const DevProblem &
     }
 }
 
-// GROUP selects the class-count range (step_group): 0 -> K 1..4 with two rows per
-// pass, 1 -> K 5..8 one row per pass, 2 -> K 9..16 generic.  A tile is always
-// kStepRows rows; narrower passes loop.
+// Persistent over a contiguous range of tiles (consecutive tiles mostly belong to the
+// same problem, so its constants are staged once).  GROUP selects the class-count
+// range (step_group): 0 -> K 1..4 with two rows per pass, 1 -> K 5..8 one row per
+// pass, 2 -> K 9..16 generic.  A tile is always kStepRows rows.
 template <int GROUP, bool FIRST>
-__global__ void __launch_bounds__(kStepThreads) k_dp_step(ChunkArgs a, int u, int64_t tile_base) {
-    __shared__ Cell sCell[kMaxStrats];
-    __shared__ double sR[kMaxClasses * kMaxClasses];
-    const int64_t tile = tile_base + blockIdx.x;
-    const int q = a.step_map[tile];
-    const DevProblem &p = a.probs[q];
-    const int S = p.S, K = p.K;
-    const Cell *prev_cells = a.cells + p.cell_off + (int64_t)(u - 1) * S;
-    for (int i = threadIdx.x; i < S; i += blockDim.x) sCell[i] = prev_cells[i];
-    const double *r_u = a.rcls + p.r_off + (int64_t)u * K * K;
-    for (int x = threadIdx.x; x < K * K; x += blockDim.x) sR[x] = r_u[x];
-    __syncthreads();
-    const int base = (int)(tile - a.step_tiles[q]) * kStepRows + threadIdx.x;
-    if (GROUP == 0) {
-        switch (K) {
-            case 1: step_rows<1, 2, FIRST, false>(a, p, u, base, sCell, sR); break;
-            case 2: step_rows<2, 2, FIRST, false>(a, p, u, base, sCell, sR); break;
-            case 3: step_rows<3, 2, FIRST, false>(a, p, u, base, sCell, sR); break;
-            default: step_rows<4, 2, FIRST, false>(a, p, u, base, sCell, sR); break;
-        }
-    } else if (GROUP == 1) {
-#pragma unroll 1
-        for (int pass = 0; pass < 2; ++pass) {
-            const int e0 = base + pass * kStepThreads;
-            switch (K) {
-                case 5: step_rows<5, 1, FIRST, false>(a, p, u, e0, sCell, sR); break;
-                case 6: step_rows<6, 1, FIRST, false>(a, p, u, e0, sCell, sR); break;
-                case 7: step_rows<7, 1, FIRST, false>(a, p, u, e0, sCell, sR); break;
-                default: step_rows<8, 1, FIRST, false>(a, p, u, e0, sCell, sR); break;
+__global__ void __launch_bounds__(kStepThreads) k_dp_step(ChunkArgs a, int u, int64_t tile_base,
+                                                           int64_t n_tiles, int tiles_per_cta) {
+    __shared__ StepShared sh;
+    const int64_t t0 = tile_base + (int64_t)blockIdx.x * tiles_per_cta;
+    const int64_t t1 = min(t0 + tiles_per_cta, tile_base + n_tiles);
+    int q_prev = -1;
+    for (int64_t tile = t0; tile < t1; ++tile) {
+        const int q = __ldg(a.step_map + tile);
+        if (q != q_prev) {
+            __syncthreads();                       // previous problem's readers are done
+            const DevProblem &p = a.probs[q];
+            const int S = p.S, K = p.K;
+            const Cell *prev_cells = a.cells + p.cell_off + (int64_t)(u - 1) * S;
+            for (int i = threadIdx.x; i < S; i += blockDim.x) sh.cell[i] = prev_cells[i];
+            const double *r_u = a.rcls + p.r_off + (int64_t)u * K * K;
+            for (int x = threadIdx.x; x < K * K; x += blockDim.x) sh.r[x] = r_u[x];
+            if (threadIdx.x == 0) {
+                sh.S = S; sh.K = K; sh.n_e = (int)(p.n_b + 1); sh.q = q;
+                sh.b_off = p.b_off; sh.par_off = p.par_off; sh.tile0 = a.step_tiles[q];
             }
+            __syncthreads();
+            q_prev = q;
         }
-    } else {
+        const int base = (int)(tile - sh.tile0) * kStepRows + threadIdx.x;
+        const int K = sh.K;
+        if (GROUP == 0) {
+            switch (K) {
+                case 1: step_rows<1, 2, FIRST, false>(a, sh, u, base); break;
+                case 2: step_rows<2, 2, FIRST, false>(a, sh, u, base); break;
+                case 3: step_rows<3, 2, FIRST, false>(a, sh, u, base); break;
+                default: step_rows<4, 2, FIRST, false>(a, sh, u, base); break;
+            }
+        } else if (GROUP == 1) {
 #pragma unroll 1
-        for (int pass = 0; pass < 2; ++pass)
-            step_rows<kMaxClasses, 1, FIRST, true>(a, p, u, base + pass * kStepThreads, sCell, sR);
+            for (int pass = 0; pass < 2; ++pass) {
+                const int e0 = base + pass * kStepThreads;
+                switch (K) {
+                    case 5: step_rows<5, 1, FIRST, false>(a, sh, u, e0); break;
+                    case 6: step_rows<6, 1, FIRST, false>(a, sh, u, e0); break;
+                    case 7: step_rows<7, 1, FIRST, false>(a, sh, u, e0); break;
+                    default: step_rows<8, 1, FIRST, false>(a, sh, u, e0); break;
+                }
+            }
+        } else {
+#pragma unroll 1
+            for (int pass = 0; pass < 2; ++pass)
+                step_rows<kMaxClasses, 1, FIRST, true>(a, sh, u, base + pass * kStepThreads);
+        }
     }
 }
 
@@ -452,10 +492,20 @@ int launch_cost_tables(const ChunkArgs &a, int64_t n_cells, int64_t n_r, void *s
 int launch_dp_step(const ChunkArgs &a, int group, int u, int64_t tile_base, int64_t n_tiles, void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
     if (n_tiles <= 0) return 0;
-    const unsigned g = (unsigned)n_tiles;
-#define GBMW_STEP(G)                                                                       \
-    if (u == 1) k_dp_step<G, true><<<g, kStepThreads, 0, st>>>(a, u, tile_base);          \
-    else k_dp_step<G, false><<<g, kStepThreads, 0, st>>>(a, u, tile_base);
+    // persistent CTAs over contiguous tile ranges, about kStepCtasPerSm per SM
+    static int sms = 0;
+    if (sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
+    }
+    const int64_t max_ctas = (int64_t)sms * kStepCtasPerSm;
+    int tpc = (int)((n_tiles + max_ctas - 1) / max_ctas);
+    if (tpc < 1) tpc = 1;
+    const unsigned grid = (unsigned)((n_tiles + tpc - 1) / tpc);
+#define GBMW_STEP(G)                                                                              \
+    if (u == 1) k_dp_step<G, true><<<grid, kStepThreads, 0, st>>>(a, u, tile_base, n_tiles, tpc);  \
+    else k_dp_step<G, false><<<grid, kStepThreads, 0, st>>>(a, u, tile_base, n_tiles, tpc);
     if (group == 0) { GBMW_STEP(0) }
     else if (group == 1) { GBMW_STEP(1) }
     else { GBMW_STEP(2) }
