@@ -217,6 +217,26 @@ int  gbmw_batch_fetch(gbmw_ctx *ctx, gbmw_batch *batch,
 int  gbmw_batch_timing(const gbmw_batch *batch, gbmw_timing *out);
 int  gbmw_batch_destroy(gbmw_batch *batch);
 
+/* ---- host-side partition logic around the search (parapilot/balance.py) ---- */
+
+/* evaluate_partition (balance.py:98-119): stage_cost of every stage of a partition
+ * under per-layer strategies; out = 3 doubles per stage (time, time_no_sync, peak). */
+int  gbmw_partition_costs(const gbmw_layer *layers, int32_t n_layers, const gbmw_strategy *per_layer,
+                          const int32_t *sizes, int32_t n_stages, const gbmw_env *env,
+                          int64_t micro_batch, int32_t n_micro, double *out);
+/* _init_partition (balance.py:180-236): objective 0 = memory-balanced, 1 = time-balanced. */
+int  gbmw_init_partition(const gbmw_layer *layers, int32_t n_layers, const gbmw_strategy *per_layer,
+                         int32_t n_stages, const gbmw_env *env, int64_t micro_batch, int32_t n_micro,
+                         int32_t objective, int32_t *out_sizes);
+/* _seed_for (balance.py:471-488): the uniform seed strategy, and (optional) its
+ * memory-balanced partition (planner.py:250-253). */
+int  gbmw_seed_for(const gbmw_layer *layers, int32_t n_layers, const gbmw_env *env, int64_t n_devices,
+                   int64_t pp_degree, int64_t micro_batch, int32_t n_micro, double budget,
+                   gbmw_strategy *out_seed, int32_t *out_sizes);
+/* CPython >= 3.12 built-in sum() of floats (Neumaier), as the reference folds sums. */
+double gbmw_py_sum(const double *x, int32_t n);
+const char *gbmw_planner_last_error(void);
+
 #ifdef __cplusplus
 }
 #endif

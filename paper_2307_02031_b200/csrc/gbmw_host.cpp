@@ -68,7 +68,7 @@ struct Chunk {
     int group_lo[kStepGroups + 1] = {0};
     std::vector<int> n_active[kStepGroups];   // per group, per u: problems of the group with U > u
     int Umax = 0, max_k = 1;
-    int64_t n_cells = 0, n_r = 0, n_bcells = 0, n_par = 0, n_tiles = 0;
+    int64_t n_cells = 0, n_r = 0, n_bcells = 0, n_par = 0, n_tiles = 0, n_units = 0;
     size_t small_off = 0;          // byte offset of this chunk's descriptor block in the arena
     // offsets inside the descriptor block
     size_t o_probs, o_cellp, o_rp, o_stepp, o_sweepp, o_cand, o_ccls, o_clsd, o_clst, o_uf, o_uc;
@@ -402,7 +402,7 @@ void prepare_problem(gbmw_batch &b, int pi, std::string *err) {
     h.n_par = (int64_t)(h.U - 1) * h.K * n_e;
     h.n_tiles = (h.n_b + kSweepThreads - 1) / kSweepThreads;
     h.n_step_tiles = (n_e + kStepRows - 1) / kStepRows;
-    h.ws_bytes = (size_t)h.n_cells * (sizeof(Cell) + sizeof(CellMem)) + (size_t)h.n_r * 8 + 8 +
+    h.ws_bytes = (size_t)h.n_cells * (sizeof(Cell) + sizeof(CellMem) + 4) + (size_t)h.U * 4 + (size_t)h.n_r * 8 + 8 +
                  (size_t)h.n_bcells * 32 + (size_t)h.n_par * 2 + (size_t)h.n_tiles * sizeof(SweepPartial);
     h.gpu = true;
 }
@@ -417,7 +417,7 @@ size_t put(std::vector<char> &blob, const T *src, size_t n) {
 
 // chunk workspace layout (byte offsets from ws base)
 struct WsLayout {
-    size_t cells, cmem, rcls, bup, tb0, tb1, fb0, fb1, par, parts, total;
+    size_t cells, cmem, rcls, bup, tb0, tb1, fb0, fb1, par, parts, uniq, nuniq, total;
 };
 WsLayout ws_layout(const Chunk &c) {
     WsLayout w;
@@ -432,6 +432,8 @@ WsLayout ws_layout(const Chunk &c) {
     w.fb1 = o; o = align_up(o + c.n_bcells * 8);
     w.par = o; o = align_up(o + c.n_par * 2);
     w.parts = o; o = align_up(o + c.n_tiles * sizeof(SweepPartial));
+    w.uniq = o; o = align_up(o + c.n_cells * 4);
+    w.nuniq = o; o = align_up(o + c.n_units * 4);
     w.total = o;
     return w;
 }
@@ -529,6 +531,7 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
             clst.insert(clst.end(), h.cls_t.begin(), h.cls_t.end());
             uf.insert(uf.end(), h.unit_first.begin(), h.unit_first.end());
             uc.insert(uc.end(), h.unit_count.begin(), h.unit_count.end());
+            c.n_units += h.U;
             c.Umax = std::max(c.Umax, h.U);
             c.max_k = std::max(c.max_k, h.K);
         }
@@ -690,6 +693,9 @@ ChunkArgs chunk_args(gbmw_batch *b, const Chunk &c, char *ws) {
     a.Fb[1] = (double *)(ws + w.fb1);
     a.par = (uint16_t *)(ws + w.par);
     a.partials = (SweepPartial *)(ws + w.parts);
+    a.uniq = (int32_t *)(ws + w.uniq);
+    a.nuniq = (int32_t *)(ws + w.nuniq);
+    a.n_units = c.n_units;
     a.results = (gbmw_result *)(arena + b->o_results);
     a.plans = (int32_t *)(arena + b->o_plans);
     a.frontier = (double *)(arena + b->o_frontier);
@@ -716,7 +722,7 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
         cudaEventRecord(c.ev[0], st);
         cudaMemsetAsync(a.bup, 0, c.probs.size() * 8, st);
         if ((rc = launch_cost_tables(a, c.n_cells, c.n_r, st))) return cuda_fail(ctx, rc, "K1 launch");
-        c.launches += (c.n_cells > 0) + (c.n_r > 0);
+        c.launches += (c.n_cells > 0) + (c.n_r > 0) + (c.n_units > 0);
         cudaEventRecord(c.ev[1], st);
         if (tables_only) continue;
         for (int u = 1; u < c.Umax; ++u) {

@@ -98,6 +98,9 @@ struct ChunkArgs {
     double *Fb[2];
     uint16_t *par;
     SweepPartial *partials;
+    int32_t *uniq;                // per (unit, slot): strategy indices with distinct (w, k, c, ef), ascending
+    int32_t *nuniq;               // per unit: number of distinct strategies
+    int64_t n_units;
     gbmw_result *results;
     int32_t *plans;
     double *frontier;

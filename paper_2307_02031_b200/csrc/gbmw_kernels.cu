@@ -90,6 +90,37 @@ __global__ void k_cost_r(ChunkArgs a, int64_t n_r) {
         a.class_d[p.class_off + kb], a.class_t[p.class_off + kb], p.micro, env.intra_island_bw);
 }
 
+// Source-side de-duplication (exact): two strategies with identical (weight, class,
+// time_c, ef_true) at unit u produce identical (T, F) in every row of the unit-u
+// table, hence identical candidates for every target; with ties resolved to the
+// first index (T1) the later one can never be an argmin.  K2 relaxes only the
+// first of each group.  One block per problem, one warp per unit.
+__global__ void k_dedupe(ChunkArgs a) {
+    const DevProblem &p = a.probs[blockIdx.x];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    for (int u = warp; u < p.U; u += nwarps) {
+        const Cell *cells = a.cells + p.cell_off + (int64_t)u * p.S;
+        int32_t *uniq = a.uniq + p.cell_off + (int64_t)u * p.S;
+        int count = 0;
+        for (int base = 0; base < p.S; base += 32) {
+            const int i = base + lane;
+            bool keep = false;
+            if (i < p.S) {
+                const Cell ci = cells[i];
+                keep = true;
+                for (int j = 0; j < i; ++j) {
+                    const Cell cj = cells[j];
+                    if (cj.w == ci.w && cj.k == ci.k && cj.c == ci.c && cj.ef == ci.ef) { keep = false; break; }
+                }
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, keep);
+            if (keep) uniq[count + __popc(m & ((1u << lane) - 1u))] = i;
+            count += __popc(m);
+        }
+        if (lane == 0) a.nuniq[p.unit_off + u] = count;
+    }
+}
+
 // ---------------------------------------------------------------- K2: min-plus layer step
 // One thread per bucket row e' of one problem.  Reads the previous unit's table row
 // T_{u-1}[e', :] (reconstructed from the class-reduced B_{u-1}, or the init row for
@@ -105,7 +136,8 @@ constexpr int kStepIB = 4;
 constexpr int kStepCtasPerSm = 6;
 
 struct StepShared {
-    Cell cell[kMaxStrats];
+    Cell cell[kMaxStrats];                // distinct source strategies of unit u-1 (ascending)
+    int idx[kMaxStrats];                  // their strategy index
     double r[kMaxClasses * kMaxClasses];
     int S, K, n_e, q;
     int64_t b_off, par_off, tile0;
@@ -151,6 +183,7 @@ __device__ __forceinline__ void step_rows(const ChunkArgs &a, const StepShared &
             const int i = i0 + b;
             if (i >= S) break;
             const Cell c = sh.cell[i];
+            const int gi = sh.idx[i];
             const double *rrow = sh.r + c.k * K;
             double Tv[NR], Fv[NR];
 #pragma unroll
@@ -168,7 +201,7 @@ __device__ __forceinline__ void step_rows(const ChunkArgs &a, const StepShared &
                         const bool better = (cand < bt[r][kk]) || (cand == bt[r][kk] && Fv[r] < bf[r][kk]);
                         bt[r][kk] = better ? cand : bt[r][kk];
                         bf[r][kk] = better ? Fv[r] : bf[r][kk];
-                        bp[r][kk] = better ? i : bp[r][kk];
+                        bp[r][kk] = better ? gi : bp[r][kk];
                     }
                 }
             }
@@ -210,11 +243,17 @@ __global__ void __launch_bounds__(kStepThreads) k_dp_step(ChunkArgs a, int u, in
             const DevProblem &p = a.probs[q];
             const int S = p.S, K = p.K;
             const Cell *prev_cells = a.cells + p.cell_off + (int64_t)(u - 1) * S;
-            for (int i = threadIdx.x; i < S; i += blockDim.x) sh.cell[i] = prev_cells[i];
+            const int32_t *ul = a.uniq + p.cell_off + (int64_t)(u - 1) * S;
+            const int nu = a.nuniq[p.unit_off + u - 1];
+            for (int n = threadIdx.x; n < nu; n += blockDim.x) {
+                const int j = ul[n];
+                sh.cell[n] = prev_cells[j];
+                sh.idx[n] = j;
+            }
             const double *r_u = a.rcls + p.r_off + (int64_t)u * K * K;
             for (int x = threadIdx.x; x < K * K; x += blockDim.x) sh.r[x] = r_u[x];
             if (threadIdx.x == 0) {
-                sh.S = S; sh.K = K; sh.n_e = (int)(p.n_b + 1); sh.q = q;
+                sh.S = nu; sh.K = K; sh.n_e = (int)(p.n_b + 1); sh.q = q;
                 sh.b_off = p.b_off; sh.par_off = p.par_off; sh.tile0 = a.step_tiles[q];
             }
             __syncthreads();
@@ -486,6 +525,7 @@ int launch_cost_tables(const ChunkArgs &a, int64_t n_cells, int64_t n_r, void *s
     cudaStream_t st = (cudaStream_t)stream;
     if (n_cells > 0) k_cost_cells<<<blocks_for(n_cells, 128), 128, 0, st>>>(a, n_cells);
     if (n_r > 0) k_cost_r<<<blocks_for(n_r, 128), 128, 0, st>>>(a, n_r);
+    if (a.n_units > 0 && a.n_probs > 0) k_dedupe<<<a.n_probs, 128, 0, st>>>(a);
     return (int)cudaGetLastError();
 }
 

@@ -1,0 +1,288 @@
+// gbmw_planner.cpp — host-side pipeline-partition logic around the search
+// (parapilot/balance.py), native so the Algorithm-1/2 drivers are not bound by
+// Python loops: stage costs of a partition, the memory/time-balanced seed
+// partitions (greedy prefix split + hill climbing) and the seed-strategy choice.
+//
+// Bit-exactness: the reference folds stage/pipeline sums with Python's built-in
+// sum(), which since CPython 3.12 is Neumaier-compensated for floats (started from
+// the int 0); py_sum() reproduces that algorithm (Objects/bltinmodule.c,
+// builtin_sum_impl).  Everything else is the cost model of costmodel.cuh.
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/gbmw.h"
+#include "costmodel.cuh"
+
+using namespace gbmw;
+
+namespace {
+
+thread_local std::string g_perr;
+
+int perr(int code, const std::string &m) {
+    g_perr = m;
+    return code;
+}
+
+// CPython >= 3.12 sum() of a float sequence with start 0 (int): the first item is
+// taken as is (0 + x == x), the rest are Neumaier-compensated.
+double py_sum(const double *x, int n) {
+    if (n <= 0) return 0.0;
+    double f = x[0], c = 0.0;
+    for (int i = 1; i < n; ++i) {
+        const double t = f + x[i];
+        if (std::fabs(f) >= std::fabs(x[i])) c += (f - t) + x[i];
+        else c += (x[i] - t) + f;
+        f = t;
+    }
+    if (c != 0.0 && std::isfinite(c)) f += c;
+    return f;
+}
+
+struct StageCostOut { double t, ns, peak; };
+
+// costs.py:322-352 stage_cost over layers[a, b) with per-layer strategies
+int stage_cost_range(const gbmw_layer *layers, const gbmw_strategy *strats, int a, int b, int stage_index,
+                     const gbmw_env &env, int64_t micro, int32_t n_micro, StageCostOut *out) {
+    double t_sum = 0.0, ns_sum = 0.0, ms = 0.0, pf = 0.0, peak = 0.0;
+    for (int l = a; l < b; ++l) {
+        const gbmw_strategy &s = strats[l];
+        const StratDeg d = strat_degrees(s);
+        if (micro % d.data != 0) return perr(GBMW_EMICRO, "micro-batch not divisible by the DP*SDP degree");
+        if (stage_index < 1 || stage_index > s.pp_degree)
+            return perr(GBMW_ESTAGE, "stage_index " + std::to_string(stage_index) + " out of range 1.." +
+                                         std::to_string(s.pp_degree));
+        if (n_micro < 1) return perr(GBMW_ESTAGE, "n_micro must be >= 1, got " + std::to_string(n_micro));
+        double t, tns;
+        layer_times(layers[l], s, d, micro, env, &t, &tns);
+        double r = 0.0;
+        if (l > a) {
+            const StratDeg pd = strat_degrees(strats[l - 1]);
+            r = transform_cost(layers[l].bnd_bytes_per_sample, pd.data, pd.tp, d.data, d.tp, micro,
+                               env.intra_island_bw);
+        }
+        t_sum = t_sum + (t + r);
+        ns_sum = ns_sum + (tns + r);
+    }
+    if (stage_index > 1) {
+        const double p2p = stage_p2p_time(layers[a].bnd_bytes_per_sample, micro, strats[a].pp_degree, env);
+        t_sum = t_sum + p2p;
+        ns_sum = ns_sum + p2p;
+    }
+    for (int l = a; l < b; ++l) {
+        const StratDeg d = strat_degrees(strats[l]);
+        const Mem m = layer_memory(layers[l], d, micro, stage_index, n_micro, env.ms_bytes_per_param_byte);
+        ms = ms + m.o_ms;
+        pf = pf + m.o_f;
+        peak = py_max(peak, pf + m.o_b);
+    }
+    out->t = t_sum;
+    out->ns = ns_sum;
+    out->peak = peak + ms;
+    return GBMW_OK;
+}
+
+// balance.py:98-119 evaluate_partition
+int partition_costs(const gbmw_layer *layers, const gbmw_strategy *strats, const int32_t *sizes, int n_stages,
+                    const gbmw_env &env, int64_t micro, int32_t n_micro, StageCostOut *out) {
+    int a = 0;
+    for (int s = 0; s < n_stages; ++s) {
+        const int rc = stage_cost_range(layers, strats, a, a + sizes[s], s + 1, env, micro, n_micro, &out[s]);
+        if (rc) return rc;
+        a += sizes[s];
+    }
+    return GBMW_OK;
+}
+
+// balance.py:62-77 balance_degrees -> alpha_t or alpha_m
+int balance_alpha(const StageCostOut *sc, int n, bool memory, double *alpha) {
+    std::vector<double> t(n), m(n);
+    double tmax = 0.0, mmax = 0.0;
+    for (int i = 0; i < n; ++i) {
+        t[i] = sc[i].t;
+        m[i] = sc[i].peak;
+        if (i == 0 || t[i] > tmax) tmax = t[i];
+        if (i == 0 || m[i] > mmax) mmax = m[i];
+    }
+    const double tt = py_sum(t.data(), n), tm = py_sum(m.data(), n);
+    if (tt <= 0 || tm <= 0) return perr(GBMW_EINVAL, "stage totals must be positive to define balance degrees");
+    *alpha = memory ? 1.0 - mmax / tm : 1.0 - tmax / tt;
+    return GBMW_OK;
+}
+
+// balance.py:122-139 _greedy_split
+std::vector<int32_t> greedy_split(const std::vector<double> &w, int S) {
+    const int n = (int)w.size();
+    const double total = py_sum(w.data(), n);
+    std::vector<int32_t> sizes;
+    int start = 0;
+    double acc = 0.0;
+    for (int stage = 0; stage < S - 1; ++stage) {
+        const int remaining = S - stage - 1;
+        const double target = (total * (double)(stage + 1)) / (double)S;
+        int end = start;
+        while (end < n - remaining && (acc + w[end] <= target || end < start + 1)) {
+            acc += w[end];
+            ++end;
+        }
+        sizes.push_back(end - start);
+        start = end;
+    }
+    sizes.push_back(n - start);
+    return sizes;
+}
+
+// balance.py:180-212 _init_partition (greedy split + hill climbing on alpha)
+int init_partition(const gbmw_layer *layers, int n_layers, const gbmw_strategy *seeds, int S,
+                   const gbmw_env &env, int64_t micro, int32_t n_micro, bool memory, std::vector<int32_t> &out) {
+    if (S > n_layers)
+        return perr(GBMW_EINVAL, "cannot split " + std::to_string(n_layers) + " layers into " + std::to_string(S) +
+                                     " pipeline stages");
+    std::vector<double> w(n_layers);
+    for (int l = 0; l < n_layers; ++l) {
+        const StratDeg d = strat_degrees(seeds[l]);
+        if (micro % d.data != 0) return perr(GBMW_EMICRO, "micro-batch not divisible by the seed's DP*SDP degree");
+        if (memory) {
+            const Mem m = layer_memory(layers[l], d, micro, seeds[l].pp_degree, n_micro, env.ms_bytes_per_param_byte);
+            w[l] = m.o_f + m.o_ms;
+        } else {
+            double t, tns;
+            layer_times(layers[l], seeds[l], d, micro, env, &t, &tns);
+            w[l] = t;
+        }
+    }
+    std::vector<StageCostOut> sc(S);
+    auto score = [&](const std::vector<int32_t> &sizes, double *alpha) {
+        int rc = partition_costs(layers, seeds, sizes.data(), S, env, micro, n_micro, sc.data());
+        if (rc) return rc;
+        return balance_alpha(sc.data(), S, memory, alpha);
+    };
+    std::vector<int32_t> best = greedy_split(w, S);
+    double best_score;
+    int rc = score(best, &best_score);
+    if (rc) return rc;
+    // balance.py:160-177 _hill_climb, max_rounds = 2 L; neighbour order of _neighbor_moves
+    for (int round = 0; round < 2 * n_layers; ++round) {
+        bool found = false;
+        std::vector<int32_t> round_best;
+        double round_score = best_score;
+        for (int b = 0; b + 1 < S; ++b) {
+            for (int dir = 0; dir < 2; ++dir) {
+                std::vector<int32_t> cand = best;
+                if (dir == 0) {
+                    if (cand[b] <= 1) continue;
+                    cand[b] -= 1; cand[b + 1] += 1;
+                } else {
+                    if (cand[b + 1] <= 1) continue;
+                    cand[b] += 1; cand[b + 1] -= 1;
+                }
+                double s;
+                if ((rc = score(cand, &s))) return rc;
+                if (s > round_score + 1e-15) { round_best = cand; round_score = s; found = true; }
+            }
+        }
+        if (!found) break;
+        best = round_best;
+        best_score = round_score;
+    }
+    out = best;
+    return GBMW_OK;
+}
+
+gbmw_strategy make_seed(int64_t pp, int64_t group, int paradigm) {
+    gbmw_strategy s;
+    std::memset(&s, 0, sizeof(s));
+    s.pp_degree = (int32_t)pp;
+    if (group > 1) {
+        s.n_levels = 1;
+        s.paradigm[0] = paradigm;
+        s.degree[0] = (int32_t)group;
+    }
+    return s;
+}
+
+}  // namespace
+
+extern "C" const char *gbmw_planner_last_error(void) { return g_perr.c_str(); }
+
+extern "C" int gbmw_partition_costs(const gbmw_layer *layers, int32_t n_layers, const gbmw_strategy *per_layer,
+                                    const int32_t *sizes, int32_t n_stages, const gbmw_env *env, int64_t micro_batch,
+                                    int32_t n_micro, double *out) {
+    if (!layers || !per_layer || !sizes || !env || !out || n_stages < 1) return perr(GBMW_EINVAL, "bad arguments");
+    int total = 0;
+    for (int s = 0; s < n_stages; ++s) {
+        if (sizes[s] < 1) return perr(GBMW_EINVAL, "every stage needs at least one layer");
+        total += sizes[s];
+    }
+    if (total != n_layers) return perr(GBMW_EINVAL, "partition does not cover the layers");
+    std::vector<StageCostOut> sc(n_stages);
+    const int rc = partition_costs(layers, per_layer, sizes, n_stages, *env, micro_batch, n_micro, sc.data());
+    if (rc) return rc;
+    for (int s = 0; s < n_stages; ++s) {
+        out[3 * s] = sc[s].t;
+        out[3 * s + 1] = sc[s].ns;
+        out[3 * s + 2] = sc[s].peak;
+    }
+    return GBMW_OK;
+}
+
+extern "C" int gbmw_init_partition(const gbmw_layer *layers, int32_t n_layers, const gbmw_strategy *per_layer,
+                                   int32_t n_stages, const gbmw_env *env, int64_t micro_batch, int32_t n_micro,
+                                   int32_t objective, int32_t *out_sizes) {
+    if (!layers || !per_layer || !env || !out_sizes || n_stages < 1) return perr(GBMW_EINVAL, "bad arguments");
+    std::vector<int32_t> sizes;
+    const int rc = init_partition(layers, n_layers, per_layer, n_stages, *env, micro_batch, n_micro, objective == 0,
+                                  sizes);
+    if (rc) return rc;
+    std::memcpy(out_sizes, sizes.data(), sizeof(int32_t) * n_stages);
+    return GBMW_OK;
+}
+
+extern "C" int gbmw_seed_for(const gbmw_layer *layers, int32_t n_layers, const gbmw_env *env, int64_t n_devices,
+                             int64_t pp_degree, int64_t micro_batch, int32_t n_micro, double budget,
+                             gbmw_strategy *out_seed, int32_t *out_sizes) {
+    // balance.py:471-488 _seed_for (+ the memory-balanced partition of the chosen seed,
+    // which galvatron_base recomputes identically, planner.py:251-253)
+    if (!layers || !env || !out_seed || pp_degree < 1) return perr(GBMW_EINVAL, "bad arguments");
+    const int64_t group = n_devices / pp_degree;
+    std::vector<gbmw_strategy> cands;
+    cands.push_back(make_seed(pp_degree, group, GBMW_DP));
+    if (group > 1) {
+        cands.push_back(make_seed(pp_degree, group, GBMW_SDP));
+        cands.push_back(make_seed(pp_degree, group, GBMW_TP));
+    }
+    std::vector<gbmw_strategy> usable;
+    for (const auto &s : cands)
+        if (micro_batch % strat_degrees(s).data == 0) usable.push_back(s);
+    if (usable.empty()) usable.push_back(cands.back());
+    std::vector<gbmw_strategy> seeds(n_layers);
+    std::vector<int32_t> sizes;
+    std::vector<StageCostOut> sc(pp_degree);
+    for (const auto &seed : usable) {
+        for (auto &x : seeds) x = seed;
+        int rc = init_partition(layers, n_layers, seeds.data(), (int)pp_degree, *env, micro_batch, n_micro, true, sizes);
+        if (rc) return rc;
+        rc = partition_costs(layers, seeds.data(), sizes.data(), (int)pp_degree, *env, micro_batch, n_micro, sc.data());
+        if (rc) return rc;
+        double mx = sc[0].peak;
+        for (int s = 1; s < (int)pp_degree; ++s) mx = py_max(mx, sc[s].peak);
+        if (mx <= budget) {
+            *out_seed = seed;
+            if (out_sizes) std::memcpy(out_sizes, sizes.data(), sizeof(int32_t) * pp_degree);
+            return GBMW_OK;
+        }
+    }
+    *out_seed = usable.back();
+    if (out_sizes) {
+        for (auto &x : seeds) x = usable.back();
+        const int rc = init_partition(layers, n_layers, seeds.data(), (int)pp_degree, *env, micro_batch, n_micro, true,
+                                      sizes);
+        if (rc) return rc;
+        std::memcpy(out_sizes, sizes.data(), sizeof(int32_t) * pp_degree);
+    }
+    return GBMW_OK;
+}
+
+extern "C" double gbmw_py_sum(const double *x, int32_t n) { return py_sum(x, n); }

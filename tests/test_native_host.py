@@ -20,7 +20,8 @@ HEADER = Path(__file__).resolve().parents[1] / "include" / "gbmw.h"
 
 def declared_symbols():
     text = HEADER.read_text()
-    return sorted(set(re.findall(r"^\s*(?:const\s+)?(?:char\s*\*|int|void)\s*\*?\s*(gbmw_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?(?:char\s*\*|int|void|double)\s*\*?\s*(gbmw_\w+)\s*\(",
+                                 text, re.M)))
 
 
 def test_library_exports_every_header_symbol():
