@@ -72,19 +72,8 @@ def describe(args, n_problems):
 
 
 def shard(T, rank, world):
-    """LPT over estimated cost; deterministic across ranks."""
-    order = np.argsort(-T, kind="stable")
-    load = np.zeros(world)
-    owner = np.empty(len(T), dtype=np.int64)
-    for i in order:
-        r = int(np.argmin(load))
-        owner[i] = r
-        load[r] += T[i] + 1e6
-    return np.flatnonzero(owner == rank)
-
-
-def subset(L, S, E, P, idx):
-    return L, S, E, P[idx].copy()
+    from paper_2307_02031_b200.distributed import shard_lpt
+    return shard_lpt(T, world, rank)
 
 
 class ClockSampler:
@@ -233,6 +222,7 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_2307_02031_b200 import _native
+    from paper_2307_02031_b200.distributed import global_winner
     from paper_2307_02031_b200.dpsearch import SearchBatch, run_native_batch
 
     torch.cuda.set_device(local)
@@ -299,18 +289,8 @@ def main():
         t0 = time.perf_counter()
         rc, msg, r, pl, _ = run_native_batch(L, S, E, Pm, ctx)
         assert rc == 0, msg
-        # local argmin over feasible searches: (time, global index)
-        t_bits = np.where(r["feasible"] != 0, r["time_s"], np.inf)
-        j = int(np.argmin(t_bits)) if len(t_bits) else 0
-        rec = torch.tensor([np.float64(t_bits[j]).view(np.int64) if len(t_bits) else np.inf,
-                            int(mine[j]) if len(mine) else -1], dtype=torch.int64, device="cuda")
-        if world > 1:
-            out = torch.empty(world * 2, dtype=torch.int64, device="cuda")
-            dist.all_gather_into_tensor(out, rec)
-            recs = out.view(world, 2).cpu().numpy()
-        else:
-            recs = rec.view(1, 2).cpu().numpy()
-        best = min(((float(np.int64(a).view(np.float64)), int(b)) for a, b in recs), key=lambda x: (x[0], x[1]))
+        # global argmin over feasible searches (min time, then lowest search index): one NCCL all-gather
+        best = global_winner(r["time_s"], r["feasible"], mine, device="cuda")
         torch.cuda.synchronize()
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
         winner = best

@@ -1,0 +1,285 @@
+"""End-to-end planning drivers: Galvatron_Search, Galvatron-Base (Algorithm 1) and
+plan_full with the BMW refinement (Algorithm 2).
+
+Names, signatures, results and tie-breaks of parapilot/planner.py:52-341.  The
+difference is batching: ``galvatron_search_batch`` sends every stage search of
+many (batch, degree, partition) cells to the device in one pass, and
+``galvatron_base`` evaluates a window of batch sizes speculatively and then
+applies the reference's sequential stop rule to the results (T4,
+planner.py:241-277), so the returned plan is the one the reference returns.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from functools import lru_cache
+from typing import Any, Sequence
+
+from .balance import (
+    BalanceReport,
+    PipelinePartition,
+    SearchOutcome,
+    _seed_and_partition,
+    balance_degrees,
+    bi_objective_multi,
+    bi_objective_optimize,
+    init_partition_memory_balanced,
+    partition_layers,
+)
+from .costs import EvalContext, layer_memory, pipeline_cost, stage_cost
+from .dpsearch import StageProblem, dp_search_batch
+from .errors import InfeasiblePlanError
+from .strategies import (
+    ParallelStrategy,
+    candidate_pp_degrees,
+    enumerate_pruned,
+    parse_strategy,
+)
+
+INF = float("inf")
+DEFAULT_GRANULARITY_BYTES = 64 * 2 ** 20
+
+
+@dataclass(frozen=True)
+class PlannerOptions:
+    batch_step: int = 8
+    max_batch: int = 4096
+    granularity_bytes: int = DEFAULT_GRANULARITY_BYTES
+    microbatch_cap_factor: int = 4
+    min_micro_size: int = 1
+    bi_objective: bool = False
+    batch_radius: int = 16
+    fuse_identical: bool = False
+    approx_prev: bool = False
+    batch_window: int = 16          # batch sizes evaluated per device pass by galvatron_base
+
+
+@dataclass(frozen=True)
+class Plan:
+    pp_degree: int
+    partition: tuple[int, ...]
+    n_micro: int
+    batch_size: int
+    strategies: tuple[ParallelStrategy, ...]
+    predicted_time_s: float
+    predicted_throughput: float
+    balance: BalanceReport
+    peak_mem_per_stage: tuple[float, ...]
+
+    def stage_layer_ids(self) -> list[list[int]]:
+        out, a = [], 0
+        for n in self.partition:
+            out.append(list(range(a, a + n)))
+            a += n
+        return out
+
+    def to_document(self, cluster=None) -> dict[str, Any]:
+        stages = [{"layers": [{"id": lid, "strategy": self.strategies[lid].to_string(cluster)} for lid in ids]}
+                  for ids in self.stage_layer_ids()]
+        return {"pp_degree": self.pp_degree, "partition": list(self.partition), "n_micro": self.n_micro,
+                "batch_size": self.batch_size, "stages": stages, "predicted_time_s": self.predicted_time_s,
+                "predicted_throughput": self.predicted_throughput, "alpha_t": self.balance.alpha_t,
+                "alpha_m": self.balance.alpha_m, "peak_mem_per_stage": list(self.peak_mem_per_stage)}
+
+
+def init_microbatch_num(batch: int, pp_degree: int, cap_factor: int = 4, min_micro_size: int = 1) -> int:
+    """Largest divisor of the batch within cap_factor * P (planner.py:110-125)."""
+    if batch < 1:
+        raise ValueError(f"batch must be >= 1, got {batch}")
+    if pp_degree <= 1:
+        return 1
+    for m in range(min(cap_factor * pp_degree, batch), 0, -1):
+        if batch % m == 0 and batch // m >= min_micro_size:
+            return m
+    return 1
+
+
+@lru_cache(maxsize=512)
+def _sset(n_devices: int, pp_degree: int):
+    return enumerate_pruned(n_devices, pp_degree)
+
+
+def galvatron_search_batch(cells: Sequence[tuple], ctx: EvalContext, opts: PlannerOptions = PlannerOptions()):
+    """Many ``galvatron_search(budget, stages, n_devices, batch, pp_degree)`` calls, one device pass."""
+    problems, spans, metas = [], [], []
+    for budget, stages, n_devices, batch, pp in cells:
+        m = init_microbatch_num(batch, pp, opts.microbatch_cap_factor, opts.min_micro_size)
+        micro = batch // m
+        sset = _sset(n_devices, pp)
+        start = len(problems)
+        for idx, layers in enumerate(stages, start=1):
+            problems.append(StageProblem(layers, budget, sset, micro, opts.granularity_bytes, ctx, idx, m,
+                                         opts.fuse_identical, opts.approx_prev))
+        spans.append((start, len(problems)))
+        metas.append(m)
+    results, costs = dp_search_batch(problems, want_stage_cost=True) if problems else ([], [])
+    out = []
+    for (a, b), m in zip(spans, metas):
+        strategies, stage_costs = [], []
+        feasible = True
+        for k in range(a, b):
+            if not results[k].feasible:         # first infeasible stage ends the search (planner.py:159-160)
+                feasible = False
+                break
+            strategies.extend(results[k].strategies)
+            stage_costs.append(costs[k])
+        if not feasible:
+            out.append(SearchOutcome(cost=INF, strategies=None, stage_costs=None, n_micro=m))
+        else:
+            out.append(SearchOutcome(cost=pipeline_cost(stage_costs, m), strategies=tuple(strategies),
+                                     stage_costs=tuple(stage_costs), n_micro=m))
+    return out
+
+
+def galvatron_search(budget_bytes: float, stages: list[list], n_devices: int, batch: int, pp_degree: int,
+                     ctx: EvalContext, opts: PlannerOptions = PlannerOptions()) -> SearchOutcome:
+    """Per-stage dynamic programming under one (batch, pipeline degree) cell (planner.py:128-172)."""
+    return galvatron_search_batch([(budget_bytes, stages, n_devices, batch, pp_degree)], ctx, opts)[0]
+
+
+class GalvatronSearch:
+    """The ``SearchFn`` plan_full hands to Algorithm 2, with a batched form."""
+
+    def __init__(self, ctx: EvalContext, opts: PlannerOptions):
+        self.ctx, self.opts = ctx, opts
+
+    def __call__(self, budget, stages, n_devices, batch, pp_degree) -> SearchOutcome:
+        return galvatron_search(budget, stages, n_devices, batch, pp_degree, self.ctx, self.opts)
+
+    def batch(self, calls) -> list[SearchOutcome]:
+        return galvatron_search_batch(calls, self.ctx, self.opts)
+
+
+def _assemble_plan(model, batch, pp_degree, partition, outcome) -> Plan:
+    return Plan(pp_degree=pp_degree, partition=partition.stage_sizes, n_micro=outcome.n_micro, batch_size=batch,
+                strategies=outcome.strategies, predicted_time_s=outcome.cost,
+                predicted_throughput=batch / outcome.cost, balance=balance_degrees(outcome.stage_costs),
+                peak_mem_per_stage=tuple(sc.peak_mem_bytes for sc in outcome.stage_costs))
+
+
+def _infeasibility_diagnostics(model, ctx, batch, opts) -> dict:
+    """Which constraint bound first at the smallest batch (planner.py:196-228)."""
+    cluster = ctx.cluster
+    diag: dict[str, Any] = {"batch_size": batch, "mem_budget_bytes": cluster.mem_budget_bytes}
+    per_p = {}
+    for p in candidate_pp_degrees(cluster.n_devices):
+        if p > model.num_layers:
+            per_p[p] = "more stages than layers"
+            continue
+        m = init_microbatch_num(batch, p, opts.microbatch_cap_factor, opts.min_micro_size)
+        micro = batch // m
+        usable = [s for s in _sset(cluster.n_devices, p) if micro % s.data_degree == 0]
+        if not usable:
+            per_p[p] = f"micro-batch {micro} indivisible by every strategy"
+            continue
+        min_states = min_total = INF
+        for layer in model.layers:
+            for s in usable:
+                o_f, _, o_ms = layer_memory(layer, s, micro, p, m, ctx.ms_multiplier)
+                min_states = min(min_states, o_ms)
+                min_total = min(min_total, o_f + o_ms)
+        if min_states > cluster.mem_budget_bytes:
+            per_p[p] = "model states alone exceed the budget under every strategy"
+        elif min_total > cluster.mem_budget_bytes:
+            per_p[p] = "single-layer footprint exceeds the budget under every strategy"
+        else:
+            per_p[p] = "no per-layer assignment satisfies the backward-peak budget"
+    diag["per_pp_degree"] = per_p
+    return diag
+
+
+def _base_cells(model, ctx, batch, opts):
+    """(pp_degree, partition, call) for every degree of one batch size (planner.py:243-262)."""
+    cluster = ctx.cluster
+    out = []
+    for p in candidate_pp_degrees(cluster.n_devices):
+        if p > model.num_layers:
+            continue
+        m = init_microbatch_num(batch, p, opts.microbatch_cap_factor, opts.min_micro_size)
+        _, part = _seed_and_partition(model, ctx, cluster.n_devices, p, batch // m, m)
+        out.append((p, part, (cluster.mem_budget_bytes, partition_layers(model, part), cluster.n_devices, batch, p)))
+    return out
+
+
+def galvatron_base(model, cluster, profile, opts: PlannerOptions = PlannerOptions()) -> Plan:
+    """Algorithm 1: raise the batch until no pipeline degree fits (planner.py:231-277)."""
+    ctx = EvalContext(model=model, cluster=cluster, profile=profile)
+    best: Plan | None = None
+    batches = list(range(opts.batch_step, opts.max_batch + 1, opts.batch_step)) if opts.batch_step > 0 else []
+    window = max(1, opts.batch_window)
+    pos = 0
+    while pos < len(batches):
+        chunk = batches[pos:pos + window]
+        pos += len(chunk)
+        per_batch = [_base_cells(model, ctx, b, opts) for b in chunk]
+        flat = [c[2] for cells in per_batch for c in cells]
+        outcomes = galvatron_search_batch(flat, ctx, opts)
+        k = 0
+        for batch, cells in zip(chunk, per_batch):
+            cell_best = None
+            for p, part, _ in cells:
+                outcome = outcomes[k]
+                k += 1
+                if outcome.cost < INF and (cell_best is None or outcome.cost < cell_best[0]):
+                    cell_best = (outcome.cost, p, part, outcome)
+            if cell_best is None:
+                if best is None:
+                    raise InfeasiblePlanError(f"no feasible plan at the smallest batch size {batch}",
+                                              diagnostics=_infeasibility_diagnostics(model, ctx, batch, opts))
+                return best
+            _, p, part, outcome = cell_best
+            plan = _assemble_plan(model, batch, p, part, outcome)
+            if best is None or plan.predicted_throughput > best.predicted_throughput:
+                best = plan
+    return best
+
+
+def plan_full(model, cluster, profile, opts: PlannerOptions = PlannerOptions()) -> Plan:
+    """Algorithm 1, then (with bi_objective) Algorithm 2 around its batch size (planner.py:280-321)."""
+    base = galvatron_base(model, cluster, profile, opts)
+    if not opts.bi_objective:
+        return base
+    ctx = EvalContext(model=model, cluster=cluster, profile=profile)
+    search = GalvatronSearch(ctx, opts)
+
+    def microbatch_policy(batch, pp_degree):
+        return init_microbatch_num(batch, pp_degree, opts.microbatch_cap_factor, opts.min_micro_size)
+
+    b0 = base.batch_size
+    lo = max(opts.batch_step, b0 - opts.batch_radius)
+    batch_sizes = list(range(lo, b0 + opts.batch_radius + 1, opts.batch_step))
+    degrees = [p for p in candidate_pp_degrees(cluster.n_devices) if 2 <= p <= model.num_layers]
+    results = bi_objective_multi(model, ctx, batch_sizes, degrees, search, microbatch_policy)
+    best = base
+    for p in degrees:
+        r = results[p]
+        if not r.feasible:
+            continue
+        plan = _assemble_plan(model, r.batch_size, p, r.partition,
+                              SearchOutcome(r.cost, r.strategies, r.stage_costs, r.n_micro))
+        if plan.predicted_throughput > best.predicted_throughput:
+            best = plan
+        elif (plan.predicted_throughput == best.predicted_throughput
+              and (plan.batch_size, plan.pp_degree) < (best.batch_size, best.pp_degree)):
+            best = plan
+    return best
+
+
+def evaluate_plan_document(doc: dict, model, cluster, profile) -> float:
+    """Re-cost a serialized plan (planner.py:324-341)."""
+    ctx = EvalContext(model=model, cluster=cluster, profile=profile)
+    m = doc["n_micro"]
+    micro = doc["batch_size"] // m
+    costs = []
+    for idx, stage in enumerate(doc["stages"], start=1):
+        layers = [model.layers[e["id"]] for e in stage["layers"]]
+        strats = [parse_strategy(e["strategy"]) for e in stage["layers"]]
+        costs.append(stage_cost(layers, strats, micro, ctx, stage_index=idx, n_micro=m))
+    return pipeline_cost(costs, m)
+
+
+__all__ = [
+    "DEFAULT_GRANULARITY_BYTES", "GalvatronSearch", "Plan", "PlannerOptions", "bi_objective_optimize",
+    "evaluate_plan_document", "galvatron_base", "galvatron_search", "galvatron_search_batch",
+    "init_microbatch_num", "init_partition_memory_balanced", "plan_full", "PipelinePartition",
+]

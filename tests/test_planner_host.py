@@ -1,0 +1,69 @@
+"""Native partition logic (csrc/gbmw_planner.cpp, restating parapilot/balance.py) against
+golden vectors from the live reference: seed choice, memory- and time-balanced
+partitions (greedy split + hill climbing), stage costs of a partition.  CPU only."""
+
+import math
+import random
+
+import numpy as np
+import pytest
+
+from golden_cases import load
+from paper_2307_02031_b200 import _native, balance as B, workloads as W
+from paper_2307_02031_b200.costs import StageCost
+
+
+def _ctx(case):
+    return W.config(case["model"], case["budget"])
+
+
+def test_partitions_match_reference():
+    for c in load("partitions.json"):
+        ctx = _ctx(c)
+        model = ctx.model
+        seeds, pm = B._seed_and_partition(model, ctx, ctx.cluster.n_devices, c["P"], c["micro"], c["n_micro"])
+        assert seeds[0].to_string() == c["seed"], c
+        assert list(pm.stage_sizes) == c["p_m"], c
+        pm2 = B.init_partition_memory_balanced(model, c["P"], seeds, c["micro"], c["n_micro"], ctx)
+        assert list(pm2.stage_sizes) == c["p_m"]
+        pt = B.init_partition_time_balanced(model, c["P"], seeds, c["micro"], c["n_micro"], ctx)
+        assert list(pt.stage_sizes) == c["p_t"], c
+        for part, key in ((pm, "costs_m"), (pt, "costs_t")):
+            costs = B.evaluate_partition(model, part, seeds, c["micro"], c["n_micro"], ctx)
+            got = [[sc.time_s.hex(), sc.time_no_sync_s.hex(), sc.peak_mem_bytes.hex()] for sc in costs]
+            assert got == c[key], (c["model"], c["P"], key)
+
+
+def test_py_sum_matches_cpython():
+    """gbmw_py_sum == CPython's built-in sum() (Neumaier since 3.12) bit for bit."""
+    rng = random.Random(5)
+    for _ in range(2000):
+        n = rng.randint(1, 40)
+        xs = [rng.choice((rng.uniform(0, 1), rng.uniform(0, 1e12), 1e-300 * rng.random(), 1e16, -1e16 * rng.random()))
+              for _ in range(n)]
+        arr = np.array(xs, dtype=np.float64)
+        got = _native.lib().gbmw_py_sum(_native.ptr(arr), n)
+        assert got.hex() == sum(xs).hex()
+
+
+def test_adjust_and_validate_rules():
+    sc = lambda t, m=1.0: StageCost(t, t, m)
+    p = B.PipelinePartition((3, 3, 3))
+    # slowest stage 1 (first max), neighbours tie -> later stage gets the layer
+    assert B.adjust_partition(p, [sc(1.0), sc(5.0), sc(1.0)]).stage_sizes == (3, 2, 4)
+    assert B.adjust_partition(p, [sc(2.0), sc(5.0), sc(1.0)]).stage_sizes == (3, 2, 4)
+    assert B.adjust_partition(p, [sc(1.0), sc(5.0), sc(2.0)]).stage_sizes == (4, 2, 3)
+    # single-layer slowest stage or no faster neighbour: fixed point
+    assert B.adjust_partition(B.PipelinePartition((1, 4)), [sc(5.0), sc(1.0)]).stage_sizes == (1, 4)
+    assert B.adjust_partition(p, [sc(5.0), sc(5.0), sc(5.0)]).stage_sizes == (3, 3, 3)
+    assert B.validate_partition(p, [sc(1.0, 2.0)] * 3, 1.0, 2.0, 2.0)
+    assert not B.validate_partition(p, [sc(1.1, 2.0)] * 3, 1.0, 2.0, 2.0)
+    assert not B.validate_partition(p, [sc(1.0, 2.1)] * 3, 1.0, 3.0, 2.0)
+    with pytest.raises(ValueError):
+        B.PipelinePartition((2, 0))
+
+
+def test_balance_degrees_reference_formula():
+    costs = [StageCost(1.0, 1.0, 4.0), StageCost(3.0, 3.0, 4.0)]
+    r = B.balance_degrees(costs)
+    assert r.alpha_t == 1.0 - 3.0 / 4.0 and r.alpha_m == 0.5
