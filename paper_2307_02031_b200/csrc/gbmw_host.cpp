@@ -402,7 +402,7 @@ void prepare_problem(gbmw_batch &b, int pi, std::string *err) {
     h.n_par = (int64_t)(h.U - 1) * h.K * n_e;
     h.n_tiles = (h.n_b + kSweepThreads - 1) / kSweepThreads;
     h.n_step_tiles = (n_e + kStepRows - 1) / kStepRows;
-    h.ws_bytes = (size_t)h.n_cells * (sizeof(Cell) + sizeof(CellMem) + 4) + (size_t)h.U * 4 + (size_t)h.n_r * 8 + 8 +
+    h.ws_bytes = (size_t)h.n_cells * (sizeof(Cell) + sizeof(CellMem) + 4) + (size_t)h.U * 12 + (size_t)h.n_r * 8 + 8 +
                  (size_t)h.n_bcells * 32 + (size_t)h.n_par * 2 + (size_t)h.n_tiles * sizeof(SweepPartial);
     h.gpu = true;
 }
@@ -417,7 +417,7 @@ size_t put(std::vector<char> &blob, const T *src, size_t n) {
 
 // chunk workspace layout (byte offsets from ws base)
 struct WsLayout {
-    size_t cells, cmem, rcls, bup, tb0, tb1, fb0, fb1, par, parts, uniq, nuniq, total;
+    size_t cells, cmem, rcls, bup, tb0, tb1, fb0, fb1, par, parts, uniq, nuniq, ulo, uhi, ctr, total;
 };
 WsLayout ws_layout(const Chunk &c) {
     WsLayout w;
@@ -434,6 +434,9 @@ WsLayout ws_layout(const Chunk &c) {
     w.parts = o; o = align_up(o + c.n_tiles * sizeof(SweepPartial));
     w.uniq = o; o = align_up(o + c.n_cells * 4);
     w.nuniq = o; o = align_up(o + c.n_units * 4);
+    w.ulo = o; o = align_up(o + c.n_units * 4);
+    w.uhi = o; o = align_up(o + c.n_units * 4);
+    w.ctr = o; o = align_up(o + (size_t)(c.Umax + 1) * kStepGroups * 8);
     w.total = o;
     return w;
 }
@@ -695,6 +698,9 @@ ChunkArgs chunk_args(gbmw_batch *b, const Chunk &c, char *ws) {
     a.partials = (SweepPartial *)(ws + w.parts);
     a.uniq = (int32_t *)(ws + w.uniq);
     a.nuniq = (int32_t *)(ws + w.nuniq);
+    a.unit_lo = (int32_t *)(ws + w.ulo);
+    a.unit_hi = (int32_t *)(ws + w.uhi);
+    a.counters = (unsigned long long *)(ws + w.ctr);
     a.n_units = c.n_units;
     a.results = (gbmw_result *)(arena + b->o_results);
     a.plans = (int32_t *)(arena + b->o_plans);
@@ -721,6 +727,7 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
         c.launches = 0;
         cudaEventRecord(c.ev[0], st);
         cudaMemsetAsync(a.bup, 0, c.probs.size() * 8, st);
+        cudaMemsetAsync(a.counters, 0, (size_t)(c.Umax + 1) * kStepGroups * 8, st);
         if ((rc = launch_cost_tables(a, c.n_cells, c.n_r, st))) return cuda_fail(ctx, rc, "K1 launch");
         c.launches += (c.n_cells > 0) + (c.n_r > 0) + (c.n_units > 0);
         cudaEventRecord(c.ev[1], st);
@@ -730,7 +737,8 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
                 const int lo = c.group_lo[g], na = c.n_active[g][u];
                 if (na == 0) continue;
                 const int64_t base = c.step_prefix[lo], n = c.step_prefix[lo + na] - base;
-                if ((rc = launch_dp_step(a, g, u, base, n, st))) return cuda_fail(ctx, rc, "K2 launch");
+                if ((rc = launch_dp_step(a, g, u, base, n, a.counters + (size_t)u * kStepGroups + g, st)))
+                    return cuda_fail(ctx, rc, "K2 launch");
                 c.launches += 1;
             }
         }

@@ -100,6 +100,8 @@ struct ChunkArgs {
     SweepPartial *partials;
     int32_t *uniq;                // per (unit, slot): strategy indices with distinct (w, k, c, ef), ascending
     int32_t *nuniq;               // per unit: number of distinct strategies
+    int32_t *unit_lo, *unit_hi;   // per unit u: live rows [L_u, H_u] of B_u (see k_dedupe)
+    unsigned long long *counters; // per K2 launch: dynamic tile counter
     int64_t n_units;
     gbmw_result *results;
     int32_t *plans;
@@ -108,7 +110,8 @@ struct ChunkArgs {
 
 // launchers (gbmw_kernels.cu); all asynchronous on `stream`, return cudaError_t as int
 int launch_cost_tables(const ChunkArgs &a, int64_t n_cells, int64_t n_r, void *stream);
-int launch_dp_step(const ChunkArgs &a, int group, int u, int64_t tile_base, int64_t n_tiles, void *stream);
+int launch_dp_step(const ChunkArgs &a, int group, int u, int64_t tile_base, int64_t n_tiles,
+                   unsigned long long *counter, void *stream);
 int launch_sweep(const ChunkArgs &a, int64_t n_tiles, void *stream);
 int launch_finalize(const ChunkArgs &a, void *stream);
 

@@ -95,18 +95,27 @@ __global__ void k_cost_r(ChunkArgs a, int64_t n_r) {
 // table, hence identical candidates for every target; with ties resolved to the
 // first index (T1) the later one can never be an argmin.  K2 relaxes only the
 // first of each group.  One block per problem, one warp per unit.
+//
+// The same pass derives the live row range of every class table B_u: with
+// wmin_v = min_i weight[v][i], T_u is +inf below m_u = sum_{v<=u} wmin_v, so
+// B_u[e'] (built from T_{u-1}[e']) is +inf for e' < L_u = m_{u-1}; and B_u is only
+// ever read at rows e - w_uj <= n_b - wmin_u = H_u.  Rows outside [L_u, H_u] are
+// neither computed nor read (readers treat them as +inf, which they are).
 __global__ void k_dedupe(ChunkArgs a) {
     const DevProblem &p = a.probs[blockIdx.x];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    __shared__ int s_wmin[kMaxUnits];
     for (int u = warp; u < p.U; u += nwarps) {
         const Cell *cells = a.cells + p.cell_off + (int64_t)u * p.S;
         int32_t *uniq = a.uniq + p.cell_off + (int64_t)u * p.S;
         int count = 0;
+        int wmin = 0x7fffffff;
         for (int base = 0; base < p.S; base += 32) {
             const int i = base + lane;
             bool keep = false;
             if (i < p.S) {
                 const Cell ci = cells[i];
+                wmin = min(wmin, ci.w);
                 keep = true;
                 for (int j = 0; j < i; ++j) {
                     const Cell cj = cells[j];
@@ -117,7 +126,21 @@ __global__ void k_dedupe(ChunkArgs a) {
             if (keep) uniq[count + __popc(m & ((1u << lane) - 1u))] = i;
             count += __popc(m);
         }
-        if (lane == 0) a.nuniq[p.unit_off + u] = count;
+        for (int off = 16; off > 0; off >>= 1) wmin = min(wmin, __shfl_xor_sync(0xffffffffu, wmin, off));
+        if (lane == 0) {
+            a.nuniq[p.unit_off + u] = count;
+            s_wmin[u] = wmin;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int64_t top = p.n_b + 1;
+        int64_t acc = 0;
+        for (int u = 0; u < p.U; ++u) {
+            a.unit_lo[p.unit_off + u] = (int32_t)(acc < top ? acc : top);   // L_u = m_{u-1}
+            a.unit_hi[p.unit_off + u] = (int32_t)(p.n_b - s_wmin[u]);       // H_u
+            acc += s_wmin[u];
+        }
     }
 }
 
@@ -133,20 +156,23 @@ __global__ void k_dedupe(ChunkArgs a) {
 // before the first relaxation.  KT is the exact class count (CTA-uniform dispatch)
 // up to 8; KT = kMaxClasses with a runtime guard covers larger strategy spaces.
 constexpr int kStepIB = 4;
-constexpr int kStepCtasPerSm = 6;
+constexpr int kStepChunk = 2;             // tiles taken per atomic grab
 
 struct StepShared {
     Cell cell[kMaxStrats];                // distinct source strategies of unit u-1 (ascending)
     int idx[kMaxStrats];                  // their strategy index
     double r[kMaxClasses * kMaxClasses];
     int S, K, n_e, q;
+    int lo_prev;                          // L_{u-1}: rows of B_{u-1} below are +inf
+    int lo, hi;                           // live rows [L_u, H_u] of B_u
     int64_t b_off, par_off, tile0;
+    int64_t next;
 };
 
 template <int KT, int NR, bool FIRST, bool GUARD>
 __device__ __forceinline__ void step_rows(const ChunkArgs &a, const StepShared &sh, int u, int e0) {
     const int S = sh.S, K = GUARD ? sh.K : KT;
-    const int n_e = sh.n_e;
+    const int n_e = sh.n_e, lo_prev = FIRST ? 0 : sh.lo_prev, lo = sh.lo, hi = sh.hi;
     const double *tin = a.Tb[(u - 1) & 1] + sh.b_off;
     const double *fin = a.Fb[(u - 1) & 1] + sh.b_off;
 
@@ -168,7 +194,7 @@ __device__ __forceinline__ void step_rows(const ChunkArgs &a, const StepShared &
                 const int e = e0 + r * kStepThreads;
                 const int src = e - c.w;
                 T[b][r] = GBMW_INF; F[b][r] = GBMW_INF;
-                if (i < S && src >= 0 && e < n_e) {
+                if (i < S && src >= lo_prev && e <= hi) {
                     if (FIRST) {                   // init row, dpsearch.py:255-259
                         T[b][r] = c.c; F[b][r] = c.ef;
                     } else {                       // T_{u-1}[e,i] = B_{u-1}[e-w,k].t + time_c
@@ -213,7 +239,7 @@ __device__ __forceinline__ void step_rows(const ChunkArgs &a, const StepShared &
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
         const int e = e0 + r * kStepThreads;
-        if (e >= n_e) continue;
+        if (e < lo || e > hi) continue;          // dead rows: never read
 #pragma unroll
         for (int kk = 0; kk < KT; ++kk) {
             if (!GUARD || kk < K) {
@@ -225,64 +251,77 @@ __device__ __forceinline__ void step_rows(const ChunkArgs &a, const StepShared &
     }
 }
 
-// Persistent over a contiguous range of tiles (consecutive tiles mostly belong to the
-// same problem, so its constants are staged once).  GROUP selects the class-count
-// range (step_group): 0 -> K 1..4 with two rows per pass, 1 -> K 5..8 one row per
-// pass, 2 -> K 9..16 generic.  A tile is always kStepRows rows.
+// Persistent CTAs pulling kStepChunk consecutive tiles at a time from a per-launch
+// atomic counter (balances the dead-row skipping); a problem's constants are staged
+// in shared memory once per problem change.  GROUP selects the class-count range
+// (step_group): 0 -> K 1..4 with two rows per pass, 1 -> K 5..8 one row per pass,
+// 2 -> K 9..16 generic.  A tile is always kStepRows rows.
 template <int GROUP, bool FIRST>
 __global__ void __launch_bounds__(kStepThreads) k_dp_step(ChunkArgs a, int u, int64_t tile_base,
-                                                           int64_t n_tiles, int tiles_per_cta) {
+                                                           int64_t n_tiles, unsigned long long *counter) {
     __shared__ StepShared sh;
-    const int64_t t0 = tile_base + (int64_t)blockIdx.x * tiles_per_cta;
-    const int64_t t1 = min(t0 + tiles_per_cta, tile_base + n_tiles);
     int q_prev = -1;
-    for (int64_t tile = t0; tile < t1; ++tile) {
-        const int q = __ldg(a.step_map + tile);
-        if (q != q_prev) {
-            __syncthreads();                       // previous problem's readers are done
+    while (true) {
+        __syncthreads();                           // everyone is done with sh.next / sh tables
+        if (threadIdx.x == 0) sh.next = (int64_t)atomicAdd(counter, (unsigned long long)kStepChunk);
+        __syncthreads();
+        const int64_t c0 = sh.next;
+        if (c0 >= n_tiles) break;
+        const int64_t c1 = min(c0 + kStepChunk, n_tiles);
+        for (int64_t t = c0; t < c1; ++t) {
+            const int64_t tile = tile_base + t;
+            const int q = __ldg(a.step_map + tile);
             const DevProblem &p = a.probs[q];
-            const int S = p.S, K = p.K;
-            const Cell *prev_cells = a.cells + p.cell_off + (int64_t)(u - 1) * S;
-            const int32_t *ul = a.uniq + p.cell_off + (int64_t)(u - 1) * S;
-            const int nu = a.nuniq[p.unit_off + u - 1];
-            for (int n = threadIdx.x; n < nu; n += blockDim.x) {
-                const int j = ul[n];
-                sh.cell[n] = prev_cells[j];
-                sh.idx[n] = j;
-            }
-            const double *r_u = a.rcls + p.r_off + (int64_t)u * K * K;
-            for (int x = threadIdx.x; x < K * K; x += blockDim.x) sh.r[x] = r_u[x];
-            if (threadIdx.x == 0) {
-                sh.S = nu; sh.K = K; sh.n_e = (int)(p.n_b + 1); sh.q = q;
-                sh.b_off = p.b_off; sh.par_off = p.par_off; sh.tile0 = a.step_tiles[q];
-            }
-            __syncthreads();
-            q_prev = q;
-        }
-        const int base = (int)(tile - sh.tile0) * kStepRows + threadIdx.x;
-        const int K = sh.K;
-        if (GROUP == 0) {
-            switch (K) {
-                case 1: step_rows<1, 2, FIRST, false>(a, sh, u, base); break;
-                case 2: step_rows<2, 2, FIRST, false>(a, sh, u, base); break;
-                case 3: step_rows<3, 2, FIRST, false>(a, sh, u, base); break;
-                default: step_rows<4, 2, FIRST, false>(a, sh, u, base); break;
-            }
-        } else if (GROUP == 1) {
-#pragma unroll 1
-            for (int pass = 0; pass < 2; ++pass) {
-                const int e0 = base + pass * kStepThreads;
-                switch (K) {
-                    case 5: step_rows<5, 1, FIRST, false>(a, sh, u, e0); break;
-                    case 6: step_rows<6, 1, FIRST, false>(a, sh, u, e0); break;
-                    case 7: step_rows<7, 1, FIRST, false>(a, sh, u, e0); break;
-                    default: step_rows<8, 1, FIRST, false>(a, sh, u, e0); break;
+            const int64_t first_row = (tile - a.step_tiles[q]) * kStepRows;
+            const int lo = a.unit_lo[p.unit_off + u], hi = a.unit_hi[p.unit_off + u];
+            if (first_row > hi || first_row + kStepRows - 1 < lo) continue;   // dead tile (CTA-uniform)
+            if (q != q_prev) {
+                __syncthreads();                   // previous problem's readers are done
+                const int S = p.S, K = p.K;
+                const Cell *prev_cells = a.cells + p.cell_off + (int64_t)(u - 1) * S;
+                const int32_t *ul = a.uniq + p.cell_off + (int64_t)(u - 1) * S;
+                const int nu = a.nuniq[p.unit_off + u - 1];
+                for (int n = threadIdx.x; n < nu; n += blockDim.x) {
+                    const int j = ul[n];
+                    sh.cell[n] = prev_cells[j];
+                    sh.idx[n] = j;
                 }
+                const double *r_u = a.rcls + p.r_off + (int64_t)u * K * K;
+                for (int x = threadIdx.x; x < K * K; x += blockDim.x) sh.r[x] = r_u[x];
+                if (threadIdx.x == 0) {
+                    sh.S = nu; sh.K = K; sh.n_e = (int)(p.n_b + 1); sh.q = q;
+                    sh.lo_prev = a.unit_lo[p.unit_off + u - 1];
+                    sh.lo = lo; sh.hi = hi;
+                    sh.b_off = p.b_off; sh.par_off = p.par_off; sh.tile0 = a.step_tiles[q];
+                }
+                __syncthreads();
+                q_prev = q;
             }
-        } else {
+            const int base = (int)first_row + threadIdx.x;
+            const int K = sh.K;
+            if (GROUP == 0) {
+                switch (K) {
+                    case 1: step_rows<1, 2, FIRST, false>(a, sh, u, base); break;
+                    case 2: step_rows<2, 2, FIRST, false>(a, sh, u, base); break;
+                    case 3: step_rows<3, 2, FIRST, false>(a, sh, u, base); break;
+                    default: step_rows<4, 2, FIRST, false>(a, sh, u, base); break;
+                }
+            } else if (GROUP == 1) {
 #pragma unroll 1
-            for (int pass = 0; pass < 2; ++pass)
-                step_rows<kMaxClasses, 1, FIRST, true>(a, sh, u, base + pass * kStepThreads);
+                for (int pass = 0; pass < 2; ++pass) {
+                    const int e0 = base + pass * kStepThreads;
+                    switch (K) {
+                        case 5: step_rows<5, 1, FIRST, false>(a, sh, u, e0); break;
+                        case 6: step_rows<6, 1, FIRST, false>(a, sh, u, e0); break;
+                        case 7: step_rows<7, 1, FIRST, false>(a, sh, u, e0); break;
+                        default: step_rows<8, 1, FIRST, false>(a, sh, u, e0); break;
+                    }
+                }
+            } else {
+#pragma unroll 1
+                for (int pass = 0; pass < 2; ++pass)
+                    step_rows<kMaxClasses, 1, FIRST, true>(a, sh, u, base + pass * kStepThreads);
+            }
         }
     }
 }
@@ -293,12 +332,13 @@ struct RowCtx {
     const int32_t *w; const int32_t *k; const double *c; const double *ef;
     const double *tin; const double *fin;
     int64_t n_e;
+    int64_t lo;        // rows of B_{U-1} below L_{U-1} are +inf (never written)
     bool init;
 };
 
 __device__ __forceinline__ void row_value(const RowCtx &r, int64_t e, int j, double &T, double &F) {
     const int w = r.w[j];
-    if (e < w) { T = GBMW_INF; F = GBMW_INF; return; }
+    if (e - w < r.lo) { T = GBMW_INF; F = GBMW_INF; return; }
     if (r.init) { T = r.c[j]; F = r.ef[j]; return; }
     const int64_t src = (int64_t)r.k[j] * r.n_e + (e - w);
     T = r.tin[src] + r.c[j];
@@ -375,6 +415,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(ChunkArgs a) {
     r.w = sW; r.k = sK; r.c = sC; r.ef = sE;
     r.n_e = p.n_b + 1;
     r.init = (last == 0);
+    r.lo = (last == 0) ? 0 : a.unit_lo[p.unit_off + last];
     r.tin = a.Tb[last & 1] + p.b_off;
     r.fin = a.Fb[last & 1] + p.b_off;
 
@@ -529,23 +570,32 @@ int launch_cost_tables(const ChunkArgs &a, int64_t n_cells, int64_t n_r, void *s
     return (int)cudaGetLastError();
 }
 
-int launch_dp_step(const ChunkArgs &a, int group, int u, int64_t tile_base, int64_t n_tiles, void *stream) {
+int launch_dp_step(const ChunkArgs &a, int group, int u, int64_t tile_base, int64_t n_tiles,
+                   unsigned long long *counter, void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
     if (n_tiles <= 0) return 0;
-    // persistent CTAs over contiguous tile ranges, about kStepCtasPerSm per SM
+    // persistent grid: as many CTAs as fit at once (per instantiation), capped by the work
     static int sms = 0;
+    static int occ[kStepGroups][2] = {{0}};
     if (sms == 0) {
         int dev = 0;
         cudaGetDevice(&dev);
         if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
     }
-    const int64_t max_ctas = (int64_t)sms * kStepCtasPerSm;
-    int tpc = (int)((n_tiles + max_ctas - 1) / max_ctas);
-    if (tpc < 1) tpc = 1;
-    const unsigned grid = (unsigned)((n_tiles + tpc - 1) / tpc);
-#define GBMW_STEP(G)                                                                              \
-    if (u == 1) k_dp_step<G, true><<<grid, kStepThreads, 0, st>>>(a, u, tile_base, n_tiles, tpc);  \
-    else k_dp_step<G, false><<<grid, kStepThreads, 0, st>>>(a, u, tile_base, n_tiles, tpc);
+    const int fi = (u == 1) ? 1 : 0;
+    if (occ[group][fi] == 0) {
+        int n = 1;
+        if (group == 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fi ? k_dp_step<0, true> : k_dp_step<0, false>, kStepThreads, 0);
+        else if (group == 1) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fi ? k_dp_step<1, true> : k_dp_step<1, false>, kStepThreads, 0);
+        else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fi ? k_dp_step<2, true> : k_dp_step<2, false>, kStepThreads, 0);
+        occ[group][fi] = n > 0 ? n : 1;
+    }
+    const int64_t max_ctas = (int64_t)sms * occ[group][fi];
+    const int64_t want = (n_tiles + kStepChunk - 1) / kStepChunk;
+    const unsigned grid = (unsigned)(want < max_ctas ? want : max_ctas);
+#define GBMW_STEP(G)                                                                                \
+    if (u == 1) k_dp_step<G, true><<<grid, kStepThreads, 0, st>>>(a, u, tile_base, n_tiles, counter);  \
+    else k_dp_step<G, false><<<grid, kStepThreads, 0, st>>>(a, u, tile_base, n_tiles, counter);
     if (group == 0) { GBMW_STEP(0) }
     else if (group == 1) { GBMW_STEP(1) }
     else { GBMW_STEP(2) }
