@@ -137,13 +137,14 @@ typedef struct gbmw_timing {
     int32_t n_launches;        /* kernels launched by the last run */
     double  transitions;       /* algorithmic sum over problems of (U-1) * n_e * S^2 */
     double  row_steps;         /* sum over problems of (U-1) * n_e */
-    double  dp_bytes;          /* algorithmic HBM bytes of K2 */
+    double  dp_bytes;          /* algorithmic HBM bytes of K2: 34 B per live class cell */
     double  dp_cells;          /* sum over problems of (U-1) * n_e * S * K (relaxations executed) */
     double  h2d_bytes;         /* bytes uploaded by gbmw_batch_create */
     double  d2h_bytes;         /* bytes downloaded by the last gbmw_batch_fetch */
     double  prep_ms;           /* host wall time of gbmw_batch_create before the upload */
     double  upload_ms;         /* host wall time of the arena allocation + upload */
     double  fetch_ms;          /* host wall time of the last gbmw_batch_fetch */
+    double  live_cells;        /* class cells K2 computed (rows inside [L_u, H_u], times K) */
 } gbmw_timing;
 
 typedef struct gbmw_ctx gbmw_ctx;

@@ -52,7 +52,8 @@ class Timing(ctypes.Structure):
                 ("transitions", ctypes.c_double), ("row_steps", ctypes.c_double),
                 ("dp_bytes", ctypes.c_double), ("dp_cells", ctypes.c_double),
                 ("h2d_bytes", ctypes.c_double), ("d2h_bytes", ctypes.c_double),
-                ("prep_ms", ctypes.c_double), ("upload_ms", ctypes.c_double), ("fetch_ms", ctypes.c_double)]
+                ("prep_ms", ctypes.c_double), ("upload_ms", ctypes.c_double), ("fetch_ms", ctypes.c_double),
+                ("live_cells", ctypes.c_double)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}

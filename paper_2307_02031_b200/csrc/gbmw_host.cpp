@@ -108,7 +108,7 @@ struct gbmw_batch {
     // device arena: inputs | chunk descriptor blocks | outputs
     void *arena = nullptr;
     size_t arena_size = 0;
-    size_t o_layers = 0, o_strats = 0, o_envs = 0, o_results = 0, o_plans = 0, o_frontier = 0;
+    size_t o_layers = 0, o_strats = 0, o_envs = 0, o_results = 0, o_plans = 0, o_frontier = 0, o_stats = 0;
     size_t max_ws = 0;
     gbmw_timing timing{};
     bool ran = false;
@@ -585,6 +585,7 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
     b->o_results = o; o = align_up(o + b->problems.size() * sizeof(gbmw_result));
     b->o_plans = o; o = align_up(o + (size_t)b->total_plan * sizeof(int32_t));
     b->o_frontier = o; o = align_up(o + (size_t)b->total_frontier * sizeof(double));
+    b->o_stats = o; o = align_up(o + (b->chunks.size() + 1) * 8);
     b->arena_size = std::max<size_t>(o, 256);
     for (Chunk &c : b->chunks) c.small_off += o_blob;
     cudaSetDevice(ctx->device);
@@ -645,7 +646,6 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
         b->timing.row_steps += rows;
         b->timing.dp_cells += rows * h.S * h.K;
         // K2 compulsory bytes: B_{u-1} (T,F) read once + B_u written + argmin written
-        b->timing.dp_bytes += rows * h.K * (16.0 + 16.0 + 2.0);
     }
     b->timing.n_chunks = (int32_t)b->chunks.size();
     *out = b;
@@ -663,7 +663,7 @@ int ensure_ws(gbmw_ctx *ctx, size_t bytes) {
     return GBMW_OK;
 }
 
-ChunkArgs chunk_args(gbmw_batch *b, const Chunk &c, char *ws) {
+ChunkArgs chunk_args(gbmw_batch *b, const Chunk &c, char *ws, size_t chunk_index) {
     char *arena = (char *)b->arena;
     char *sm = arena + c.small_off;
     ChunkArgs a;
@@ -705,6 +705,7 @@ ChunkArgs chunk_args(gbmw_batch *b, const Chunk &c, char *ws) {
     a.results = (gbmw_result *)(arena + b->o_results);
     a.plans = (int32_t *)(arena + b->o_plans);
     a.frontier = (double *)(arena + b->o_frontier);
+    a.live_cells = (unsigned long long *)(arena + b->o_stats) + chunk_index;
     return a;
 }
 
@@ -720,10 +721,11 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
     b->timing.total_ms = b->timing.dp_ms = b->timing.sweep_ms = b->timing.tables_ms = b->timing.finalize_ms = 0.f;
     b->timing.n_launches = 0;
     cudaStream_t st = ctx->stream;
+    cudaMemsetAsync((char *)b->arena + b->o_stats, 0, (b->chunks.size() + 1) * 8, st);
     for (Chunk &c : b->chunks) {
         for (auto &e : c.ev)
             if (!e) cudaEventCreate(&e);
-        ChunkArgs a = chunk_args(b, c, (char *)ctx->ws);
+        ChunkArgs a = chunk_args(b, c, (char *)ctx->ws, (size_t)(&c - b->chunks.data()));
         c.launches = 0;
         cudaEventRecord(c.ev[0], st);
         cudaMemsetAsync(a.bup, 0, c.probs.size() * 8, st);
@@ -760,6 +762,15 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
         cudaEventElapsedTime(&t, c.ev[2], c.ev[3]); b->timing.sweep_ms += t;
         cudaEventElapsedTime(&t, c.ev[3], c.ev[4]); b->timing.finalize_ms += t;
         cudaEventElapsedTime(&t, c.ev[0], c.ev[4]); b->timing.total_ms += t;
+    }
+    if (!tables_only && !b->chunks.empty()) {
+        // K2 algorithmic bytes = 34 B per live class cell
+        std::vector<unsigned long long> live(b->chunks.size());
+        cudaMemcpy(live.data(), (char *)b->arena + b->o_stats, live.size() * 8, cudaMemcpyDeviceToHost);
+        double cells = 0.0;
+        for (auto v : live) cells += (double)v;
+        b->timing.dp_bytes = cells * (16.0 + 16.0 + 2.0);
+        b->timing.live_cells = cells;
     }
     b->ran = true;
     return GBMW_OK;

@@ -136,11 +136,16 @@ __global__ void k_dedupe(ChunkArgs a) {
     if (threadIdx.x == 0) {
         const int64_t top = p.n_b + 1;
         int64_t acc = 0;
+        unsigned long long live = 0;
         for (int u = 0; u < p.U; ++u) {
-            a.unit_lo[p.unit_off + u] = (int32_t)(acc < top ? acc : top);   // L_u = m_{u-1}
-            a.unit_hi[p.unit_off + u] = (int32_t)(p.n_b - s_wmin[u]);       // H_u
+            const int64_t lo = acc < top ? acc : top, hi = p.n_b - s_wmin[u];
+            a.unit_lo[p.unit_off + u] = (int32_t)lo;                          // L_u = m_{u-1}
+            a.unit_hi[p.unit_off + u] = (int32_t)hi;                          // H_u
+            if (u >= 1 && hi >= lo) live += (unsigned long long)(hi - lo + 1);
             acc += s_wmin[u];
         }
+        // live class cells written by K2 (algorithmic-bytes accounting)
+        atomicAdd(a.live_cells, live * (unsigned long long)p.K);
     }
 }
 
