@@ -417,7 +417,7 @@ size_t put(std::vector<char> &blob, const T *src, size_t n) {
 
 // chunk workspace layout (byte offsets from ws base)
 struct WsLayout {
-    size_t cells, cmem, rcls, bup, tb0, tb1, fb0, fb1, par, parts, uniq, nuniq, ulo, uhi, ctr, total;
+    size_t cells, cmem, rcls, bup, tf0, tf1, par, parts, uniq, nuniq, ulo, uhi, ctr, total;
 };
 WsLayout ws_layout(const Chunk &c) {
     WsLayout w;
@@ -426,10 +426,8 @@ WsLayout ws_layout(const Chunk &c) {
     w.cmem = o; o = align_up(o + c.n_cells * sizeof(CellMem));
     w.rcls = o; o = align_up(o + c.n_r * 8);
     w.bup = o; o = align_up(o + c.probs.size() * 8);
-    w.tb0 = o; o = align_up(o + c.n_bcells * 8);
-    w.tb1 = o; o = align_up(o + c.n_bcells * 8);
-    w.fb0 = o; o = align_up(o + c.n_bcells * 8);
-    w.fb1 = o; o = align_up(o + c.n_bcells * 8);
+    w.tf0 = o; o = align_up(o + c.n_bcells * sizeof(TFCell));
+    w.tf1 = o; o = align_up(o + c.n_bcells * sizeof(TFCell));
     w.par = o; o = align_up(o + c.n_par * 2);
     w.parts = o; o = align_up(o + c.n_tiles * sizeof(SweepPartial));
     w.uniq = o; o = align_up(o + c.n_cells * 4);
@@ -690,10 +688,8 @@ ChunkArgs chunk_args(gbmw_batch *b, const Chunk &c, char *ws, size_t chunk_index
     a.cmem = (CellMem *)(ws + w.cmem);
     a.rcls = (double *)(ws + w.rcls);
     a.bup = (unsigned long long *)(ws + w.bup);
-    a.Tb[0] = (double *)(ws + w.tb0);
-    a.Tb[1] = (double *)(ws + w.tb1);
-    a.Fb[0] = (double *)(ws + w.fb0);
-    a.Fb[1] = (double *)(ws + w.fb1);
+    a.TF[0] = (TFCell *)(ws + w.tf0);
+    a.TF[1] = (TFCell *)(ws + w.tf1);
     a.par = (uint16_t *)(ws + w.par);
     a.partials = (SweepPartial *)(ws + w.parts);
     a.uniq = (int32_t *)(ws + w.uniq);

@@ -6,7 +6,7 @@
 //   cells[U][S]        {time_c, ef_true, weight, class}        dpsearch.py:131-145
 //   cmem [U][S]        {O_f, O_b, O_ms} of one layer of the unit (E_all check)
 //   rcls [U][K][K]     transform cost between classes for unit u (dpsearch.py:149-160)
-//   Tb/Fb[2][K][n_e]   class-reduced frontier B_u (ping-pong), column-major by class
+//   TF[2][K][n_e]      class-reduced frontier B_u = (t, f) pairs (ping-pong), column-major by class
 //   par  [U-1][K][n_e] argmin strategy of B_u (uint16)
 // B_u[e'][k] = lexmin_i (T_{u-1}[e',i] + R_u[cls(i),k], F_{u-1}[e',i], i), from which
 // the reference table is T_u[e,j] = B_u[e-w_uj][cls j].t + time_c[u,j]  (exact
@@ -49,7 +49,7 @@ struct DevProblem {
     double budget;
     int64_t cell_off;       // into cells / cmem  (U*S)
     int64_t r_off;          // into rcls (U*K*K)
-    int64_t b_off;          // into Tb/Fb buffers (K*n_e)
+    int64_t b_off;          // into the TF buffers (K*n_e)
     int64_t par_off;        // into par ((U-1)*K*n_e)
     int64_t tile_off;       // into sweep partials (n_sweep_tiles)
     int64_t plan_off;       // into plans (n_layers)
@@ -62,6 +62,11 @@ struct DevProblem {
     int32_t result_index;   // slot in the batch result array
     int32_t n_sweep_tiles;
     int32_t pad_;
+};
+
+struct alignas(16) TFCell {
+    double t;       // lexmin candidate time
+    double f;       // accumulated true forward bytes of its path (tie-break)
 };
 
 struct SweepPartial {
@@ -94,8 +99,7 @@ struct ChunkArgs {
     CellMem *cmem;
     double *rcls;
     unsigned long long *bup;      // per problem, bits of max O_b (all >= 0)
-    double *Tb[2];
-    double *Fb[2];
+    TFCell *TF[2];
     uint16_t *par;
     SweepPartial *partials;
     int32_t *uniq;                // per (unit, slot): strategy indices with distinct (w, k, c, ef), ascending

@@ -157,11 +157,11 @@ __global__ void k_dedupe(ChunkArgs a) {
 //
 // Each thread owns NR rows (stride kStepThreads) so the per-strategy constants and
 // transform costs read from shared memory are shared by its rows; the strategy loop
-// is processed in batches of kStepIB so 2*NR*kStepIB independent loads are in flight
+// is processed in batches of IB so 2*NR*IB independent 16-byte loads are in flight
 // before the first relaxation.  KT is the exact class count (CTA-uniform dispatch)
 // up to 8; KT = kMaxClasses with a runtime guard covers larger strategy spaces.
-constexpr int kStepIB = 4;
-constexpr int kStepChunk = 2;             // tiles taken per atomic grab
+constexpr int kStepIB = 4;            // strategy batch (K >= 5 groups); K <= 4 uses 2
+constexpr int kStepChunk = 4;             // tiles taken per atomic grab
 
 struct StepShared {
     Cell cell[kMaxStrats];                // distinct source strategies of unit u-1 (ascending)
@@ -174,12 +174,11 @@ struct StepShared {
     int64_t next;
 };
 
-template <int KT, int NR, bool FIRST, bool GUARD>
+template <int KT, int NR, int IB, bool FIRST, bool GUARD>
 __device__ __forceinline__ void step_rows(const ChunkArgs &a, const StepShared &sh, int u, int e0) {
     const int S = sh.S, K = GUARD ? sh.K : KT;
     const int n_e = sh.n_e, lo_prev = FIRST ? 0 : sh.lo_prev, lo = sh.lo, hi = sh.hi;
-    const double *tin = a.Tb[(u - 1) & 1] + sh.b_off;
-    const double *fin = a.Fb[(u - 1) & 1] + sh.b_off;
+    const TFCell *bin = a.TF[(u - 1) & 1] + sh.b_off;
 
     double bt[NR][KT], bf[NR][KT];
     int bp[NR][KT];
@@ -188,10 +187,10 @@ __device__ __forceinline__ void step_rows(const ChunkArgs &a, const StepShared &
 #pragma unroll
         for (int kk = 0; kk < KT; ++kk) { bt[r][kk] = GBMW_INF; bf[r][kk] = GBMW_INF; bp[r][kk] = 0; }
 
-    for (int i0 = 0; i0 < S; i0 += kStepIB) {
-        double T[kStepIB][NR], F[kStepIB][NR];
+    for (int i0 = 0; i0 < S; i0 += IB) {
+        double T[IB][NR], F[kStepIB][NR];
 #pragma unroll
-        for (int b = 0; b < kStepIB; ++b) {
+        for (int b = 0; b < IB; ++b) {
             const int i = i0 + b;
             const Cell c = sh.cell[i < S ? i : 0];
 #pragma unroll
@@ -203,14 +202,15 @@ __device__ __forceinline__ void step_rows(const ChunkArgs &a, const StepShared &
                     if (FIRST) {                   // init row, dpsearch.py:255-259
                         T[b][r] = c.c; F[b][r] = c.ef;
                     } else {                       // T_{u-1}[e,i] = B_{u-1}[e-w,k].t + time_c
-                        T[b][r] = __ldg(tin + c.k * n_e + src);
-                        F[b][r] = __ldg(fin + c.k * n_e + src);
+                        const double2 v = __ldg(reinterpret_cast<const double2 *>(bin + c.k * n_e + src));
+                        T[b][r] = v.x;
+                        F[b][r] = v.y;
                     }
                 }
             }
         }
 #pragma unroll
-        for (int b = 0; b < kStepIB; ++b) {
+        for (int b = 0; b < IB; ++b) {
             const int i = i0 + b;
             if (i >= S) break;
             const Cell c = sh.cell[i];
@@ -238,8 +238,7 @@ __device__ __forceinline__ void step_rows(const ChunkArgs &a, const StepShared &
             }
         }
     }
-    double *tout = a.Tb[u & 1] + sh.b_off;
-    double *fout = a.Fb[u & 1] + sh.b_off;
+    TFCell *bout = a.TF[u & 1] + sh.b_off;
     uint16_t *pout = a.par + sh.par_off + (int64_t)(u - 1) * K * n_e;
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
@@ -248,8 +247,7 @@ __device__ __forceinline__ void step_rows(const ChunkArgs &a, const StepShared &
 #pragma unroll
         for (int kk = 0; kk < KT; ++kk) {
             if (!GUARD || kk < K) {
-                tout[kk * n_e + e] = bt[r][kk];
-                fout[kk * n_e + e] = bf[r][kk];
+                reinterpret_cast<double2 *>(bout)[kk * n_e + e] = make_double2(bt[r][kk], bf[r][kk]);
                 pout[kk * n_e + e] = (uint16_t)bp[r][kk];
             }
         }
@@ -262,7 +260,7 @@ __device__ __forceinline__ void step_rows(const ChunkArgs &a, const StepShared &
 // (step_group): 0 -> K 1..4 with two rows per pass, 1 -> K 5..8 one row per pass,
 // 2 -> K 9..16 generic.  A tile is always kStepRows rows.
 template <int GROUP, bool FIRST>
-__global__ void __launch_bounds__(kStepThreads) k_dp_step(ChunkArgs a, int u, int64_t tile_base,
+__global__ void __launch_bounds__(kStepThreads, GROUP == 0 ? 3 : 2) k_dp_step(ChunkArgs a, int u, int64_t tile_base,
                                                            int64_t n_tiles, unsigned long long *counter) {
     __shared__ StepShared sh;
     int q_prev = -1;
@@ -306,26 +304,26 @@ __global__ void __launch_bounds__(kStepThreads) k_dp_step(ChunkArgs a, int u, in
             const int K = sh.K;
             if (GROUP == 0) {
                 switch (K) {
-                    case 1: step_rows<1, 2, FIRST, false>(a, sh, u, base); break;
-                    case 2: step_rows<2, 2, FIRST, false>(a, sh, u, base); break;
-                    case 3: step_rows<3, 2, FIRST, false>(a, sh, u, base); break;
-                    default: step_rows<4, 2, FIRST, false>(a, sh, u, base); break;
+                    case 1: step_rows<1, 2, 2, FIRST, false>(a, sh, u, base); break;
+                    case 2: step_rows<2, 2, 2, FIRST, false>(a, sh, u, base); break;
+                    case 3: step_rows<3, 2, 2, FIRST, false>(a, sh, u, base); break;
+                    default: step_rows<4, 2, 2, FIRST, false>(a, sh, u, base); break;
                 }
             } else if (GROUP == 1) {
 #pragma unroll 1
                 for (int pass = 0; pass < 2; ++pass) {
                     const int e0 = base + pass * kStepThreads;
                     switch (K) {
-                        case 5: step_rows<5, 1, FIRST, false>(a, sh, u, e0); break;
-                        case 6: step_rows<6, 1, FIRST, false>(a, sh, u, e0); break;
-                        case 7: step_rows<7, 1, FIRST, false>(a, sh, u, e0); break;
-                        default: step_rows<8, 1, FIRST, false>(a, sh, u, e0); break;
+                        case 5: step_rows<5, 1, kStepIB, FIRST, false>(a, sh, u, e0); break;
+                        case 6: step_rows<6, 1, kStepIB, FIRST, false>(a, sh, u, e0); break;
+                        case 7: step_rows<7, 1, kStepIB, FIRST, false>(a, sh, u, e0); break;
+                        default: step_rows<8, 1, kStepIB, FIRST, false>(a, sh, u, e0); break;
                     }
                 }
             } else {
 #pragma unroll 1
                 for (int pass = 0; pass < 2; ++pass)
-                    step_rows<kMaxClasses, 1, FIRST, true>(a, sh, u, base + pass * kStepThreads);
+                    step_rows<kMaxClasses, 1, kStepIB, FIRST, true>(a, sh, u, base + pass * kStepThreads);
             }
         }
     }
@@ -335,7 +333,7 @@ __global__ void __launch_bounds__(kStepThreads) k_dp_step(ChunkArgs a, int u, in
 // reference table of the last unit at row e, strategy j
 struct RowCtx {
     const int32_t *w; const int32_t *k; const double *c; const double *ef;
-    const double *tin; const double *fin;
+    const TFCell *bin;
     int64_t n_e;
     int64_t lo;        // rows of B_{U-1} below L_{U-1} are +inf (never written)
     bool init;
@@ -346,8 +344,9 @@ __device__ __forceinline__ void row_value(const RowCtx &r, int64_t e, int j, dou
     if (e - w < r.lo) { T = GBMW_INF; F = GBMW_INF; return; }
     if (r.init) { T = r.c[j]; F = r.ef[j]; return; }
     const int64_t src = (int64_t)r.k[j] * r.n_e + (e - w);
-    T = r.tin[src] + r.c[j];
-    F = r.fin[src] + r.ef[j];
+    const double2 v = __ldg(reinterpret_cast<const double2 *>(r.bin + src));
+    T = v.x + r.c[j];
+    F = v.y + r.ef[j];
 }
 
 // Walk the argmin pointers back from (last unit, e, j) (dpsearch.py:292-301).
@@ -421,8 +420,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(ChunkArgs a) {
     r.n_e = p.n_b + 1;
     r.init = (last == 0);
     r.lo = (last == 0) ? 0 : a.unit_lo[p.unit_off + last];
-    r.tin = a.Tb[last & 1] + p.b_off;
-    r.fin = a.Fb[last & 1] + p.b_off;
+    r.bin = a.TF[last & 1] + p.b_off;
 
     const int tile = blockIdx.x - (int)a.sweep_tiles[q];
     const int64_t e = 1 + (int64_t)tile * kSweepThreads + threadIdx.x;
