@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="bounded CPU-baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="one device pass only (for ncu launch lists)")
     return ap.parse_args()
 
 
@@ -238,6 +239,13 @@ def main():
     flush = torch.empty(256 * MiB // 4, dtype=torch.int32, device="cuda")
 
     batch = SearchBatch(L, S, E, Pm, ctx)
+    if args.profile:
+        batch.run()
+        t = batch.timing()
+        print(json.dumps({"profile_pass": True, "device_ms": t["total_ms"], "launches": t["n_launches"]}))
+        batch.close()
+        ctx.close()
+        return 0
     for _ in range(max(args.warmup, 3)):
         batch.run()
     # timed region: K device passes, barrier + synchronize on both sides

@@ -417,7 +417,7 @@ size_t put(std::vector<char> &blob, const T *src, size_t n) {
 
 // chunk workspace layout (byte offsets from ws base)
 struct WsLayout {
-    size_t cells, cmem, rcls, bup, tf0, tf1, par, parts, uniq, nuniq, ulo, uhi, ctr, total;
+    size_t cells, cmem, rcls, bup, tf0, tf1, par, parts, bestp, uniq, nuniq, ulo, uhi, ctr, total;
 };
 WsLayout ws_layout(const Chunk &c) {
     WsLayout w;
@@ -430,6 +430,7 @@ WsLayout ws_layout(const Chunk &c) {
     w.tf1 = o; o = align_up(o + c.n_bcells * sizeof(TFCell));
     w.par = o; o = align_up(o + c.n_par * 2);
     w.parts = o; o = align_up(o + c.n_tiles * sizeof(SweepPartial));
+    w.bestp = o; o = align_up(o + c.probs.size() * sizeof(SweepPartial));
     w.uniq = o; o = align_up(o + c.n_cells * 4);
     w.nuniq = o; o = align_up(o + c.n_units * 4);
     w.ulo = o; o = align_up(o + c.n_units * 4);
@@ -692,6 +693,7 @@ ChunkArgs chunk_args(gbmw_batch *b, const Chunk &c, char *ws, size_t chunk_index
     a.TF[1] = (TFCell *)(ws + w.tf1);
     a.par = (uint16_t *)(ws + w.par);
     a.partials = (SweepPartial *)(ws + w.parts);
+    a.best = (SweepPartial *)(ws + w.bestp);
     a.uniq = (int32_t *)(ws + w.uniq);
     a.nuniq = (int32_t *)(ws + w.nuniq);
     a.unit_lo = (int32_t *)(ws + w.ulo);
@@ -744,7 +746,7 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
         if ((rc = launch_sweep(a, c.n_tiles, st))) return cuda_fail(ctx, rc, "K3 launch");
         cudaEventRecord(c.ev[3], st);
         if ((rc = launch_finalize(a, st))) return cuda_fail(ctx, rc, "K4 launch");
-        c.launches += 2;
+        c.launches += 3;
         cudaEventRecord(c.ev[4], st);
     }
     cudaError_t ce = cudaStreamSynchronize(st);

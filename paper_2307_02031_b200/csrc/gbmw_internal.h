@@ -101,7 +101,8 @@ struct ChunkArgs {
     unsigned long long *bup;      // per problem, bits of max O_b (all >= 0)
     TFCell *TF[2];
     uint16_t *par;
-    SweepPartial *partials;
+    SweepPartial *partials;       // K3 per-tile best safe bucket
+    SweepPartial *best;           // per problem: overall best bucket (K3b)
     int32_t *uniq;                // per (unit, slot): strategy indices with distinct (w, k, c, ef), ascending
     int32_t *nuniq;               // per unit: number of distinct strategies
     int32_t *unit_lo, *unit_hi;   // per unit u: live rows [L_u, H_u] of B_u (see k_dedupe)

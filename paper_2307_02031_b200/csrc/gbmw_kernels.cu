@@ -392,6 +392,29 @@ __device__ __forceinline__ bool cand_better(double t1, int64_t e1, double t2, in
     return (t1 < t2) || (t1 == t2 && e1 > e2);
 }
 
+// block-wide best (t, larger e) of one candidate per thread; result valid in all threads
+__device__ __forceinline__ SweepPartial block_best(double t, int64_t e, int j, double *red_t, long long *red_e,
+                                                   int *red_j) {
+    for (int off = 16; off > 0; off >>= 1) {
+        const double ot = __shfl_down_sync(0xffffffffu, t, off);
+        const long long oe = __shfl_down_sync(0xffffffffu, (long long)e, off);
+        const int oj = __shfl_down_sync(0xffffffffu, j, off);
+        if (cand_better(ot, oe, t, e)) { t = ot; e = oe; j = oj; }
+    }
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    __syncthreads();                    // red_* may still be read by a previous call
+    if (lane == 0) { red_t[wid] = t; red_e[wid] = e; red_j[wid] = j; }
+    __syncthreads();
+    double bt = red_t[0];
+    long long be = red_e[0];
+    int bj = red_j[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+        if (cand_better(red_t[w], red_e[w], bt, be)) { bt = red_t[w]; be = red_e[w]; bj = red_j[w]; }
+    SweepPartial sp;
+    sp.t = bt; sp.e = be; sp.j = bj; sp.pad_ = 0;
+    return sp;
+}
+
 // ---------------------------------------------------------------- K3: E_fwd sweep
 // One thread per bucket e in [1, n_b].  f(e) = first strategy in (T, F, j) order that
 // is finite and fits (inside the safe zone everything fits); the tile keeps the
@@ -439,54 +462,109 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(ChunkArgs a) {
         if (p.frontier_off >= 0) a.frontier[p.frontier_off + e - 1] = t0;
         if (j0 >= 0) {
             const double safe_limit = p.budget - __longlong_as_double((long long)a.bup[q]);
-            const bool safe = int_le_double(e * p.gran, safe_limit);
-            if (safe) {
-                best_t = t0; best_e = e; best_j = j0;
-            } else {
-                uint16_t path[kMaxUnits];
-                double ct = t0, cf = f0;
-                int cj = j0;
-                while (true) {
-                    backtrack(a, p, e, cj, path);
-                    if (plan_e_all(a, p, path) <= p.budget) {
-                        best_t = ct; best_e = e; best_j = cj;
-                        break;
-                    }
-                    // next candidate in (T, F, j) order
-                    double nt = GBMW_INF, nf = GBMW_INF;
-                    int nj = -1;
-                    for (int j = 0; j < S; ++j) {
-                        double T, F;
-                        row_value(r, e, j, T, F);
-                        if (!(T < GBMW_INF)) continue;
-                        if (!lex_less(ct, cf, cj, T, F, j)) continue;
-                        if (nj < 0 || lex_less(T, F, j, nt, nf, nj)) { nt = T; nf = F; nj = j; }
-                    }
-                    if (nj < 0) break;
-                    ct = nt; cf = nf; cj = nj;
-                }
-            }
+            if (int_le_double(e * p.gran, safe_limit)) { best_t = t0; best_e = e; best_j = j0; }
+            // unsafe rows: k_sweep_unsafe (top-down, pruned)
         }
     }
-    // tile reduction: (t, larger e)
-    for (int off = 16; off > 0; off >>= 1) {
-        const double ot = __shfl_down_sync(0xffffffffu, best_t, off);
-        const long long oe = __shfl_down_sync(0xffffffffu, (long long)best_e, off);
-        const int oj = __shfl_down_sync(0xffffffffu, best_j, off);
-        if (cand_better(ot, oe, best_t, best_e)) { best_t = ot; best_e = oe; best_j = oj; }
+    SweepPartial sp = block_best(best_t, best_e, best_j, red_t, red_e, red_j);
+    if (threadIdx.x == 0) a.partials[p.tile_off + tile] = sp;
+}
+
+// Unsafe zone (e_fwd > budget - b_up): every candidate needs the backward-peak check
+// (a walk of U argmin pointers + the forward E_all fold).  One CTA per problem walks
+// the unsafe buckets from the top down, a block of rows at a time.  A row can only
+// win if its candidate is strictly faster than the best unsafe row found so far (those
+// have larger e, which wins ties) and no slower than the best safe row (smaller e,
+// which loses ties); candidates are visited in (T, F, j) order, so each row's walk
+// stops at the first candidate that fits or cannot win.  The surviving winner is the
+// reference's (dpsearch.py:196-208).  Writes the problem's overall best (safe and
+// unsafe) for K4.
+__global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
+    __shared__ int32_t sW[kMaxStrats];
+    __shared__ int32_t sK[kMaxStrats];
+    __shared__ double sC[kMaxStrats];
+    __shared__ double sE[kMaxStrats];
+    __shared__ double red_t[kSweepThreads / 32];
+    __shared__ long long red_e[kSweepThreads / 32];
+    __shared__ int red_j[kSweepThreads / 32];
+    __shared__ SweepPartial s_safe, s_uns;
+    __shared__ int64_t s_elo;
+    const int q = blockIdx.x;
+    const DevProblem &p = a.probs[q];
+    // best safe row from K3's tile partials
+    double bt = GBMW_INF;
+    int64_t be = -1;
+    int bj = 0;
+    for (int t = threadIdx.x; t < p.n_sweep_tiles; t += blockDim.x) {
+        const SweepPartial sp = a.partials[p.tile_off + t];
+        if (cand_better(sp.t, sp.e, bt, be)) { bt = sp.t; be = sp.e; bj = sp.j; }
     }
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    if (lane == 0) { red_t[wid] = best_t; red_e[wid] = best_e; red_j[wid] = best_j; }
-    __syncthreads();
+    const SweepPartial safe = block_best(bt, be, bj, red_t, red_e, red_j);
+    const int S = p.S;
+    const int last = p.U - 1;
+    const Cell *lc = a.cells + p.cell_off + (int64_t)last * S;
+    for (int i = threadIdx.x; i < S; i += blockDim.x) {
+        const Cell c = lc[i];
+        sW[i] = c.w; sK[i] = c.k; sC[i] = c.c; sE[i] = c.ef;
+    }
     if (threadIdx.x == 0) {
-        double bt = red_t[0];
-        long long be = red_e[0];
-        int bj = red_j[0];
-        for (int w = 1; w < kSweepThreads / 32; ++w)
-            if (cand_better(red_t[w], red_e[w], bt, be)) { bt = red_t[w]; be = red_e[w]; bj = red_j[w]; }
-        SweepPartial sp;
-        sp.t = bt; sp.e = be; sp.j = bj; sp.pad_ = 0;
-        a.partials[p.tile_off + tile] = sp;
+        s_safe = safe;
+        s_uns.t = GBMW_INF; s_uns.e = -1; s_uns.j = 0; s_uns.pad_ = 0;
+        // first unsafe bucket: smallest e >= 1 with !(e * gran <= safe_limit)
+        const double safe_limit = p.budget - __longlong_as_double((long long)a.bup[q]);
+        double x = floor(safe_limit / (double)p.gran);
+        if (!(x >= 0.0)) x = 0.0;
+        if (x > (double)p.n_b) x = (double)p.n_b;
+        int64_t elo = (int64_t)x + 1;
+        while (elo > 1 && !int_le_double((elo - 1) * p.gran, safe_limit)) --elo;
+        while (elo <= p.n_b && int_le_double(elo * p.gran, safe_limit)) ++elo;
+        s_elo = elo;
+    }
+    __syncthreads();
+    RowCtx r;
+    r.w = sW; r.k = sK; r.c = sC; r.ef = sE;
+    r.n_e = p.n_b + 1;
+    r.init = (last == 0);
+    r.lo = (last == 0) ? 0 : a.unit_lo[p.unit_off + last];
+    r.bin = a.TF[last & 1] + p.b_off;
+    const int64_t elo = s_elo;
+    uint16_t path[kMaxUnits];
+    for (int64_t top = p.n_b; top >= elo; top -= kSweepThreads) {
+        const int64_t e = top - threadIdx.x;
+        const double tu = s_uns.t, ts = s_safe.t;
+        const bool have_u = s_uns.e >= 0, have_s = s_safe.e >= 0;
+        double mt = GBMW_INF;
+        int64_t me = -1;
+        int mj = 0;
+        if (e >= elo) {
+            double ct = 0.0, cf = 0.0;
+            int cj = -1;
+            while (true) {
+                // next candidate in (T, F, j) order after (ct, cf, cj)
+                double nt = GBMW_INF, nf = GBMW_INF;
+                int nj = -1;
+                for (int j = 0; j < S; ++j) {
+                    double T, F;
+                    row_value(r, e, j, T, F);
+                    if (!(T < GBMW_INF)) continue;
+                    if (cj >= 0 && !lex_less(ct, cf, cj, T, F, j)) continue;
+                    if (nj < 0 || lex_less(T, F, j, nt, nf, nj)) { nt = T; nf = F; nj = j; }
+                }
+                if (nj < 0) break;
+                if ((have_u && !(nt < tu)) || (have_s && nt > ts)) break;     // cannot win
+                backtrack(a, p, e, nj, path);
+                if (plan_e_all(a, p, path) <= p.budget) { mt = nt; me = e; mj = nj; break; }
+                ct = nt; cf = nf; cj = nj;
+            }
+        }
+        const SweepPartial blk = block_best(mt, me, mj, red_t, red_e, red_j);
+        if (threadIdx.x == 0 && cand_better(blk.t, blk.e, s_uns.t, s_uns.e)) s_uns = blk;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        SweepPartial best = s_safe;
+        if (cand_better(s_uns.t, s_uns.e, best.t, best.e)) best = s_uns;
+        a.best[q] = best;
     }
 }
 
@@ -495,13 +573,10 @@ __global__ void k_finalize(ChunkArgs a) {
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= a.n_probs) return;
     const DevProblem &p = a.probs[q];
-    double bt = GBMW_INF;
-    int64_t be = -1;
-    int bj = 0;
-    for (int t = 0; t < p.n_sweep_tiles; ++t) {
-        const SweepPartial sp = a.partials[p.tile_off + t];
-        if (cand_better(sp.t, sp.e, bt, be)) { bt = sp.t; be = sp.e; bj = sp.j; }
-    }
+    const SweepPartial best = a.best[q];
+    const double bt = best.t;
+    const int64_t be = best.e;
+    const int bj = best.j;
     gbmw_result res;
     res.frontier_offset = -1;
     res.status = GBMW_OK;
@@ -607,8 +682,8 @@ int launch_dp_step(const ChunkArgs &a, int group, int u, int64_t tile_base, int6
 }
 
 int launch_sweep(const ChunkArgs &a, int64_t n_tiles, void *stream) {
-    if (n_tiles <= 0) return 0;
-    k_sweep<<<(unsigned)n_tiles, kSweepThreads, 0, (cudaStream_t)stream>>>(a);
+    if (n_tiles > 0) k_sweep<<<(unsigned)n_tiles, kSweepThreads, 0, (cudaStream_t)stream>>>(a);
+    if (a.n_probs > 0) k_sweep_unsafe<<<(unsigned)a.n_probs, kSweepThreads, 0, (cudaStream_t)stream>>>(a);
     return (int)cudaGetLastError();
 }
 
