@@ -15,6 +15,9 @@
 #include <string>
 #include <vector>
 #include <chrono>
+#include <map>
+#include <memory>
+#include <tuple>
 
 static double now_ms() {
     return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
@@ -50,10 +53,27 @@ bool prod_exact(int64_t a, int64_t b) {
     return (double)a * (double)b < kTwo53 * 0.5;   // margin for rounding of the test
 }
 
+// Per (strategy list, micro-batch): usable strategies and their (data, tp) classes.
+struct StratInfo {
+    std::vector<int32_t> cand, cand_cls, cls_d, cls_t;
+    int status = GBMW_OK;
+    std::string err;
+    int32_t min_pp = 0, max_pp = 0;
+};
+
+// Per (layer range, fusion flag): units and byte maxima for the 2^53 checks.
+struct UnitInfo {
+    std::vector<int32_t> unit_first, unit_count;
+    int status = GBMW_OK;
+    std::string err;
+    int64_t max_bnd = 0, max_int = 0;
+};
+
 struct HostProb {
     int status = GBMW_OK;
     bool gpu = false;              // has device work
-    std::vector<int32_t> cand, cand_cls, cls_d, cls_t, unit_first, unit_count;
+    const StratInfo *si = nullptr;
+    const UnitInfo *ui = nullptr;
     int U = 0, S = 0, K = 0;
     int64_t n_b = 0;
     int64_t plan_off = 0, frontier_off = -1;
@@ -104,6 +124,8 @@ struct gbmw_batch {
     std::vector<gbmw_problem> problems;
     std::vector<HostProb> hp;
     std::vector<Chunk> chunks;
+    std::map<std::tuple<int32_t, int32_t, int64_t>, std::unique_ptr<StratInfo>> strat_cache;
+    std::map<std::tuple<int32_t, int32_t, int>, std::unique_ptr<UnitInfo>> unit_cache;
     int64_t total_plan = 0, total_frontier = 0;
     // device arena: inputs | chunk descriptor blocks | outputs
     void *arena = nullptr;
@@ -313,7 +335,65 @@ extern "C" int gbmw_ctx_destroy(gbmw_ctx *ctx) {
 // ----------------------------------------------------------------------------- batch set-up
 namespace {
 
-// dp_search argument checks and host bookkeeping (dpsearch.py:103-125, :42-43, :71-86)
+// usable strategies + classes of one strategy list at one micro-batch (dpsearch.py:42-43)
+const StratInfo *strat_info(gbmw_batch &b, const gbmw_problem &P) {
+    auto key = std::make_tuple(P.strat_begin, P.n_strats, P.micro_batch);
+    auto it = b.strat_cache.find(key);
+    if (it != b.strat_cache.end()) return it->second.get();
+    auto si = std::make_unique<StratInfo>();
+    for (int i = 0; i < P.n_strats && si->status == GBMW_OK; ++i) {
+        const gbmw_strategy &s = b.strats[P.strat_begin + i];
+        const int rc = check_strategy(s, &si->err);
+        if (rc) { si->status = rc; break; }
+        const StratDeg d = strat_degrees(s);
+        if (P.micro_batch % d.data != 0) continue;
+        const int gi = P.strat_begin + i;
+        si->cand.push_back(gi);
+        si->min_pp = si->cand.size() == 1 ? s.pp_degree : std::min(si->min_pp, s.pp_degree);
+        si->max_pp = si->cand.size() == 1 ? s.pp_degree : std::max(si->max_pp, s.pp_degree);
+        int k = -1;                                   // (data, tp) classes in first-appearance order
+        for (int c = 0; c < (int)si->cls_d.size(); ++c)
+            if (si->cls_d[c] == d.data && si->cls_t[c] == d.tp) { k = c; break; }
+        if (k < 0) { k = (int)si->cls_d.size(); si->cls_d.push_back(d.data); si->cls_t.push_back(d.tp); }
+        si->cand_cls.push_back(k);
+    }
+    const StratInfo *out = si.get();
+    b.strat_cache.emplace(key, std::move(si));
+    return out;
+}
+
+// units of one stage (dpsearch.py:71-86): fusion key (kind, param, bnd, int, raw fwd_time, frac)
+const UnitInfo *unit_info(gbmw_batch &b, const gbmw_problem &P) {
+    const bool fuse = (P.flags & GBMW_FUSE) != 0;
+    auto key = std::make_tuple(P.layer_begin, P.n_layers, (int)fuse);
+    auto it = b.unit_cache.find(key);
+    if (it != b.unit_cache.end()) return it->second.get();
+    auto ui = std::make_unique<UnitInfo>();
+    for (int i = 0; i < P.n_layers; ++i) {
+        const int gl = P.layer_begin + i;
+        const gbmw_layer &B = b.layers[gl];
+        const int rc = check_layer(B, &ui->err);
+        if (rc) { ui->status = rc; break; }
+        ui->max_bnd = std::max(ui->max_bnd, B.bnd_bytes_per_sample);
+        ui->max_int = std::max(ui->max_int, B.int_bytes_per_sample);
+        if (fuse && !ui->unit_first.empty()) {
+            const gbmw_layer &A = b.layers[ui->unit_first.back()];
+            if (A.kind_id == B.kind_id && A.param_bytes == B.param_bytes &&
+                A.bnd_bytes_per_sample == B.bnd_bytes_per_sample && A.int_bytes_per_sample == B.int_bytes_per_sample &&
+                A.fwd_time_raw == B.fwd_time_raw && A.tp_act_replication_fraction == B.tp_act_replication_fraction) {
+                ui->unit_count.back() += 1;
+                continue;
+            }
+        }
+        ui->unit_first.push_back(gl);
+        ui->unit_count.push_back(1);
+    }
+    const UnitInfo *out = ui.get();
+    b.unit_cache.emplace(key, std::move(ui));
+    return out;
+}
+
+// dp_search argument checks and host bookkeeping (dpsearch.py:103-125)
 void prepare_problem(gbmw_batch &b, int pi, std::string *err) {
     const gbmw_problem &P = b.problems[pi];
     HostProb &h = b.hp[pi];
@@ -333,67 +413,32 @@ void prepare_problem(gbmw_batch &b, int pi, std::string *err) {
     if (P.env_index < 0 || P.env_index >= (int)b.envs.size()) return fail(GBMW_EINVAL, "problem env index out of bounds");
     if (P.budget_bytes >= kTwo53) return fail(GBMW_ERANGE, "budget_bytes must be < 2^53");
     h.n_b = P.n_buckets;
-    for (int i = 0; i < P.n_strats; ++i) {
-        const gbmw_strategy &s = b.strats[P.strat_begin + i];
-        int rc = check_strategy(s, err);
-        if (rc) { h.status = rc; return; }
-        const StratDeg d = strat_degrees(s);
-        if (P.micro_batch % d.data == 0) h.cand.push_back(P.strat_begin + i);
-    }
-    h.S = (int)h.cand.size();
+    const StratInfo *si = strat_info(b, P);
+    if (si->status) return fail(si->status, si->err);
+    h.si = si;
+    h.S = (int)si->cand.size();
     if (h.S == 0 || h.n_b == 0) return;    // infeasible, dpsearch.py:119-121
-    for (int i = 0; i < P.n_layers; ++i) {
-        int rc = check_layer(b.layers[P.layer_begin + i], err);
-        if (rc) { h.status = rc; return; }
-    }
+    const UnitInfo *ui = unit_info(b, P);
+    if (ui->status) return fail(ui->status, ui->err);
+    h.ui = ui;
     // layer_memory range checks (costs.py:207-210), raised on the first table cell
-    for (int32_t gi : h.cand) {
-        const gbmw_strategy &s = b.strats[gi];
-        if (P.stage_index < 1 || P.stage_index > s.pp_degree)
-            return fail(GBMW_ESTAGE, "stage_index " + std::to_string(P.stage_index) + " out of range 1.." + std::to_string(s.pp_degree));
-        if (P.n_micro < 1) return fail(GBMW_ESTAGE, "n_micro must be >= 1, got " + std::to_string(P.n_micro));
-    }
-    // exactness of Python int arithmetic in fp64 (SURVEY.md §8 a0)
-    int64_t max_stash = 1;
-    for (int32_t gi : h.cand) max_stash = std::max<int64_t>(max_stash, (int64_t)b.strats[gi].pp_degree);
-    max_stash = std::min<int64_t>(max_stash, std::max<int32_t>(1, P.n_micro));
-    for (int i = 0; i < P.n_layers; ++i) {
-        const gbmw_layer &L = b.layers[P.layer_begin + i];
-        if (!prod_exact(L.bnd_bytes_per_sample, P.micro_batch) ||
-            !prod_exact(L.bnd_bytes_per_sample * (P.micro_batch), max_stash) ||
-            !prod_exact(L.int_bytes_per_sample, P.micro_batch))
-            return fail(GBMW_ERANGE, "byte products of layer " + std::to_string(i) + " reach 2^53; fp64 would not be exact");
-    }
-    if (h.S > kMaxStrats || h.S > 65535) return fail(GBMW_ENOTSUP, "more than " + std::to_string(kMaxStrats) + " usable strategies");
-    // (data, tp) classes in first-appearance order
-    for (int32_t gi : h.cand) {
-        const StratDeg d = strat_degrees(b.strats[gi]);
-        int k = -1;
-        for (int c = 0; c < (int)h.cls_d.size(); ++c)
-            if (h.cls_d[c] == d.data && h.cls_t[c] == d.tp) { k = c; break; }
-        if (k < 0) { k = (int)h.cls_d.size(); h.cls_d.push_back(d.data); h.cls_t.push_back(d.tp); }
-        h.cand_cls.push_back(k);
-    }
-    h.K = (int)h.cls_d.size();
-    if (h.K > kMaxClasses) return fail(GBMW_ENOTSUP, "more than " + std::to_string(kMaxClasses) + " (data, tp) classes");
-    // units (dpsearch.py:71-86): fusion key (kind, param, bnd, int, raw fwd_time, frac)
-    const bool fuse = (P.flags & GBMW_FUSE) != 0;
-    for (int i = 0; i < P.n_layers; ++i) {
-        const int gl = P.layer_begin + i;
-        if (fuse && !h.unit_first.empty()) {
-            const gbmw_layer &A = b.layers[h.unit_first.back()];
-            const gbmw_layer &B = b.layers[gl];
-            if (A.kind_id == B.kind_id && A.param_bytes == B.param_bytes &&
-                A.bnd_bytes_per_sample == B.bnd_bytes_per_sample && A.int_bytes_per_sample == B.int_bytes_per_sample &&
-                A.fwd_time_raw == B.fwd_time_raw && A.tp_act_replication_fraction == B.tp_act_replication_fraction) {
-                h.unit_count.back() += 1;
-                continue;
-            }
+    if (P.stage_index < 1 || P.stage_index > si->min_pp)
+        for (int32_t gi : si->cand) {
+            const gbmw_strategy &s = b.strats[gi];
+            if (P.stage_index < 1 || P.stage_index > s.pp_degree)
+                return fail(GBMW_ESTAGE, "stage_index " + std::to_string(P.stage_index) + " out of range 1.." +
+                                             std::to_string(s.pp_degree));
         }
-        h.unit_first.push_back(gl);
-        h.unit_count.push_back(1);
-    }
-    h.U = (int)h.unit_first.size();
+    if (P.n_micro < 1) return fail(GBMW_ESTAGE, "n_micro must be >= 1, got " + std::to_string(P.n_micro));
+    // exactness of Python int arithmetic in fp64 (SURVEY.md §8 a0)
+    const int64_t max_stash = std::min<int64_t>(std::max<int32_t>(1, si->max_pp), std::max<int32_t>(1, P.n_micro));
+    if (!prod_exact(ui->max_bnd, P.micro_batch) || !prod_exact(ui->max_bnd * P.micro_batch, max_stash) ||
+        !prod_exact(ui->max_int, P.micro_batch))
+        return fail(GBMW_ERANGE, "byte products of a stage layer reach 2^53; fp64 would not be exact");
+    if (h.S > kMaxStrats || h.S > 65535) return fail(GBMW_ENOTSUP, "more than " + std::to_string(kMaxStrats) + " usable strategies");
+    h.K = (int)si->cls_d.size();
+    if (h.K > kMaxClasses) return fail(GBMW_ENOTSUP, "more than " + std::to_string(kMaxClasses) + " (data, tp) classes");
+    h.U = (int)ui->unit_first.size();
     if (h.U > kMaxUnits) return fail(GBMW_ENOTSUP, "more than " + std::to_string(kMaxUnits) + " units in one stage");
     const int64_t n_e = h.n_b + 1;
     h.n_cells = (int64_t)h.U * h.S;
@@ -403,7 +448,8 @@ void prepare_problem(gbmw_batch &b, int pi, std::string *err) {
     h.n_tiles = (h.n_b + kSweepThreads - 1) / kSweepThreads;
     h.n_step_tiles = (n_e + kStepRows - 1) / kStepRows;
     h.ws_bytes = (size_t)h.n_cells * (sizeof(Cell) + sizeof(CellMem) + 4) + (size_t)h.U * 12 + (size_t)h.n_r * 8 + 8 +
-                 (size_t)h.n_bcells * 32 + (size_t)h.n_par * 2 + (size_t)h.n_tiles * sizeof(SweepPartial);
+                 (size_t)h.n_bcells * 2 * sizeof(TFCell) + (size_t)h.n_par * 2 +
+                 (size_t)(h.n_tiles + 1) * sizeof(SweepPartial);
     h.gpu = true;
 }
 
@@ -509,6 +555,8 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
         std::vector<DevProblem> dps;
         std::vector<int64_t> cellp{0}, rp{0}, stepp{0}, sweepp{0};
         std::vector<int32_t> cand, ccls, clsd, clst, uf, uc;
+        std::map<const StratInfo *, std::pair<int32_t, int32_t>> soff;
+        std::map<const UnitInfo *, int32_t> uoff;
         for (int pi : c.probs) {
             const HostProb &h = b->hp[pi];
             const gbmw_problem &P = b->problems[pi];
@@ -519,7 +567,22 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
             d.n_b = h.n_b; d.micro = P.micro_batch; d.gran = P.granularity_bytes; d.budget = P.budget_bytes;
             d.cell_off = c.n_cells; d.r_off = c.n_r; d.b_off = c.n_bcells; d.par_off = c.n_par; d.tile_off = c.n_tiles;
             d.plan_off = h.plan_off; d.frontier_off = h.frontier_off;
-            d.cand_off = (int32_t)cand.size(); d.class_off = (int32_t)clsd.size(); d.unit_off = (int32_t)uf.size();
+            auto sit = soff.find(h.si);
+            if (sit == soff.end()) {
+                sit = soff.emplace(h.si, std::make_pair((int32_t)cand.size(), (int32_t)clsd.size())).first;
+                cand.insert(cand.end(), h.si->cand.begin(), h.si->cand.end());
+                ccls.insert(ccls.end(), h.si->cand_cls.begin(), h.si->cand_cls.end());
+                clsd.insert(clsd.end(), h.si->cls_d.begin(), h.si->cls_d.end());
+                clst.insert(clst.end(), h.si->cls_t.begin(), h.si->cls_t.end());
+            }
+            auto uit = uoff.find(h.ui);
+            if (uit == uoff.end()) {
+                uit = uoff.emplace(h.ui, (int32_t)uf.size()).first;
+                uf.insert(uf.end(), h.ui->unit_first.begin(), h.ui->unit_first.end());
+                uc.insert(uc.end(), h.ui->unit_count.begin(), h.ui->unit_count.end());
+            }
+            d.cand_off = sit->second.first; d.class_off = sit->second.second; d.unit_off = uit->second;
+            d.ustate_off = (int32_t)c.n_units;
             d.layer_begin = P.layer_begin; d.strat_begin = P.strat_begin; d.result_index = pi;
             d.n_sweep_tiles = (int32_t)h.n_tiles;
             dps.push_back(d);
@@ -527,12 +590,6 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
             cellp.push_back(c.n_cells); rp.push_back(c.n_r);
             stepp.push_back(stepp.back() + h.n_step_tiles);
             sweepp.push_back(c.n_tiles);
-            cand.insert(cand.end(), h.cand.begin(), h.cand.end());
-            ccls.insert(ccls.end(), h.cand_cls.begin(), h.cand_cls.end());
-            clsd.insert(clsd.end(), h.cls_d.begin(), h.cls_d.end());
-            clst.insert(clst.end(), h.cls_t.begin(), h.cls_t.end());
-            uf.insert(uf.end(), h.unit_first.begin(), h.unit_first.end());
-            uc.insert(uc.end(), h.unit_count.begin(), h.unit_count.end());
             c.n_units += h.U;
             c.Umax = std::max(c.Umax, h.U);
             c.max_k = std::max(c.max_k, h.K);
@@ -867,7 +924,7 @@ extern "C" int gbmw_cost_tables(gbmw_ctx *ctx, const gbmw_layer *layers, int64_t
     if (n_usable) *n_usable = h.S;
     if (n_units) *n_units = h.U;
     if (usable)
-        for (int i = 0; i < h.S; ++i) usable[i] = h.cand[i] - problem->strat_begin;
+        for (int i = 0; i < h.S; ++i) usable[i] = h.si->cand[i] - problem->strat_begin;
     if (!h.gpu) { gbmw_batch_destroy(b); return GBMW_OK; }
     rc = run_chunks(ctx, b, true);
     if (rc == GBMW_OK) {

@@ -56,12 +56,12 @@ struct DevProblem {
     int64_t frontier_off;   // into frontier (n_b), -1 if not requested
     int32_t cand_off;       // into cand_strat / cand_cls (S)
     int32_t class_off;      // into class_d / class_t (K)
-    int32_t unit_off;       // into unit_first / unit_count (U)
+    int32_t unit_off;       // into unit_first / unit_count (U), shared by problems with equal stages
     int32_t layer_begin;    // global layer index of the first stage layer
     int32_t strat_begin;    // global index of the problem's strategy list
     int32_t result_index;   // slot in the batch result array
     int32_t n_sweep_tiles;
-    int32_t pad_;
+    int32_t ustate_off;     // into per-problem unit state: nuniq / unit_lo / unit_hi (U)
 };
 
 struct alignas(16) TFCell {

@@ -128,7 +128,7 @@ __global__ void k_dedupe(ChunkArgs a) {
         }
         for (int off = 16; off > 0; off >>= 1) wmin = min(wmin, __shfl_xor_sync(0xffffffffu, wmin, off));
         if (lane == 0) {
-            a.nuniq[p.unit_off + u] = count;
+            a.nuniq[p.ustate_off + u] = count;
             s_wmin[u] = wmin;
         }
     }
@@ -139,8 +139,8 @@ __global__ void k_dedupe(ChunkArgs a) {
         unsigned long long live = 0;
         for (int u = 0; u < p.U; ++u) {
             const int64_t lo = acc < top ? acc : top, hi = p.n_b - s_wmin[u];
-            a.unit_lo[p.unit_off + u] = (int32_t)lo;                          // L_u = m_{u-1}
-            a.unit_hi[p.unit_off + u] = (int32_t)hi;                          // H_u
+            a.unit_lo[p.ustate_off + u] = (int32_t)lo;                          // L_u = m_{u-1}
+            a.unit_hi[p.ustate_off + u] = (int32_t)hi;                          // H_u
             if (u >= 1 && hi >= lo) live += (unsigned long long)(hi - lo + 1);
             acc += s_wmin[u];
         }
@@ -276,14 +276,14 @@ __global__ void __launch_bounds__(kStepThreads, GROUP == 0 ? 3 : 2) k_dp_step(Ch
             const int q = __ldg(a.step_map + tile);
             const DevProblem &p = a.probs[q];
             const int64_t first_row = (tile - a.step_tiles[q]) * kStepRows;
-            const int lo = a.unit_lo[p.unit_off + u], hi = a.unit_hi[p.unit_off + u];
+            const int lo = a.unit_lo[p.ustate_off + u], hi = a.unit_hi[p.ustate_off + u];
             if (first_row > hi || first_row + kStepRows - 1 < lo) continue;   // dead tile (CTA-uniform)
             if (q != q_prev) {
                 __syncthreads();                   // previous problem's readers are done
                 const int S = p.S, K = p.K;
                 const Cell *prev_cells = a.cells + p.cell_off + (int64_t)(u - 1) * S;
                 const int32_t *ul = a.uniq + p.cell_off + (int64_t)(u - 1) * S;
-                const int nu = a.nuniq[p.unit_off + u - 1];
+                const int nu = a.nuniq[p.ustate_off + u - 1];
                 for (int n = threadIdx.x; n < nu; n += blockDim.x) {
                     const int j = ul[n];
                     sh.cell[n] = prev_cells[j];
@@ -293,7 +293,7 @@ __global__ void __launch_bounds__(kStepThreads, GROUP == 0 ? 3 : 2) k_dp_step(Ch
                 for (int x = threadIdx.x; x < K * K; x += blockDim.x) sh.r[x] = r_u[x];
                 if (threadIdx.x == 0) {
                     sh.S = nu; sh.K = K; sh.n_e = (int)(p.n_b + 1); sh.q = q;
-                    sh.lo_prev = a.unit_lo[p.unit_off + u - 1];
+                    sh.lo_prev = a.unit_lo[p.ustate_off + u - 1];
                     sh.lo = lo; sh.hi = hi;
                     sh.b_off = p.b_off; sh.par_off = p.par_off; sh.tile0 = a.step_tiles[q];
                 }
@@ -442,7 +442,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(ChunkArgs a) {
     r.w = sW; r.k = sK; r.c = sC; r.ef = sE;
     r.n_e = p.n_b + 1;
     r.init = (last == 0);
-    r.lo = (last == 0) ? 0 : a.unit_lo[p.unit_off + last];
+    r.lo = (last == 0) ? 0 : a.unit_lo[p.ustate_off + last];
     r.bin = a.TF[last & 1] + p.b_off;
 
     const int tile = blockIdx.x - (int)a.sweep_tiles[q];
@@ -525,7 +525,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
     r.w = sW; r.k = sK; r.c = sC; r.ef = sE;
     r.n_e = p.n_b + 1;
     r.init = (last == 0);
-    r.lo = (last == 0) ? 0 : a.unit_lo[p.unit_off + last];
+    r.lo = (last == 0) ? 0 : a.unit_lo[p.ustate_off + last];
     r.bin = a.TF[last & 1] + p.b_off;
     const int64_t elo = s_elo;
     uint16_t path[kMaxUnits];
