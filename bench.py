@@ -52,6 +52,9 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="bounded CPU-baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true", help="one device pass only (for ncu launch lists)")
+    ap.add_argument("--workload", default="sweep10k",
+                    help="sweep10k (default, BASELINE config 5) or a full planner search: "
+                         "gpt96[-bmw] | bert[-bmw] | t5-<GiB>[-bmw] | vit[-bmw] | swin[-bmw]")
     return ap.parse_args()
 
 
@@ -212,11 +215,65 @@ def _cpu_model():
     return "unknown"
 
 
+def full_search(args, rank):
+    """One full planner search (Algorithm 1, optionally + Algorithm 2) at the given
+    granularity: wall-clock latency of plan_full and the algorithmic transitions of
+    every stage search it issued (SURVEY.md §8(d) full-search latency)."""
+    if rank != 0:
+        return 0
+    import torch
+    from paper_2307_02031_b200 import dpsearch, workloads as W
+    from paper_2307_02031_b200.planner import PlannerOptions, plan_full
+
+    name = args.workload
+    bmw = name.endswith("-bmw")
+    base = name[:-4] if bmw else name
+    budget = None
+    if base.startswith("t5-"):
+        budget = int(base.split("-")[1]) << 30
+        base = "t5"
+    if base == "gpt96":
+        base = "gpt"
+    ctx = W.config(base, budget)
+    opts = PlannerOptions(granularity_bytes=args.granularity, bi_objective=bmw)
+    torch.cuda.set_device(0)
+    lat = []
+    plan = None
+    for k in range(max(1, args.warmup) + args.steps):
+        dpsearch.reset_stats()
+        t0 = time.perf_counter()
+        plan = plan_full(ctx.model, ctx.cluster, ctx.profile, opts)
+        dt = time.perf_counter() - t0
+        if k >= max(1, args.warmup):
+            lat.append(dt)
+    st = dict(dpsearch.STATS)
+    ms = 1e3 * float(np.median(lat))
+    line = {"metric": METRIC, "value": st["transitions"] / (ms / 1e3), "unit": UNIT, "n_gpus": 1,
+            "steps": args.steps, "warmup": max(1, args.warmup), "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "none", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"plan_full {name}: {ctx.model.name} on {ctx.cluster.n_devices} simulated GPUs, "
+                                   f"{ctx.cluster.mem_budget_bytes >> 30} GiB, granularity {args.granularity} B"
+                                   + (", BMW bi-objective refinement" if bmw else "")},
+            "full_search_latency_ms": ms, "stage_searches": st["problems"], "device_batches": st["batches"],
+            "device_ms": st["total_ms"], "transitions": st["transitions"],
+            "plan": {"batch_size": plan.batch_size, "pp_degree": plan.pp_degree, "partition": list(plan.partition),
+                     "n_micro": plan.n_micro, "predicted_time_s": plan.predicted_time_s,
+                     "predicted_throughput": plan.predicted_throughput}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.workload != "sweep10k":
+        if args.impl == "reference":
+            print(json.dumps({"impl": "reference", "unavailable": "full-search workloads are GPU-only; the CPU "
+                                                                  "reference arm times the sweep10k workload"}))
+            return 0
+        return full_search(args, rank)
     if args.impl == "reference":
         return impl_reference(args, rank, world)
 

@@ -216,6 +216,8 @@ int  gbmw_batch_run(gbmw_ctx *ctx, gbmw_batch *batch);
 int  gbmw_batch_fetch(gbmw_ctx *ctx, gbmw_batch *batch,
                       gbmw_result *results, int32_t *plans, double *frontier);
 int  gbmw_batch_timing(const gbmw_batch *batch, gbmw_timing *out);
+/* timing of the last batch run on this context (incl. one-shot gbmw_search_batch calls) */
+int  gbmw_ctx_last_timing(const gbmw_ctx *ctx, gbmw_timing *out);
 int  gbmw_batch_destroy(gbmw_batch *batch);
 
 /* ---- host-side partition logic around the search (parapilot/balance.py) ---- */

@@ -63,7 +63,7 @@ EXPORTS = (
     "gbmw_version", "gbmw_abi_version", "gbmw_limits", "gbmw_ctx_create", "gbmw_ctx_destroy",
     "gbmw_last_error", "gbmw_last_error_global", "gbmw_ctx_stream", "gbmw_enumerate", "gbmw_layer_cost",
     "gbmw_transform_cost", "gbmw_comm_breakdown", "gbmw_cost_tables", "gbmw_search_batch", "gbmw_batch_create",
-    "gbmw_batch_run", "gbmw_batch_fetch", "gbmw_batch_timing", "gbmw_batch_destroy",
+    "gbmw_batch_run", "gbmw_batch_fetch", "gbmw_batch_timing", "gbmw_ctx_last_timing", "gbmw_batch_destroy",
     "gbmw_partition_costs", "gbmw_init_partition", "gbmw_seed_for", "gbmw_py_sum", "gbmw_planner_last_error",
 )
 
@@ -104,6 +104,7 @@ def lib() -> ctypes.CDLL:
             L.gbmw_batch_run.argtypes = [vp, vp]
             L.gbmw_batch_fetch.argtypes = [vp, vp, vp, vp, vp]
             L.gbmw_batch_timing.argtypes = [vp, ctypes.POINTER(Timing)]
+            L.gbmw_ctx_last_timing.argtypes = [vp, ctypes.POINTER(Timing)]
             L.gbmw_batch_destroy.argtypes = [vp]
             L.gbmw_partition_costs.argtypes = [vp, i32, vp, vp, i32, vp, i64, i32, vp]
             L.gbmw_init_partition.argtypes = [vp, i32, vp, i32, vp, i64, i32, i32, vp]

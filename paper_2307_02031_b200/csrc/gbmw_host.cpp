@@ -114,6 +114,7 @@ struct gbmw_ctx {
     // grow-only pinned staging buffer for uploads
     void *pinned = nullptr;
     size_t pinned_cap = 0;
+    gbmw_timing last{};
     std::string err;
 };
 
@@ -449,7 +450,7 @@ void prepare_problem(gbmw_batch &b, int pi, std::string *err) {
     h.n_step_tiles = (n_e + kStepRows - 1) / kStepRows;
     h.ws_bytes = (size_t)h.n_cells * (sizeof(Cell) + sizeof(CellMem) + 4) + (size_t)h.U * 12 + (size_t)h.n_r * 8 + 8 +
                  (size_t)h.n_bcells * 2 * sizeof(TFCell) + (size_t)h.n_par * 2 +
-                 (size_t)(h.n_tiles + 1) * sizeof(SweepPartial);
+                 (size_t)(2 * h.n_tiles + 1) * sizeof(SweepPartial) + 8;
     h.gpu = true;
 }
 
@@ -463,7 +464,7 @@ size_t put(std::vector<char> &blob, const T *src, size_t n) {
 
 // chunk workspace layout (byte offsets from ws base)
 struct WsLayout {
-    size_t cells, cmem, rcls, bup, tf0, tf1, par, parts, bestp, uniq, nuniq, ulo, uhi, ctr, total;
+    size_t cells, cmem, rcls, bup, tf0, tf1, par, parts, uparts, bestp, bound, uniq, nuniq, ulo, uhi, ctr, total;
 };
 WsLayout ws_layout(const Chunk &c) {
     WsLayout w;
@@ -476,7 +477,9 @@ WsLayout ws_layout(const Chunk &c) {
     w.tf1 = o; o = align_up(o + c.n_bcells * sizeof(TFCell));
     w.par = o; o = align_up(o + c.n_par * 2);
     w.parts = o; o = align_up(o + c.n_tiles * sizeof(SweepPartial));
+    w.uparts = o; o = align_up(o + c.n_tiles * sizeof(SweepPartial));
     w.bestp = o; o = align_up(o + c.probs.size() * sizeof(SweepPartial));
+    w.bound = o; o = align_up(o + c.probs.size() * 8);
     w.uniq = o; o = align_up(o + c.n_cells * 4);
     w.nuniq = o; o = align_up(o + c.n_units * 4);
     w.ulo = o; o = align_up(o + c.n_units * 4);
@@ -751,6 +754,8 @@ ChunkArgs chunk_args(gbmw_batch *b, const Chunk &c, char *ws, size_t chunk_index
     a.par = (uint16_t *)(ws + w.par);
     a.partials = (SweepPartial *)(ws + w.parts);
     a.best = (SweepPartial *)(ws + w.bestp);
+    a.upartials = (SweepPartial *)(ws + w.uparts);
+    a.bound = (unsigned long long *)(ws + w.bound);
     a.uniq = (int32_t *)(ws + w.uniq);
     a.nuniq = (int32_t *)(ws + w.nuniq);
     a.unit_lo = (int32_t *)(ws + w.ulo);
@@ -803,7 +808,7 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
         if ((rc = launch_sweep(a, c.n_tiles, st))) return cuda_fail(ctx, rc, "K3 launch");
         cudaEventRecord(c.ev[3], st);
         if ((rc = launch_finalize(a, st))) return cuda_fail(ctx, rc, "K4 launch");
-        c.launches += 3;
+        c.launches += 4;
         cudaEventRecord(c.ev[4], st);
     }
     cudaError_t ce = cudaStreamSynchronize(st);
@@ -828,6 +833,7 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
         b->timing.live_cells = cells;
     }
     b->ran = true;
+    ctx->last = b->timing;
     return GBMW_OK;
 }
 }  // namespace
@@ -877,12 +883,19 @@ extern "C" int gbmw_batch_fetch(gbmw_ctx *ctx, gbmw_batch *b, gbmw_result *resul
     }
     if (first == GBMW_EINTERNAL) set_err(&ctx->err, first, "dp_search produced a plan exceeding the memory budget");
     b->timing.fetch_ms = now_ms() - t0;
+    ctx->last = b->timing;
     return first;
 }
 
 extern "C" int gbmw_batch_timing(const gbmw_batch *b, gbmw_timing *out) {
     if (!b || !out) return set_err(nullptr, GBMW_EINVAL, "null batch/out");
     *out = b->timing;
+    return GBMW_OK;
+}
+
+extern "C" int gbmw_ctx_last_timing(const gbmw_ctx *ctx, gbmw_timing *out) {
+    if (!ctx || !out) return set_err(nullptr, GBMW_EINVAL, "null ctx/out");
+    *out = ctx->last;
     return GBMW_OK;
 }
 

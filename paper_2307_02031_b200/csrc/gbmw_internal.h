@@ -102,7 +102,9 @@ struct ChunkArgs {
     TFCell *TF[2];
     uint16_t *par;
     SweepPartial *partials;       // K3 per-tile best safe bucket
-    SweepPartial *best;           // per problem: overall best bucket (K3b)
+    SweepPartial *best;           // per problem: best safe bucket
+    SweepPartial *upartials;      // K3b per-tile best unsafe bucket
+    unsigned long long *bound;    // per problem: running pruning bound (bits of t) of the unsafe walks
     int32_t *uniq;                // per (unit, slot): strategy indices with distinct (w, k, c, ef), ascending
     int32_t *nuniq;               // per unit: number of distinct strategies
     int32_t *unit_lo, *unit_hi;   // per unit u: live rows [L_u, H_u] of B_u (see k_dedupe)

@@ -470,15 +470,41 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(ChunkArgs a) {
     if (threadIdx.x == 0) a.partials[p.tile_off + tile] = sp;
 }
 
+// Per problem: best safe bucket from K3's tile partials; it also seeds the pruning
+// bound of the unsafe walks (bits of a non-negative double order like its value).
+__global__ void k_sweep_safe_best(ChunkArgs a) {
+    const int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (q >= a.n_probs) return;
+    const DevProblem &p = a.probs[q];
+    double bt = GBMW_INF;
+    int64_t be = -1;
+    int bj = 0;
+    for (int t = lane; t < p.n_sweep_tiles; t += 32) {
+        const SweepPartial sp = a.partials[p.tile_off + t];
+        if (cand_better(sp.t, sp.e, bt, be)) { bt = sp.t; be = sp.e; bj = sp.j; }
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+        const double ot = __shfl_down_sync(0xffffffffu, bt, off);
+        const long long oe = __shfl_down_sync(0xffffffffu, (long long)be, off);
+        const int oj = __shfl_down_sync(0xffffffffu, bj, off);
+        if (cand_better(ot, oe, bt, be)) { bt = ot; be = oe; bj = oj; }
+    }
+    if (lane == 0) {
+        SweepPartial sp;
+        sp.t = bt; sp.e = be; sp.j = bj; sp.pad_ = 0;
+        a.best[q] = sp;
+        a.bound[q] = (unsigned long long)__double_as_longlong(bt);
+    }
+}
+
 // Unsafe zone (e_fwd > budget - b_up): every candidate needs the backward-peak check
-// (a walk of U argmin pointers + the forward E_all fold).  One CTA per problem walks
-// the unsafe buckets from the top down, a block of rows at a time.  A row can only
-// win if its candidate is strictly faster than the best unsafe row found so far (those
-// have larger e, which wins ties) and no slower than the best safe row (smaller e,
-// which loses ties); candidates are visited in (T, F, j) order, so each row's walk
-// stops at the first candidate that fits or cannot win.  The surviving winner is the
-// reference's (dpsearch.py:196-208).  Writes the problem's overall best (safe and
-// unsafe) for K4.
+// (a walk of U argmin pointers + the forward E_all fold).  One thread per unsafe
+// bucket walks its candidates in (T, F, j) order and stops at the first that fits
+// (that is f(e), dpsearch.py:202-208) or as soon as T exceeds the problem's running
+// bound: the best t found so far by any bucket (safe or unsafe), published with
+// atomicMin.  A candidate with T > bound can never be the reference's winner
+// (min t; ties keep the larger e, so T == bound is still checked).
 __global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
     __shared__ int32_t sW[kMaxStrats];
     __shared__ int32_t sK[kMaxStrats];
@@ -487,38 +513,24 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
     __shared__ double red_t[kSweepThreads / 32];
     __shared__ long long red_e[kSweepThreads / 32];
     __shared__ int red_j[kSweepThreads / 32];
-    __shared__ SweepPartial s_safe, s_uns;
-    __shared__ int64_t s_elo;
-    const int q = blockIdx.x;
+    const int q = a.sweep_map[blockIdx.x];
     const DevProblem &p = a.probs[q];
-    // best safe row from K3's tile partials
-    double bt = GBMW_INF;
-    int64_t be = -1;
-    int bj = 0;
-    for (int t = threadIdx.x; t < p.n_sweep_tiles; t += blockDim.x) {
-        const SweepPartial sp = a.partials[p.tile_off + t];
-        if (cand_better(sp.t, sp.e, bt, be)) { bt = sp.t; be = sp.e; bj = sp.j; }
+    const int tile = blockIdx.x - (int)a.sweep_tiles[q];
+    const int64_t e0 = 1 + (int64_t)tile * kSweepThreads;
+    const double safe_limit = p.budget - __longlong_as_double((long long)a.bup[q]);
+    const int64_t e_last = min(e0 + kSweepThreads - 1, (int64_t)p.n_b);
+    SweepPartial none;
+    none.t = GBMW_INF; none.e = -1; none.j = 0; none.pad_ = 0;
+    if (int_le_double(e_last * p.gran, safe_limit)) {      // whole tile in the safe zone
+        if (threadIdx.x == 0) a.upartials[p.tile_off + tile] = none;
+        return;
     }
-    const SweepPartial safe = block_best(bt, be, bj, red_t, red_e, red_j);
     const int S = p.S;
     const int last = p.U - 1;
     const Cell *lc = a.cells + p.cell_off + (int64_t)last * S;
     for (int i = threadIdx.x; i < S; i += blockDim.x) {
         const Cell c = lc[i];
         sW[i] = c.w; sK[i] = c.k; sC[i] = c.c; sE[i] = c.ef;
-    }
-    if (threadIdx.x == 0) {
-        s_safe = safe;
-        s_uns.t = GBMW_INF; s_uns.e = -1; s_uns.j = 0; s_uns.pad_ = 0;
-        // first unsafe bucket: smallest e >= 1 with !(e * gran <= safe_limit)
-        const double safe_limit = p.budget - __longlong_as_double((long long)a.bup[q]);
-        double x = floor(safe_limit / (double)p.gran);
-        if (!(x >= 0.0)) x = 0.0;
-        if (x > (double)p.n_b) x = (double)p.n_b;
-        int64_t elo = (int64_t)x + 1;
-        while (elo > 1 && !int_le_double((elo - 1) * p.gran, safe_limit)) --elo;
-        while (elo <= p.n_b && int_le_double(elo * p.gran, safe_limit)) ++elo;
-        s_elo = elo;
     }
     __syncthreads();
     RowCtx r;
@@ -527,45 +539,38 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
     r.init = (last == 0);
     r.lo = (last == 0) ? 0 : a.unit_lo[p.ustate_off + last];
     r.bin = a.TF[last & 1] + p.b_off;
-    const int64_t elo = s_elo;
-    uint16_t path[kMaxUnits];
-    for (int64_t top = p.n_b; top >= elo; top -= kSweepThreads) {
-        const int64_t e = top - threadIdx.x;
-        const double tu = s_uns.t, ts = s_safe.t;
-        const bool have_u = s_uns.e >= 0, have_s = s_safe.e >= 0;
-        double mt = GBMW_INF;
-        int64_t me = -1;
-        int mj = 0;
-        if (e >= elo) {
-            double ct = 0.0, cf = 0.0;
-            int cj = -1;
-            while (true) {
-                // next candidate in (T, F, j) order after (ct, cf, cj)
-                double nt = GBMW_INF, nf = GBMW_INF;
-                int nj = -1;
-                for (int j = 0; j < S; ++j) {
-                    double T, F;
-                    row_value(r, e, j, T, F);
-                    if (!(T < GBMW_INF)) continue;
-                    if (cj >= 0 && !lex_less(ct, cf, cj, T, F, j)) continue;
-                    if (nj < 0 || lex_less(T, F, j, nt, nf, nj)) { nt = T; nf = F; nj = j; }
-                }
-                if (nj < 0) break;
-                if ((have_u && !(nt < tu)) || (have_s && nt > ts)) break;     // cannot win
-                backtrack(a, p, e, nj, path);
-                if (plan_e_all(a, p, path) <= p.budget) { mt = nt; me = e; mj = nj; break; }
-                ct = nt; cf = nf; cj = nj;
+    volatile unsigned long long *bound = a.bound + q;
+    const int64_t e = e0 + threadIdx.x;
+    double mt = GBMW_INF;
+    int64_t me = -1;
+    int mj = 0;
+    if (e <= p.n_b && !int_le_double(e * p.gran, safe_limit)) {
+        uint16_t path[kMaxUnits];
+        double ct = 0.0, cf = 0.0;
+        int cj = -1;
+        while (true) {
+            double nt = GBMW_INF, nf = GBMW_INF;            // next candidate in (T, F, j) order
+            int nj = -1;
+            for (int j = 0; j < S; ++j) {
+                double T, F;
+                row_value(r, e, j, T, F);
+                if (!(T < GBMW_INF)) continue;
+                if (cj >= 0 && !lex_less(ct, cf, cj, T, F, j)) continue;
+                if (nj < 0 || lex_less(T, F, j, nt, nf, nj)) { nt = T; nf = F; nj = j; }
             }
+            if (nj < 0) break;
+            if (nt > __longlong_as_double((long long)*bound)) break;      // cannot win
+            backtrack(a, p, e, nj, path);
+            if (plan_e_all(a, p, path) <= p.budget) {
+                mt = nt; me = e; mj = nj;
+                atomicMin((unsigned long long *)bound, (unsigned long long)__double_as_longlong(nt));
+                break;
+            }
+            ct = nt; cf = nf; cj = nj;
         }
-        const SweepPartial blk = block_best(mt, me, mj, red_t, red_e, red_j);
-        if (threadIdx.x == 0 && cand_better(blk.t, blk.e, s_uns.t, s_uns.e)) s_uns = blk;
-        __syncthreads();
     }
-    if (threadIdx.x == 0) {
-        SweepPartial best = s_safe;
-        if (cand_better(s_uns.t, s_uns.e, best.t, best.e)) best = s_uns;
-        a.best[q] = best;
-    }
+    const SweepPartial blk = block_best(mt, me, mj, red_t, red_e, red_j);
+    if (threadIdx.x == 0) a.upartials[p.tile_off + tile] = blk;
 }
 
 // ---------------------------------------------------------------- K4: finalize
@@ -573,10 +578,14 @@ __global__ void k_finalize(ChunkArgs a) {
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= a.n_probs) return;
     const DevProblem &p = a.probs[q];
-    const SweepPartial best = a.best[q];
-    const double bt = best.t;
-    const int64_t be = best.e;
-    const int bj = best.j;
+    const SweepPartial safe = a.best[q];
+    double bt = safe.t;
+    int64_t be = safe.e;
+    int bj = safe.j;
+    for (int t = 0; t < p.n_sweep_tiles; ++t) {
+        const SweepPartial sp = a.upartials[p.tile_off + t];
+        if (cand_better(sp.t, sp.e, bt, be)) { bt = sp.t; be = sp.e; bj = sp.j; }
+    }
     gbmw_result res;
     res.frontier_offset = -1;
     res.status = GBMW_OK;
@@ -682,8 +691,10 @@ int launch_dp_step(const ChunkArgs &a, int group, int u, int64_t tile_base, int6
 }
 
 int launch_sweep(const ChunkArgs &a, int64_t n_tiles, void *stream) {
-    if (n_tiles > 0) k_sweep<<<(unsigned)n_tiles, kSweepThreads, 0, (cudaStream_t)stream>>>(a);
-    if (a.n_probs > 0) k_sweep_unsafe<<<(unsigned)a.n_probs, kSweepThreads, 0, (cudaStream_t)stream>>>(a);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n_tiles > 0) k_sweep<<<(unsigned)n_tiles, kSweepThreads, 0, st>>>(a);
+    if (a.n_probs > 0) k_sweep_safe_best<<<blocks_for(a.n_probs, 4), 128, 0, st>>>(a);
+    if (n_tiles > 0) k_sweep_unsafe<<<(unsigned)n_tiles, kSweepThreads, 0, st>>>(a);
     return (int)cudaGetLastError();
 }
 

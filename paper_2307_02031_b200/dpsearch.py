@@ -143,7 +143,23 @@ def run_native_batch(layers, strats, envs, probs, context=None):
             _native.ptr(envs), len(envs), _native.ptr(probs), len(probs),
             _native.ptr(results), _native.ptr(plans), _native.ptr(frontier))
         msg = ctx.error() if rc != _native.OK else ""
+        t = _native.Timing()
+        if _native.lib().gbmw_ctx_last_timing(ctx.handle, ctypes.byref(t)) == _native.OK:
+            STATS["batches"] += 1
+            STATS["problems"] += len(probs)
+            for k in ("transitions", "total_ms", "dp_ms", "sweep_ms", "n_launches"):
+                STATS[k] += float(getattr(t, k))
     return rc, msg, results, plans, frontier
+
+
+# device work issued through run_native_batch since import (or the last reset_stats())
+STATS = {"batches": 0, "problems": 0, "transitions": 0.0, "total_ms": 0.0, "dp_ms": 0.0, "sweep_ms": 0.0,
+         "n_launches": 0.0}
+
+
+def reset_stats():
+    for k in STATS:
+        STATS[k] = 0 if isinstance(STATS[k], int) else 0.0
 
 
 def dp_search_batch(problems: Sequence[StageProblem], want_stage_cost: bool = False):
