@@ -427,14 +427,32 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(ChunkArgs a) {
     __shared__ double red_t[kSweepThreads / 32];
     __shared__ long long red_e[kSweepThreads / 32];
     __shared__ int red_j[kSweepThreads / 32];
+    __shared__ int32_t sJ[kMaxStrats];
     const int q = a.sweep_map[blockIdx.x];
     const DevProblem &p = a.probs[q];
-    const int S = p.S;
     const int last = p.U - 1;
-    const Cell *lc = a.cells + p.cell_off + (int64_t)last * S;
-    for (int i = threadIdx.x; i < S; i += blockDim.x) {
-        const Cell c = lc[i];
-        sW[i] = c.w; sK[i] = c.k; sC[i] = c.c; sE[i] = c.ef;
+    const int tile = blockIdx.x - (int)a.sweep_tiles[q];
+    const int64_t e = 1 + (int64_t)tile * kSweepThreads + threadIdx.x;
+    // first bucket with a finite row: m_{U-1} = L_{U-1} + wmin_{U-1} (k_dedupe)
+    const int64_t lo = a.unit_lo[p.ustate_off + last];
+    const int64_t first_finite = lo + (p.n_b - a.unit_hi[p.ustate_off + last]);
+    if (1 + (int64_t)tile * kSweepThreads + kSweepThreads - 1 < first_finite) {   // whole tile +inf
+        if (e <= p.n_b && p.frontier_off >= 0) a.frontier[p.frontier_off + e - 1] = GBMW_INF;
+        if (threadIdx.x == 0) {
+            SweepPartial none;
+            none.t = GBMW_INF; none.e = -1; none.j = 0; none.pad_ = 0;
+            a.partials[p.tile_off + tile] = none;
+        }
+        return;
+    }
+    // rank-0 candidate = lexmin over the distinct strategies (duplicates never win ties)
+    const Cell *lc = a.cells + p.cell_off + (int64_t)last * p.S;
+    const int32_t *ul = a.uniq + p.cell_off + (int64_t)last * p.S;
+    const int S = a.nuniq[p.ustate_off + last];
+    for (int n = threadIdx.x; n < S; n += blockDim.x) {
+        const int j = ul[n];
+        const Cell c = lc[j];
+        sW[n] = c.w; sK[n] = c.k; sC[n] = c.c; sE[n] = c.ef; sJ[n] = j;
     }
     __syncthreads();
 
@@ -442,21 +460,19 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(ChunkArgs a) {
     r.w = sW; r.k = sK; r.c = sC; r.ef = sE;
     r.n_e = p.n_b + 1;
     r.init = (last == 0);
-    r.lo = (last == 0) ? 0 : a.unit_lo[p.ustate_off + last];
+    r.lo = (last == 0) ? 0 : lo;
     r.bin = a.TF[last & 1] + p.b_off;
 
-    const int tile = blockIdx.x - (int)a.sweep_tiles[q];
-    const int64_t e = 1 + (int64_t)tile * kSweepThreads + threadIdx.x;
     double best_t = GBMW_INF;
     int64_t best_e = -1;
     int best_j = 0;
     if (e <= p.n_b) {
-        // rank-0 candidate
         double t0 = GBMW_INF, f0 = GBMW_INF;
         int j0 = -1;
-        for (int j = 0; j < S; ++j) {
+        for (int n = 0; n < S; ++n) {
             double T, F;
-            row_value(r, e, j, T, F);
+            row_value(r, e, n, T, F);
+            const int j = sJ[n];
             if (T < GBMW_INF && (j0 < 0 || lex_less(T, F, j, t0, f0, j0))) { t0 = T; f0 = F; j0 = j; }
         }
         if (p.frontier_off >= 0) a.frontier[p.frontier_off + e - 1] = t0;

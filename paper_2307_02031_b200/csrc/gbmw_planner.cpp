@@ -134,6 +134,75 @@ std::vector<int32_t> greedy_split(const std::vector<double> &w, int S) {
     return sizes;
 }
 
+// The partition-independent pieces of costs.stage_cost (costs.py:322-352) for a fixed
+// per-layer strategy list: layer times, transform cost from the previous layer, model
+// states, O_b, and O_f per stage index (the 1F1B stash depends on it), p2p per stage
+// start.  stage() folds them in exactly the reference's order.
+struct PartitionTables {
+    int L = 0, S = 0;
+    std::vector<double> t, tns, r, ob, oms, p2p, of;   // of: L x S (stage index 1..S)
+
+    int build(const gbmw_layer *layers, int n_layers, const gbmw_strategy *strats, int n_stages,
+              const gbmw_env &env, int64_t micro, int32_t n_micro) {
+        L = n_layers;
+        S = n_stages;
+        t.resize(L); tns.resize(L); r.assign(L, 0.0); ob.resize(L); oms.resize(L); p2p.resize(L);
+        of.resize((size_t)L * S);
+        if (n_micro < 1) return perr(GBMW_ESTAGE, "n_micro must be >= 1, got " + std::to_string(n_micro));
+        for (int l = 0; l < L; ++l) {
+            const gbmw_strategy &s = strats[l];
+            const StratDeg d = strat_degrees(s);
+            if (micro % d.data != 0) return perr(GBMW_EMICRO, "micro-batch not divisible by the DP*SDP degree");
+            if (S > s.pp_degree)
+                return perr(GBMW_ESTAGE, "stage_index " + std::to_string(s.pp_degree + 1) + " out of range 1.." +
+                                             std::to_string(s.pp_degree));
+            layer_times(layers[l], s, d, micro, env, &t[l], &tns[l]);
+            if (l > 0) {
+                const StratDeg pd = strat_degrees(strats[l - 1]);
+                r[l] = transform_cost(layers[l].bnd_bytes_per_sample, pd.data, pd.tp, d.data, d.tp, micro,
+                                      env.intra_island_bw);
+            }
+            p2p[l] = stage_p2p_time(layers[l].bnd_bytes_per_sample, micro, s.pp_degree, env);
+            for (int st = 1; st <= S; ++st) {
+                const Mem m = layer_memory(layers[l], d, micro, st, n_micro, env.ms_bytes_per_param_byte);
+                of[(size_t)l * S + (st - 1)] = m.o_f;
+                ob[l] = m.o_b;
+                oms[l] = m.o_ms;
+            }
+        }
+        return GBMW_OK;
+    }
+
+    StageCostOut stage(int a, int b, int stage_index) const {
+        double ts = 0.0, ns = 0.0;
+        for (int l = a; l < b; ++l) {
+            const double rr = (l == a) ? 0.0 : r[l];
+            ts = ts + (t[l] + rr);
+            ns = ns + (tns[l] + rr);
+        }
+        if (stage_index > 1) {
+            ts = ts + p2p[a];
+            ns = ns + p2p[a];
+        }
+        double ms = 0.0, pf = 0.0, peak = 0.0;
+        for (int l = a; l < b; ++l) {
+            ms = ms + oms[l];
+            pf = pf + of[(size_t)l * S + (stage_index - 1)];
+            peak = py_max(peak, pf + ob[l]);
+        }
+        StageCostOut o;
+        o.t = ts; o.ns = ns; o.peak = peak + ms;
+        return o;
+    }
+
+    void costs(const std::vector<int32_t> &sizes, StageCostOut *out) const {
+        for (int s = 0, a = 0; s < S; ++s) {
+            out[s] = stage(a, a + sizes[s], s + 1);
+            a += sizes[s];
+        }
+    }
+};
+
 // balance.py:180-212 _init_partition (greedy split + hill climbing on alpha)
 int init_partition(const gbmw_layer *layers, int n_layers, const gbmw_strategy *seeds, int S,
                    const gbmw_env &env, int64_t micro, int32_t n_micro, bool memory, std::vector<int32_t> &out) {
@@ -153,39 +222,47 @@ int init_partition(const gbmw_layer *layers, int n_layers, const gbmw_strategy *
             w[l] = t;
         }
     }
-    std::vector<StageCostOut> sc(S);
-    auto score = [&](const std::vector<int32_t> &sizes, double *alpha) {
-        int rc = partition_costs(layers, seeds, sizes.data(), S, env, micro, n_micro, sc.data());
-        if (rc) return rc;
-        return balance_alpha(sc.data(), S, memory, alpha);
-    };
-    std::vector<int32_t> best = greedy_split(w, S);
-    double best_score;
-    int rc = score(best, &best_score);
+    // Per-layer pieces of stage_cost are independent of the partition except through
+    // the stage index (stash, p2p) and the stage start (no transform cost): tabulate
+    // them once, then a stage's cost is an O(stage length) fold in the reference's
+    // order, and a neighbour move re-costs only the two stages it changes.
+    PartitionTables tab;
+    int rc = tab.build(layers, n_layers, seeds, S, env, micro, n_micro);
     if (rc) return rc;
+    std::vector<int32_t> best = greedy_split(w, S);
+    std::vector<StageCostOut> sc(S), cand_sc(S);
+    tab.costs(best, sc.data());
+    double best_score;
+    if ((rc = balance_alpha(sc.data(), S, memory, &best_score))) return rc;
     // balance.py:160-177 _hill_climb, max_rounds = 2 L; neighbour order of _neighbor_moves
+    std::vector<int32_t> starts(S);
     for (int round = 0; round < 2 * n_layers; ++round) {
         bool found = false;
         std::vector<int32_t> round_best;
         double round_score = best_score;
+        for (int s = 0, a = 0; s < S; ++s) { starts[s] = a; a += best[s]; }
         for (int b = 0; b + 1 < S; ++b) {
             for (int dir = 0; dir < 2; ++dir) {
-                std::vector<int32_t> cand = best;
-                if (dir == 0) {
-                    if (cand[b] <= 1) continue;
-                    cand[b] -= 1; cand[b + 1] += 1;
-                } else {
-                    if (cand[b + 1] <= 1) continue;
-                    cand[b] += 1; cand[b + 1] -= 1;
-                }
+                if (dir == 0 ? best[b] <= 1 : best[b + 1] <= 1) continue;
+                const int mid = starts[b] + best[b] + (dir == 0 ? -1 : 1);   // new boundary
+                cand_sc = sc;
+                cand_sc[b] = tab.stage(starts[b], mid, b + 1);
+                cand_sc[b + 1] = tab.stage(mid, starts[b + 1] + best[b + 1], b + 2);
                 double s;
-                if ((rc = score(cand, &s))) return rc;
-                if (s > round_score + 1e-15) { round_best = cand; round_score = s; found = true; }
+                if ((rc = balance_alpha(cand_sc.data(), S, memory, &s))) return rc;
+                if (s > round_score + 1e-15) {
+                    round_best = best;
+                    if (dir == 0) { round_best[b] -= 1; round_best[b + 1] += 1; }
+                    else { round_best[b] += 1; round_best[b + 1] -= 1; }
+                    round_score = s;
+                    found = true;
+                }
             }
         }
         if (!found) break;
         best = round_best;
         best_score = round_score;
+        tab.costs(best, sc.data());
     }
     out = best;
     return GBMW_OK;

@@ -15,6 +15,8 @@ from dataclasses import dataclass
 from functools import lru_cache
 from typing import Any, Sequence
 
+import numpy as np
+
 from .balance import (
     BalanceReport,
     PipelinePartition,
@@ -26,7 +28,7 @@ from .balance import (
     init_partition_memory_balanced,
     partition_layers,
 )
-from .costs import EvalContext, layer_memory, pipeline_cost, stage_cost
+from .costs import EvalContext, StageCost, layer_memory, pipeline_cost, stage_cost
 from .dpsearch import StageProblem, dp_search_batch
 from .errors import InfeasiblePlanError
 from .strategies import (
@@ -99,8 +101,102 @@ def _sset(n_devices: int, pp_degree: int):
     return enumerate_pruned(n_devices, pp_degree)
 
 
+def _stage_ranges(model, stages):
+    """(start, length) of each stage if the stages are consecutive slices of model.layers."""
+    layers = model.layers
+    index = _layer_index(model)
+    out = []
+    for st in stages:
+        if not st:
+            return None
+        a = index.get(id(st[0]))
+        if a is None or a + len(st) > len(layers) or any(layers[a + i] is not l for i, l in enumerate(st)):
+            return None
+        out.append((a, len(st)))
+    return out
+
+
+_index_cache: dict = {}
+
+
+def _layer_index(model):
+    hit = _index_cache.get(id(model))
+    if hit is None or hit[0] is not model:
+        if len(_index_cache) > 32:
+            _index_cache.clear()
+        hit = (model, {id(l): i for i, l in enumerate(model.layers)})
+        _index_cache[id(model)] = hit
+    return hit[1]
+
+
+def _search_slices(cells, ctx, opts):
+    """galvatron_search for cells whose stages are slices of ctx.model: one flat problem
+    table over a single copy of the model's layers, no per-stage Python objects."""
+    from . import _native
+    from .dpsearch import MAX_BUCKETS, _Marshal, run_native_batch
+    if opts.approx_prev:
+        raise NotImplementedError("approx_prev (collapsed-state DP, dpsearch.py:306-375) is not "
+                                  "implemented on the device path yet")
+    gran = opts.granularity_bytes
+    mar = _Marshal()
+    base = mar.layer_range(list(ctx.model.layers), ctx.profile)
+    env = mar.env(ctx)
+    flags = _native.STAGE_COST | (_native.FUSE if opts.fuse_identical else 0)
+    rows, metas = [], []
+    for budget, ranges, n_devices, batch, pp in cells:
+        m = init_microbatch_num(batch, pp, opts.microbatch_cap_factor, opts.min_micro_size)
+        micro = batch // m
+        sset = _sset(n_devices, pp)
+        strats = sset.strategies
+        if gran <= 0:
+            raise ValueError(f"granularity_bytes must be positive, got {gran}")
+        if budget < 0:
+            raise ValueError(f"budget_bytes must be non-negative, got {budget}")
+        nb = int(budget // gran)
+        if nb > MAX_BUCKETS:
+            raise ValueError(f"budget/granularity yields {nb} buckets (> {MAX_BUCKETS}); "
+                             f"increase the memory granularity")
+        if nb == 0 or not any(micro % s.data_degree == 0 for s in strats):
+            metas.append((m, None, None, strats))
+            continue
+        sb = mar.strat_range(sset, list(strats))
+        r0 = len(rows)
+        for idx, (start, n) in enumerate(ranges, start=1):
+            rows.append((base + start, n, sb, len(strats), env, idx, m, flags, micro, gran, float(budget), nb))
+        metas.append((m, r0, len(rows), strats))
+    out = []
+    if rows:
+        layers, loffs, strats_arr, soffs, envs = mar.finish()
+        probs = np.array(rows, dtype=_native.PROBLEM_DT)
+        probs["layer_begin"] += loffs[0]
+        probs["strat_begin"] = [soffs[r] for r in probs["strat_begin"]]
+        rc, msg, res, plans, _ = run_native_batch(layers, strats_arr, envs, probs)
+        if rc != _native.OK:
+            bad = np.flatnonzero(res["status"] != 0)
+            _native.raise_status(int(res["status"][bad[0]]) if len(bad) else rc, msg)
+        plan_off = np.concatenate(([0], np.cumsum(probs["n_layers"])))
+    for m, r0, r1, strats in metas:
+        if r0 is None or not res["feasible"][r0:r1].all():      # first infeasible stage (planner.py:159-160)
+            out.append(SearchOutcome(cost=INF, strategies=None, stage_costs=None, n_micro=m))
+            continue
+        idx = plans[plan_off[r0]:plan_off[r1]]
+        costs = tuple(StageCost(float(a), float(b), float(c)) for a, b, c in
+                      zip(res["stage_time"][r0:r1], res["stage_ns"][r0:r1], res["stage_peak"][r0:r1]))
+        out.append(SearchOutcome(cost=pipeline_cost(costs, m), strategies=tuple(strats[j] for j in idx),
+                                 stage_costs=costs, n_micro=m))
+    return out
+
+
 def galvatron_search_batch(cells: Sequence[tuple], ctx: EvalContext, opts: PlannerOptions = PlannerOptions()):
     """Many ``galvatron_search(budget, stages, n_devices, batch, pp_degree)`` calls, one device pass."""
+    sliced = []
+    for budget, stages, n_devices, batch, pp in cells:
+        ranges = _stage_ranges(ctx.model, stages)
+        if ranges is None:
+            break
+        sliced.append((budget, ranges, n_devices, batch, pp))
+    else:
+        return _search_slices(sliced, ctx, opts)
     problems, spans, metas = [], [], []
     for budget, stages, n_devices, batch, pp in cells:
         m = init_microbatch_num(batch, pp, opts.microbatch_cap_factor, opts.min_micro_size)
@@ -188,17 +284,39 @@ def _infeasibility_diagnostics(model, ctx, batch, opts) -> dict:
     return diag
 
 
-def _base_cells(model, ctx, batch, opts):
-    """(pp_degree, partition, call) for every degree of one batch size (planner.py:243-262)."""
+_pool = None
+
+
+def _executor():
+    """Host threads for the native seed partitions (the ctypes calls release the GIL)."""
+    global _pool
+    if _pool is None:
+        import os
+        from concurrent.futures import ThreadPoolExecutor
+        _pool = ThreadPoolExecutor(max_workers=max(1, min(32, len(os.sched_getaffinity(0)))))
+    return _pool
+
+
+def _base_cells_window(model, ctx, batches, opts):
+    """Per batch size: (pp_degree, partition, call) for every degree (planner.py:243-262);
+    the seed partitions of all (batch, degree) pairs are computed concurrently."""
     cluster = ctx.cluster
-    out = []
-    for p in candidate_pp_degrees(cluster.n_devices):
-        if p > model.num_layers:
-            continue
-        m = init_microbatch_num(batch, p, opts.microbatch_cap_factor, opts.min_micro_size)
-        _, part = _seed_and_partition(model, ctx, cluster.n_devices, p, batch // m, m)
-        out.append((p, part, (cluster.mem_budget_bytes, partition_layers(model, part), cluster.n_devices, batch, p)))
-    return out
+    pairs = [(b, p) for b in batches for p in candidate_pp_degrees(cluster.n_devices) if p <= model.num_layers]
+
+    def seed(bp):
+        b, p = bp
+        m = init_microbatch_num(b, p, opts.microbatch_cap_factor, opts.min_micro_size)
+        return _seed_and_partition(model, ctx, cluster.n_devices, p, b // m, m)[1]
+
+    parts = list(_executor().map(seed, pairs)) if len(pairs) > 1 else [seed(bp) for bp in pairs]
+    out = {b: [] for b in batches}
+    for (b, p), part in zip(pairs, parts):
+        out[b].append((p, part, (cluster.mem_budget_bytes, partition_layers(model, part), cluster.n_devices, b, p)))
+    return [out[b] for b in batches]
+
+
+def _base_cells(model, ctx, batch, opts):
+    return _base_cells_window(model, ctx, [batch], opts)[0]
 
 
 def galvatron_base(model, cluster, profile, opts: PlannerOptions = PlannerOptions()) -> Plan:
@@ -211,7 +329,7 @@ def galvatron_base(model, cluster, profile, opts: PlannerOptions = PlannerOption
     while pos < len(batches):
         chunk = batches[pos:pos + window]
         pos += len(chunk)
-        per_batch = [_base_cells(model, ctx, b, opts) for b in chunk]
+        per_batch = _base_cells_window(model, ctx, chunk, opts)
         flat = [c[2] for cells in per_batch for c in cells]
         outcomes = galvatron_search_batch(flat, ctx, opts)
         k = 0
