@@ -78,7 +78,7 @@ struct HostProb {
     int64_t n_b = 0;
     int64_t plan_off = 0, frontier_off = -1;
     // workspace footprint (elements)
-    int64_t n_cells = 0, n_r = 0, n_bcells = 0, n_par = 0, n_tiles = 0, n_step_tiles = 0;
+    int64_t n_cells = 0, n_r = 0, n_bcells = 0, n_par = 0, n_tiles = 0, n_step_tiles = 0, n_flagw = 0;
     size_t ws_bytes = 0;
 };
 
@@ -88,7 +88,7 @@ struct Chunk {
     int group_lo[kStepGroups + 1] = {0};
     std::vector<int> n_active[kStepGroups];   // per group, per u: problems of the group with U > u
     int Umax = 0, max_k = 1;
-    int64_t n_cells = 0, n_r = 0, n_bcells = 0, n_par = 0, n_tiles = 0, n_units = 0;
+    int64_t n_cells = 0, n_r = 0, n_bcells = 0, n_par = 0, n_tiles = 0, n_units = 0, n_flagw = 0;
     size_t small_off = 0;          // byte offset of this chunk's descriptor block in the arena
     // offsets inside the descriptor block
     size_t o_probs, o_cellp, o_rp, o_stepp, o_sweepp, o_cand, o_ccls, o_clsd, o_clst, o_uf, o_uc;
@@ -448,9 +448,10 @@ void prepare_problem(gbmw_batch &b, int pi, std::string *err) {
     h.n_par = (int64_t)(h.U - 1) * h.K * n_e;
     h.n_tiles = (h.n_b + kSweepThreads - 1) / kSweepThreads;
     h.n_step_tiles = (n_e + kStepRows - 1) / kStepRows;
+    h.n_flagw = (h.U > 1) ? (int64_t)h.K * flag_words(n_e) : 0;
     h.ws_bytes = (size_t)h.n_cells * (sizeof(Cell) + sizeof(CellMem) + 4) + (size_t)h.U * 12 + (size_t)h.n_r * 8 + 8 +
                  (size_t)h.n_bcells * 2 * sizeof(TFCell) + (size_t)h.n_par * 2 +
-                 (size_t)(2 * h.n_tiles + 1) * sizeof(SweepPartial) + 8;
+                 (size_t)(2 * h.n_tiles + 1) * sizeof(SweepPartial) + 8 + (size_t)h.n_flagw * 8;
     h.gpu = true;
 }
 
@@ -464,7 +465,7 @@ size_t put(std::vector<char> &blob, const T *src, size_t n) {
 
 // chunk workspace layout (byte offsets from ws base)
 struct WsLayout {
-    size_t cells, cmem, rcls, bup, tf0, tf1, par, parts, uparts, bestp, bound, uniq, nuniq, ulo, uhi, ctr, total;
+    size_t cells, cmem, rcls, bup, tf0, tf1, chg0, chg1, par, parts, uparts, bestp, bound, uniq, nuniq, ulo, uhi, ctr, total;
 };
 WsLayout ws_layout(const Chunk &c) {
     WsLayout w;
@@ -475,6 +476,8 @@ WsLayout ws_layout(const Chunk &c) {
     w.bup = o; o = align_up(o + c.probs.size() * 8);
     w.tf0 = o; o = align_up(o + c.n_bcells * sizeof(TFCell));
     w.tf1 = o; o = align_up(o + c.n_bcells * sizeof(TFCell));
+    w.chg0 = o; o = align_up(o + c.n_flagw * 4);
+    w.chg1 = o; o = align_up(o + c.n_flagw * 4);
     w.par = o; o = align_up(o + c.n_par * 2);
     w.parts = o; o = align_up(o + c.n_tiles * sizeof(SweepPartial));
     w.uparts = o; o = align_up(o + c.n_tiles * sizeof(SweepPartial));
@@ -586,6 +589,7 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
             }
             d.cand_off = sit->second.first; d.class_off = sit->second.second; d.unit_off = uit->second;
             d.ustate_off = (int32_t)c.n_units;
+            d.flag_off = c.n_flagw;
             d.layer_begin = P.layer_begin; d.strat_begin = P.strat_begin; d.result_index = pi;
             d.n_sweep_tiles = (int32_t)h.n_tiles;
             dps.push_back(d);
@@ -594,6 +598,7 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
             stepp.push_back(stepp.back() + h.n_step_tiles);
             sweepp.push_back(c.n_tiles);
             c.n_units += h.U;
+            c.n_flagw += h.n_flagw;
             c.Umax = std::max(c.Umax, h.U);
             c.max_k = std::max(c.max_k, h.K);
         }
@@ -644,7 +649,7 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
     b->o_results = o; o = align_up(o + b->problems.size() * sizeof(gbmw_result));
     b->o_plans = o; o = align_up(o + (size_t)b->total_plan * sizeof(int32_t));
     b->o_frontier = o; o = align_up(o + (size_t)b->total_frontier * sizeof(double));
-    b->o_stats = o; o = align_up(o + (b->chunks.size() + 1) * 8);
+    b->o_stats = o; o = align_up(o + 2 * (b->chunks.size() + 1) * 8);
     b->arena_size = std::max<size_t>(o, 256);
     for (Chunk &c : b->chunks) c.small_off += o_blob;
     cudaSetDevice(ctx->device);
@@ -751,6 +756,8 @@ ChunkArgs chunk_args(gbmw_batch *b, const Chunk &c, char *ws, size_t chunk_index
     a.bup = (unsigned long long *)(ws + w.bup);
     a.TF[0] = (TFCell *)(ws + w.tf0);
     a.TF[1] = (TFCell *)(ws + w.tf1);
+    a.chg[0] = (uint32_t *)(ws + w.chg0);
+    a.chg[1] = (uint32_t *)(ws + w.chg1);
     a.par = (uint16_t *)(ws + w.par);
     a.partials = (SweepPartial *)(ws + w.parts);
     a.best = (SweepPartial *)(ws + w.bestp);
@@ -766,6 +773,7 @@ ChunkArgs chunk_args(gbmw_batch *b, const Chunk &c, char *ws, size_t chunk_index
     a.plans = (int32_t *)(arena + b->o_plans);
     a.frontier = (double *)(arena + b->o_frontier);
     a.live_cells = (unsigned long long *)(arena + b->o_stats) + chunk_index;
+    a.computed_cells = (unsigned long long *)(arena + b->o_stats) + (b->chunks.size() + 1) + chunk_index;
     return a;
 }
 
@@ -781,7 +789,7 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
     b->timing.total_ms = b->timing.dp_ms = b->timing.sweep_ms = b->timing.tables_ms = b->timing.finalize_ms = 0.f;
     b->timing.n_launches = 0;
     cudaStream_t st = ctx->stream;
-    cudaMemsetAsync((char *)b->arena + b->o_stats, 0, (b->chunks.size() + 1) * 8, st);
+    cudaMemsetAsync((char *)b->arena + b->o_stats, 0, 2 * (b->chunks.size() + 1) * 8, st);
     for (Chunk &c : b->chunks) {
         for (auto &e : c.ev)
             if (!e) cudaEventCreate(&e);
@@ -825,11 +833,15 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
     }
     if (!tables_only && !b->chunks.empty()) {
         // K2 algorithmic bytes = 34 B per live class cell
-        std::vector<unsigned long long> live(b->chunks.size());
+        std::vector<unsigned long long> live(2 * (b->chunks.size() + 1));
         cudaMemcpy(live.data(), (char *)b->arena + b->o_stats, live.size() * 8, cudaMemcpyDeviceToHost);
         double cells = 0.0;
         for (auto v : live) cells += (double)v;
-        b->timing.dp_bytes = cells * (16.0 + 16.0 + 2.0);
+        double computed = 0.0;
+        for (size_t i = 0; i < b->chunks.size(); ++i) computed += (double)live[b->chunks.size() + 1 + i];
+        // writes of every live class cell (t, f, argmin) + source reads of the rows evaluated
+        b->timing.dp_bytes = cells * 18.0 + computed * 16.0;
+        b->timing.dp_cells = computed;
         b->timing.live_cells = cells;
     }
     b->ran = true;

@@ -21,8 +21,13 @@ constexpr int kMaxUnits = 1024;      // backtrack path held in local memory
 constexpr int kMaxClasses = 16;
 constexpr int kMaxStrats = 512;      // smem staging of per-strategy constants
 constexpr int kStepThreads = 256;    // threads per K2 CTA
-constexpr int kStepRowsPerThread = 2;
-constexpr int kStepRows = kStepThreads * kStepRowsPerThread;   // rows per K2 tile
+constexpr int kStepRows = 2048;      // rows per K2 tile (64 groups of 32)
+
+// change-bit words per class column of n_e rows (one spare word for 2-word window reads)
+#if defined(__CUDACC__)
+__host__ __device__
+#endif
+inline int64_t flag_words(int64_t n_e) { return (n_e + 31) / 32 + 2; }
 constexpr int kSweepThreads = 256;   // rows per K3 tile
 
 // K2 is instantiated per class-count group so a problem with few classes does not
@@ -62,6 +67,7 @@ struct DevProblem {
     int32_t result_index;   // slot in the batch result array
     int32_t n_sweep_tiles;
     int32_t ustate_off;     // into per-problem unit state: nuniq / unit_lo / unit_hi (U)
+    int64_t flag_off;       // into the change-bit buffers (K * flag_words(n_e) words)
 };
 
 struct alignas(16) TFCell {
@@ -100,6 +106,8 @@ struct ChunkArgs {
     double *rcls;
     unsigned long long *bup;      // per problem, bits of max O_b (all >= 0)
     TFCell *TF[2];
+    uint32_t *chg[2];             // change bits of B_u (ping-pong with TF): bit x = row x != row x-1
+    unsigned long long *computed_cells;   // class cells K2 evaluated (rows x K), per chunk
     uint16_t *par;
     SweepPartial *partials;       // K3 per-tile best safe bucket
     SweepPartial *best;           // per problem: best safe bucket

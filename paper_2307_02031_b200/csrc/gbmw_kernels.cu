@@ -149,185 +149,7 @@ __global__ void k_dedupe(ChunkArgs a) {
     }
 }
 
-// ---------------------------------------------------------------- K2: min-plus layer step
-// One thread per bucket row e' of one problem.  Reads the previous unit's table row
-// T_{u-1}[e', :] (reconstructed from the class-reduced B_{u-1}, or the init row for
-// u == 1), relaxes it against every target class and writes B_u[e', k] and its argmin.
-// Tie-break T1 (dpsearch.py:271-276): lexicographic (cand, F, i), first i wins.
-//
-// Each thread owns NR rows (stride kStepThreads) so the per-strategy constants and
-// transform costs read from shared memory are shared by its rows; the strategy loop
-// is processed in batches of IB so 2*NR*IB independent 16-byte loads are in flight
-// before the first relaxation.  KT is the exact class count (CTA-uniform dispatch)
-// up to 8; KT = kMaxClasses with a runtime guard covers larger strategy spaces.
-constexpr int kStepIB = 4;            // strategy batch (K >= 5 groups); K <= 4 uses 2
-constexpr int kStepChunk = 4;             // tiles taken per atomic grab
-
-struct StepShared {
-    Cell cell[kMaxStrats];                // distinct source strategies of unit u-1 (ascending)
-    int idx[kMaxStrats];                  // their strategy index
-    double r[kMaxClasses * kMaxClasses];
-    int S, K, n_e, q;
-    int lo_prev;                          // L_{u-1}: rows of B_{u-1} below are +inf
-    int lo, hi;                           // live rows [L_u, H_u] of B_u
-    int64_t b_off, par_off, tile0;
-    int64_t next;
-};
-
-template <int KT, int NR, int IB, bool FIRST, bool GUARD>
-__device__ __forceinline__ void step_rows(const ChunkArgs &a, const StepShared &sh, int u, int e0) {
-    const int S = sh.S, K = GUARD ? sh.K : KT;
-    const int n_e = sh.n_e, lo_prev = FIRST ? 0 : sh.lo_prev, lo = sh.lo, hi = sh.hi;
-    const TFCell *bin = a.TF[(u - 1) & 1] + sh.b_off;
-
-    double bt[NR][KT], bf[NR][KT];
-    int bp[NR][KT];
-#pragma unroll
-    for (int r = 0; r < NR; ++r)
-#pragma unroll
-        for (int kk = 0; kk < KT; ++kk) { bt[r][kk] = GBMW_INF; bf[r][kk] = GBMW_INF; bp[r][kk] = 0; }
-
-    for (int i0 = 0; i0 < S; i0 += IB) {
-        double T[IB][NR], F[kStepIB][NR];
-#pragma unroll
-        for (int b = 0; b < IB; ++b) {
-            const int i = i0 + b;
-            const Cell c = sh.cell[i < S ? i : 0];
-#pragma unroll
-            for (int r = 0; r < NR; ++r) {
-                const int e = e0 + r * kStepThreads;
-                const int src = e - c.w;
-                T[b][r] = GBMW_INF; F[b][r] = GBMW_INF;
-                if (i < S && src >= lo_prev && e <= hi) {
-                    if (FIRST) {                   // init row, dpsearch.py:255-259
-                        T[b][r] = c.c; F[b][r] = c.ef;
-                    } else {                       // T_{u-1}[e,i] = B_{u-1}[e-w,k].t + time_c
-                        const double2 v = __ldg(reinterpret_cast<const double2 *>(bin + c.k * n_e + src));
-                        T[b][r] = v.x;
-                        F[b][r] = v.y;
-                    }
-                }
-            }
-        }
-#pragma unroll
-        for (int b = 0; b < IB; ++b) {
-            const int i = i0 + b;
-            if (i >= S) break;
-            const Cell c = sh.cell[i];
-            const int gi = sh.idx[i];
-            const double *rrow = sh.r + c.k * K;
-            double Tv[NR], Fv[NR];
-#pragma unroll
-            for (int r = 0; r < NR; ++r) {
-                Tv[r] = FIRST ? T[b][r] : T[b][r] + c.c;
-                Fv[r] = FIRST ? F[b][r] : F[b][r] + c.ef;
-            }
-#pragma unroll
-            for (int kk = 0; kk < KT; ++kk) {
-                if (!GUARD || kk < K) {
-                    const double rv = rrow[kk];
-#pragma unroll
-                    for (int r = 0; r < NR; ++r) {
-                        const double cand = Tv[r] + rv;
-                        const bool better = (cand < bt[r][kk]) || (cand == bt[r][kk] && Fv[r] < bf[r][kk]);
-                        bt[r][kk] = better ? cand : bt[r][kk];
-                        bf[r][kk] = better ? Fv[r] : bf[r][kk];
-                        bp[r][kk] = better ? gi : bp[r][kk];
-                    }
-                }
-            }
-        }
-    }
-    TFCell *bout = a.TF[u & 1] + sh.b_off;
-    uint16_t *pout = a.par + sh.par_off + (int64_t)(u - 1) * K * n_e;
-#pragma unroll
-    for (int r = 0; r < NR; ++r) {
-        const int e = e0 + r * kStepThreads;
-        if (e < lo || e > hi) continue;          // dead rows: never read
-#pragma unroll
-        for (int kk = 0; kk < KT; ++kk) {
-            if (!GUARD || kk < K) {
-                reinterpret_cast<double2 *>(bout)[kk * n_e + e] = make_double2(bt[r][kk], bf[r][kk]);
-                pout[kk * n_e + e] = (uint16_t)bp[r][kk];
-            }
-        }
-    }
-}
-
-// Persistent CTAs pulling kStepChunk consecutive tiles at a time from a per-launch
-// atomic counter (balances the dead-row skipping); a problem's constants are staged
-// in shared memory once per problem change.  GROUP selects the class-count range
-// (step_group): 0 -> K 1..4 with two rows per pass, 1 -> K 5..8 one row per pass,
-// 2 -> K 9..16 generic.  A tile is always kStepRows rows.
-template <int GROUP, bool FIRST>
-__global__ void __launch_bounds__(kStepThreads, GROUP == 0 ? 3 : 2) k_dp_step(ChunkArgs a, int u, int64_t tile_base,
-                                                           int64_t n_tiles, unsigned long long *counter) {
-    __shared__ StepShared sh;
-    int q_prev = -1;
-    while (true) {
-        __syncthreads();                           // everyone is done with sh.next / sh tables
-        if (threadIdx.x == 0) sh.next = (int64_t)atomicAdd(counter, (unsigned long long)kStepChunk);
-        __syncthreads();
-        const int64_t c0 = sh.next;
-        if (c0 >= n_tiles) break;
-        const int64_t c1 = min(c0 + kStepChunk, n_tiles);
-        for (int64_t t = c0; t < c1; ++t) {
-            const int64_t tile = tile_base + t;
-            const int q = __ldg(a.step_map + tile);
-            const DevProblem &p = a.probs[q];
-            const int64_t first_row = (tile - a.step_tiles[q]) * kStepRows;
-            const int lo = a.unit_lo[p.ustate_off + u], hi = a.unit_hi[p.ustate_off + u];
-            if (first_row > hi || first_row + kStepRows - 1 < lo) continue;   // dead tile (CTA-uniform)
-            if (q != q_prev) {
-                __syncthreads();                   // previous problem's readers are done
-                const int S = p.S, K = p.K;
-                const Cell *prev_cells = a.cells + p.cell_off + (int64_t)(u - 1) * S;
-                const int32_t *ul = a.uniq + p.cell_off + (int64_t)(u - 1) * S;
-                const int nu = a.nuniq[p.ustate_off + u - 1];
-                for (int n = threadIdx.x; n < nu; n += blockDim.x) {
-                    const int j = ul[n];
-                    sh.cell[n] = prev_cells[j];
-                    sh.idx[n] = j;
-                }
-                const double *r_u = a.rcls + p.r_off + (int64_t)u * K * K;
-                for (int x = threadIdx.x; x < K * K; x += blockDim.x) sh.r[x] = r_u[x];
-                if (threadIdx.x == 0) {
-                    sh.S = nu; sh.K = K; sh.n_e = (int)(p.n_b + 1); sh.q = q;
-                    sh.lo_prev = a.unit_lo[p.ustate_off + u - 1];
-                    sh.lo = lo; sh.hi = hi;
-                    sh.b_off = p.b_off; sh.par_off = p.par_off; sh.tile0 = a.step_tiles[q];
-                }
-                __syncthreads();
-                q_prev = q;
-            }
-            const int base = (int)first_row + threadIdx.x;
-            const int K = sh.K;
-            if (GROUP == 0) {
-                switch (K) {
-                    case 1: step_rows<1, 2, 2, FIRST, false>(a, sh, u, base); break;
-                    case 2: step_rows<2, 2, 2, FIRST, false>(a, sh, u, base); break;
-                    case 3: step_rows<3, 2, 2, FIRST, false>(a, sh, u, base); break;
-                    default: step_rows<4, 2, 2, FIRST, false>(a, sh, u, base); break;
-                }
-            } else if (GROUP == 1) {
-#pragma unroll 1
-                for (int pass = 0; pass < 2; ++pass) {
-                    const int e0 = base + pass * kStepThreads;
-                    switch (K) {
-                        case 5: step_rows<5, 1, kStepIB, FIRST, false>(a, sh, u, e0); break;
-                        case 6: step_rows<6, 1, kStepIB, FIRST, false>(a, sh, u, e0); break;
-                        case 7: step_rows<7, 1, kStepIB, FIRST, false>(a, sh, u, e0); break;
-                        default: step_rows<8, 1, kStepIB, FIRST, false>(a, sh, u, e0); break;
-                    }
-                }
-            } else {
-#pragma unroll 1
-                for (int pass = 0; pass < 2; ++pass)
-                    step_rows<kMaxClasses, 1, kStepIB, FIRST, true>(a, sh, u, base + pass * kStepThreads);
-            }
-        }
-    }
-}
+// K2 (the min-plus layer step) lives in gbmw_step.cu.
 
 // ---------------------------------------------------------------- shared helpers
 // reference table of the last unit at row e, strategy j
@@ -670,39 +492,6 @@ int launch_cost_tables(const ChunkArgs &a, int64_t n_cells, int64_t n_r, void *s
     if (n_cells > 0) k_cost_cells<<<blocks_for(n_cells, 128), 128, 0, st>>>(a, n_cells);
     if (n_r > 0) k_cost_r<<<blocks_for(n_r, 128), 128, 0, st>>>(a, n_r);
     if (a.n_units > 0 && a.n_probs > 0) k_dedupe<<<a.n_probs, 128, 0, st>>>(a);
-    return (int)cudaGetLastError();
-}
-
-int launch_dp_step(const ChunkArgs &a, int group, int u, int64_t tile_base, int64_t n_tiles,
-                   unsigned long long *counter, void *stream) {
-    cudaStream_t st = (cudaStream_t)stream;
-    if (n_tiles <= 0) return 0;
-    // persistent grid: as many CTAs as fit at once (per instantiation), capped by the work
-    static int sms = 0;
-    static int occ[kStepGroups][2] = {{0}};
-    if (sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
-    }
-    const int fi = (u == 1) ? 1 : 0;
-    if (occ[group][fi] == 0) {
-        int n = 1;
-        if (group == 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fi ? k_dp_step<0, true> : k_dp_step<0, false>, kStepThreads, 0);
-        else if (group == 1) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fi ? k_dp_step<1, true> : k_dp_step<1, false>, kStepThreads, 0);
-        else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fi ? k_dp_step<2, true> : k_dp_step<2, false>, kStepThreads, 0);
-        occ[group][fi] = n > 0 ? n : 1;
-    }
-    const int64_t max_ctas = (int64_t)sms * occ[group][fi];
-    const int64_t want = (n_tiles + kStepChunk - 1) / kStepChunk;
-    const unsigned grid = (unsigned)(want < max_ctas ? want : max_ctas);
-#define GBMW_STEP(G)                                                                                \
-    if (u == 1) k_dp_step<G, true><<<grid, kStepThreads, 0, st>>>(a, u, tile_base, n_tiles, counter);  \
-    else k_dp_step<G, false><<<grid, kStepThreads, 0, st>>>(a, u, tile_base, n_tiles, counter);
-    if (group == 0) { GBMW_STEP(0) }
-    else if (group == 1) { GBMW_STEP(1) }
-    else { GBMW_STEP(2) }
-#undef GBMW_STEP
     return (int)cudaGetLastError();
 }
 

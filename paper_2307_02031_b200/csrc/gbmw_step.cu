@@ -1,0 +1,351 @@
+// gbmw_step.cu — K2, the min-plus layer step of the stage search, run-length aware.
+//
+// Reference step (dpsearch.py:261-280), restated per source row e' and target class k
+// (DESIGN.md §3):
+//   B_u[e',k] = lexmin_i (T_{u-1}[e',i] + R_u[cls i, k], F_{u-1}[e',i], i),
+//   T_{u-1}[e',i] = B_{u-1}[e'-w_{u-1,i}, cls i].t + time_c[u-1,i]   (init row for u == 1).
+// B is a step function of e': most aligned 32-row groups see the same (T, F) vector in
+// every row (SURVEY-scale configs: 86-100 % of live groups).  A group is "flat" when,
+// for every distinct source strategy i, the 32-row source window of column cls(i) of
+// B_{u-1} contains no change point; its 32 outputs are then the output of its first
+// row, computed once.  Change points of B_u are emitted as one bit per (class, row)
+// (bit x = row x differs from row x-1), exactly; a spurious 1 bit would only cost
+// work, never exactness.
+//
+// One CTA processes one tile of kStepRows rows of one problem:
+//   1. classify the tile's 32-row groups (dead / flat / full) from the change bits,
+//   2. compute the list of rows that need it: every row of a full group (one warp per
+//      group, lanes in row order), one row per flat group, and the row before the
+//      tile (for the first change bit),
+//   3. write flat groups' rows from shared memory, and the change-bit words.
+// Tie-break T1 (lexicographic (cand, F, i), first i) is the one of every row.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "gbmw_internal.h"
+
+namespace gbmw {
+
+#define GBMW_STEP_INF __longlong_as_double(0x7ff0000000000000LL)
+
+constexpr int kStepIB = 4;                  // strategy batch: independent loads in flight
+constexpr int kGroups = kStepRows / 32;     // 32-row groups per tile
+
+struct StepShared {
+    Cell cell[kMaxStrats];                  // distinct source strategies of unit u-1 (ascending)
+    int idx[kMaxStrats];                    // their strategy index
+    double r[kMaxClasses * kMaxClasses];
+    int S, K, n_e, q, lo_prev, lo, hi, nw;
+    int64_t b_off, par_off, tile0, f_off;
+    int64_t next;
+    // per tile
+    int kind[kGroups];                      // 0 dead, 1 flat, 2 full
+    int list_np[kGroups], list_fl[kGroups];
+    int n_np, n_fl;
+    unsigned bits[kGroups][kMaxClasses];
+    double first_t[kGroups][kMaxClasses], first_f[kGroups][kMaxClasses];
+    double last_t[kGroups][kMaxClasses], last_f[kGroups][kMaxClasses];
+    int rep_p[kGroups][kMaxClasses];
+    double prev_t[kMaxClasses], prev_f[kMaxClasses];
+    int prev_ok;
+    unsigned long long stat_rows;
+};
+
+// K lexmins of one source row e' (T1 tie-break).  Rows outside [lo_prev + w, hi] read +inf.
+template <int KT, bool FIRST, bool GUARD>
+__device__ __forceinline__ void relax_row(const ChunkArgs &a, const StepShared &sh, int u, int e,
+                                          double *bt, double *bf, int *bp) {
+    const int S = sh.S, K = GUARD ? sh.K : KT;
+    const int n_e = sh.n_e, lo_prev = FIRST ? 0 : sh.lo_prev, hi = sh.hi;
+    const TFCell *bin = a.TF[(u - 1) & 1] + sh.b_off;
+#pragma unroll
+    for (int kk = 0; kk < KT; ++kk) { bt[kk] = GBMW_STEP_INF; bf[kk] = GBMW_STEP_INF; bp[kk] = 0; }
+    const bool row_ok = e >= 0 && e <= hi;
+    for (int i0 = 0; i0 < S; i0 += kStepIB) {
+        double T[kStepIB], F[kStepIB];
+#pragma unroll
+        for (int b = 0; b < kStepIB; ++b) {
+            const int i = i0 + b;
+            const Cell c = sh.cell[i < S ? i : 0];
+            const int src = e - c.w;
+            T[b] = GBMW_STEP_INF; F[b] = GBMW_STEP_INF;
+            if (i < S && row_ok && src >= lo_prev) {
+                if (FIRST) {                       // init row, dpsearch.py:255-259
+                    T[b] = c.c; F[b] = c.ef;
+                } else {
+                    const double2 v = __ldg(reinterpret_cast<const double2 *>(bin + c.k * n_e + src));
+                    T[b] = v.x + c.c;
+                    F[b] = v.y + c.ef;
+                }
+            }
+        }
+#pragma unroll
+        for (int b = 0; b < kStepIB; ++b) {
+            const int i = i0 + b;
+            if (i >= S) break;
+            const int ck = sh.cell[i].k;
+            const int gi = sh.idx[i];
+            const double *rrow = sh.r + ck * K;
+#pragma unroll
+            for (int kk = 0; kk < KT; ++kk) {
+                if (!GUARD || kk < K) {
+                    const double cand = T[b] + rrow[kk];
+                    const bool better = (cand < bt[kk]) || (cand == bt[kk] && F[b] < bf[kk]);
+                    bt[kk] = better ? cand : bt[kk];
+                    bf[kk] = better ? F[b] : bf[kk];
+                    bp[kk] = better ? gi : bp[kk];
+                }
+            }
+        }
+    }
+}
+
+// Is column k of B_{u-1} constant on source rows [x0, x0 + 31]?  Rows below lo_prev are
+// +inf (never written); a window straddling lo_prev mixes +inf and finite rows.
+__device__ __forceinline__ bool window_flat(int x0, int lo_prev, const uint32_t *flags_k) {
+    const int x1 = x0 + 31;
+    if (x1 < lo_prev) return true;
+    if (x0 < lo_prev) return false;
+    const int lb = x0 + 1;                                  // change bits of rows x0+1 .. x1
+    const int w0 = lb >> 5, s = lb & 31;
+    const unsigned long long v =
+        ((unsigned long long)__ldg(flags_k + w0 + 1) << 32 | (unsigned long long)__ldg(flags_k + w0)) >> s;
+    return (v & 0x7fffffffull) == 0ull;
+}
+
+template <int KT, bool FIRST, bool GUARD>
+__device__ void step_tile(const ChunkArgs &a, StepShared &sh, int u, int first_row) {
+    const int K = GUARD ? sh.K : KT;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthr = blockDim.x;
+    const int n_e = sh.n_e, lo = sh.lo, hi = sh.hi, S = sh.S;
+    // ---- 1. classify groups
+    for (int g = tid; g < kGroups; g += nthr) {
+        const int r0 = first_row + 32 * g, r1 = r0 + 31;
+        sh.kind[g] = (r1 < lo || r0 > hi) ? 0 : ((r0 >= lo && r1 <= hi) ? 1 : 2);
+    }
+    __syncthreads();
+    const uint32_t *fin = a.chg[(u - 1) & 1] + sh.f_off;
+    for (int x = tid; x < kGroups * S; x += nthr) {
+        const int g = x / S, n = x - g * S;
+        if (sh.kind[g] != 1) continue;
+        const Cell c = sh.cell[n];
+        const int r0 = first_row + 32 * g;
+        bool flat;
+        if (FIRST) flat = (r0 >= c.w) || (r0 + 31 < c.w);
+        else flat = window_flat(r0 - c.w, sh.lo_prev, fin + (int64_t)c.k * sh.nw);
+        if (!flat) sh.kind[g] = 2;
+    }
+    __syncthreads();
+    // ---- 2. row list: full groups (32 rows, one warp each), then flat representatives
+    if (warp == 0) {
+        int np = 0, nf = 0;
+        for (int base = 0; base < kGroups; base += 32) {
+            const int g = base + lane;
+            const int kd = g < kGroups ? sh.kind[g] : 0;
+            const unsigned mnp = __ballot_sync(0xffffffffu, kd == 2), mfl = __ballot_sync(0xffffffffu, kd == 1);
+            const unsigned below = (1u << lane) - 1u;
+            if (kd == 2) sh.list_np[np + __popc(mnp & below)] = g;
+            if (kd == 1) sh.list_fl[nf + __popc(mfl & below)] = g;
+            np += __popc(mnp);
+            nf += __popc(mfl);
+        }
+        if (lane == 0) {
+            sh.n_np = np;
+            sh.n_fl = nf;
+            sh.stat_rows += (unsigned long long)(32 * np + nf + 1) * (unsigned long long)K;
+        }
+    }
+    __syncthreads();
+    const int n_np = sh.n_np, n_fl = sh.n_fl;
+    const int n_list = 32 * n_np + n_fl + 1;                // + the row before the tile
+    TFCell *bout = a.TF[u & 1] + sh.b_off;
+    uint16_t *pout = a.par + sh.par_off + (int64_t)(u - 1) * K * n_e;
+    const int n_pass = (n_list + nthr - 1) / nthr;
+    for (int pass = 0; pass < n_pass; ++pass) {
+        const int x = pass * nthr + tid;
+        double bt[KT], bf[KT];
+        int bp[KT];
+        int e = -1, kind = -1, g = -1;
+        if (x < 32 * n_np) {
+            g = sh.list_np[x >> 5]; e = first_row + 32 * g + lane; kind = 2;
+        } else if (x < 32 * n_np + n_fl) {
+            g = sh.list_fl[x - 32 * n_np]; e = first_row + 32 * g; kind = 1;
+        } else if (x == 32 * n_np + n_fl) {
+            e = first_row - 1; kind = 3;
+        }
+        relax_row<KT, FIRST, GUARD>(a, sh, u, (kind >= 0 && e >= lo && e <= hi && e < n_e) ? e : -1, bt, bf, bp);
+        if (kind == 2) {
+            const bool live = e >= lo && e <= hi;
+            if (live) {
+#pragma unroll
+                for (int kk = 0; kk < KT; ++kk)
+                    if (!GUARD || kk < K) {
+                        reinterpret_cast<double2 *>(bout)[kk * n_e + e] = make_double2(bt[kk], bf[kk]);
+                        pout[kk * n_e + e] = (uint16_t)bp[kk];
+                    }
+            }
+        }
+        // change bits inside full groups (a full group is exactly one warp of this pass)
+        const bool in_np = (pass * nthr + warp * 32) < 32 * n_np;
+#pragma unroll
+        for (int kk = 0; kk < KT; ++kk) {
+            if (GUARD && kk >= K) break;
+            if (in_np) {
+                const double pt = __shfl_up_sync(0xffffffffu, bt[kk], 1);
+                const double pf = __shfl_up_sync(0xffffffffu, bf[kk], 1);
+                const bool chg = lane > 0 && (pt != bt[kk] || pf != bf[kk]);
+                const unsigned m = __ballot_sync(0xffffffffu, chg);
+                if (lane == 0) { sh.bits[g][kk] = m; sh.first_t[g][kk] = bt[kk]; sh.first_f[g][kk] = bf[kk]; }
+                if (lane == 31) { sh.last_t[g][kk] = bt[kk]; sh.last_f[g][kk] = bf[kk]; }
+            } else if (kind == 1) {
+                sh.bits[g][kk] = 0u;
+                sh.first_t[g][kk] = sh.last_t[g][kk] = bt[kk];
+                sh.first_f[g][kk] = sh.last_f[g][kk] = bf[kk];
+                sh.rep_p[g][kk] = bp[kk];
+            } else if (kind == 3) {
+                sh.prev_t[kk] = bt[kk];
+                sh.prev_f[kk] = bf[kk];
+            }
+        }
+        if (kind == 3) sh.prev_ok = (e >= lo && e <= hi) ? 1 : 0;
+    }
+    __syncthreads();
+    // ---- 3a. flat groups: 32 copies of the representative row
+    for (int x = tid; x < 32 * n_fl; x += nthr) {
+        const int g = sh.list_fl[x >> 5];
+        const int e = first_row + 32 * g + (x & 31);
+#pragma unroll
+        for (int kk = 0; kk < KT; ++kk)
+            if (!GUARD || kk < K) {
+                reinterpret_cast<double2 *>(bout)[kk * n_e + e] = make_double2(sh.first_t[g][kk], sh.first_f[g][kk]);
+                pout[kk * n_e + e] = (uint16_t)sh.rep_p[g][kk];
+            }
+    }
+    // ---- 3b. change-bit words of B_u (bit 0 of a group compares with the previous row)
+    uint32_t *fout = a.chg[u & 1] + sh.f_off;
+    const int w_first = first_row >> 5;
+    for (int x = tid; x < kGroups * K; x += nthr) {
+        const int g = x / K, kk = x - g * K;
+        const int wi = w_first + g;
+        if (wi >= sh.nw) continue;
+        unsigned word;
+        if (sh.kind[g] == 0) {
+            word = 0xffffffffu;                              // dead rows: never read as flat
+        } else {
+            word = sh.bits[g][kk];
+            bool same;
+            if (g == 0) same = sh.prev_ok && sh.prev_t[kk] == sh.first_t[0][kk] && sh.prev_f[kk] == sh.first_f[0][kk];
+            else same = sh.kind[g - 1] != 0 && sh.last_t[g - 1][kk] == sh.first_t[g][kk] &&
+                        sh.last_f[g - 1][kk] == sh.first_f[g][kk];
+            if (!same) word |= 1u;
+        }
+        fout[(int64_t)kk * sh.nw + wi] = word;
+    }
+    __syncthreads();
+}
+
+template <int GROUP, bool FIRST>
+__global__ void __launch_bounds__(kStepThreads) k_dp_step(ChunkArgs a, int u, int64_t tile_base, int64_t n_tiles,
+                                                           unsigned long long *counter) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    StepShared &sh = *reinterpret_cast<StepShared *>(smem_raw);
+    int q_prev = -1;
+    if (threadIdx.x == 0) sh.stat_rows = 0;
+    while (true) {
+        __syncthreads();
+        if (threadIdx.x == 0) sh.next = (int64_t)atomicAdd(counter, 1ull);
+        __syncthreads();
+        const int64_t t = sh.next;
+        if (t >= n_tiles) break;
+        const int64_t tile = tile_base + t;
+        const int q = __ldg(a.step_map + tile);
+        const DevProblem &p = a.probs[q];
+        const int64_t first_row = (tile - a.step_tiles[q]) * kStepRows;
+        const int lo = a.unit_lo[p.ustate_off + u], hi = a.unit_hi[p.ustate_off + u];
+        if (first_row > hi || first_row + kStepRows - 1 < lo) continue;      // dead tile (CTA-uniform)
+        if (q != q_prev) {
+            __syncthreads();
+            const int S = p.S, K = p.K;
+            const Cell *prev_cells = a.cells + p.cell_off + (int64_t)(u - 1) * S;
+            const int32_t *ul = a.uniq + p.cell_off + (int64_t)(u - 1) * S;
+            const int nu = a.nuniq[p.ustate_off + u - 1];
+            for (int n = threadIdx.x; n < nu; n += blockDim.x) {
+                const int j = ul[n];
+                sh.cell[n] = prev_cells[j];
+                sh.idx[n] = j;
+            }
+            const double *r_u = a.rcls + p.r_off + (int64_t)u * K * K;
+            for (int x = threadIdx.x; x < K * K; x += blockDim.x) sh.r[x] = r_u[x];
+            if (threadIdx.x == 0) {
+                sh.S = nu; sh.K = K; sh.n_e = (int)(p.n_b + 1); sh.q = q;
+                sh.lo_prev = a.unit_lo[p.ustate_off + u - 1];
+                sh.lo = lo; sh.hi = hi;
+                sh.b_off = p.b_off; sh.par_off = p.par_off; sh.tile0 = a.step_tiles[q];
+                sh.f_off = p.flag_off; sh.nw = (int)flag_words(p.n_b + 1);
+            }
+            __syncthreads();
+            q_prev = q;
+        }
+        const int K = sh.K;
+        if (GROUP == 0) {
+            switch (K) {
+                case 1: step_tile<1, FIRST, false>(a, sh, u, (int)first_row); break;
+                case 2: step_tile<2, FIRST, false>(a, sh, u, (int)first_row); break;
+                case 3: step_tile<3, FIRST, false>(a, sh, u, (int)first_row); break;
+                default: step_tile<4, FIRST, false>(a, sh, u, (int)first_row); break;
+            }
+        } else if (GROUP == 1) {
+            switch (K) {
+                case 5: step_tile<5, FIRST, false>(a, sh, u, (int)first_row); break;
+                case 6: step_tile<6, FIRST, false>(a, sh, u, (int)first_row); break;
+                case 7: step_tile<7, FIRST, false>(a, sh, u, (int)first_row); break;
+                default: step_tile<8, FIRST, false>(a, sh, u, (int)first_row); break;
+            }
+        } else {
+            step_tile<kMaxClasses, FIRST, true>(a, sh, u, (int)first_row);
+        }
+    }
+    if (threadIdx.x == 0 && sh.stat_rows) atomicAdd(a.computed_cells, sh.stat_rows);
+}
+
+int launch_dp_step(const ChunkArgs &a, int group, int u, int64_t tile_base, int64_t n_tiles,
+                   unsigned long long *counter, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n_tiles <= 0) return 0;
+    const size_t smem = sizeof(StepShared);
+    static int sms = 0;
+    static int occ[kStepGroups][2] = {{0}};
+    if (sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
+    }
+    const int fi = (u == 1) ? 1 : 0;
+#define GBMW_KFN(G, F) k_dp_step<G, F>
+#define GBMW_PREP(G, F)                                                                             \
+    do {                                                                                            \
+        cudaFuncSetAttribute(GBMW_KFN(G, F), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        int n = 1;                                                                                  \
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, GBMW_KFN(G, F), kStepThreads, smem);      \
+        occ[G][F ? 1 : 0] = n > 0 ? n : 1;                                                          \
+    } while (0)
+    if (occ[group][fi] == 0) {
+        if (group == 0) { if (fi) GBMW_PREP(0, true); else GBMW_PREP(0, false); }
+        else if (group == 1) { if (fi) GBMW_PREP(1, true); else GBMW_PREP(1, false); }
+        else { if (fi) GBMW_PREP(2, true); else GBMW_PREP(2, false); }
+    }
+    const int64_t max_ctas = (int64_t)sms * occ[group][fi];
+    const unsigned grid = (unsigned)(n_tiles < max_ctas ? n_tiles : max_ctas);
+#define GBMW_STEP(G)                                                                                        \
+    if (fi) GBMW_KFN(G, true)<<<grid, kStepThreads, smem, st>>>(a, u, tile_base, n_tiles, counter);          \
+    else GBMW_KFN(G, false)<<<grid, kStepThreads, smem, st>>>(a, u, tile_base, n_tiles, counter);
+    if (group == 0) { GBMW_STEP(0) }
+    else if (group == 1) { GBMW_STEP(1) }
+    else { GBMW_STEP(2) }
+#undef GBMW_STEP
+#undef GBMW_PREP
+#undef GBMW_KFN
+    return (int)cudaGetLastError();
+}
+
+}  // namespace gbmw
