@@ -70,6 +70,22 @@ struct DevProblem {
     int64_t flag_off;       // into the change-bit buffers (K * flag_words(n_e) words)
 };
 
+#if defined(__CUDACC__)
+// Is column k of B (change bits flags_k, bit x = row x differs from row x-1) constant on
+// rows [x0, x0 + 31]?  Rows below lo are +inf (never written); a window straddling lo
+// mixes +inf and finite rows.  Only the bits of rows x0+1 .. x0+31 are read.
+__device__ __forceinline__ bool window_flat(int x0, int lo, const uint32_t *flags_k) {
+    const int x1 = x0 + 31;
+    if (x1 < lo) return true;
+    if (x0 < lo) return false;
+    const int lb = x0 + 1;
+    const int w0 = lb >> 5, s = lb & 31;
+    const unsigned long long v =
+        ((unsigned long long)__ldg(flags_k + w0 + 1) << 32 | (unsigned long long)__ldg(flags_k + w0)) >> s;
+    return (v & 0x7fffffffull) == 0ull;
+}
+#endif
+
 struct alignas(16) TFCell {
     double t;       // lexmin candidate time
     double f;       // accumulated true forward bytes of its path (tie-break)

@@ -288,12 +288,27 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(ChunkArgs a) {
     double best_t = GBMW_INF;
     int64_t best_e = -1;
     int best_j = 0;
+    // Flat warp: every distinct strategy's 32-row source window of B_{U-1} is constant, so
+    // all rows of the warp have the same table row; read it at the warp's first row
+    // (uniform, broadcast loads).  Exact; see gbmw_step.cu for the change bits.
+    const int lane = threadIdx.x & 31;
+    const int64_t e_w0 = e - lane;
+    bool flat = true;
+    const uint32_t *fl = a.chg[last & 1] + p.flag_off;
+    const int nw = (int)flag_words(p.n_b + 1);
+    for (int n = lane; n < S; n += 32) {
+        const int w = sW[n];
+        if (last == 0) flat = flat && ((e_w0 >= w) || (e_w0 + 31 < w));
+        else flat = flat && window_flat((int)(e_w0 - w), (int)lo, fl + (int64_t)sK[n] * nw);
+    }
+    flat = __all_sync(0xffffffffu, flat);
+    const int64_t e_val = flat ? e_w0 : e;
     if (e <= p.n_b) {
         double t0 = GBMW_INF, f0 = GBMW_INF;
         int j0 = -1;
         for (int n = 0; n < S; ++n) {
             double T, F;
-            row_value(r, e, n, T, F);
+            row_value(r, e_val, n, T, F);
             const int j = sJ[n];
             if (T < GBMW_INF && (j0 < 0 || lex_less(T, F, j, t0, f0, j0))) { t0 = T; f0 = F; j0 = j; }
         }

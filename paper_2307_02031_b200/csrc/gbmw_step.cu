@@ -31,10 +31,12 @@ namespace gbmw {
 constexpr int kStepIB = 4;                  // strategy batch: independent loads in flight
 constexpr int kGroups = kStepRows / 32;     // 32-row groups per tile
 
+// KM: class capacity of the instantiation (4 / 8 / kMaxClasses), sizes the per-group arrays
+template <int KM>
 struct StepShared {
     Cell cell[kMaxStrats];                  // distinct source strategies of unit u-1 (ascending)
     int idx[kMaxStrats];                    // their strategy index
-    double r[kMaxClasses * kMaxClasses];
+    double r[KM * KM];
     int S, K, n_e, q, lo_prev, lo, hi, nw;
     int64_t b_off, par_off, tile0, f_off;
     int64_t next;
@@ -42,18 +44,18 @@ struct StepShared {
     int kind[kGroups];                      // 0 dead, 1 flat, 2 full
     int list_np[kGroups], list_fl[kGroups];
     int n_np, n_fl;
-    unsigned bits[kGroups][kMaxClasses];
-    double first_t[kGroups][kMaxClasses], first_f[kGroups][kMaxClasses];
-    double last_t[kGroups][kMaxClasses], last_f[kGroups][kMaxClasses];
-    int rep_p[kGroups][kMaxClasses];
-    double prev_t[kMaxClasses], prev_f[kMaxClasses];
+    unsigned bits[kGroups][KM];
+    double first_t[kGroups][KM], first_f[kGroups][KM];
+    double last_t[kGroups][KM], last_f[kGroups][KM];
+    int rep_p[kGroups][KM];
+    double prev_t[KM], prev_f[KM];
     int prev_ok;
     unsigned long long stat_rows;
 };
 
 // K lexmins of one source row e' (T1 tie-break).  Rows outside [lo_prev + w, hi] read +inf.
-template <int KT, bool FIRST, bool GUARD>
-__device__ __forceinline__ void relax_row(const ChunkArgs &a, const StepShared &sh, int u, int e,
+template <int KT, bool FIRST, bool GUARD, class SH>
+__device__ __forceinline__ void relax_row(const ChunkArgs &a, const SH &sh, int u, int e,
                                           double *bt, double *bf, int *bp) {
     const int S = sh.S, K = GUARD ? sh.K : KT;
     const int n_e = sh.n_e, lo_prev = FIRST ? 0 : sh.lo_prev, hi = sh.hi;
@@ -100,21 +102,8 @@ __device__ __forceinline__ void relax_row(const ChunkArgs &a, const StepShared &
     }
 }
 
-// Is column k of B_{u-1} constant on source rows [x0, x0 + 31]?  Rows below lo_prev are
-// +inf (never written); a window straddling lo_prev mixes +inf and finite rows.
-__device__ __forceinline__ bool window_flat(int x0, int lo_prev, const uint32_t *flags_k) {
-    const int x1 = x0 + 31;
-    if (x1 < lo_prev) return true;
-    if (x0 < lo_prev) return false;
-    const int lb = x0 + 1;                                  // change bits of rows x0+1 .. x1
-    const int w0 = lb >> 5, s = lb & 31;
-    const unsigned long long v =
-        ((unsigned long long)__ldg(flags_k + w0 + 1) << 32 | (unsigned long long)__ldg(flags_k + w0)) >> s;
-    return (v & 0x7fffffffull) == 0ull;
-}
-
-template <int KT, bool FIRST, bool GUARD>
-__device__ void step_tile(const ChunkArgs &a, StepShared &sh, int u, int first_row) {
+template <int KT, bool FIRST, bool GUARD, class SH>
+__device__ void step_tile(const ChunkArgs &a, SH &sh, int u, int first_row) {
     const int K = GUARD ? sh.K : KT;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthr = blockDim.x;
     const int n_e = sh.n_e, lo = sh.lo, hi = sh.hi, S = sh.S;
@@ -245,10 +234,11 @@ __device__ void step_tile(const ChunkArgs &a, StepShared &sh, int u, int first_r
 }
 
 template <int GROUP, bool FIRST>
-__global__ void __launch_bounds__(kStepThreads) k_dp_step(ChunkArgs a, int u, int64_t tile_base, int64_t n_tiles,
+__global__ void __launch_bounds__(kStepThreads, GROUP == 2 ? 2 : 3) k_dp_step(ChunkArgs a, int u, int64_t tile_base, int64_t n_tiles,
                                                            unsigned long long *counter) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    StepShared &sh = *reinterpret_cast<StepShared *>(smem_raw);
+    using SH = StepShared<GROUP == 0 ? 4 : (GROUP == 1 ? 8 : kMaxClasses)>;
+    SH &sh = *reinterpret_cast<SH *>(smem_raw);
     int q_prev = -1;
     if (threadIdx.x == 0) sh.stat_rows = 0;
     while (true) {
@@ -312,7 +302,8 @@ int launch_dp_step(const ChunkArgs &a, int group, int u, int64_t tile_base, int6
                    unsigned long long *counter, void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
     if (n_tiles <= 0) return 0;
-    const size_t smem = sizeof(StepShared);
+    const size_t smem = group == 0 ? sizeof(StepShared<4>) : (group == 1 ? sizeof(StepShared<8>)
+                                                                           : sizeof(StepShared<kMaxClasses>));
     static int sms = 0;
     static int occ[kStepGroups][2] = {{0}};
     if (sms == 0) {
