@@ -288,21 +288,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(ChunkArgs a) {
     double best_t = GBMW_INF;
     int64_t best_e = -1;
     int best_j = 0;
-    // Flat warp: every distinct strategy's 32-row source window of B_{U-1} is constant, so
-    // all rows of the warp have the same table row; read it at the warp's first row
-    // (uniform, broadcast loads).  Exact; see gbmw_step.cu for the change bits.
-    const int lane = threadIdx.x & 31;
-    const int64_t e_w0 = e - lane;
-    bool flat = true;
-    const uint32_t *fl = a.chg[last & 1] + p.flag_off;
-    const int nw = (int)flag_words(p.n_b + 1);
-    for (int n = lane; n < S; n += 32) {
-        const int w = sW[n];
-        if (last == 0) flat = flat && ((e_w0 >= w) || (e_w0 + 31 < w));
-        else flat = flat && window_flat((int)(e_w0 - w), (int)lo, fl + (int64_t)sK[n] * nw);
-    }
-    flat = __all_sync(0xffffffffu, flat);
-    const int64_t e_val = flat ? e_w0 : e;
+    const int64_t e_val = e;
     if (e <= p.n_b) {
         double t0 = GBMW_INF, f0 = GBMW_INF;
         int j0 = -1;
@@ -394,6 +380,22 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
     r.bin = a.TF[last & 1] + p.b_off;
     volatile unsigned long long *bound = a.bound + q;
     const int64_t e = e0 + threadIdx.x;
+    // flat warp (see k_sweep): the candidate order is the same in all its rows; read
+    // the row values at the warp's first row (broadcast).  Walks stay per row.
+    const int lane = threadIdx.x & 31;
+    const int64_t e_w0 = e - lane;
+    bool flat = true;
+    {
+        const uint32_t *fl = a.chg[last & 1] + p.flag_off;
+        const int nw = (int)flag_words(p.n_b + 1);
+        for (int n = lane; n < S; n += 32) {
+            const int w = sW[n];
+            if (last == 0) flat = flat && ((e_w0 >= w) || (e_w0 + 31 < w));
+            else flat = flat && window_flat((int)(e_w0 - w), (int)r.lo, fl + (int64_t)sK[n] * nw);
+        }
+    }
+    flat = __all_sync(0xffffffffu, flat);
+    const int64_t e_val = flat ? e_w0 : e;
     double mt = GBMW_INF;
     int64_t me = -1;
     int mj = 0;
@@ -406,7 +408,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
             int nj = -1;
             for (int j = 0; j < S; ++j) {
                 double T, F;
-                row_value(r, e, j, T, F);
+                row_value(r, e_val, j, T, F);
                 if (!(T < GBMW_INF)) continue;
                 if (cj >= 0 && !lex_less(ct, cf, cj, T, F, j)) continue;
                 if (nj < 0 || lex_less(T, F, j, nt, nf, nj)) { nt = T; nf = F; nj = j; }
