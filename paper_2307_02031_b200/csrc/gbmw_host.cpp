@@ -78,7 +78,7 @@ struct HostProb {
     int64_t n_b = 0;
     int64_t plan_off = 0, frontier_off = -1;
     // workspace footprint (elements)
-    int64_t n_cells = 0, n_r = 0, n_bcells = 0, n_par = 0, n_tiles = 0, n_step_tiles = 0, n_flagw = 0;
+    int64_t n_cells = 0, n_r = 0, n_bcells = 0, n_par = 0, n_tiles = 0, n_step_tiles = 0, n_flagw = 0, n_gflat = 0;
     size_t ws_bytes = 0;
 };
 
@@ -88,7 +88,7 @@ struct Chunk {
     int group_lo[kStepGroups + 1] = {0};
     std::vector<int> n_active[kStepGroups];   // per group, per u: problems of the group with U > u
     int Umax = 0, max_k = 1;
-    int64_t n_cells = 0, n_r = 0, n_bcells = 0, n_par = 0, n_tiles = 0, n_units = 0, n_flagw = 0;
+    int64_t n_cells = 0, n_r = 0, n_bcells = 0, n_par = 0, n_tiles = 0, n_units = 0, n_flagw = 0, n_gflat = 0;
     size_t small_off = 0;          // byte offset of this chunk's descriptor block in the arena
     // offsets inside the descriptor block
     size_t o_probs, o_cellp, o_rp, o_stepp, o_sweepp, o_cand, o_ccls, o_clsd, o_clst, o_uf, o_uc;
@@ -449,9 +449,10 @@ void prepare_problem(gbmw_batch &b, int pi, std::string *err) {
     h.n_tiles = (h.n_b + kSweepThreads - 1) / kSweepThreads;
     h.n_step_tiles = (n_e + kStepRows - 1) / kStepRows;
     h.n_flagw = (h.U > 1) ? (int64_t)h.K * flag_words(n_e) : 0;
+    h.n_gflat = (int64_t)(h.U > 1 ? h.U - 1 : 0) * gflat_words(n_e);
     h.ws_bytes = (size_t)h.n_cells * (sizeof(Cell) + sizeof(CellMem) + 4) + (size_t)h.U * 12 + (size_t)h.n_r * 8 + 8 +
                  (size_t)h.n_bcells * 2 * sizeof(TFCell) + (size_t)h.n_par * 2 +
-                 (size_t)(2 * h.n_tiles + 1) * sizeof(SweepPartial) + 8 + (size_t)h.n_flagw * 8;
+                 (size_t)(2 * h.n_tiles + 1) * sizeof(SweepPartial) + 8 + (size_t)h.n_flagw * 8 + (size_t)h.n_gflat * 4;
     h.gpu = true;
 }
 
@@ -465,7 +466,7 @@ size_t put(std::vector<char> &blob, const T *src, size_t n) {
 
 // chunk workspace layout (byte offsets from ws base)
 struct WsLayout {
-    size_t cells, cmem, rcls, bup, tf0, tf1, chg0, chg1, par, parts, uparts, bestp, bound, uniq, nuniq, ulo, uhi, ctr, total;
+    size_t cells, cmem, rcls, bup, tf0, tf1, chg0, chg1, gflat, par, parts, uparts, bestp, bound, uniq, nuniq, ulo, uhi, ctr, total;
 };
 WsLayout ws_layout(const Chunk &c) {
     WsLayout w;
@@ -478,6 +479,7 @@ WsLayout ws_layout(const Chunk &c) {
     w.tf1 = o; o = align_up(o + c.n_bcells * sizeof(TFCell));
     w.chg0 = o; o = align_up(o + c.n_flagw * 4);
     w.chg1 = o; o = align_up(o + c.n_flagw * 4);
+    w.gflat = o; o = align_up(o + c.n_gflat * 4);
     w.par = o; o = align_up(o + c.n_par * 2);
     w.parts = o; o = align_up(o + c.n_tiles * sizeof(SweepPartial));
     w.uparts = o; o = align_up(o + c.n_tiles * sizeof(SweepPartial));
@@ -590,6 +592,7 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
             d.cand_off = sit->second.first; d.class_off = sit->second.second; d.unit_off = uit->second;
             d.ustate_off = (int32_t)c.n_units;
             d.flag_off = c.n_flagw;
+            d.gflat_off = c.n_gflat;
             d.layer_begin = P.layer_begin; d.strat_begin = P.strat_begin; d.result_index = pi;
             d.n_sweep_tiles = (int32_t)h.n_tiles;
             dps.push_back(d);
@@ -599,6 +602,7 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
             sweepp.push_back(c.n_tiles);
             c.n_units += h.U;
             c.n_flagw += h.n_flagw;
+            c.n_gflat += h.n_gflat;
             c.Umax = std::max(c.Umax, h.U);
             c.max_k = std::max(c.max_k, h.K);
         }
@@ -758,6 +762,7 @@ ChunkArgs chunk_args(gbmw_batch *b, const Chunk &c, char *ws, size_t chunk_index
     a.TF[1] = (TFCell *)(ws + w.tf1);
     a.chg[0] = (uint32_t *)(ws + w.chg0);
     a.chg[1] = (uint32_t *)(ws + w.chg1);
+    a.gflat = (uint32_t *)(ws + w.gflat);
     a.par = (uint16_t *)(ws + w.par);
     a.partials = (SweepPartial *)(ws + w.parts);
     a.best = (SweepPartial *)(ws + w.bestp);

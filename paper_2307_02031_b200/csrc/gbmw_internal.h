@@ -28,6 +28,12 @@ constexpr int kStepRows = 2048;      // rows per K2 tile (64 groups of 32)
 __host__ __device__
 #endif
 inline int64_t flag_words(int64_t n_e) { return (n_e + 31) / 32 + 2; }
+
+// flat-group mask words per unit: one bit per aligned 32-row group of B_u
+#if defined(__CUDACC__)
+__host__ __device__
+#endif
+inline int64_t gflat_words(int64_t n_e) { return ((n_e + 31) / 32 + 31) / 32 + 1; }
 constexpr int kSweepThreads = 256;   // rows per K3 tile
 
 // K2 is instantiated per class-count group so a problem with few classes does not
@@ -68,6 +74,7 @@ struct DevProblem {
     int32_t n_sweep_tiles;
     int32_t ustate_off;     // into per-problem unit state: nuniq / unit_lo / unit_hi (U)
     int64_t flag_off;       // into the change-bit buffers (K * flag_words(n_e) words)
+    int64_t gflat_off;      // into the flat-group masks ((U-1) * gflat_words(n_e) words)
 };
 
 #if defined(__CUDACC__)
@@ -83,6 +90,13 @@ __device__ __forceinline__ bool window_flat(int x0, int lo, const uint32_t *flag
     const unsigned long long v =
         ((unsigned long long)__ldg(flags_k + w0 + 1) << 32 | (unsigned long long)__ldg(flags_k + w0)) >> s;
     return (v & 0x7fffffffull) == 0ull;
+}
+
+// B_u stores one representative row (the first) per flat 32-row group; every reader of a
+// B_u row or of its argmin goes through this (gf_u = that unit's flat-group mask).
+__device__ __forceinline__ int flat_row(const uint32_t *gf_u, int row) {
+    const int g = row >> 5;
+    return ((__ldg(gf_u + (g >> 5)) >> (g & 31)) & 1u) ? (row & ~31) : row;
 }
 #endif
 
@@ -123,6 +137,7 @@ struct ChunkArgs {
     unsigned long long *bup;      // per problem, bits of max O_b (all >= 0)
     TFCell *TF[2];
     uint32_t *chg[2];             // change bits of B_u (ping-pong with TF): bit x = row x != row x-1
+    uint32_t *gflat;              // per unit u >= 1: bit g = 32-row group g of B_u is flat (stored once)
     unsigned long long *computed_cells;   // class cells K2 evaluated (rows x K), per chunk
     uint16_t *par;
     SweepPartial *partials;       // K3 per-tile best safe bucket

@@ -156,6 +156,7 @@ __global__ void k_dedupe(ChunkArgs a) {
 struct RowCtx {
     const int32_t *w; const int32_t *k; const double *c; const double *ef;
     const TFCell *bin;
+    const uint32_t *gf;  // flat-group mask of B_{U-1} (rows of flat groups are stored once)
     int64_t n_e;
     int64_t lo;        // rows of B_{U-1} below L_{U-1} are +inf (never written)
     bool init;
@@ -165,7 +166,7 @@ __device__ __forceinline__ void row_value(const RowCtx &r, int64_t e, int j, dou
     const int w = r.w[j];
     if (e - w < r.lo) { T = GBMW_INF; F = GBMW_INF; return; }
     if (r.init) { T = r.c[j]; F = r.ef[j]; return; }
-    const int64_t src = (int64_t)r.k[j] * r.n_e + (e - w);
+    const int64_t src = (int64_t)r.k[j] * r.n_e + flat_row(r.gf, (int)(e - w));
     const double2 v = __ldg(reinterpret_cast<const double2 *>(r.bin + src));
     T = v.x + r.c[j];
     F = v.y + r.ef[j];
@@ -178,11 +179,13 @@ __device__ __forceinline__ void backtrack(const ChunkArgs &a, const DevProblem &
     const int64_t n_e = p.n_b + 1;
     const Cell *cells = a.cells + p.cell_off;
     const uint16_t *par = a.par + p.par_off;
+    const int gw = (int)gflat_words(n_e);
     path[U - 1] = (uint16_t)j;
     for (int u = U - 1; u >= 1; --u) {
         const Cell c = cells[(int64_t)u * S + j];
         e -= c.w;
-        j = par[((int64_t)(u - 1) * K + c.k) * n_e + e];
+        const int er = flat_row(a.gflat + p.gflat_off + (int64_t)(u - 1) * gw, (int)e);
+        j = par[((int64_t)(u - 1) * K + c.k) * n_e + er];
         path[u - 1] = (uint16_t)j;
     }
 }
@@ -284,6 +287,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(ChunkArgs a) {
     r.init = (last == 0);
     r.lo = (last == 0) ? 0 : lo;
     r.bin = a.TF[last & 1] + p.b_off;
+    r.gf = a.gflat + p.gflat_off + (int64_t)(last >= 1 ? last - 1 : 0) * gflat_words(p.n_b + 1);
 
     double best_t = GBMW_INF;
     int64_t best_e = -1;
@@ -378,6 +382,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
     r.init = (last == 0);
     r.lo = (last == 0) ? 0 : a.unit_lo[p.ustate_off + last];
     r.bin = a.TF[last & 1] + p.b_off;
+    r.gf = a.gflat + p.gflat_off + (int64_t)(last >= 1 ? last - 1 : 0) * gflat_words(p.n_b + 1);
     volatile unsigned long long *bound = a.bound + q;
     const int64_t e = e0 + threadIdx.x;
     // flat warp (see k_sweep): the candidate order is the same in all its rows; read

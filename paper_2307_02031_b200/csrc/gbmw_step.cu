@@ -39,6 +39,8 @@ struct StepShared {
     double r[KM * KM];
     int S, K, n_e, q, lo_prev, lo, hi, nw;
     int64_t b_off, par_off, tile0, f_off;
+    int64_t gf_prev, gf_cur;                // flat-group masks of B_{u-1} / B_u (offsets into a.gflat)
+    int gw;
     int64_t next;
     // per tile
     int kind[kGroups];                      // 0 dead, 1 flat, 2 full
@@ -75,7 +77,8 @@ __device__ __forceinline__ void relax_row(const ChunkArgs &a, const SH &sh, int 
                 if (FIRST) {                       // init row, dpsearch.py:255-259
                     T[b] = c.c; F[b] = c.ef;
                 } else {
-                    const double2 v = __ldg(reinterpret_cast<const double2 *>(bin + c.k * n_e + src));
+                    const int rs = flat_row(a.gflat + sh.gf_prev, src);
+                    const double2 v = __ldg(reinterpret_cast<const double2 *>(bin + c.k * n_e + rs));
                     T[b] = v.x + c.c;
                     F[b] = v.y + c.ef;
                 }
@@ -199,16 +202,20 @@ __device__ void step_tile(const ChunkArgs &a, SH &sh, int u, int first_row) {
         if (kind == 3) sh.prev_ok = (e >= lo && e <= hi) ? 1 : 0;
     }
     __syncthreads();
-    // ---- 3a. flat groups: 32 copies of the representative row
-    for (int x = tid; x < 32 * n_fl; x += nthr) {
-        const int g = sh.list_fl[x >> 5];
-        const int e = first_row + 32 * g + (x & 31);
-#pragma unroll
-        for (int kk = 0; kk < KT; ++kk)
-            if (!GUARD || kk < K) {
-                reinterpret_cast<double2 *>(bout)[kk * n_e + e] = make_double2(sh.first_t[g][kk], sh.first_f[g][kk]);
-                pout[kk * n_e + e] = (uint16_t)sh.rep_p[g][kk];
-            }
+    // ---- 3a. flat groups: the representative (first) row only, plus the group's mask bit;
+    // readers redirect rows of flat groups to it (flat_row)
+    for (int x = tid; x < n_fl * KT; x += nthr) {
+        const int g = sh.list_fl[x / KT], kk = x - (x / KT) * KT;
+        if (GUARD && kk >= K) continue;
+        const int e = first_row + 32 * g;
+        reinterpret_cast<double2 *>(bout)[kk * n_e + e] = make_double2(sh.first_t[g][kk], sh.first_f[g][kk]);
+        pout[kk * n_e + e] = (uint16_t)sh.rep_p[g][kk];
+    }
+    if (tid < kGroups / 32) {
+        unsigned m = 0u;
+        for (int b = 0; b < 32; ++b) m |= (sh.kind[32 * tid + b] == 1 ? 1u : 0u) << b;
+        const int wi = (first_row >> 10) + tid;
+        if (wi < sh.gw) a.gflat[sh.gf_cur + wi] = m;
     }
     // ---- 3b. change-bit words of B_u (bit 0 of a group compares with the previous row)
     uint32_t *fout = a.chg[u & 1] + sh.f_off;
@@ -272,6 +279,9 @@ __global__ void __launch_bounds__(kStepThreads, GROUP == 0 ? 3 : 2) k_dp_step(Ch
                 sh.lo = lo; sh.hi = hi;
                 sh.b_off = p.b_off; sh.par_off = p.par_off; sh.tile0 = a.step_tiles[q];
                 sh.f_off = p.flag_off; sh.nw = (int)flag_words(p.n_b + 1);
+                sh.gw = (int)gflat_words(p.n_b + 1);
+                sh.gf_cur = p.gflat_off + (int64_t)(u - 1) * sh.gw;
+                sh.gf_prev = p.gflat_off + (int64_t)(u >= 2 ? u - 2 : 0) * sh.gw;
             }
             __syncthreads();
             q_prev = q;
