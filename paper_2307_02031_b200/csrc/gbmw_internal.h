@@ -35,6 +35,7 @@ __host__ __device__
 #endif
 inline int64_t gflat_words(int64_t n_e) { return ((n_e + 31) / 32 + 31) / 32 + 1; }
 constexpr int kSweepThreads = 256;   // rows per K3 tile
+constexpr int kSweepWK = 4096;       // (unit, strategy) pairs staged in shared memory by K3b
 
 // K2 is instantiated per class-count group so a problem with few classes does not
 // pay the register footprint of the widest one: K <= 4, 5..8, 9..kMaxClasses.

@@ -190,6 +190,24 @@ __device__ __forceinline__ void backtrack(const ChunkArgs &a, const DevProblem &
     }
 }
 
+// Same walk with (weight, class) of every (unit, strategy) staged in shared memory: the
+// chain per unit is then one global load (the argmin) instead of three.
+__device__ __forceinline__ void backtrack_wk(const ChunkArgs &a, const DevProblem &p, int64_t e, int j,
+                                             uint16_t *path, const int2 *wk) {
+    const int U = p.U, S = p.S, K = p.K;
+    const int64_t n_e = p.n_b + 1;
+    const uint16_t *par = a.par + p.par_off;
+    const int gw = (int)gflat_words(n_e);
+    path[U - 1] = (uint16_t)j;
+    for (int u = U - 1; u >= 1; --u) {
+        const int2 c = wk[u * S + j];
+        e -= c.x;
+        const int er = flat_row(a.gflat + p.gflat_off + (int64_t)(u - 1) * gw, (int)e);
+        j = par[((int64_t)(u - 1) * K + c.y) * n_e + er];
+        path[u - 1] = (uint16_t)j;
+    }
+}
+
 // E_all of the expanded plan in layer order (costs.py:307-318).
 __device__ __forceinline__ double plan_e_all(const ChunkArgs &a, const DevProblem &p, const uint16_t *path) {
     double total_ms = 0.0, prefix_f = 0.0, peak = 0.0;
@@ -258,10 +276,26 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(ChunkArgs a) {
     const int last = p.U - 1;
     const int tile = blockIdx.x - (int)a.sweep_tiles[q];
     const int64_t e = 1 + (int64_t)tile * kSweepThreads + threadIdx.x;
+    const int64_t t_lo = 1 + (int64_t)tile * kSweepThreads, t_hi = t_lo + kSweepThreads - 1;
     // first bucket with a finite row: m_{U-1} = L_{U-1} + wmin_{U-1} (k_dedupe)
     const int64_t lo = a.unit_lo[p.ustate_off + last];
     const int64_t first_finite = lo + (p.n_b - a.unit_hi[p.ustate_off + last]);
-    if (1 + (int64_t)tile * kSweepThreads + kSweepThreads - 1 < first_finite) {   // whole tile +inf
+    // Every T[., j] is non-increasing in the bucket (min-plus of non-increasing columns),
+    // so the rank-0 time t0(e) is too: the best safe bucket (min t0, ties -> larger e) is
+    // the largest safe bucket e_s.  Only it is evaluated unless the frontier is wanted.
+    const double safe_limit = p.budget - __longlong_as_double((long long)a.bup[q]);
+    int64_t e_s;
+    {
+        double x = floor(safe_limit / (double)p.gran);
+        if (!(x >= 0.0)) x = 0.0;
+        if (x > (double)p.n_b) x = (double)p.n_b;
+        e_s = (int64_t)x;
+        while (e_s >= 1 && !int_le_double(e_s * p.gran, safe_limit)) --e_s;
+        while (e_s + 1 <= p.n_b && int_le_double((e_s + 1) * p.gran, safe_limit)) ++e_s;
+    }
+    const bool want_frontier = p.frontier_off >= 0;
+    if ((!want_frontier && !(e_s >= t_lo && e_s <= t_hi)) || t_hi < first_finite) {
+        if (want_frontier && e <= p.n_b) a.frontier[p.frontier_off + e - 1] = GBMW_INF;
         if (e <= p.n_b && p.frontier_off >= 0) a.frontier[p.frontier_off + e - 1] = GBMW_INF;
         if (threadIdx.x == 0) {
             SweepPartial none;
@@ -292,22 +326,18 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(ChunkArgs a) {
     double best_t = GBMW_INF;
     int64_t best_e = -1;
     int best_j = 0;
-    const int64_t e_val = e;
-    if (e <= p.n_b) {
+    if (e <= p.n_b && (want_frontier || e == e_s)) {
         double t0 = GBMW_INF, f0 = GBMW_INF;
         int j0 = -1;
         for (int n = 0; n < S; ++n) {
             double T, F;
-            row_value(r, e_val, n, T, F);
+            row_value(r, e, n, T, F);
             const int j = sJ[n];
             if (T < GBMW_INF && (j0 < 0 || lex_less(T, F, j, t0, f0, j0))) { t0 = T; f0 = F; j0 = j; }
         }
-        if (p.frontier_off >= 0) a.frontier[p.frontier_off + e - 1] = t0;
-        if (j0 >= 0) {
-            const double safe_limit = p.budget - __longlong_as_double((long long)a.bup[q]);
-            if (int_le_double(e * p.gran, safe_limit)) { best_t = t0; best_e = e; best_j = j0; }
-            // unsafe rows: k_sweep_unsafe (top-down, pruned)
-        }
+        if (want_frontier) a.frontier[p.frontier_off + e - 1] = t0;
+        if (j0 >= 0 && e == e_s) { best_t = t0; best_e = e; best_j = j0; }
+        // unsafe rows (e > e_s): k_sweep_unsafe
     }
     SweepPartial sp = block_best(best_t, best_e, best_j, red_t, red_e, red_j);
     if (threadIdx.x == 0) a.partials[p.tile_off + tile] = sp;
@@ -375,6 +405,12 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
         const Cell c = lc[i];
         sW[i] = c.w; sK[i] = c.k; sC[i] = c.c; sE[i] = c.ef;
     }
+    __shared__ int2 sWK[kSweepWK];                      // (weight, class) per (unit, strategy)
+    const bool wk_smem = p.U * S <= kSweepWK;
+    if (wk_smem) {
+        const Cell *cells = a.cells + p.cell_off;
+        for (int x = threadIdx.x; x < p.U * S; x += blockDim.x) sWK[x] = make_int2(cells[x].w, cells[x].k);
+    }
     __syncthreads();
     RowCtx r;
     r.w = sW; r.k = sK; r.c = sC; r.ef = sE;
@@ -420,7 +456,8 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
             }
             if (nj < 0) break;
             if (nt > __longlong_as_double((long long)*bound)) break;      // cannot win
-            backtrack(a, p, e, nj, path);
+            if (wk_smem) backtrack_wk(a, p, e, nj, path, sWK);
+            else backtrack(a, p, e, nj, path);
             if (plan_e_all(a, p, path) <= p.budget) {
                 mt = nt; me = e; mj = nj;
                 atomicMin((unsigned long long *)bound, (unsigned long long)__double_as_longlong(nt));
