@@ -65,6 +65,7 @@ extern "C" {
 #define GBMW_FUSE        1   /* fuse_identical (dpsearch.py:71-86) */
 #define GBMW_FRONTIER    2   /* collect_frontier (dpsearch.py:194-199) */
 #define GBMW_STAGE_COST  4   /* also evaluate costs.stage_cost of the returned plan */
+#define GBMW_APPROX      8   /* approx_prev: collapsed-state DP (dpsearch.py:306-375) */
 
 /* ParallelStrategy (strategies.py:28-70): <= 3 ordered levels + ckpt flag. */
 typedef struct gbmw_strategy {

@@ -283,6 +283,64 @@ static int lex_lt(double t1, double f1, int j1, double t2, double f2, int j2) {
 }
 
 /*
+ * _run_dp_collapsed (dpsearch.py:306-375) and its sweep (dpsearch.py:194-208 with
+ * ranked_at = [(table[e], 0)] if finite): state (unit, bucket) only, one recorded
+ * strategy per cell; the transform cost is charged against that recorded strategy.
+ * _lex_pick (dpsearch.py:237-242) = first j minimising (cand, cand_f).
+ */
+static void approx_search(const DP *d, double safe_limit, double *frontier, int *picks, int *best_picks,
+                          int *have_best, double *best_t, int64_t *best_e) {
+    const int U = d->U, S = d->S;
+    const int64_t n_b = d->n_b, n_e = n_b + 1;
+    double *tab = (double *)malloc(sizeof(double) * n_e), *fwd = (double *)malloc(sizeof(double) * n_e);
+    double *nt = (double *)malloc(sizeof(double) * n_e), *nf = (double *)malloc(sizeof(double) * n_e);
+    int16_t *choice = (int16_t *)malloc(sizeof(int16_t) * (size_t)U * n_e);
+    for (int u = 0; u < U; ++u) {
+        const int16_t *prev = choice + (size_t)(u - 1) * n_e;
+        int16_t *cur = choice + (size_t)u * n_e;
+        const double *Ru = d->R + (size_t)u * S * S;
+        for (int64_t e = 0; e < n_e; ++e) {
+            double bt = OR_INF, bf = OR_INF;
+            int bj = -1;
+            for (int j = 0; j < S; ++j) {
+                const int64_t w = d->w[u * S + j];
+                if (w > n_b || e < w) continue;
+                double c, f;
+                if (u == 0) {
+                    c = d->time_c[j]; f = d->ef[j];
+                } else {
+                    const int64_t src = e - w;
+                    if (prev[src] < 0) continue;
+                    c = (tab[src] + Ru[prev[src] * S + j]) + d->time_c[u * S + j];
+                    f = fwd[src] + d->ef[u * S + j];
+                }
+                if (bj < 0 || c < bt || (c == bt && f < bf)) { bt = c; bf = f; bj = j; }
+            }
+            nt[e] = bt; nf[e] = bf; cur[e] = (int16_t)bj;
+        }
+        double *x = tab; tab = nt; nt = x;
+        x = fwd; fwd = nf; nf = x;
+    }
+    for (int64_t e = 1; e <= n_b; ++e) {
+        const double t = tab[e];
+        if (frontier) frontier[e - 1] = (t < OR_INF) ? t : OR_INF;
+        if (!(t < OR_INF)) continue;
+        if (*have_best && t > *best_t) continue;
+        int64_t ce = e;
+        for (int u = U - 1; u >= 0; --u) {
+            const int j = choice[(size_t)u * n_e + ce];
+            picks[u] = j;
+            ce -= d->w[u * S + j];
+        }
+        if (int_le_double(e * d->gran, safe_limit) || plan_e_all(d, picks) <= d->budget) {
+            *have_best = 1; *best_t = t; *best_e = e;
+            memcpy(best_picks, picks, sizeof(int) * U);
+        }
+    }
+    free(tab); free(fwd); free(nt); free(nf); free(choice);
+}
+
+/*
  * One dp_search (dpsearch.py:89-227) on already-validated arguments.
  * plan: n_layers ints (index into the caller's strategy list), -1 if infeasible.
  * frontier (optional): n_b doubles.  stage (optional): stage_cost of the plan.
@@ -347,6 +405,15 @@ int or_dp_search(const gbmw_layer *layers, int n_layers, const gbmw_strategy *st
         }
     }
     const double safe_limit = budget - b_up;
+    int *picks = (int *)malloc(sizeof(int) * U);
+    int *best_picks = (int *)malloc(sizeof(int) * U);
+    int have_best = 0;
+    double best_t = OR_INF;
+    int64_t best_e = 0;
+    if (flags & GBMW_APPROX) {
+        approx_search(&d, safe_limit, frontier, picks, best_picks, &have_best, &best_t, &best_e);
+        goto done;
+    }
     /* _run_dp_exact (dpsearch.py:251-282) */
     double *T = (double *)malloc(sizeof(double) * n_e * S), *F = (double *)malloc(sizeof(double) * n_e * S);
     double *T2 = (double *)malloc(sizeof(double) * n_e * S), *F2 = (double *)malloc(sizeof(double) * n_e * S);
@@ -386,12 +453,7 @@ int or_dp_search(const gbmw_layer *layers, int n_layers, const gbmw_strategy *st
         tmp = F; F = F2; F2 = tmp;
     }
     /* E_fwd sweep (dpsearch.py:194-208) */
-    int *picks = (int *)malloc(sizeof(int) * U);
-    int *best_picks = (int *)malloc(sizeof(int) * U);
     char *tried = (char *)malloc(S);
-    int have_best = 0;
-    double best_t = OR_INF;
-    int64_t best_e = 0;
     for (int64_t e = 1; e <= n_b; ++e) {
         const double *trow = T + e * S, *frow = F + e * S;
         memset(tried, 0, S);
@@ -416,6 +478,9 @@ int or_dp_search(const gbmw_layer *layers, int n_layers, const gbmw_strategy *st
             }
         }
     }
+    free(tried);
+    free(T); free(F); free(T2); free(F2); free(d.par);
+done:;
     int rc = 0;
     if (have_best) {
         double e_all = plan_e_all(&d, best_picks);
@@ -428,8 +493,7 @@ int or_dp_search(const gbmw_layer *layers, int n_layers, const gbmw_strategy *st
         if (stage_out) or_stage_cost(layers, ls, n_layers, micro, env, stage, n_micro, stage_out);
         free(ls);
     }
-    free(picks); free(best_picks); free(tried);
-    free(T); free(F); free(T2); free(F2); free(d.par);
+    free(picks); free(best_picks);
     free(d.time_c); free(d.ef); free(d.ob); free(d.w); free(d.R);
     free(d.unit_first); free(d.unit_count); free(cidx); free(d.cands);
     return rc;

@@ -24,7 +24,7 @@ EINVAL_GRAN, EINVAL_BUDGET, EEMPTY, EMICRO, EBUCKETS = -1, -2, -3, -4, -5
 ECUDA, ENOMEM, EINVAL, ERANGE, ENOTSUP, EINTERNAL, ESTAGE = -6, -7, -8, -9, -10, -11, -12
 MAX_BUCKETS = 1_000_000
 
-FUSE, FRONTIER, STAGE_COST = 1, 2, 4
+FUSE, FRONTIER, STAGE_COST, APPROX = 1, 2, 4, 8
 PARADIGM_CODE = {"dp": 0, "sdp": 1, "tp": 2}
 PARADIGM_NAME = ("dp", "sdp", "tp")
 

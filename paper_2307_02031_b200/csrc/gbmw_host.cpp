@@ -85,8 +85,9 @@ struct HostProb {
 struct Chunk {
     std::vector<int> probs;        // host problem indices, sorted by (K group, U descending)
     std::vector<int64_t> step_prefix;
-    int group_lo[kStepGroups + 1] = {0};
-    std::vector<int> n_active[kStepGroups];   // per group, per u: problems of the group with U > u
+    int group_lo[kNumGroups + 1] = {0};
+    std::vector<int> n_active[kNumGroups];    // per group, per u: problems of the group with U > u
+    int n_approx = 0;
     int Umax = 0, max_k = 1;
     int64_t n_cells = 0, n_r = 0, n_bcells = 0, n_par = 0, n_tiles = 0, n_units = 0, n_flagw = 0, n_gflat = 0;
     size_t small_off = 0;          // byte offset of this chunk's descriptor block in the arena
@@ -444,12 +445,13 @@ void prepare_problem(gbmw_batch &b, int pi, std::string *err) {
     const int64_t n_e = h.n_b + 1;
     h.n_cells = (int64_t)h.U * h.S;
     h.n_r = (int64_t)h.U * h.K * h.K;
-    h.n_bcells = (h.U > 1) ? (int64_t)h.K * n_e : 0;
-    h.n_par = (int64_t)(h.U - 1) * h.K * n_e;
+    const bool approx = (P.flags & GBMW_APPROX) != 0;
+    h.n_bcells = approx ? n_e : ((h.U > 1) ? (int64_t)h.K * n_e : 0);
+    h.n_par = approx ? (int64_t)h.U * n_e : (int64_t)(h.U - 1) * h.K * n_e;
     h.n_tiles = (h.n_b + kSweepThreads - 1) / kSweepThreads;
     h.n_step_tiles = (n_e + kStepRows - 1) / kStepRows;
-    h.n_flagw = (h.U > 1) ? (int64_t)h.K * flag_words(n_e) : 0;
-    h.n_gflat = (int64_t)(h.U > 1 ? h.U - 1 : 0) * gflat_words(n_e);
+    h.n_flagw = (!approx && h.U > 1) ? (int64_t)h.K * flag_words(n_e) : 0;
+    h.n_gflat = approx ? 0 : (int64_t)(h.U > 1 ? h.U - 1 : 0) * gflat_words(n_e);
     h.ws_bytes = (size_t)h.n_cells * (sizeof(Cell) + sizeof(CellMem) + 4) + (size_t)h.U * 12 + (size_t)h.n_r * 8 + 8 +
                  (size_t)h.n_bcells * 2 * sizeof(TFCell) + (size_t)h.n_par * 2 +
                  (size_t)(2 * h.n_tiles + 1) * sizeof(SweepPartial) + 8 + (size_t)h.n_flagw * 8 + (size_t)h.n_gflat * 4;
@@ -489,7 +491,7 @@ WsLayout ws_layout(const Chunk &c) {
     w.nuniq = o; o = align_up(o + c.n_units * 4);
     w.ulo = o; o = align_up(o + c.n_units * 4);
     w.uhi = o; o = align_up(o + c.n_units * 4);
-    w.ctr = o; o = align_up(o + (size_t)(c.Umax + 1) * kStepGroups * 8);
+    w.ctr = o; o = align_up(o + (size_t)(c.Umax + 1) * kNumGroups * 8);
     w.total = o;
     return w;
 }
@@ -556,7 +558,8 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
     std::vector<char> blob;
     for (Chunk &c : b->chunks) {
         std::stable_sort(c.probs.begin(), c.probs.end(), [&](int x, int y) {
-            const int gx = step_group(b->hp[x].K), gy = step_group(b->hp[y].K);
+            const int gx = problem_group(b->hp[x].K, b->problems[x].flags);
+            const int gy = problem_group(b->hp[y].K, b->problems[y].flags);
             if (gx != gy) return gx < gy;
             return b->hp[x].U > b->hp[y].U;
         });
@@ -604,15 +607,16 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
             c.n_flagw += h.n_flagw;
             c.n_gflat += h.n_gflat;
             c.Umax = std::max(c.Umax, h.U);
+            if (P.flags & GBMW_APPROX) c.n_approx++;
             c.max_k = std::max(c.max_k, h.K);
         }
         c.step_prefix = stepp;
         // groups are contiguous in sorted order; within a group U is descending, so
         // the problems still active at unit u are a prefix of the group
         const int np = (int)c.probs.size();
-        for (int g = 0, s = 0; g < kStepGroups; ++g) {
+        for (int g = 0, s = 0; g < kNumGroups; ++g) {
             c.group_lo[g] = s;
-            while (s < np && step_group(b->hp[c.probs[s]].K) == g) ++s;
+            while (s < np && problem_group(b->hp[c.probs[s]].K, b->problems[c.probs[s]].flags) == g) ++s;
             c.group_lo[g + 1] = s;
             c.n_active[g].assign(c.Umax + 1, 0);
             for (int x = c.group_lo[g]; x < s; ++x)
@@ -802,7 +806,7 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
         c.launches = 0;
         cudaEventRecord(c.ev[0], st);
         cudaMemsetAsync(a.bup, 0, c.probs.size() * 8, st);
-        cudaMemsetAsync(a.counters, 0, (size_t)(c.Umax + 1) * kStepGroups * 8, st);
+        cudaMemsetAsync(a.counters, 0, (size_t)(c.Umax + 1) * kNumGroups * 8, st);
         if ((rc = launch_cost_tables(a, c.n_cells, c.n_r, st))) return cuda_fail(ctx, rc, "K1 launch");
         c.launches += (c.n_cells > 0) + (c.n_r > 0) + (c.n_units > 0);
         cudaEventRecord(c.ev[1], st);
@@ -812,16 +816,25 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
                 const int lo = c.group_lo[g], na = c.n_active[g][u];
                 if (na == 0) continue;
                 const int64_t base = c.step_prefix[lo], n = c.step_prefix[lo + na] - base;
-                if ((rc = launch_dp_step(a, g, u, base, n, a.counters + (size_t)u * kStepGroups + g, st)))
+                if ((rc = launch_dp_step(a, g, u, base, n, a.counters + (size_t)u * kNumGroups + g, st)))
                     return cuda_fail(ctx, rc, "K2 launch");
                 c.launches += 1;
             }
         }
+        // approx_prev problems: collapsed-state layer steps, unit 0 included
+        for (int u = 0; u < c.Umax; ++u) {
+            const int lo = c.group_lo[kApproxGroup], na = c.n_active[kApproxGroup][u];
+            if (na == 0) continue;
+            const int64_t base = c.step_prefix[lo], n = c.step_prefix[lo + na] - base;
+            if ((rc = launch_approx_step(a, u, base, n, a.counters + (size_t)u * kNumGroups + kApproxGroup, st)))
+                return cuda_fail(ctx, rc, "K2c launch");
+            c.launches += 1;
+        }
         cudaEventRecord(c.ev[2], st);
-        if ((rc = launch_sweep(a, c.n_tiles, st))) return cuda_fail(ctx, rc, "K3 launch");
+        if ((rc = launch_sweep(a, c.n_tiles, c.n_approx > 0, st))) return cuda_fail(ctx, rc, "K3 launch");
         cudaEventRecord(c.ev[3], st);
         if ((rc = launch_finalize(a, st))) return cuda_fail(ctx, rc, "K4 launch");
-        c.launches += 4;
+        c.launches += 4 + (c.n_approx > 0);
         cudaEventRecord(c.ev[4], st);
     }
     cudaError_t ce = cudaStreamSynchronize(st);

@@ -41,6 +41,10 @@ constexpr int kSweepWK = 4096;       // (unit, strategy) pairs staged in shared 
 // pay the register footprint of the widest one: K <= 4, 5..8, 9..kMaxClasses.
 constexpr int kStepGroups = 3;
 inline int step_group(int K) { return K <= 4 ? 0 : (K <= 8 ? 1 : 2); }
+// problems with approx_prev (collapsed state, dpsearch.py:306-375) form their own group
+constexpr int kApproxGroup = kStepGroups;
+constexpr int kNumGroups = kStepGroups + 1;
+inline int problem_group(int K, int flags) { return (flags & GBMW_APPROX) ? kApproxGroup : step_group(K); }
 
 struct Cell {
     double c;       // time_c = t * count
@@ -160,7 +164,9 @@ struct ChunkArgs {
 int launch_cost_tables(const ChunkArgs &a, int64_t n_cells, int64_t n_r, void *stream);
 int launch_dp_step(const ChunkArgs &a, int group, int u, int64_t tile_base, int64_t n_tiles,
                    unsigned long long *counter, void *stream);
-int launch_sweep(const ChunkArgs &a, int64_t n_tiles, void *stream);
+int launch_sweep(const ChunkArgs &a, int64_t n_tiles, bool approx, void *stream);
+int launch_approx_step(const ChunkArgs &a, int u, int64_t tile_base, int64_t n_tiles, unsigned long long *counter,
+                       void *stream);
 int launch_finalize(const ChunkArgs &a, void *stream);
 
 }  // namespace gbmw

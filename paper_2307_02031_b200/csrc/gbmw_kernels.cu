@@ -145,7 +145,7 @@ __global__ void k_dedupe(ChunkArgs a) {
             acc += s_wmin[u];
         }
         // live class cells written by K2 (algorithmic-bytes accounting)
-        atomicAdd(a.live_cells, live * (unsigned long long)p.K);
+        if (!(p.flags & GBMW_APPROX)) atomicAdd(a.live_cells, live * (unsigned long long)p.K);
     }
 }
 
@@ -273,6 +273,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(ChunkArgs a) {
     __shared__ int32_t sJ[kMaxStrats];
     const int q = a.sweep_map[blockIdx.x];
     const DevProblem &p = a.probs[q];
+    if (p.flags & GBMW_APPROX) return;                   // k_approx_sweep
     const int last = p.U - 1;
     const int tile = blockIdx.x - (int)a.sweep_tiles[q];
     const int64_t e = 1 + (int64_t)tile * kSweepThreads + threadIdx.x;
@@ -388,6 +389,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
     __shared__ int red_j[kSweepThreads / 32];
     const int q = a.sweep_map[blockIdx.x];
     const DevProblem &p = a.probs[q];
+    if (p.flags & GBMW_APPROX) return;                   // k_approx_sweep
     const int tile = blockIdx.x - (int)a.sweep_tiles[q];
     const int64_t e0 = 1 + (int64_t)tile * kSweepThreads;
     const double safe_limit = p.budget - __longlong_as_double((long long)a.bup[q]);
@@ -471,6 +473,139 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
 }
 
 // ---------------------------------------------------------------- K4: finalize
+// ---------------------------------------------------------------- approx_prev (collapsed DP)
+// dpsearch.py:306-375: state (unit, bucket) only.  table_u[e] = lexmin_j (cand, cand_f, j)
+// with cand = (table_{u-1}[e-w] + R(choice_{u-1}[e-w] -> j)) + time_c, cand_f =
+// fwd_{u-1}[e-w] + ef_true (_lex_pick: min time, then min tiebreak, then first j).
+// Per problem: table/fwd ping-pong = one TF column, choices = U x n_e int16 in `par`.
+constexpr int kApproxRowsPerThread = kStepRows / kStepThreads;
+
+template <bool FIRST>
+__global__ void __launch_bounds__(kStepThreads) k_approx_step(ChunkArgs a, int u, int64_t tile_base, int64_t n_tiles,
+                                                               unsigned long long *counter) {
+    __shared__ int32_t sW[kMaxStrats];
+    __shared__ int32_t sK[kMaxStrats];
+    __shared__ double sC[kMaxStrats];
+    __shared__ double sE[kMaxStrats];
+    __shared__ double sR[kMaxClasses * kMaxClasses];
+    __shared__ int64_t s_next;
+    int q_prev = -1;
+    while (true) {
+        __syncthreads();
+        if (threadIdx.x == 0) s_next = (int64_t)atomicAdd(counter, 1ull);
+        __syncthreads();
+        const int64_t t = s_next;
+        if (t >= n_tiles) break;
+        const int64_t tile = tile_base + t;
+        const int q = a.step_map[tile];
+        const DevProblem &p = a.probs[q];
+        if (q != q_prev) {
+            __syncthreads();
+            const Cell *uc = a.cells + p.cell_off + (int64_t)u * p.S;
+            for (int j = threadIdx.x; j < p.S; j += blockDim.x) {
+                const Cell c = uc[j];
+                sW[j] = c.w; sK[j] = c.k; sC[j] = c.c; sE[j] = c.ef;
+            }
+            const double *r_u = a.rcls + p.r_off + (int64_t)u * p.K * p.K;
+            for (int x = threadIdx.x; x < p.K * p.K; x += blockDim.x) sR[x] = r_u[x];
+            __syncthreads();
+            q_prev = q;
+        }
+        const int S = p.S, K = p.K;
+        const int64_t n_e = p.n_b + 1;
+        const TFCell *tin = a.TF[(u - 1) & 1] + p.b_off;
+        TFCell *tout = a.TF[u & 1] + p.b_off;
+        const int16_t *cin = reinterpret_cast<const int16_t *>(a.par + p.par_off) + (int64_t)(u - 1) * n_e;
+        int16_t *cout = reinterpret_cast<int16_t *>(a.par + p.par_off) + (int64_t)u * n_e;
+        const int64_t first_row = (tile - a.step_tiles[q]) * kStepRows;
+        for (int rr = 0; rr < kApproxRowsPerThread; ++rr) {
+            const int64_t e = first_row + rr * kStepThreads + threadIdx.x;
+            if (e >= n_e) break;
+            double bt = GBMW_INF, bf = GBMW_INF;
+            int bj = -1;
+            for (int j = 0; j < S; ++j) {
+                const int w = sW[j];
+                if (w > p.n_b || e < w) continue;
+                double tc, fc;
+                if (FIRST) {
+                    tc = sC[j]; fc = sE[j];
+                } else {
+                    const int64_t src = e - w;
+                    const int pj = cin[src];
+                    if (pj < 0) continue;                 // +inf source (no recorded choice)
+                    const TFCell s = tin[src];
+                    tc = (s.t + sR[sK[pj] * K + sK[j]]) + sC[j];
+                    fc = s.f + sE[j];
+                }
+                if (bj < 0 || tc < bt || (tc == bt && fc < bf)) { bt = tc; bf = fc; bj = j; }
+            }
+            TFCell o;
+            o.t = bt; o.f = bf;
+            tout[e] = o;
+            cout[e] = (int16_t)bj;
+        }
+    }
+}
+
+// choices of the collapsed DP, walked back from bucket e (dpsearch.py:366-373)
+__device__ __forceinline__ void approx_reconstruct(const ChunkArgs &a, const DevProblem &p, int64_t e,
+                                                   uint16_t *path) {
+    const int64_t n_e = p.n_b + 1;
+    const int16_t *ch = reinterpret_cast<const int16_t *>(a.par + p.par_off);
+    const Cell *cells = a.cells + p.cell_off;
+    for (int u = p.U - 1; u >= 0; --u) {
+        const int j = ch[(int64_t)u * n_e + e];
+        path[u] = (uint16_t)j;
+        e -= cells[(int64_t)u * p.S + j].w;
+    }
+}
+
+// Sweep of the collapsed DP: one recorded candidate per bucket (dpsearch.py:360-364);
+// safe buckets accept it, unsafe ones check E_all of the reconstructed plan.
+__global__ void __launch_bounds__(kSweepThreads) k_approx_sweep(ChunkArgs a) {
+    __shared__ double red_t[kSweepThreads / 32];
+    __shared__ long long red_e[kSweepThreads / 32];
+    __shared__ int red_j[kSweepThreads / 32];
+    const int q = a.sweep_map[blockIdx.x];
+    const DevProblem &p = a.probs[q];
+    if (!(p.flags & GBMW_APPROX)) return;
+    const int tile = blockIdx.x - (int)a.sweep_tiles[q];
+    const int64_t e = 1 + (int64_t)tile * kSweepThreads + threadIdx.x;
+    const double safe_limit = p.budget - __longlong_as_double((long long)a.bup[q]);
+    const TFCell *tab = a.TF[(p.U - 1) & 1] + p.b_off;
+    double mt = GBMW_INF;
+    int64_t me = -1;
+    if (e <= p.n_b) {
+        const double t = tab[e].t;
+        if (p.frontier_off >= 0) a.frontier[p.frontier_off + e - 1] = t;
+        if (t < GBMW_INF) {
+            bool fits = int_le_double(e * p.gran, safe_limit);
+            if (!fits) {
+                uint16_t path[kMaxUnits];
+                approx_reconstruct(a, p, e, path);
+                fits = plan_e_all(a, p, path) <= p.budget;
+            }
+            if (fits) { mt = t; me = e; }
+        }
+    }
+    const SweepPartial blk = block_best(mt, me, 0, red_t, red_e, red_j);
+    if (threadIdx.x == 0) {
+        a.partials[p.tile_off + tile] = blk;
+        SweepPartial none;
+        none.t = GBMW_INF; none.e = -1; none.j = 0; none.pad_ = 0;
+        a.upartials[p.tile_off + tile] = none;
+    }
+}
+
+int launch_approx_step(const ChunkArgs &a, int u, int64_t tile_base, int64_t n_tiles, unsigned long long *counter,
+                       void *stream) {
+    if (n_tiles <= 0) return 0;
+    const unsigned grid = (unsigned)(n_tiles < 148 * 8 ? n_tiles : 148 * 8);
+    if (u == 0) k_approx_step<true><<<grid, kStepThreads, 0, (cudaStream_t)stream>>>(a, u, tile_base, n_tiles, counter);
+    else k_approx_step<false><<<grid, kStepThreads, 0, (cudaStream_t)stream>>>(a, u, tile_base, n_tiles, counter);
+    return (int)cudaGetLastError();
+}
+
 __global__ void k_finalize(ChunkArgs a) {
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= a.n_probs) return;
@@ -495,7 +630,8 @@ __global__ void k_finalize(ChunkArgs a) {
         return;
     }
     uint16_t path[kMaxUnits];
-    backtrack(a, p, be, bj, path);
+    if (p.flags & GBMW_APPROX) approx_reconstruct(a, p, be, path);
+    else backtrack(a, p, be, bj, path);
     const double e_all = plan_e_all(a, p, path);
     res.time_s = bt;
     res.e_fwd_used = (double)(be * p.gran);
@@ -554,9 +690,10 @@ int launch_cost_tables(const ChunkArgs &a, int64_t n_cells, int64_t n_r, void *s
     return (int)cudaGetLastError();
 }
 
-int launch_sweep(const ChunkArgs &a, int64_t n_tiles, void *stream) {
+int launch_sweep(const ChunkArgs &a, int64_t n_tiles, bool approx, void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
     if (n_tiles > 0) k_sweep<<<(unsigned)n_tiles, kSweepThreads, 0, st>>>(a);
+    if (n_tiles > 0 && approx) k_approx_sweep<<<(unsigned)n_tiles, kSweepThreads, 0, st>>>(a);
     if (a.n_probs > 0) k_sweep_safe_best<<<blocks_for(a.n_probs, 4), 128, 0, st>>>(a);
     if (n_tiles > 0) k_sweep_unsafe<<<(unsigned)n_tiles, kSweepThreads, 0, st>>>(a);
     return (int)cudaGetLastError();

@@ -70,9 +70,6 @@ def _check(p: StageProblem):
                          f"increase the memory granularity")
     if not _usable(strats, p.micro_batch) or n_buckets == 0:
         return n_buckets, strats, DpResult(time_s=INF, strategies=None, e_fwd_used=0.0, feasible=False)
-    if p.approx_prev:
-        raise NotImplementedError("approx_prev (collapsed-state DP, dpsearch.py:306-375) is not "
-                                  "implemented on the device path yet")
     return n_buckets, strats, None
 
 
@@ -182,7 +179,8 @@ def dp_search_batch(problems: Sequence[StageProblem], want_stage_cost: bool = Fa
         lb = m.layer_range(p.stage_layers, p.ctx.profile)
         sb = m.strat_range(p.strategies, strats)
         flags = (_native.FUSE if p.fuse_identical else 0) | (_native.FRONTIER if p.collect_frontier else 0) | \
-                (_native.STAGE_COST if want_stage_cost else 0)
+                (_native.STAGE_COST if want_stage_cost else 0) | \
+                (_native.APPROX if p.approx_prev else 0)
         rows.append((lb, len(p.stage_layers), sb, len(strats), m.env(p.ctx), int(p.stage_index),
                      int(p.n_micro), flags, int(p.micro_batch), int(p.granularity_bytes),
                      float(p.budget_bytes), n_buckets))

@@ -134,14 +134,12 @@ def _search_slices(cells, ctx, opts):
     table over a single copy of the model's layers, no per-stage Python objects."""
     from . import _native
     from .dpsearch import MAX_BUCKETS, _Marshal, run_native_batch
-    if opts.approx_prev:
-        raise NotImplementedError("approx_prev (collapsed-state DP, dpsearch.py:306-375) is not "
-                                  "implemented on the device path yet")
     gran = opts.granularity_bytes
     mar = _Marshal()
     base = mar.layer_range(list(ctx.model.layers), ctx.profile)
     env = mar.env(ctx)
-    flags = _native.STAGE_COST | (_native.FUSE if opts.fuse_identical else 0)
+    flags = _native.STAGE_COST | (_native.FUSE if opts.fuse_identical else 0) | \
+        (_native.APPROX if opts.approx_prev else 0)
     rows, metas = [], []
     for budget, ranges, n_devices, batch, pp in cells:
         m = init_microbatch_num(batch, pp, opts.microbatch_cap_factor, opts.min_micro_size)

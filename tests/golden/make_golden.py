@@ -66,11 +66,12 @@ def env_doc(ctx):
             "overrides": {str(k): hx(v) for k, v in p.layer_overrides.items()}}
 
 
-def dp_case(name, layers, budget, sset, micro, gran, ctx, stage=1, n_micro=1, fuse=False, frontier=False):
+def dp_case(name, layers, budget, sset, micro, gran, ctx, stage=1, n_micro=1, fuse=False, frontier=False,
+            approx=False):
     strats = list(sset)
     t0 = time.time()
     res = RD.dp_search(list(layers), budget, sset, micro, gran, ctx, stage_index=stage, n_micro=n_micro,
-                       fuse_identical=fuse, collect_frontier=frontier)
+                       fuse_identical=fuse, approx_prev=approx, collect_frontier=frontier)
     dt = time.time() - t0
     out = {"feasible": res.feasible, "time": hx(res.time_s), "e_fwd": hx(res.e_fwd_used)}
     if res.feasible:
@@ -85,7 +86,8 @@ def dp_case(name, layers, budget, sset, micro, gran, ctx, stage=1, n_micro=1, fu
     return {"name": name, "layers": [layer_doc(l) for l in layers], "budget": budget,
             "budget_is_int": isinstance(budget, int), "strategies": [s.to_string() for s in strats],
             "micro": micro, "gran": gran, "stage": stage, "n_micro": n_micro, "fuse": fuse,
-            "collect_frontier": frontier, "env": env_doc(ctx), "out": out, "ref_seconds": round(dt, 4)}
+            "collect_frontier": frontier, "approx": approx, "env": env_doc(ctx), "out": out,
+            "ref_seconds": round(dt, 4)}
 
 
 def gen_enumeration():
@@ -217,8 +219,51 @@ def gen_configs():
     return cases
 
 
+def gen_approx():
+    """approx_prev=True (collapsed-state DP, dpsearch.py:306-375) on the fuzz family, the
+    small_context family and a few benchmark-model stages."""
+    cases = []
+    for seed, count, gran, fuse in ((31, 60, 1, False), (32, 40, 8, True), (33, 40, 1, False)):
+        rng = random.Random(seed)
+        for k in range(count):
+            model, cluster, ctx, sset, micro = RH.fuzz_dp_instance(rng)
+            cases.append(dp_case(f"approx{seed}_{k}", model.layers, cluster.mem_budget_bytes, sset, micro, gran,
+                                 ctx, fuse=fuse, frontier=(k % 2 == 0), approx=True))
+    for nl, budget, gran in ((3, 4096, 1), (4, 16384, 1), (3, 1024, 1), (4, 1 << 19, 1)):
+        model = RH.uniform_model(nl, param=64, bnd=16, intb=96, fwd=0.01)
+        ctx = RH.make_ctx(model, RH.make_cluster(n=4, budget=budget, intra=1e6))
+        sset = R.prune_dp_sdp(R.enumerate_strategies(4, 1))
+        for fuse in (False, True):
+            cases.append(dp_case(f"approx_small{nl}_{budget}_{fuse}", model.layers, budget, sset, 8, gran, ctx,
+                                 fuse=fuse, frontier=True, approx=True))
+    rng = random.Random(77)
+    for name, budget, gran in (("bert", 16 * GiB, 64 * MiB), ("t5", 8 * GiB, 16 * MiB), ("vit", 16 * GiB, 64 * MiB),
+                               ("swin", 16 * GiB, 64 * MiB), ("gpt", 80 * GiB, 256 * MiB)):
+        ctx0 = W.config(name, budget)
+        ctx = R.EvalContext(R.ModelSpec(ctx0.model.name, tuple(
+            R.LayerSpec(l.id, l.kind, l.param_bytes, l.bnd_bytes_per_sample, l.int_bytes_per_sample,
+                        l.fwd_time_per_sample, l.tp_act_replication_fraction) for l in ctx0.model.layers),
+            ctx0.model.ms_bytes_per_param_byte), R.ClusterSpec(**ctx0.cluster.to_document()), R.CostProfile())
+        N, L = ctx.cluster.n_devices, ctx.model.num_layers
+        for P in [p for p in candidate_pp_degrees(N) if p <= L][:4]:
+            B = rng.choice([8, 32, 128])
+            m = W.microbatch_num(B, P)
+            parts = W.even_partition(L, P)
+            si = rng.randrange(P)
+            a = sum(parts[:si])
+            cases.append(dp_case(f"approx_{name}_P{P}_B{B}_s{si + 1}", ctx.model.layers[a:a + parts[si]], budget,
+                                 R.prune_dp_sdp(R.enumerate_strategies(N, P)), B // m, gran, ctx, stage=si + 1,
+                                 n_micro=m, fuse=rng.random() < 0.5, frontier=True, approx=True))
+    return cases
+
+
 def main():
     t0 = time.time()
+    if sys.argv[1:] == ["approx"]:
+        cases = gen_approx()
+        (OUT / "dp_approx.json").write_text(json.dumps(cases, separators=(",", ":")))
+        print(f"approx: {len(cases)} cases, {time.time() - t0:.1f}s")
+        return
     (OUT / "enumeration.json").write_text(json.dumps(gen_enumeration(), separators=(",", ":")))
     (OUT / "cost_cells.json").write_text(json.dumps(gen_cells(), separators=(",", ":")))
     print(f"enumeration + cells: {time.time() - t0:.1f}s")

@@ -52,7 +52,7 @@ def flat_batch(cases, stage_cost=True):
         S.append(_native.strategies_array(list(sset)))
         E.append(_native.env_record(ctx))
         flags = (_native.FUSE if c["fuse"] else 0) | (_native.FRONTIER if c["collect_frontier"] else 0) | \
-                (_native.STAGE_COST if stage_cost else 0)
+                (_native.STAGE_COST if stage_cost else 0) | (_native.APPROX if c.get("approx") else 0)
         nb = int(budget // c["gran"])
         P.append((lo, len(layers), so, len(sset), i, c["stage"], c["n_micro"], flags, c["micro"], c["gran"],
                   float(budget), nb))

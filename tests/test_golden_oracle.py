@@ -41,7 +41,7 @@ def test_cost_cells_match_reference():
         assert [x.hex() for x in got] == c["out"][:5], c
 
 
-@pytest.mark.parametrize("fixture", ["dp_fuzz.json", "dp_configs.json"])
+@pytest.mark.parametrize("fixture", ["dp_fuzz.json", "dp_configs.json", "dp_approx.json"])
 def test_dp_search_matches_reference(fixture):
     cases = load(fixture)
     layers, strats, envs, probs = flat_batch(cases)

@@ -38,7 +38,7 @@ def _check_against(cases, context=None):
         plan_off += nl
 
 
-@pytest.mark.parametrize("fixture", ["dp_fuzz.json", "dp_configs.json"])
+@pytest.mark.parametrize("fixture", ["dp_fuzz.json", "dp_configs.json", "dp_approx.json"])
 def test_golden_bit_exact(gpu, fixture):
     _check_against(load(fixture))
 
@@ -52,10 +52,11 @@ def test_golden_bit_exact_when_chunked(gpu):
 
 
 def test_api_dp_search_golden(gpu):
-    for c in load("dp_fuzz.json")[:80] + load("dp_configs.json")[:40]:
+    for c in load("dp_fuzz.json")[:80] + load("dp_configs.json")[:40] + load("dp_approx.json")[::3]:
         layers, budget, sset, ctx = case_objects(c)
         res = dp_search(layers, budget, sset, c["micro"], c["gran"], ctx, stage_index=c["stage"],
-                        n_micro=c["n_micro"], fuse_identical=c["fuse"], collect_frontier=c["collect_frontier"])
+                        n_micro=c["n_micro"], fuse_identical=c["fuse"], approx_prev=c.get("approx", False),
+                        collect_frontier=c["collect_frontier"])
         out = c["out"]
         assert res.feasible == out["feasible"]
         assert res.time_s.hex() == out["time"]
@@ -69,7 +70,7 @@ def test_api_dp_search_golden(gpu):
             assert [e for e, _ in res.frontier] == [k * c["gran"] for k in range(1, len(res.frontier) + 1)]
 
 
-def _random_problems(rng, n, fine=False):
+def _random_problems(rng, n, fine=False, approx=0.0):
     """Seeded realistic stage searches across the benchmark models."""
     probs = []
     for _ in range(n):
@@ -88,7 +89,7 @@ def _random_problems(rng, n, fine=False):
         gran = rng.choice((4 * MiB, 8 * MiB)) if fine else rng.choice((32 * MiB, 64 * MiB, 128 * MiB))
         probs.append(StageProblem(list(ctx.model.layers[a:a + parts[si]]), budget, enumerate_pruned(N, P), B // m,
                                   gran, ctx, si + 1, m, fuse_identical=rng.random() < 0.25,
-                                  collect_frontier=rng.random() < 0.3))
+                                  approx_prev=rng.random() < approx, collect_frontier=rng.random() < 0.3))
     return probs
 
 
@@ -99,7 +100,7 @@ def _flat(problems):
         strats = list(p.strategies)
         nb = int(p.budget_bytes // p.granularity_bytes)
         flags = (_native.FUSE if p.fuse_identical else 0) | (_native.FRONTIER if p.collect_frontier else 0) | \
-                _native.STAGE_COST
+                _native.STAGE_COST | (_native.APPROX if p.approx_prev else 0)
         rows.append((m.layer_range(p.stage_layers, p.ctx.profile), len(p.stage_layers),
                      m.strat_range(p.strategies, strats), len(strats), m.env(p.ctx), p.stage_index, p.n_micro,
                      flags, p.micro_batch, p.granularity_bytes, float(p.budget_bytes), nb))
@@ -133,6 +134,42 @@ def _compare_with_oracle(problems, context=None):
 def test_random_configs_vs_oracle(gpu):
     res = _compare_with_oracle(_random_problems(random.Random(1234), 300))
     assert res["feasible"].sum() > 50
+
+
+def test_random_configs_approx_vs_oracle(gpu):
+    """approx_prev (collapsed-state DP) mixed with exact searches in the same chunks."""
+    res = _compare_with_oracle(_random_problems(random.Random(4321), 200, approx=0.5))
+    assert res["feasible"].sum() > 30
+
+
+def test_random_fine_granularity_approx_vs_oracle(gpu):
+    res = _compare_with_oracle(_random_problems(random.Random(98), 16, fine=True, approx=1.0))
+    assert res["feasible"].sum() > 3
+
+
+def test_collapsed_prev_state_never_beats_exact(gpu):
+    """Reference test_dpsearch.py:221-237 on the device path: the collapsed DP never beats
+    the exact one, and its reported time is the true cost of the plan it returns."""
+    from paper_2307_02031_b200.costs import layer_time
+    n_feasible = 0
+    for c in load("dp_approx.json"):
+        layers, budget, sset, ctx = case_objects(c)
+        kw = dict(stage_index=c["stage"], n_micro=c["n_micro"], fuse_identical=c["fuse"])
+        micro = c["micro"]
+        exact = dp_search(layers, budget, sset, micro, c["gran"], ctx, **kw)
+        approx = dp_search(layers, budget, sset, micro, c["gran"], ctx, approx_prev=True, **kw)
+        assert approx.time_s.hex() == c["out"]["time"]
+        if approx.feasible:
+            n_feasible += 1
+            assert exact.feasible
+            assert approx.time_s >= exact.time_s - 1e-12
+            true_cost, prev = 0.0, None
+            for layer, s in zip(layers, approx.strategies):
+                true_cost += layer_time(layer, s, micro, ctx.cluster, ctx.profile)
+                true_cost += transform_cost(layer, prev, s, micro, ctx.cluster)
+                prev = s
+            assert approx.time_s == pytest.approx(true_cost, rel=1e-12)
+    assert n_feasible > 100
 
 
 def test_random_fine_granularity_vs_oracle(gpu):
