@@ -92,8 +92,9 @@ struct Chunk {
     int64_t n_cells = 0, n_r = 0, n_bcells = 0, n_par = 0, n_tiles = 0, n_units = 0, n_flagw = 0, n_gflat = 0;
     size_t small_off = 0;          // byte offset of this chunk's descriptor block in the arena
     // offsets inside the descriptor block
-    size_t o_probs, o_cellp, o_rp, o_stepp, o_sweepp, o_cand, o_ccls, o_clsd, o_clst, o_uf, o_uc;
-    size_t o_stepmap, o_sweepmap;
+    size_t o_probs, o_cellp, o_rp, o_stepp, o_cand, o_ccls, o_clsd, o_clst, o_uf, o_uc;
+    size_t o_stepmap, o_aux;
+    int64_t n_aux = 0;
     size_t small_bytes = 0;
     size_t ws_bytes = 0;
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -454,7 +455,8 @@ void prepare_problem(gbmw_batch &b, int pi, std::string *err) {
     h.n_gflat = approx ? 0 : (int64_t)(h.U > 1 ? h.U - 1 : 0) * gflat_words(n_e);
     h.ws_bytes = (size_t)h.n_cells * (sizeof(Cell) + sizeof(CellMem) + 4) + (size_t)h.U * 12 + (size_t)h.n_r * 8 + 8 +
                  (size_t)h.n_bcells * 2 * sizeof(TFCell) + (size_t)h.n_par * 2 +
-                 (size_t)(2 * h.n_tiles + 1) * sizeof(SweepPartial) + 8 + (size_t)h.n_flagw * 8 + (size_t)h.n_gflat * 4;
+                 (size_t)h.n_tiles * sizeof(SweepPartial) + sizeof(SweepPartial) + 28 + (size_t)h.n_flagw * 8 +
+                 (size_t)h.n_gflat * 4;
     h.gpu = true;
 }
 
@@ -468,7 +470,8 @@ size_t put(std::vector<char> &blob, const T *src, size_t n) {
 
 // chunk workspace layout (byte offsets from ws base)
 struct WsLayout {
-    size_t cells, cmem, rcls, bup, tf0, tf1, chg0, chg1, gflat, par, parts, uparts, bestp, bound, uniq, nuniq, ulo, uhi, ctr, total;
+    size_t cells, cmem, rcls, bup, tf0, tf1, chg0, chg1, gflat, par, parts, bestp, bound, ufirst, uprefix, uctr, uniq, nuniq,
+        ulo, uhi, ctr, total;
 };
 WsLayout ws_layout(const Chunk &c) {
     WsLayout w;
@@ -484,9 +487,11 @@ WsLayout ws_layout(const Chunk &c) {
     w.gflat = o; o = align_up(o + c.n_gflat * 4);
     w.par = o; o = align_up(o + c.n_par * 2);
     w.parts = o; o = align_up(o + c.n_tiles * sizeof(SweepPartial));
-    w.uparts = o; o = align_up(o + c.n_tiles * sizeof(SweepPartial));
     w.bestp = o; o = align_up(o + c.probs.size() * sizeof(SweepPartial));
     w.bound = o; o = align_up(o + c.probs.size() * 8);
+    w.ufirst = o; o = align_up(o + c.probs.size() * 4);
+    w.uprefix = o; o = align_up(o + (c.probs.size() + 1) * 8);
+    w.uctr = o; o = align_up(o + 8);
     w.uniq = o; o = align_up(o + c.n_cells * 4);
     w.nuniq = o; o = align_up(o + c.n_units * 4);
     w.ulo = o; o = align_up(o + c.n_units * 4);
@@ -564,7 +569,8 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
             return b->hp[x].U > b->hp[y].U;
         });
         std::vector<DevProblem> dps;
-        std::vector<int64_t> cellp{0}, rp{0}, stepp{0}, sweepp{0};
+        std::vector<int64_t> cellp{0}, rp{0}, stepp{0};
+        std::vector<int2> aux;
         std::vector<int32_t> cand, ccls, clsd, clst, uf, uc;
         std::map<const StratInfo *, std::pair<int32_t, int32_t>> soff;
         std::map<const UnitInfo *, int32_t> uoff;
@@ -602,7 +608,6 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
             c.n_cells += h.n_cells; c.n_r += h.n_r; c.n_bcells += h.n_bcells; c.n_par += h.n_par; c.n_tiles += h.n_tiles;
             cellp.push_back(c.n_cells); rp.push_back(c.n_r);
             stepp.push_back(stepp.back() + h.n_step_tiles);
-            sweepp.push_back(c.n_tiles);
             c.n_units += h.U;
             c.n_flagw += h.n_flagw;
             c.n_gflat += h.n_gflat;
@@ -622,11 +627,14 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
             for (int x = c.group_lo[g]; x < s; ++x)
                 for (int u = 0; u < b->hp[c.probs[x]].U && u <= c.Umax; ++u) c.n_active[g][u]++;
         }
-        std::vector<int32_t> stepmap(stepp.back()), sweepmap(sweepp.back());
+        std::vector<int32_t> stepmap(stepp.back());
         for (int x = 0; x < np; ++x) {
             for (int64_t t = stepp[x]; t < stepp[x + 1]; ++t) stepmap[t] = x;
-            for (int64_t t = sweepp[x]; t < sweepp[x + 1]; ++t) sweepmap[t] = x;
+            // every row of frontier / collapsed-DP problems is swept (K3r)
+            if (b->problems[c.probs[x]].flags & (GBMW_FRONTIER | GBMW_APPROX))
+                for (int t = 0; t < dps[x].n_sweep_tiles; ++t) aux.push_back(make_int2(x, t));
         }
+        c.n_aux = (int64_t)aux.size();
         const size_t base = align_up(blob.size(), 256);
         blob.resize(base);
         c.small_off = base;
@@ -634,7 +642,6 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
         c.o_cellp = put(blob, cellp.data(), cellp.size()) - base;
         c.o_rp = put(blob, rp.data(), rp.size()) - base;
         c.o_stepp = put(blob, stepp.data(), stepp.size()) - base;
-        c.o_sweepp = put(blob, sweepp.data(), sweepp.size()) - base;
         c.o_cand = put(blob, cand.data(), cand.size()) - base;
         c.o_ccls = put(blob, ccls.data(), ccls.size()) - base;
         c.o_clsd = put(blob, clsd.data(), clsd.size()) - base;
@@ -642,7 +649,7 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
         c.o_uf = put(blob, uf.data(), uf.size()) - base;
         c.o_uc = put(blob, uc.data(), uc.size()) - base;
         c.o_stepmap = put(blob, stepmap.data(), stepmap.size()) - base;
-        c.o_sweepmap = put(blob, sweepmap.data(), sweepmap.size()) - base;
+        c.o_aux = put(blob, aux.data(), aux.size()) - base;
         c.small_bytes = blob.size() - base;
         c.ws_bytes = ws_layout(c).total;
         b->max_ws = std::max(b->max_ws, c.ws_bytes);
@@ -748,7 +755,6 @@ ChunkArgs chunk_args(gbmw_batch *b, const Chunk &c, char *ws, size_t chunk_index
     a.cell_prefix = (const int64_t *)(sm + c.o_cellp);
     a.r_prefix = (const int64_t *)(sm + c.o_rp);
     a.step_tiles = (const int64_t *)(sm + c.o_stepp);
-    a.sweep_tiles = (const int64_t *)(sm + c.o_sweepp);
     a.cand_strat = (const int32_t *)(sm + c.o_cand);
     a.cand_cls = (const int32_t *)(sm + c.o_ccls);
     a.class_d = (const int32_t *)(sm + c.o_clsd);
@@ -756,7 +762,8 @@ ChunkArgs chunk_args(gbmw_batch *b, const Chunk &c, char *ws, size_t chunk_index
     a.unit_first = (const int32_t *)(sm + c.o_uf);
     a.unit_count = (const int32_t *)(sm + c.o_uc);
     a.step_map = (const int32_t *)(sm + c.o_stepmap);
-    a.sweep_map = (const int32_t *)(sm + c.o_sweepmap);
+    a.aux_map = (const int2 *)(sm + c.o_aux);
+    a.n_aux = c.n_aux;
     const WsLayout w = ws_layout(c);
     a.cells = (Cell *)(ws + w.cells);
     a.cmem = (CellMem *)(ws + w.cmem);
@@ -770,8 +777,10 @@ ChunkArgs chunk_args(gbmw_batch *b, const Chunk &c, char *ws, size_t chunk_index
     a.par = (uint16_t *)(ws + w.par);
     a.partials = (SweepPartial *)(ws + w.parts);
     a.best = (SweepPartial *)(ws + w.bestp);
-    a.upartials = (SweepPartial *)(ws + w.uparts);
     a.bound = (unsigned long long *)(ws + w.bound);
+    a.ufirst = (int32_t *)(ws + w.ufirst);
+    a.uprefix = (int64_t *)(ws + w.uprefix);
+    a.ucounter = (unsigned long long *)(ws + w.uctr);
     a.uniq = (int32_t *)(ws + w.uniq);
     a.nuniq = (int32_t *)(ws + w.nuniq);
     a.unit_lo = (int32_t *)(ws + w.ulo);
@@ -831,10 +840,10 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
             c.launches += 1;
         }
         cudaEventRecord(c.ev[2], st);
-        if ((rc = launch_sweep(a, c.n_tiles, c.n_approx > 0, st))) return cuda_fail(ctx, rc, "K3 launch");
+        if ((rc = launch_sweep(a, st))) return cuda_fail(ctx, rc, "K3 launch");
         cudaEventRecord(c.ev[3], st);
         if ((rc = launch_finalize(a, st))) return cuda_fail(ctx, rc, "K4 launch");
-        c.launches += 4 + (c.n_approx > 0);
+        c.launches += 4 + (c.n_aux > 0);
         cudaEventRecord(c.ev[4], st);
     }
     cudaError_t ce = cudaStreamSynchronize(st);

@@ -13,6 +13,7 @@
 // restatement of dpsearch.py:261-280: R depends on (i, j) only through their classes).
 #pragma once
 #include <stdint.h>
+#include <vector_types.h>
 #include "../../include/gbmw.h"
 
 namespace gbmw {
@@ -128,9 +129,9 @@ struct ChunkArgs {
     const int64_t *cell_prefix;   // n_probs + 1
     const int64_t *r_prefix;      // n_probs + 1
     const int64_t *step_tiles;    // n_probs + 1, tiles of ceil(n_e / kStepRows)
-    const int64_t *sweep_tiles;   // n_probs + 1
     const int32_t *step_map;      // K2 tile -> problem (sorted position)
-    const int32_t *sweep_map;     // K3 tile -> problem
+    const int2 *aux_map;          // K3r tiles: (problem, tile) of frontier / collapsed-DP problems
+    int64_t n_aux;
     const int32_t *cand_strat;    // global strategy index
     const int32_t *cand_cls;
     const int32_t *class_d, *class_t;
@@ -145,10 +146,12 @@ struct ChunkArgs {
     uint32_t *gflat;              // per unit u >= 1: bit g = 32-row group g of B_u is flat (stored once)
     unsigned long long *computed_cells;   // class cells K2 evaluated (rows x K), per chunk
     uint16_t *par;
-    SweepPartial *partials;       // K3 per-tile best safe bucket
-    SweepPartial *best;           // per problem: best safe bucket
-    SweepPartial *upartials;      // K3b per-tile best unsafe bucket
+    SweepPartial *partials;       // per sweep tile: best bucket of an unsafe (K3b) or collapsed-DP (K3r) tile
+    SweepPartial *best;           // per problem: best safe bucket (K3a)
     unsigned long long *bound;    // per problem: running pruning bound (bits of t) of the unsafe walks
+    int32_t *ufirst;              // per problem: first sweep tile holding unsafe rows
+    int64_t *uprefix;             // n_probs + 1: exclusive prefix of unsafe tiles (K3b work list)
+    unsigned long long *ucounter; // K3b work counter
     int32_t *uniq;                // per (unit, slot): strategy indices with distinct (w, k, c, ef), ascending
     int32_t *nuniq;               // per unit: number of distinct strategies
     int32_t *unit_lo, *unit_hi;   // per unit u: live rows [L_u, H_u] of B_u (see k_dedupe)
@@ -164,7 +167,7 @@ struct ChunkArgs {
 int launch_cost_tables(const ChunkArgs &a, int64_t n_cells, int64_t n_r, void *stream);
 int launch_dp_step(const ChunkArgs &a, int group, int u, int64_t tile_base, int64_t n_tiles,
                    unsigned long long *counter, void *stream);
-int launch_sweep(const ChunkArgs &a, int64_t n_tiles, bool approx, void *stream);
+int launch_sweep(const ChunkArgs &a, void *stream);
 int launch_approx_step(const ChunkArgs &a, int u, int64_t tile_base, int64_t n_tiles, unsigned long long *counter,
                        void *stream);
 int launch_finalize(const ChunkArgs &a, void *stream);

@@ -259,10 +259,136 @@ __device__ __forceinline__ SweepPartial block_best(double t, int64_t e, int j, d
 }
 
 // ---------------------------------------------------------------- K3: E_fwd sweep
-// One thread per bucket e in [1, n_b].  f(e) = first strategy in (T, F, j) order that
-// is finite and fits (inside the safe zone everything fits); the tile keeps the
-// best f(e) by (t, larger e).  Equivalent to the sequential sweep.
-__global__ void __launch_bounds__(kSweepThreads) k_sweep(ChunkArgs a) {
+// The sweep (dpsearch.py:194-208) keeps the best f(e) over e = 1..n_b, f(e) being the
+// first candidate of row e in (T, F, j) order that fits; ties on t go to the larger e.
+//  - safe zone (e * gran <= budget - b_up): everything fits and f(e) is the rank-0
+//    candidate.  Every T[., j] is non-increasing in e (min-plus of non-increasing
+//    columns), so the rank-0 time is too: the best safe bucket is the largest one, e_s.
+//    K3a evaluates that row only (one warp per problem).
+//  - unsafe zone: K3b walks the candidates of every unsafe row with the backward-peak
+//    check, pruned by a per-problem bound (persistent CTAs over a compact tile list).
+//  - K3r evaluates every row of the problems that want the frontier (rank-0 time per
+//    row) or use the collapsed DP (one candidate per row, not monotone in e).
+
+// largest safe bucket e_s in [0, n_b] (0: none); Python's `int <= float` is exact
+__device__ __forceinline__ int64_t safe_bucket(const DevProblem &p, double safe_limit) {
+    double x = floor(safe_limit / (double)p.gran);
+    if (!(x >= 0.0)) x = 0.0;
+    if (x > (double)p.n_b) x = (double)p.n_b;
+    int64_t e_s = (int64_t)x;
+    while (e_s >= 1 && !int_le_double(e_s * p.gran, safe_limit)) --e_s;
+    while (e_s + 1 <= p.n_b && int_le_double((e_s + 1) * p.gran, safe_limit)) ++e_s;
+    return e_s;
+}
+
+// safe_limit = budget - b_up (dpsearch.py:162-164)
+__device__ __forceinline__ double safe_limit_of(const ChunkArgs &a, const DevProblem &p, int q) {
+    return p.budget - __longlong_as_double((long long)a.bup[q]);
+}
+
+// first bucket with a finite row of the last unit: m_{U-1} = L_{U-1} + wmin_{U-1} (k_dedupe)
+__device__ __forceinline__ int64_t first_finite_row(const ChunkArgs &a, const DevProblem &p) {
+    const int last = p.U - 1;
+    return (int64_t)a.unit_lo[p.ustate_off + last] + (p.n_b - a.unit_hi[p.ustate_off + last]);
+}
+
+__device__ __forceinline__ void lex_min_warp(double &t, double &f, int &j) {
+    for (int off = 16; off > 0; off >>= 1) {
+        const double ot = __shfl_xor_sync(0xffffffffu, t, off);
+        const double of = __shfl_xor_sync(0xffffffffu, f, off);
+        const int oj = __shfl_xor_sync(0xffffffffu, j, off);
+        if (oj >= 0 && (j < 0 || lex_less(ot, of, oj, t, f, j))) { t = ot; f = of; j = oj; }
+    }
+}
+
+// K3a: per problem, the rank-0 candidate at e_s, the pruning bound it seeds, and the
+// first tile of the unsafe rows [max(e_s + 1, first finite row), n_b].
+__global__ void k_sweep_safe(ChunkArgs a) {
+    const int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (q >= a.n_probs) return;
+    const DevProblem &p = a.probs[q];
+    double t0 = GBMW_INF, f0 = GBMW_INF;
+    int j0 = -1;
+    int64_t e_s = 0;
+    int32_t first_tile = 0;                              // approx_prev: K3r writes every tile
+    if (!(p.flags & GBMW_APPROX)) {
+        const int last = p.U - 1;
+        const int64_t first_finite = first_finite_row(a, p);
+        e_s = safe_bucket(p, safe_limit_of(a, p, q));
+        if (e_s >= 1 && e_s >= first_finite) {
+            const Cell *lc = a.cells + p.cell_off + (int64_t)last * p.S;
+            const int32_t *ul = a.uniq + p.cell_off + (int64_t)last * p.S;
+            const int S = a.nuniq[p.ustate_off + last];
+            const int64_t n_e = p.n_b + 1;
+            const int64_t lo = (last == 0) ? 0 : a.unit_lo[p.ustate_off + last];
+            const TFCell *bin = a.TF[last & 1] + p.b_off;
+            const uint32_t *gf = a.gflat + p.gflat_off + (int64_t)(last >= 1 ? last - 1 : 0) * gflat_words(n_e);
+            for (int n = lane; n < S; n += 32) {
+                const int j = ul[n];
+                const Cell c = lc[j];
+                if (e_s - c.w < lo) continue;
+                double T, F;
+                if (last == 0) {
+                    T = c.c; F = c.ef;
+                } else {
+                    const double2 v = __ldg(reinterpret_cast<const double2 *>(
+                        bin + (int64_t)c.k * n_e + flat_row(gf, (int)(e_s - c.w))));
+                    T = v.x + c.c;
+                    F = v.y + c.ef;
+                }
+                if (T < GBMW_INF && (j0 < 0 || lex_less(T, F, j, t0, f0, j0))) { t0 = T; f0 = F; j0 = j; }
+            }
+            lex_min_warp(t0, f0, j0);
+        }
+        const int64_t e_lo = max(e_s + 1, first_finite);
+        first_tile = (e_lo <= p.n_b) ? (int32_t)((e_lo - 1) / kSweepThreads) : p.n_sweep_tiles;
+    }
+    if (lane == 0) {
+        SweepPartial sp;
+        sp.t = t0; sp.e = (j0 >= 0) ? e_s : -1; sp.j = (j0 >= 0) ? j0 : 0; sp.pad_ = 0;
+        a.best[q] = sp;
+        a.bound[q] = (unsigned long long)__double_as_longlong(t0);
+        a.ufirst[q] = first_tile;
+    }
+}
+
+// Exclusive prefix of the unsafe tile counts over the chunk's problems (one CTA of 1024).
+__global__ void __launch_bounds__(1024) k_sweep_scan(ChunkArgs a) {
+    __shared__ long long s_sum[1024];
+    const int n = a.n_probs, tid = threadIdx.x;
+    const int per = (n + 1023) / 1024;
+    const int b0 = min(n, tid * per), b1 = min(n, b0 + per);
+    long long s = 0;
+    for (int q = b0; q < b1; ++q)
+        if (!(a.probs[q].flags & GBMW_APPROX)) s += a.probs[q].n_sweep_tiles - a.ufirst[q];
+    s_sum[tid] = s;
+    __syncthreads();
+    for (int off = 1; off < 1024; off <<= 1) {
+        const long long v = (tid >= off) ? s_sum[tid - off] : 0;
+        __syncthreads();
+        s_sum[tid] += v;
+        __syncthreads();
+    }
+    long long run = s_sum[tid] - s;
+    for (int q = b0; q < b1; ++q) {
+        a.uprefix[q] = run;
+        if (!(a.probs[q].flags & GBMW_APPROX)) run += a.probs[q].n_sweep_tiles - a.ufirst[q];
+    }
+    if (tid == 1023) a.uprefix[n] = s_sum[1023];
+    if (tid == 0) *a.ucounter = 0ull;
+}
+
+// K3b, unsafe zone (e_fwd > budget - b_up): every candidate needs the backward-peak check
+// (a walk of U argmin pointers + the forward E_all fold).  One thread per unsafe bucket
+// walks its candidates in (T, F, j) order and stops at the first that fits (f(e),
+// dpsearch.py:202-208) or as soon as T exceeds the problem's running bound: the best t
+// found so far by any bucket (safe or unsafe), published with atomicMin.  A candidate
+// with T > bound can never be the reference's winner (min t; ties keep the larger e, so
+// T == bound is still checked).  Persistent CTAs take (problem, tile) items from the
+// compact list K3a/K3scan built, highest buckets of a problem first (they carry the
+// lowest times, so the bound tightens soonest).
+__global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
     __shared__ int32_t sW[kMaxStrats];
     __shared__ int32_t sK[kMaxStrats];
     __shared__ double sC[kMaxStrats];
@@ -270,39 +396,152 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(ChunkArgs a) {
     __shared__ double red_t[kSweepThreads / 32];
     __shared__ long long red_e[kSweepThreads / 32];
     __shared__ int red_j[kSweepThreads / 32];
-    __shared__ int32_t sJ[kMaxStrats];
-    const int q = a.sweep_map[blockIdx.x];
-    const DevProblem &p = a.probs[q];
-    if (p.flags & GBMW_APPROX) return;                   // k_approx_sweep
-    const int last = p.U - 1;
-    const int tile = blockIdx.x - (int)a.sweep_tiles[q];
-    const int64_t e = 1 + (int64_t)tile * kSweepThreads + threadIdx.x;
-    const int64_t t_lo = 1 + (int64_t)tile * kSweepThreads, t_hi = t_lo + kSweepThreads - 1;
-    // first bucket with a finite row: m_{U-1} = L_{U-1} + wmin_{U-1} (k_dedupe)
-    const int64_t lo = a.unit_lo[p.ustate_off + last];
-    const int64_t first_finite = lo + (p.n_b - a.unit_hi[p.ustate_off + last]);
-    // Every T[., j] is non-increasing in the bucket (min-plus of non-increasing columns),
-    // so the rank-0 time t0(e) is too: the best safe bucket (min t0, ties -> larger e) is
-    // the largest safe bucket e_s.  Only it is evaluated unless the frontier is wanted.
-    const double safe_limit = p.budget - __longlong_as_double((long long)a.bup[q]);
-    int64_t e_s;
-    {
-        double x = floor(safe_limit / (double)p.gran);
-        if (!(x >= 0.0)) x = 0.0;
-        if (x > (double)p.n_b) x = (double)p.n_b;
-        e_s = (int64_t)x;
-        while (e_s >= 1 && !int_le_double(e_s * p.gran, safe_limit)) --e_s;
-        while (e_s + 1 <= p.n_b && int_le_double((e_s + 1) * p.gran, safe_limit)) ++e_s;
-    }
-    const bool want_frontier = p.frontier_off >= 0;
-    if ((!want_frontier && !(e_s >= t_lo && e_s <= t_hi)) || t_hi < first_finite) {
-        if (want_frontier && e <= p.n_b) a.frontier[p.frontier_off + e - 1] = GBMW_INF;
-        if (e <= p.n_b && p.frontier_off >= 0) a.frontier[p.frontier_off + e - 1] = GBMW_INF;
-        if (threadIdx.x == 0) {
-            SweepPartial none;
-            none.t = GBMW_INF; none.e = -1; none.j = 0; none.pad_ = 0;
-            a.partials[p.tile_off + tile] = none;
+    __shared__ int2 sWK[kSweepWK];                      // (weight, class) per (unit, strategy)
+    __shared__ long long s_next;
+    const long long total = a.uprefix[a.n_probs];
+    const int lane = threadIdx.x & 31;
+    int q_prev = -1;
+    while (true) {
+        __syncthreads();
+        if (threadIdx.x == 0) s_next = (long long)atomicAdd(a.ucounter, 1ull);
+        __syncthreads();
+        const long long g = s_next;
+        if (g >= total) break;
+        const int q = find_slot(a.uprefix, a.n_probs, g);
+        const DevProblem &p = a.probs[q];
+        const int tile = p.n_sweep_tiles - 1 - (int)(g - a.uprefix[q]);
+        const int S = p.S;
+        const int last = p.U - 1;
+        const bool wk_smem = p.U * S <= kSweepWK;
+        if (q != q_prev) {
+            const Cell *lc = a.cells + p.cell_off + (int64_t)last * S;
+            for (int i = threadIdx.x; i < S; i += blockDim.x) {
+                const Cell c = lc[i];
+                sW[i] = c.w; sK[i] = c.k; sC[i] = c.c; sE[i] = c.ef;
+            }
+            if (wk_smem) {
+                const Cell *cells = a.cells + p.cell_off;
+                for (int x = threadIdx.x; x < p.U * S; x += blockDim.x) sWK[x] = make_int2(cells[x].w, cells[x].k);
+            }
+            __syncthreads();
+            q_prev = q;
         }
+        const double safe_limit = safe_limit_of(a, p, q);
+        RowCtx r;
+        r.w = sW; r.k = sK; r.c = sC; r.ef = sE;
+        r.n_e = p.n_b + 1;
+        r.init = (last == 0);
+        r.lo = (last == 0) ? 0 : a.unit_lo[p.ustate_off + last];
+        r.bin = a.TF[last & 1] + p.b_off;
+        r.gf = a.gflat + p.gflat_off + (int64_t)(last >= 1 ? last - 1 : 0) * gflat_words(p.n_b + 1);
+        volatile unsigned long long *bound = a.bound + q;
+        const int64_t e = 1 + (int64_t)tile * kSweepThreads + threadIdx.x;
+        // flat warp: the candidate order is the same in all its rows; read the row values
+        // at the warp's first row (broadcast).  Walks stay per row.
+        const int64_t e_w0 = e - lane;
+        bool flat = true;
+        {
+            const uint32_t *fl = a.chg[last & 1] + p.flag_off;
+            const int nw = (int)flag_words(p.n_b + 1);
+            for (int n = lane; n < S; n += 32) {
+                const int w = sW[n];
+                if (last == 0) flat = flat && ((e_w0 >= w) || (e_w0 + 31 < w));
+                else flat = flat && window_flat((int)(e_w0 - w), (int)r.lo, fl + (int64_t)sK[n] * nw);
+            }
+        }
+        flat = __all_sync(0xffffffffu, flat);
+        const int64_t e_val = flat ? e_w0 : e;
+        double mt = GBMW_INF;
+        int64_t me = -1;
+        int mj = 0;
+        if (e <= p.n_b && !int_le_double(e * p.gran, safe_limit)) {
+            uint16_t path[kMaxUnits];
+            double ct = 0.0, cf = 0.0;
+            int cj = -1;
+            while (true) {
+                double nt = GBMW_INF, nf = GBMW_INF;            // next candidate in (T, F, j) order
+                int nj = -1;
+                for (int j = 0; j < S; ++j) {
+                    double T, F;
+                    row_value(r, e_val, j, T, F);
+                    if (!(T < GBMW_INF)) continue;
+                    if (cj >= 0 && !lex_less(ct, cf, cj, T, F, j)) continue;
+                    if (nj < 0 || lex_less(T, F, j, nt, nf, nj)) { nt = T; nf = F; nj = j; }
+                }
+                if (nj < 0) break;
+                if (nt > __longlong_as_double((long long)*bound)) break;      // cannot win
+                if (wk_smem) backtrack_wk(a, p, e, nj, path, sWK);
+                else backtrack(a, p, e, nj, path);
+                if (plan_e_all(a, p, path) <= p.budget) {
+                    mt = nt; me = e; mj = nj;
+                    atomicMin((unsigned long long *)bound, (unsigned long long)__double_as_longlong(nt));
+                    break;
+                }
+                ct = nt; cf = nf; cj = nj;
+            }
+        }
+        const SweepPartial blk = block_best(mt, me, mj, red_t, red_e, red_j);
+        if (threadIdx.x == 0) a.partials[p.tile_off + tile] = blk;
+    }
+}
+
+// choices of the collapsed DP, walked back from bucket e (dpsearch.py:366-373)
+__device__ __forceinline__ void approx_reconstruct(const ChunkArgs &a, const DevProblem &p, int64_t e,
+                                                   uint16_t *path) {
+    const int64_t n_e = p.n_b + 1;
+    const int16_t *ch = reinterpret_cast<const int16_t *>(a.par + p.par_off);
+    const Cell *cells = a.cells + p.cell_off;
+    for (int u = p.U - 1; u >= 0; --u) {
+        const int j = ch[(int64_t)u * n_e + e];
+        path[u] = (uint16_t)j;
+        e -= cells[(int64_t)u * p.S + j].w;
+    }
+}
+
+// K3r: every row of one tile of a problem that wants the frontier or uses the collapsed
+// DP.  Frontier: the rank-0 time of each row (dpsearch.py:197-199).  Collapsed DP: the
+// one recorded candidate per row (dpsearch.py:360-364); safe rows accept it, unsafe ones
+// check E_all of the reconstructed plan; the tile's best goes to partials.
+__global__ void __launch_bounds__(kSweepThreads) k_sweep_rows(ChunkArgs a) {
+    __shared__ int32_t sW[kMaxStrats];
+    __shared__ int32_t sK[kMaxStrats];
+    __shared__ double sC[kMaxStrats];
+    __shared__ double sE[kMaxStrats];
+    __shared__ int32_t sJ[kMaxStrats];
+    __shared__ double red_t[kSweepThreads / 32];
+    __shared__ long long red_e[kSweepThreads / 32];
+    __shared__ int red_j[kSweepThreads / 32];
+    const int2 m = a.aux_map[blockIdx.x];
+    const int q = m.x, tile = m.y;
+    const DevProblem &p = a.probs[q];
+    const int64_t e = 1 + (int64_t)tile * kSweepThreads + threadIdx.x;
+    if (p.flags & GBMW_APPROX) {
+        const double safe_limit = safe_limit_of(a, p, q);
+        const TFCell *tab = a.TF[(p.U - 1) & 1] + p.b_off;
+        double mt = GBMW_INF;
+        int64_t me = -1;
+        if (e <= p.n_b) {
+            const double t = tab[e].t;
+            if (p.frontier_off >= 0) a.frontier[p.frontier_off + e - 1] = t;
+            if (t < GBMW_INF) {
+                bool fits = int_le_double(e * p.gran, safe_limit);
+                if (!fits) {
+                    uint16_t path[kMaxUnits];
+                    approx_reconstruct(a, p, e, path);
+                    fits = plan_e_all(a, p, path) <= p.budget;
+                }
+                if (fits) { mt = t; me = e; }
+            }
+        }
+        const SweepPartial blk = block_best(mt, me, 0, red_t, red_e, red_j);
+        if (threadIdx.x == 0) a.partials[p.tile_off + tile] = blk;
+        return;
+    }
+    if (p.frontier_off < 0) return;
+    const int last = p.U - 1;
+    const int64_t t_hi = (int64_t)tile * kSweepThreads + kSweepThreads;
+    if (t_hi < first_finite_row(a, p)) {
+        if (e <= p.n_b) a.frontier[p.frontier_off + e - 1] = GBMW_INF;
         return;
     }
     // rank-0 candidate = lexmin over the distinct strategies (duplicates never win ties)
@@ -315,19 +554,14 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(ChunkArgs a) {
         sW[n] = c.w; sK[n] = c.k; sC[n] = c.c; sE[n] = c.ef; sJ[n] = j;
     }
     __syncthreads();
-
     RowCtx r;
     r.w = sW; r.k = sK; r.c = sC; r.ef = sE;
     r.n_e = p.n_b + 1;
     r.init = (last == 0);
-    r.lo = (last == 0) ? 0 : lo;
+    r.lo = (last == 0) ? 0 : a.unit_lo[p.ustate_off + last];
     r.bin = a.TF[last & 1] + p.b_off;
     r.gf = a.gflat + p.gflat_off + (int64_t)(last >= 1 ? last - 1 : 0) * gflat_words(p.n_b + 1);
-
-    double best_t = GBMW_INF;
-    int64_t best_e = -1;
-    int best_j = 0;
-    if (e <= p.n_b && (want_frontier || e == e_s)) {
+    if (e <= p.n_b) {
         double t0 = GBMW_INF, f0 = GBMW_INF;
         int j0 = -1;
         for (int n = 0; n < S; ++n) {
@@ -336,143 +570,10 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(ChunkArgs a) {
             const int j = sJ[n];
             if (T < GBMW_INF && (j0 < 0 || lex_less(T, F, j, t0, f0, j0))) { t0 = T; f0 = F; j0 = j; }
         }
-        if (want_frontier) a.frontier[p.frontier_off + e - 1] = t0;
-        if (j0 >= 0 && e == e_s) { best_t = t0; best_e = e; best_j = j0; }
-        // unsafe rows (e > e_s): k_sweep_unsafe
-    }
-    SweepPartial sp = block_best(best_t, best_e, best_j, red_t, red_e, red_j);
-    if (threadIdx.x == 0) a.partials[p.tile_off + tile] = sp;
-}
-
-// Per problem: best safe bucket from K3's tile partials; it also seeds the pruning
-// bound of the unsafe walks (bits of a non-negative double order like its value).
-__global__ void k_sweep_safe_best(ChunkArgs a) {
-    const int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
-    if (q >= a.n_probs) return;
-    const DevProblem &p = a.probs[q];
-    double bt = GBMW_INF;
-    int64_t be = -1;
-    int bj = 0;
-    for (int t = lane; t < p.n_sweep_tiles; t += 32) {
-        const SweepPartial sp = a.partials[p.tile_off + t];
-        if (cand_better(sp.t, sp.e, bt, be)) { bt = sp.t; be = sp.e; bj = sp.j; }
-    }
-    for (int off = 16; off > 0; off >>= 1) {
-        const double ot = __shfl_down_sync(0xffffffffu, bt, off);
-        const long long oe = __shfl_down_sync(0xffffffffu, (long long)be, off);
-        const int oj = __shfl_down_sync(0xffffffffu, bj, off);
-        if (cand_better(ot, oe, bt, be)) { bt = ot; be = oe; bj = oj; }
-    }
-    if (lane == 0) {
-        SweepPartial sp;
-        sp.t = bt; sp.e = be; sp.j = bj; sp.pad_ = 0;
-        a.best[q] = sp;
-        a.bound[q] = (unsigned long long)__double_as_longlong(bt);
+        a.frontier[p.frontier_off + e - 1] = t0;
     }
 }
 
-// Unsafe zone (e_fwd > budget - b_up): every candidate needs the backward-peak check
-// (a walk of U argmin pointers + the forward E_all fold).  One thread per unsafe
-// bucket walks its candidates in (T, F, j) order and stops at the first that fits
-// (that is f(e), dpsearch.py:202-208) or as soon as T exceeds the problem's running
-// bound: the best t found so far by any bucket (safe or unsafe), published with
-// atomicMin.  A candidate with T > bound can never be the reference's winner
-// (min t; ties keep the larger e, so T == bound is still checked).
-__global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
-    __shared__ int32_t sW[kMaxStrats];
-    __shared__ int32_t sK[kMaxStrats];
-    __shared__ double sC[kMaxStrats];
-    __shared__ double sE[kMaxStrats];
-    __shared__ double red_t[kSweepThreads / 32];
-    __shared__ long long red_e[kSweepThreads / 32];
-    __shared__ int red_j[kSweepThreads / 32];
-    const int q = a.sweep_map[blockIdx.x];
-    const DevProblem &p = a.probs[q];
-    if (p.flags & GBMW_APPROX) return;                   // k_approx_sweep
-    const int tile = blockIdx.x - (int)a.sweep_tiles[q];
-    const int64_t e0 = 1 + (int64_t)tile * kSweepThreads;
-    const double safe_limit = p.budget - __longlong_as_double((long long)a.bup[q]);
-    const int64_t e_last = min(e0 + kSweepThreads - 1, (int64_t)p.n_b);
-    SweepPartial none;
-    none.t = GBMW_INF; none.e = -1; none.j = 0; none.pad_ = 0;
-    if (int_le_double(e_last * p.gran, safe_limit)) {      // whole tile in the safe zone
-        if (threadIdx.x == 0) a.upartials[p.tile_off + tile] = none;
-        return;
-    }
-    const int S = p.S;
-    const int last = p.U - 1;
-    const Cell *lc = a.cells + p.cell_off + (int64_t)last * S;
-    for (int i = threadIdx.x; i < S; i += blockDim.x) {
-        const Cell c = lc[i];
-        sW[i] = c.w; sK[i] = c.k; sC[i] = c.c; sE[i] = c.ef;
-    }
-    __shared__ int2 sWK[kSweepWK];                      // (weight, class) per (unit, strategy)
-    const bool wk_smem = p.U * S <= kSweepWK;
-    if (wk_smem) {
-        const Cell *cells = a.cells + p.cell_off;
-        for (int x = threadIdx.x; x < p.U * S; x += blockDim.x) sWK[x] = make_int2(cells[x].w, cells[x].k);
-    }
-    __syncthreads();
-    RowCtx r;
-    r.w = sW; r.k = sK; r.c = sC; r.ef = sE;
-    r.n_e = p.n_b + 1;
-    r.init = (last == 0);
-    r.lo = (last == 0) ? 0 : a.unit_lo[p.ustate_off + last];
-    r.bin = a.TF[last & 1] + p.b_off;
-    r.gf = a.gflat + p.gflat_off + (int64_t)(last >= 1 ? last - 1 : 0) * gflat_words(p.n_b + 1);
-    volatile unsigned long long *bound = a.bound + q;
-    const int64_t e = e0 + threadIdx.x;
-    // flat warp (see k_sweep): the candidate order is the same in all its rows; read
-    // the row values at the warp's first row (broadcast).  Walks stay per row.
-    const int lane = threadIdx.x & 31;
-    const int64_t e_w0 = e - lane;
-    bool flat = true;
-    {
-        const uint32_t *fl = a.chg[last & 1] + p.flag_off;
-        const int nw = (int)flag_words(p.n_b + 1);
-        for (int n = lane; n < S; n += 32) {
-            const int w = sW[n];
-            if (last == 0) flat = flat && ((e_w0 >= w) || (e_w0 + 31 < w));
-            else flat = flat && window_flat((int)(e_w0 - w), (int)r.lo, fl + (int64_t)sK[n] * nw);
-        }
-    }
-    flat = __all_sync(0xffffffffu, flat);
-    const int64_t e_val = flat ? e_w0 : e;
-    double mt = GBMW_INF;
-    int64_t me = -1;
-    int mj = 0;
-    if (e <= p.n_b && !int_le_double(e * p.gran, safe_limit)) {
-        uint16_t path[kMaxUnits];
-        double ct = 0.0, cf = 0.0;
-        int cj = -1;
-        while (true) {
-            double nt = GBMW_INF, nf = GBMW_INF;            // next candidate in (T, F, j) order
-            int nj = -1;
-            for (int j = 0; j < S; ++j) {
-                double T, F;
-                row_value(r, e_val, j, T, F);
-                if (!(T < GBMW_INF)) continue;
-                if (cj >= 0 && !lex_less(ct, cf, cj, T, F, j)) continue;
-                if (nj < 0 || lex_less(T, F, j, nt, nf, nj)) { nt = T; nf = F; nj = j; }
-            }
-            if (nj < 0) break;
-            if (nt > __longlong_as_double((long long)*bound)) break;      // cannot win
-            if (wk_smem) backtrack_wk(a, p, e, nj, path, sWK);
-            else backtrack(a, p, e, nj, path);
-            if (plan_e_all(a, p, path) <= p.budget) {
-                mt = nt; me = e; mj = nj;
-                atomicMin((unsigned long long *)bound, (unsigned long long)__double_as_longlong(nt));
-                break;
-            }
-            ct = nt; cf = nf; cj = nj;
-        }
-    }
-    const SweepPartial blk = block_best(mt, me, mj, red_t, red_e, red_j);
-    if (threadIdx.x == 0) a.upartials[p.tile_off + tile] = blk;
-}
-
-// ---------------------------------------------------------------- K4: finalize
 // ---------------------------------------------------------------- approx_prev (collapsed DP)
 // dpsearch.py:306-375: state (unit, bucket) only.  table_u[e] = lexmin_j (cand, cand_f, j)
 // with cand = (table_{u-1}[e-w] + R(choice_{u-1}[e-w] -> j)) + time_c, cand_f =
@@ -547,56 +648,6 @@ __global__ void __launch_bounds__(kStepThreads) k_approx_step(ChunkArgs a, int u
     }
 }
 
-// choices of the collapsed DP, walked back from bucket e (dpsearch.py:366-373)
-__device__ __forceinline__ void approx_reconstruct(const ChunkArgs &a, const DevProblem &p, int64_t e,
-                                                   uint16_t *path) {
-    const int64_t n_e = p.n_b + 1;
-    const int16_t *ch = reinterpret_cast<const int16_t *>(a.par + p.par_off);
-    const Cell *cells = a.cells + p.cell_off;
-    for (int u = p.U - 1; u >= 0; --u) {
-        const int j = ch[(int64_t)u * n_e + e];
-        path[u] = (uint16_t)j;
-        e -= cells[(int64_t)u * p.S + j].w;
-    }
-}
-
-// Sweep of the collapsed DP: one recorded candidate per bucket (dpsearch.py:360-364);
-// safe buckets accept it, unsafe ones check E_all of the reconstructed plan.
-__global__ void __launch_bounds__(kSweepThreads) k_approx_sweep(ChunkArgs a) {
-    __shared__ double red_t[kSweepThreads / 32];
-    __shared__ long long red_e[kSweepThreads / 32];
-    __shared__ int red_j[kSweepThreads / 32];
-    const int q = a.sweep_map[blockIdx.x];
-    const DevProblem &p = a.probs[q];
-    if (!(p.flags & GBMW_APPROX)) return;
-    const int tile = blockIdx.x - (int)a.sweep_tiles[q];
-    const int64_t e = 1 + (int64_t)tile * kSweepThreads + threadIdx.x;
-    const double safe_limit = p.budget - __longlong_as_double((long long)a.bup[q]);
-    const TFCell *tab = a.TF[(p.U - 1) & 1] + p.b_off;
-    double mt = GBMW_INF;
-    int64_t me = -1;
-    if (e <= p.n_b) {
-        const double t = tab[e].t;
-        if (p.frontier_off >= 0) a.frontier[p.frontier_off + e - 1] = t;
-        if (t < GBMW_INF) {
-            bool fits = int_le_double(e * p.gran, safe_limit);
-            if (!fits) {
-                uint16_t path[kMaxUnits];
-                approx_reconstruct(a, p, e, path);
-                fits = plan_e_all(a, p, path) <= p.budget;
-            }
-            if (fits) { mt = t; me = e; }
-        }
-    }
-    const SweepPartial blk = block_best(mt, me, 0, red_t, red_e, red_j);
-    if (threadIdx.x == 0) {
-        a.partials[p.tile_off + tile] = blk;
-        SweepPartial none;
-        none.t = GBMW_INF; none.e = -1; none.j = 0; none.pad_ = 0;
-        a.upartials[p.tile_off + tile] = none;
-    }
-}
-
 int launch_approx_step(const ChunkArgs &a, int u, int64_t tile_base, int64_t n_tiles, unsigned long long *counter,
                        void *stream) {
     if (n_tiles <= 0) return 0;
@@ -606,6 +657,7 @@ int launch_approx_step(const ChunkArgs &a, int u, int64_t tile_base, int64_t n_t
     return (int)cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- K4: finalize
 __global__ void k_finalize(ChunkArgs a) {
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= a.n_probs) return;
@@ -614,8 +666,8 @@ __global__ void k_finalize(ChunkArgs a) {
     double bt = safe.t;
     int64_t be = safe.e;
     int bj = safe.j;
-    for (int t = 0; t < p.n_sweep_tiles; ++t) {
-        const SweepPartial sp = a.upartials[p.tile_off + t];
+    for (int t = a.ufirst[q]; t < p.n_sweep_tiles; ++t) {       // unsafe (or collapsed-DP) tiles
+        const SweepPartial sp = a.partials[p.tile_off + t];
         if (cand_better(sp.t, sp.e, bt, be)) { bt = sp.t; be = sp.e; bj = sp.j; }
     }
     gbmw_result res;
@@ -690,12 +742,23 @@ int launch_cost_tables(const ChunkArgs &a, int64_t n_cells, int64_t n_r, void *s
     return (int)cudaGetLastError();
 }
 
-int launch_sweep(const ChunkArgs &a, int64_t n_tiles, bool approx, void *stream) {
+int launch_sweep(const ChunkArgs &a, void *stream) {
+    if (a.n_probs <= 0) return 0;
     cudaStream_t st = (cudaStream_t)stream;
-    if (n_tiles > 0) k_sweep<<<(unsigned)n_tiles, kSweepThreads, 0, st>>>(a);
-    if (n_tiles > 0 && approx) k_approx_sweep<<<(unsigned)n_tiles, kSweepThreads, 0, st>>>(a);
-    if (a.n_probs > 0) k_sweep_safe_best<<<blocks_for(a.n_probs, 4), 128, 0, st>>>(a);
-    if (n_tiles > 0) k_sweep_unsafe<<<(unsigned)n_tiles, kSweepThreads, 0, st>>>(a);
+    k_sweep_safe<<<blocks_for(a.n_probs, 4), 128, 0, st>>>(a);
+    if (a.n_aux > 0) k_sweep_rows<<<(unsigned)a.n_aux, kSweepThreads, 0, st>>>(a);
+    k_sweep_scan<<<1, 1024, 0, st>>>(a);
+    static int grid[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (!grid[dev]) {
+        int occ = 0, sms = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sweep_unsafe, kSweepThreads, 0);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        grid[dev] = (occ > 0 ? occ : 1) * (sms > 0 ? sms : 148);
+    }
+    k_sweep_unsafe<<<grid[dev], kSweepThreads, 0, st>>>(a);
     return (int)cudaGetLastError();
 }
 
