@@ -455,7 +455,7 @@ void prepare_problem(gbmw_batch &b, int pi, std::string *err) {
     h.n_gflat = approx ? 0 : (int64_t)(h.U > 1 ? h.U - 1 : 0) * gflat_words(n_e);
     h.ws_bytes = (size_t)h.n_cells * (sizeof(Cell) + sizeof(CellMem) + 4) + (size_t)h.U * 12 + (size_t)h.n_r * 8 + 8 +
                  (size_t)h.n_bcells * 2 * sizeof(TFCell) + (size_t)h.n_par * 2 +
-                 (size_t)h.n_tiles * sizeof(SweepPartial) + sizeof(SweepPartial) + 28 + (size_t)h.n_flagw * 8 +
+                 (size_t)h.n_tiles * sizeof(SweepPartial) + sizeof(SweepPartial) + 36 + (size_t)h.n_flagw * 8 +
                  (size_t)h.n_gflat * 4;
     h.gpu = true;
 }
@@ -488,7 +488,7 @@ WsLayout ws_layout(const Chunk &c) {
     w.par = o; o = align_up(o + c.n_par * 2);
     w.parts = o; o = align_up(o + c.n_tiles * sizeof(SweepPartial));
     w.bestp = o; o = align_up(o + c.probs.size() * sizeof(SweepPartial));
-    w.bound = o; o = align_up(o + c.probs.size() * 8);
+    w.bound = o; o = align_up(o + c.probs.size() * 16);
     w.ufirst = o; o = align_up(o + c.probs.size() * 4);
     w.uprefix = o; o = align_up(o + (c.probs.size() + 1) * 8);
     w.uctr = o; o = align_up(o + 8);

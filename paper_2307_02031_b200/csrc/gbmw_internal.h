@@ -148,7 +148,7 @@ struct ChunkArgs {
     uint16_t *par;
     SweepPartial *partials;       // per sweep tile: best bucket of an unsafe (K3b) or collapsed-DP (K3r) tile
     SweepPartial *best;           // per problem: best safe bucket (K3a)
-    unsigned long long *bound;    // per problem: running pruning bound (bits of t) of the unsafe walks
+    unsigned long long *bound;    // per problem, 16 B: running best {bits of t, e + 1} of the sweep (K3a, K3b)
     int32_t *ufirst;              // per problem: first sweep tile holding unsafe rows
     int64_t *uprefix;             // n_probs + 1: exclusive prefix of unsafe tiles (K3b work list)
     unsigned long long *ucounter; // K3b work counter

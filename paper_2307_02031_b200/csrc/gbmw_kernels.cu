@@ -301,6 +301,38 @@ __device__ __forceinline__ void lex_min_warp(double &t, double &f, int &j) {
     }
 }
 
+// Running best (t, e) of a problem's sweep as one 16-byte word {bits of t, e + 1}, updated
+// with 128-bit CAS (t >= 0, so the bits of t order like t).  Order: smaller t, ties ->
+// larger e (dpsearch.py:203-207).  Reads go through the CAS too (single-copy atomic).
+__device__ __forceinline__ void cas128(unsigned long long *addr, unsigned long long c0, unsigned long long c1,
+                                       unsigned long long n0, unsigned long long n1, unsigned long long &o0,
+                                       unsigned long long &o1) {
+    asm volatile("{\n\t.reg .b128 d, c, n;\n\tmov.b128 c, {%2, %3};\n\tmov.b128 n, {%4, %5};\n\t"
+                 "atom.relaxed.gpu.global.cas.b128 d, [%6], c, n;\n\tmov.b128 {%0, %1}, d;\n\t}"
+                 : "=l"(o0), "=l"(o1)
+                 : "l"(c0), "l"(c1), "l"(n0), "l"(n1), "l"(addr)
+                 : "memory");
+}
+
+__device__ __forceinline__ void bound_read(unsigned long long *b, double &t, int64_t &e) {
+    unsigned long long o0, o1;
+    cas128(b, 0ull, 0ull, 0ull, 0ull, o0, o1);
+    t = __longlong_as_double((long long)o0);
+    e = (int64_t)o1 - 1;
+}
+
+__device__ __forceinline__ void bound_offer(unsigned long long *b, double t, int64_t e) {
+    unsigned long long c0, c1;
+    cas128(b, 0ull, 0ull, 0ull, 0ull, c0, c1);
+    const unsigned long long n0 = (unsigned long long)__double_as_longlong(t), n1 = (unsigned long long)(e + 1);
+    while (cand_better(t, e, __longlong_as_double((long long)c0), (int64_t)c1 - 1)) {
+        unsigned long long o0, o1;
+        cas128(b, c0, c1, n0, n1, o0, o1);
+        if (o0 == c0 && o1 == c1) break;
+        c0 = o0; c1 = o1;
+    }
+}
+
 // K3a: per problem, the rank-0 candidate at e_s, the pruning bound it seeds, and the
 // first tile of the unsafe rows [max(e_s + 1, first finite row), n_b].
 __global__ void k_sweep_safe(ChunkArgs a) {
@@ -348,7 +380,8 @@ __global__ void k_sweep_safe(ChunkArgs a) {
         SweepPartial sp;
         sp.t = t0; sp.e = (j0 >= 0) ? e_s : -1; sp.j = (j0 >= 0) ? j0 : 0; sp.pad_ = 0;
         a.best[q] = sp;
-        a.bound[q] = (unsigned long long)__double_as_longlong(t0);
+        a.bound[2 * q] = (unsigned long long)__double_as_longlong(t0);
+        a.bound[2 * q + 1] = (unsigned long long)((j0 >= 0 ? e_s : -1) + 1);
         a.ufirst[q] = first_tile;
     }
 }
@@ -382,10 +415,9 @@ __global__ void __launch_bounds__(1024) k_sweep_scan(ChunkArgs a) {
 // K3b, unsafe zone (e_fwd > budget - b_up): every candidate needs the backward-peak check
 // (a walk of U argmin pointers + the forward E_all fold).  One thread per unsafe bucket
 // walks its candidates in (T, F, j) order and stops at the first that fits (f(e),
-// dpsearch.py:202-208) or as soon as T exceeds the problem's running bound: the best t
-// found so far by any bucket (safe or unsafe), published with atomicMin.  A candidate
-// with T > bound can never be the reference's winner (min t; ties keep the larger e, so
-// T == bound is still checked).  Persistent CTAs take (problem, tile) items from the
+// dpsearch.py:202-208) or as soon as its candidate cannot beat the problem's running best
+// (t*, e*) of any bucket (safe or unsafe): T > t*, or T == t* at a bucket below e* (ties
+// keep the larger e).  Persistent CTAs take (problem, tile) items from the
 // compact list K3a/K3scan built, highest buckets of a problem first (they carry the
 // lowest times, so the bound tightens soonest).
 __global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
@@ -434,7 +466,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
         r.lo = (last == 0) ? 0 : a.unit_lo[p.ustate_off + last];
         r.bin = a.TF[last & 1] + p.b_off;
         r.gf = a.gflat + p.gflat_off + (int64_t)(last >= 1 ? last - 1 : 0) * gflat_words(p.n_b + 1);
-        volatile unsigned long long *bound = a.bound + q;
+        unsigned long long *bound = a.bound + 2 * q;
         const int64_t e = 1 + (int64_t)tile * kSweepThreads + threadIdx.x;
         // flat warp: the candidate order is the same in all its rows; read the row values
         // at the warp's first row (broadcast).  Walks stay per row.
@@ -469,12 +501,17 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
                     if (nj < 0 || lex_less(T, F, j, nt, nf, nj)) { nt = T; nf = F; nj = j; }
                 }
                 if (nj < 0) break;
-                if (nt > __longlong_as_double((long long)*bound)) break;      // cannot win
+                {
+                    double bt;
+                    int64_t be;
+                    bound_read(bound, bt, be);
+                    if (nt > bt || (nt == bt && e < be)) break;            // cannot win
+                }
                 if (wk_smem) backtrack_wk(a, p, e, nj, path, sWK);
                 else backtrack(a, p, e, nj, path);
                 if (plan_e_all(a, p, path) <= p.budget) {
                     mt = nt; me = e; mj = nj;
-                    atomicMin((unsigned long long *)bound, (unsigned long long)__double_as_longlong(nt));
+                    bound_offer(bound, nt, e);
                     break;
                 }
                 ct = nt; cf = nf; cj = nj;
