@@ -303,7 +303,10 @@ __device__ __forceinline__ void lex_min_warp(double &t, double &f, int &j) {
 
 // Running best (t, e) of a problem's sweep as one 16-byte word {bits of t, e + 1}, updated
 // with 128-bit CAS (t >= 0, so the bits of t order like t).  Order: smaller t, ties ->
-// larger e (dpsearch.py:203-207).  Reads go through the CAS too (single-copy atomic).
+// larger e (dpsearch.py:203-207).  Updates are rare (a fitting candidate) and monotone:
+// t never increases and e only grows while t stays.  Readers use plain loads, t / e / t:
+// if both reads of t agree, t was constant in between and e belongs to it; otherwise
+// only t (the later read) is used and the tie rule is not applied (conservative).
 __device__ __forceinline__ void cas128(unsigned long long *addr, unsigned long long c0, unsigned long long c1,
                                        unsigned long long n0, unsigned long long n1, unsigned long long &o0,
                                        unsigned long long &o1) {
@@ -314,16 +317,29 @@ __device__ __forceinline__ void cas128(unsigned long long *addr, unsigned long l
                  : "memory");
 }
 
-__device__ __forceinline__ void bound_read(unsigned long long *b, double &t, int64_t &e) {
-    unsigned long long o0, o1;
-    cas128(b, 0ull, 0ull, 0ull, 0ull, o0, o1);
-    t = __longlong_as_double((long long)o0);
-    e = (int64_t)o1 - 1;
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// (t, e); e = INT64_MIN when the tie rule must not be used
+__device__ __forceinline__ void bound_read(const unsigned long long *b, double &t, int64_t &e) {
+    const unsigned long long t0 = ld_acquire(b);
+    const unsigned long long e1 = ld_acquire(b + 1);
+    const unsigned long long t1 = ld_relaxed(b);
+    t = __longlong_as_double((long long)t1);
+    e = (t0 == t1) ? (int64_t)e1 - 1 : INT64_MIN;
 }
 
 __device__ __forceinline__ void bound_offer(unsigned long long *b, double t, int64_t e) {
-    unsigned long long c0, c1;
-    cas128(b, 0ull, 0ull, 0ull, 0ull, c0, c1);
+    unsigned long long c0 = ld_relaxed(b), c1 = ld_relaxed(b + 1);
     const unsigned long long n0 = (unsigned long long)__double_as_longlong(t), n1 = (unsigned long long)(e + 1);
     while (cand_better(t, e, __longlong_as_double((long long)c0), (int64_t)c1 - 1)) {
         unsigned long long o0, o1;
