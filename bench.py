@@ -398,6 +398,8 @@ def main():
                          "traffic": (tr or {}).get("bytes_per_launch") if tr else None,
                          "algorithmic_bytes": "K per row-step * (16 B read + 16 B write + 2 B argmin), "
                                               "see DESIGN.md §4"},
+            "sweep_work": {k: timing[k] for k in ("sweep_rows", "sweep_cands", "sweep_checks")},
+            "dp_work": {"live_cells": timing["live_cells"], "computed_cells": timing["dp_cells"]},
             "gpu_launches": int(allst[:, 5].sum()),
             "clocks": clk,
             "e2e": {"value": total_T / (e2e_step_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_step_ms,

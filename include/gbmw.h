@@ -146,6 +146,9 @@ typedef struct gbmw_timing {
     double  upload_ms;         /* host wall time of the arena allocation + upload */
     double  fetch_ms;          /* host wall time of the last gbmw_batch_fetch */
     double  live_cells;        /* class cells K2 computed (rows inside [L_u, H_u], times K) */
+    double  sweep_rows;        /* unsafe buckets walked by K3b */
+    double  sweep_cands;       /* candidates K3b examined (rejected by the F + O_b bound or checked) */
+    double  sweep_checks;      /* candidates K3b backtracked for the exact E_all check */
 } gbmw_timing;
 
 typedef struct gbmw_ctx gbmw_ctx;

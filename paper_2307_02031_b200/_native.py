@@ -53,7 +53,8 @@ class Timing(ctypes.Structure):
                 ("dp_bytes", ctypes.c_double), ("dp_cells", ctypes.c_double),
                 ("h2d_bytes", ctypes.c_double), ("d2h_bytes", ctypes.c_double),
                 ("prep_ms", ctypes.c_double), ("upload_ms", ctypes.c_double), ("fetch_ms", ctypes.c_double),
-                ("live_cells", ctypes.c_double)]
+                ("live_cells", ctypes.c_double), ("sweep_rows", ctypes.c_double),
+                ("sweep_cands", ctypes.c_double), ("sweep_checks", ctypes.c_double)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}

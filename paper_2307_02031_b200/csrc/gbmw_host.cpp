@@ -664,7 +664,7 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
     b->o_results = o; o = align_up(o + b->problems.size() * sizeof(gbmw_result));
     b->o_plans = o; o = align_up(o + (size_t)b->total_plan * sizeof(int32_t));
     b->o_frontier = o; o = align_up(o + (size_t)b->total_frontier * sizeof(double));
-    b->o_stats = o; o = align_up(o + 2 * (b->chunks.size() + 1) * 8);
+    b->o_stats = o; o = align_up(o + 5 * (b->chunks.size() + 1) * 8);
     b->arena_size = std::max<size_t>(o, 256);
     for (Chunk &c : b->chunks) c.small_off += o_blob;
     cudaSetDevice(ctx->device);
@@ -791,6 +791,7 @@ ChunkArgs chunk_args(gbmw_batch *b, const Chunk &c, char *ws, size_t chunk_index
     a.plans = (int32_t *)(arena + b->o_plans);
     a.frontier = (double *)(arena + b->o_frontier);
     a.live_cells = (unsigned long long *)(arena + b->o_stats) + chunk_index;
+    a.sweep_stats = (unsigned long long *)(arena + b->o_stats) + 2 * (b->chunks.size() + 1);
     a.computed_cells = (unsigned long long *)(arena + b->o_stats) + (b->chunks.size() + 1) + chunk_index;
     return a;
 }
@@ -807,7 +808,7 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
     b->timing.total_ms = b->timing.dp_ms = b->timing.sweep_ms = b->timing.tables_ms = b->timing.finalize_ms = 0.f;
     b->timing.n_launches = 0;
     cudaStream_t st = ctx->stream;
-    cudaMemsetAsync((char *)b->arena + b->o_stats, 0, 2 * (b->chunks.size() + 1) * 8, st);
+    cudaMemsetAsync((char *)b->arena + b->o_stats, 0, 5 * (b->chunks.size() + 1) * 8, st);
     for (Chunk &c : b->chunks) {
         for (auto &e : c.ev)
             if (!e) cudaEventCreate(&e);
@@ -860,12 +861,16 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
     }
     if (!tables_only && !b->chunks.empty()) {
         // K2 algorithmic bytes = 34 B per live class cell
-        std::vector<unsigned long long> live(2 * (b->chunks.size() + 1));
+        std::vector<unsigned long long> live(5 * (b->chunks.size() + 1));
         cudaMemcpy(live.data(), (char *)b->arena + b->o_stats, live.size() * 8, cudaMemcpyDeviceToHost);
+        const size_t nc = b->chunks.size();
         double cells = 0.0;
-        for (auto v : live) cells += (double)v;
+        for (size_t i = 0; i <= nc; ++i) cells += (double)live[i];
         double computed = 0.0;
-        for (size_t i = 0; i < b->chunks.size(); ++i) computed += (double)live[b->chunks.size() + 1 + i];
+        for (size_t i = 0; i < nc; ++i) computed += (double)live[nc + 1 + i];
+        b->timing.sweep_rows = (double)live[2 * (nc + 1)];
+        b->timing.sweep_cands = (double)live[2 * (nc + 1) + 1];
+        b->timing.sweep_checks = (double)live[2 * (nc + 1) + 2];
         // writes of every live class cell (t, f, argmin) + source reads of the rows evaluated
         b->timing.dp_bytes = cells * 18.0 + computed * 16.0;
         b->timing.dp_cells = computed;

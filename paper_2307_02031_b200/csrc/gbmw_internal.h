@@ -157,6 +157,7 @@ struct ChunkArgs {
     int32_t *unit_lo, *unit_hi;   // per unit u: live rows [L_u, H_u] of B_u (see k_dedupe)
     unsigned long long *counters; // per K2 launch: dynamic tile counter
     unsigned long long *live_cells;   // sum over problems and units of K * live rows
+    unsigned long long *sweep_stats;  // K3b: unsafe rows walked, candidates examined, E_all checks
     int64_t n_units;
     gbmw_result *results;
     int32_t *plans;

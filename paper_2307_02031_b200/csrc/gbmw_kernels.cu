@@ -190,20 +190,21 @@ __device__ __forceinline__ void backtrack(const ChunkArgs &a, const DevProblem &
     }
 }
 
-// Same walk with (weight, class) of every (unit, strategy) staged in shared memory: the
-// chain per unit is then one global load (the argmin) instead of three.
+// Same walk with (weight, class) of every (unit, strategy) staged in shared memory, packed
+// as weight << 4 | class (weight <= n_b + 1 < 2^27): the chain per unit is then one global
+// load (the argmin) instead of three.
 __device__ __forceinline__ void backtrack_wk(const ChunkArgs &a, const DevProblem &p, int64_t e, int j,
-                                             uint16_t *path, const int2 *wk) {
+                                             uint16_t *path, const uint32_t *wk) {
     const int U = p.U, S = p.S, K = p.K;
     const int64_t n_e = p.n_b + 1;
     const uint16_t *par = a.par + p.par_off;
     const int gw = (int)gflat_words(n_e);
     path[U - 1] = (uint16_t)j;
     for (int u = U - 1; u >= 1; --u) {
-        const int2 c = wk[u * S + j];
-        e -= c.x;
+        const uint32_t c = wk[u * S + j];
+        e -= (int64_t)(c >> 4);
         const int er = flat_row(a.gflat + p.gflat_off + (int64_t)(u - 1) * gw, (int)e);
-        j = par[((int64_t)(u - 1) * K + c.y) * n_e + er];
+        j = par[((int64_t)(u - 1) * K + (int)(c & 15u)) * n_e + er];
         path[u - 1] = (uint16_t)j;
     }
 }
@@ -444,11 +445,13 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
     __shared__ double red_t[kSweepThreads / 32];
     __shared__ long long red_e[kSweepThreads / 32];
     __shared__ int red_j[kSweepThreads / 32];
-    __shared__ int2 sWK[kSweepWK];                      // (weight, class) per (unit, strategy)
+    __shared__ double sOB[kMaxStrats];                  // O_b of one layer of the last unit
+    __shared__ uint32_t sWK[kSweepWK];                  // weight << 4 | class per (unit, strategy)
     __shared__ long long s_next;
     const long long total = a.uprefix[a.n_probs];
     const int lane = threadIdx.x & 31;
     int q_prev = -1;
+    unsigned long long n_rows = 0, n_cands = 0, n_checks = 0;
     while (true) {
         __syncthreads();
         if (threadIdx.x == 0) s_next = (long long)atomicAdd(a.ucounter, 1ull);
@@ -463,13 +466,16 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
         const bool wk_smem = p.U * S <= kSweepWK;
         if (q != q_prev) {
             const Cell *lc = a.cells + p.cell_off + (int64_t)last * S;
+            const CellMem *lm = a.cmem + p.cell_off + (int64_t)last * S;
             for (int i = threadIdx.x; i < S; i += blockDim.x) {
                 const Cell c = lc[i];
                 sW[i] = c.w; sK[i] = c.k; sC[i] = c.c; sE[i] = c.ef;
+                sOB[i] = lm[i].o_b;
             }
             if (wk_smem) {
                 const Cell *cells = a.cells + p.cell_off;
-                for (int x = threadIdx.x; x < p.U * S; x += blockDim.x) sWK[x] = make_int2(cells[x].w, cells[x].k);
+                for (int x = threadIdx.x; x < p.U * S; x += blockDim.x)
+                    sWK[x] = ((uint32_t)cells[x].w << 4) | (uint32_t)cells[x].k;
             }
             __syncthreads();
             q_prev = q;
@@ -503,6 +509,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
         int64_t me = -1;
         int mj = 0;
         if (e <= p.n_b && !int_le_double(e * p.gran, safe_limit)) {
+            ++n_rows;
             uint16_t path[kMaxUnits];
             double ct = 0.0, cf = 0.0;
             int cj = -1;
@@ -523,6 +530,14 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
                     bound_read(bound, bt, be);
                     if (nt > bt || (nt == bt && e < be)) break;            // cannot win
                 }
+                ++n_cands;
+                // E_all >= sum(O_f) + sum(O_ms) + O_b(last layer) = F + O_b(last unit, nj): a
+                // candidate over the budget by more than the rounding of both sums cannot fit
+                if ((nf + sOB[nj]) * (1.0 - 1e-9) > p.budget) {
+                    ct = nt; cf = nf; cj = nj;
+                    continue;
+                }
+                ++n_checks;
                 if (wk_smem) backtrack_wk(a, p, e, nj, path, sWK);
                 else backtrack(a, p, e, nj, path);
                 if (plan_e_all(a, p, path) <= p.budget) {
@@ -535,6 +550,16 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
         }
         const SweepPartial blk = block_best(mt, me, mj, red_t, red_e, red_j);
         if (threadIdx.x == 0) a.partials[p.tile_off + tile] = blk;
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+        n_rows += __shfl_xor_sync(0xffffffffu, n_rows, off);
+        n_cands += __shfl_xor_sync(0xffffffffu, n_cands, off);
+        n_checks += __shfl_xor_sync(0xffffffffu, n_checks, off);
+    }
+    if (lane == 0 && n_rows) {
+        atomicAdd(a.sweep_stats, n_rows);
+        atomicAdd(a.sweep_stats + 1, n_cands);
+        atomicAdd(a.sweep_stats + 2, n_checks);
     }
 }
 
