@@ -8,19 +8,17 @@
 // every row (SURVEY-scale configs: 86-100 % of live groups).  A group is "flat" when,
 // for every distinct source strategy i, the 32-row source window of column cls(i) of
 // B_{u-1} contains no change point; its 32 outputs are then the output of its first
-// row, computed once and stored once (readers redirect through the flat-group mask).
-// Change points of B_u are emitted as one bit per (class, row) (bit x = row x differs
-// from row x-1), exactly.
+// row, computed once.  Change points of B_u are emitted as one bit per (class, row)
+// (bit x = row x differs from row x-1), exactly; a spurious 1 bit would only cost
+// work, never exactness.
 //
-// Work split: a CTA takes tiles of kStepRows rows (dynamic tile counter); inside a tile
-// each warp takes 32-row groups (dynamic group counter) and finishes them on its own:
-//   - window check: lanes over the source strategies, one 64-bit read of change bits each;
-//   - flat group: its first row, warp-cooperatively (lanes over sources, shuffle lexmin);
-//   - full group: one row per lane;
-//   - bit 0 of the group (row r0 vs r0-1): free when every source window extends one row
-//     down unchanged (33-row check), else row r0-1 is computed warp-cooperatively.
-// Only the tile boundaries synchronise the CTA.  Tie-break T1 (lexicographic (cand, F,
-// i), first i) is the one of every row; the cooperative lexmin reduces (t, f, i).
+// One CTA processes one tile of kStepRows rows of one problem:
+//   1. classify the tile's 32-row groups (dead / flat / full) from the change bits,
+//   2. compute the list of rows that need it: every row of a full group (one warp per
+//      group, lanes in row order), one row per flat group, and the row before the
+//      tile (for the first change bit),
+//   3. write flat groups' rows from shared memory, and the change-bit words.
+// Tie-break T1 (lexicographic (cand, F, i), first i) is the one of every row.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -30,246 +28,287 @@ namespace gbmw {
 
 #define GBMW_STEP_INF __longlong_as_double(0x7ff0000000000000LL)
 
-constexpr int kStepIB = 4;                  // sources per lane in flight
+constexpr int kStepIB = 4;                  // strategy batch: independent loads in flight
+constexpr int kClassifyIB = 8;              // window checks per thread in flight
 constexpr int kGroups = kStepRows / 32;     // 32-row groups per tile
 constexpr int kMaxGfWords = (int)(((GBMW_MAX_BUCKETS + 1 + 31) / 32 + 31) / 32 + 1);   // gflat_words(max n_e)
 
-// KM: class capacity of the instantiation (4 / 8 / kMaxClasses)
+// KM: class capacity of the instantiation (4 / 8 / kMaxClasses), sizes the per-group arrays
 template <int KM>
 struct StepShared {
     Cell cell[kMaxStrats];                  // distinct source strategies of unit u-1 (ascending)
     int idx[kMaxStrats];                    // their strategy index
+    CellMem mem[kMaxStrats];                // their per-layer O_f, O_b, O_ms (path-state fold)
     double r[KM * KM];
-    uint32_t gfp[kMaxGfWords];              // flat-group mask of B_{u-1}
-    int S, K, n_e, lo_prev, lo, hi, nw, gw;
-    int64_t b_off, par_off, f_off, gf_cur;
+    uint32_t gfp[kMaxGfWords];              // flat-group mask of B_{u-1} (read redirection, flat_row)
+    int S, K, n_e, q, lo_prev, lo, hi, nw, cnt_prev;
+    int64_t b_off, par_off, tile0, f_off;
+    int64_t gf_cur;                         // flat-group mask of B_u (offset into a.gflat)
+    int gw;
     int64_t next;
-    int gnext;
-    uint32_t gmask[kGroups / 32];           // flat-group bits of the current tile
-    // per warp: row r0 of its current group and the change bits of rows r0+1 .. r0+31
-    double wt[kStepThreads / 32][KM], wf[kStepThreads / 32][KM];
-    uint32_t wm[kStepThreads / 32][KM];
+    // per tile
+    int kind[kGroups];                      // 0 dead, 1 flat, 2 full
+    int list_np[kGroups], list_fl[kGroups];
+    int n_np, n_fl;
+    unsigned bits[kGroups][KM];
+    double first_t[kGroups][KM], first_f[kGroups][KM];
+    double last_t[kGroups][KM], last_f[kGroups][KM];
+    double prev_t[KM], prev_f[KM];
+    int prev_ok;
+    unsigned long long stat_rows;
 };
 
-__device__ __forceinline__ int flat_row_s(const uint32_t *gfs, int row) {
-    const int g = row >> 5;
-    return ((gfs[g >> 5] >> (g & 31)) & 1u) ? (row & ~31) : row;
-}
-
-// (T, F) of source strategy c at target row e (reference table T_{u-1}[e, i])
-template <bool FIRST, class SH>
-__device__ __forceinline__ void src_value(const SH &sh, const TFCell *bin, const Cell &c, int e, bool ok, double &T,
-                                          double &F) {
-    T = GBMW_STEP_INF; F = GBMW_STEP_INF;
-    const int src = e - c.w;
-    if (ok && src >= (FIRST ? 0 : sh.lo_prev)) {
-        if (FIRST) {                        // init row, dpsearch.py:255-259
-            T = c.c; F = c.ef;
-        } else {
-            const double2 v = __ldg(reinterpret_cast<const double2 *>(bin + c.k * sh.n_e + flat_row_s(sh.gfp, src)));
-            T = v.x + c.c;
-            F = v.y + c.ef;
-        }
-    }
-}
-
-// fold candidate (T, F) of source n into the running lexmins (strict: first n wins ties)
-template <int KT, bool GUARD, class SH>
-__device__ __forceinline__ void fold(const SH &sh, int n, double T, double F, double *bt, double *bf, int *bp) {
-    const int K = GUARD ? sh.K : KT;
-    const double *rrow = sh.r + sh.cell[n].k * K;
-    const int gi = sh.idx[n];
-#pragma unroll
-    for (int kk = 0; kk < KT; ++kk) {
-        if (!GUARD || kk < K) {
-            const double cand = T + rrow[kk];
-            const bool better = (cand < bt[kk]) || (cand == bt[kk] && F < bf[kk]);
-            bt[kk] = better ? cand : bt[kk];
-            bf[kk] = better ? F : bf[kk];
-            bp[kk] = better ? gi : bp[kk];
-        }
-    }
-}
-
-// K lexmins of row e, one row per lane (e < 0: dead row, +inf)
+// K lexmins of one source row e' (T1 tie-break).  Rows outside [lo_prev + w, hi] read +inf.
 template <int KT, bool FIRST, bool GUARD, class SH>
-__device__ __forceinline__ void relax_row(const ChunkArgs &a, const SH &sh, int u, int e, double *bt, double *bf,
-                                          int *bp) {
-    const int S = sh.S;
+__device__ __forceinline__ void relax_row(const ChunkArgs &a, const SH &sh, int u, int e,
+                                          double *bt, double *bf, int *bp) {
+    const int S = sh.S, K = GUARD ? sh.K : KT;
+    const int n_e = sh.n_e, lo_prev = FIRST ? 0 : sh.lo_prev, hi = sh.hi;
     const TFCell *bin = a.TF[(u - 1) & 1] + sh.b_off;
 #pragma unroll
     for (int kk = 0; kk < KT; ++kk) { bt[kk] = GBMW_STEP_INF; bf[kk] = GBMW_STEP_INF; bp[kk] = 0; }
-    const bool row_ok = e >= 0;
+    const bool row_ok = e >= 0 && e <= hi;
     for (int i0 = 0; i0 < S; i0 += kStepIB) {
         double T[kStepIB], F[kStepIB];
 #pragma unroll
         for (int b = 0; b < kStepIB; ++b) {
             const int i = i0 + b;
-            src_value<FIRST>(sh, bin, sh.cell[i < S ? i : 0], e, i < S && row_ok, T[b], F[b]);
-        }
-#pragma unroll
-        for (int b = 0; b < kStepIB; ++b) {
-            if (i0 + b >= S) break;
-            fold<KT, GUARD>(sh, i0 + b, T[b], F[b], bt, bf, bp);
-        }
-    }
-}
-
-// K lexmins of one row e, warp-cooperatively: lane l takes sources l, l+32, ...; the
-// partial lexmins are reduced over (t, f, strategy index).  Result in every lane.
-template <int KT, bool FIRST, bool GUARD, class SH>
-__device__ __forceinline__ void relax_coop(const ChunkArgs &a, const SH &sh, int u, int e, int lane, double *bt,
-                                           double *bf, int *bp) {
-    const int S = sh.S, K = GUARD ? sh.K : KT;
-    const TFCell *bin = a.TF[(u - 1) & 1] + sh.b_off;
-#pragma unroll
-    for (int kk = 0; kk < KT; ++kk) { bt[kk] = GBMW_STEP_INF; bf[kk] = GBMW_STEP_INF; bp[kk] = 0; }
-    for (int n0 = lane; n0 < S; n0 += 32 * kStepIB) {
-        double T[kStepIB], F[kStepIB];
-#pragma unroll
-        for (int b = 0; b < kStepIB; ++b) {
-            const int n = n0 + 32 * b;
-            src_value<FIRST>(sh, bin, sh.cell[n < S ? n : 0], e, n < S, T[b], F[b]);
-        }
-#pragma unroll
-        for (int b = 0; b < kStepIB; ++b) {
-            const int n = n0 + 32 * b;
-            if (n >= S) break;
-            fold<KT, GUARD>(sh, n, T[b], F[b], bt, bf, bp);
-        }
-    }
-#pragma unroll
-    for (int kk = 0; kk < KT; ++kk) {
-        if (GUARD && kk >= K) break;
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            const double ot = __shfl_xor_sync(0xffffffffu, bt[kk], off);
-            const double of = __shfl_xor_sync(0xffffffffu, bf[kk], off);
-            const int op = __shfl_xor_sync(0xffffffffu, bp[kk], off);
-            const bool take = (ot < bt[kk]) || (ot == bt[kk] && (of < bf[kk] || (of == bf[kk] && op < bp[kk])));
-            bt[kk] = take ? ot : bt[kk];
-            bf[kk] = take ? of : bf[kk];
-            bp[kk] = take ? op : bp[kk];
-        }
-    }
-}
-
-// Source window of rows [x0, x0+31] of one class column (change bits fl, rows below lo
-// are +inf): f32 = constant on the window, e33 = constant on [x0-1, x0+31].
-__device__ __forceinline__ void window_bits(int x0, int lo, const uint32_t *fl, bool &f32, bool &e33) {
-    if (x0 + 31 < lo) { f32 = true; e33 = true; return; }
-    if (x0 < lo) { f32 = false; e33 = false; return; }
-    const int w0 = x0 >> 5, s = x0 & 31;
-    const unsigned long long v =
-        ((unsigned long long)__ldg(fl + w0 + 1) << 32 | (unsigned long long)__ldg(fl + w0)) >> s;
-    f32 = (v & 0xfffffffeull) == 0ull;                 // bits of rows x0+1 .. x0+31
-    e33 = (x0 - 1 >= lo) && (v & 0xffffffffull) == 0ull;   // and row x0 vs x0-1
-}
-
-// One 32-row group of B_u, by one warp.  Returns the rows computed (for the work counter).
-template <int KT, bool FIRST, bool GUARD, class SH>
-__device__ __forceinline__ int step_group(const ChunkArgs &a, SH &sh, int u, int r0, int g, int lane) {
-    const int K = GUARD ? sh.K : KT;
-    const int n_e = sh.n_e, lo = sh.lo, hi = sh.hi, r1 = r0 + 31;
-    const int wi = r0 >> 5;
-    uint32_t *fout = a.chg[u & 1] + sh.f_off;
-    if (r1 < lo || r0 > hi) {                                   // dead rows: never read as flat
-        if (wi < sh.nw)
-            for (int kk = lane; kk < K; kk += 32) fout[(int64_t)kk * sh.nw + wi] = 0xffffffffu;
-        return 0;
-    }
-    TFCell *bout = a.TF[u & 1] + sh.b_off;
-    uint16_t *pout = a.par + sh.par_off + (int64_t)(u - 1) * K * n_e;
-    const bool whole = r0 >= lo && r1 <= hi;
-    bool flat = whole, ext = whole;
-    if (whole) {
-        const uint32_t *fin = a.chg[(u - 1) & 1] + sh.f_off;
-        for (int n = lane; n < sh.S; n += 32) {
-            const int x0 = r0 - sh.cell[n].w;
-            bool f32, e33;
-            if (FIRST) {
-                f32 = (x0 >= 0) || (x0 + 31 < 0);
-                e33 = (x0 - 1 >= 0) || (x0 + 31 < 0);
-            } else {
-                window_bits(x0, sh.lo_prev, fin + (int64_t)sh.cell[n].k * sh.nw, f32, e33);
+            const Cell c = sh.cell[i < S ? i : 0];
+            const int src = e - c.w;
+            T[b] = GBMW_STEP_INF; F[b] = GBMW_STEP_INF;
+            if (i < S && row_ok && src >= lo_prev) {
+                if (FIRST) {                       // init row, dpsearch.py:255-259
+                    T[b] = c.c; F[b] = c.ef;
+                } else {
+                    const int g = src >> 5;
+                    const int rs = ((sh.gfp[g >> 5] >> (g & 31)) & 1u) ? (src & ~31) : src;
+                    const double2 v = __ldg(reinterpret_cast<const double2 *>(bin + c.k * n_e + rs));
+                    T[b] = v.x + c.c;
+                    F[b] = v.y + c.ef;
+                }
             }
-            flat = flat && f32;
-            ext = ext && e33;
         }
-        flat = __all_sync(0xffffffffu, flat);
-        ext = __all_sync(0xffffffffu, ext);
+#pragma unroll
+        for (int b = 0; b < kStepIB; ++b) {
+            const int i = i0 + b;
+            if (i >= S) break;
+            const int ck = sh.cell[i].k;
+            const double *rrow = sh.r + ck * K;
+#pragma unroll
+            for (int kk = 0; kk < KT; ++kk) {
+                if (!GUARD || kk < K) {
+                    const double cand = T[b] + rrow[kk];
+                    const bool better = (cand < bt[kk]) || (cand == bt[kk] && F[b] < bf[kk]);
+                    bt[kk] = better ? cand : bt[kk];
+                    bf[kk] = better ? F[b] : bf[kk];
+                    bp[kk] = better ? i : bp[kk];       // position in the distinct list
+                }
+            }
+        }
     }
-    const int warp = threadIdx.x >> 5;
-    int rows;
-    {
+}
+
+// Path state of B_u[e] with argmin source n (distinct-list position): the source cell's
+// state (load_state) folded over the layers of unit u-1 with strategy n, in plan_e_all's
+// order (fold_state).
+template <class SH>
+__device__ __forceinline__ void load_state(const ChunkArgs &a, const SH &sh, int u, int e, int n, double &pf,
+                                           double &ms, double &peak) {
+    const Cell c = sh.cell[n];
+    const int src = e - c.w;
+    const int g = src >> 5;
+    const int rs = ((sh.gfp[g >> 5] >> (g & 31)) & 1u) ? (src & ~31) : src;
+    const PathState *ps = a.PS[(u - 1) & 1] + sh.b_off + (int64_t)c.k * sh.n_e + rs;
+    const double2 v0 = __ldg(reinterpret_cast<const double2 *>(ps));
+    pf = v0.x; ms = v0.y;
+    peak = __ldg(&ps->peak);
+}
+
+template <class SH>
+__device__ __forceinline__ void fold_state(const SH &sh, int n, double &pf, double &ms, double &peak) {
+    const CellMem m = sh.mem[n];
+    for (int r = 0; r < sh.cnt_prev; ++r) {
+        ms = ms + m.o_ms;
+        pf = pf + m.o_f;
+        const double x = pf + m.o_b;
+        peak = (x > peak) ? x : peak;                      // Python max(peak, x)
+    }
+}
+
+template <int KT, bool FIRST, bool GUARD, class SH>
+__device__ void step_tile(const ChunkArgs &a, SH &sh, int u, int first_row) {
+    const int K = GUARD ? sh.K : KT;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthr = blockDim.x;
+    const int n_e = sh.n_e, lo = sh.lo, hi = sh.hi, S = sh.S;
+    // ---- 1. classify groups
+    for (int g = tid; g < kGroups; g += nthr) {
+        const int r0 = first_row + 32 * g, r1 = r0 + 31;
+        sh.kind[g] = (r1 < lo || r0 > hi) ? 0 : ((r0 >= lo && r1 <= hi) ? 1 : 2);
+    }
+    __syncthreads();
+    const uint32_t *fin = a.chg[(u - 1) & 1] + sh.f_off;
+    // (group, source) window checks, kClassifyIB per thread in flight
+    const int n_checks = kGroups * S;
+    for (int x0 = tid; x0 < n_checks; x0 += nthr * kClassifyIB) {
+        uint32_t w0[kClassifyIB], w1[kClassifyIB];
+        int sh_[kClassifyIB], gg[kClassifyIB];
+        bool load[kClassifyIB];
+#pragma unroll
+        for (int b = 0; b < kClassifyIB; ++b) {
+            const int x = x0 + b * nthr;
+            gg[b] = -1; load[b] = false; sh_[b] = 0;
+            w0[b] = 0u; w1[b] = 0u;
+            if (x < n_checks) {
+                const int g = x / S, n = x - g * S;
+                if (sh.kind[g] == 1) {
+                    const Cell c = sh.cell[n];
+                    const int r0 = first_row + 32 * g;
+                    if (FIRST) {
+                        if (!((r0 >= c.w) || (r0 + 31 < c.w))) gg[b] = g;
+                    } else {
+                        const int xs = r0 - c.w;
+                        if (xs + 31 < sh.lo_prev) {
+                            // all +inf: flat
+                        } else if (xs < sh.lo_prev) {
+                            gg[b] = g;
+                        } else {
+                            const int lb = xs + 1;
+                            const uint32_t *fl = fin + (int64_t)c.k * sh.nw + (lb >> 5);
+                            w0[b] = __ldg(fl); w1[b] = __ldg(fl + 1);
+                            sh_[b] = lb & 31;
+                            load[b] = true;
+                            gg[b] = g;
+                        }
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int b = 0; b < kClassifyIB; ++b) {
+            if (gg[b] < 0) continue;
+            bool flat = false;
+            if (load[b]) {
+                const unsigned long long v = ((unsigned long long)w1[b] << 32 | (unsigned long long)w0[b]) >> sh_[b];
+                flat = (v & 0x7fffffffull) == 0ull;
+            }
+            if (!flat) sh.kind[gg[b]] = 2;
+        }
+    }
+    __syncthreads();
+    // ---- 2. row list: full groups (32 rows, one warp each), then flat representatives
+    if (warp == 0) {
+        int np = 0, nf = 0;
+        for (int base = 0; base < kGroups; base += 32) {
+            const int g = base + lane;
+            const int kd = g < kGroups ? sh.kind[g] : 0;
+            const unsigned mnp = __ballot_sync(0xffffffffu, kd == 2), mfl = __ballot_sync(0xffffffffu, kd == 1);
+            const unsigned below = (1u << lane) - 1u;
+            if (kd == 2) sh.list_np[np + __popc(mnp & below)] = g;
+            if (kd == 1) sh.list_fl[nf + __popc(mfl & below)] = g;
+            np += __popc(mnp);
+            nf += __popc(mfl);
+        }
+        if (lane == 0) {
+            sh.n_np = np;
+            sh.n_fl = nf;
+            sh.stat_rows += (unsigned long long)(32 * np + nf + 1) * (unsigned long long)K;
+        }
+    }
+    __syncthreads();
+    const int n_np = sh.n_np, n_fl = sh.n_fl;
+    const int n_list = 32 * n_np + n_fl + 1;                // + the row before the tile
+    TFCell *bout = a.TF[u & 1] + sh.b_off;
+    PathState *psout = a.PS[u & 1] + sh.b_off;
+    uint16_t *pout = a.par + sh.par_off + (int64_t)(u - 1) * K * n_e;
+    const int n_pass = (n_list + nthr - 1) / nthr;
+    for (int pass = 0; pass < n_pass; ++pass) {
+        const int x = pass * nthr + tid;
         double bt[KT], bf[KT];
         int bp[KT];
-        if (flat) {
-            relax_coop<KT, FIRST, GUARD>(a, sh, u, r0, lane, bt, bf, bp);
-            rows = 1;
-#pragma unroll
-            for (int kk = 0; kk < KT; ++kk) {
-                if (GUARD && kk >= K) break;
-                if (lane == kk) {
-                    reinterpret_cast<double2 *>(bout)[(int64_t)kk * n_e + r0] = make_double2(bt[kk], bf[kk]);
-                    pout[(int64_t)kk * n_e + r0] = (uint16_t)bp[kk];
-                    sh.wt[warp][kk] = bt[kk]; sh.wf[warp][kk] = bf[kk]; sh.wm[warp][kk] = 0u;
-                }
-            }
-            if (lane == 0) atomicOr(&sh.gmask[g >> 5], 1u << (g & 31));
-        } else {
-            const int e = r0 + lane;
-            const bool live = e >= lo && e <= hi;
-            relax_row<KT, FIRST, GUARD>(a, sh, u, live ? e : -1, bt, bf, bp);
-            rows = 32;
-#pragma unroll
-            for (int kk = 0; kk < KT; ++kk) {
-                if (GUARD && kk >= K) break;
-                if (live) {
-                    reinterpret_cast<double2 *>(bout)[(int64_t)kk * n_e + e] = make_double2(bt[kk], bf[kk]);
-                    pout[(int64_t)kk * n_e + e] = (uint16_t)bp[kk];
-                }
-                const double ut = __shfl_up_sync(0xffffffffu, bt[kk], 1);
-                const double uf = __shfl_up_sync(0xffffffffu, bf[kk], 1);
-                const unsigned m = __ballot_sync(0xffffffffu, lane > 0 && (ut != bt[kk] || uf != bf[kk]));
-                if (lane == 0) { sh.wt[warp][kk] = bt[kk]; sh.wf[warp][kk] = bf[kk]; sh.wm[warp][kk] = m; }
-            }
+        int e = -1, kind = -1, g = -1;
+        if (x < 32 * n_np) {
+            g = sh.list_np[x >> 5]; e = first_row + 32 * g + lane; kind = 2;
+        } else if (x < 32 * n_np + n_fl) {
+            g = sh.list_fl[x - 32 * n_np]; e = first_row + 32 * g; kind = 1;
+        } else if (x == 32 * n_np + n_fl) {
+            e = first_row - 1; kind = 3;
         }
-    }
-    __syncwarp();
-    // bit 0 (row r0 vs r0-1): settled by the 33-row source windows, else row r0-1 is computed
-    const bool need_b = !ext && (r0 - 1 >= lo);
-    if (need_b) {
-        double pt[KT], pf[KT];
-        int pp[KT];
-        relax_coop<KT, FIRST, GUARD>(a, sh, u, r0 - 1, lane, pt, pf, pp);
-        rows += 1;
+        relax_row<KT, FIRST, GUARD>(a, sh, u, (kind >= 0 && e >= lo && e <= hi && e < n_e) ? e : -1, bt, bf, bp);
+        // stored rows: live rows of full groups, the first row of flat groups
+        if ((kind == 2 && e >= lo && e <= hi) || kind == 1) {
+            double spf[KT], sms[KT], spk[KT];
+#pragma unroll
+            for (int kk = 0; kk < KT; ++kk) {
+                spf[kk] = 0.0; sms[kk] = 0.0; spk[kk] = 0.0;
+                if (!FIRST && (!GUARD || kk < K) && bt[kk] < GBMW_STEP_INF)
+                    load_state(a, sh, u, e, bp[kk], spf[kk], sms[kk], spk[kk]);
+            }
+#pragma unroll
+            for (int kk = 0; kk < KT; ++kk)
+                if (!GUARD || kk < K) {
+                    reinterpret_cast<double2 *>(bout)[kk * n_e + e] = make_double2(bt[kk], bf[kk]);
+                    pout[kk * n_e + e] = (uint16_t)sh.idx[bp[kk]];
+                    if (bt[kk] < GBMW_STEP_INF) {
+                        fold_state(sh, bp[kk], spf[kk], sms[kk], spk[kk]);
+                        PathState *dst = psout + (int64_t)kk * n_e + e;
+                        reinterpret_cast<double2 *>(dst)[0] = make_double2(spf[kk], sms[kk]);
+                        reinterpret_cast<double2 *>(dst)[1] = make_double2(spk[kk], 0.0);
+                    }
+                }
+        }
+        // change bits inside full groups (a full group is exactly one warp of this pass)
+        const bool in_np = (pass * nthr + warp * 32) < 32 * n_np;
 #pragma unroll
         for (int kk = 0; kk < KT; ++kk) {
             if (GUARD && kk >= K) break;
-            if (lane == kk && wi < sh.nw) {
-                const bool same = pt[kk] == sh.wt[warp][kk] && pf[kk] == sh.wf[warp][kk];
-                fout[(int64_t)kk * sh.nw + wi] = sh.wm[warp][kk] | (same ? 0u : 1u);
+            if (in_np) {
+                const double pt = __shfl_up_sync(0xffffffffu, bt[kk], 1);
+                const double pf = __shfl_up_sync(0xffffffffu, bf[kk], 1);
+                const bool chg = lane > 0 && (pt != bt[kk] || pf != bf[kk]);
+                const unsigned m = __ballot_sync(0xffffffffu, chg);
+                if (lane == 0) { sh.bits[g][kk] = m; sh.first_t[g][kk] = bt[kk]; sh.first_f[g][kk] = bf[kk]; }
+                if (lane == 31) { sh.last_t[g][kk] = bt[kk]; sh.last_f[g][kk] = bf[kk]; }
+            } else if (kind == 1) {
+                sh.bits[g][kk] = 0u;
+                sh.first_t[g][kk] = sh.last_t[g][kk] = bt[kk];
+                sh.first_f[g][kk] = sh.last_f[g][kk] = bf[kk];
+            } else if (kind == 3) {
+                sh.prev_t[kk] = bt[kk];
+                sh.prev_f[kk] = bf[kk];
             }
         }
-    } else if (wi < sh.nw) {
-        for (int kk = lane; kk < K; kk += 32) fout[(int64_t)kk * sh.nw + wi] = sh.wm[warp][kk] | (ext ? 0u : 1u);
+        if (kind == 3) sh.prev_ok = (e >= lo && e <= hi) ? 1 : 0;
     }
-    __syncwarp();
-    return rows;
-}
-
-template <int KT, bool FIRST, bool GUARD, class SH>
-__device__ void step_tile(const ChunkArgs &a, SH &sh, int u, int first_row, unsigned long long &stat_rows) {
-    const int lane = threadIdx.x & 31;
-    while (true) {
-        int g = 0;
-        if (lane == 0) g = atomicAdd(&sh.gnext, 1);
-        g = __shfl_sync(0xffffffffu, g, 0);
-        if (g >= kGroups) break;
-        const int rows = step_group<KT, FIRST, GUARD>(a, sh, u, first_row + 32 * g, g, lane);
-        stat_rows += (unsigned long long)rows * (unsigned long long)(GUARD ? sh.K : KT);
+    __syncthreads();
+    // ---- 3a. flat groups store their first row only (written above); readers redirect the
+    // other rows to it through the group mask (flat_row)
+    if (tid < kGroups / 32) {
+        unsigned m = 0u;
+        for (int b = 0; b < 32; ++b) m |= (sh.kind[32 * tid + b] == 1 ? 1u : 0u) << b;
+        const int wi = (first_row >> 10) + tid;
+        if (wi < sh.gw) a.gflat[sh.gf_cur + wi] = m;
     }
+    // ---- 3b. change-bit words of B_u (bit 0 of a group compares with the previous row)
+    uint32_t *fout = a.chg[u & 1] + sh.f_off;
+    const int w_first = first_row >> 5;
+    for (int x = tid; x < kGroups * K; x += nthr) {
+        const int g = x / K, kk = x - g * K;
+        const int wi = w_first + g;
+        if (wi >= sh.nw) continue;
+        unsigned word;
+        if (sh.kind[g] == 0) {
+            word = 0xffffffffu;                              // dead rows: never read as flat
+        } else {
+            word = sh.bits[g][kk];
+            bool same;
+            if (g == 0) same = sh.prev_ok && sh.prev_t[kk] == sh.first_t[0][kk] && sh.prev_f[kk] == sh.first_f[0][kk];
+            else same = sh.kind[g - 1] != 0 && sh.last_t[g - 1][kk] == sh.first_t[g][kk] &&
+                        sh.last_f[g - 1][kk] == sh.first_f[g][kk];
+            if (!same) word |= 1u;
+        }
+        fout[(int64_t)kk * sh.nw + wi] = word;
+    }
+    __syncthreads();
 }
 
 template <int GROUP, bool FIRST>
@@ -279,7 +318,7 @@ __global__ void __launch_bounds__(kStepThreads, GROUP == 0 ? 3 : 2) k_dp_step(Ch
     using SH = StepShared<GROUP == 0 ? 4 : (GROUP == 1 ? 8 : kMaxClasses)>;
     SH &sh = *reinterpret_cast<SH *>(smem_raw);
     int q_prev = -1;
-    unsigned long long stat_rows = 0;
+    if (threadIdx.x == 0) sh.stat_rows = 0;
     while (true) {
         __syncthreads();
         if (threadIdx.x == 0) sh.next = (int64_t)atomicAdd(counter, 1ull);
@@ -293,64 +332,58 @@ __global__ void __launch_bounds__(kStepThreads, GROUP == 0 ? 3 : 2) k_dp_step(Ch
         const int lo = a.unit_lo[p.ustate_off + u], hi = a.unit_hi[p.ustate_off + u];
         if (first_row > hi || first_row + kStepRows - 1 < lo) continue;      // dead tile (CTA-uniform)
         if (q != q_prev) {
+            __syncthreads();
             const int S = p.S, K = p.K;
             const Cell *prev_cells = a.cells + p.cell_off + (int64_t)(u - 1) * S;
             const int32_t *ul = a.uniq + p.cell_off + (int64_t)(u - 1) * S;
             const int nu = a.nuniq[p.ustate_off + u - 1];
+            const CellMem *prev_mem = a.cmem + p.cell_off + (int64_t)(u - 1) * S;
             for (int n = threadIdx.x; n < nu; n += blockDim.x) {
                 const int j = ul[n];
                 sh.cell[n] = prev_cells[j];
                 sh.idx[n] = j;
+                sh.mem[n] = prev_mem[j];
             }
             const double *r_u = a.rcls + p.r_off + (int64_t)u * K * K;
             for (int x = threadIdx.x; x < K * K; x += blockDim.x) sh.r[x] = r_u[x];
-            const int gw = (int)gflat_words(p.n_b + 1);
             if (!FIRST) {
+                const int gw = (int)gflat_words(p.n_b + 1);
                 const uint32_t *gsrc = a.gflat + p.gflat_off + (int64_t)(u - 2) * gw;
                 for (int x = threadIdx.x; x < gw; x += blockDim.x) sh.gfp[x] = gsrc[x];
             }
             if (threadIdx.x == 0) {
-                sh.S = nu; sh.K = K; sh.n_e = (int)(p.n_b + 1);
+                sh.S = nu; sh.K = K; sh.n_e = (int)(p.n_b + 1); sh.q = q;
+                sh.cnt_prev = a.unit_count[p.unit_off + u - 1];
                 sh.lo_prev = a.unit_lo[p.ustate_off + u - 1];
                 sh.lo = lo; sh.hi = hi;
-                sh.b_off = p.b_off; sh.par_off = p.par_off;
+                sh.b_off = p.b_off; sh.par_off = p.par_off; sh.tile0 = a.step_tiles[q];
                 sh.f_off = p.flag_off; sh.nw = (int)flag_words(p.n_b + 1);
-                sh.gw = gw;
-                sh.gf_cur = p.gflat_off + (int64_t)(u - 1) * gw;
+                sh.gw = (int)gflat_words(p.n_b + 1);
+                sh.gf_cur = p.gflat_off + (int64_t)(u - 1) * sh.gw;
             }
+            __syncthreads();
             q_prev = q;
         }
-        if (threadIdx.x < kGroups / 32) sh.gmask[threadIdx.x] = 0u;
-        if (threadIdx.x == 0) sh.gnext = 0;
-        __syncthreads();
         const int K = sh.K;
         if (GROUP == 0) {
             switch (K) {
-                case 1: step_tile<1, FIRST, false>(a, sh, u, (int)first_row, stat_rows); break;
-                case 2: step_tile<2, FIRST, false>(a, sh, u, (int)first_row, stat_rows); break;
-                case 3: step_tile<3, FIRST, false>(a, sh, u, (int)first_row, stat_rows); break;
-                default: step_tile<4, FIRST, false>(a, sh, u, (int)first_row, stat_rows); break;
+                case 1: step_tile<1, FIRST, false>(a, sh, u, (int)first_row); break;
+                case 2: step_tile<2, FIRST, false>(a, sh, u, (int)first_row); break;
+                case 3: step_tile<3, FIRST, false>(a, sh, u, (int)first_row); break;
+                default: step_tile<4, FIRST, false>(a, sh, u, (int)first_row); break;
             }
         } else if (GROUP == 1) {
             switch (K) {
-                case 5: step_tile<5, FIRST, false>(a, sh, u, (int)first_row, stat_rows); break;
-                case 6: step_tile<6, FIRST, false>(a, sh, u, (int)first_row, stat_rows); break;
-                case 7: step_tile<7, FIRST, false>(a, sh, u, (int)first_row, stat_rows); break;
-                default: step_tile<8, FIRST, false>(a, sh, u, (int)first_row, stat_rows); break;
+                case 5: step_tile<5, FIRST, false>(a, sh, u, (int)first_row); break;
+                case 6: step_tile<6, FIRST, false>(a, sh, u, (int)first_row); break;
+                case 7: step_tile<7, FIRST, false>(a, sh, u, (int)first_row); break;
+                default: step_tile<8, FIRST, false>(a, sh, u, (int)first_row); break;
             }
         } else {
-            step_tile<kMaxClasses, FIRST, true>(a, sh, u, (int)first_row, stat_rows);
-        }
-        __syncthreads();
-        // flat-group mask words of this tile (tiles are 1024-row-word aligned)
-        if (threadIdx.x < kGroups / 32) {
-            const int wi = (int)(first_row >> 10) + threadIdx.x;
-            if (wi < sh.gw) a.gflat[sh.gf_cur + wi] = sh.gmask[threadIdx.x];
+            step_tile<kMaxClasses, FIRST, true>(a, sh, u, (int)first_row);
         }
     }
-    // work counter: one atomic per warp
-    for (int off = 16; off > 0; off >>= 1) stat_rows += __shfl_xor_sync(0xffffffffu, stat_rows, off);
-    if ((threadIdx.x & 31) == 0 && stat_rows) atomicAdd(a.computed_cells, stat_rows);
+    if (threadIdx.x == 0 && sh.stat_rows) atomicAdd(a.computed_cells, sh.stat_rows);
 }
 
 int launch_dp_step(const ChunkArgs &a, int group, int u, int64_t tile_base, int64_t n_tiles,
