@@ -316,7 +316,7 @@ extern "C" int gbmw_ctx_create(int32_t device, uint64_t workspace_bytes, gbmw_ct
     if (workspace_bytes == 0) {
         size_t fr = 0, tot = 0;
         cudaMemGetInfo(&fr, &tot);
-        workspace_bytes = std::min<uint64_t>((uint64_t)(fr * 0.4), 32ull << 30);
+        workspace_bytes = std::min<uint64_t>((uint64_t)(fr * 0.6), 120ull << 30);
         if (workspace_bytes < (64ull << 20)) workspace_bytes = 64ull << 20;
     }
     c->workspace_limit = workspace_bytes;
@@ -470,7 +470,8 @@ size_t put(std::vector<char> &blob, const T *src, size_t n) {
 
 // chunk workspace layout (byte offsets from ws base)
 struct WsLayout {
-    size_t cells, cmem, rcls, bup, tf0, tf1, ps0, ps1, chg0, chg1, gflat, par, parts, bestp, bound, ufirst, uprefix, uctr, uniq, nuniq,
+    size_t cells, cmem, rcls, bup, tf0, tf1, ps0, ps1, chg0, chg1, gflat, par, parts, bestp, bound, ufirst, usorted, uprefix, uctr,
+        uniq, nuniq,
         ulo, uhi, ctr, total;
 };
 WsLayout ws_layout(const Chunk &c) {
@@ -492,7 +493,8 @@ WsLayout ws_layout(const Chunk &c) {
     w.bestp = o; o = align_up(o + c.probs.size() * sizeof(SweepPartial));
     w.bound = o; o = align_up(o + c.probs.size() * 16);
     w.ufirst = o; o = align_up(o + c.probs.size() * 4);
-    w.uprefix = o; o = align_up(o + (c.probs.size() + 1) * 8);
+    w.usorted = o; o = align_up(o + c.probs.size() * 4);
+    w.uprefix = o; o = align_up(o + (kMaxSweepRanks + 1) * 8);
     w.uctr = o; o = align_up(o + 8);
     w.uniq = o; o = align_up(o + c.n_cells * 4);
     w.nuniq = o; o = align_up(o + c.n_units * 4);
@@ -783,6 +785,7 @@ ChunkArgs chunk_args(gbmw_batch *b, const Chunk &c, char *ws, size_t chunk_index
     a.best = (SweepPartial *)(ws + w.bestp);
     a.bound = (unsigned long long *)(ws + w.bound);
     a.ufirst = (int32_t *)(ws + w.ufirst);
+    a.usorted = (int32_t *)(ws + w.usorted);
     a.uprefix = (int64_t *)(ws + w.uprefix);
     a.ucounter = (unsigned long long *)(ws + w.uctr);
     a.uniq = (int32_t *)(ws + w.uniq);

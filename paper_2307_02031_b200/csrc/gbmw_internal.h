@@ -36,6 +36,7 @@ __host__ __device__
 #endif
 inline int64_t gflat_words(int64_t n_e) { return ((n_e + 31) / 32 + 31) / 32 + 1; }
 constexpr int kSweepThreads = 256;   // rows per K3 tile
+constexpr int kMaxSweepRanks = 4096; // >= sweep tiles of one problem: ceil(GBMW_MAX_BUCKETS / kSweepThreads)
 
 // K2 is instantiated per class-count group so a problem with few classes does not
 // pay the register footprint of the widest one: K <= 4, 5..8, 9..kMaxClasses.
@@ -158,7 +159,8 @@ struct ChunkArgs {
     SweepPartial *best;           // per problem: best safe bucket (K3a)
     unsigned long long *bound;    // per problem, 16 B: running best {bits of t, e + 1} of the sweep (K3a, K3b)
     int32_t *ufirst;              // per problem: first sweep tile holding unsafe rows
-    int64_t *uprefix;             // n_probs + 1: exclusive prefix of unsafe tiles (K3b work list)
+    int32_t *usorted;             // problems with unsafe tiles, by unsafe tile count descending
+    int64_t *uprefix;             // kMaxSweepRanks + 1: K3b items before rank r (rank = tile from the top)
     unsigned long long *ucounter; // K3b work counter
     int32_t *uniq;                // per (unit, slot): strategy indices with distinct (w, k, c, ef), ascending
     int32_t *nuniq;               // per unit: number of distinct strategies

@@ -157,6 +157,7 @@ struct RowCtx {
     const int32_t *w; const int32_t *k; const double *c; const double *ef;
     const TFCell *bin;
     const uint32_t *gf;  // flat-group mask of B_{U-1} (rows of flat groups are stored once)
+    const uint32_t *gfs; // the same mask staged in shared memory, or nullptr
     int64_t n_e;
     int64_t lo;        // rows of B_{U-1} below L_{U-1} are +inf (never written)
     bool init;
@@ -166,7 +167,14 @@ __device__ __forceinline__ void row_value(const RowCtx &r, int64_t e, int j, dou
     const int w = r.w[j];
     if (e - w < r.lo) { T = GBMW_INF; F = GBMW_INF; return; }
     if (r.init) { T = r.c[j]; F = r.ef[j]; return; }
-    const int64_t src = (int64_t)r.k[j] * r.n_e + flat_row(r.gf, (int)(e - w));
+    int row;
+    if (r.gfs) {
+        const int x = (int)(e - w), g = x >> 5;
+        row = ((r.gfs[g >> 5] >> (g & 31)) & 1u) ? (x & ~31) : x;
+    } else {
+        row = flat_row(r.gf, (int)(e - w));
+    }
+    const int64_t src = (int64_t)r.k[j] * r.n_e + row;
     const double2 v = __ldg(reinterpret_cast<const double2 *>(r.bin + src));
     T = v.x + r.c[j];
     F = v.y + r.ef[j];
@@ -384,29 +392,86 @@ __global__ void k_sweep_safe(ChunkArgs a) {
     }
 }
 
-// Exclusive prefix of the unsafe tile counts over the chunk's problems (one CTA of 1024).
+// K3b work list (one CTA of 1024): items are (rank, problem), rank r = r-th unsafe tile
+// of the problem from the top, ordered rank-major so that every problem's highest (lowest
+// time) tiles run first and tighten its bound before its lower tiles start.  Problems are
+// counting-sorted by unsafe tile count n_q, descending: the problems with n_q > r are
+// then the first cnt_gt[r] of usorted, and uprefix[r] = sum_{r' < r} cnt_gt[r'].
+__device__ __forceinline__ int unsafe_tiles(const ChunkArgs &a, int q) {
+    const DevProblem &p = a.probs[q];
+    return (p.flags & GBMW_APPROX) ? 0 : p.n_sweep_tiles - a.ufirst[q];
+}
+
 __global__ void __launch_bounds__(1024) k_sweep_scan(ChunkArgs a) {
-    __shared__ long long s_sum[1024];
+    __shared__ int s_cnt[kMaxSweepRanks + 1];       // histogram of n_q, then slots
+    __shared__ long long s_part[1024];
+    constexpr int kPer = (kMaxSweepRanks + 1023) / 1024;
     const int n = a.n_probs, tid = threadIdx.x;
-    const int per = (n + 1023) / 1024;
-    const int b0 = min(n, tid * per), b1 = min(n, b0 + per);
-    long long s = 0;
-    for (int q = b0; q < b1; ++q)
-        if (!(a.probs[q].flags & GBMW_APPROX)) s += a.probs[q].n_sweep_tiles - a.ufirst[q];
-    s_sum[tid] = s;
+    for (int m = tid; m <= kMaxSweepRanks; m += 1024) s_cnt[m] = 0;
+    __syncthreads();
+    for (int q = tid; q < n; q += 1024) {
+        const int c = unsafe_tiles(a, q);
+        if (c > 0) atomicAdd(&s_cnt[c], 1);
+    }
+    __syncthreads();
+    // cnt_gt[r] = #{q : n_q > r} = sum of hist over (r, kMaxSweepRanks]: suffix scan, kPer bins per thread
+    int loc[kPer];
+    long long sum = 0;
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+        const int m = tid * kPer + i + 1;                // hist bin m contributes to cnt_gt[r] for r < m
+        loc[i] = (m <= kMaxSweepRanks) ? s_cnt[m] : 0;
+        sum += loc[i];
+    }
+    s_part[tid] = sum;
+    __syncthreads();
+    for (int off = 1; off < 1024; off <<= 1) {          // inclusive suffix scan of thread sums
+        const long long v = (tid + off < 1024) ? s_part[tid + off] : 0;
+        __syncthreads();
+        s_part[tid] += v;
+        __syncthreads();
+    }
+    int gt[kPer];
+    {
+        long long run = (tid + 1 < 1024) ? s_part[tid + 1] : 0;   // bins above this thread's range
+        for (int i = kPer - 1; i >= 0; --i) {
+            run += loc[i];
+            gt[i] = (int)run;                             // cnt_gt[tid * kPer + i]
+        }
+    }
+    // rank prefix: uprefix[r] = sum_{r' < r} cnt_gt[r'] (exclusive scan over r)
+    long long rs = 0;
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) rs += gt[i];
+    __syncthreads();
+    s_part[tid] = rs;
     __syncthreads();
     for (int off = 1; off < 1024; off <<= 1) {
-        const long long v = (tid >= off) ? s_sum[tid - off] : 0;
+        const long long v = (tid >= off) ? s_part[tid - off] : 0;
         __syncthreads();
-        s_sum[tid] += v;
+        s_part[tid] += v;
         __syncthreads();
     }
-    long long run = s_sum[tid] - s;
-    for (int q = b0; q < b1; ++q) {
-        a.uprefix[q] = run;
-        if (!(a.probs[q].flags & GBMW_APPROX)) run += a.probs[q].n_sweep_tiles - a.ufirst[q];
+    long long run = s_part[tid] - rs;
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+        const int r = tid * kPer + i;
+        if (r <= kMaxSweepRanks) a.uprefix[r] = run;
+        run += gt[i];
     }
-    if (tid == 1023) a.uprefix[n] = s_sum[1023];
+    if (tid == 1023) a.uprefix[kMaxSweepRanks] = run;
+    // slots of the descending counting sort: bin m starts at cnt_gt[m] (problems with n_q > m)
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+        const int r = tid * kPer + i;
+        if (r <= kMaxSweepRanks) s_cnt[r] = gt[i];
+    }
+    __syncthreads();
+    for (int q = tid; q < n; q += 1024) {
+        const int c = unsafe_tiles(a, q);
+        if (c > 0) a.usorted[atomicAdd(&s_cnt[c], 1)] = q;
+    }
     if (tid == 0) *a.ucounter = 0ull;
 }
 
@@ -429,8 +494,10 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
     __shared__ double sOF[kMaxStrats];                  // O_f, O_b, O_ms of one layer of the last unit
     __shared__ double sOB[kMaxStrats];
     __shared__ double sOM[kMaxStrats];
+    __shared__ uint32_t sGF[(GBMW_MAX_BUCKETS + 1 + 1023) / 1024 + 2];   // flat-group mask of B_{U-1}
     __shared__ long long s_next;
-    const long long total = a.uprefix[a.n_probs];
+    __shared__ int s_skip;
+    const long long total = a.uprefix[kMaxSweepRanks];
     const int lane = threadIdx.x & 31;
     int q_prev = -1;
     unsigned long long n_rows = 0, n_cands = 0, n_checks = 0;
@@ -440,9 +507,10 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
         __syncthreads();
         const long long g = s_next;
         if (g >= total) break;
-        const int q = find_slot(a.uprefix, a.n_probs, g);
+        const int rank = find_slot(a.uprefix, kMaxSweepRanks, g);
+        const int q = a.usorted[g - a.uprefix[rank]];
         const DevProblem &p = a.probs[q];
-        const int tile = p.n_sweep_tiles - 1 - (int)(g - a.uprefix[q]);
+        const int tile = p.n_sweep_tiles - 1 - rank;
         const int S = p.S;
         const int last = p.U - 1;
         if (q != q_prev) {
@@ -453,6 +521,11 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
                 sW[i] = c.w; sK[i] = c.k; sC[i] = c.c; sE[i] = c.ef;
                 const CellMem m = lm[i];
                 sOF[i] = m.o_f; sOB[i] = m.o_b; sOM[i] = m.o_ms;
+            }
+            if (last >= 1) {
+                const int gw = (int)gflat_words(p.n_b + 1);
+                const uint32_t *gsrc = a.gflat + p.gflat_off + (int64_t)(last - 1) * gw;
+                for (int x = threadIdx.x; x < gw; x += blockDim.x) sGF[x] = gsrc[x];
             }
             __syncthreads();
             q_prev = q;
@@ -465,8 +538,36 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
         r.lo = (last == 0) ? 0 : a.unit_lo[p.ustate_off + last];
         r.bin = a.TF[last & 1] + p.b_off;
         r.gf = a.gflat + p.gflat_off + (int64_t)(last >= 1 ? last - 1 : 0) * gflat_words(p.n_b + 1);
+        r.gfs = sGF;
         unsigned long long *bound = a.bound + 2 * q;
         const int64_t e = 1 + (int64_t)tile * kSweepThreads + threadIdx.x;
+        // whole-tile prune: every candidate of the tile has T >= t0(top row) (the rank-0 time
+        // is non-increasing in e), so the tile cannot win if t0(top) loses to the bound
+        if (threadIdx.x < 32) {
+            const int64_t e_top = min((int64_t)tile * kSweepThreads + kSweepThreads, p.n_b);
+            double tmin = GBMW_INF;
+            for (int j = lane; j < S; j += 32) {
+                double T, F;
+                row_value(r, e_top, j, T, F);
+                tmin = fmin(tmin, T);
+            }
+            for (int off = 16; off > 0; off >>= 1) tmin = fmin(tmin, __shfl_xor_sync(0xffffffffu, tmin, off));
+            if (lane == 0) {
+                double bt;
+                int64_t be;
+                bound_read(bound, bt, be);
+                s_skip = !(tmin < GBMW_INF) || tmin > bt || (tmin == bt && e_top < be);
+            }
+        }
+        __syncthreads();
+        if (s_skip) {
+            if (threadIdx.x == 0) {
+                SweepPartial none;
+                none.t = GBMW_INF; none.e = -1; none.j = 0; none.pad_ = 0;
+                a.partials[p.tile_off + tile] = none;
+            }
+            continue;
+        }
         // flat warp: the candidate order is the same in all its rows; read the row values
         // at the warp's first row (broadcast).  Walks stay per row.
         const int64_t e_w0 = e - lane;
@@ -520,8 +621,9 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
                 // last unit (costs.py:307-318 in layer order; K2 carries the state)
                 double pf = 0.0, ms = 0.0, peak = 0.0;
                 if (last > 0) {
-                    const int64_t src = e - sW[nj];
-                    const PathState *ps = ps_in + (int64_t)sK[nj] * r.n_e + flat_row(r.gf, (int)src);
+                    const int src = (int)(e - sW[nj]), sg = src >> 5;
+                    const int row = ((sGF[sg >> 5] >> (sg & 31)) & 1u) ? (src & ~31) : src;
+                    const PathState *ps = ps_in + (int64_t)sK[nj] * r.n_e + row;
                     const double2 v0 = __ldg(reinterpret_cast<const double2 *>(ps));
                     pf = v0.x; ms = v0.y;
                     peak = __ldg(&ps->peak);
@@ -630,6 +732,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_rows(ChunkArgs a) {
     r.lo = (last == 0) ? 0 : a.unit_lo[p.ustate_off + last];
     r.bin = a.TF[last & 1] + p.b_off;
     r.gf = a.gflat + p.gflat_off + (int64_t)(last >= 1 ? last - 1 : 0) * gflat_words(p.n_b + 1);
+    r.gfs = nullptr;
     if (e <= p.n_b) {
         double t0 = GBMW_INF, f0 = GBMW_INF;
         int j0 = -1;

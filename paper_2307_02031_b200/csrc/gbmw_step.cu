@@ -53,6 +53,9 @@ struct StepShared {
     unsigned bits[kGroups][KM];
     double first_t[kGroups][KM], first_f[kGroups][KM];
     double last_t[kGroups][KM], last_f[kGroups][KM];
+    int first_p[kGroups][KM], last_p[kGroups][KM];
+    unsigned first_pc[kGroups];             // bit kk: the first row's path differs below its argmin
+    int prev_p[KM];
     double prev_t[KM], prev_f[KM];
     int prev_ok;
     unsigned long long stat_rows;
@@ -122,6 +125,18 @@ __device__ __forceinline__ void load_state(const ChunkArgs &a, const SH &sh, int
     const double2 v0 = __ldg(reinterpret_cast<const double2 *>(ps));
     pf = v0.x; ms = v0.y;
     peak = __ldg(&ps->peak);
+}
+
+// Path-change bit of row e with argmin source n: the source cell B_{u-1}[e - w_n] differs
+// (in value, argmin or path) from B_{u-1}[e - 1 - w_n].  Rows of B_u are "equal" (no change
+// bit) only when value, argmin and the whole path behind match, so a flat group's first
+// row stands for every row of the group, argmin chain included.
+template <class SH>
+__device__ __forceinline__ unsigned src_path_change(const ChunkArgs &a, const SH &sh, int u, int e, int n) {
+    const Cell c = sh.cell[n];
+    const int src = e - c.w;
+    const uint32_t *fl = a.chg[(u - 1) & 1] + sh.f_off + (int64_t)c.k * sh.nw;
+    return (__ldg(fl + (src >> 5)) >> (src & 31)) & 1u;
 }
 
 template <class SH>
@@ -233,16 +248,22 @@ __device__ void step_tile(const ChunkArgs &a, SH &sh, int u, int first_row) {
         } else if (x == 32 * n_np + n_fl) {
             e = first_row - 1; kind = 3;
         }
-        relax_row<KT, FIRST, GUARD>(a, sh, u, (kind >= 0 && e >= lo && e <= hi && e < n_e) ? e : -1, bt, bf, bp);
-        // stored rows: live rows of full groups, the first row of flat groups
-        if ((kind == 2 && e >= lo && e <= hi) || kind == 1) {
-            double spf[KT], sms[KT], spk[KT];
+        const bool row_live = kind >= 0 && e >= lo && e <= hi && e < n_e;
+        relax_row<KT, FIRST, GUARD>(a, sh, u, row_live ? e : -1, bt, bf, bp);
+        // per class: source path-change bit, and the path state of stored rows (live rows of
+        // full groups, the first row of flat groups); all loads issued before use
+        const bool stored = row_live && (kind == 2 || kind == 1);
+        unsigned pcm = 0u;
+        double spf[KT], sms[KT], spk[KT];
 #pragma unroll
-            for (int kk = 0; kk < KT; ++kk) {
-                spf[kk] = 0.0; sms[kk] = 0.0; spk[kk] = 0.0;
-                if (!FIRST && (!GUARD || kk < K) && bt[kk] < GBMW_STEP_INF)
-                    load_state(a, sh, u, e, bp[kk], spf[kk], sms[kk], spk[kk]);
+        for (int kk = 0; kk < KT; ++kk) {
+            spf[kk] = 0.0; sms[kk] = 0.0; spk[kk] = 0.0;
+            if (!FIRST && (!GUARD || kk < K) && row_live && bt[kk] < GBMW_STEP_INF) {
+                pcm |= src_path_change(a, sh, u, e, bp[kk]) << kk;
+                if (stored) load_state(a, sh, u, e, bp[kk], spf[kk], sms[kk], spk[kk]);
             }
+        }
+        if (stored) {
 #pragma unroll
             for (int kk = 0; kk < KT; ++kk)
                 if (!GUARD || kk < K) {
@@ -264,19 +285,26 @@ __device__ void step_tile(const ChunkArgs &a, SH &sh, int u, int first_row) {
             if (in_np) {
                 const double pt = __shfl_up_sync(0xffffffffu, bt[kk], 1);
                 const double pf = __shfl_up_sync(0xffffffffu, bf[kk], 1);
-                const bool chg = lane > 0 && (pt != bt[kk] || pf != bf[kk]);
+                const int pp = __shfl_up_sync(0xffffffffu, bp[kk], 1);
+                const bool chg = lane > 0 && (pt != bt[kk] || pf != bf[kk] || pp != bp[kk] || ((pcm >> kk) & 1u));
                 const unsigned m = __ballot_sync(0xffffffffu, chg);
-                if (lane == 0) { sh.bits[g][kk] = m; sh.first_t[g][kk] = bt[kk]; sh.first_f[g][kk] = bf[kk]; }
-                if (lane == 31) { sh.last_t[g][kk] = bt[kk]; sh.last_f[g][kk] = bf[kk]; }
+                if (lane == 0) {
+                    sh.bits[g][kk] = m;
+                    sh.first_t[g][kk] = bt[kk]; sh.first_f[g][kk] = bf[kk]; sh.first_p[g][kk] = bp[kk];
+                }
+                if (lane == 31) { sh.last_t[g][kk] = bt[kk]; sh.last_f[g][kk] = bf[kk]; sh.last_p[g][kk] = bp[kk]; }
             } else if (kind == 1) {
                 sh.bits[g][kk] = 0u;
                 sh.first_t[g][kk] = sh.last_t[g][kk] = bt[kk];
                 sh.first_f[g][kk] = sh.last_f[g][kk] = bf[kk];
+                sh.first_p[g][kk] = sh.last_p[g][kk] = bp[kk];
             } else if (kind == 3) {
                 sh.prev_t[kk] = bt[kk];
                 sh.prev_f[kk] = bf[kk];
+                sh.prev_p[kk] = bp[kk];
             }
         }
+        if ((in_np && lane == 0) || kind == 1) sh.first_pc[g] = pcm;
         if (kind == 3) sh.prev_ok = (e >= lo && e <= hi) ? 1 : 0;
     }
     __syncthreads();
@@ -301,9 +329,11 @@ __device__ void step_tile(const ChunkArgs &a, SH &sh, int u, int first_row) {
         } else {
             word = sh.bits[g][kk];
             bool same;
-            if (g == 0) same = sh.prev_ok && sh.prev_t[kk] == sh.first_t[0][kk] && sh.prev_f[kk] == sh.first_f[0][kk];
+            if (g == 0) same = sh.prev_ok && sh.prev_t[kk] == sh.first_t[0][kk] && sh.prev_f[kk] == sh.first_f[0][kk] &&
+                               sh.prev_p[kk] == sh.first_p[0][kk];
             else same = sh.kind[g - 1] != 0 && sh.last_t[g - 1][kk] == sh.first_t[g][kk] &&
-                        sh.last_f[g - 1][kk] == sh.first_f[g][kk];
+                        sh.last_f[g - 1][kk] == sh.first_f[g][kk] && sh.last_p[g - 1][kk] == sh.first_p[g][kk];
+            same = same && !((sh.first_pc[g] >> kk) & 1u);
             if (!same) word |= 1u;
         }
         fout[(int64_t)kk * sh.nw + wi] = word;
