@@ -454,7 +454,7 @@ void prepare_problem(gbmw_batch &b, int pi, std::string *err) {
     h.n_flagw = (!approx && h.U > 1) ? (int64_t)h.K * flag_words(n_e) : 0;
     h.n_gflat = approx ? 0 : (int64_t)(h.U > 1 ? h.U - 1 : 0) * gflat_words(n_e);
     h.ws_bytes = (size_t)h.n_cells * (sizeof(Cell) + sizeof(CellMem) + 4) + (size_t)h.U * 12 + (size_t)h.n_r * 8 + 8 +
-                 (size_t)h.n_bcells * 2 * (sizeof(TFCell) + sizeof(PathState)) + (size_t)h.n_par * 2 +
+                 (size_t)h.n_bcells * 2 * sizeof(TFCell) + (size_t)h.n_par * 2 +
                  (size_t)h.n_tiles * sizeof(SweepPartial) + sizeof(SweepPartial) + 36 + (size_t)h.n_flagw * 8 +
                  (size_t)h.n_gflat * 4;
     h.gpu = true;
@@ -470,7 +470,7 @@ size_t put(std::vector<char> &blob, const T *src, size_t n) {
 
 // chunk workspace layout (byte offsets from ws base)
 struct WsLayout {
-    size_t cells, cmem, rcls, bup, tf0, tf1, ps0, ps1, chg0, chg1, gflat, par, parts, bestp, bound, ufirst, usorted, uprefix, uctr,
+    size_t cells, cmem, rcls, bup, tf0, tf1, chg0, chg1, gflat, par, parts, bestp, bound, ufirst, usorted, uprefix, uctr,
         uniq, nuniq,
         ulo, uhi, ctr, total;
 };
@@ -483,8 +483,6 @@ WsLayout ws_layout(const Chunk &c) {
     w.bup = o; o = align_up(o + c.probs.size() * 8);
     w.tf0 = o; o = align_up(o + c.n_bcells * sizeof(TFCell));
     w.tf1 = o; o = align_up(o + c.n_bcells * sizeof(TFCell));
-    w.ps0 = o; o = align_up(o + c.n_bcells * sizeof(PathState));
-    w.ps1 = o; o = align_up(o + c.n_bcells * sizeof(PathState));
     w.chg0 = o; o = align_up(o + c.n_flagw * 4);
     w.chg1 = o; o = align_up(o + c.n_flagw * 4);
     w.gflat = o; o = align_up(o + c.n_gflat * 4);
@@ -775,8 +773,6 @@ ChunkArgs chunk_args(gbmw_batch *b, const Chunk &c, char *ws, size_t chunk_index
     a.bup = (unsigned long long *)(ws + w.bup);
     a.TF[0] = (TFCell *)(ws + w.tf0);
     a.TF[1] = (TFCell *)(ws + w.tf1);
-    a.PS[0] = (PathState *)(ws + w.ps0);
-    a.PS[1] = (PathState *)(ws + w.ps1);
     a.chg[0] = (uint32_t *)(ws + w.chg0);
     a.chg[1] = (uint32_t *)(ws + w.chg1);
     a.gflat = (uint32_t *)(ws + w.gflat);

@@ -36,6 +36,7 @@ __host__ __device__
 #endif
 inline int64_t gflat_words(int64_t n_e) { return ((n_e + 31) / 32 + 31) / 32 + 1; }
 constexpr int kSweepThreads = 256;   // rows per K3 tile
+constexpr int kSweepWK = 4096;       // (unit, strategy) pairs staged in shared memory by K3b
 constexpr int kMaxSweepRanks = 4096; // >= sweep tiles of one problem: ceil(GBMW_MAX_BUCKETS / kSweepThreads)
 
 // K2 is instantiated per class-count group so a problem with few classes does not
@@ -111,14 +112,6 @@ struct alignas(16) TFCell {
     double f;       // accumulated true forward bytes of its path (tie-break)
 };
 
-// E_all fold state of the path behind a B cell (costs.py:307-318 restated layer by layer):
-// prefix of O_f, running sum of O_ms, running peak of prefix_f + O_b.  Carried through the
-// DP along the argmin chain so the sweep checks a candidate's backward peak without
-// walking the chain: E_all(e, j) = fold(state(B_{U-1}[e - w_j, cls j]), last unit, j).
-struct alignas(16) PathState {
-    double pf, ms, peak, pad_;
-};
-
 struct SweepPartial {
     double t;
     int64_t e;
@@ -150,7 +143,6 @@ struct ChunkArgs {
     double *rcls;
     unsigned long long *bup;      // per problem, bits of max O_b (all >= 0)
     TFCell *TF[2];
-    PathState *PS[2];             // E_all fold state of each B cell (ping-pong with TF)
     uint32_t *chg[2];             // change bits of B_u (ping-pong with TF): bit x = row x != row x-1
     uint32_t *gflat;              // per unit u >= 1: bit g = 32-row group g of B_u is flat (stored once)
     unsigned long long *computed_cells;   // class cells K2 evaluated (rows x K), per chunk

@@ -198,6 +198,28 @@ __device__ __forceinline__ void backtrack(const ChunkArgs &a, const DevProblem &
     }
 }
 
+// Same walk with (weight, class) of every (unit, strategy) staged in shared memory, packed
+// as weight << 4 | class (weight <= n_b + 1 < 2^27): the chain per unit is then one global
+// load (the argmin) instead of three.
+__device__ __forceinline__ void backtrack_wk(const ChunkArgs &a, const DevProblem &p, int64_t e, int j,
+                                             uint16_t *path, const uint32_t *wk, const uint32_t *gfs) {
+    const int U = p.U, S = p.S, K = p.K;
+    const int64_t n_e = p.n_b + 1;
+    const uint16_t *par = a.par + p.par_off;
+    const int gw = (int)gflat_words(n_e);
+    path[U - 1] = (uint16_t)j;
+    for (int u = U - 1; u >= 1; --u) {
+        const uint32_t c = wk[u * S + j];
+        e -= (int64_t)(c >> 4);
+        const int er = (u == U - 1) ? [&] {
+            const int x = (int)e, g = x >> 5;
+            return ((gfs[g >> 5] >> (g & 31)) & 1u) ? (x & ~31) : x;
+        }() : flat_row(a.gflat + p.gflat_off + (int64_t)(u - 1) * gw, (int)e);
+        j = par[((int64_t)(u - 1) * K + (int)(c & 15u)) * n_e + er];
+        path[u - 1] = (uint16_t)j;
+    }
+}
+
 // E_all of the expanded plan in layer order (costs.py:307-318).
 __device__ __forceinline__ double plan_e_all(const ChunkArgs &a, const DevProblem &p, const uint16_t *path) {
     double total_ms = 0.0, prefix_f = 0.0, peak = 0.0;
@@ -491,9 +513,8 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
     __shared__ double red_t[kSweepThreads / 32];
     __shared__ long long red_e[kSweepThreads / 32];
     __shared__ int red_j[kSweepThreads / 32];
-    __shared__ double sOF[kMaxStrats];                  // O_f, O_b, O_ms of one layer of the last unit
-    __shared__ double sOB[kMaxStrats];
-    __shared__ double sOM[kMaxStrats];
+    __shared__ double sOB[kMaxStrats];                  // O_b of one layer of the last unit
+    __shared__ uint32_t sWK[kSweepWK];                  // weight << 4 | class per (unit, strategy)
     __shared__ uint32_t sGF[(GBMW_MAX_BUCKETS + 1 + 1023) / 1024 + 2];   // flat-group mask of B_{U-1}
     __shared__ long long s_next;
     __shared__ int s_skip;
@@ -519,8 +540,12 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
             for (int i = threadIdx.x; i < S; i += blockDim.x) {
                 const Cell c = lc[i];
                 sW[i] = c.w; sK[i] = c.k; sC[i] = c.c; sE[i] = c.ef;
-                const CellMem m = lm[i];
-                sOF[i] = m.o_f; sOB[i] = m.o_b; sOM[i] = m.o_ms;
+                sOB[i] = lm[i].o_b;
+            }
+            if (p.U * S <= kSweepWK) {
+                const Cell *cells = a.cells + p.cell_off;
+                for (int x = threadIdx.x; x < p.U * S; x += blockDim.x)
+                    sWK[x] = ((uint32_t)cells[x].w << 4) | (uint32_t)cells[x].k;
             }
             if (last >= 1) {
                 const int gw = (int)gflat_words(p.n_b + 1);
@@ -586,10 +611,10 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
         double mt = GBMW_INF;
         int64_t me = -1;
         int mj = 0;
-        const int cnt_last = a.unit_count[p.unit_off + last];
-        const PathState *ps_in = a.PS[last & 1] + p.b_off;
+        const bool wk_smem = p.U * S <= kSweepWK;
         if (e <= p.n_b && !int_le_double(e * p.gran, safe_limit)) {
             ++n_rows;
+            uint16_t path[kMaxUnits];
             double ct = 0.0, cf = 0.0;
             int cj = -1;
             while (true) {
@@ -617,23 +642,9 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
                     continue;
                 }
                 ++n_checks;
-                // E_all of the candidate's plan: the path state of its B cell folded over the
-                // last unit (costs.py:307-318 in layer order; K2 carries the state)
-                double pf = 0.0, ms = 0.0, peak = 0.0;
-                if (last > 0) {
-                    const int src = (int)(e - sW[nj]), sg = src >> 5;
-                    const int row = ((sGF[sg >> 5] >> (sg & 31)) & 1u) ? (src & ~31) : src;
-                    const PathState *ps = ps_in + (int64_t)sK[nj] * r.n_e + row;
-                    const double2 v0 = __ldg(reinterpret_cast<const double2 *>(ps));
-                    pf = v0.x; ms = v0.y;
-                    peak = __ldg(&ps->peak);
-                }
-                for (int l = 0; l < cnt_last; ++l) {
-                    ms = ms + sOM[nj];
-                    pf = pf + sOF[nj];
-                    peak = py_max(peak, pf + sOB[nj]);
-                }
-                if (peak + ms <= p.budget) {
+                if (wk_smem) backtrack_wk(a, p, e, nj, path, sWK, sGF);
+                else backtrack(a, p, e, nj, path);
+                if (plan_e_all(a, p, path) <= p.budget) {
                     mt = nt; me = e; mj = nj;
                     bound_offer(bound, nt, e);
                     break;

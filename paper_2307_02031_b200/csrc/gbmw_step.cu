@@ -38,10 +38,9 @@ template <int KM>
 struct StepShared {
     Cell cell[kMaxStrats];                  // distinct source strategies of unit u-1 (ascending)
     int idx[kMaxStrats];                    // their strategy index
-    CellMem mem[kMaxStrats];                // their per-layer O_f, O_b, O_ms (path-state fold)
     double r[KM * KM];
     uint32_t gfp[kMaxGfWords];              // flat-group mask of B_{u-1} (read redirection, flat_row)
-    int S, K, n_e, q, lo_prev, lo, hi, nw, cnt_prev;
+    int S, K, n_e, q, lo_prev, lo, hi, nw;
     int64_t b_off, par_off, tile0, f_off;
     int64_t gf_cur;                         // flat-group mask of B_u (offset into a.gflat)
     int gw;
@@ -111,22 +110,6 @@ __device__ __forceinline__ void relax_row(const ChunkArgs &a, const SH &sh, int 
     }
 }
 
-// Path state of B_u[e] with argmin source n (distinct-list position): the source cell's
-// state (load_state) folded over the layers of unit u-1 with strategy n, in plan_e_all's
-// order (fold_state).
-template <class SH>
-__device__ __forceinline__ void load_state(const ChunkArgs &a, const SH &sh, int u, int e, int n, double &pf,
-                                           double &ms, double &peak) {
-    const Cell c = sh.cell[n];
-    const int src = e - c.w;
-    const int g = src >> 5;
-    const int rs = ((sh.gfp[g >> 5] >> (g & 31)) & 1u) ? (src & ~31) : src;
-    const PathState *ps = a.PS[(u - 1) & 1] + sh.b_off + (int64_t)c.k * sh.n_e + rs;
-    const double2 v0 = __ldg(reinterpret_cast<const double2 *>(ps));
-    pf = v0.x; ms = v0.y;
-    peak = __ldg(&ps->peak);
-}
-
 // Path-change bit of row e with argmin source n: the source cell B_{u-1}[e - w_n] differs
 // (in value, argmin or path) from B_{u-1}[e - 1 - w_n].  Rows of B_u are "equal" (no change
 // bit) only when value, argmin and the whole path behind match, so a flat group's first
@@ -137,17 +120,6 @@ __device__ __forceinline__ unsigned src_path_change(const ChunkArgs &a, const SH
     const int src = e - c.w;
     const uint32_t *fl = a.chg[(u - 1) & 1] + sh.f_off + (int64_t)c.k * sh.nw;
     return (__ldg(fl + (src >> 5)) >> (src & 31)) & 1u;
-}
-
-template <class SH>
-__device__ __forceinline__ void fold_state(const SH &sh, int n, double &pf, double &ms, double &peak) {
-    const CellMem m = sh.mem[n];
-    for (int r = 0; r < sh.cnt_prev; ++r) {
-        ms = ms + m.o_ms;
-        pf = pf + m.o_f;
-        const double x = pf + m.o_b;
-        peak = (x > peak) ? x : peak;                      // Python max(peak, x)
-    }
 }
 
 template <int KT, bool FIRST, bool GUARD, class SH>
@@ -233,7 +205,6 @@ __device__ void step_tile(const ChunkArgs &a, SH &sh, int u, int first_row) {
     const int n_np = sh.n_np, n_fl = sh.n_fl;
     const int n_list = 32 * n_np + n_fl + 1;                // + the row before the tile
     TFCell *bout = a.TF[u & 1] + sh.b_off;
-    PathState *psout = a.PS[u & 1] + sh.b_off;
     uint16_t *pout = a.par + sh.par_off + (int64_t)(u - 1) * K * n_e;
     const int n_pass = (n_list + nthr - 1) / nthr;
     for (int pass = 0; pass < n_pass; ++pass) {
@@ -250,31 +221,19 @@ __device__ void step_tile(const ChunkArgs &a, SH &sh, int u, int first_row) {
         }
         const bool row_live = kind >= 0 && e >= lo && e <= hi && e < n_e;
         relax_row<KT, FIRST, GUARD>(a, sh, u, row_live ? e : -1, bt, bf, bp);
-        // per class: source path-change bit, and the path state of stored rows (live rows of
-        // full groups, the first row of flat groups); all loads issued before use
-        const bool stored = row_live && (kind == 2 || kind == 1);
+        // per class: source path-change bit (all loads issued before use)
         unsigned pcm = 0u;
-        double spf[KT], sms[KT], spk[KT];
 #pragma unroll
-        for (int kk = 0; kk < KT; ++kk) {
-            spf[kk] = 0.0; sms[kk] = 0.0; spk[kk] = 0.0;
-            if (!FIRST && (!GUARD || kk < K) && row_live && bt[kk] < GBMW_STEP_INF) {
+        for (int kk = 0; kk < KT; ++kk)
+            if (!FIRST && (!GUARD || kk < K) && row_live && bt[kk] < GBMW_STEP_INF)
                 pcm |= src_path_change(a, sh, u, e, bp[kk]) << kk;
-                if (stored) load_state(a, sh, u, e, bp[kk], spf[kk], sms[kk], spk[kk]);
-            }
-        }
-        if (stored) {
+        // stored rows: live rows of full groups, the first row of flat groups
+        if (row_live && (kind == 2 || kind == 1)) {
 #pragma unroll
             for (int kk = 0; kk < KT; ++kk)
                 if (!GUARD || kk < K) {
                     reinterpret_cast<double2 *>(bout)[kk * n_e + e] = make_double2(bt[kk], bf[kk]);
                     pout[kk * n_e + e] = (uint16_t)sh.idx[bp[kk]];
-                    if (bt[kk] < GBMW_STEP_INF) {
-                        fold_state(sh, bp[kk], spf[kk], sms[kk], spk[kk]);
-                        PathState *dst = psout + (int64_t)kk * n_e + e;
-                        reinterpret_cast<double2 *>(dst)[0] = make_double2(spf[kk], sms[kk]);
-                        reinterpret_cast<double2 *>(dst)[1] = make_double2(spk[kk], 0.0);
-                    }
                 }
         }
         // change bits inside full groups (a full group is exactly one warp of this pass)
@@ -367,12 +326,10 @@ __global__ void __launch_bounds__(kStepThreads, GROUP == 0 ? 3 : 2) k_dp_step(Ch
             const Cell *prev_cells = a.cells + p.cell_off + (int64_t)(u - 1) * S;
             const int32_t *ul = a.uniq + p.cell_off + (int64_t)(u - 1) * S;
             const int nu = a.nuniq[p.ustate_off + u - 1];
-            const CellMem *prev_mem = a.cmem + p.cell_off + (int64_t)(u - 1) * S;
             for (int n = threadIdx.x; n < nu; n += blockDim.x) {
                 const int j = ul[n];
                 sh.cell[n] = prev_cells[j];
                 sh.idx[n] = j;
-                sh.mem[n] = prev_mem[j];
             }
             const double *r_u = a.rcls + p.r_off + (int64_t)u * K * K;
             for (int x = threadIdx.x; x < K * K; x += blockDim.x) sh.r[x] = r_u[x];
@@ -383,7 +340,6 @@ __global__ void __launch_bounds__(kStepThreads, GROUP == 0 ? 3 : 2) k_dp_step(Ch
             }
             if (threadIdx.x == 0) {
                 sh.S = nu; sh.K = K; sh.n_e = (int)(p.n_b + 1); sh.q = q;
-                sh.cnt_prev = a.unit_count[p.unit_off + u - 1];
                 sh.lo_prev = a.unit_lo[p.ustate_off + u - 1];
                 sh.lo = lo; sh.hi = hi;
                 sh.b_off = p.b_off; sh.par_off = p.par_off; sh.tile0 = a.step_tiles[q];
