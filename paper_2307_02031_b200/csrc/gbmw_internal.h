@@ -21,8 +21,8 @@ namespace gbmw {
 constexpr int kMaxUnits = 1024;      // backtrack path held in local memory
 constexpr int kMaxClasses = 16;
 constexpr int kMaxStrats = 512;      // smem staging of per-strategy constants
-constexpr int kStepThreads = 256;    // threads per K2 CTA
-constexpr int kStepRows = 2048;      // rows per K2 tile (64 groups of 32)
+constexpr int kStepThreads = 128;    // threads per K2 CTA
+constexpr int kStepRows = 1024;      // rows per K2 tile (32 groups of 32, one flat-mask word)
 
 // change-bit words per class column of n_e rows (one spare word for 2-word window reads)
 #if defined(__CUDACC__)

@@ -301,7 +301,7 @@ __device__ void step_tile(const ChunkArgs &a, SH &sh, int u, int first_row) {
 }
 
 template <int GROUP, bool FIRST>
-__global__ void __launch_bounds__(kStepThreads, GROUP == 0 ? 3 : 2) k_dp_step(ChunkArgs a, int u, int64_t tile_base, int64_t n_tiles,
+__global__ void __launch_bounds__(kStepThreads, GROUP == 0 ? 6 : 4) k_dp_step(ChunkArgs a, int u, int64_t tile_base, int64_t n_tiles,
                                                            unsigned long long *counter) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     using SH = StepShared<GROUP == 0 ? 4 : (GROUP == 1 ? 8 : kMaxClasses)>;
