@@ -93,8 +93,11 @@ struct Chunk {
     size_t small_off = 0;          // byte offset of this chunk's descriptor block in the arena
     // offsets inside the descriptor block
     size_t o_probs, o_cellp, o_rp, o_stepp, o_cand, o_ccls, o_clsd, o_clst, o_uf, o_uc;
-    size_t o_stepmap, o_aux;
+    size_t o_stepmap, o_aux, o_slists;
     int64_t n_aux = 0;
+    std::vector<StepList> slists;  // K2 launches (unit, group), in launch order
+    std::vector<int> slist_group;
+    int64_t n_items = 0;           // upper bound of live K2 items over all launches
     size_t small_bytes = 0;
     size_t ws_bytes = 0;
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -456,7 +459,7 @@ void prepare_problem(gbmw_batch &b, int pi, std::string *err) {
     h.ws_bytes = (size_t)h.n_cells * (sizeof(Cell) + sizeof(CellMem) + 4) + (size_t)h.U * 12 + (size_t)h.n_r * 8 + 8 +
                  (size_t)h.n_bcells * 2 * sizeof(TFCell) + (size_t)h.n_par * 2 +
                  (size_t)h.n_tiles * sizeof(SweepPartial) + sizeof(SweepPartial) + 36 + (size_t)h.n_flagw * 8 +
-                 (size_t)h.n_gflat * 4;
+                 (size_t)h.n_gflat * 4 + (size_t)(h.U > 1 ? h.U - 1 : 0) * (h.n_step_tiles * 8 + 8);
     h.gpu = true;
 }
 
@@ -470,7 +473,7 @@ size_t put(std::vector<char> &blob, const T *src, size_t n) {
 
 // chunk workspace layout (byte offsets from ws base)
 struct WsLayout {
-    size_t cells, cmem, rcls, bup, tf0, tf1, chg0, chg1, gflat, par, parts, bestp, bound, ufirst, usorted, uprefix, uctr,
+    size_t cells, cmem, rcls, bup, items, scount, tf0, tf1, chg0, chg1, gflat, par, parts, bestp, bound, ufirst, usorted, uprefix, uctr,
         uniq, nuniq,
         ulo, uhi, ctr, total;
 };
@@ -481,6 +484,8 @@ WsLayout ws_layout(const Chunk &c) {
     w.cmem = o; o = align_up(o + c.n_cells * sizeof(CellMem));
     w.rcls = o; o = align_up(o + c.n_r * 8);
     w.bup = o; o = align_up(o + c.probs.size() * 8);
+    w.items = o; o = align_up(o + c.n_items * sizeof(int2));
+    w.scount = o; o = align_up(o + c.slists.size() * 8);
     w.tf0 = o; o = align_up(o + c.n_bcells * sizeof(TFCell));
     w.tf1 = o; o = align_up(o + c.n_bcells * sizeof(TFCell));
     w.chg0 = o; o = align_up(o + c.n_flagw * 4);
@@ -652,6 +657,19 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
         c.o_uc = put(blob, uc.data(), uc.size()) - base;
         c.o_stepmap = put(blob, stepmap.data(), stepmap.size()) - base;
         c.o_aux = put(blob, aux.data(), aux.size()) - base;
+        // K2 launches: items bounded by all tiles of the active problems
+        c.slists.clear(); c.slist_group.clear(); c.n_items = 0;
+        for (int u = 1; u < c.Umax; ++u)
+            for (int g = 0; g < kStepGroups; ++g) {
+                const int lo = c.group_lo[g], na = c.n_active[g][u];
+                if (na == 0) continue;
+                StepList sl;
+                sl.u = u; sl.lo = lo; sl.n = na; sl.pad_ = 0; sl.base = c.n_items;
+                c.slists.push_back(sl);
+                c.slist_group.push_back(g);
+                c.n_items += c.step_prefix[lo + na] - c.step_prefix[lo];
+            }
+        c.o_slists = put(blob, c.slists.data(), c.slists.size()) - base;
         c.small_bytes = blob.size() - base;
         c.ws_bytes = ws_layout(c).total;
         b->max_ws = std::max(b->max_ws, c.ws_bytes);
@@ -765,12 +783,16 @@ ChunkArgs chunk_args(gbmw_batch *b, const Chunk &c, char *ws, size_t chunk_index
     a.unit_count = (const int32_t *)(sm + c.o_uc);
     a.step_map = (const int32_t *)(sm + c.o_stepmap);
     a.aux_map = (const int2 *)(sm + c.o_aux);
+    a.step_lists = (const StepList *)(sm + c.o_slists);
+    a.n_step_lists = (int32_t)c.slists.size();
     a.n_aux = c.n_aux;
     const WsLayout w = ws_layout(c);
     a.cells = (Cell *)(ws + w.cells);
     a.cmem = (CellMem *)(ws + w.cmem);
     a.rcls = (double *)(ws + w.rcls);
     a.bup = (unsigned long long *)(ws + w.bup);
+    a.step_items = (int2 *)(ws + w.items);
+    a.step_count = (int64_t *)(ws + w.scount);
     a.TF[0] = (TFCell *)(ws + w.tf0);
     a.TF[1] = (TFCell *)(ws + w.tf1);
     a.chg[0] = (uint32_t *)(ws + w.chg0);
@@ -824,15 +846,18 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
         c.launches += (c.n_cells > 0) + (c.n_r > 0) + (c.n_units > 0);
         cudaEventRecord(c.ev[1], st);
         if (tables_only) continue;
-        for (int u = 1; u < c.Umax; ++u) {
-            for (int g = 0; g < kStepGroups; ++g) {
-                const int lo = c.group_lo[g], na = c.n_active[g][u];
-                if (na == 0) continue;
-                const int64_t base = c.step_prefix[lo], n = c.step_prefix[lo + na] - base;
-                if ((rc = launch_dp_step(a, g, u, base, n, a.counters + (size_t)u * kNumGroups + g, st)))
-                    return cuda_fail(ctx, rc, "K2 launch");
-                c.launches += 1;
-            }
+        if (!c.slists.empty()) {
+            if ((rc = launch_step_lists(a, st))) return cuda_fail(ctx, rc, "K2 list launch");
+            c.launches += 1;
+        }
+        for (size_t s = 0; s < c.slists.size(); ++s) {
+            const StepList &sl = c.slists[s];
+            const int g = c.slist_group[s];
+            const int64_t ub = c.step_prefix[sl.lo + sl.n] - c.step_prefix[sl.lo];
+            if ((rc = launch_dp_step(a, g, sl.u, a.step_items + sl.base, a.step_count + s, ub,
+                                     a.counters + (size_t)sl.u * kNumGroups + g, st)))
+                return cuda_fail(ctx, rc, "K2 launch");
+            c.launches += 1;
         }
         // approx_prev problems: collapsed-state layer steps, unit 0 included
         for (int u = 0; u < c.Umax; ++u) {

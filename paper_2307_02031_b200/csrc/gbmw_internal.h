@@ -21,8 +21,8 @@ namespace gbmw {
 constexpr int kMaxUnits = 1024;      // backtrack path held in local memory
 constexpr int kMaxClasses = 16;
 constexpr int kMaxStrats = 512;      // smem staging of per-strategy constants
-constexpr int kStepThreads = 128;    // threads per K2 CTA
-constexpr int kStepRows = 1024;      // rows per K2 tile (32 groups of 32, one flat-mask word)
+constexpr int kStepThreads = 256;    // threads per K2 CTA
+constexpr int kStepRows = 2048;      // rows per K2 tile (64 groups of 32)
 
 // change-bit words per class column of n_e rows (one spare word for 2-word window reads)
 #if defined(__CUDACC__)
@@ -119,6 +119,14 @@ struct SweepPartial {
     int32_t pad_;
 };
 
+// One K2 launch (unit u, class-count group): its problems are [lo, lo + n) in sorted order;
+// k_step_lists writes their live tiles (rows [L_u, H_u] only) as (problem, tile) items at
+// items[base ...] and the item count to step_count[index].
+struct StepList {
+    int32_t u, lo, n, pad_;
+    int64_t base;
+};
+
 // Everything a chunk's kernels read or write (device pointers).
 struct ChunkArgs {
     const gbmw_layer *layers;
@@ -132,6 +140,10 @@ struct ChunkArgs {
     const int64_t *step_tiles;    // n_probs + 1, tiles of ceil(n_e / kStepRows)
     const int32_t *step_map;      // K2 tile -> problem (sorted position)
     const int2 *aux_map;          // K3r tiles: (problem, tile) of frontier / collapsed-DP problems
+    const StepList *step_lists;   // K2 launches of the chunk
+    int32_t n_step_lists;
+    int2 *step_items;             // live (problem, tile) items of every K2 launch
+    int64_t *step_count;          // per K2 launch: number of items
     int64_t n_aux;
     const int32_t *cand_strat;    // global strategy index
     const int32_t *cand_cls;
@@ -168,7 +180,8 @@ struct ChunkArgs {
 
 // launchers (gbmw_kernels.cu); all asynchronous on `stream`, return cudaError_t as int
 int launch_cost_tables(const ChunkArgs &a, int64_t n_cells, int64_t n_r, void *stream);
-int launch_dp_step(const ChunkArgs &a, int group, int u, int64_t tile_base, int64_t n_tiles,
+int launch_step_lists(const ChunkArgs &a, void *stream);
+int launch_dp_step(const ChunkArgs &a, int group, int u, const int2 *items, const int64_t *count, int64_t max_items,
                    unsigned long long *counter, void *stream);
 int launch_sweep(const ChunkArgs &a, void *stream);
 int launch_approx_step(const ChunkArgs &a, int u, int64_t tile_base, int64_t n_tiles, unsigned long long *counter,

@@ -300,26 +300,65 @@ __device__ void step_tile(const ChunkArgs &a, SH &sh, int u, int first_row) {
     __syncthreads();
 }
 
+// Live-tile work lists of every K2 launch of the chunk (one CTA per launch): tiles of the
+// rows [L_u, H_u] of each active problem, so K2 never fetches a dead tile.
+__global__ void __launch_bounds__(1024) k_step_lists(ChunkArgs a) {
+    __shared__ long long s_part[1024];
+    const StepList sl = a.step_lists[blockIdx.x];
+    const int tid = threadIdx.x;
+    const int per = (sl.n + 1023) / 1024;
+    const int x0 = sl.lo + min(sl.n, tid * per), x1 = sl.lo + min(sl.n, tid * per + per);
+    long long cnt = 0;
+    for (int x = x0; x < x1; ++x) {
+        const DevProblem &p = a.probs[x];
+        const int lo = a.unit_lo[p.ustate_off + sl.u], hi = a.unit_hi[p.ustate_off + sl.u];
+        if (hi >= lo) cnt += (hi / kStepRows) - (lo / kStepRows) + 1;
+    }
+    s_part[tid] = cnt;
+    __syncthreads();
+    for (int off = 1; off < 1024; off <<= 1) {
+        const long long v = (tid >= off) ? s_part[tid - off] : 0;
+        __syncthreads();
+        s_part[tid] += v;
+        __syncthreads();
+    }
+    long long at = sl.base + s_part[tid] - cnt;
+    for (int x = x0; x < x1; ++x) {
+        const DevProblem &p = a.probs[x];
+        const int lo = a.unit_lo[p.ustate_off + sl.u], hi = a.unit_hi[p.ustate_off + sl.u];
+        if (hi < lo) continue;
+        for (int t = lo / kStepRows; t <= hi / kStepRows; ++t) a.step_items[at++] = make_int2(x, t);
+    }
+    if (tid == 1023) a.step_count[blockIdx.x] = s_part[1023];
+}
+
+int launch_step_lists(const ChunkArgs &a, void *stream) {
+    if (a.n_step_lists <= 0) return 0;
+    k_step_lists<<<a.n_step_lists, 1024, 0, (cudaStream_t)stream>>>(a);
+    return (int)cudaGetLastError();
+}
+
 template <int GROUP, bool FIRST>
-__global__ void __launch_bounds__(kStepThreads, GROUP == 0 ? 6 : 4) k_dp_step(ChunkArgs a, int u, int64_t tile_base, int64_t n_tiles,
-                                                           unsigned long long *counter) {
+__global__ void __launch_bounds__(kStepThreads, GROUP == 0 ? 3 : 2) k_dp_step(ChunkArgs a, int u, const int2 *items,
+                                                                              const int64_t *count,
+                                                                              unsigned long long *counter) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     using SH = StepShared<GROUP == 0 ? 4 : (GROUP == 1 ? 8 : kMaxClasses)>;
     SH &sh = *reinterpret_cast<SH *>(smem_raw);
     int q_prev = -1;
     if (threadIdx.x == 0) sh.stat_rows = 0;
+    const int64_t n_items = *count;
     while (true) {
         __syncthreads();
         if (threadIdx.x == 0) sh.next = (int64_t)atomicAdd(counter, 1ull);
         __syncthreads();
         const int64_t t = sh.next;
-        if (t >= n_tiles) break;
-        const int64_t tile = tile_base + t;
-        const int q = __ldg(a.step_map + tile);
+        if (t >= n_items) break;
+        const int2 item = __ldg(items + t);
+        const int q = item.x;
         const DevProblem &p = a.probs[q];
-        const int64_t first_row = (tile - a.step_tiles[q]) * kStepRows;
+        const int64_t first_row = (int64_t)item.y * kStepRows;
         const int lo = a.unit_lo[p.ustate_off + u], hi = a.unit_hi[p.ustate_off + u];
-        if (first_row > hi || first_row + kStepRows - 1 < lo) continue;      // dead tile (CTA-uniform)
         if (q != q_prev) {
             __syncthreads();
             const int S = p.S, K = p.K;
@@ -372,7 +411,7 @@ __global__ void __launch_bounds__(kStepThreads, GROUP == 0 ? 6 : 4) k_dp_step(Ch
     if (threadIdx.x == 0 && sh.stat_rows) atomicAdd(a.computed_cells, sh.stat_rows);
 }
 
-int launch_dp_step(const ChunkArgs &a, int group, int u, int64_t tile_base, int64_t n_tiles,
+int launch_dp_step(const ChunkArgs &a, int group, int u, const int2 *items, const int64_t *count, int64_t n_tiles,
                    unsigned long long *counter, void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
     if (n_tiles <= 0) return 0;
@@ -402,8 +441,8 @@ int launch_dp_step(const ChunkArgs &a, int group, int u, int64_t tile_base, int6
     const int64_t max_ctas = (int64_t)sms * occ[group][fi];
     const unsigned grid = (unsigned)(n_tiles < max_ctas ? n_tiles : max_ctas);
 #define GBMW_STEP(G)                                                                                        \
-    if (fi) GBMW_KFN(G, true)<<<grid, kStepThreads, smem, st>>>(a, u, tile_base, n_tiles, counter);          \
-    else GBMW_KFN(G, false)<<<grid, kStepThreads, smem, st>>>(a, u, tile_base, n_tiles, counter);
+    if (fi) GBMW_KFN(G, true)<<<grid, kStepThreads, smem, st>>>(a, u, items, count, counter);                \
+    else GBMW_KFN(G, false)<<<grid, kStepThreads, smem, st>>>(a, u, items, count, counter);
     if (group == 0) { GBMW_STEP(0) }
     else if (group == 1) { GBMW_STEP(1) }
     else { GBMW_STEP(2) }
