@@ -459,7 +459,7 @@ void prepare_problem(gbmw_batch &b, int pi, std::string *err) {
     h.ws_bytes = (size_t)h.n_cells * (sizeof(Cell) + sizeof(CellMem) + 4) + (size_t)h.U * 12 + (size_t)h.n_r * 8 + 8 +
                  (size_t)h.n_bcells * 2 * sizeof(TFCell) + (size_t)h.n_par * 2 +
                  (size_t)h.n_tiles * sizeof(SweepPartial) + sizeof(SweepPartial) + 36 + (size_t)h.n_flagw * 8 +
-                 (size_t)h.n_gflat * 4 + (size_t)(h.U > 1 ? h.U - 1 : 0) * (h.n_step_tiles * 8 + 8);
+                 (size_t)h.n_gflat * 4 + (size_t)(h.U > 1 ? h.U - 1 : 0) * (h.n_step_tiles * 16 + 8);
     h.gpu = true;
 }
 
@@ -484,7 +484,7 @@ WsLayout ws_layout(const Chunk &c) {
     w.cmem = o; o = align_up(o + c.n_cells * sizeof(CellMem));
     w.rcls = o; o = align_up(o + c.n_r * 8);
     w.bup = o; o = align_up(o + c.probs.size() * 8);
-    w.items = o; o = align_up(o + c.n_items * sizeof(int2));
+    w.items = o; o = align_up(o + c.n_items * sizeof(int4));
     w.scount = o; o = align_up(o + c.slists.size() * 8);
     w.tf0 = o; o = align_up(o + c.n_bcells * sizeof(TFCell));
     w.tf1 = o; o = align_up(o + c.n_bcells * sizeof(TFCell));
@@ -791,7 +791,7 @@ ChunkArgs chunk_args(gbmw_batch *b, const Chunk &c, char *ws, size_t chunk_index
     a.cmem = (CellMem *)(ws + w.cmem);
     a.rcls = (double *)(ws + w.rcls);
     a.bup = (unsigned long long *)(ws + w.bup);
-    a.step_items = (int2 *)(ws + w.items);
+    a.step_items = (int4 *)(ws + w.items);
     a.step_count = (int64_t *)(ws + w.scount);
     a.TF[0] = (TFCell *)(ws + w.tf0);
     a.TF[1] = (TFCell *)(ws + w.tf1);

@@ -142,7 +142,7 @@ struct ChunkArgs {
     const int2 *aux_map;          // K3r tiles: (problem, tile) of frontier / collapsed-DP problems
     const StepList *step_lists;   // K2 launches of the chunk
     int32_t n_step_lists;
-    int2 *step_items;             // live (problem, tile) items of every K2 launch
+    int4 *step_items;             // live (problem, tile, L_u, H_u) items of every K2 launch
     int64_t *step_count;          // per K2 launch: number of items
     int64_t n_aux;
     const int32_t *cand_strat;    // global strategy index
@@ -181,7 +181,7 @@ struct ChunkArgs {
 // launchers (gbmw_kernels.cu); all asynchronous on `stream`, return cudaError_t as int
 int launch_cost_tables(const ChunkArgs &a, int64_t n_cells, int64_t n_r, void *stream);
 int launch_step_lists(const ChunkArgs &a, void *stream);
-int launch_dp_step(const ChunkArgs &a, int group, int u, const int2 *items, const int64_t *count, int64_t max_items,
+int launch_dp_step(const ChunkArgs &a, int group, int u, const int4 *items, const int64_t *count, int64_t max_items,
                    unsigned long long *counter, void *stream);
 int launch_sweep(const ChunkArgs &a, void *stream);
 int launch_approx_step(const ChunkArgs &a, int u, int64_t tile_base, int64_t n_tiles, unsigned long long *counter,

@@ -45,6 +45,7 @@ struct StepShared {
     int64_t gf_cur;                         // flat-group mask of B_u (offset into a.gflat)
     int gw;
     int64_t next;
+    int4 item;
     // per tile
     int kind[kGroups];                      // 0 dead, 1 flat, 2 full
     int list_np[kGroups], list_fl[kGroups];
@@ -327,7 +328,7 @@ __global__ void __launch_bounds__(1024) k_step_lists(ChunkArgs a) {
         const DevProblem &p = a.probs[x];
         const int lo = a.unit_lo[p.ustate_off + sl.u], hi = a.unit_hi[p.ustate_off + sl.u];
         if (hi < lo) continue;
-        for (int t = lo / kStepRows; t <= hi / kStepRows; ++t) a.step_items[at++] = make_int2(x, t);
+        for (int t = lo / kStepRows; t <= hi / kStepRows; ++t) a.step_items[at++] = make_int4(x, t, lo, hi);
     }
     if (tid == 1023) a.step_count[blockIdx.x] = s_part[1023];
 }
@@ -339,7 +340,7 @@ int launch_step_lists(const ChunkArgs &a, void *stream) {
 }
 
 template <int GROUP, bool FIRST>
-__global__ void __launch_bounds__(kStepThreads, GROUP == 0 ? 3 : 2) k_dp_step(ChunkArgs a, int u, const int2 *items,
+__global__ void __launch_bounds__(kStepThreads, GROUP == 0 ? 3 : 2) k_dp_step(ChunkArgs a, int u, const int4 *items,
                                                                               const int64_t *count,
                                                                               unsigned long long *counter) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -348,17 +349,30 @@ __global__ void __launch_bounds__(kStepThreads, GROUP == 0 ? 3 : 2) k_dp_step(Ch
     int q_prev = -1;
     if (threadIdx.x == 0) sh.stat_rows = 0;
     const int64_t n_items = *count;
+    // thread 0 runs one item ahead: the next item's counter value and record are fetched
+    // while the current tile is evaluated
+    long long t_cur = 0, t_next = 0;
+    int4 it_cur = make_int4(0, 0, 0, -1);
+    if (threadIdx.x == 0) {
+        t_cur = (long long)atomicAdd(counter, 1ull);
+        if (t_cur < n_items) it_cur = __ldg(items + t_cur);
+        t_next = (long long)atomicAdd(counter, 1ull);
+    }
     while (true) {
         __syncthreads();
-        if (threadIdx.x == 0) sh.next = (int64_t)atomicAdd(counter, 1ull);
+        if (threadIdx.x == 0) { sh.next = t_cur; sh.item = it_cur; }
         __syncthreads();
-        const int64_t t = sh.next;
-        if (t >= n_items) break;
-        const int2 item = __ldg(items + t);
+        if (sh.next >= n_items) break;
+        const int4 item = sh.item;
+        if (threadIdx.x == 0) {
+            t_cur = t_next;
+            if (t_cur < n_items) it_cur = __ldg(items + t_cur);
+            t_next = (long long)atomicAdd(counter, 1ull);
+        }
         const int q = item.x;
         const DevProblem &p = a.probs[q];
         const int64_t first_row = (int64_t)item.y * kStepRows;
-        const int lo = a.unit_lo[p.ustate_off + u], hi = a.unit_hi[p.ustate_off + u];
+        const int lo = item.z, hi = item.w;
         if (q != q_prev) {
             __syncthreads();
             const int S = p.S, K = p.K;
@@ -411,7 +425,7 @@ __global__ void __launch_bounds__(kStepThreads, GROUP == 0 ? 3 : 2) k_dp_step(Ch
     if (threadIdx.x == 0 && sh.stat_rows) atomicAdd(a.computed_cells, sh.stat_rows);
 }
 
-int launch_dp_step(const ChunkArgs &a, int group, int u, const int2 *items, const int64_t *count, int64_t n_tiles,
+int launch_dp_step(const ChunkArgs &a, int group, int u, const int4 *items, const int64_t *count, int64_t n_tiles,
                    unsigned long long *counter, void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
     if (n_tiles <= 0) return 0;
