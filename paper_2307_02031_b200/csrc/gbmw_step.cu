@@ -33,7 +33,7 @@ constexpr int kClassifyIB = 8;              // window checks per thread in fligh
 constexpr int kGroups = kStepRows / 32;     // 32-row groups per tile
 constexpr int kMaxGfWords = (int)(((GBMW_MAX_BUCKETS + 1 + 31) / 32 + 31) / 32 + 1);   // gflat_words(max n_e)
 
-// KM: class capacity of the instantiation (4 / 8 / kMaxClasses), sizes the per-group arrays
+// KM: class capacity of the instantiation (4 / 8 / kMaxClasses), sizes the per-entry arrays
 template <int KM>
 struct StepShared {
     Cell cell[kMaxStrats];                  // distinct source strategies of unit u-1 (ascending)
@@ -41,23 +41,22 @@ struct StepShared {
     double r[KM * KM];
     uint32_t gfp[kMaxGfWords];              // flat-group mask of B_{u-1} (read redirection, flat_row)
     int S, K, n_e, q, lo_prev, lo, hi, nw;
-    int64_t b_off, par_off, tile0, f_off;
+    int64_t b_off, par_off, f_off;
     int64_t gf_cur;                         // flat-group mask of B_u (offset into a.gflat)
     int gw;
     int64_t next;
-    int4 item;
     // per tile
     int kind[kGroups];                      // 0 dead, 1 flat, 2 full
-    int list_np[kGroups], list_fl[kGroups];
-    int n_np, n_fl;
-    unsigned bits[kGroups][KM];
-    double first_t[kGroups][KM], first_f[kGroups][KM];
-    double last_t[kGroups][KM], last_f[kGroups][KM];
-    int first_p[kGroups][KM], last_p[kGroups][KM];
-    unsigned first_pc[kGroups];             // bit kk: the first row's path differs below its argmin
-    int prev_p[KM];
-    double prev_t[KM], prev_f[KM];
+    unsigned seg[kGroups];                  // bit x (1..31): row x of the group starts a new segment
+    int ebase[kGroups + 1];                 // first entry of each group; entry 0 = row first_row - 1
+    int erow[kStepRows + 1];                // row of each entry (rows that are evaluated)
+    int rg[kGroups + 1];                    // round r covers groups [rg[r], rg[r + 1])
+    int n_rounds;
     int prev_ok;
+    // per round: slot 0 = the last entry of the previous round, slot 1 + i = entry E0 + i
+    double et[kStepThreads + 1][KM], ef[kStepThreads + 1][KM];
+    int ep[kStepThreads + 1][KM];
+    unsigned epc[kStepThreads + 1];         // bit kk: the argmin's source path changes at this row
     unsigned long long stat_rows;
 };
 
@@ -123,50 +122,60 @@ __device__ __forceinline__ unsigned src_path_change(const ChunkArgs &a, const SH
     return (__ldg(fl + (src >> 5)) >> (src & 31)) & 1u;
 }
 
+// Segment starts of a 32-row group contributed by one source: rows x (1..31) where the
+// source's value T_{u-1}[r0 + x, i] may differ from row r0 + x - 1, i.e. the change bits of
+// its window [x0, x0 + 31] of column cls(i) (rows below lo are +inf and constant).
+__device__ __forceinline__ unsigned window_segments(unsigned long long v, int x0, int lo) {
+    unsigned m = (unsigned)v;                            // bit j: row x0 + j vs x0 + j - 1
+    if (x0 < lo) {
+        const int j0 = lo - x0;                          // first finite row of the window
+        m = (m & ~((2u << j0) - 1u)) | (1u << j0);
+    }
+    return m & 0xfffffffeu;
+}
+
+// One tile of B_u.  Rows are evaluated only where some source changes (segment starts):
+// B_u is constant between them in value, argmin and path.  A group without segment starts
+// is flat (its first row stands for all, stored once); other groups are evaluated at their
+// first row and at each segment start and written in full.  Evaluated rows ("entries") are
+// processed in rounds of at most kStepThreads, one thread each.
 template <int KT, bool FIRST, bool GUARD, class SH>
 __device__ void step_tile(const ChunkArgs &a, SH &sh, int u, int first_row) {
     const int K = GUARD ? sh.K : KT;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthr = blockDim.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthr = blockDim.x, nwarp = nthr >> 5;
     const int n_e = sh.n_e, lo = sh.lo, hi = sh.hi, S = sh.S;
-    // ---- 1. classify groups
+    // ---- 1. classify groups: dead / whole-live (segments from the source windows) / partial
     for (int g = tid; g < kGroups; g += nthr) {
         const int r0 = first_row + 32 * g, r1 = r0 + 31;
-        sh.kind[g] = (r1 < lo || r0 > hi) ? 0 : ((r0 >= lo && r1 <= hi) ? 1 : 2);
+        const bool dead = r1 < lo || r0 > hi;
+        const bool whole = r0 >= lo && r1 <= hi;
+        sh.kind[g] = dead ? 0 : (whole ? 1 : 2);
+        sh.seg[g] = whole ? 0u : 0xfffffffeu;            // partial groups: every row evaluated
     }
     __syncthreads();
     const uint32_t *fin = a.chg[(u - 1) & 1] + sh.f_off;
-    // (group, source) window checks, kClassifyIB per thread in flight
     const int n_checks = kGroups * S;
     for (int x0 = tid; x0 < n_checks; x0 += nthr * kClassifyIB) {
         uint32_t w0[kClassifyIB], w1[kClassifyIB];
-        int sh_[kClassifyIB], gg[kClassifyIB];
-        bool load[kClassifyIB];
+        int xs_[kClassifyIB], gg[kClassifyIB];
 #pragma unroll
         for (int b = 0; b < kClassifyIB; ++b) {
             const int x = x0 + b * nthr;
-            gg[b] = -1; load[b] = false; sh_[b] = 0;
-            w0[b] = 0u; w1[b] = 0u;
+            gg[b] = -1; xs_[b] = 0; w0[b] = 0u; w1[b] = 0u;
             if (x < n_checks) {
                 const int g = x / S, n = x - g * S;
                 if (sh.kind[g] == 1) {
                     const Cell c = sh.cell[n];
                     const int r0 = first_row + 32 * g;
+                    const int xs = r0 - c.w;
+                    xs_[b] = xs;
                     if (FIRST) {
-                        if (!((r0 >= c.w) || (r0 + 31 < c.w))) gg[b] = g;
-                    } else {
-                        const int xs = r0 - c.w;
-                        if (xs + 31 < sh.lo_prev) {
-                            // all +inf: flat
-                        } else if (xs < sh.lo_prev) {
-                            gg[b] = g;
-                        } else {
-                            const int lb = xs + 1;
-                            const uint32_t *fl = fin + (int64_t)c.k * sh.nw + (lb >> 5);
-                            w0[b] = __ldg(fl); w1[b] = __ldg(fl + 1);
-                            sh_[b] = lb & 31;
-                            load[b] = true;
-                            gg[b] = g;
-                        }
+                        gg[b] = g;
+                    } else if (xs + 31 >= sh.lo_prev) {
+                        const int xl = xs < 0 ? 0 : xs;
+                        const uint32_t *fl = fin + (int64_t)c.k * sh.nw + (xl >> 5);
+                        w0[b] = __ldg(fl); w1[b] = __ldg(fl + 1);
+                        gg[b] = g;
                     }
                 }
             }
@@ -174,129 +183,173 @@ __device__ void step_tile(const ChunkArgs &a, SH &sh, int u, int first_row) {
 #pragma unroll
         for (int b = 0; b < kClassifyIB; ++b) {
             if (gg[b] < 0) continue;
-            bool flat = false;
-            if (load[b]) {
-                const unsigned long long v = ((unsigned long long)w1[b] << 32 | (unsigned long long)w0[b]) >> sh_[b];
-                flat = (v & 0x7fffffffull) == 0ull;
+            const int xs = xs_[b];
+            unsigned m;
+            if (FIRST) {
+                // T_0[e, i] is finite from e = w_i on: one segment start at row w_i
+                const int j = -xs;                       // w_i - r0
+                m = (j >= 1 && j <= 31) ? (1u << j) : 0u;
+            } else {
+                const int xl = xs < 0 ? 0 : xs;
+                const unsigned long long v =
+                    ((unsigned long long)w1[b] << 32 | (unsigned long long)w0[b]) >> (xl & 31);
+                // v bit j = row xl + j; rows below xl (negative rows) are +inf like rows below lo
+                const unsigned long long vv = (xs < 0) ? (v << (-xs)) : v;
+                m = window_segments(vv, xs, sh.lo_prev);
             }
-            if (!flat) sh.kind[gg[b]] = 2;
+            if (m) atomicOr(&sh.seg[gg[b]], m);
         }
     }
     __syncthreads();
-    // ---- 2. row list: full groups (32 rows, one warp each), then flat representatives
+    // ---- 2. entries: row first_row - 1, then per group its first row and segment starts
     if (warp == 0) {
-        int np = 0, nf = 0;
+        int run = 1;
         for (int base = 0; base < kGroups; base += 32) {
             const int g = base + lane;
-            const int kd = g < kGroups ? sh.kind[g] : 0;
-            const unsigned mnp = __ballot_sync(0xffffffffu, kd == 2), mfl = __ballot_sync(0xffffffffu, kd == 1);
-            const unsigned below = (1u << lane) - 1u;
-            if (kd == 2) sh.list_np[np + __popc(mnp & below)] = g;
-            if (kd == 1) sh.list_fl[nf + __popc(mfl & below)] = g;
-            np += __popc(mnp);
-            nf += __popc(mfl);
+            int cnt = 0;
+            if (g < kGroups) {
+                const int kd = sh.kind[g];
+                if (kd == 1 && sh.seg[g] != 0u) sh.kind[g] = 2;
+                cnt = (kd == 0) ? 0 : 1 + __popc(sh.seg[g]);
+            }
+            int incl = cnt;
+            for (int off = 1; off < 32; off <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, incl, off);
+                if (lane >= off) incl += v;
+            }
+            if (g < kGroups) sh.ebase[g] = run + incl - cnt;
+            run += __shfl_sync(0xffffffffu, incl, 31);
         }
         if (lane == 0) {
-            sh.n_np = np;
-            sh.n_fl = nf;
-            sh.stat_rows += (unsigned long long)(32 * np + nf + 1) * (unsigned long long)K;
+            sh.ebase[kGroups] = run;
+            sh.erow[0] = first_row - 1;
+            sh.prev_ok = (first_row - 1 >= lo && first_row - 1 <= hi) ? 1 : 0;
+            sh.stat_rows += (unsigned long long)run * (unsigned long long)K;
         }
     }
     __syncthreads();
-    const int n_np = sh.n_np, n_fl = sh.n_fl;
-    const int n_list = 32 * n_np + n_fl + 1;                // + the row before the tile
+    for (int g = tid; g < kGroups; g += nthr) {
+        if (sh.kind[g] == 0) continue;
+        const int r0 = first_row + 32 * g;
+        int at = sh.ebase[g];
+        sh.erow[at++] = r0;
+        unsigned m = sh.seg[g];
+        while (m) {
+            const int x = __ffs(m) - 1;
+            m &= m - 1u;
+            sh.erow[at++] = r0 + x;
+        }
+    }
+    if (tid == 0) {                                      // rounds of <= nthr entries, whole groups
+        int r = 0, start = 0;
+        sh.rg[0] = 0;
+        for (int g = 0; g < kGroups; ++g)
+            if (sh.ebase[g + 1] - start > nthr) { sh.rg[++r] = g; start = sh.ebase[g]; }
+        sh.rg[r + 1] = kGroups;
+        sh.n_rounds = r + 1;
+    }
+    __syncthreads();
     TFCell *bout = a.TF[u & 1] + sh.b_off;
     uint16_t *pout = a.par + sh.par_off + (int64_t)(u - 1) * K * n_e;
-    const int n_pass = (n_list + nthr - 1) / nthr;
-    for (int pass = 0; pass < n_pass; ++pass) {
-        const int x = pass * nthr + tid;
-        double bt[KT], bf[KT];
-        int bp[KT];
-        int e = -1, kind = -1, g = -1;
-        if (x < 32 * n_np) {
-            g = sh.list_np[x >> 5]; e = first_row + 32 * g + lane; kind = 2;
-        } else if (x < 32 * n_np + n_fl) {
-            g = sh.list_fl[x - 32 * n_np]; e = first_row + 32 * g; kind = 1;
-        } else if (x == 32 * n_np + n_fl) {
-            e = first_row - 1; kind = 3;
-        }
-        const bool row_live = kind >= 0 && e >= lo && e <= hi && e < n_e;
-        relax_row<KT, FIRST, GUARD>(a, sh, u, row_live ? e : -1, bt, bf, bp);
-        // per class: source path-change bit (all loads issued before use)
-        unsigned pcm = 0u;
-#pragma unroll
-        for (int kk = 0; kk < KT; ++kk)
-            if (!FIRST && (!GUARD || kk < K) && row_live && bt[kk] < GBMW_STEP_INF)
-                pcm |= src_path_change(a, sh, u, e, bp[kk]) << kk;
-        // stored rows: live rows of full groups, the first row of flat groups
-        if (row_live && (kind == 2 || kind == 1)) {
+    uint32_t *fout = a.chg[u & 1] + sh.f_off;
+    const int w_first = first_row >> 5;
+    const int n_rounds = sh.n_rounds;
+    for (int rd = 0; rd < n_rounds; ++rd) {
+        const int g0 = sh.rg[rd], g1 = sh.rg[rd + 1];
+        const int E0 = (rd == 0) ? 0 : sh.ebase[g0], E1 = sh.ebase[g1];
+        // ---- 3. evaluate the round's entries
+        if (E0 + tid < E1) {
+            const int e = sh.erow[E0 + tid];
+            const bool live = e >= lo && e <= hi && e < n_e;
+            double bt[KT], bf[KT];
+            int bp[KT];
+            relax_row<KT, FIRST, GUARD>(a, sh, u, live ? e : -1, bt, bf, bp);
+            unsigned pcm = 0u;
 #pragma unroll
             for (int kk = 0; kk < KT; ++kk)
-                if (!GUARD || kk < K) {
-                    reinterpret_cast<double2 *>(bout)[kk * n_e + e] = make_double2(bt[kk], bf[kk]);
-                    pout[kk * n_e + e] = (uint16_t)sh.idx[bp[kk]];
-                }
-        }
-        // change bits inside full groups (a full group is exactly one warp of this pass)
-        const bool in_np = (pass * nthr + warp * 32) < 32 * n_np;
+                if (!FIRST && (!GUARD || kk < K) && live && bt[kk] < GBMW_STEP_INF)
+                    pcm |= src_path_change(a, sh, u, e, bp[kk]) << kk;
+            const int s = 1 + tid;
 #pragma unroll
-        for (int kk = 0; kk < KT; ++kk) {
-            if (GUARD && kk >= K) break;
-            if (in_np) {
-                const double pt = __shfl_up_sync(0xffffffffu, bt[kk], 1);
-                const double pf = __shfl_up_sync(0xffffffffu, bf[kk], 1);
-                const int pp = __shfl_up_sync(0xffffffffu, bp[kk], 1);
-                const bool chg = lane > 0 && (pt != bt[kk] || pf != bf[kk] || pp != bp[kk] || ((pcm >> kk) & 1u));
-                const unsigned m = __ballot_sync(0xffffffffu, chg);
-                if (lane == 0) {
-                    sh.bits[g][kk] = m;
-                    sh.first_t[g][kk] = bt[kk]; sh.first_f[g][kk] = bf[kk]; sh.first_p[g][kk] = bp[kk];
+            for (int kk = 0; kk < KT; ++kk)
+                if (!GUARD || kk < K) { sh.et[s][kk] = bt[kk]; sh.ef[s][kk] = bf[kk]; sh.ep[s][kk] = bp[kk]; }
+            sh.epc[s] = pcm;
+        }
+        __syncthreads();
+        // ---- 4. write the round's groups: rows, change-bit words, flat-group bits
+        for (int g = g0 + warp; g < g1; g += nwarp) {
+            const int kd = sh.kind[g];
+            if (kd == 0) continue;
+            const int r0 = first_row + 32 * g;
+            const int wi = w_first + g;
+            // predecessor of the group's first row: the last entry before it (row r0 - 1)
+            const int sp = sh.ebase[g] - E0;             // its slot (0 = carried from the previous round)
+            const bool pred_ok = (g == 0) ? (sh.prev_ok != 0) : (sh.kind[g - 1] != 0);
+            const int s0 = sh.ebase[g] - E0 + 1;
+            if (kd == 1) {
+#pragma unroll
+                for (int kk = 0; kk < KT; ++kk) {
+                    if (GUARD && kk >= K) break;
+                    if (lane == kk) {
+                        reinterpret_cast<double2 *>(bout)[(int64_t)kk * n_e + r0] =
+                            make_double2(sh.et[s0][kk], sh.ef[s0][kk]);
+                        pout[(int64_t)kk * n_e + r0] = (uint16_t)sh.idx[sh.ep[s0][kk]];
+                        const bool same = pred_ok && sh.et[sp][kk] == sh.et[s0][kk] && sh.ef[sp][kk] == sh.ef[s0][kk] &&
+                                          sh.ep[sp][kk] == sh.ep[s0][kk] && !((sh.epc[s0] >> kk) & 1u);
+                        if (wi < sh.nw) fout[(int64_t)kk * sh.nw + wi] = same ? 0u : 1u;
+                    }
                 }
-                if (lane == 31) { sh.last_t[g][kk] = bt[kk]; sh.last_f[g][kk] = bf[kk]; sh.last_p[g][kk] = bp[kk]; }
-            } else if (kind == 1) {
-                sh.bits[g][kk] = 0u;
-                sh.first_t[g][kk] = sh.last_t[g][kk] = bt[kk];
-                sh.first_f[g][kk] = sh.last_f[g][kk] = bf[kk];
-                sh.first_p[g][kk] = sh.last_p[g][kk] = bp[kk];
-            } else if (kind == 3) {
-                sh.prev_t[kk] = bt[kk];
-                sh.prev_f[kk] = bf[kk];
-                sh.prev_p[kk] = bp[kk];
+            } else {
+                const unsigned segm = sh.seg[g];
+                const int e = r0 + lane;
+                const bool live = e >= lo && e <= hi;
+                const int s = s0 + __popc(segm & ((2u << lane) - 2u));   // segment holding row e
+                const bool start = lane > 0 && ((segm >> lane) & 1u);
+#pragma unroll
+                for (int kk = 0; kk < KT; ++kk) {
+                    if (GUARD && kk >= K) break;
+                    const double t = sh.et[s][kk], f = sh.ef[s][kk];
+                    const int pp = sh.ep[s][kk];
+                    if (live) {
+                        reinterpret_cast<double2 *>(bout)[(int64_t)kk * n_e + e] = make_double2(t, f);
+                        pout[(int64_t)kk * n_e + e] = (uint16_t)sh.idx[pp];
+                    }
+                    bool chg;
+                    const int sq = (lane == 0) ? sp : s - 1;     // the row before e
+                    const bool q_ok = (lane == 0) ? pred_ok : true;
+                    if (lane > 0 && !start) {
+                        chg = false;                             // no source changes: same row
+                    } else {
+                        chg = !(q_ok && sh.et[sq][kk] == t && sh.ef[sq][kk] == f && sh.ep[sq][kk] == pp &&
+                                !((sh.epc[s] >> kk) & 1u));
+                    }
+                    const unsigned m = __ballot_sync(0xffffffffu, chg);
+                    if (lane == 0 && wi < sh.nw) fout[(int64_t)kk * sh.nw + wi] = m;
+                }
             }
         }
-        if ((in_np && lane == 0) || kind == 1) sh.first_pc[g] = pcm;
-        if (kind == 3) sh.prev_ok = (e >= lo && e <= hi) ? 1 : 0;
+        __syncthreads();
+        // carry the round's last entry into slot 0 for the next round
+        if (rd + 1 < n_rounds) {
+            const int sl = E1 - E0;                      // slot of entry E1 - 1
+            if (tid < KT && (!GUARD || tid < K)) {
+                sh.et[0][tid] = sh.et[sl][tid]; sh.ef[0][tid] = sh.ef[sl][tid]; sh.ep[0][tid] = sh.ep[sl][tid];
+            }
+            if (tid == 0) sh.epc[0] = sh.epc[sl];
+            __syncthreads();
+        }
     }
-    __syncthreads();
-    // ---- 3a. flat groups store their first row only (written above); readers redirect the
-    // other rows to it through the group mask (flat_row)
+    // ---- 5. dead groups' change words, flat-group mask words
+    for (int x = tid; x < kGroups * K; x += nthr) {
+        const int g = x / K, kk = x - g * K;
+        const int wi = w_first + g;
+        if (sh.kind[g] == 0 && wi < sh.nw) fout[(int64_t)kk * sh.nw + wi] = 0xffffffffu;   // never read as flat
+    }
     if (tid < kGroups / 32) {
         unsigned m = 0u;
         for (int b = 0; b < 32; ++b) m |= (sh.kind[32 * tid + b] == 1 ? 1u : 0u) << b;
         const int wi = (first_row >> 10) + tid;
         if (wi < sh.gw) a.gflat[sh.gf_cur + wi] = m;
-    }
-    // ---- 3b. change-bit words of B_u (bit 0 of a group compares with the previous row)
-    uint32_t *fout = a.chg[u & 1] + sh.f_off;
-    const int w_first = first_row >> 5;
-    for (int x = tid; x < kGroups * K; x += nthr) {
-        const int g = x / K, kk = x - g * K;
-        const int wi = w_first + g;
-        if (wi >= sh.nw) continue;
-        unsigned word;
-        if (sh.kind[g] == 0) {
-            word = 0xffffffffu;                              // dead rows: never read as flat
-        } else {
-            word = sh.bits[g][kk];
-            bool same;
-            if (g == 0) same = sh.prev_ok && sh.prev_t[kk] == sh.first_t[0][kk] && sh.prev_f[kk] == sh.first_f[0][kk] &&
-                               sh.prev_p[kk] == sh.first_p[0][kk];
-            else same = sh.kind[g - 1] != 0 && sh.last_t[g - 1][kk] == sh.first_t[g][kk] &&
-                        sh.last_f[g - 1][kk] == sh.first_f[g][kk] && sh.last_p[g - 1][kk] == sh.first_p[g][kk];
-            same = same && !((sh.first_pc[g] >> kk) & 1u);
-            if (!same) word |= 1u;
-        }
-        fout[(int64_t)kk * sh.nw + wi] = word;
     }
     __syncthreads();
 }
@@ -349,26 +402,13 @@ __global__ void __launch_bounds__(kStepThreads, GROUP == 0 ? 3 : 2) k_dp_step(Ch
     int q_prev = -1;
     if (threadIdx.x == 0) sh.stat_rows = 0;
     const int64_t n_items = *count;
-    // thread 0 runs one item ahead: the next item's counter value and record are fetched
-    // while the current tile is evaluated
-    long long t_cur = 0, t_next = 0;
-    int4 it_cur = make_int4(0, 0, 0, -1);
-    if (threadIdx.x == 0) {
-        t_cur = (long long)atomicAdd(counter, 1ull);
-        if (t_cur < n_items) it_cur = __ldg(items + t_cur);
-        t_next = (long long)atomicAdd(counter, 1ull);
-    }
     while (true) {
         __syncthreads();
-        if (threadIdx.x == 0) { sh.next = t_cur; sh.item = it_cur; }
+        if (threadIdx.x == 0) sh.next = (int64_t)atomicAdd(counter, 1ull);
         __syncthreads();
-        if (sh.next >= n_items) break;
-        const int4 item = sh.item;
-        if (threadIdx.x == 0) {
-            t_cur = t_next;
-            if (t_cur < n_items) it_cur = __ldg(items + t_cur);
-            t_next = (long long)atomicAdd(counter, 1ull);
-        }
+        const int64_t t = sh.next;
+        if (t >= n_items) break;
+        const int4 item = __ldg(items + t);
         const int q = item.x;
         const DevProblem &p = a.probs[q];
         const int64_t first_row = (int64_t)item.y * kStepRows;
@@ -395,7 +435,7 @@ __global__ void __launch_bounds__(kStepThreads, GROUP == 0 ? 3 : 2) k_dp_step(Ch
                 sh.S = nu; sh.K = K; sh.n_e = (int)(p.n_b + 1); sh.q = q;
                 sh.lo_prev = a.unit_lo[p.ustate_off + u - 1];
                 sh.lo = lo; sh.hi = hi;
-                sh.b_off = p.b_off; sh.par_off = p.par_off; sh.tile0 = a.step_tiles[q];
+                sh.b_off = p.b_off; sh.par_off = p.par_off;
                 sh.f_off = p.flag_off; sh.nw = (int)flag_words(p.n_b + 1);
                 sh.gw = (int)gflat_words(p.n_b + 1);
                 sh.gf_cur = p.gflat_off + (int64_t)(u - 1) * sh.gw;
