@@ -97,7 +97,7 @@ struct Chunk {
     int64_t n_aux = 0;
     std::vector<StepList> slists;  // K2 launches (unit, group), in launch order
     std::vector<int> slist_group;
-    int64_t n_items = 0;           // upper bound of live K2 items over all launches
+    int64_t n_items = 0;           // K2 items (active problems) over all launches
     size_t small_bytes = 0;
     size_t ws_bytes = 0;
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -459,7 +459,7 @@ void prepare_problem(gbmw_batch &b, int pi, std::string *err) {
     h.ws_bytes = (size_t)h.n_cells * (sizeof(Cell) + sizeof(CellMem) + 4) + (size_t)h.U * 12 + (size_t)h.n_r * 8 + 8 +
                  (size_t)h.n_bcells * 2 * sizeof(TFCell) + (size_t)h.n_par * 2 +
                  (size_t)h.n_tiles * sizeof(SweepPartial) + sizeof(SweepPartial) + 36 + (size_t)h.n_flagw * 8 +
-                 (size_t)h.n_gflat * 4 + (size_t)(h.U > 1 ? h.U - 1 : 0) * (h.n_step_tiles * 16 + 8);
+                 (size_t)h.n_gflat * 4 + (size_t)(h.U > 1 ? h.U - 1 : 0) * 24;
     h.gpu = true;
 }
 
@@ -667,7 +667,7 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
                 sl.u = u; sl.lo = lo; sl.n = na; sl.pad_ = 0; sl.base = c.n_items;
                 c.slists.push_back(sl);
                 c.slist_group.push_back(g);
-                c.n_items += c.step_prefix[lo + na] - c.step_prefix[lo];
+                c.n_items += na;                   // one item per active problem
             }
         c.o_slists = put(blob, c.slists.data(), c.slists.size()) - base;
         c.small_bytes = blob.size() - base;
@@ -853,7 +853,7 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
         for (size_t s = 0; s < c.slists.size(); ++s) {
             const StepList &sl = c.slists[s];
             const int g = c.slist_group[s];
-            const int64_t ub = c.step_prefix[sl.lo + sl.n] - c.step_prefix[sl.lo];
+            const int64_t ub = sl.n;
             if ((rc = launch_dp_step(a, g, sl.u, a.step_items + sl.base, a.step_count + s, ub,
                                      a.counters + (size_t)sl.u * kNumGroups + g, st)))
                 return cuda_fail(ctx, rc, "K2 launch");

@@ -120,8 +120,8 @@ struct SweepPartial {
 };
 
 // One K2 launch (unit u, class-count group): its problems are [lo, lo + n) in sorted order;
-// k_step_lists writes their live tiles (rows [L_u, H_u] only) as (problem, tile) items at
-// items[base ...] and the item count to step_count[index].
+// k_step_lists writes the ones with live rows as (problem, first warp tile, last warp tile)
+// items at items[base ...] (rows [L_u, H_u] only) and the item count to step_count[index].
 struct StepList {
     int32_t u, lo, n, pad_;
     int64_t base;
@@ -142,7 +142,7 @@ struct ChunkArgs {
     const int2 *aux_map;          // K3r tiles: (problem, tile) of frontier / collapsed-DP problems
     const StepList *step_lists;   // K2 launches of the chunk
     int32_t n_step_lists;
-    int4 *step_items;             // live (problem, tile, L_u, H_u) items of every K2 launch
+    int4 *step_items;             // (problem, first tile, last tile) items of every K2 launch
     int64_t *step_count;          // per K2 launch: number of items
     int64_t n_aux;
     const int32_t *cand_strat;    // global strategy index

@@ -33,31 +33,31 @@ constexpr int kClassifyIB = 8;              // window checks per thread in fligh
 constexpr int kGroups = kStepRows / 32;     // 32-row groups per tile
 constexpr int kMaxGfWords = (int)(((GBMW_MAX_BUCKETS + 1 + 31) / 32 + 31) / 32 + 1);   // gflat_words(max n_e)
 
-// KM: class capacity of the instantiation (4 / 8 / kMaxClasses), sizes the per-entry arrays
+constexpr int kWarpRows = 1024;             // rows per warp tile: 32 groups, one flat-mask word
+constexpr int kSlots = 65;                  // evaluated rows held per round (+ slot 0: carry)
+
+// Per-warp scratch of one tile.  Entry = an evaluated row; entry 0 is the row before the tile.
+template <int KM>
+struct WarpScratch {
+    double et[kSlots][KM], ef[kSlots][KM];  // per round: slot 0 = last entry of the previous round
+    int16_t ep[kSlots][KM];                 // argmin (position in the distinct list)
+    unsigned epc[kSlots];                   // bit kk: the argmin's source path changes at this row
+    uint16_t erow[kWarpRows + 2];           // row of each entry, relative to the tile's first row - 1
+};
+
+// KM: class capacity of the instantiation (4 / 8 / kMaxClasses)
 template <int KM>
 struct StepShared {
     Cell cell[kMaxStrats];                  // distinct source strategies of unit u-1 (ascending)
     int idx[kMaxStrats];                    // their strategy index
     double r[KM * KM];
     uint32_t gfp[kMaxGfWords];              // flat-group mask of B_{u-1} (read redirection, flat_row)
-    int S, K, n_e, q, lo_prev, lo, hi, nw;
+    int S, K, n_e, lo_prev, lo, hi, nw, gw;
     int64_t b_off, par_off, f_off;
     int64_t gf_cur;                         // flat-group mask of B_u (offset into a.gflat)
-    int gw;
     int64_t next;
-    // per tile
-    int kind[kGroups];                      // 0 dead, 1 flat, 2 full
-    unsigned seg[kGroups];                  // bit x (1..31): row x of the group starts a new segment
-    int ebase[kGroups + 1];                 // first entry of each group; entry 0 = row first_row - 1
-    int erow[kStepRows + 1];                // row of each entry (rows that are evaluated)
-    int rg[kGroups + 1];                    // round r covers groups [rg[r], rg[r + 1])
-    int n_rounds;
-    int prev_ok;
-    // per round: slot 0 = the last entry of the previous round, slot 1 + i = entry E0 + i
-    double et[kStepThreads + 1][KM], ef[kStepThreads + 1][KM];
-    int ep[kStepThreads + 1][KM];
-    unsigned epc[kStepThreads + 1];         // bit kk: the argmin's source path changes at this row
-    unsigned long long stat_rows;
+    int tnext, tlast;                       // warp tiles of the current problem
+    WarpScratch<KM> w[kStepThreads / 32];
 };
 
 // K lexmins of one source row e' (T1 tie-break).  Rows outside [lo_prev + w, hi] read +inf.
@@ -134,254 +134,205 @@ __device__ __forceinline__ unsigned window_segments(unsigned long long v, int x0
     return m & 0xfffffffeu;
 }
 
-// One tile of B_u.  Rows are evaluated only where some source changes (segment starts):
-// B_u is constant between them in value, argmin and path.  A group without segment starts
-// is flat (its first row stands for all, stored once); other groups are evaluated at their
-// first row and at each segment start and written in full.  Evaluated rows ("entries") are
-// processed in rounds of at most kStepThreads, one thread each.
-template <int KT, bool FIRST, bool GUARD, class SH>
-__device__ void step_tile(const ChunkArgs &a, SH &sh, int u, int first_row) {
+// One warp tile (kWarpRows rows) of B_u, by one warp; lane g owns 32-row group g.
+// Rows are evaluated only where some source changes (segment starts): B_u is constant
+// between them in value, argmin and path.  A group without segment starts is flat (its
+// first row stands for all, stored once); other groups are evaluated at their first row and
+// at each segment start and written in full.  Warp-synchronous: no CTA barrier.
+template <int KT, bool FIRST, bool GUARD, class SH, class WS>
+__device__ __forceinline__ unsigned long long warp_tile(const ChunkArgs &a, const SH &sh, WS &w, int u, int r_base,
+                                                        int lane) {
     const int K = GUARD ? sh.K : KT;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthr = blockDim.x, nwarp = nthr >> 5;
     const int n_e = sh.n_e, lo = sh.lo, hi = sh.hi, S = sh.S;
-    // ---- 1. classify groups: dead / whole-live (segments from the source windows) / partial
-    for (int g = tid; g < kGroups; g += nthr) {
-        const int r0 = first_row + 32 * g, r1 = r0 + 31;
-        const bool dead = r1 < lo || r0 > hi;
-        const bool whole = r0 >= lo && r1 <= hi;
-        sh.kind[g] = dead ? 0 : (whole ? 1 : 2);
-        sh.seg[g] = whole ? 0u : 0xfffffffeu;            // partial groups: every row evaluated
-    }
-    __syncthreads();
-    const uint32_t *fin = a.chg[(u - 1) & 1] + sh.f_off;
-    const int n_checks = kGroups * S;
-    for (int x0 = tid; x0 < n_checks; x0 += nthr * kClassifyIB) {
-        uint32_t w0[kClassifyIB], w1[kClassifyIB];
-        int xs_[kClassifyIB], gg[kClassifyIB];
+    const int g = lane, r0 = r_base + 32 * g, r1 = r0 + 31;
+    const bool dead = r1 < lo || r0 > hi;
+    const bool whole = r0 >= lo && r1 <= hi;
+    // ---- 1. segment starts of the group: change bits of every source window
+    unsigned seg = (dead || whole) ? 0u : 0xfffffffeu;      // partial groups: every row evaluated
+    if (whole) {
+        const uint32_t *fin = a.chg[(u - 1) & 1] + sh.f_off;
+        for (int n0 = 0; n0 < S; n0 += kClassifyIB) {
+            uint32_t w0[kClassifyIB], w1[kClassifyIB];
+            int xs_[kClassifyIB];
+            bool ld[kClassifyIB];
 #pragma unroll
-        for (int b = 0; b < kClassifyIB; ++b) {
-            const int x = x0 + b * nthr;
-            gg[b] = -1; xs_[b] = 0; w0[b] = 0u; w1[b] = 0u;
-            if (x < n_checks) {
-                const int g = x / S, n = x - g * S;
-                if (sh.kind[g] == 1) {
-                    const Cell c = sh.cell[n];
-                    const int r0 = first_row + 32 * g;
-                    const int xs = r0 - c.w;
-                    xs_[b] = xs;
-                    if (FIRST) {
-                        gg[b] = g;
-                    } else if (xs + 31 >= sh.lo_prev) {
-                        const int xl = xs < 0 ? 0 : xs;
-                        const uint32_t *fl = fin + (int64_t)c.k * sh.nw + (xl >> 5);
-                        w0[b] = __ldg(fl); w1[b] = __ldg(fl + 1);
-                        gg[b] = g;
-                    }
+            for (int b = 0; b < kClassifyIB; ++b) {
+                const int n = n0 + b;
+                const Cell c = sh.cell[n < S ? n : 0];
+                const int xs = r0 - c.w;
+                xs_[b] = xs; w0[b] = 0u; w1[b] = 0u;
+                ld[b] = n < S && (FIRST || xs + 31 >= sh.lo_prev);
+                if (!FIRST && ld[b]) {
+                    const int xl = xs < 0 ? 0 : xs;
+                    const uint32_t *fl = fin + (int64_t)c.k * sh.nw + (xl >> 5);
+                    w0[b] = __ldg(fl); w1[b] = __ldg(fl + 1);
+                }
+            }
+#pragma unroll
+            for (int b = 0; b < kClassifyIB; ++b) {
+                if (!ld[b]) continue;
+                const int xs = xs_[b];
+                if (FIRST) {
+                    const int j = -xs;                   // T_0[e, i] is finite from e = w_i on
+                    seg |= (j >= 1 && j <= 31) ? (1u << j) : 0u;
+                } else {
+                    const int xl = xs < 0 ? 0 : xs;
+                    const unsigned long long v =
+                        ((unsigned long long)w1[b] << 32 | (unsigned long long)w0[b]) >> (xl & 31);
+                    seg |= window_segments((xs < 0) ? (v << (-xs)) : v, xs, sh.lo_prev);
                 }
             }
         }
+    }
+    const bool flat = whole && seg == 0u;
+    // ---- 2. entries: 0 = row r_base - 1, then per group its first row and segment starts
+    const int cnt = dead ? 0 : 1 + __popc(seg);
+    int incl = cnt;
 #pragma unroll
-        for (int b = 0; b < kClassifyIB; ++b) {
-            if (gg[b] < 0) continue;
-            const int xs = xs_[b];
-            unsigned m;
-            if (FIRST) {
-                // T_0[e, i] is finite from e = w_i on: one segment start at row w_i
-                const int j = -xs;                       // w_i - r0
-                m = (j >= 1 && j <= 31) ? (1u << j) : 0u;
-            } else {
-                const int xl = xs < 0 ? 0 : xs;
-                const unsigned long long v =
-                    ((unsigned long long)w1[b] << 32 | (unsigned long long)w0[b]) >> (xl & 31);
-                // v bit j = row xl + j; rows below xl (negative rows) are +inf like rows below lo
-                const unsigned long long vv = (xs < 0) ? (v << (-xs)) : v;
-                m = window_segments(vv, xs, sh.lo_prev);
-            }
-            if (m) atomicOr(&sh.seg[gg[b]], m);
-        }
+    for (int off = 1; off < 32; off <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += v;
     }
-    __syncthreads();
-    // ---- 2. entries: row first_row - 1, then per group its first row and segment starts
-    if (warp == 0) {
-        int run = 1;
-        for (int base = 0; base < kGroups; base += 32) {
-            const int g = base + lane;
-            int cnt = 0;
-            if (g < kGroups) {
-                const int kd = sh.kind[g];
-                if (kd == 1 && sh.seg[g] != 0u) sh.kind[g] = 2;
-                cnt = (kd == 0) ? 0 : 1 + __popc(sh.seg[g]);
-            }
-            int incl = cnt;
-            for (int off = 1; off < 32; off <<= 1) {
-                const int v = __shfl_up_sync(0xffffffffu, incl, off);
-                if (lane >= off) incl += v;
-            }
-            if (g < kGroups) sh.ebase[g] = run + incl - cnt;
-            run += __shfl_sync(0xffffffffu, incl, 31);
-        }
-        if (lane == 0) {
-            sh.ebase[kGroups] = run;
-            sh.erow[0] = first_row - 1;
-            sh.prev_ok = (first_row - 1 >= lo && first_row - 1 <= hi) ? 1 : 0;
-            sh.stat_rows += (unsigned long long)run * (unsigned long long)K;
-        }
-    }
-    __syncthreads();
-    for (int g = tid; g < kGroups; g += nthr) {
-        if (sh.kind[g] == 0) continue;
-        const int r0 = first_row + 32 * g;
-        int at = sh.ebase[g];
-        sh.erow[at++] = r0;
-        unsigned m = sh.seg[g];
+    const int ebase = 1 + incl - cnt, eend = 1 + incl;
+    const int n_ent = 1 + __shfl_sync(0xffffffffu, incl, 31);
+    if (!dead) {
+        int at = ebase;
+        w.erow[at++] = (uint16_t)(32 * g + 1);
+        unsigned m = seg;
         while (m) {
             const int x = __ffs(m) - 1;
             m &= m - 1u;
-            sh.erow[at++] = r0 + x;
+            w.erow[at++] = (uint16_t)(32 * g + 1 + x);
         }
     }
-    if (tid == 0) {                                      // rounds of <= nthr entries, whole groups
-        int r = 0, start = 0;
-        sh.rg[0] = 0;
-        for (int g = 0; g < kGroups; ++g)
-            if (sh.ebase[g + 1] - start > nthr) { sh.rg[++r] = g; start = sh.ebase[g]; }
-        sh.rg[r + 1] = kGroups;
-        sh.n_rounds = r + 1;
-    }
-    __syncthreads();
+    if (lane == 0) w.erow[0] = 0;
+    const bool prev_ok = r_base - 1 >= lo && r_base - 1 <= hi;
+    const bool dead_prev = __shfl_up_sync(0xffffffffu, dead, 1);
+    const bool pred_ok = (g == 0) ? prev_ok : !dead_prev;
+    __syncwarp();
     TFCell *bout = a.TF[u & 1] + sh.b_off;
     uint16_t *pout = a.par + sh.par_off + (int64_t)(u - 1) * K * n_e;
     uint32_t *fout = a.chg[u & 1] + sh.f_off;
-    const int w_first = first_row >> 5;
-    const int n_rounds = sh.n_rounds;
-    for (int rd = 0; rd < n_rounds; ++rd) {
-        const int g0 = sh.rg[rd], g1 = sh.rg[rd + 1];
-        const int E0 = (rd == 0) ? 0 : sh.ebase[g0], E1 = sh.ebase[g1];
-        // ---- 3. evaluate the round's entries
-        if (E0 + tid < E1) {
-            const int e = sh.erow[E0 + tid];
-            const bool live = e >= lo && e <= hi && e < n_e;
-            double bt[KT], bf[KT];
-            int bp[KT];
-            relax_row<KT, FIRST, GUARD>(a, sh, u, live ? e : -1, bt, bf, bp);
-            unsigned pcm = 0u;
+    const int wi = (r_base >> 5) + g;
+    // ---- 3. rounds: whole groups whose entries fit the slots
+    int gs = 0, E0 = 0;
+    while (gs < 32) {
+        const unsigned okm = __ballot_sync(0xffffffffu, g >= gs && eend - E0 <= kSlots - 1);
+        const int ge = gs + __popc(okm);
+        const int E1 = __shfl_sync(0xffffffffu, eend, ge - 1);
+        for (int e0 = E0; e0 < E1; e0 += 32) {
+            const int en = e0 + lane;
+            if (en < E1) {
+                const int e = r_base - 1 + (int)w.erow[en];
+                const bool live = e >= lo && e <= hi && e < n_e;
+                double bt[KT], bf[KT];
+                int bp[KT];
+                relax_row<KT, FIRST, GUARD>(a, sh, u, live ? e : -1, bt, bf, bp);
+                unsigned pcm = 0u;
 #pragma unroll
-            for (int kk = 0; kk < KT; ++kk)
-                if (!FIRST && (!GUARD || kk < K) && live && bt[kk] < GBMW_STEP_INF)
-                    pcm |= src_path_change(a, sh, u, e, bp[kk]) << kk;
-            const int s = 1 + tid;
+                for (int kk = 0; kk < KT; ++kk)
+                    if (!FIRST && (!GUARD || kk < K) && live && bt[kk] < GBMW_STEP_INF)
+                        pcm |= src_path_change(a, sh, u, e, bp[kk]) << kk;
+                const int s = 1 + en - E0;
 #pragma unroll
-            for (int kk = 0; kk < KT; ++kk)
-                if (!GUARD || kk < K) { sh.et[s][kk] = bt[kk]; sh.ef[s][kk] = bf[kk]; sh.ep[s][kk] = bp[kk]; }
-            sh.epc[s] = pcm;
-        }
-        __syncthreads();
-        // ---- 4. write the round's groups: rows, change-bit words, flat-group bits
-        for (int g = g0 + warp; g < g1; g += nwarp) {
-            const int kd = sh.kind[g];
-            if (kd == 0) continue;
-            const int r0 = first_row + 32 * g;
-            const int wi = w_first + g;
-            // predecessor of the group's first row: the last entry before it (row r0 - 1)
-            const int sp = sh.ebase[g] - E0;             // its slot (0 = carried from the previous round)
-            const bool pred_ok = (g == 0) ? (sh.prev_ok != 0) : (sh.kind[g - 1] != 0);
-            const int s0 = sh.ebase[g] - E0 + 1;
-            if (kd == 1) {
-#pragma unroll
-                for (int kk = 0; kk < KT; ++kk) {
-                    if (GUARD && kk >= K) break;
-                    if (lane == kk) {
-                        reinterpret_cast<double2 *>(bout)[(int64_t)kk * n_e + r0] =
-                            make_double2(sh.et[s0][kk], sh.ef[s0][kk]);
-                        pout[(int64_t)kk * n_e + r0] = (uint16_t)sh.idx[sh.ep[s0][kk]];
-                        const bool same = pred_ok && sh.et[sp][kk] == sh.et[s0][kk] && sh.ef[sp][kk] == sh.ef[s0][kk] &&
-                                          sh.ep[sp][kk] == sh.ep[s0][kk] && !((sh.epc[s0] >> kk) & 1u);
-                        if (wi < sh.nw) fout[(int64_t)kk * sh.nw + wi] = same ? 0u : 1u;
-                    }
-                }
-            } else {
-                const unsigned segm = sh.seg[g];
-                const int e = r0 + lane;
-                const bool live = e >= lo && e <= hi;
-                const int s = s0 + __popc(segm & ((2u << lane) - 2u));   // segment holding row e
-                const bool start = lane > 0 && ((segm >> lane) & 1u);
-#pragma unroll
-                for (int kk = 0; kk < KT; ++kk) {
-                    if (GUARD && kk >= K) break;
-                    const double t = sh.et[s][kk], f = sh.ef[s][kk];
-                    const int pp = sh.ep[s][kk];
-                    if (live) {
-                        reinterpret_cast<double2 *>(bout)[(int64_t)kk * n_e + e] = make_double2(t, f);
-                        pout[(int64_t)kk * n_e + e] = (uint16_t)sh.idx[pp];
-                    }
-                    bool chg;
-                    const int sq = (lane == 0) ? sp : s - 1;     // the row before e
-                    const bool q_ok = (lane == 0) ? pred_ok : true;
-                    if (lane > 0 && !start) {
-                        chg = false;                             // no source changes: same row
-                    } else {
-                        chg = !(q_ok && sh.et[sq][kk] == t && sh.ef[sq][kk] == f && sh.ep[sq][kk] == pp &&
-                                !((sh.epc[s] >> kk) & 1u));
-                    }
-                    const unsigned m = __ballot_sync(0xffffffffu, chg);
-                    if (lane == 0 && wi < sh.nw) fout[(int64_t)kk * sh.nw + wi] = m;
-                }
+                for (int kk = 0; kk < KT; ++kk)
+                    if (!GUARD || kk < K) { w.et[s][kk] = bt[kk]; w.ef[s][kk] = bf[kk]; w.ep[s][kk] = (int16_t)bp[kk]; }
+                w.epc[s] = pcm;
             }
         }
-        __syncthreads();
-        // carry the round's last entry into slot 0 for the next round
-        if (rd + 1 < n_rounds) {
-            const int sl = E1 - E0;                      // slot of entry E1 - 1
-            if (tid < KT && (!GUARD || tid < K)) {
-                sh.et[0][tid] = sh.et[sl][tid]; sh.ef[0][tid] = sh.ef[sl][tid]; sh.ep[0][tid] = sh.ep[sl][tid];
+        __syncwarp();
+        const bool in_r = g >= gs && g < ge;
+        const int s0 = ebase - E0 + 1, sp = s0 - 1;    // sp = 0: carried from the previous round
+        // flat groups: one lane each
+        if (in_r && flat) {
+            for (int kk = 0; kk < K; ++kk) {
+                const double t = w.et[s0][kk], f = w.ef[s0][kk];
+                const int pp = w.ep[s0][kk];
+                reinterpret_cast<double2 *>(bout)[(int64_t)kk * n_e + r0] = make_double2(t, f);
+                pout[(int64_t)kk * n_e + r0] = (uint16_t)sh.idx[pp];
+                const bool same = pred_ok && w.et[sp][kk] == t && w.ef[sp][kk] == f && w.ep[sp][kk] == pp &&
+                                  !((w.epc[s0] >> kk) & 1u);
+                if (wi < sh.nw) fout[(int64_t)kk * sh.nw + wi] = same ? 0u : 1u;
             }
-            if (tid == 0) sh.epc[0] = sh.epc[sl];
-            __syncthreads();
         }
+        // evaluated groups: the warp writes their 32 rows, one lane per row
+        unsigned fullm = __ballot_sync(0xffffffffu, in_r && !dead && !flat);
+        while (fullm) {
+            const int gf = __ffs(fullm) - 1;
+            fullm &= fullm - 1u;
+            const unsigned segm = __shfl_sync(0xffffffffu, seg, gf);
+            const int sf = __shfl_sync(0xffffffffu, s0, gf);
+            const bool pok = __shfl_sync(0xffffffffu, pred_ok, gf);
+            const int e = r_base + 32 * gf + lane;
+            const bool live = e >= lo && e <= hi;
+            const int s = sf + __popc(segm & ((2u << lane) - 2u));      // entry of row e's segment
+            const bool start = lane > 0 && ((segm >> lane) & 1u);
+            const int sq = (lane == 0) ? sf - 1 : s - 1;                // entry of the row before e
+            const bool q_ok = (lane == 0) ? pok : true;
+#pragma unroll
+            for (int kk = 0; kk < KT; ++kk) {
+                if (GUARD && kk >= K) break;
+                const double t = w.et[s][kk], f = w.ef[s][kk];
+                const int pp = w.ep[s][kk];
+                if (live) {
+                    reinterpret_cast<double2 *>(bout)[(int64_t)kk * n_e + e] = make_double2(t, f);
+                    pout[(int64_t)kk * n_e + e] = (uint16_t)sh.idx[pp];
+                }
+                bool chg = false;                       // inside a segment: same row
+                if (lane == 0 || start)
+                    chg = !(q_ok && w.et[sq][kk] == t && w.ef[sq][kk] == f && w.ep[sq][kk] == pp &&
+                            !((w.epc[s] >> kk) & 1u));
+                const unsigned m = __ballot_sync(0xffffffffu, chg);
+                const int wf = (r_base >> 5) + gf;
+                if (lane == 0 && wf < sh.nw) fout[(int64_t)kk * sh.nw + wf] = m;
+            }
+        }
+        __syncwarp();
+        if (ge < 32) {                                   // carry the round's last entry
+            const int sl = E1 - E0;
+            for (int kk = lane; kk < K; kk += 32) { w.et[0][kk] = w.et[sl][kk]; w.ef[0][kk] = w.ef[sl][kk]; w.ep[0][kk] = w.ep[sl][kk]; }
+            if (lane == 0) w.epc[0] = w.epc[sl];
+            __syncwarp();
+        }
+        gs = ge;
+        E0 = E1;
     }
-    // ---- 5. dead groups' change words, flat-group mask words
-    for (int x = tid; x < kGroups * K; x += nthr) {
-        const int g = x / K, kk = x - g * K;
-        const int wi = w_first + g;
-        if (sh.kind[g] == 0 && wi < sh.nw) fout[(int64_t)kk * sh.nw + wi] = 0xffffffffu;   // never read as flat
-    }
-    if (tid < kGroups / 32) {
-        unsigned m = 0u;
-        for (int b = 0; b < 32; ++b) m |= (sh.kind[32 * tid + b] == 1 ? 1u : 0u) << b;
-        const int wi = (first_row >> 10) + tid;
-        if (wi < sh.gw) a.gflat[sh.gf_cur + wi] = m;
-    }
-    __syncthreads();
+    // ---- 4. dead groups' change words (never read as flat), the tile's flat-group word
+    if (dead && wi < sh.nw)
+        for (int kk = 0; kk < K; ++kk) fout[(int64_t)kk * sh.nw + wi] = 0xffffffffu;
+    const unsigned fm = __ballot_sync(0xffffffffu, flat);
+    if (lane == 0 && (r_base >> 10) < sh.gw) a.gflat[sh.gf_cur + (r_base >> 10)] = fm;
+    __syncwarp();
+    return (unsigned long long)n_ent * (unsigned long long)K;
 }
 
-// Live-tile work lists of every K2 launch of the chunk (one CTA per launch): tiles of the
-// rows [L_u, H_u] of each active problem, so K2 never fetches a dead tile.
+// Live-row work lists of every K2 launch of the chunk (one CTA per launch): per active
+// problem with live rows, its warp tiles [L_u / kWarpRows, H_u / kWarpRows].
 __global__ void __launch_bounds__(1024) k_step_lists(ChunkArgs a) {
-    __shared__ long long s_part[1024];
+    __shared__ int s_part[1024];
     const StepList sl = a.step_lists[blockIdx.x];
     const int tid = threadIdx.x;
     const int per = (sl.n + 1023) / 1024;
     const int x0 = sl.lo + min(sl.n, tid * per), x1 = sl.lo + min(sl.n, tid * per + per);
-    long long cnt = 0;
+    int cnt = 0;
     for (int x = x0; x < x1; ++x) {
         const DevProblem &p = a.probs[x];
-        const int lo = a.unit_lo[p.ustate_off + sl.u], hi = a.unit_hi[p.ustate_off + sl.u];
-        if (hi >= lo) cnt += (hi / kStepRows) - (lo / kStepRows) + 1;
+        if (a.unit_hi[p.ustate_off + sl.u] >= a.unit_lo[p.ustate_off + sl.u]) ++cnt;
     }
     s_part[tid] = cnt;
     __syncthreads();
     for (int off = 1; off < 1024; off <<= 1) {
-        const long long v = (tid >= off) ? s_part[tid - off] : 0;
+        const int v = (tid >= off) ? s_part[tid - off] : 0;
         __syncthreads();
         s_part[tid] += v;
         __syncthreads();
     }
-    long long at = sl.base + s_part[tid] - cnt;
+    int64_t at = sl.base + s_part[tid] - cnt;
     for (int x = x0; x < x1; ++x) {
         const DevProblem &p = a.probs[x];
         const int lo = a.unit_lo[p.ustate_off + sl.u], hi = a.unit_hi[p.ustate_off + sl.u];
         if (hi < lo) continue;
-        for (int t = lo / kStepRows; t <= hi / kStepRows; ++t) a.step_items[at++] = make_int4(x, t, lo, hi);
+        a.step_items[at++] = make_int4(x, lo / kWarpRows, hi / kWarpRows, 0);
     }
     if (tid == 1023) a.step_count[blockIdx.x] = s_part[1023];
 }
@@ -392,15 +343,16 @@ int launch_step_lists(const ChunkArgs &a, void *stream) {
     return (int)cudaGetLastError();
 }
 
+// CTAs take problems (dynamic counter); their warps take the problem's warp tiles.
 template <int GROUP, bool FIRST>
-__global__ void __launch_bounds__(kStepThreads, GROUP == 0 ? 3 : 2) k_dp_step(ChunkArgs a, int u, const int4 *items,
-                                                                              const int64_t *count,
-                                                                              unsigned long long *counter) {
+__global__ void __launch_bounds__(kStepThreads, GROUP == 0 ? 3 : (GROUP == 1 ? 2 : 1))
+    k_dp_step(ChunkArgs a, int u, const int4 *items, const int64_t *count, unsigned long long *counter) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     using SH = StepShared<GROUP == 0 ? 4 : (GROUP == 1 ? 8 : kMaxClasses)>;
     SH &sh = *reinterpret_cast<SH *>(smem_raw);
-    int q_prev = -1;
-    if (threadIdx.x == 0) sh.stat_rows = 0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    auto &w = sh.w[warp];
+    unsigned long long stat_rows = 0;
     const int64_t n_items = *count;
     while (true) {
         __syncthreads();
@@ -411,10 +363,7 @@ __global__ void __launch_bounds__(kStepThreads, GROUP == 0 ? 3 : 2) k_dp_step(Ch
         const int4 item = __ldg(items + t);
         const int q = item.x;
         const DevProblem &p = a.probs[q];
-        const int64_t first_row = (int64_t)item.y * kStepRows;
-        const int lo = item.z, hi = item.w;
-        if (q != q_prev) {
-            __syncthreads();
+        {
             const int S = p.S, K = p.K;
             const Cell *prev_cells = a.cells + p.cell_off + (int64_t)(u - 1) * S;
             const int32_t *ul = a.uniq + p.cell_off + (int64_t)(u - 1) * S;
@@ -426,43 +375,50 @@ __global__ void __launch_bounds__(kStepThreads, GROUP == 0 ? 3 : 2) k_dp_step(Ch
             }
             const double *r_u = a.rcls + p.r_off + (int64_t)u * K * K;
             for (int x = threadIdx.x; x < K * K; x += blockDim.x) sh.r[x] = r_u[x];
+            const int gw = (int)gflat_words(p.n_b + 1);
             if (!FIRST) {
-                const int gw = (int)gflat_words(p.n_b + 1);
                 const uint32_t *gsrc = a.gflat + p.gflat_off + (int64_t)(u - 2) * gw;
                 for (int x = threadIdx.x; x < gw; x += blockDim.x) sh.gfp[x] = gsrc[x];
             }
             if (threadIdx.x == 0) {
-                sh.S = nu; sh.K = K; sh.n_e = (int)(p.n_b + 1); sh.q = q;
+                sh.S = nu; sh.K = K; sh.n_e = (int)(p.n_b + 1);
                 sh.lo_prev = a.unit_lo[p.ustate_off + u - 1];
-                sh.lo = lo; sh.hi = hi;
+                sh.lo = a.unit_lo[p.ustate_off + u]; sh.hi = a.unit_hi[p.ustate_off + u];
                 sh.b_off = p.b_off; sh.par_off = p.par_off;
                 sh.f_off = p.flag_off; sh.nw = (int)flag_words(p.n_b + 1);
-                sh.gw = (int)gflat_words(p.n_b + 1);
-                sh.gf_cur = p.gflat_off + (int64_t)(u - 1) * sh.gw;
+                sh.gw = gw;
+                sh.gf_cur = p.gflat_off + (int64_t)(u - 1) * gw;
+                sh.tnext = item.y; sh.tlast = item.z;
             }
-            __syncthreads();
-            q_prev = q;
         }
+        __syncthreads();
         const int K = sh.K;
-        if (GROUP == 0) {
-            switch (K) {
-                case 1: step_tile<1, FIRST, false>(a, sh, u, (int)first_row); break;
-                case 2: step_tile<2, FIRST, false>(a, sh, u, (int)first_row); break;
-                case 3: step_tile<3, FIRST, false>(a, sh, u, (int)first_row); break;
-                default: step_tile<4, FIRST, false>(a, sh, u, (int)first_row); break;
+        while (true) {
+            int tile = 0;
+            if (lane == 0) tile = atomicAdd(&sh.tnext, 1);
+            tile = __shfl_sync(0xffffffffu, tile, 0);
+            if (tile > sh.tlast) break;
+            const int r_base = tile * kWarpRows;
+            if (GROUP == 0) {
+                switch (K) {
+                    case 1: stat_rows += warp_tile<1, FIRST, false>(a, sh, w, u, r_base, lane); break;
+                    case 2: stat_rows += warp_tile<2, FIRST, false>(a, sh, w, u, r_base, lane); break;
+                    case 3: stat_rows += warp_tile<3, FIRST, false>(a, sh, w, u, r_base, lane); break;
+                    default: stat_rows += warp_tile<4, FIRST, false>(a, sh, w, u, r_base, lane); break;
+                }
+            } else if (GROUP == 1) {
+                switch (K) {
+                    case 5: stat_rows += warp_tile<5, FIRST, false>(a, sh, w, u, r_base, lane); break;
+                    case 6: stat_rows += warp_tile<6, FIRST, false>(a, sh, w, u, r_base, lane); break;
+                    case 7: stat_rows += warp_tile<7, FIRST, false>(a, sh, w, u, r_base, lane); break;
+                    default: stat_rows += warp_tile<8, FIRST, false>(a, sh, w, u, r_base, lane); break;
+                }
+            } else {
+                stat_rows += warp_tile<kMaxClasses, FIRST, true>(a, sh, w, u, r_base, lane);
             }
-        } else if (GROUP == 1) {
-            switch (K) {
-                case 5: step_tile<5, FIRST, false>(a, sh, u, (int)first_row); break;
-                case 6: step_tile<6, FIRST, false>(a, sh, u, (int)first_row); break;
-                case 7: step_tile<7, FIRST, false>(a, sh, u, (int)first_row); break;
-                default: step_tile<8, FIRST, false>(a, sh, u, (int)first_row); break;
-            }
-        } else {
-            step_tile<kMaxClasses, FIRST, true>(a, sh, u, (int)first_row);
         }
     }
-    if (threadIdx.x == 0 && sh.stat_rows) atomicAdd(a.computed_cells, sh.stat_rows);
+    if (lane == 0 && stat_rows) atomicAdd(a.computed_cells, stat_rows);
 }
 
 int launch_dp_step(const ChunkArgs &a, int group, int u, const int4 *items, const int64_t *count, int64_t n_tiles,
