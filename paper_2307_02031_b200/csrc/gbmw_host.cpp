@@ -78,7 +78,7 @@ struct HostProb {
     int64_t n_b = 0;
     int64_t plan_off = 0, frontier_off = -1;
     // workspace footprint (elements)
-    int64_t n_cells = 0, n_r = 0, n_bcells = 0, n_par = 0, n_tiles = 0, n_step_tiles = 0, n_flagw = 0, n_gflat = 0;
+    int64_t n_cells = 0, n_r = 0, n_bcells = 0, n_par = 0, n_tiles = 0, n_step_tiles = 0, n_flagw = 0, n_rmap = 0;
     size_t ws_bytes = 0;
 };
 
@@ -89,7 +89,7 @@ struct Chunk {
     std::vector<int> n_active[kNumGroups];    // per group, per u: problems of the group with U > u
     int n_approx = 0;
     int Umax = 0, max_k = 1;
-    int64_t n_cells = 0, n_r = 0, n_bcells = 0, n_par = 0, n_tiles = 0, n_units = 0, n_flagw = 0, n_gflat = 0;
+    int64_t n_cells = 0, n_r = 0, n_bcells = 0, n_par = 0, n_tiles = 0, n_units = 0, n_flagw = 0, n_rmap = 0;
     size_t small_off = 0;          // byte offset of this chunk's descriptor block in the arena
     // offsets inside the descriptor block
     size_t o_probs, o_cellp, o_rp, o_stepp, o_cand, o_ccls, o_clsd, o_clst, o_uf, o_uc;
@@ -455,11 +455,11 @@ void prepare_problem(gbmw_batch &b, int pi, std::string *err) {
     h.n_tiles = (h.n_b + kSweepThreads - 1) / kSweepThreads;
     h.n_step_tiles = (n_e + kStepRows - 1) / kStepRows;
     h.n_flagw = (!approx && h.U > 1) ? (int64_t)h.K * flag_words(n_e) : 0;
-    h.n_gflat = approx ? 0 : (int64_t)(h.U > 1 ? h.U - 1 : 0) * gflat_words(n_e);
+    h.n_rmap = approx ? 0 : (int64_t)(h.U > 1 ? h.U - 1 : 0) * rmap_groups(n_e);
     h.ws_bytes = (size_t)h.n_cells * (sizeof(Cell) + sizeof(CellMem) + 4) + (size_t)h.U * 12 + (size_t)h.n_r * 8 + 8 +
                  (size_t)h.n_bcells * 2 * sizeof(TFCell) + (size_t)h.n_par * 2 +
                  (size_t)h.n_tiles * sizeof(SweepPartial) + sizeof(SweepPartial) + 36 + (size_t)h.n_flagw * 8 +
-                 (size_t)h.n_gflat * 4 + (size_t)(h.U > 1 ? h.U - 1 : 0) * 24;
+                 (size_t)h.n_rmap * 8 + (size_t)(h.U > 1 ? h.U - 1 : 0) * 24;
     h.gpu = true;
 }
 
@@ -473,7 +473,7 @@ size_t put(std::vector<char> &blob, const T *src, size_t n) {
 
 // chunk workspace layout (byte offsets from ws base)
 struct WsLayout {
-    size_t cells, cmem, rcls, bup, items, scount, tf0, tf1, chg0, chg1, gflat, par, parts, bestp, bound, ufirst, usorted, uprefix, uctr,
+    size_t cells, cmem, rcls, bup, items, scount, tf0, tf1, chg0, chg1, rmap, par, parts, bestp, bound, ufirst, usorted, uprefix, uctr,
         uniq, nuniq,
         ulo, uhi, ctr, total;
 };
@@ -490,7 +490,7 @@ WsLayout ws_layout(const Chunk &c) {
     w.tf1 = o; o = align_up(o + c.n_bcells * sizeof(TFCell));
     w.chg0 = o; o = align_up(o + c.n_flagw * 4);
     w.chg1 = o; o = align_up(o + c.n_flagw * 4);
-    w.gflat = o; o = align_up(o + c.n_gflat * 4);
+    w.rmap = o; o = align_up(o + c.n_rmap * 8);
     w.par = o; o = align_up(o + c.n_par * 2);
     w.parts = o; o = align_up(o + c.n_tiles * sizeof(SweepPartial));
     w.bestp = o; o = align_up(o + c.probs.size() * sizeof(SweepPartial));
@@ -608,7 +608,7 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
             d.cand_off = sit->second.first; d.class_off = sit->second.second; d.unit_off = uit->second;
             d.ustate_off = (int32_t)c.n_units;
             d.flag_off = c.n_flagw;
-            d.gflat_off = c.n_gflat;
+            d.rmap_off = c.n_rmap;
             d.layer_begin = P.layer_begin; d.strat_begin = P.strat_begin; d.result_index = pi;
             d.n_sweep_tiles = (int32_t)h.n_tiles;
             dps.push_back(d);
@@ -617,7 +617,7 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
             stepp.push_back(stepp.back() + h.n_step_tiles);
             c.n_units += h.U;
             c.n_flagw += h.n_flagw;
-            c.n_gflat += h.n_gflat;
+            c.n_rmap += h.n_rmap;
             c.Umax = std::max(c.Umax, h.U);
             if (P.flags & GBMW_APPROX) c.n_approx++;
             c.max_k = std::max(c.max_k, h.K);
@@ -667,7 +667,9 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
                 sl.u = u; sl.lo = lo; sl.n = na; sl.pad_ = 0; sl.base = c.n_items;
                 c.slists.push_back(sl);
                 c.slist_group.push_back(g);
-                c.n_items += na;                   // one item per active problem
+                // items of <= kItemTiles warp tiles: a problem's warp tiles number at most
+                // 2 * (its 2048-row tiles), so ceil(that / kItemTiles) <= that / kItemTiles + 1
+                c.n_items += 2 * (c.step_prefix[lo + na] - c.step_prefix[lo]) / kItemTiles + na;
             }
         c.o_slists = put(blob, c.slists.data(), c.slists.size()) - base;
         c.small_bytes = blob.size() - base;
@@ -797,7 +799,7 @@ ChunkArgs chunk_args(gbmw_batch *b, const Chunk &c, char *ws, size_t chunk_index
     a.TF[1] = (TFCell *)(ws + w.tf1);
     a.chg[0] = (uint32_t *)(ws + w.chg0);
     a.chg[1] = (uint32_t *)(ws + w.chg1);
-    a.gflat = (uint32_t *)(ws + w.gflat);
+    a.rmap = (int2 *)(ws + w.rmap);
     a.par = (uint16_t *)(ws + w.par);
     a.partials = (SweepPartial *)(ws + w.parts);
     a.best = (SweepPartial *)(ws + w.bestp);
@@ -853,7 +855,7 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
         for (size_t s = 0; s < c.slists.size(); ++s) {
             const StepList &sl = c.slists[s];
             const int g = c.slist_group[s];
-            const int64_t ub = sl.n;
+            const int64_t ub = (s + 1 < c.slists.size() ? c.slists[s + 1].base : c.n_items) - sl.base;   // item bound
             if ((rc = launch_dp_step(a, g, sl.u, a.step_items + sl.base, a.step_count + s, ub,
                                      a.counters + (size_t)sl.u * kNumGroups + g, st)))
                 return cuda_fail(ctx, rc, "K2 launch");

@@ -23,6 +23,7 @@ constexpr int kMaxClasses = 16;
 constexpr int kMaxStrats = 512;      // smem staging of per-strategy constants
 constexpr int kStepThreads = 256;    // threads per K2 CTA
 constexpr int kStepRows = 2048;      // rows per K2 tile (64 groups of 32)
+constexpr int kItemTiles = 8;        // K2 work item: at most this many 1024-row warp tiles of one problem
 
 // change-bit words per class column of n_e rows (one spare word for 2-word window reads)
 #if defined(__CUDACC__)
@@ -30,13 +31,14 @@ __host__ __device__
 #endif
 inline int64_t flag_words(int64_t n_e) { return (n_e + 31) / 32 + 2; }
 
-// flat-group mask words per unit: one bit per aligned 32-row group of B_u
+// row-map entries per unit: one per aligned 32-row group of B_u (see stored_row)
 #if defined(__CUDACC__)
 __host__ __device__
 #endif
-inline int64_t gflat_words(int64_t n_e) { return ((n_e + 31) / 32 + 31) / 32 + 1; }
+inline int64_t rmap_groups(int64_t n_e) { return (n_e + 31) / 32; }
 constexpr int kSweepThreads = 256;   // rows per K3 tile
 constexpr int kSweepWK = 4096;       // (unit, strategy) pairs staged in shared memory by K3b
+constexpr int kSweepRmap = 1536;     // row-map entries of B_{U-1} staged in shared memory by K3b (n_e <= 49152)
 constexpr int kMaxSweepRanks = 4096; // >= sweep tiles of one problem: ceil(GBMW_MAX_BUCKETS / kSweepThreads)
 
 // K2 is instantiated per class-count group so a problem with few classes does not
@@ -81,7 +83,7 @@ struct DevProblem {
     int32_t n_sweep_tiles;
     int32_t ustate_off;     // into per-problem unit state: nuniq / unit_lo / unit_hi (U)
     int64_t flag_off;       // into the change-bit buffers (K * flag_words(n_e) words)
-    int64_t gflat_off;      // into the flat-group masks ((U-1) * gflat_words(n_e) words)
+    int64_t rmap_off;       // into the row maps ((U-1) * rmap_groups(n_e) entries)
 };
 
 #if defined(__CUDACC__)
@@ -99,11 +101,17 @@ __device__ __forceinline__ bool window_flat(int x0, int lo, const uint32_t *flag
     return (v & 0x7fffffffull) == 0ull;
 }
 
-// B_u stores one representative row (the first) per flat 32-row group; every reader of a
-// B_u row or of its argmin goes through this (gf_u = that unit's flat-group mask).
-__device__ __forceinline__ int flat_row(const uint32_t *gf_u, int row) {
-    const int g = row >> 5;
-    return ((__ldg(gf_u + (g >> 5)) >> (g & 31)) & 1u) ? (row & ~31) : row;
+// B_u is stored only at its "stored rows" (the first live row of every 1024-row tile and
+// every row where some column changes); between two stored rows every column is constant
+// in value, argmin and argmin path.  The row map of unit u holds per 32-row group g
+// {bit x: row 32g + x is stored, last stored row before the group}; every reader of a
+// B_u row or of its argmin maps the row to the stored row at or before it (rows >= L_u).
+__device__ __forceinline__ int stored_row(int2 m, int row) {
+    const unsigned b = (unsigned)m.x & (0xffffffffu >> (31 - (row & 31)));
+    return b ? (row & ~31) + 31 - __clz(b) : m.y;
+}
+__device__ __forceinline__ int stored_row(const int2 *rm_u, int row) {
+    return stored_row(__ldg(rm_u + (row >> 5)), row);
 }
 #endif
 
@@ -156,7 +164,7 @@ struct ChunkArgs {
     unsigned long long *bup;      // per problem, bits of max O_b (all >= 0)
     TFCell *TF[2];
     uint32_t *chg[2];             // change bits of B_u (ping-pong with TF): bit x = row x != row x-1
-    uint32_t *gflat;              // per unit u >= 1: bit g = 32-row group g of B_u is flat (stored once)
+    int2 *rmap;                   // per unit u >= 1: row map of B_u (stored rows, see stored_row)
     unsigned long long *computed_cells;   // class cells K2 evaluated (rows x K), per chunk
     uint16_t *par;
     SweepPartial *partials;       // per sweep tile: best bucket of an unsafe (K3b) or collapsed-DP (K3r) tile

@@ -156,8 +156,8 @@ __global__ void k_dedupe(ChunkArgs a) {
 struct RowCtx {
     const int32_t *w; const int32_t *k; const double *c; const double *ef;
     const TFCell *bin;
-    const uint32_t *gf;  // flat-group mask of B_{U-1} (rows of flat groups are stored once)
-    const uint32_t *gfs; // the same mask staged in shared memory, or nullptr
+    const int2 *rm;      // row map of B_{U-1} (B is stored only at its stored rows)
+    const int2 *rms;     // the same map staged in shared memory, or nullptr
     int64_t n_e;
     int64_t lo;        // rows of B_{U-1} below L_{U-1} are +inf (never written)
     bool init;
@@ -167,13 +167,8 @@ __device__ __forceinline__ void row_value(const RowCtx &r, int64_t e, int j, dou
     const int w = r.w[j];
     if (e - w < r.lo) { T = GBMW_INF; F = GBMW_INF; return; }
     if (r.init) { T = r.c[j]; F = r.ef[j]; return; }
-    int row;
-    if (r.gfs) {
-        const int x = (int)(e - w), g = x >> 5;
-        row = ((r.gfs[g >> 5] >> (g & 31)) & 1u) ? (x & ~31) : x;
-    } else {
-        row = flat_row(r.gf, (int)(e - w));
-    }
+    const int x = (int)(e - w);
+    const int row = r.rms ? stored_row(r.rms[x >> 5], x) : stored_row(r.rm, x);
     const int64_t src = (int64_t)r.k[j] * r.n_e + row;
     const double2 v = __ldg(reinterpret_cast<const double2 *>(r.bin + src));
     T = v.x + r.c[j];
@@ -187,12 +182,12 @@ __device__ __forceinline__ void backtrack(const ChunkArgs &a, const DevProblem &
     const int64_t n_e = p.n_b + 1;
     const Cell *cells = a.cells + p.cell_off;
     const uint16_t *par = a.par + p.par_off;
-    const int gw = (int)gflat_words(n_e);
+    const int64_t ng = rmap_groups(n_e);
     path[U - 1] = (uint16_t)j;
     for (int u = U - 1; u >= 1; --u) {
         const Cell c = cells[(int64_t)u * S + j];
         e -= c.w;
-        const int er = flat_row(a.gflat + p.gflat_off + (int64_t)(u - 1) * gw, (int)e);
+        const int er = stored_row(a.rmap + p.rmap_off + (int64_t)(u - 1) * ng, (int)e);
         j = par[((int64_t)(u - 1) * K + c.k) * n_e + er];
         path[u - 1] = (uint16_t)j;
     }
@@ -200,21 +195,21 @@ __device__ __forceinline__ void backtrack(const ChunkArgs &a, const DevProblem &
 
 // Same walk with (weight, class) of every (unit, strategy) staged in shared memory, packed
 // as weight << 4 | class (weight <= n_b + 1 < 2^27): the chain per unit is then one global
-// load (the argmin) instead of three.
+// load (the argmin) after the row-map entry.  rms: row map of the last unit in shared
+// memory, or nullptr.
 __device__ __forceinline__ void backtrack_wk(const ChunkArgs &a, const DevProblem &p, int64_t e, int j,
-                                             uint16_t *path, const uint32_t *wk, const uint32_t *gfs) {
+                                             uint16_t *path, const uint32_t *wk, const int2 *rms) {
     const int U = p.U, S = p.S, K = p.K;
     const int64_t n_e = p.n_b + 1;
     const uint16_t *par = a.par + p.par_off;
-    const int gw = (int)gflat_words(n_e);
+    const int64_t ng = rmap_groups(n_e);
     path[U - 1] = (uint16_t)j;
     for (int u = U - 1; u >= 1; --u) {
         const uint32_t c = wk[u * S + j];
         e -= (int64_t)(c >> 4);
-        const int er = (u == U - 1) ? [&] {
-            const int x = (int)e, g = x >> 5;
-            return ((gfs[g >> 5] >> (g & 31)) & 1u) ? (x & ~31) : x;
-        }() : flat_row(a.gflat + p.gflat_off + (int64_t)(u - 1) * gw, (int)e);
+        const int x = (int)e;
+        const int er = (u == U - 1 && rms) ? stored_row(rms[x >> 5], x)
+                                           : stored_row(a.rmap + p.rmap_off + (int64_t)(u - 1) * ng, x);
         j = par[((int64_t)(u - 1) * K + (int)(c & 15u)) * n_e + er];
         path[u - 1] = (uint16_t)j;
     }
@@ -383,7 +378,7 @@ __global__ void k_sweep_safe(ChunkArgs a) {
             const int64_t n_e = p.n_b + 1;
             const int64_t lo = (last == 0) ? 0 : a.unit_lo[p.ustate_off + last];
             const TFCell *bin = a.TF[last & 1] + p.b_off;
-            const uint32_t *gf = a.gflat + p.gflat_off + (int64_t)(last >= 1 ? last - 1 : 0) * gflat_words(n_e);
+            const int2 *rm = a.rmap + p.rmap_off + (int64_t)(last >= 1 ? last - 1 : 0) * rmap_groups(n_e);
             for (int n = lane; n < S; n += 32) {
                 const int j = ul[n];
                 const Cell c = lc[j];
@@ -393,7 +388,7 @@ __global__ void k_sweep_safe(ChunkArgs a) {
                     T = c.c; F = c.ef;
                 } else {
                     const double2 v = __ldg(reinterpret_cast<const double2 *>(
-                        bin + (int64_t)c.k * n_e + flat_row(gf, (int)(e_s - c.w))));
+                        bin + (int64_t)c.k * n_e + stored_row(rm, (int)(e_s - c.w))));
                     T = v.x + c.c;
                     F = v.y + c.ef;
                 }
@@ -515,7 +510,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
     __shared__ int red_j[kSweepThreads / 32];
     __shared__ double sOB[kMaxStrats];                  // O_b of one layer of the last unit
     __shared__ uint32_t sWK[kSweepWK];                  // weight << 4 | class per (unit, strategy)
-    __shared__ uint32_t sGF[(GBMW_MAX_BUCKETS + 1 + 1023) / 1024 + 2];   // flat-group mask of B_{U-1}
+    __shared__ int2 sRM[kSweepRmap];                    // row map of B_{U-1}, when it fits
     __shared__ long long s_next;
     __shared__ int s_skip;
     const long long total = a.uprefix[kMaxSweepRanks];
@@ -547,10 +542,10 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
                 for (int x = threadIdx.x; x < p.U * S; x += blockDim.x)
                     sWK[x] = ((uint32_t)cells[x].w << 4) | (uint32_t)cells[x].k;
             }
-            if (last >= 1) {
-                const int gw = (int)gflat_words(p.n_b + 1);
-                const uint32_t *gsrc = a.gflat + p.gflat_off + (int64_t)(last - 1) * gw;
-                for (int x = threadIdx.x; x < gw; x += blockDim.x) sGF[x] = gsrc[x];
+            if (last >= 1 && rmap_groups(p.n_b + 1) <= kSweepRmap) {
+                const int ng = (int)rmap_groups(p.n_b + 1);
+                const int2 *src = a.rmap + p.rmap_off + (int64_t)(last - 1) * ng;
+                for (int x = threadIdx.x; x < ng; x += blockDim.x) sRM[x] = src[x];
             }
             __syncthreads();
             q_prev = q;
@@ -562,8 +557,8 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
         r.init = (last == 0);
         r.lo = (last == 0) ? 0 : a.unit_lo[p.ustate_off + last];
         r.bin = a.TF[last & 1] + p.b_off;
-        r.gf = a.gflat + p.gflat_off + (int64_t)(last >= 1 ? last - 1 : 0) * gflat_words(p.n_b + 1);
-        r.gfs = sGF;
+        r.rm = a.rmap + p.rmap_off + (int64_t)(last >= 1 ? last - 1 : 0) * rmap_groups(p.n_b + 1);
+        r.rms = (rmap_groups(p.n_b + 1) <= kSweepRmap) ? sRM : nullptr;
         unsigned long long *bound = a.bound + 2 * q;
         const int64_t e = 1 + (int64_t)tile * kSweepThreads + threadIdx.x;
         // whole-tile prune: every candidate of the tile has T >= t0(top row) (the rank-0 time
@@ -642,7 +637,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
                     continue;
                 }
                 ++n_checks;
-                if (wk_smem) backtrack_wk(a, p, e, nj, path, sWK, sGF);
+                if (wk_smem) backtrack_wk(a, p, e, nj, path, sWK, r.rms);
                 else backtrack(a, p, e, nj, path);
                 if (plan_e_all(a, p, path) <= p.budget) {
                     mt = nt; me = e; mj = nj;
@@ -742,8 +737,8 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_rows(ChunkArgs a) {
     r.init = (last == 0);
     r.lo = (last == 0) ? 0 : a.unit_lo[p.ustate_off + last];
     r.bin = a.TF[last & 1] + p.b_off;
-    r.gf = a.gflat + p.gflat_off + (int64_t)(last >= 1 ? last - 1 : 0) * gflat_words(p.n_b + 1);
-    r.gfs = nullptr;
+    r.rm = a.rmap + p.rmap_off + (int64_t)(last >= 1 ? last - 1 : 0) * rmap_groups(p.n_b + 1);
+    r.rms = nullptr;
     if (e <= p.n_b) {
         double t0 = GBMW_INF, f0 = GBMW_INF;
         int j0 = -1;

@@ -1,24 +1,20 @@
-// gbmw_step.cu — K2, the min-plus layer step of the stage search, run-length aware.
+// gbmw_step.cu — K2, the min-plus layer step of the stage search, breakpoint-driven.
 //
 // Reference step (dpsearch.py:261-280), restated per source row e' and target class k
 // (DESIGN.md §3):
 //   B_u[e',k] = lexmin_i (T_{u-1}[e',i] + R_u[cls i, k], F_{u-1}[e',i], i),
 //   T_{u-1}[e',i] = B_{u-1}[e'-w_{u-1,i}, cls i].t + time_c[u-1,i]   (init row for u == 1).
-// B is a step function of e': most aligned 32-row groups see the same (T, F) vector in
-// every row (SURVEY-scale configs: 86-100 % of live groups).  A group is "flat" when,
-// for every distinct source strategy i, the 32-row source window of column cls(i) of
-// B_{u-1} contains no change point; its 32 outputs are then the output of its first
-// row, computed once.  Change points of B_u are emitted as one bit per (class, row)
-// (bit x = row x differs from row x-1), exactly; a spurious 1 bit would only cost
-// work, never exactness.
-//
-// One CTA processes one tile of kStepRows rows of one problem:
-//   1. classify the tile's 32-row groups (dead / flat / full) from the change bits,
-//   2. compute the list of rows that need it: every row of a full group (one warp per
-//      group, lanes in row order), one row per flat group, and the row before the
-//      tile (for the first change bit),
-//   3. write flat groups' rows from shared memory, and the change-bit words.
-// Tie-break T1 (lexicographic (cand, F, i), first i) is the one of every row.
+// B is a step function of e' with few steps.  Row e' of B_u can differ from row e'-1 only
+// where some source T_{u-1}[., i] changes between them — a "breakpoint": a change bit of
+// column cls(i) of B_{u-1} at row e' - w_{u-1,i} (or the row where the source turns
+// finite).  K2 evaluates B_u only at the breakpoints (plus the first live row of every
+// 1024-row tile), and stores a row only where some column actually changes (value, argmin,
+// or the path behind the argmin) or where a tile starts: the "stored rows".  Every reader
+// maps a row to the stored row at or before it through the unit's row map (stored_row).
+// Outputs per step: the per-column change bits of B_u (bit x: row x differs from row
+// x-1, exact up to spurious 1 bits at tile starts, which only cost work downstream), the
+// row map, and (t, f, argmin) at the stored rows.  Tie-break T1 (lexicographic
+// (cand, F, i), first i) is the reference's for every row.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -28,21 +24,15 @@ namespace gbmw {
 
 #define GBMW_STEP_INF __longlong_as_double(0x7ff0000000000000LL)
 
-constexpr int kStepIB = 4;                  // strategy batch: independent loads in flight
 constexpr int kClassifyIB = 8;              // window checks per thread in flight
-constexpr int kGroups = kStepRows / 32;     // 32-row groups per tile
-constexpr int kMaxGfWords = (int)(((GBMW_MAX_BUCKETS + 1 + 31) / 32 + 31) / 32 + 1);   // gflat_words(max n_e)
+constexpr int kStepIB = 4;                  // sources per lane in flight (lane-per-row evaluation)
+constexpr int kCoopMax = 6;                 // tiles with more entries evaluate a row per lane
+constexpr int kWarpRows = 1024;             // rows per warp tile: 32 groups of 32
 
-constexpr int kWarpRows = 1024;             // rows per warp tile: 32 groups, one flat-mask word
-constexpr int kSlots = 65;                  // evaluated rows held per round (+ slot 0: carry)
-
-// Per-warp scratch of one tile.  Entry = an evaluated row; entry 0 is the row before the tile.
-template <int KM>
+// Per-warp scratch of one tile: its entries (evaluated rows) in row order.
 struct WarpScratch {
-    double et[kSlots][KM], ef[kSlots][KM];  // per round: slot 0 = last entry of the previous round
-    int16_t ep[kSlots][KM];                 // argmin (position in the distinct list)
-    unsigned epc[kSlots];                   // bit kk: the argmin's source path changes at this row
-    uint16_t erow[kWarpRows + 2];           // row of each entry, relative to the tile's first row - 1
+    uint16_t erow[kWarpRows];               // row of each entry, relative to the tile's first row
+    uint16_t echg[kWarpRows];               // bit kk: column kk changes at the entry's row
 };
 
 // KM: class capacity of the instantiation (4 / 8 / kMaxClasses)
@@ -51,78 +41,163 @@ struct StepShared {
     Cell cell[kMaxStrats];                  // distinct source strategies of unit u-1 (ascending)
     int idx[kMaxStrats];                    // their strategy index
     double r[KM * KM];
-    uint32_t gfp[kMaxGfWords];              // flat-group mask of B_{u-1} (read redirection, flat_row)
-    int S, K, n_e, lo_prev, lo, hi, nw, gw;
+    int S, K, n_e, lo_prev, lo, hi, nw;
     int64_t b_off, par_off, f_off;
-    int64_t gf_cur;                         // flat-group mask of B_u (offset into a.gflat)
+    int64_t rm_prev, rm_cur;                // row maps of B_{u-1} and B_u (offsets into a.rmap)
     int64_t next;
-    int tnext, tlast;                       // warp tiles of the current problem
-    WarpScratch<KM> w[kStepThreads / 32];
+    int tnext, tlast;                       // warp tiles of the current item
+    WarpScratch w[kStepThreads / 32];
 };
 
-// K lexmins of one source row e' (T1 tie-break).  Rows outside [lo_prev + w, hi] read +inf.
+// lexicographic (t, f, key) order; key = 2 * position in the distinct list + path bit, so
+// comparing keys compares positions (T1: first i among equal (cand, F))
+__device__ __forceinline__ bool lex3_less(double t1, double f1, int k1, double t2, double f2, int k2) {
+    return t1 < t2 || (t1 == t2 && (f1 < f2 || (f1 == f2 && k1 < k2)));
+}
+
+// K lexmins of row e of B_u, the warp cooperating: lane l takes the distinct sources
+// l, l + 32, ...; a butterfly leaves the result in every lane.  key = 2 * argmin position +
+// (1 if the argmin's source row is a change point of its column of B_{u-1}).
 template <int KT, bool FIRST, bool GUARD, class SH>
-__device__ __forceinline__ void relax_row(const ChunkArgs &a, const SH &sh, int u, int e,
-                                          double *bt, double *bf, int *bp) {
+__device__ __forceinline__ void eval_row(const ChunkArgs &a, const SH &sh, int u, int e, int lane,
+                                         double *bt, double *bf, int *bk) {
     const int S = sh.S, K = GUARD ? sh.K : KT;
-    const int n_e = sh.n_e, lo_prev = FIRST ? 0 : sh.lo_prev, hi = sh.hi;
+    const int n_e = sh.n_e, lo_prev = FIRST ? 0 : sh.lo_prev;
     const TFCell *bin = a.TF[(u - 1) & 1] + sh.b_off;
+    const int2 *rm = a.rmap + sh.rm_prev;
+    const uint32_t *fin = a.chg[(u - 1) & 1] + sh.f_off;
 #pragma unroll
-    for (int kk = 0; kk < KT; ++kk) { bt[kk] = GBMW_STEP_INF; bf[kk] = GBMW_STEP_INF; bp[kk] = 0; }
-    const bool row_ok = e >= 0 && e <= hi;
+    for (int kk = 0; kk < KT; ++kk) { bt[kk] = GBMW_STEP_INF; bf[kk] = GBMW_STEP_INF; bk[kk] = 0x7fffffff; }
+    for (int i0 = 0; i0 < S; i0 += 64) {
+        double T[2], F[2];
+        int key[2];
+        bool ok[2];
+        int src_[2], k_[2];
+        int2 m[2];
+        uint32_t cw[2];
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+            const int i = i0 + 32 * b + lane;
+            const Cell c = sh.cell[i < S ? i : 0];
+            const int src = e - c.w;
+            src_[b] = src; k_[b] = c.k;
+            ok[b] = i < S && src >= lo_prev;
+            T[b] = GBMW_STEP_INF; F[b] = GBMW_STEP_INF; key[b] = 2 * i;
+            if (!FIRST && ok[b]) {
+                m[b] = __ldg(rm + (src >> 5));
+                cw[b] = __ldg(fin + (int64_t)c.k * sh.nw + (src >> 5));
+            }
+        }
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+            if (!ok[b]) continue;
+            const int i = i0 + 32 * b + lane;
+            const Cell c = sh.cell[i];
+            if (FIRST) {                       // init row, dpsearch.py:255-259
+                T[b] = c.c; F[b] = c.ef;
+            } else {
+                const int row = stored_row(m[b], src_[b]);
+                const double2 v = __ldg(reinterpret_cast<const double2 *>(bin + (int64_t)k_[b] * n_e + row));
+                T[b] = v.x + c.c;
+                F[b] = v.y + c.ef;
+                key[b] |= (int)((cw[b] >> (src_[b] & 31)) & 1u);
+            }
+        }
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+            const int i = i0 + 32 * b + lane;
+            if (i >= S) continue;
+            const double *rrow = sh.r + k_[b] * K;
+#pragma unroll
+            for (int kk = 0; kk < KT; ++kk) {
+                if (!GUARD || kk < K) {
+                    const double cand = T[b] + rrow[kk];
+                    const bool better = lex3_less(cand, F[b], key[b], bt[kk], bf[kk], bk[kk]);
+                    bt[kk] = better ? cand : bt[kk];
+                    bf[kk] = better ? F[b] : bf[kk];
+                    bk[kk] = better ? key[b] : bk[kk];
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int kk = 0; kk < KT; ++kk) {
+        if (GUARD && kk >= K) break;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const double ot = __shfl_xor_sync(0xffffffffu, bt[kk], off);
+            const double of = __shfl_xor_sync(0xffffffffu, bf[kk], off);
+            const int ok2 = __shfl_xor_sync(0xffffffffu, bk[kk], off);
+            if (lex3_less(ot, of, ok2, bt[kk], bf[kk], bk[kk])) { bt[kk] = ot; bf[kk] = of; bk[kk] = ok2; }
+        }
+    }
+}
+
+// The same K lexmins computed by one lane alone (rows with many entries: a lane per row).
+// e < 0: no row (results +inf).  Sources in ascending order, kStepIB loads in flight.
+template <int KT, bool FIRST, bool GUARD, class SH>
+__device__ __forceinline__ void eval_row_lane(const ChunkArgs &a, const SH &sh, int u, int e,
+                                              double *bt, double *bf, int *bk) {
+    const int S = sh.S, K = GUARD ? sh.K : KT;
+    const int n_e = sh.n_e, lo_prev = FIRST ? 0 : sh.lo_prev;
+    const TFCell *bin = a.TF[(u - 1) & 1] + sh.b_off;
+    const int2 *rm = a.rmap + sh.rm_prev;
+    const uint32_t *fin = a.chg[(u - 1) & 1] + sh.f_off;
+#pragma unroll
+    for (int kk = 0; kk < KT; ++kk) { bt[kk] = GBMW_STEP_INF; bf[kk] = GBMW_STEP_INF; bk[kk] = 0x7fffffff; }
     for (int i0 = 0; i0 < S; i0 += kStepIB) {
         double T[kStepIB], F[kStepIB];
+        int key[kStepIB], src_[kStepIB];
+        bool ok[kStepIB];
+        int2 m[kStepIB];
+        uint32_t cw[kStepIB];
 #pragma unroll
         for (int b = 0; b < kStepIB; ++b) {
             const int i = i0 + b;
             const Cell c = sh.cell[i < S ? i : 0];
             const int src = e - c.w;
-            T[b] = GBMW_STEP_INF; F[b] = GBMW_STEP_INF;
-            if (i < S && row_ok && src >= lo_prev) {
-                if (FIRST) {                       // init row, dpsearch.py:255-259
-                    T[b] = c.c; F[b] = c.ef;
-                } else {
-                    const int g = src >> 5;
-                    const int rs = ((sh.gfp[g >> 5] >> (g & 31)) & 1u) ? (src & ~31) : src;
-                    const double2 v = __ldg(reinterpret_cast<const double2 *>(bin + c.k * n_e + rs));
-                    T[b] = v.x + c.c;
-                    F[b] = v.y + c.ef;
-                }
+            src_[b] = src;
+            ok[b] = i < S && e >= 0 && src >= lo_prev;
+            T[b] = GBMW_STEP_INF; F[b] = GBMW_STEP_INF; key[b] = 2 * i;
+            if (!FIRST && ok[b]) {
+                m[b] = __ldg(rm + (src >> 5));
+                cw[b] = __ldg(fin + (int64_t)c.k * sh.nw + (src >> 5));
+            }
+        }
+#pragma unroll
+        for (int b = 0; b < kStepIB; ++b) {
+            if (!ok[b]) continue;
+            const Cell c = sh.cell[i0 + b];
+            if (FIRST) {
+                T[b] = c.c; F[b] = c.ef;
+            } else {
+                const int row = stored_row(m[b], src_[b]);
+                const double2 v = __ldg(reinterpret_cast<const double2 *>(bin + (int64_t)c.k * n_e + row));
+                T[b] = v.x + c.c;
+                F[b] = v.y + c.ef;
+                key[b] |= (int)((cw[b] >> (src_[b] & 31)) & 1u);
             }
         }
 #pragma unroll
         for (int b = 0; b < kStepIB; ++b) {
             const int i = i0 + b;
             if (i >= S) break;
-            const int ck = sh.cell[i].k;
-            const double *rrow = sh.r + ck * K;
+            const double *rrow = sh.r + sh.cell[i].k * K;
 #pragma unroll
             for (int kk = 0; kk < KT; ++kk) {
                 if (!GUARD || kk < K) {
                     const double cand = T[b] + rrow[kk];
-                    const bool better = (cand < bt[kk]) || (cand == bt[kk] && F[b] < bf[kk]);
+                    const bool better = lex3_less(cand, F[b], key[b], bt[kk], bf[kk], bk[kk]);
                     bt[kk] = better ? cand : bt[kk];
                     bf[kk] = better ? F[b] : bf[kk];
-                    bp[kk] = better ? i : bp[kk];       // position in the distinct list
+                    bk[kk] = better ? key[b] : bk[kk];
                 }
             }
         }
     }
 }
 
-// Path-change bit of row e with argmin source n: the source cell B_{u-1}[e - w_n] differs
-// (in value, argmin or path) from B_{u-1}[e - 1 - w_n].  Rows of B_u are "equal" (no change
-// bit) only when value, argmin and the whole path behind match, so a flat group's first
-// row stands for every row of the group, argmin chain included.
-template <class SH>
-__device__ __forceinline__ unsigned src_path_change(const ChunkArgs &a, const SH &sh, int u, int e, int n) {
-    const Cell c = sh.cell[n];
-    const int src = e - c.w;
-    const uint32_t *fl = a.chg[(u - 1) & 1] + sh.f_off + (int64_t)c.k * sh.nw;
-    return (__ldg(fl + (src >> 5)) >> (src & 31)) & 1u;
-}
-
-// Segment starts of a 32-row group contributed by one source: rows x (1..31) where the
+// Breakpoints of a 32-row group contributed by one source: rows x (0..31) where the
 // source's value T_{u-1}[r0 + x, i] may differ from row r0 + x - 1, i.e. the change bits of
 // its window [x0, x0 + 31] of column cls(i) (rows below lo are +inf and constant).
 __device__ __forceinline__ unsigned window_segments(unsigned long long v, int x0, int lo) {
@@ -131,24 +206,28 @@ __device__ __forceinline__ unsigned window_segments(unsigned long long v, int x0
         const int j0 = lo - x0;                          // first finite row of the window
         m = (m & ~((2u << j0) - 1u)) | (1u << j0);
     }
-    return m & 0xfffffffeu;
+    return m;
 }
 
 // One warp tile (kWarpRows rows) of B_u, by one warp; lane g owns 32-row group g.
-// Rows are evaluated only where some source changes (segment starts): B_u is constant
-// between them in value, argmin and path.  A group without segment starts is flat (its
-// first row stands for all, stored once); other groups are evaluated at their first row and
-// at each segment start and written in full.  Warp-synchronous: no CTA barrier.
-template <int KT, bool FIRST, bool GUARD, class SH, class WS>
-__device__ __forceinline__ unsigned long long warp_tile(const ChunkArgs &a, const SH &sh, WS &w, int u, int r_base,
-                                                        int lane) {
+//   1. lane g: the breakpoints of its group (change bits of every source window); the
+//      tile's first live row is always an entry (it anchors the row map);
+//   2. the warp evaluates the entries in row order (eval_row) and compares each with the
+//      previous one: unchanged columns keep their change bit 0; entries where some column
+//      changes (and the first) are stored;
+//   3. lane g writes its group's change-bit words and row-map entry.
+// Warp-synchronous: no CTA barrier.
+template <int KT, bool FIRST, bool GUARD, class SH>
+__device__ __forceinline__ unsigned long long warp_tile(const ChunkArgs &a, const SH &sh, WarpScratch &w, int u,
+                                                        int r_base, int lane) {
     const int K = GUARD ? sh.K : KT;
     const int n_e = sh.n_e, lo = sh.lo, hi = sh.hi, S = sh.S;
     const int g = lane, r0 = r_base + 32 * g, r1 = r0 + 31;
     const bool dead = r1 < lo || r0 > hi;
     const bool whole = r0 >= lo && r1 <= hi;
-    // ---- 1. segment starts of the group: change bits of every source window
-    unsigned seg = (dead || whole) ? 0u : 0xfffffffeu;      // partial groups: every row evaluated
+    const int f0 = r_base > lo ? r_base : lo;            // first live row of the tile (<= hi)
+    // ---- 1. breakpoints of the group
+    unsigned seg = 0u;
     if (whole) {
         const uint32_t *fin = a.chg[(u - 1) & 1] + sh.f_off;
         for (int n0 = 0; n0 < S; n0 += kClassifyIB) {
@@ -174,7 +253,7 @@ __device__ __forceinline__ unsigned long long warp_tile(const ChunkArgs &a, cons
                 const int xs = xs_[b];
                 if (FIRST) {
                     const int j = -xs;                   // T_0[e, i] is finite from e = w_i on
-                    seg |= (j >= 1 && j <= 31) ? (1u << j) : 0u;
+                    seg |= (j >= 0 && j <= 31) ? (1u << j) : 0u;
                 } else {
                     const int xl = xs < 0 ? 0 : xs;
                     const unsigned long long v =
@@ -183,131 +262,145 @@ __device__ __forceinline__ unsigned long long warp_tile(const ChunkArgs &a, cons
                 }
             }
         }
+    } else if (!dead) {                                  // partial group: every live row
+        const int a0 = lo > r0 ? lo - r0 : 0, a1 = hi < r1 ? hi - r0 : 31;
+        seg = (0xffffffffu >> (31 - a1)) & ~((1u << a0) - 1u);
     }
-    const bool flat = whole && seg == 0u;
-    // ---- 2. entries: 0 = row r_base - 1, then per group its first row and segment starts
-    const int cnt = dead ? 0 : 1 + __popc(seg);
+    // the tile's first live row: an entry; its change bits are exact only when it is no breakpoint
+    const bool first_bp = __shfl_sync(0xffffffffu, (seg >> ((f0 - r_base) & 31)) & 1u, (f0 - r_base) >> 5) != 0u;
+    if (!dead && f0 >= r0 && f0 <= r1) seg |= 1u << (f0 - r0);
+    // ---- 2. entries in row order
+    const int cnt = __popc(seg);
     int incl = cnt;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
         const int v = __shfl_up_sync(0xffffffffu, incl, off);
         if (lane >= off) incl += v;
     }
-    const int ebase = 1 + incl - cnt, eend = 1 + incl;
-    const int n_ent = 1 + __shfl_sync(0xffffffffu, incl, 31);
-    if (!dead) {
+    const int ebase = incl - cnt;
+    const int n_ent = __shfl_sync(0xffffffffu, incl, 31);
+    {
         int at = ebase;
-        w.erow[at++] = (uint16_t)(32 * g + 1);
         unsigned m = seg;
         while (m) {
             const int x = __ffs(m) - 1;
             m &= m - 1u;
-            w.erow[at++] = (uint16_t)(32 * g + 1 + x);
+            w.erow[at++] = (uint16_t)(32 * g + x);
         }
     }
-    if (lane == 0) w.erow[0] = 0;
-    const bool prev_ok = r_base - 1 >= lo && r_base - 1 <= hi;
-    const bool dead_prev = __shfl_up_sync(0xffffffffu, dead, 1);
-    const bool pred_ok = (g == 0) ? prev_ok : !dead_prev;
     __syncwarp();
     TFCell *bout = a.TF[u & 1] + sh.b_off;
     uint16_t *pout = a.par + sh.par_off + (int64_t)(u - 1) * K * n_e;
-    uint32_t *fout = a.chg[u & 1] + sh.f_off;
-    const int wi = (r_base >> 5) + g;
-    // ---- 3. rounds: whole groups whose entries fit the slots
-    int gs = 0, E0 = 0;
-    while (gs < 32) {
-        const unsigned okm = __ballot_sync(0xffffffffu, g >= gs && eend - E0 <= kSlots - 1);
-        const int ge = gs + __popc(okm);
-        const int E1 = __shfl_sync(0xffffffffu, eend, ge - 1);
-        for (int e0 = E0; e0 < E1; e0 += 32) {
-            const int en = e0 + lane;
-            if (en < E1) {
-                const int e = r_base - 1 + (int)w.erow[en];
-                const bool live = e >= lo && e <= hi && e < n_e;
-                double bt[KT], bf[KT];
-                int bp[KT];
-                relax_row<KT, FIRST, GUARD>(a, sh, u, live ? e : -1, bt, bf, bp);
-                unsigned pcm = 0u;
+    if (n_ent <= kCoopMax) {
+        // few entries: the warp evaluates each row together (sources across lanes)
+        double pt = GBMW_STEP_INF, pf = GBMW_STEP_INF;   // lane kk: column kk of the previous entry
+        int pk = 0;
+        for (int n = 0; n < n_ent; ++n) {
+            const int e = r_base + (int)w.erow[n];
+            double bt[KT], bf[KT];
+            int bk[KT];
+            eval_row<KT, FIRST, GUARD>(a, sh, u, e, lane, bt, bf, bk);
+            double ct = GBMW_STEP_INF, cf = GBMW_STEP_INF;    // lane kk: column kk of this entry
+            int ck = 0;
 #pragma unroll
-                for (int kk = 0; kk < KT; ++kk)
-                    if (!FIRST && (!GUARD || kk < K) && live && bt[kk] < GBMW_STEP_INF)
-                        pcm |= src_path_change(a, sh, u, e, bp[kk]) << kk;
-                const int s = 1 + en - E0;
+            for (int kk = 0; kk < KT; ++kk)
+                if (lane == kk) { ct = bt[kk]; cf = bf[kk]; ck = bk[kk]; }
+            const bool col = lane < K;
+            unsigned chg;
+            if (n == 0) {
+                chg = (e == lo || first_bp) ? 0xffffffffu : 0u;
+            } else {
+                const bool same = ct == pt && cf == pf && (ck >> 1) == (pk >> 1) && !(ck & 1);
+                chg = __ballot_sync(0xffffffffu, col && !same);
+            }
+            chg &= (1u << K) - 1u;
+            if ((n == 0 || chg) && col) {
+                reinterpret_cast<double2 *>(bout)[(int64_t)lane * n_e + e] = make_double2(ct, cf);
+                pout[(int64_t)lane * n_e + e] = (uint16_t)sh.idx[ck >> 1];
+            }
+            if (lane == 0) w.echg[n] = (uint16_t)chg;
+            pt = ct; pf = cf; pk = ck;
+        }
+    } else {
+        // many entries: a lane per row, rounds of 32 rows; the previous entry of lane l is
+        // lane l - 1 (lane 31 of the previous round for lane 0)
+        double ct_[KT], cf_[KT];
+        int ck_[KT];
 #pragma unroll
-                for (int kk = 0; kk < KT; ++kk)
-                    if (!GUARD || kk < K) { w.et[s][kk] = bt[kk]; w.ef[s][kk] = bf[kk]; w.ep[s][kk] = (int16_t)bp[kk]; }
-                w.epc[s] = pcm;
-            }
-        }
-        __syncwarp();
-        const bool in_r = g >= gs && g < ge;
-        const int s0 = ebase - E0 + 1, sp = s0 - 1;    // sp = 0: carried from the previous round
-        // flat groups: one lane each
-        if (in_r && flat) {
-            for (int kk = 0; kk < K; ++kk) {
-                const double t = w.et[s0][kk], f = w.ef[s0][kk];
-                const int pp = w.ep[s0][kk];
-                reinterpret_cast<double2 *>(bout)[(int64_t)kk * n_e + r0] = make_double2(t, f);
-                pout[(int64_t)kk * n_e + r0] = (uint16_t)sh.idx[pp];
-                const bool same = pred_ok && w.et[sp][kk] == t && w.ef[sp][kk] == f && w.ep[sp][kk] == pp &&
-                                  !((w.epc[s0] >> kk) & 1u);
-                if (wi < sh.nw) fout[(int64_t)kk * sh.nw + wi] = same ? 0u : 1u;
-            }
-        }
-        // evaluated groups: the warp writes their 32 rows, one lane per row
-        unsigned fullm = __ballot_sync(0xffffffffu, in_r && !dead && !flat);
-        while (fullm) {
-            const int gf = __ffs(fullm) - 1;
-            fullm &= fullm - 1u;
-            const unsigned segm = __shfl_sync(0xffffffffu, seg, gf);
-            const int sf = __shfl_sync(0xffffffffu, s0, gf);
-            const bool pok = __shfl_sync(0xffffffffu, pred_ok, gf);
-            const int e = r_base + 32 * gf + lane;
-            const bool live = e >= lo && e <= hi;
-            const int s = sf + __popc(segm & ((2u << lane) - 2u));      // entry of row e's segment
-            const bool start = lane > 0 && ((segm >> lane) & 1u);
-            const int sq = (lane == 0) ? sf - 1 : s - 1;                // entry of the row before e
-            const bool q_ok = (lane == 0) ? pok : true;
+        for (int kk = 0; kk < KT; ++kk) { ct_[kk] = GBMW_STEP_INF; cf_[kk] = GBMW_STEP_INF; ck_[kk] = 0; }
+        for (int n0 = 0; n0 < n_ent; n0 += 32) {
+            const int n = n0 + lane;
+            const int e = (n < n_ent) ? r_base + (int)w.erow[n] : -1;
+            double bt[KT], bf[KT];
+            int bk[KT];
+            eval_row_lane<KT, FIRST, GUARD>(a, sh, u, e, bt, bf, bk);
+            unsigned chg = 0u;
 #pragma unroll
             for (int kk = 0; kk < KT; ++kk) {
                 if (GUARD && kk >= K) break;
-                const double t = w.et[s][kk], f = w.ef[s][kk];
-                const int pp = w.ep[s][kk];
-                if (live) {
-                    reinterpret_cast<double2 *>(bout)[(int64_t)kk * n_e + e] = make_double2(t, f);
-                    pout[(int64_t)kk * n_e + e] = (uint16_t)sh.idx[pp];
+                double pt = __shfl_up_sync(0xffffffffu, bt[kk], 1);
+                double pf = __shfl_up_sync(0xffffffffu, bf[kk], 1);
+                int pk = __shfl_up_sync(0xffffffffu, bk[kk], 1);
+                const double ct31 = __shfl_sync(0xffffffffu, ct_[kk], 31);
+                const double cf31 = __shfl_sync(0xffffffffu, cf_[kk], 31);
+                const int ck31 = __shfl_sync(0xffffffffu, ck_[kk], 31);
+                if (lane == 0) { pt = ct31; pf = cf31; pk = ck31; }
+                const bool same = bt[kk] == pt && bf[kk] == pf && (bk[kk] >> 1) == (pk >> 1) && !(bk[kk] & 1);
+                chg |= same ? 0u : (1u << kk);
+                ct_[kk] = bt[kk]; cf_[kk] = bf[kk]; ck_[kk] = bk[kk];
+            }
+            if (n == 0) chg = (e == lo || first_bp) ? 0xffffu : 0u;
+            chg &= (1u << K) - 1u;
+            if (n < n_ent) {
+                if (n == 0 || chg) {
+#pragma unroll
+                    for (int kk = 0; kk < KT; ++kk) {
+                        if (GUARD && kk >= K) break;
+                        reinterpret_cast<double2 *>(bout)[(int64_t)kk * n_e + e] = make_double2(bt[kk], bf[kk]);
+                        pout[(int64_t)kk * n_e + e] = (uint16_t)sh.idx[bk[kk] >> 1];
+                    }
                 }
-                bool chg = false;                       // inside a segment: same row
-                if (lane == 0 || start)
-                    chg = !(q_ok && w.et[sq][kk] == t && w.ef[sq][kk] == f && w.ep[sq][kk] == pp &&
-                            !((w.epc[s] >> kk) & 1u));
-                const unsigned m = __ballot_sync(0xffffffffu, chg);
-                const int wf = (r_base >> 5) + gf;
-                if (lane == 0 && wf < sh.nw) fout[(int64_t)kk * sh.nw + wf] = m;
+                w.echg[n] = (uint16_t)chg;
             }
         }
-        __syncwarp();
-        if (ge < 32) {                                   // carry the round's last entry
-            const int sl = E1 - E0;
-            for (int kk = lane; kk < K; kk += 32) { w.et[0][kk] = w.et[sl][kk]; w.ef[0][kk] = w.ef[sl][kk]; w.ep[0][kk] = w.ep[sl][kk]; }
-            if (lane == 0) w.epc[0] = w.epc[sl];
-            __syncwarp();
-        }
-        gs = ge;
-        E0 = E1;
     }
-    // ---- 4. dead groups' change words (never read as flat), the tile's flat-group word
-    if (dead && wi < sh.nw)
-        for (int kk = 0; kk < K; ++kk) fout[(int64_t)kk * sh.nw + wi] = 0xffffffffu;
-    const unsigned fm = __ballot_sync(0xffffffffu, flat);
-    if (lane == 0 && (r_base >> 10) < sh.gw) a.gflat[sh.gf_cur + (r_base >> 10)] = fm;
+    __syncwarp();
+    // ---- 3. change-bit words and row map of the group
+    int last = -1;                                       // last stored row of the group
+    unsigned sbits = 0u;
+    uint32_t cwd[KT];
+#pragma unroll
+    for (int kk = 0; kk < KT; ++kk) cwd[kk] = 0u;
+    for (int n = ebase; n < ebase + cnt; ++n) {
+        const int x = w.erow[n] & 31;
+        const unsigned m = w.echg[n];
+#pragma unroll
+        for (int kk = 0; kk < KT; ++kk) cwd[kk] |= ((m >> kk) & 1u) << x;
+        if (m || n == 0) { sbits |= 1u << x; last = r_base + (int)w.erow[n]; }   // entry 0: the tile's anchor
+    }
+    int before = last;                                   // exclusive max-scan over the groups
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, before, off);
+        if (lane >= off) before = max(before, v);
+    }
+    before = __shfl_up_sync(0xffffffffu, before, 1);
+    if (lane == 0) before = -1;
+    const int wi = (r_base >> 5) + g;
+    if (!dead) {
+        uint32_t *fout = a.chg[u & 1] + sh.f_off;
+#pragma unroll
+        for (int kk = 0; kk < KT; ++kk)
+            if (!GUARD || kk < K) fout[(int64_t)kk * sh.nw + wi] = cwd[kk];
+        a.rmap[sh.rm_cur + wi] = make_int2((int)sbits, before);
+    }
     __syncwarp();
     return (unsigned long long)n_ent * (unsigned long long)K;
 }
 
 // Live-row work lists of every K2 launch of the chunk (one CTA per launch): per active
-// problem with live rows, its warp tiles [L_u / kWarpRows, H_u / kWarpRows].
+// problem with live rows, its warp tiles [L_u / kWarpRows, H_u / kWarpRows] in items of
+// at most kItemTiles tiles (a large problem spreads over many CTAs).
 __global__ void __launch_bounds__(1024) k_step_lists(ChunkArgs a) {
     __shared__ int s_part[1024];
     const StepList sl = a.step_lists[blockIdx.x];
@@ -317,7 +410,8 @@ __global__ void __launch_bounds__(1024) k_step_lists(ChunkArgs a) {
     int cnt = 0;
     for (int x = x0; x < x1; ++x) {
         const DevProblem &p = a.probs[x];
-        if (a.unit_hi[p.ustate_off + sl.u] >= a.unit_lo[p.ustate_off + sl.u]) ++cnt;
+        const int lo = a.unit_lo[p.ustate_off + sl.u], hi = a.unit_hi[p.ustate_off + sl.u];
+        if (hi >= lo) cnt += (hi / kWarpRows - lo / kWarpRows) / kItemTiles + 1;
     }
     s_part[tid] = cnt;
     __syncthreads();
@@ -332,7 +426,9 @@ __global__ void __launch_bounds__(1024) k_step_lists(ChunkArgs a) {
         const DevProblem &p = a.probs[x];
         const int lo = a.unit_lo[p.ustate_off + sl.u], hi = a.unit_hi[p.ustate_off + sl.u];
         if (hi < lo) continue;
-        a.step_items[at++] = make_int4(x, lo / kWarpRows, hi / kWarpRows, 0);
+        const int t1 = hi / kWarpRows;
+        for (int t0 = lo / kWarpRows; t0 <= t1; t0 += kItemTiles)
+            a.step_items[at++] = make_int4(x, t0, min(t1, t0 + kItemTiles - 1), 0);
     }
     if (tid == 1023) a.step_count[blockIdx.x] = s_part[1023];
 }
@@ -343,9 +439,9 @@ int launch_step_lists(const ChunkArgs &a, void *stream) {
     return (int)cudaGetLastError();
 }
 
-// CTAs take problems (dynamic counter); their warps take the problem's warp tiles.
+// CTAs take items (dynamic counter); their warps take the item's warp tiles.
 template <int GROUP, bool FIRST>
-__global__ void __launch_bounds__(kStepThreads, GROUP == 0 ? 3 : (GROUP == 1 ? 2 : 1))
+__global__ void __launch_bounds__(kStepThreads, GROUP <= 1 ? 2 : 1)
     k_dp_step(ChunkArgs a, int u, const int4 *items, const int64_t *count, unsigned long long *counter) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     using SH = StepShared<GROUP == 0 ? 4 : (GROUP == 1 ? 8 : kMaxClasses)>;
@@ -375,19 +471,15 @@ __global__ void __launch_bounds__(kStepThreads, GROUP == 0 ? 3 : (GROUP == 1 ? 2
             }
             const double *r_u = a.rcls + p.r_off + (int64_t)u * K * K;
             for (int x = threadIdx.x; x < K * K; x += blockDim.x) sh.r[x] = r_u[x];
-            const int gw = (int)gflat_words(p.n_b + 1);
-            if (!FIRST) {
-                const uint32_t *gsrc = a.gflat + p.gflat_off + (int64_t)(u - 2) * gw;
-                for (int x = threadIdx.x; x < gw; x += blockDim.x) sh.gfp[x] = gsrc[x];
-            }
             if (threadIdx.x == 0) {
+                const int64_t ng = rmap_groups(p.n_b + 1);
                 sh.S = nu; sh.K = K; sh.n_e = (int)(p.n_b + 1);
                 sh.lo_prev = a.unit_lo[p.ustate_off + u - 1];
                 sh.lo = a.unit_lo[p.ustate_off + u]; sh.hi = a.unit_hi[p.ustate_off + u];
                 sh.b_off = p.b_off; sh.par_off = p.par_off;
                 sh.f_off = p.flag_off; sh.nw = (int)flag_words(p.n_b + 1);
-                sh.gw = gw;
-                sh.gf_cur = p.gflat_off + (int64_t)(u - 1) * gw;
+                sh.rm_prev = p.rmap_off + (int64_t)(u >= 2 ? u - 2 : 0) * ng;
+                sh.rm_cur = p.rmap_off + (int64_t)(u - 1) * ng;
                 sh.tnext = item.y; sh.tlast = item.z;
             }
         }
