@@ -686,7 +686,7 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
     b->o_results = o; o = align_up(o + b->problems.size() * sizeof(gbmw_result));
     b->o_plans = o; o = align_up(o + (size_t)b->total_plan * sizeof(int32_t));
     b->o_frontier = o; o = align_up(o + (size_t)b->total_frontier * sizeof(double));
-    b->o_stats = o; o = align_up(o + 5 * (b->chunks.size() + 1) * 8);
+    b->o_stats = o; o = align_up(o + (5 * (b->chunks.size() + 1) + 64) * 8);
     b->arena_size = std::max<size_t>(o, 256);
     for (Chunk &c : b->chunks) c.small_off += o_blob;
     cudaSetDevice(ctx->device);
@@ -820,6 +820,9 @@ ChunkArgs chunk_args(gbmw_batch *b, const Chunk &c, char *ws, size_t chunk_index
     a.live_cells = (unsigned long long *)(arena + b->o_stats) + chunk_index;
     a.sweep_stats = (unsigned long long *)(arena + b->o_stats) + 2 * (b->chunks.size() + 1);
     a.computed_cells = (unsigned long long *)(arena + b->o_stats) + (b->chunks.size() + 1) + chunk_index;
+    // GBMW_K2_HIST=1: per-tile entry-count histogram of K2 (log2 bins: tiles, entries), printed by run
+    static const bool k2_hist = getenv("GBMW_K2_HIST") && getenv("GBMW_K2_HIST")[0] == '1';
+    a.k2_hist = k2_hist ? (unsigned long long *)(arena + b->o_stats) + 5 * (b->chunks.size() + 1) : nullptr;
     return a;
 }
 
@@ -835,7 +838,7 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
     b->timing.total_ms = b->timing.dp_ms = b->timing.sweep_ms = b->timing.tables_ms = b->timing.finalize_ms = 0.f;
     b->timing.n_launches = 0;
     cudaStream_t st = ctx->stream;
-    cudaMemsetAsync((char *)b->arena + b->o_stats, 0, 5 * (b->chunks.size() + 1) * 8, st);
+    cudaMemsetAsync((char *)b->arena + b->o_stats, 0, (5 * (b->chunks.size() + 1) + 64) * 8, st);
     for (Chunk &c : b->chunks) {
         for (auto &e : c.ev)
             if (!e) cudaEventCreate(&e);
@@ -905,6 +908,14 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
         b->timing.dp_bytes = cells * 18.0 + computed * 16.0;
         b->timing.dp_cells = computed;
         b->timing.live_cells = cells;
+        if (getenv("GBMW_K2_HIST") && getenv("GBMW_K2_HIST")[0] == '1') {
+            std::vector<unsigned long long> h(64);
+            cudaMemcpy(h.data(), (char *)b->arena + b->o_stats + 5 * (nc + 1) * 8, 64 * 8, cudaMemcpyDeviceToHost);
+            fprintf(stderr, "K2 tiles by entries (bin: <2^b entries): ");
+            for (int i = 0; i < 32; ++i)
+                if (h[i]) fprintf(stderr, "[%d] %llu tiles %llu ent  ", i, h[i], h[32 + i]);
+            fprintf(stderr, "\n");
+        }
     }
     b->ran = true;
     ctx->last = b->timing;

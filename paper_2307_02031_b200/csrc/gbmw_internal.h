@@ -166,6 +166,7 @@ struct ChunkArgs {
     uint32_t *chg[2];             // change bits of B_u (ping-pong with TF): bit x = row x != row x-1
     int2 *rmap;                   // per unit u >= 1: row map of B_u (stored rows, see stored_row)
     unsigned long long *computed_cells;   // class cells K2 evaluated (rows x K), per chunk
+    unsigned long long *k2_hist;  // debug (GBMW_K2_HIST=1): [32] tiles, [32] entries by log2 entry count; or null
     uint16_t *par;
     SweepPartial *partials;       // per sweep tile: best bucket of an unsafe (K3b) or collapsed-DP (K3r) tile
     SweepPartial *best;           // per problem: best safe bucket (K3a)

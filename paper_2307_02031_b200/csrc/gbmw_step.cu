@@ -29,11 +29,14 @@ constexpr int kStepIB = 4;                  // sources per lane in flight (lane-
 constexpr int kCoopMax = 6;                 // tiles with more entries evaluate a row per lane
 constexpr int kWarpRows = 1024;             // rows per warp tile: 32 groups of 32
 
-// Per-warp scratch of one tile: its entries (evaluated rows) in row order.
-struct WarpScratch {
+// Scratch of one warp tile of the item: its entries (rows to evaluate) in row order.
+struct TileScratch {
     uint16_t erow[kWarpRows];               // row of each entry, relative to the tile's first row
     uint16_t echg[kWarpRows];               // bit kk: column kk changes at the entry's row
 };
+
+constexpr int kItemWarps = kStepThreads / 32;
+static_assert(kItemTiles <= kItemWarps, "one warp classifies each tile of an item");
 
 // KM: class capacity of the instantiation (4 / 8 / kMaxClasses)
 template <int KM>
@@ -45,8 +48,12 @@ struct StepShared {
     int64_t b_off, par_off, f_off;
     int64_t rm_prev, rm_cur;                // row maps of B_{u-1} and B_u (offsets into a.rmap)
     int64_t next;
-    int tnext, tlast;                       // warp tiles of the current item
-    WarpScratch w[kStepThreads / 32];
+    int t0, nt;                             // the item's warp tiles [t0, t0 + nt)
+    int n_ent[kItemTiles];                  // entries per tile
+    int first_bp[kItemTiles];               // the tile's first live row is a breakpoint
+    int rpre[kItemTiles + 1];               // evaluation rounds before tile t
+    int rnext;                              // round counter
+    TileScratch tile[kItemTiles];
 };
 
 // lexicographic (t, f, key) order; key = 2 * position in the distinct list + path bit, so
@@ -55,11 +62,13 @@ __device__ __forceinline__ bool lex3_less(double t1, double f1, int k1, double t
     return t1 < t2 || (t1 == t2 && (f1 < f2 || (f1 == f2 && k1 < k2)));
 }
 
-// K lexmins of row e of B_u, the warp cooperating: lane l takes the distinct sources
-// l, l + 32, ...; a butterfly leaves the result in every lane.  key = 2 * argmin position +
-// (1 if the argmin's source row is a change point of its column of B_{u-1}).
+// K lexmins of row e of B_u by a segment of L lanes (L = 1, 2, 4, ..., 32; lane offset
+// l in the segment takes the distinct sources l, l + L, ...); a butterfly inside the
+// segment leaves the result in each of its lanes.  e < 0: no row (+inf).
+// key = 2 * argmin position + (1 if the argmin's source row is a change point of its
+// column of B_{u-1}: the path behind the argmin changes there).
 template <int KT, bool FIRST, bool GUARD, class SH>
-__device__ __forceinline__ void eval_row(const ChunkArgs &a, const SH &sh, int u, int e, int lane,
+__device__ __forceinline__ void eval_row(const ChunkArgs &a, const SH &sh, int u, int e, int L, int l,
                                          double *bt, double *bf, int *bk) {
     const int S = sh.S, K = GUARD ? sh.K : KT;
     const int n_e = sh.n_e, lo_prev = FIRST ? 0 : sh.lo_prev;
@@ -68,20 +77,19 @@ __device__ __forceinline__ void eval_row(const ChunkArgs &a, const SH &sh, int u
     const uint32_t *fin = a.chg[(u - 1) & 1] + sh.f_off;
 #pragma unroll
     for (int kk = 0; kk < KT; ++kk) { bt[kk] = GBMW_STEP_INF; bf[kk] = GBMW_STEP_INF; bk[kk] = 0x7fffffff; }
-    for (int i0 = 0; i0 < S; i0 += 64) {
-        double T[2], F[2];
-        int key[2];
-        bool ok[2];
-        int src_[2], k_[2];
-        int2 m[2];
-        uint32_t cw[2];
+    for (int i0 = l; i0 < S; i0 += kStepIB * L) {
+        double T[kStepIB], F[kStepIB];
+        int key[kStepIB], src_[kStepIB], k_[kStepIB];
+        bool ok[kStepIB];
+        int2 m[kStepIB];
+        uint32_t cw[kStepIB];
 #pragma unroll
-        for (int b = 0; b < 2; ++b) {
-            const int i = i0 + 32 * b + lane;
+        for (int b = 0; b < kStepIB; ++b) {
+            const int i = i0 + b * L;
             const Cell c = sh.cell[i < S ? i : 0];
             const int src = e - c.w;
             src_[b] = src; k_[b] = c.k;
-            ok[b] = i < S && src >= lo_prev;
+            ok[b] = i < S && e >= 0 && src >= lo_prev;
             T[b] = GBMW_STEP_INF; F[b] = GBMW_STEP_INF; key[b] = 2 * i;
             if (!FIRST && ok[b]) {
                 m[b] = __ldg(rm + (src >> 5));
@@ -89,10 +97,9 @@ __device__ __forceinline__ void eval_row(const ChunkArgs &a, const SH &sh, int u
             }
         }
 #pragma unroll
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < kStepIB; ++b) {
             if (!ok[b]) continue;
-            const int i = i0 + 32 * b + lane;
-            const Cell c = sh.cell[i];
+            const Cell c = sh.cell[i0 + b * L];
             if (FIRST) {                       // init row, dpsearch.py:255-259
                 T[b] = c.c; F[b] = c.ef;
             } else {
@@ -104,9 +111,8 @@ __device__ __forceinline__ void eval_row(const ChunkArgs &a, const SH &sh, int u
             }
         }
 #pragma unroll
-        for (int b = 0; b < 2; ++b) {
-            const int i = i0 + 32 * b + lane;
-            if (i >= S) continue;
+        for (int b = 0; b < kStepIB; ++b) {
+            if (i0 + b * L >= S) break;
             const double *rrow = sh.r + k_[b] * K;
 #pragma unroll
             for (int kk = 0; kk < KT; ++kk) {
@@ -120,79 +126,14 @@ __device__ __forceinline__ void eval_row(const ChunkArgs &a, const SH &sh, int u
             }
         }
     }
+    for (int off = L >> 1; off > 0; off >>= 1) {
 #pragma unroll
-    for (int kk = 0; kk < KT; ++kk) {
-        if (GUARD && kk >= K) break;
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
+        for (int kk = 0; kk < KT; ++kk) {
+            if (GUARD && kk >= K) break;
             const double ot = __shfl_xor_sync(0xffffffffu, bt[kk], off);
             const double of = __shfl_xor_sync(0xffffffffu, bf[kk], off);
             const int ok2 = __shfl_xor_sync(0xffffffffu, bk[kk], off);
             if (lex3_less(ot, of, ok2, bt[kk], bf[kk], bk[kk])) { bt[kk] = ot; bf[kk] = of; bk[kk] = ok2; }
-        }
-    }
-}
-
-// The same K lexmins computed by one lane alone (rows with many entries: a lane per row).
-// e < 0: no row (results +inf).  Sources in ascending order, kStepIB loads in flight.
-template <int KT, bool FIRST, bool GUARD, class SH>
-__device__ __forceinline__ void eval_row_lane(const ChunkArgs &a, const SH &sh, int u, int e,
-                                              double *bt, double *bf, int *bk) {
-    const int S = sh.S, K = GUARD ? sh.K : KT;
-    const int n_e = sh.n_e, lo_prev = FIRST ? 0 : sh.lo_prev;
-    const TFCell *bin = a.TF[(u - 1) & 1] + sh.b_off;
-    const int2 *rm = a.rmap + sh.rm_prev;
-    const uint32_t *fin = a.chg[(u - 1) & 1] + sh.f_off;
-#pragma unroll
-    for (int kk = 0; kk < KT; ++kk) { bt[kk] = GBMW_STEP_INF; bf[kk] = GBMW_STEP_INF; bk[kk] = 0x7fffffff; }
-    for (int i0 = 0; i0 < S; i0 += kStepIB) {
-        double T[kStepIB], F[kStepIB];
-        int key[kStepIB], src_[kStepIB];
-        bool ok[kStepIB];
-        int2 m[kStepIB];
-        uint32_t cw[kStepIB];
-#pragma unroll
-        for (int b = 0; b < kStepIB; ++b) {
-            const int i = i0 + b;
-            const Cell c = sh.cell[i < S ? i : 0];
-            const int src = e - c.w;
-            src_[b] = src;
-            ok[b] = i < S && e >= 0 && src >= lo_prev;
-            T[b] = GBMW_STEP_INF; F[b] = GBMW_STEP_INF; key[b] = 2 * i;
-            if (!FIRST && ok[b]) {
-                m[b] = __ldg(rm + (src >> 5));
-                cw[b] = __ldg(fin + (int64_t)c.k * sh.nw + (src >> 5));
-            }
-        }
-#pragma unroll
-        for (int b = 0; b < kStepIB; ++b) {
-            if (!ok[b]) continue;
-            const Cell c = sh.cell[i0 + b];
-            if (FIRST) {
-                T[b] = c.c; F[b] = c.ef;
-            } else {
-                const int row = stored_row(m[b], src_[b]);
-                const double2 v = __ldg(reinterpret_cast<const double2 *>(bin + (int64_t)c.k * n_e + row));
-                T[b] = v.x + c.c;
-                F[b] = v.y + c.ef;
-                key[b] |= (int)((cw[b] >> (src_[b] & 31)) & 1u);
-            }
-        }
-#pragma unroll
-        for (int b = 0; b < kStepIB; ++b) {
-            const int i = i0 + b;
-            if (i >= S) break;
-            const double *rrow = sh.r + sh.cell[i].k * K;
-#pragma unroll
-            for (int kk = 0; kk < KT; ++kk) {
-                if (!GUARD || kk < K) {
-                    const double cand = T[b] + rrow[kk];
-                    const bool better = lex3_less(cand, F[b], key[b], bt[kk], bf[kk], bk[kk]);
-                    bt[kk] = better ? cand : bt[kk];
-                    bf[kk] = better ? F[b] : bf[kk];
-                    bk[kk] = better ? key[b] : bk[kk];
-                }
-            }
         }
     }
 }
@@ -209,24 +150,17 @@ __device__ __forceinline__ unsigned window_segments(unsigned long long v, int x0
     return m;
 }
 
-// One warp tile (kWarpRows rows) of B_u, by one warp; lane g owns 32-row group g.
-//   1. lane g: the breakpoints of its group (change bits of every source window); the
-//      tile's first live row is always an entry (it anchors the row map);
-//   2. the warp evaluates the entries in row order (eval_row) and compares each with the
-//      previous one: unchanged columns keep their change bit 0; entries where some column
-//      changes (and the first) are stored;
-//   3. lane g writes its group's change-bit words and row-map entry.
-// Warp-synchronous: no CTA barrier.
-template <int KT, bool FIRST, bool GUARD, class SH>
-__device__ __forceinline__ unsigned long long warp_tile(const ChunkArgs &a, const SH &sh, WarpScratch &w, int u,
-                                                        int r_base, int lane) {
-    const int K = GUARD ? sh.K : KT;
-    const int n_e = sh.n_e, lo = sh.lo, hi = sh.hi, S = sh.S;
+// Phase A, one warp per tile (kWarpRows rows of B_u), lane g owns 32-row group g: the
+// breakpoints of the group (change bits of every source window) become the tile's entries;
+// the tile's first live row is always an entry (it anchors the row map).
+template <bool FIRST, class SH>
+__device__ __forceinline__ void classify_tile(const ChunkArgs &a, SH &sh, int u, int ti, int lane) {
+    const int lo = sh.lo, hi = sh.hi, S = sh.S;
+    const int r_base = (sh.t0 + ti) * kWarpRows;
     const int g = lane, r0 = r_base + 32 * g, r1 = r0 + 31;
     const bool dead = r1 < lo || r0 > hi;
     const bool whole = r0 >= lo && r1 <= hi;
     const int f0 = r_base > lo ? r_base : lo;            // first live row of the tile (<= hi)
-    // ---- 1. breakpoints of the group
     unsigned seg = 0u;
     if (whole) {
         const uint32_t *fin = a.chg[(u - 1) & 1] + sh.f_off;
@@ -267,9 +201,8 @@ __device__ __forceinline__ unsigned long long warp_tile(const ChunkArgs &a, cons
         seg = (0xffffffffu >> (31 - a1)) & ~((1u << a0) - 1u);
     }
     // the tile's first live row: an entry; its change bits are exact only when it is no breakpoint
-    const bool first_bp = __shfl_sync(0xffffffffu, (seg >> ((f0 - r_base) & 31)) & 1u, (f0 - r_base) >> 5) != 0u;
+    const bool fbp = __shfl_sync(0xffffffffu, (seg >> ((f0 - r_base) & 31)) & 1u, (f0 - r_base) >> 5) != 0u;
     if (!dead && f0 >= r0 && f0 <= r1) seg |= 1u << (f0 - r0);
-    // ---- 2. entries in row order
     const int cnt = __popc(seg);
     int incl = cnt;
 #pragma unroll
@@ -277,106 +210,103 @@ __device__ __forceinline__ unsigned long long warp_tile(const ChunkArgs &a, cons
         const int v = __shfl_up_sync(0xffffffffu, incl, off);
         if (lane >= off) incl += v;
     }
-    const int ebase = incl - cnt;
-    const int n_ent = __shfl_sync(0xffffffffu, incl, 31);
-    {
-        int at = ebase;
-        unsigned m = seg;
-        while (m) {
-            const int x = __ffs(m) - 1;
-            m &= m - 1u;
-            w.erow[at++] = (uint16_t)(32 * g + x);
-        }
+    int at = incl - cnt;
+    TileScratch &w = sh.tile[ti];
+    unsigned m = seg;
+    while (m) {
+        const int x = __ffs(m) - 1;
+        m &= m - 1u;
+        w.erow[at++] = (uint16_t)(32 * g + x);
     }
-    __syncwarp();
-    TFCell *bout = a.TF[u & 1] + sh.b_off;
-    uint16_t *pout = a.par + sh.par_off + (int64_t)(u - 1) * K * n_e;
-    if (n_ent <= kCoopMax) {
-        // few entries: the warp evaluates each row together (sources across lanes)
-        double pt = GBMW_STEP_INF, pf = GBMW_STEP_INF;   // lane kk: column kk of the previous entry
-        int pk = 0;
-        for (int n = 0; n < n_ent; ++n) {
-            const int e = r_base + (int)w.erow[n];
-            double bt[KT], bf[KT];
-            int bk[KT];
-            eval_row<KT, FIRST, GUARD>(a, sh, u, e, lane, bt, bf, bk);
-            double ct = GBMW_STEP_INF, cf = GBMW_STEP_INF;    // lane kk: column kk of this entry
-            int ck = 0;
-#pragma unroll
-            for (int kk = 0; kk < KT; ++kk)
-                if (lane == kk) { ct = bt[kk]; cf = bf[kk]; ck = bk[kk]; }
-            const bool col = lane < K;
-            unsigned chg;
-            if (n == 0) {
-                chg = (e == lo || first_bp) ? 0xffffffffu : 0u;
-            } else {
-                const bool same = ct == pt && cf == pf && (ck >> 1) == (pk >> 1) && !(ck & 1);
-                chg = __ballot_sync(0xffffffffu, col && !same);
-            }
-            chg &= (1u << K) - 1u;
-            if ((n == 0 || chg) && col) {
-                reinterpret_cast<double2 *>(bout)[(int64_t)lane * n_e + e] = make_double2(ct, cf);
-                pout[(int64_t)lane * n_e + e] = (uint16_t)sh.idx[ck >> 1];
-            }
-            if (lane == 0) w.echg[n] = (uint16_t)chg;
-            pt = ct; pf = cf; pk = ck;
-        }
+    if (lane == 31) { sh.n_ent[ti] = incl; sh.first_bp[ti] = (f0 == lo || fbp) ? 1 : 0; }
+}
+
+// evaluation rounds of a tile with n entries: one round of up to 32 entries (a segment of
+// 32 / next_pow2(n) lanes per entry), then rounds of 31 new entries, a lane each (lane 0
+// re-evaluates the previous entry for the comparison)
+__device__ __forceinline__ int tile_rounds(int n) { return n <= 32 ? 1 : 1 + (n - 32 + 30) / 31; }
+
+// Phase B, one round of one tile by one warp: evaluate its entries, compare each with the
+// previous entry (unchanged columns keep change bit 0), store (t, f, argmin) of the
+// entries where some column changes (and of the tile's first entry, the anchor).
+template <int KT, bool FIRST, bool GUARD, class SH>
+__device__ __forceinline__ void eval_round(const ChunkArgs &a, SH &sh, int u, int ti, int r, int lane) {
+    const int K = GUARD ? sh.K : KT;
+    const int n_e = sh.n_e, n = sh.n_ent[ti];
+    const int r_base = (sh.t0 + ti) * kWarpRows;
+    TileScratch &w = sh.tile[ti];
+    int L, j0, nr;                                       // lanes per entry, first entry, entries
+    if (r == 0) {
+        nr = n < 32 ? n : 32;
+        L = 32;
+        while (L > 1 && (32 / L) < nr) L >>= 1;
+        j0 = 0;
     } else {
-        // many entries: a lane per row, rounds of 32 rows; the previous entry of lane l is
-        // lane l - 1 (lane 31 of the previous round for lane 0)
-        double ct_[KT], cf_[KT];
-        int ck_[KT];
+        L = 1;
+        j0 = 31 * r;                                     // = (first new entry) - 1
+        nr = min(32, n - j0);
+    }
+    const int seg = lane / L, l = lane - seg * L;
+    const int j = j0 + seg;
+    const bool have = seg < nr;
+    const int e = have ? r_base + (int)w.erow[j] : -1;
+    double bt[KT], bf[KT];
+    int bk[KT];
+    eval_row<KT, FIRST, GUARD>(a, sh, u, e, L, l, bt, bf, bk);
+    unsigned chg = 0u;
 #pragma unroll
-        for (int kk = 0; kk < KT; ++kk) { ct_[kk] = GBMW_STEP_INF; cf_[kk] = GBMW_STEP_INF; ck_[kk] = 0; }
-        for (int n0 = 0; n0 < n_ent; n0 += 32) {
-            const int n = n0 + lane;
-            const int e = (n < n_ent) ? r_base + (int)w.erow[n] : -1;
-            double bt[KT], bf[KT];
-            int bk[KT];
-            eval_row_lane<KT, FIRST, GUARD>(a, sh, u, e, bt, bf, bk);
-            unsigned chg = 0u;
+    for (int kk = 0; kk < KT; ++kk) {
+        if (GUARD && kk >= K) break;
+        const double pt = __shfl_up_sync(0xffffffffu, bt[kk], L);
+        const double pf = __shfl_up_sync(0xffffffffu, bf[kk], L);
+        const int pk = __shfl_up_sync(0xffffffffu, bk[kk], L);
+        const bool same = bt[kk] == pt && bf[kk] == pf && (bk[kk] >> 1) == (pk >> 1) && !(bk[kk] & 1);
+        chg |= same ? 0u : (1u << kk);
+    }
+    if (j == 0) chg = sh.first_bp[ti] ? 0xffffu : 0u;
+    chg &= (1u << K) - 1u;
+    const bool out = have && l == 0 && (r == 0 || seg > 0);   // lane 0 of a later round: the previous entry
+    if (out) {
+        if (j == 0 || chg) {
+            TFCell *bout = a.TF[u & 1] + sh.b_off;
+            uint16_t *pout = a.par + sh.par_off + (int64_t)(u - 1) * K * n_e;
 #pragma unroll
             for (int kk = 0; kk < KT; ++kk) {
                 if (GUARD && kk >= K) break;
-                double pt = __shfl_up_sync(0xffffffffu, bt[kk], 1);
-                double pf = __shfl_up_sync(0xffffffffu, bf[kk], 1);
-                int pk = __shfl_up_sync(0xffffffffu, bk[kk], 1);
-                const double ct31 = __shfl_sync(0xffffffffu, ct_[kk], 31);
-                const double cf31 = __shfl_sync(0xffffffffu, cf_[kk], 31);
-                const int ck31 = __shfl_sync(0xffffffffu, ck_[kk], 31);
-                if (lane == 0) { pt = ct31; pf = cf31; pk = ck31; }
-                const bool same = bt[kk] == pt && bf[kk] == pf && (bk[kk] >> 1) == (pk >> 1) && !(bk[kk] & 1);
-                chg |= same ? 0u : (1u << kk);
-                ct_[kk] = bt[kk]; cf_[kk] = bf[kk]; ck_[kk] = bk[kk];
-            }
-            if (n == 0) chg = (e == lo || first_bp) ? 0xffffu : 0u;
-            chg &= (1u << K) - 1u;
-            if (n < n_ent) {
-                if (n == 0 || chg) {
-#pragma unroll
-                    for (int kk = 0; kk < KT; ++kk) {
-                        if (GUARD && kk >= K) break;
-                        reinterpret_cast<double2 *>(bout)[(int64_t)kk * n_e + e] = make_double2(bt[kk], bf[kk]);
-                        pout[(int64_t)kk * n_e + e] = (uint16_t)sh.idx[bk[kk] >> 1];
-                    }
-                }
-                w.echg[n] = (uint16_t)chg;
+                reinterpret_cast<double2 *>(bout)[(int64_t)kk * n_e + e] = make_double2(bt[kk], bf[kk]);
+                pout[(int64_t)kk * n_e + e] = (uint16_t)sh.idx[bk[kk] >> 1];
             }
         }
+        w.echg[j] = (uint16_t)chg;
     }
-    __syncwarp();
-    // ---- 3. change-bit words and row map of the group
+}
+
+// Phase C, one warp per tile, lane g: the change-bit words and the row-map entry of group g.
+template <int KT, bool GUARD, class SH>
+__device__ __forceinline__ void finish_tile(const ChunkArgs &a, const SH &sh, int u, int ti, int lane) {
+    const int K = GUARD ? sh.K : KT;
+    const int lo = sh.lo, hi = sh.hi, n = sh.n_ent[ti];
+    const int r_base = (sh.t0 + ti) * kWarpRows;
+    const int g = lane, r0 = r_base + 32 * g, r1 = r0 + 31;
+    const bool dead = r1 < lo || r0 > hi;
+    const TileScratch &w = sh.tile[ti];
+    // entries of group g: binary search of the first entry with row >= 32 g
+    int b0 = 0, b1 = n;
+    while (b0 < b1) {
+        const int mid = (b0 + b1) >> 1;
+        if ((int)w.erow[mid] < 32 * g) b0 = mid + 1; else b1 = mid;
+    }
     int last = -1;                                       // last stored row of the group
     unsigned sbits = 0u;
     uint32_t cwd[KT];
 #pragma unroll
     for (int kk = 0; kk < KT; ++kk) cwd[kk] = 0u;
-    for (int n = ebase; n < ebase + cnt; ++n) {
-        const int x = w.erow[n] & 31;
-        const unsigned m = w.echg[n];
+    for (int x0 = b0; x0 < n && (int)w.erow[x0] < 32 * g + 32; ++x0) {
+        const int x = w.erow[x0] & 31;
+        const unsigned m = w.echg[x0];
 #pragma unroll
         for (int kk = 0; kk < KT; ++kk) cwd[kk] |= ((m >> kk) & 1u) << x;
-        if (m || n == 0) { sbits |= 1u << x; last = r_base + (int)w.erow[n]; }   // entry 0: the tile's anchor
+        if (m || x0 == 0) { sbits |= 1u << x; last = r_base + (int)w.erow[x0]; }   // entry 0: the anchor
     }
     int before = last;                                   // exclusive max-scan over the groups
 #pragma unroll
@@ -386,16 +316,19 @@ __device__ __forceinline__ unsigned long long warp_tile(const ChunkArgs &a, cons
     }
     before = __shfl_up_sync(0xffffffffu, before, 1);
     if (lane == 0) before = -1;
-    const int wi = (r_base >> 5) + g;
     if (!dead) {
+        const int wi = (r_base >> 5) + g;
         uint32_t *fout = a.chg[u & 1] + sh.f_off;
 #pragma unroll
         for (int kk = 0; kk < KT; ++kk)
             if (!GUARD || kk < K) fout[(int64_t)kk * sh.nw + wi] = cwd[kk];
         a.rmap[sh.rm_cur + wi] = make_int2((int)sbits, before);
     }
-    __syncwarp();
-    return (unsigned long long)n_ent * (unsigned long long)K;
+    if (a.k2_hist && lane == 0) {
+        const int bin = 32 - __clz(n);
+        atomicAdd(a.k2_hist + bin, 1ull);
+        atomicAdd(a.k2_hist + 32 + bin, (unsigned long long)n);
+    }
 }
 
 // Live-row work lists of every K2 launch of the chunk (one CTA per launch): per active
@@ -439,15 +372,36 @@ int launch_step_lists(const ChunkArgs &a, void *stream) {
     return (int)cudaGetLastError();
 }
 
-// CTAs take items (dynamic counter); their warps take the item's warp tiles.
+// CTAs take items (dynamic counter) of up to kItemTiles warp tiles of one problem:
+// classify the tiles (a warp each), evaluate all their entries in rounds shared by the
+// CTA's warps (heaviest tiles first), then write each tile's change bits and row map.
+#define GBMW_K2_DISPATCH(CALL)                                                       \
+    if (GROUP == 0) {                                                                \
+        switch (K) {                                                                 \
+            case 1: CALL(1, false); break;                                           \
+            case 2: CALL(2, false); break;                                           \
+            case 3: CALL(3, false); break;                                           \
+            default: CALL(4, false); break;                                          \
+        }                                                                            \
+    } else if (GROUP == 1) {                                                         \
+        switch (K) {                                                                 \
+            case 5: CALL(5, false); break;                                           \
+            case 6: CALL(6, false); break;                                           \
+            case 7: CALL(7, false); break;                                           \
+            default: CALL(8, false); break;                                          \
+        }                                                                            \
+    } else {                                                                         \
+        CALL(kMaxClasses, true);                                                     \
+    }
+
 template <int GROUP, bool FIRST>
 __global__ void __launch_bounds__(kStepThreads, GROUP <= 1 ? 2 : 1)
     k_dp_step(ChunkArgs a, int u, const int4 *items, const int64_t *count, unsigned long long *counter) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     using SH = StepShared<GROUP == 0 ? 4 : (GROUP == 1 ? 8 : kMaxClasses)>;
     SH &sh = *reinterpret_cast<SH *>(smem_raw);
+    __shared__ int s_order[kItemTiles];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    auto &w = sh.w[warp];
     unsigned long long stat_rows = 0;
     const int64_t n_items = *count;
     while (true) {
@@ -480,38 +434,49 @@ __global__ void __launch_bounds__(kStepThreads, GROUP <= 1 ? 2 : 1)
                 sh.f_off = p.flag_off; sh.nw = (int)flag_words(p.n_b + 1);
                 sh.rm_prev = p.rmap_off + (int64_t)(u >= 2 ? u - 2 : 0) * ng;
                 sh.rm_cur = p.rmap_off + (int64_t)(u - 1) * ng;
-                sh.tnext = item.y; sh.tlast = item.z;
+                sh.t0 = item.y; sh.nt = item.z - item.y + 1;
             }
         }
         __syncthreads();
-        const int K = sh.K;
-        while (true) {
-            int tile = 0;
-            if (lane == 0) tile = atomicAdd(&sh.tnext, 1);
-            tile = __shfl_sync(0xffffffffu, tile, 0);
-            if (tile > sh.tlast) break;
-            const int r_base = tile * kWarpRows;
-            if (GROUP == 0) {
-                switch (K) {
-                    case 1: stat_rows += warp_tile<1, FIRST, false>(a, sh, w, u, r_base, lane); break;
-                    case 2: stat_rows += warp_tile<2, FIRST, false>(a, sh, w, u, r_base, lane); break;
-                    case 3: stat_rows += warp_tile<3, FIRST, false>(a, sh, w, u, r_base, lane); break;
-                    default: stat_rows += warp_tile<4, FIRST, false>(a, sh, w, u, r_base, lane); break;
-                }
-            } else if (GROUP == 1) {
-                switch (K) {
-                    case 5: stat_rows += warp_tile<5, FIRST, false>(a, sh, w, u, r_base, lane); break;
-                    case 6: stat_rows += warp_tile<6, FIRST, false>(a, sh, w, u, r_base, lane); break;
-                    case 7: stat_rows += warp_tile<7, FIRST, false>(a, sh, w, u, r_base, lane); break;
-                    default: stat_rows += warp_tile<8, FIRST, false>(a, sh, w, u, r_base, lane); break;
-                }
-            } else {
-                stat_rows += warp_tile<kMaxClasses, FIRST, true>(a, sh, w, u, r_base, lane);
+        const int K = sh.K, nt = sh.nt;
+        if (warp < nt) classify_tile<FIRST>(a, sh, u, warp, lane);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            // rounds of the heaviest tiles first
+            for (int x = 0; x < nt; ++x) {
+                int y = x;
+                while (y > 0 && sh.n_ent[s_order[y - 1]] < sh.n_ent[x]) { s_order[y] = s_order[y - 1]; --y; }
+                s_order[y] = x;
             }
+            sh.rpre[0] = 0;
+            for (int x = 0; x < nt; ++x) sh.rpre[x + 1] = sh.rpre[x] + tile_rounds(sh.n_ent[s_order[x]]);
+            sh.rnext = 0;
+        }
+        __syncthreads();
+        const int total = sh.rpre[nt];
+        while (true) {
+            int R = 0;
+            if (lane == 0) R = atomicAdd(&sh.rnext, 1);
+            R = __shfl_sync(0xffffffffu, R, 0);
+            if (R >= total) break;
+            int x = 0;
+            while (x + 1 < nt && sh.rpre[x + 1] <= R) ++x;
+            const int ti = s_order[x], r = R - sh.rpre[x];
+#define GBMW_K2_EVAL(KT, G) eval_round<KT, FIRST, G>(a, sh, u, ti, r, lane)
+            GBMW_K2_DISPATCH(GBMW_K2_EVAL)
+#undef GBMW_K2_EVAL
+        }
+        __syncthreads();
+        if (warp < nt) {
+#define GBMW_K2_FINISH(KT, G) finish_tile<KT, G>(a, sh, u, warp, lane)
+            GBMW_K2_DISPATCH(GBMW_K2_FINISH)
+#undef GBMW_K2_FINISH
+            stat_rows += (unsigned long long)sh.n_ent[warp] * (unsigned long long)K;
         }
     }
     if (lane == 0 && stat_rows) atomicAdd(a.computed_cells, stat_rows);
 }
+#undef GBMW_K2_DISPATCH
 
 int launch_dp_step(const ChunkArgs &a, int group, int u, const int4 *items, const int64_t *count, int64_t n_tiles,
                    unsigned long long *counter, void *stream) {
