@@ -667,9 +667,9 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
                 sl.u = u; sl.lo = lo; sl.n = na; sl.pad_ = 0; sl.base = c.n_items;
                 c.slists.push_back(sl);
                 c.slist_group.push_back(g);
-                // items of <= kItemTiles warp tiles: a problem's warp tiles number at most
-                // 2 * (its 2048-row tiles), so ceil(that / kItemTiles) <= that / kItemTiles + 1
-                c.n_items += 2 * (c.step_prefix[lo + na] - c.step_prefix[lo]) / kItemTiles + na;
+                // items of >= 1 warp tile: a problem's warp tiles number at most 2 * (its
+                // 2048-row tiles)
+                c.n_items += 2 * (c.step_prefix[lo + na] - c.step_prefix[lo]);
             }
         c.o_slists = put(blob, c.slists.data(), c.slists.size()) - base;
         c.small_bytes = blob.size() - base;

@@ -26,7 +26,7 @@ namespace gbmw {
 
 constexpr int kClassifyIB = 8;              // window checks per thread in flight
 constexpr int kStepIB = 4;                  // sources per lane in flight (lane-per-row evaluation)
-constexpr int kCoopMax = 6;                 // tiles with more entries evaluate a row per lane
+constexpr int kStepItemTarget = 1200;       // K2 items per launch worth splitting tiles for (~4 per CTA)
 constexpr int kWarpRows = 1024;             // rows per warp tile: 32 groups of 32
 
 // Scratch of one warp tile of the item: its entries (rows to evaluate) in row order.
@@ -336,16 +336,34 @@ __device__ __forceinline__ void finish_tile(const ChunkArgs &a, const SH &sh, in
 // at most kItemTiles tiles (a large problem spreads over many CTAs).
 __global__ void __launch_bounds__(1024) k_step_lists(ChunkArgs a) {
     __shared__ int s_part[1024];
+    __shared__ int s_it;
     const StepList sl = a.step_lists[blockIdx.x];
     const int tid = threadIdx.x;
     const int per = (sl.n + 1023) / 1024;
     const int x0 = sl.lo + min(sl.n, tid * per), x1 = sl.lo + min(sl.n, tid * per + per);
+    // item size: kItemTiles, smaller when the launch has few tiles (>= kStepItemTarget items)
+    int tiles = 0;
+    for (int x = x0; x < x1; ++x) {
+        const DevProblem &p = a.probs[x];
+        const int lo = a.unit_lo[p.ustate_off + sl.u], hi = a.unit_hi[p.ustate_off + sl.u];
+        if (hi >= lo) tiles += hi / kWarpRows - lo / kWarpRows + 1;
+    }
+    s_part[tid] = tiles;
+    __syncthreads();
+    for (int off = 512; off > 0; off >>= 1) {
+        if (tid < off) s_part[tid] += s_part[tid + off];
+        __syncthreads();
+    }
+    if (tid == 0) s_it = max(1, min(kItemTiles, s_part[0] / kStepItemTarget));
+    __syncthreads();
+    const int it = s_it;
     int cnt = 0;
     for (int x = x0; x < x1; ++x) {
         const DevProblem &p = a.probs[x];
         const int lo = a.unit_lo[p.ustate_off + sl.u], hi = a.unit_hi[p.ustate_off + sl.u];
-        if (hi >= lo) cnt += (hi / kWarpRows - lo / kWarpRows) / kItemTiles + 1;
+        if (hi >= lo) cnt += (hi / kWarpRows - lo / kWarpRows) / it + 1;
     }
+    __syncthreads();
     s_part[tid] = cnt;
     __syncthreads();
     for (int off = 1; off < 1024; off <<= 1) {
@@ -360,8 +378,8 @@ __global__ void __launch_bounds__(1024) k_step_lists(ChunkArgs a) {
         const int lo = a.unit_lo[p.ustate_off + sl.u], hi = a.unit_hi[p.ustate_off + sl.u];
         if (hi < lo) continue;
         const int t1 = hi / kWarpRows;
-        for (int t0 = lo / kWarpRows; t0 <= t1; t0 += kItemTiles)
-            a.step_items[at++] = make_int4(x, t0, min(t1, t0 + kItemTiles - 1), 0);
+        for (int t0 = lo / kWarpRows; t0 <= t1; t0 += it)
+            a.step_items[at++] = make_int4(x, t0, min(t1, t0 + it - 1), 0);
     }
     if (tid == 1023) a.step_count[blockIdx.x] = s_part[1023];
 }
