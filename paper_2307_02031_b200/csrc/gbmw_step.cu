@@ -53,6 +53,7 @@ struct StepShared {
     int first_bp[kItemTiles];               // the tile's first live row is a breakpoint
     int rpre[kItemTiles + 1];               // evaluation rounds before tile t
     int rnext;                              // round counter
+    uint32_t gseg[kItemTiles * 32];         // breakpoints of each 32-row group of the item
     TileScratch tile[kItemTiles];
 };
 
@@ -150,27 +151,31 @@ __device__ __forceinline__ unsigned window_segments(unsigned long long v, int x0
     return m;
 }
 
-// Phase A, one warp per tile (kWarpRows rows of B_u), lane g owns 32-row group g: the
-// breakpoints of the group (change bits of every source window) become the tile's entries;
-// the tile's first live row is always an entry (it anchors the row map).
+// Phase A1, all threads: the breakpoints of every 32-row group of the item's tiles
+// (change bits of every source window).
 template <bool FIRST, class SH>
-__device__ __forceinline__ void classify_tile(const ChunkArgs &a, SH &sh, int u, int ti, int lane) {
+__device__ __forceinline__ void group_breakpoints(const ChunkArgs &a, SH &sh, int u, int tid) {
+    // thread tid: group gi = tid / tpg of the item, sources n = sub, sub + tpg, ... (the
+    // CTA's threads spread over the item's nt * 32 groups whatever nt is)
+    const int ng = sh.nt * 32;
+    int tpg = kStepThreads / ng;
+    tpg = tpg >= 8 ? 8 : (tpg >= 4 ? 4 : (tpg >= 2 ? 2 : 1));
+    const int gi = tid / tpg, sub = tid - gi * tpg;
     const int lo = sh.lo, hi = sh.hi, S = sh.S;
-    const int r_base = (sh.t0 + ti) * kWarpRows;
-    const int g = lane, r0 = r_base + 32 * g, r1 = r0 + 31;
-    const bool dead = r1 < lo || r0 > hi;
-    const bool whole = r0 >= lo && r1 <= hi;
-    const int f0 = r_base > lo ? r_base : lo;            // first live row of the tile (<= hi)
+    const int r0 = (sh.t0 + (gi >> 5)) * kWarpRows + 32 * (gi & 31), r1 = r0 + 31;
+    const bool act = gi < ng;
+    const bool dead = !act || r1 < lo || r0 > hi;
+    const bool whole = act && r0 >= lo && r1 <= hi;
     unsigned seg = 0u;
     if (whole) {
         const uint32_t *fin = a.chg[(u - 1) & 1] + sh.f_off;
-        for (int n0 = 0; n0 < S; n0 += kClassifyIB) {
+        for (int n0 = sub; n0 < S; n0 += kClassifyIB * tpg) {
             uint32_t w0[kClassifyIB], w1[kClassifyIB];
             int xs_[kClassifyIB];
             bool ld[kClassifyIB];
 #pragma unroll
             for (int b = 0; b < kClassifyIB; ++b) {
-                const int n = n0 + b;
+                const int n = n0 + b * tpg;
                 const Cell c = sh.cell[n < S ? n : 0];
                 const int xs = r0 - c.w;
                 xs_[b] = xs; w0[b] = 0u; w1[b] = 0u;
@@ -200,6 +205,21 @@ __device__ __forceinline__ void classify_tile(const ChunkArgs &a, SH &sh, int u,
         const int a0 = lo > r0 ? lo - r0 : 0, a1 = hi < r1 ? hi - r0 : 31;
         seg = (0xffffffffu >> (31 - a1)) & ~((1u << a0) - 1u);
     }
+    for (int off = tpg >> 1; off > 0; off >>= 1) seg |= __shfl_xor_sync(0xffffffffu, seg, off);
+    if (act && sub == 0) sh.gseg[gi] = seg;
+}
+
+// Phase A2, one warp per tile (kWarpRows rows of B_u), lane g owns 32-row group g: the
+// breakpoints of the groups become the tile's entries; the tile's first live row is always
+// an entry (it anchors the row map).
+template <class SH>
+__device__ __forceinline__ void classify_tile(SH &sh, int ti, int lane) {
+    const int lo = sh.lo, hi = sh.hi;
+    const int r_base = (sh.t0 + ti) * kWarpRows;
+    const int g = lane, r0 = r_base + 32 * g, r1 = r0 + 31;
+    const bool dead = r1 < lo || r0 > hi;
+    const int f0 = r_base > lo ? r_base : lo;            // first live row of the tile (<= hi)
+    unsigned seg = sh.gseg[ti * 32 + g];
     // the tile's first live row: an entry; its change bits are exact only when it is no breakpoint
     const bool fbp = __shfl_sync(0xffffffffu, (seg >> ((f0 - r_base) & 31)) & 1u, (f0 - r_base) >> 5) != 0u;
     if (!dead && f0 >= r0 && f0 <= r1) seg |= 1u << (f0 - r0);
@@ -457,7 +477,9 @@ __global__ void __launch_bounds__(kStepThreads, GROUP <= 1 ? 2 : 1)
         }
         __syncthreads();
         const int K = sh.K, nt = sh.nt;
-        if (warp < nt) classify_tile<FIRST>(a, sh, u, warp, lane);
+        group_breakpoints<FIRST>(a, sh, u, threadIdx.x);
+        __syncthreads();
+        if (warp < nt) classify_tile(sh, warp, lane);
         __syncthreads();
         if (threadIdx.x == 0) {
             // rounds of the heaviest tiles first
