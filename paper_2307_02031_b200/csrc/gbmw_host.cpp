@@ -454,7 +454,7 @@ void prepare_problem(gbmw_batch &b, int pi, std::string *err) {
     h.n_par = approx ? (int64_t)h.U * n_e : (int64_t)(h.U - 1) * h.K * n_e;
     h.n_tiles = (h.n_b + kSweepThreads - 1) / kSweepThreads;
     h.n_step_tiles = (n_e + kStepRows - 1) / kStepRows;
-    h.n_flagw = (!approx && h.U > 1) ? (int64_t)h.K * flag_words(n_e) : 0;
+    h.n_flagw = (!approx && h.U > 1) ? (int64_t)h.K * (flag_words(n_e) + sum_words(n_e)) : 0;
     h.n_rmap = approx ? 0 : (int64_t)(h.U > 1 ? h.U - 1 : 0) * rmap_groups(n_e);
     h.ws_bytes = (size_t)h.n_cells * (sizeof(Cell) + sizeof(CellMem) + 4) + (size_t)h.U * 12 + (size_t)h.n_r * 8 + 8 +
                  (size_t)h.n_bcells * 2 * sizeof(TFCell) + (size_t)h.n_par * 2 +

@@ -31,6 +31,13 @@ __host__ __device__
 #endif
 inline int64_t flag_words(int64_t n_e) { return (n_e + 31) / 32 + 2; }
 
+// change-summary words per class column: bit g of word t = 32-row group 32 t + g of the
+// column has a change bit (stored after the column's change-bit words)
+#if defined(__CUDACC__)
+__host__ __device__
+#endif
+inline int64_t sum_words(int64_t n_e) { return (n_e + 1023) / 1024 + 1; }
+
 // row-map entries per unit: one per aligned 32-row group of B_u (see stored_row)
 #if defined(__CUDACC__)
 __host__ __device__

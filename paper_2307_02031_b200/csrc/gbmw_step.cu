@@ -31,8 +31,8 @@ constexpr int kWarpRows = 1024;             // rows per warp tile: 32 groups of 
 
 // Scratch of one warp tile of the item: its entries (rows to evaluate) in row order.
 struct TileScratch {
-    uint16_t erow[kWarpRows];               // row of each entry, relative to the tile's first row
-    uint16_t echg[kWarpRows];               // bit kk: column kk changes at the entry's row
+    uint16_t erow[kWarpRows + 1];           // row of each entry, relative to the row before the tile
+    uint16_t echg[kWarpRows + 1];           // bit kk: column kk changes at the entry's row
 };
 
 constexpr int kItemWarps = kStepThreads / 32;
@@ -54,6 +54,10 @@ struct StepShared {
     int rpre[kItemTiles + 1];               // evaluation rounds before tile t
     int rnext;                              // round counter
     uint32_t gseg[kItemTiles * 32];         // breakpoints of each 32-row group of the item
+    int pre[kItemTiles];                    // entry 0 of a later tile: the row before its first breakpoint
+    int tlast[kItemTiles];                  // last stored row of each tile (-1: none)
+    int na[kItemTiles];                     // sources with a change inside each tile's window
+    uint16_t alist[kItemTiles][kMaxStrats]; // ... their positions in the distinct list
     TileScratch tile[kItemTiles];
 };
 
@@ -151,35 +155,74 @@ __device__ __forceinline__ unsigned window_segments(unsigned long long v, int x0
     return m;
 }
 
+// Phase A0, one warp per tile: the sources whose window over the tile holds a change of
+// their column of B_{u-1} (change summaries, 1 bit per 32 rows) or the column's first
+// finite row; the others contribute no breakpoint anywhere in the tile.
+template <bool FIRST, class SH>
+__device__ __forceinline__ void tile_sources(const ChunkArgs &a, SH &sh, int u, int ti, int lane) {
+    const int S = sh.S, lo_prev = sh.lo_prev;
+    const int r_base = (sh.t0 + ti) * kWarpRows;
+    const int ns = (int)sum_words(sh.n_e);
+    const uint32_t *sum = a.chg[(u - 1) & 1] + sh.f_off + (int64_t)sh.K * sh.nw;
+    int cnt = 0;
+    for (int n0 = 0; n0 < S; n0 += 32) {
+        const int n = n0 + lane;
+        bool act = false;
+        if (n < S) {
+            const Cell c = sh.cell[n];
+            const int A = r_base - c.w, B = A + kWarpRows - 1;     // source rows of the tile's windows
+            if (FIRST) {
+                act = c.w >= r_base && c.w < r_base + kWarpRows;    // T_0[., i] turns finite at w_i
+            } else if (B >= lo_prev) {
+                act = lo_prev >= A;                                 // the column's first finite row
+                if (!act) {
+                    const int ga = A >> 5, gb = B >> 5;             // 32-row groups [ga, gb]
+                    const uint32_t *sk = sum + (int64_t)c.k * ns;
+                    const uint32_t w0 = __ldg(sk + (ga >> 5)), w1 = __ldg(sk + (gb >> 5));
+                    const uint32_t m0 = w0 & (0xffffffffu << (ga & 31));
+                    const uint32_t m1 = w1 & (0xffffffffu >> (31 - (gb & 31)));
+                    act = ((ga >> 5) == (gb >> 5)) ? (m0 & m1) != 0u : (m0 | m1) != 0u;
+                }
+            }
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, act);
+        if (act) sh.alist[ti][cnt + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)n;
+        cnt += __popc(bal);
+    }
+    if (lane == 0) sh.na[ti] = cnt;
+}
+
 // Phase A1, all threads: the breakpoints of every 32-row group of the item's tiles
-// (change bits of every source window).
+// (change bits of the tile's active source windows).
 template <bool FIRST, class SH>
 __device__ __forceinline__ void group_breakpoints(const ChunkArgs &a, SH &sh, int u, int tid) {
-    // thread tid: group gi = tid / tpg of the item, sources n = sub, sub + tpg, ... (the
+    // thread tid: group gi = tid / tpg of the item, active sources sub, sub + tpg, ... (the
     // CTA's threads spread over the item's nt * 32 groups whatever nt is)
     const int ng = sh.nt * 32;
     int tpg = kStepThreads / ng;
     tpg = tpg >= 8 ? 8 : (tpg >= 4 ? 4 : (tpg >= 2 ? 2 : 1));
     const int gi = tid / tpg, sub = tid - gi * tpg;
-    const int lo = sh.lo, hi = sh.hi, S = sh.S;
+    const int lo = sh.lo, hi = sh.hi;
     const int r0 = (sh.t0 + (gi >> 5)) * kWarpRows + 32 * (gi & 31), r1 = r0 + 31;
     const bool act = gi < ng;
     const bool dead = !act || r1 < lo || r0 > hi;
     const bool whole = act && r0 >= lo && r1 <= hi;
+    const int NA = act ? sh.na[gi >> 5] : 0;
+    const uint16_t *al = sh.alist[act ? gi >> 5 : 0];
     unsigned seg = 0u;
     if (whole) {
         const uint32_t *fin = a.chg[(u - 1) & 1] + sh.f_off;
-        for (int n0 = sub; n0 < S; n0 += kClassifyIB * tpg) {
+        for (int n0 = sub; n0 < NA; n0 += kClassifyIB * tpg) {
             uint32_t w0[kClassifyIB], w1[kClassifyIB];
             int xs_[kClassifyIB];
             bool ld[kClassifyIB];
 #pragma unroll
             for (int b = 0; b < kClassifyIB; ++b) {
                 const int n = n0 + b * tpg;
-                const Cell c = sh.cell[n < S ? n : 0];
+                const Cell c = sh.cell[n < NA ? al[n] : 0];
                 const int xs = r0 - c.w;
                 xs_[b] = xs; w0[b] = 0u; w1[b] = 0u;
-                ld[b] = n < S && (FIRST || xs + 31 >= sh.lo_prev);
+                ld[b] = n < NA && (FIRST || xs + 31 >= sh.lo_prev);
                 if (!FIRST && ld[b]) {
                     const int xl = xs < 0 ? 0 : xs;
                     const uint32_t *fl = fin + (int64_t)c.k * sh.nw + (xl >> 5);
@@ -210,8 +253,10 @@ __device__ __forceinline__ void group_breakpoints(const ChunkArgs &a, SH &sh, in
 }
 
 // Phase A2, one warp per tile (kWarpRows rows of B_u), lane g owns 32-row group g: the
-// breakpoints of the groups become the tile's entries; the tile's first live row is always
-// an entry (it anchors the row map).
+// breakpoints of the groups become the tile's entries (rows relative to the row before the
+// tile).  The item's first tile always has its first live row as entry 0 (the anchor of the
+// row map, stored); a later tile with breakpoints gets the row before its first one as
+// entry 0 (evaluated for the comparison only, never stored).
 template <class SH>
 __device__ __forceinline__ void classify_tile(SH &sh, int ti, int lane) {
     const int lo = sh.lo, hi = sh.hi;
@@ -220,9 +265,11 @@ __device__ __forceinline__ void classify_tile(SH &sh, int ti, int lane) {
     const bool dead = r1 < lo || r0 > hi;
     const int f0 = r_base > lo ? r_base : lo;            // first live row of the tile (<= hi)
     unsigned seg = sh.gseg[ti * 32 + g];
-    // the tile's first live row: an entry; its change bits are exact only when it is no breakpoint
-    const bool fbp = __shfl_sync(0xffffffffu, (seg >> ((f0 - r_base) & 31)) & 1u, (f0 - r_base) >> 5) != 0u;
-    if (!dead && f0 >= r0 && f0 <= r1) seg |= 1u << (f0 - r0);
+    bool fbp = false;
+    if (ti == 0) {                                       // anchor: change bits exact unless a breakpoint
+        fbp = __shfl_sync(0xffffffffu, (seg >> ((f0 - r_base) & 31)) & 1u, (f0 - r_base) >> 5) != 0u;
+        if (!dead && f0 >= r0 && f0 <= r1) seg |= 1u << (f0 - r0);
+    }
     const int cnt = __popc(seg);
     int incl = cnt;
 #pragma unroll
@@ -230,15 +277,22 @@ __device__ __forceinline__ void classify_tile(SH &sh, int ti, int lane) {
         const int v = __shfl_up_sync(0xffffffffu, incl, off);
         if (lane >= off) incl += v;
     }
-    int at = incl - cnt;
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    const int pre = (ti > 0 && total > 0) ? 1 : 0;
+    int at = pre + incl - cnt;
     TileScratch &w = sh.tile[ti];
     unsigned m = seg;
+    bool first = pre && incl == cnt && cnt > 0;          // this lane holds the tile's first breakpoint
     while (m) {
         const int x = __ffs(m) - 1;
         m &= m - 1u;
-        w.erow[at++] = (uint16_t)(32 * g + x);
+        if (first) { w.erow[0] = (uint16_t)(32 * g + x); first = false; }   // its row - 1 (relative + 1)
+        w.erow[at++] = (uint16_t)(32 * g + x + 1);
     }
-    if (lane == 31) { sh.n_ent[ti] = incl; sh.first_bp[ti] = (f0 == lo || fbp) ? 1 : 0; }
+    if (lane == 31) {
+        sh.n_ent[ti] = total + pre; sh.pre[ti] = pre;
+        sh.first_bp[ti] = (f0 == lo || fbp) ? 1 : 0;
+    }
 }
 
 // evaluation rounds of a tile with n entries: one round of up to 32 entries (a segment of
@@ -269,7 +323,7 @@ __device__ __forceinline__ void eval_round(const ChunkArgs &a, SH &sh, int u, in
     const int seg = lane / L, l = lane - seg * L;
     const int j = j0 + seg;
     const bool have = seg < nr;
-    const int e = have ? r_base + (int)w.erow[j] : -1;
+    const int e = have ? r_base - 1 + (int)w.erow[j] : -1;
     double bt[KT], bf[KT];
     int bk[KT];
     eval_row<KT, FIRST, GUARD>(a, sh, u, e, L, l, bt, bf, bk);
@@ -283,9 +337,11 @@ __device__ __forceinline__ void eval_round(const ChunkArgs &a, SH &sh, int u, in
         const bool same = bt[kk] == pt && bf[kk] == pf && (bk[kk] >> 1) == (pk >> 1) && !(bk[kk] & 1);
         chg |= same ? 0u : (1u << kk);
     }
-    if (j == 0) chg = sh.first_bp[ti] ? 0xffffu : 0u;
+    const bool pre = sh.pre[ti] != 0;
+    if (j == 0) chg = (!pre && sh.first_bp[ti]) ? 0xffffu : 0u;
     chg &= (1u << K) - 1u;
-    const bool out = have && l == 0 && (r == 0 || seg > 0);   // lane 0 of a later round: the previous entry
+    // lane 0 of a later round: the previous entry; entry 0 of a later tile: comparison only
+    const bool out = have && l == 0 && (r == 0 || seg > 0) && !(j == 0 && pre);
     if (out) {
         if (j == 0 || chg) {
             TFCell *bout = a.TF[u & 1] + sh.b_off;
@@ -302,6 +358,39 @@ __device__ __forceinline__ void eval_round(const ChunkArgs &a, SH &sh, int u, in
 }
 
 // Phase C, one warp per tile, lane g: the change-bit words and the row-map entry of group g.
+// entries of group g of a tile: [b0, b1) (binary search; entry 0 of a later tile is the
+// comparison row, skipped)
+template <class SH>
+__device__ __forceinline__ void group_entries(const SH &sh, int ti, int g, int &b0, int &b1) {
+    const TileScratch &w = sh.tile[ti];
+    const int n = sh.n_ent[ti];
+    int x0 = sh.pre[ti], x1 = n;
+    while (x0 < x1) {
+        const int mid = (x0 + x1) >> 1;
+        if ((int)w.erow[mid] < 32 * g + 1) x0 = mid + 1; else x1 = mid;
+    }
+    b0 = x0;
+    b1 = b0;
+    while (b1 < n && (int)w.erow[b1] < 32 * g + 33) ++b1;
+}
+
+__device__ __forceinline__ bool entry_stored(int j, unsigned m, bool pre) { return m != 0u || (j == 0 && !pre); }
+
+// Phase C1, one warp per tile: the tile's last stored row (the row-map carry of later tiles).
+template <class SH>
+__device__ __forceinline__ void tile_last(SH &sh, int ti, int lane) {
+    const int r_base = (sh.t0 + ti) * kWarpRows;
+    const TileScratch &w = sh.tile[ti];
+    const bool pre = sh.pre[ti] != 0;
+    int last = -1;
+    for (int j = lane; j < sh.n_ent[ti]; j += 32)
+        if (!(j == 0 && pre) && entry_stored(j, w.echg[j], pre)) last = r_base - 1 + (int)w.erow[j];
+    for (int off = 16; off > 0; off >>= 1) last = max(last, __shfl_xor_sync(0xffffffffu, last, off));
+    if (lane == 0) sh.tlast[ti] = last;
+}
+
+// Phase C2, one warp per tile, lane g: the change-bit words and the row-map entry of group g,
+// and the tile's change-summary word per column.
 template <int KT, bool GUARD, class SH>
 __device__ __forceinline__ void finish_tile(const ChunkArgs &a, const SH &sh, int u, int ti, int lane) {
     const int K = GUARD ? sh.K : KT;
@@ -309,25 +398,24 @@ __device__ __forceinline__ void finish_tile(const ChunkArgs &a, const SH &sh, in
     const int r_base = (sh.t0 + ti) * kWarpRows;
     const int g = lane, r0 = r_base + 32 * g, r1 = r0 + 31;
     const bool dead = r1 < lo || r0 > hi;
+    const bool pre = sh.pre[ti] != 0;
     const TileScratch &w = sh.tile[ti];
-    // entries of group g: binary search of the first entry with row >= 32 g
-    int b0 = 0, b1 = n;
-    while (b0 < b1) {
-        const int mid = (b0 + b1) >> 1;
-        if ((int)w.erow[mid] < 32 * g) b0 = mid + 1; else b1 = mid;
-    }
+    int b0, b1;
+    group_entries(sh, ti, g, b0, b1);
     int last = -1;                                       // last stored row of the group
     unsigned sbits = 0u;
     uint32_t cwd[KT];
 #pragma unroll
     for (int kk = 0; kk < KT; ++kk) cwd[kk] = 0u;
-    for (int x0 = b0; x0 < n && (int)w.erow[x0] < 32 * g + 32; ++x0) {
-        const int x = w.erow[x0] & 31;
+    for (int x0 = b0; x0 < b1; ++x0) {
+        const int x = ((int)w.erow[x0] - 1) & 31;
         const unsigned m = w.echg[x0];
 #pragma unroll
         for (int kk = 0; kk < KT; ++kk) cwd[kk] |= ((m >> kk) & 1u) << x;
-        if (m || x0 == 0) { sbits |= 1u << x; last = r_base + (int)w.erow[x0]; }   // entry 0: the anchor
+        if (entry_stored(x0, m, pre)) { sbits |= 1u << x; last = r_base - 1 + (int)w.erow[x0]; }
     }
+    int carry = -1;                                      // stored rows of the item's earlier tiles
+    for (int t = 0; t < ti; ++t) carry = max(carry, sh.tlast[t]);
     int before = last;                                   // exclusive max-scan over the groups
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
@@ -336,14 +424,19 @@ __device__ __forceinline__ void finish_tile(const ChunkArgs &a, const SH &sh, in
     }
     before = __shfl_up_sync(0xffffffffu, before, 1);
     if (lane == 0) before = -1;
-    if (!dead) {
-        const int wi = (r_base >> 5) + g;
-        uint32_t *fout = a.chg[u & 1] + sh.f_off;
+    before = max(before, carry);
+    const int ns = (int)sum_words(sh.n_e);
+    uint32_t *fout = a.chg[u & 1] + sh.f_off;
+    uint32_t *sout = fout + (int64_t)K * sh.nw;
+    const int wi = (r_base >> 5) + g;
 #pragma unroll
-        for (int kk = 0; kk < KT; ++kk)
-            if (!GUARD || kk < K) fout[(int64_t)kk * sh.nw + wi] = cwd[kk];
-        a.rmap[sh.rm_cur + wi] = make_int2((int)sbits, before);
+    for (int kk = 0; kk < KT; ++kk) {
+        if (GUARD && kk >= K) break;
+        if (!dead) fout[(int64_t)kk * sh.nw + wi] = cwd[kk];
+        const unsigned sm = __ballot_sync(0xffffffffu, cwd[kk] != 0u);
+        if (lane == 0) sout[(int64_t)kk * ns + (r_base >> 10)] = sm;
     }
+    if (!dead) a.rmap[sh.rm_cur + wi] = make_int2((int)sbits, before);
     if (a.k2_hist && lane == 0) {
         const int bin = 32 - __clz(n);
         atomicAdd(a.k2_hist + bin, 1ull);
@@ -477,6 +570,8 @@ __global__ void __launch_bounds__(kStepThreads, GROUP <= 1 ? 2 : 1)
         }
         __syncthreads();
         const int K = sh.K, nt = sh.nt;
+        if (warp < nt) tile_sources<FIRST>(a, sh, u, warp, lane);
+        __syncthreads();
         group_breakpoints<FIRST>(a, sh, u, threadIdx.x);
         __syncthreads();
         if (warp < nt) classify_tile(sh, warp, lane);
@@ -506,6 +601,8 @@ __global__ void __launch_bounds__(kStepThreads, GROUP <= 1 ? 2 : 1)
             GBMW_K2_DISPATCH(GBMW_K2_EVAL)
 #undef GBMW_K2_EVAL
         }
+        __syncthreads();
+        if (warp < nt) tile_last(sh, warp, lane);
         __syncthreads();
         if (warp < nt) {
 #define GBMW_K2_FINISH(KT, G) finish_tile<KT, G>(a, sh, u, warp, lane)
