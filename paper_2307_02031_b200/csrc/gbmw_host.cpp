@@ -915,6 +915,21 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
             for (int i = 0; i < 32; ++i)
                 if (h[i]) fprintf(stderr, "[%d] %llu tiles %llu ent  ", i, h[i], h[32 + i]);
             fprintf(stderr, "\n");
+            // per launch: items, tiles (first chunk)
+            const Chunk &c0 = b->chunks[0];
+            const Chunk &cl = b->chunks.back();
+            (void)c0;
+            ChunkArgs a0 = chunk_args(b, cl, (char *)ctx->ws, b->chunks.size() - 1);
+            std::vector<int64_t> cnt(cl.slists.size());
+            std::vector<int4> items(cl.n_items);
+            cudaMemcpy(cnt.data(), a0.step_count, cnt.size() * 8, cudaMemcpyDeviceToHost);
+            cudaMemcpy(items.data(), a0.step_items, items.size() * sizeof(int4), cudaMemcpyDeviceToHost);
+            for (size_t l = 0; l < cl.slists.size(); ++l) {
+                long long tiles = 0;
+                for (int64_t i = 0; i < cnt[l]; ++i) tiles += items[cl.slists[l].base + i].z - items[cl.slists[l].base + i].y + 1;
+                fprintf(stderr, "u=%d g=%d problems=%d items=%lld tiles=%lld\n", cl.slists[l].u, cl.slist_group[l],
+                        cl.slists[l].n, (long long)cnt[l], tiles);
+            }
         }
     }
     b->ran = true;

@@ -526,7 +526,7 @@ int launch_step_lists(const ChunkArgs &a, void *stream) {
     }
 
 template <int GROUP, bool FIRST>
-__global__ void __launch_bounds__(kStepThreads, GROUP <= 1 ? 2 : 1)
+__global__ void __launch_bounds__(kStepThreads, GROUP <= 1 ? 3 : 1)
     k_dp_step(ChunkArgs a, int u, const int4 *items, const int64_t *count, unsigned long long *counter) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     using SH = StepShared<GROUP == 0 ? 4 : (GROUP == 1 ? 8 : kMaxClasses)>;
