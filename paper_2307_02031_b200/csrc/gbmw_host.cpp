@@ -109,6 +109,8 @@ struct Chunk {
 struct gbmw_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t aux[kNumGroups] = {nullptr};   // K2 groups 1.. run concurrently with group 0
+    cudaEvent_t fork = nullptr, join[kNumGroups] = {nullptr};
     uint64_t workspace_limit = 0;
     void *ws = nullptr;
     size_t ws_size = 0;
@@ -333,6 +335,11 @@ extern "C" int gbmw_ctx_destroy(gbmw_ctx *ctx) {
     if (ctx->ws) cudaFree(ctx->ws);
     if (ctx->arena) cudaFree(ctx->arena);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    for (int g = 0; g < kNumGroups; ++g) {
+        if (ctx->aux[g]) cudaStreamDestroy(ctx->aux[g]);
+        if (ctx->join[g]) cudaEventDestroy(ctx->join[g]);
+    }
+    if (ctx->fork) cudaEventDestroy(ctx->fork);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
     return GBMW_OK;
@@ -855,12 +862,34 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
             if ((rc = launch_step_lists(a, st))) return cuda_fail(ctx, rc, "K2 list launch");
             c.launches += 1;
         }
+        // the class-count groups (and the collapsed-DP problems) are independent problems:
+        // group 0 on the main stream, the others on their own streams, joined before K3
+        bool used[kNumGroups] = {false};
+        for (size_t s = 0; s < c.slists.size(); ++s) used[c.slist_group[s]] = true;
+        used[kApproxGroup] = c.n_active[kApproxGroup].size() > 1 && c.n_active[kApproxGroup][0] > 0;
+        cudaStream_t gs[kNumGroups];
+        gs[0] = st;
+        bool forked = false;
+        for (int g = 1; g < kNumGroups; ++g) {
+            gs[g] = st;
+            if (!used[g]) continue;
+            if (!ctx->aux[g]) {
+                if (cudaStreamCreateWithFlags(&ctx->aux[g], cudaStreamNonBlocking) != cudaSuccess ||
+                    cudaEventCreateWithFlags(&ctx->join[g], cudaEventDisableTiming) != cudaSuccess)
+                    return cuda_fail(ctx, (int)cudaGetLastError(), "aux stream");
+            }
+            if (!ctx->fork && cudaEventCreateWithFlags(&ctx->fork, cudaEventDisableTiming) != cudaSuccess)
+                return cuda_fail(ctx, (int)cudaGetLastError(), "fork event");
+            if (!forked) { cudaEventRecord(ctx->fork, st); forked = true; }
+            cudaStreamWaitEvent(ctx->aux[g], ctx->fork, 0);
+            gs[g] = ctx->aux[g];
+        }
         for (size_t s = 0; s < c.slists.size(); ++s) {
             const StepList &sl = c.slists[s];
             const int g = c.slist_group[s];
             const int64_t ub = (s + 1 < c.slists.size() ? c.slists[s + 1].base : c.n_items) - sl.base;   // item bound
             if ((rc = launch_dp_step(a, g, sl.u, a.step_items + sl.base, a.step_count + s, ub,
-                                     a.counters + (size_t)sl.u * kNumGroups + g, st)))
+                                     a.counters + (size_t)sl.u * kNumGroups + g, gs[g])))
                 return cuda_fail(ctx, rc, "K2 launch");
             c.launches += 1;
         }
@@ -869,9 +898,15 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
             const int lo = c.group_lo[kApproxGroup], na = c.n_active[kApproxGroup][u];
             if (na == 0) continue;
             const int64_t base = c.step_prefix[lo], n = c.step_prefix[lo + na] - base;
-            if ((rc = launch_approx_step(a, u, base, n, a.counters + (size_t)u * kNumGroups + kApproxGroup, st)))
+            if ((rc = launch_approx_step(a, u, base, n, a.counters + (size_t)u * kNumGroups + kApproxGroup,
+                                         gs[kApproxGroup])))
                 return cuda_fail(ctx, rc, "K2c launch");
             c.launches += 1;
+        }
+        for (int g = 1; g < kNumGroups; ++g) {
+            if (gs[g] == st) continue;
+            cudaEventRecord(ctx->join[g], gs[g]);
+            cudaStreamWaitEvent(st, ctx->join[g], 0);
         }
         cudaEventRecord(c.ev[2], st);
         if ((rc = launch_sweep(a, st))) return cuda_fail(ctx, rc, "K3 launch");
