@@ -577,8 +577,8 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
     std::vector<char> blob;
     for (Chunk &c : b->chunks) {
         std::stable_sort(c.probs.begin(), c.probs.end(), [&](int x, int y) {
-            const int gx = problem_group(b->hp[x].K, b->problems[x].flags);
-            const int gy = problem_group(b->hp[y].K, b->problems[y].flags);
+            const int gx = problem_group(b->hp[x].K, b->problems[x].flags, b->hp[x].U);
+            const int gy = problem_group(b->hp[y].K, b->problems[y].flags, b->hp[y].U);
             if (gx != gy) return gx < gy;
             return b->hp[x].U > b->hp[y].U;
         });
@@ -635,7 +635,7 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
         const int np = (int)c.probs.size();
         for (int g = 0, s = 0; g < kNumGroups; ++g) {
             c.group_lo[g] = s;
-            while (s < np && problem_group(b->hp[c.probs[s]].K, b->problems[c.probs[s]].flags) == g) ++s;
+            while (s < np && problem_group(b->hp[c.probs[s]].K, b->problems[c.probs[s]].flags, b->hp[c.probs[s]].U) == g) ++s;
             c.group_lo[g + 1] = s;
             c.n_active[g].assign(c.Umax + 1, 0);
             for (int x = c.group_lo[g]; x < s; ++x)
@@ -667,7 +667,7 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
         // K2 launches: items bounded by all tiles of the active problems
         c.slists.clear(); c.slist_group.clear(); c.n_items = 0;
         for (int u = 1; u < c.Umax; ++u)
-            for (int g = 0; g < kStepGroups; ++g) {
+            for (int g = 0; g < kStepVGroups; ++g) {
                 const int lo = c.group_lo[g], na = c.n_active[g][u];
                 if (na == 0) continue;
                 StepList sl;
@@ -888,7 +888,7 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
             const StepList &sl = c.slists[s];
             const int g = c.slist_group[s];
             const int64_t ub = (s + 1 < c.slists.size() ? c.slists[s + 1].base : c.n_items) - sl.base;   // item bound
-            if ((rc = launch_dp_step(a, g, sl.u, a.step_items + sl.base, a.step_count + s, ub,
+            if ((rc = launch_dp_step(a, g / kBands, sl.u, a.step_items + sl.base, a.step_count + s, ub,
                                      a.counters + (size_t)sl.u * kNumGroups + g, gs[g])))
                 return cuda_fail(ctx, rc, "K2 launch");
             c.launches += 1;

@@ -52,10 +52,18 @@ constexpr int kMaxSweepRanks = 4096; // >= sweep tiles of one problem: ceil(GBMW
 // pay the register footprint of the widest one: K <= 4, 5..8, 9..kMaxClasses.
 constexpr int kStepGroups = 3;
 inline int step_group(int K) { return K <= 4 ? 0 : (K <= 8 ? 1 : 2); }
+// Each class-count group is split into bands by depth (deep problems first); every band
+// has its own K2 launches on its own stream, so the many short launches of deep problems
+// overlap the few wide launches of shallow ones.
+constexpr int kBands = 2;
+constexpr int kDeepUnits = 16;       // band 0: more units than this
+constexpr int kStepVGroups = kStepGroups * kBands;
 // problems with approx_prev (collapsed state, dpsearch.py:306-375) form their own group
-constexpr int kApproxGroup = kStepGroups;
-constexpr int kNumGroups = kStepGroups + 1;
-inline int problem_group(int K, int flags) { return (flags & GBMW_APPROX) ? kApproxGroup : step_group(K); }
+constexpr int kApproxGroup = kStepVGroups;
+constexpr int kNumGroups = kStepVGroups + 1;
+inline int problem_group(int K, int flags, int U) {
+    return (flags & GBMW_APPROX) ? kApproxGroup : step_group(K) * kBands + (U > kDeepUnits ? 0 : 1);
+}
 
 struct Cell {
     double c;       // time_c = t * count
