@@ -140,6 +140,18 @@ def peaks():
     return 6650.0, "fallback"
 
 
+def algorithmic_bytes(P, T):
+    """SURVEY.md §8(d) regime B: 33/S HBM bytes per algorithmic transition (the uint8
+    argmin per (e, j) cell plus reading T, F and writing T', F' in fp64), summed over the
+    searches: 33 * T / S with S recovered from T = (U - 1) * n_e * S^2."""
+    units = P["n_layers"].astype(np.float64) - 1.0
+    rows = P["n_buckets"].astype(np.float64) + 1.0
+    ok = (units > 0) & (T > 0)
+    S = np.zeros_like(T)
+    S[ok] = np.rint(np.sqrt(T[ok] / (units[ok] * rows[ok])))
+    return float(np.sum(np.where(ok & (S > 0), 33.0 * T / np.maximum(S, 1.0), 0.0)))
+
+
 def k2_traffic():
     """dram bytes per K2 launch from the committed ncu --set full capture, if any."""
     f = ROOT / "profiles" / "k2_traffic.json"
@@ -383,8 +395,15 @@ def main():
     if rank == 0:
         hbm, kind = peaks()
         dp_time = float(allst[0, 1]) / 1e3
-        achieved = float(allst[0, 4]) / dp_time / 1e9 if dp_time > 0 else 0.0
+        # K2 roofline per SURVEY.md §8(d): algorithmic bytes of the reference's min-plus
+        # recurrence (33/S B per transition) over K2 device time; the exact reformulations
+        # (class reduction, breakpoint-only evaluation) move far fewer bytes,
+        # so frac > 1 means the kernel beats the reference formulation's HBM roofline.
+        alg = algorithmic_bytes(Pm, Tm)
+        achieved = alg / dp_time / 1e9 if dp_time > 0 else 0.0
         tr = k2_traffic()
+        n_k2 = int((tr or {}).get("launches") or 190)
+        dram = (tr or {}).get("k2_dram_bytes_per_step")
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong",
@@ -396,8 +415,12 @@ def main():
             "roofline": {"kernel": "k_dp_step (K2)", "bound": "hbm", "achieved": achieved, "peak": hbm,
                          "peak_kind": kind, "unit": "GB/s", "frac": achieved / hbm,
                          "traffic": (tr or {}).get("bytes_per_launch") if tr else None,
-                         "algorithmic_bytes": "K per row-step * (16 B read + 16 B write + 2 B argmin), "
-                                              "see DESIGN.md §4"},
+                         "algorithmic_bytes_per_launch": alg / n_k2,
+                         "model": "SURVEY.md §8(d) regime B: 33/S bytes per algorithmic transition; "
+                                  "frac > 1: the exact reformulation reads/writes fewer bytes than the "
+                                  "reference recurrence needs (DESIGN.md §4)",
+                         "measured_dram_GBs": (dram / dp_time / 1e9) if dram and dp_time > 0 else None,
+                         "measured_dram_frac": (dram / dp_time / 1e9 / hbm) if dram and dp_time > 0 else None},
             "sweep_work": {k: timing[k] for k in ("sweep_rows", "sweep_cands", "sweep_checks")},
             "dp_work": {"live_cells": timing["live_cells"], "computed_cells": timing["dp_cells"]},
             "gpu_launches": int(allst[:, 5].sum()),
