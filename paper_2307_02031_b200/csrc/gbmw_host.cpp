@@ -111,6 +111,7 @@ struct gbmw_ctx {
     cudaStream_t stream = nullptr;
     cudaStream_t aux[kNumGroups] = {nullptr};   // K2 groups 1.. run concurrently with group 0
     cudaEvent_t fork = nullptr, join[kNumGroups] = {nullptr};
+    cudaEvent_t gspan[kNumGroups][2] = {{nullptr}};   // debug (GBMW_K2_HIST): per-stream K2 span
     uint64_t workspace_limit = 0;
     void *ws = nullptr;
     size_t ws_size = 0;
@@ -884,6 +885,13 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
             cudaStreamWaitEvent(ctx->aux[g], ctx->fork, 0);
             gs[g] = ctx->aux[g];
         }
+        static const bool k2_spans = getenv("GBMW_K2_HIST") && getenv("GBMW_K2_HIST")[0] == '1';
+        if (k2_spans)
+            for (int g = 0; g < kNumGroups; ++g) {
+                if (!used[g] && g != 0) continue;
+                if (!ctx->gspan[g][0]) { cudaEventCreate(&ctx->gspan[g][0]); cudaEventCreate(&ctx->gspan[g][1]); }
+                cudaEventRecord(ctx->gspan[g][0], gs[g]);
+            }
         for (size_t s = 0; s < c.slists.size(); ++s) {
             const StepList &sl = c.slists[s];
             const int g = c.slist_group[s];
@@ -903,6 +911,9 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
                 return cuda_fail(ctx, rc, "K2c launch");
             c.launches += 1;
         }
+        if (k2_spans)
+            for (int g = 0; g < kNumGroups; ++g)
+                if (used[g] || g == 0) cudaEventRecord(ctx->gspan[g][1], gs[g]);
         for (int g = 1; g < kNumGroups; ++g) {
             if (gs[g] == st) continue;
             cudaEventRecord(ctx->join[g], gs[g]);
@@ -946,6 +957,11 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
         if (getenv("GBMW_K2_HIST") && getenv("GBMW_K2_HIST")[0] == '1') {
             std::vector<unsigned long long> h(64);
             cudaMemcpy(h.data(), (char *)b->arena + b->o_stats + 5 * (nc + 1) * 8, 64 * 8, cudaMemcpyDeviceToHost);
+            for (int g = 0; g < kNumGroups; ++g) {
+                float ms = 0.f;
+                if (ctx->gspan[g][0] && cudaEventElapsedTime(&ms, ctx->gspan[g][0], ctx->gspan[g][1]) == cudaSuccess)
+                    fprintf(stderr, "K2 stream of group %d: %.3f ms\n", g, ms);
+            }
             fprintf(stderr, "K2 tiles by entries (bin: <2^b entries): ");
             for (int i = 0; i < 32; ++i)
                 if (h[i]) fprintf(stderr, "[%d] %llu tiles %llu ent  ", i, h[i], h[32 + i]);
