@@ -464,10 +464,11 @@ void prepare_problem(gbmw_batch &b, int pi, std::string *err) {
     h.n_step_tiles = (n_e + kStepRows - 1) / kStepRows;
     h.n_flagw = (!approx && h.U > 1) ? (int64_t)h.K * (flag_words(n_e) + sum_words(n_e)) : 0;
     h.n_rmap = approx ? 0 : (int64_t)(h.U > 1 ? h.U - 1 : 0) * rmap_groups(n_e);
-    h.ws_bytes = (size_t)h.n_cells * (sizeof(Cell) + sizeof(CellMem) + 4) + (size_t)h.U * 12 + (size_t)h.n_r * 8 + 8 +
+    h.ws_bytes = (size_t)h.n_cells * (2 * sizeof(Cell) + sizeof(CellMem) + 4) + (size_t)h.U * 12 + (size_t)h.n_r * 8 + 8 +
                  (size_t)h.n_bcells * 2 * sizeof(TFCell) + (size_t)h.n_par * 2 +
                  (size_t)h.n_tiles * sizeof(SweepPartial) + sizeof(SweepPartial) + 36 + (size_t)h.n_flagw * 8 +
-                 (size_t)h.n_rmap * 8 + (size_t)(h.U > 1 ? h.U - 1 : 0) * 24;
+                 (size_t)h.n_rmap * 8 + (size_t)(h.U > 1 ? h.U - 1 : 0) * 24 +
+                 (size_t)h.n_step_tiles * 2 * (kK2SlotEntries * 4 + kK2HeavyBytes + kK2RoundsPerSlot * 8);
     h.gpu = true;
 }
 
@@ -482,8 +483,8 @@ size_t put(std::vector<char> &blob, const T *src, size_t n) {
 // chunk workspace layout (byte offsets from ws base)
 struct WsLayout {
     size_t cells, cmem, rcls, bup, items, scount, tf0, tf1, chg0, chg1, rmap, par, parts, bestp, bound, ufirst, usorted, uprefix, uctr,
-        uniq, nuniq,
-        ulo, uhi, ctr, total;
+        uniq, ucell, nuniq,
+        ulo, uhi, ctr, k2e, k2c, k2h, k2r, total;
 };
 WsLayout ws_layout(const Chunk &c) {
     WsLayout w;
@@ -508,10 +509,18 @@ WsLayout ws_layout(const Chunk &c) {
     w.uprefix = o; o = align_up(o + (kMaxSweepRanks + 1) * 8);
     w.uctr = o; o = align_up(o + 8);
     w.uniq = o; o = align_up(o + c.n_cells * 4);
+    w.ucell = o; o = align_up(o + c.n_cells * sizeof(Cell));
     w.nuniq = o; o = align_up(o + c.n_units * 4);
     w.ulo = o; o = align_up(o + c.n_units * 4);
     w.uhi = o; o = align_up(o + c.n_units * 4);
-    w.ctr = o; o = align_up(o + (size_t)(c.Umax + 1) * kNumGroups * 8);
+    w.ctr = o; o = align_up(o + (size_t)(c.Umax + 1) * kNumGroups * 3 * 8);
+    {
+        const size_t slots = 2 * (size_t)c.step_prefix.back();
+        w.k2e = o; o = align_up(o + slots * kK2SlotEntries * 2);
+        w.k2c = o; o = align_up(o + slots * kK2SlotEntries * 2);
+        w.k2h = o; o = align_up(o + slots * kK2HeavyBytes);
+        w.k2r = o; o = align_up(o + slots * kK2RoundsPerSlot * sizeof(int2));
+    }
     w.total = o;
     return w;
 }
@@ -808,6 +817,10 @@ ChunkArgs chunk_args(gbmw_batch *b, const Chunk &c, char *ws, size_t chunk_index
     a.chg[0] = (uint32_t *)(ws + w.chg0);
     a.chg[1] = (uint32_t *)(ws + w.chg1);
     a.rmap = (int2 *)(ws + w.rmap);
+    a.k2_erow = (uint16_t *)(ws + w.k2e);
+    a.k2_echg = (uint16_t *)(ws + w.k2c);
+    a.k2_heavy = (void *)(ws + w.k2h);
+    a.k2_rounds = (int2 *)(ws + w.k2r);
     a.par = (uint16_t *)(ws + w.par);
     a.partials = (SweepPartial *)(ws + w.parts);
     a.best = (SweepPartial *)(ws + w.bestp);
@@ -817,6 +830,7 @@ ChunkArgs chunk_args(gbmw_batch *b, const Chunk &c, char *ws, size_t chunk_index
     a.uprefix = (int64_t *)(ws + w.uprefix);
     a.ucounter = (unsigned long long *)(ws + w.uctr);
     a.uniq = (int32_t *)(ws + w.uniq);
+    a.ucell = (Cell *)(ws + w.ucell);
     a.nuniq = (int32_t *)(ws + w.nuniq);
     a.unit_lo = (int32_t *)(ws + w.ulo);
     a.unit_hi = (int32_t *)(ws + w.uhi);
@@ -854,7 +868,7 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
         c.launches = 0;
         cudaEventRecord(c.ev[0], st);
         cudaMemsetAsync(a.bup, 0, c.probs.size() * 8, st);
-        cudaMemsetAsync(a.counters, 0, (size_t)(c.Umax + 1) * kNumGroups * 8, st);
+        cudaMemsetAsync(a.counters, 0, (size_t)(c.Umax + 1) * kNumGroups * 3 * 8, st);
         if ((rc = launch_cost_tables(a, c.n_cells, c.n_r, st))) return cuda_fail(ctx, rc, "K1 launch");
         c.launches += (c.n_cells > 0) + (c.n_r > 0) + (c.n_units > 0);
         cudaEventRecord(c.ev[1], st);
@@ -896,8 +910,9 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
             const StepList &sl = c.slists[s];
             const int g = c.slist_group[s];
             const int64_t ub = (s + 1 < c.slists.size() ? c.slists[s + 1].base : c.n_items) - sl.base;   // item bound
+            int2 *rounds = a.k2_rounds + 2 * c.step_prefix[c.group_lo[g]] * kK2RoundsPerSlot;
             if ((rc = launch_dp_step(a, g / kBands, sl.u, a.step_items + sl.base, a.step_count + s, ub,
-                                     a.counters + (size_t)sl.u * kNumGroups + g, gs[g])))
+                                     a.counters + ((size_t)sl.u * kNumGroups + g) * 3, rounds, gs[g])))
                 return cuda_fail(ctx, rc, "K2 launch");
             c.launches += 1;
         }
@@ -906,7 +921,7 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
             const int lo = c.group_lo[kApproxGroup], na = c.n_active[kApproxGroup][u];
             if (na == 0) continue;
             const int64_t base = c.step_prefix[lo], n = c.step_prefix[lo + na] - base;
-            if ((rc = launch_approx_step(a, u, base, n, a.counters + (size_t)u * kNumGroups + kApproxGroup,
+            if ((rc = launch_approx_step(a, u, base, n, a.counters + ((size_t)u * kNumGroups + kApproxGroup) * 3,
                                          gs[kApproxGroup])))
                 return cuda_fail(ctx, rc, "K2c launch");
             c.launches += 1;

@@ -23,7 +23,9 @@ constexpr int kMaxClasses = 16;
 constexpr int kMaxStrats = 512;      // smem staging of per-strategy constants
 constexpr int kStepThreads = 256;    // threads per K2 CTA
 constexpr int kStepRows = 2048;      // rows per K2 tile (64 groups of 32)
-constexpr int kItemTiles = 8;        // K2 work item: at most this many 1024-row warp tiles of one problem
+constexpr int kK2SlotEntries = 1024; // entries of one 1024-row K2 tile (anchor + breakpoints)
+constexpr int kK2RoundsPerSlot = 33; // evaluation rounds of a tile with 1024 entries
+constexpr int kK2HeavyBytes = 32;    // HeavyTile record
 
 // change-bit words per class column of n_e rows (one spare word for 2-word window reads)
 #if defined(__CUDACC__)
@@ -181,6 +183,9 @@ struct ChunkArgs {
     uint32_t *chg[2];             // change bits of B_u (ping-pong with TF): bit x = row x != row x-1
     int2 *rmap;                   // per unit u >= 1: row map of B_u (stored rows, see stored_row)
     unsigned long long *computed_cells;   // class cells K2 evaluated (rows x K), per chunk
+    uint16_t *k2_erow, *k2_echg;  // per K2 tile slot (2 per 2048-row step tile): entries of a heavy tile
+    void *k2_heavy;               // per tile slot: HeavyTile record (gbmw_step.cu)
+    int2 *k2_rounds;              // heavy-tile rounds (slot, round); per-group regions of 33 per slot
     unsigned long long *k2_hist;  // debug (GBMW_K2_HIST=1): [32] tiles, [32] entries by log2 entry count; or null
     uint16_t *par;
     SweepPartial *partials;       // per sweep tile: best bucket of an unsafe (K3b) or collapsed-DP (K3r) tile
@@ -191,6 +196,7 @@ struct ChunkArgs {
     int64_t *uprefix;             // kMaxSweepRanks + 1: K3b items before rank r (rank = tile from the top)
     unsigned long long *ucounter; // K3b work counter
     int32_t *uniq;                // per (unit, slot): strategy indices with distinct (w, k, c, ef), ascending
+    Cell *ucell;                  // per (unit, slot): the distinct cells themselves (cells[uniq])
     int32_t *nuniq;               // per unit: number of distinct strategies
     int32_t *unit_lo, *unit_hi;   // per unit u: live rows [L_u, H_u] of B_u (see k_dedupe)
     unsigned long long *counters; // per K2 launch: dynamic tile counter
@@ -206,7 +212,7 @@ struct ChunkArgs {
 int launch_cost_tables(const ChunkArgs &a, int64_t n_cells, int64_t n_r, void *stream);
 int launch_step_lists(const ChunkArgs &a, void *stream);
 int launch_dp_step(const ChunkArgs &a, int group, int u, const int4 *items, const int64_t *count, int64_t max_items,
-                   unsigned long long *counter, void *stream);
+                   unsigned long long *counters3, int2 *rounds, void *stream);
 int launch_sweep(const ChunkArgs &a, void *stream);
 int launch_approx_step(const ChunkArgs &a, int u, int64_t tile_base, int64_t n_tiles, unsigned long long *counter,
                        void *stream);

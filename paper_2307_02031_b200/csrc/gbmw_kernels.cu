@@ -123,7 +123,11 @@ __global__ void k_dedupe(ChunkArgs a) {
                 }
             }
             const unsigned m = __ballot_sync(0xffffffffu, keep);
-            if (keep) uniq[count + __popc(m & ((1u << lane) - 1u))] = i;
+            if (keep) {
+                const int slot = count + __popc(m & ((1u << lane) - 1u));
+                uniq[slot] = i;
+                a.ucell[p.cell_off + (int64_t)u * p.S + slot] = cells[i];
+            }
             count += __popc(m);
         }
         for (int off = 16; off > 0; off >>= 1) wmin = min(wmin, __shfl_xor_sync(0xffffffffu, wmin, off));
