@@ -121,6 +121,7 @@ struct gbmw_ctx {
     bool arena_busy = false;
     // grow-only pinned staging buffer for uploads
     void *pinned = nullptr;
+    std::vector<char> blob;                  // descriptor staging, reused across batches (no page faults)
     size_t pinned_cap = 0;
     gbmw_timing last{};
     std::string err;
@@ -475,8 +476,8 @@ void prepare_problem(gbmw_batch &b, int pi, std::string *err) {
 template <class T>
 size_t put(std::vector<char> &blob, const T *src, size_t n) {
     const size_t off = align_up(blob.size(), 16);
-    blob.resize(off + n * sizeof(T));
-    if (n) std::memcpy(blob.data() + off, src, n * sizeof(T));
+    blob.resize(off);
+    if (n) blob.insert(blob.end(), reinterpret_cast<const char *>(src), reinterpret_cast<const char *>(src + n));
     return off;
 }
 
@@ -548,6 +549,7 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
         prepare_problem(*b, (int)i, &msg);
         if (b->hp[i].status != GBMW_OK && first_err == GBMW_OK) { first_err = b->hp[i].status; first_msg = msg; }
     }
+    const double t_probs = now_ms();
     // output offsets
     int64_t plan = 0, front = 0;
     for (int64_t i = 0; i < n_problems; ++i) {
@@ -583,17 +585,33 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
         cur_bytes += need;
     }
     flush();
+    const double t_chunks = now_ms();
     // per-chunk descriptors
-    std::vector<char> blob;
+    std::vector<char> &blob = ctx->blob;
+    blob.clear();
+    {
+        size_t est = 0;                                  // one allocation for the descriptor blob
+        for (const Chunk &c : b->chunks) {
+            int64_t st = 0;
+            for (int pi : c.probs) st += b->hp[pi].n_step_tiles;
+            est += c.probs.size() * (sizeof(DevProblem) + 3 * 8 + 64) + (size_t)st * 4 + 64 * 1024;
+        }
+        blob.reserve(est);
+    }
+    double td[6] = {0, 0, 0, 0, 0, 0};
     for (Chunk &c : b->chunks) {
+        double tq = now_ms();
         std::stable_sort(c.probs.begin(), c.probs.end(), [&](int x, int y) {
             const int gx = problem_group(b->hp[x].K, b->problems[x].flags, b->hp[x].U);
             const int gy = problem_group(b->hp[y].K, b->problems[y].flags, b->hp[y].U);
             if (gx != gy) return gx < gy;
             return b->hp[x].U > b->hp[y].U;
         });
+        td[0] += now_ms() - tq; tq = now_ms();
         std::vector<DevProblem> dps;
         std::vector<int64_t> cellp{0}, rp{0}, stepp{0};
+        dps.reserve(c.probs.size());
+        cellp.reserve(c.probs.size() + 1); rp.reserve(c.probs.size() + 1); stepp.reserve(c.probs.size() + 1);
         std::vector<int2> aux;
         std::vector<int32_t> cand, ccls, clsd, clst, uf, uc;
         std::map<const StratInfo *, std::pair<int32_t, int32_t>> soff;
@@ -639,6 +657,7 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
             if (P.flags & GBMW_APPROX) c.n_approx++;
             c.max_k = std::max(c.max_k, h.K);
         }
+        td[1] += now_ms() - tq; tq = now_ms();
         c.step_prefix = stepp;
         // groups are contiguous in sorted order; within a group U is descending, so
         // the problems still active at unit u are a prefix of the group
@@ -651,6 +670,7 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
             for (int x = c.group_lo[g]; x < s; ++x)
                 for (int u = 0; u < b->hp[c.probs[x]].U && u <= c.Umax; ++u) c.n_active[g][u]++;
         }
+        td[2] += now_ms() - tq; tq = now_ms();
         std::vector<int32_t> stepmap(stepp.back());
         for (int x = 0; x < np; ++x) {
             for (int64_t t = stepp[x]; t < stepp[x + 1]; ++t) stepmap[t] = x;
@@ -659,6 +679,7 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
                 for (int t = 0; t < dps[x].n_sweep_tiles; ++t) aux.push_back(make_int2(x, t));
         }
         c.n_aux = (int64_t)aux.size();
+        td[3] += now_ms() - tq; tq = now_ms();
         const size_t base = align_up(blob.size(), 256);
         blob.resize(base);
         c.small_off = base;
@@ -689,11 +710,16 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
                 c.n_items += 2 * (c.step_prefix[lo + na] - c.step_prefix[lo]);
             }
         c.o_slists = put(blob, c.slists.data(), c.slists.size()) - base;
+        td[4] += now_ms() - tq; tq = now_ms();
         c.small_bytes = blob.size() - base;
         c.ws_bytes = ws_layout(c).total;
         b->max_ws = std::max(b->max_ws, c.ws_bytes);
     }
     const double t_prep = now_ms();
+    if (getenv("GBMW_K2_HIST") && getenv("GBMW_K2_HIST")[0] == '1')
+        fprintf(stderr, "create: problems %.3f ms, chunking %.3f ms, descriptors %.3f ms (sort %.3f loop %.3f groups %.3f "
+                "stepmap %.3f puts %.3f)\n", t_probs - t_start, t_chunks - t_probs, t_prep - t_chunks, td[0], td[1], td[2],
+                td[3], td[4]);
     // arena: inputs | descriptor blob | outputs
     size_t o = 0;
     b->o_layers = o; o = align_up(o + b->layers.size() * sizeof(gbmw_layer));
