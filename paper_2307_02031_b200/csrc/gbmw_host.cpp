@@ -483,7 +483,7 @@ size_t put(std::vector<char> &blob, const T *src, size_t n) {
 
 // chunk workspace layout (byte offsets from ws base)
 struct WsLayout {
-    size_t cells, cmem, rcls, bup, items, scount, tf0, tf1, chg0, chg1, rmap, par, parts, bestp, bound, ufirst, usorted, uprefix, uctr,
+    size_t cells, cmem, rcls, bup, items, scount, tf0, tf1, chg0, chg1, rmap, par, parts, bestp, bound, ufirst, upruned, usorted, uprefix, uctr,
         uniq, ucell, nuniq,
         ulo, uhi, ctr, k2e, k2c, k2h, k2r, total;
 };
@@ -506,6 +506,7 @@ WsLayout ws_layout(const Chunk &c) {
     w.bestp = o; o = align_up(o + c.probs.size() * sizeof(SweepPartial));
     w.bound = o; o = align_up(o + c.probs.size() * 16);
     w.ufirst = o; o = align_up(o + c.probs.size() * 4);
+    w.upruned = o; o = align_up(o + c.probs.size() * 4);
     w.usorted = o; o = align_up(o + c.probs.size() * 4);
     w.uprefix = o; o = align_up(o + (kMaxSweepRanks + 1) * 8);
     w.uctr = o; o = align_up(o + 8);
@@ -852,6 +853,7 @@ ChunkArgs chunk_args(gbmw_batch *b, const Chunk &c, char *ws, size_t chunk_index
     a.best = (SweepPartial *)(ws + w.bestp);
     a.bound = (unsigned long long *)(ws + w.bound);
     a.ufirst = (int32_t *)(ws + w.ufirst);
+    a.upruned = (int32_t *)(ws + w.upruned);
     a.usorted = (int32_t *)(ws + w.usorted);
     a.uprefix = (int64_t *)(ws + w.uprefix);
     a.ucounter = (unsigned long long *)(ws + w.uctr);

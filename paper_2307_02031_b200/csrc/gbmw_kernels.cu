@@ -410,6 +410,7 @@ __global__ void k_sweep_safe(ChunkArgs a) {
         a.bound[2 * q] = (unsigned long long)__double_as_longlong(t0);
         a.bound[2 * q + 1] = (unsigned long long)((j0 >= 0 ? e_s : -1) + 1);
         a.ufirst[q] = first_tile;
+        a.upruned[q] = 0;
     }
 }
 
@@ -516,21 +517,35 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
     __shared__ uint32_t sWK[kSweepWK];                  // weight << 4 | class per (unit, strategy)
     __shared__ int2 sRM[kSweepRmap];                    // row map of B_{U-1}, when it fits
     __shared__ long long s_next;
-    __shared__ int s_skip;
+    __shared__ int s_skip, s_q, s_tile;
     const long long total = a.uprefix[kMaxSweepRanks];
     const int lane = threadIdx.x & 31;
     int q_prev = -1;
     unsigned long long n_rows = 0, n_cands = 0, n_checks = 0;
     while (true) {
         __syncthreads();
-        if (threadIdx.x == 0) s_next = (long long)atomicAdd(a.ucounter, 1ull);
+        if (threadIdx.x == 0) {
+            const long long g = (long long)atomicAdd(a.ucounter, 1ull);
+            s_next = g;
+            if (g < total) {
+                const int rank = find_slot(a.uprefix, kMaxSweepRanks, g);
+                const int q = a.usorted[g - a.uprefix[rank]];
+                const int tile = a.probs[q].n_sweep_tiles - 1 - rank;
+                s_q = q; s_tile = tile;
+                // a higher tile of q was pruned: this one cannot win either (t0 is monotone)
+                s_skip = *(volatile int32_t *)(a.upruned + q);
+                if (s_skip) {
+                    SweepPartial none;
+                    none.t = GBMW_INF; none.e = -1; none.j = 0; none.pad_ = 0;
+                    a.partials[a.probs[q].tile_off + tile] = none;
+                }
+            }
+        }
         __syncthreads();
-        const long long g = s_next;
-        if (g >= total) break;
-        const int rank = find_slot(a.uprefix, kMaxSweepRanks, g);
-        const int q = a.usorted[g - a.uprefix[rank]];
+        if (s_next >= total) break;
+        if (s_skip) continue;
+        const int q = s_q, tile = s_tile;
         const DevProblem &p = a.probs[q];
-        const int tile = p.n_sweep_tiles - 1 - rank;
         const int S = p.S;
         const int last = p.U - 1;
         if (q != q_prev) {
@@ -589,6 +604,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
                 SweepPartial none;
                 none.t = GBMW_INF; none.e = -1; none.j = 0; none.pad_ = 0;
                 a.partials[p.tile_off + tile] = none;
+                a.upruned[q] = 1;
             }
             continue;
         }
