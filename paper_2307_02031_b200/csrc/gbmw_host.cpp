@@ -315,7 +315,11 @@ extern "C" int gbmw_ctx_create(int32_t device, uint64_t workspace_bytes, gbmw_ct
     if (ce != cudaSuccess) return set_err(nullptr, GBMW_ECUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(ce));
     gbmw_ctx *c = new gbmw_ctx();
     c->device = dev;
-    ce = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    {
+        int lo_pri = 0, hi_pri = 0;                      // the main stream carries the deep band of group 0
+        cudaDeviceGetStreamPriorityRange(&lo_pri, &hi_pri);
+        ce = cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, hi_pri);
+    }
     if (ce != cudaSuccess) {
         delete c;
         return set_err(nullptr, GBMW_ECUDA, std::string("cudaStreamCreate: ") + cudaGetErrorString(ce));
@@ -873,6 +877,12 @@ ChunkArgs chunk_args(gbmw_batch *b, const Chunk &c, char *ws, size_t chunk_index
     // GBMW_K2_HIST=1: per-tile entry-count histogram of K2 (log2 bins: tiles, entries), printed by run
     static const bool k2_hist = getenv("GBMW_K2_HIST") && getenv("GBMW_K2_HIST")[0] == '1';
     a.k2_hist = k2_hist ? (unsigned long long *)(arena + b->o_stats) + 5 * (b->chunks.size() + 1) : nullptr;
+    a.k2_tl = nullptr;
+    if (k2_hist) {
+        static unsigned long long *tl = nullptr;
+        if (!tl) cudaMalloc(&tl, 4096 * 2 * 8);
+        a.k2_tl = tl;
+    }
     return a;
 }
 
@@ -917,7 +927,11 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
             gs[g] = st;
             if (!used[g]) continue;
             if (!ctx->aux[g]) {
-                if (cudaStreamCreateWithFlags(&ctx->aux[g], cudaStreamNonBlocking) != cudaSuccess ||
+                // deep bands (the critical path: one launch per unit) get the higher priority
+                int lo_pri = 0, hi_pri = 0;
+                cudaDeviceGetStreamPriorityRange(&lo_pri, &hi_pri);
+                const int pri = (g < kStepVGroups && g % kBands == 0) ? hi_pri : lo_pri;
+                if (cudaStreamCreateWithPriority(&ctx->aux[g], cudaStreamNonBlocking, pri) != cudaSuccess ||
                     cudaEventCreateWithFlags(&ctx->join[g], cudaEventDisableTiming) != cudaSuccess)
                     return cuda_fail(ctx, (int)cudaGetLastError(), "aux stream");
             }
@@ -928,6 +942,12 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
             gs[g] = ctx->aux[g];
         }
         static const bool k2_spans = getenv("GBMW_K2_HIST") && getenv("GBMW_K2_HIST")[0] == '1';
+        if (k2_spans && a.k2_tl) {
+            std::vector<unsigned long long> init(4096 * 2);
+            for (size_t i = 0; i < init.size(); i += 2) { init[i] = ~0ull; init[i + 1] = 0ull; }
+            cudaMemcpyAsync(a.k2_tl, init.data(), init.size() * 8, cudaMemcpyHostToDevice, st);
+            cudaStreamSynchronize(st);
+        }
         if (k2_spans)
             for (int g = 0; g < kNumGroups; ++g) {
                 if (!used[g] && g != 0) continue;
@@ -940,7 +960,7 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
             const int64_t ub = (s + 1 < c.slists.size() ? c.slists[s + 1].base : c.n_items) - sl.base;   // item bound
             int2 *rounds = a.k2_rounds + 2 * c.step_prefix[c.group_lo[g]] * kK2RoundsPerSlot;
             if ((rc = launch_dp_step(a, g / kBands, sl.u, a.step_items + sl.base, a.step_count + s, ub,
-                                     a.counters + ((size_t)sl.u * kNumGroups + g) * 3, rounds, gs[g])))
+                                     a.counters + ((size_t)sl.u * kNumGroups + g) * 3, rounds, (int)s, gs[g])))
                 return cuda_fail(ctx, rc, "K2 launch");
             c.launches += 1;
         }
@@ -1004,6 +1024,20 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
                 float ms = 0.f;
                 if (ctx->gspan[g][0] && cudaEventElapsedTime(&ms, ctx->gspan[g][0], ctx->gspan[g][1]) == cudaSuccess)
                     fprintf(stderr, "K2 stream of group %d: %.3f ms\n", g, ms);
+            }
+            {
+                ChunkArgs al = chunk_args(b, b->chunks.back(), (char *)ctx->ws, b->chunks.size() - 1);
+                if (al.k2_tl) {
+                    const Chunk &cc = b->chunks.back();
+                    std::vector<unsigned long long> tl(4096 * 2);
+                    cudaMemcpy(tl.data(), al.k2_tl, tl.size() * 8, cudaMemcpyDeviceToHost);
+                    unsigned long long t0 = ~0ull;
+                    for (size_t l = 0; l < 2 * cc.slists.size(); ++l) t0 = std::min(t0, tl[2 * l]);
+                    for (size_t l = 0; l < cc.slists.size(); ++l)
+                        fprintf(stderr, "TL u=%d g=%d a=[%.1f, %.1f] b=[%.1f, %.1f] us\n", cc.slists[l].u, cc.slist_group[l],
+                                (tl[4 * l] - t0) / 1e3, (tl[4 * l + 1] - t0) / 1e3, (tl[4 * l + 2] - t0) / 1e3,
+                                (tl[4 * l + 3] - t0) / 1e3);
+                }
             }
             fprintf(stderr, "K2 tiles by entries (bin: <2^b entries): ");
             for (int i = 0; i < 32; ++i)

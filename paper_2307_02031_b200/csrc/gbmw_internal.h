@@ -186,6 +186,7 @@ struct ChunkArgs {
     uint16_t *k2_erow, *k2_echg;  // per K2 tile slot (2 per 2048-row step tile): entries of a heavy tile
     void *k2_heavy;               // per tile slot: HeavyTile record (gbmw_step.cu)
     int2 *k2_rounds;              // heavy-tile rounds (slot, round); per-group regions of 33 per slot
+    unsigned long long *k2_tl;    // debug (GBMW_K2_HIST=1): per launch {min start, max end} globaltimer, or null
     unsigned long long *k2_hist;  // debug (GBMW_K2_HIST=1): [32] tiles, [32] entries by log2 entry count; or null
     uint16_t *par;
     SweepPartial *partials;       // per sweep tile: best bucket of an unsafe (K3b) or collapsed-DP (K3r) tile
@@ -213,7 +214,7 @@ struct ChunkArgs {
 int launch_cost_tables(const ChunkArgs &a, int64_t n_cells, int64_t n_r, void *stream);
 int launch_step_lists(const ChunkArgs &a, void *stream);
 int launch_dp_step(const ChunkArgs &a, int group, int u, const int4 *items, const int64_t *count, int64_t max_items,
-                   unsigned long long *counters3, int2 *rounds, void *stream);
+                   unsigned long long *counters3, int2 *rounds, int tl_id, void *stream);
 int launch_sweep(const ChunkArgs &a, void *stream);
 int launch_approx_step(const ChunkArgs &a, int u, int64_t tile_base, int64_t n_tiles, unsigned long long *counter,
                        void *stream);

@@ -454,11 +454,24 @@ int launch_step_lists(const ChunkArgs &a, void *stream) {
         CALL(kMaxClasses, true);                                                     \
     }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+// debug timeline: slot 2 * id = earliest CTA start, 2 * id + 1 = latest CTA end
+__device__ __forceinline__ void tl_mark(unsigned long long *tl, int id, bool end) {
+    if (!tl || threadIdx.x != 0) return;
+    if (end) atomicMax(tl + 2 * id + 1, gtimer()); else atomicMin(tl + 2 * id, gtimer());
+}
+
 // K2a: a warp per tile (dynamic counter over the launch's tiles).  Tiles whose entries fit
 // one round are finished here; heavier ones are handed to K2b.
 template <int GROUP, bool FIRST>
 __global__ void __launch_bounds__(kStepThreads, GROUP <= 1 ? 3 : 1)
-    k_dp_classify(ChunkArgs a, int u, const int4 *items, const int64_t *count, unsigned long long *ctr, int2 *rlist) {
+    k_dp_classify(ChunkArgs a, int u, const int4 *items, const int64_t *count, unsigned long long *ctr, int2 *rlist,
+                  int tl_id) {
+    tl_mark(a.k2_tl, tl_id, false);
     __shared__ TileCtx s_t[kK2Warps];
     __shared__ uint16_t s_erow[kK2Warps][kWarpRows];
     __shared__ uint16_t s_echg[kK2Warps][kWarpRows];
@@ -468,10 +481,10 @@ __global__ void __launch_bounds__(kStepThreads, GROUP <= 1 ? 3 : 1)
     const int64_t n_items = *count;
     unsigned long long stat_rows = 0;
     int q_prev = -1;
-    while (true) {
-        int64_t it = 0;
-        if (lane == 0) it = (int64_t)atomicAdd(ctr, 1ull);
-        it = __shfl_sync(0xffffffffu, it, 0);
+    // non-persistent: warp w of CTA b takes item b * kK2Warps + w and retires, so slots free
+    // up continuously and the deep bands' (higher-priority) CTAs get them
+    for (int pass = 0; pass < 1; ++pass) {
+        const int64_t it = (int64_t)blockIdx.x * kK2Warps + warp;
         if (it >= n_items) break;
         const int4 item = __ldg(items + it);
         if (lane == 0) {
@@ -513,13 +526,16 @@ __global__ void __launch_bounds__(kStepThreads, GROUP <= 1 ? 3 : 1)
         __syncwarp();
     }
     if (lane == 0 && stat_rows) atomicAdd(a.computed_cells, stat_rows);
+    __syncthreads();
+    tl_mark(a.k2_tl, tl_id, true);
 }
 
 // K2b: a warp per round of the launch's heavy tiles; the warp completing a tile's last round
 // finishes the tile.
 template <int GROUP, bool FIRST>
 __global__ void __launch_bounds__(kStepThreads, GROUP <= 1 ? 3 : 1)
-    k_dp_rounds(ChunkArgs a, int u, unsigned long long *ctr, const int2 *rlist) {
+    k_dp_rounds(ChunkArgs a, int u, unsigned long long *ctr, const int2 *rlist, int tl_id) {
+    tl_mark(a.k2_tl, tl_id, false);
     __shared__ TileCtx s_t[kK2Warps];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     TileCtx &t = s_t[warp];
@@ -556,11 +572,13 @@ __global__ void __launch_bounds__(kStepThreads, GROUP <= 1 ? 3 : 1)
         }
         __syncwarp();
     }
+    __syncthreads();
+    tl_mark(a.k2_tl, tl_id, true);
 }
 #undef GBMW_K2_DISPATCH
 
 int launch_dp_step(const ChunkArgs &a, int group, int u, const int4 *items, const int64_t *count, int64_t n_items,
-                   unsigned long long *ctr, int2 *rounds, void *stream) {
+                   unsigned long long *ctr, int2 *rounds, int tl_id, void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
     if (n_items <= 0) return 0;
     static int sms = 0;
@@ -584,17 +602,15 @@ int launch_dp_step(const ChunkArgs &a, int group, int u, const int4 *items, cons
         else if (group == 1) { if (fi) GBMW_PREP(1, true); else GBMW_PREP(1, false); }
         else { if (fi) GBMW_PREP(2, true); else GBMW_PREP(2, false); }
     }
-    const int64_t want = (n_items + kK2Warps - 1) / kK2Warps;
-    const int64_t max_a = (int64_t)sms * occ[group][fi][0];
-    const unsigned grid_a = (unsigned)(want < max_a ? want : max_a);
+    const unsigned grid_a = (unsigned)((n_items + kK2Warps - 1) / kK2Warps);   // one item per warp
     const unsigned grid_b = (unsigned)(sms * occ[group][fi][1]);
 #define GBMW_STEP(G)                                                                                    \
     if (fi) {                                                                                           \
-        k_dp_classify<G, true><<<grid_a, kStepThreads, 0, st>>>(a, u, items, count, ctr, rounds);              \
-        k_dp_rounds<G, true><<<grid_b, kStepThreads, 0, st>>>(a, u, ctr, rounds);                              \
+        k_dp_classify<G, true><<<grid_a, kStepThreads, 0, st>>>(a, u, items, count, ctr, rounds, 2 * tl_id);              \
+        k_dp_rounds<G, true><<<grid_b, kStepThreads, 0, st>>>(a, u, ctr, rounds, 2 * tl_id + 1);                              \
     } else {                                                                                            \
-        k_dp_classify<G, false><<<grid_a, kStepThreads, 0, st>>>(a, u, items, count, ctr, rounds);             \
-        k_dp_rounds<G, false><<<grid_b, kStepThreads, 0, st>>>(a, u, ctr, rounds);                             \
+        k_dp_classify<G, false><<<grid_a, kStepThreads, 0, st>>>(a, u, items, count, ctr, rounds, 2 * tl_id);             \
+        k_dp_rounds<G, false><<<grid_b, kStepThreads, 0, st>>>(a, u, ctr, rounds, 2 * tl_id + 1);                             \
     }
     if (group == 0) { GBMW_STEP(0) }
     else if (group == 1) { GBMW_STEP(1) }
