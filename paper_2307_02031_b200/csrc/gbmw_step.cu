@@ -454,6 +454,11 @@ int launch_step_lists(const ChunkArgs &a, void *stream) {
         CALL(kMaxClasses, true);                                                     \
     }
 
+// Programmatic dependent launch: every K2 kernel waits for its stream predecessor's
+// results before touching memory, and lets its successor launch once it is done.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -471,6 +476,7 @@ template <int GROUP, bool FIRST>
 __global__ void __launch_bounds__(kStepThreads, GROUP <= 1 ? 3 : 1)
     k_dp_classify(ChunkArgs a, int u, const int4 *items, const int64_t *count, unsigned long long *ctr, int2 *rlist,
                   int tl_id) {
+    pdl_wait();
     tl_mark(a.k2_tl, tl_id, false);
     __shared__ TileCtx s_t[kK2Warps];
     __shared__ uint16_t s_erow[kK2Warps][kWarpRows];
@@ -528,6 +534,7 @@ __global__ void __launch_bounds__(kStepThreads, GROUP <= 1 ? 3 : 1)
     if (lane == 0 && stat_rows) atomicAdd(a.computed_cells, stat_rows);
     __syncthreads();
     tl_mark(a.k2_tl, tl_id, true);
+    pdl_trigger();
 }
 
 // K2b: a warp per round of the launch's heavy tiles; the warp completing a tile's last round
@@ -535,6 +542,7 @@ __global__ void __launch_bounds__(kStepThreads, GROUP <= 1 ? 3 : 1)
 template <int GROUP, bool FIRST>
 __global__ void __launch_bounds__(kStepThreads, GROUP <= 1 ? 3 : 1)
     k_dp_rounds(ChunkArgs a, int u, unsigned long long *ctr, const int2 *rlist, int tl_id) {
+    pdl_wait();
     tl_mark(a.k2_tl, tl_id, false);
     __shared__ TileCtx s_t[kK2Warps];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -574,6 +582,7 @@ __global__ void __launch_bounds__(kStepThreads, GROUP <= 1 ? 3 : 1)
     }
     __syncthreads();
     tl_mark(a.k2_tl, tl_id, true);
+    pdl_trigger();
 }
 #undef GBMW_K2_DISPATCH
 
@@ -604,13 +613,21 @@ int launch_dp_step(const ChunkArgs &a, int group, int u, const int4 *items, cons
     }
     const unsigned grid_a = (unsigned)((n_items + kK2Warps - 1) / kK2Warps);   // one item per warp
     const unsigned grid_b = (unsigned)(sms * occ[group][fi][1]);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg_a = {}, cfg_b = {};
+    cfg_a.gridDim = dim3(grid_a); cfg_a.blockDim = dim3(kStepThreads); cfg_a.stream = st;
+    cfg_a.attrs = attr; cfg_a.numAttrs = 1;
+    cfg_b = cfg_a; cfg_b.gridDim = dim3(grid_b);
+    const int ta = 2 * tl_id, tb = 2 * tl_id + 1;
 #define GBMW_STEP(G)                                                                                    \
     if (fi) {                                                                                           \
-        k_dp_classify<G, true><<<grid_a, kStepThreads, 0, st>>>(a, u, items, count, ctr, rounds, 2 * tl_id);              \
-        k_dp_rounds<G, true><<<grid_b, kStepThreads, 0, st>>>(a, u, ctr, rounds, 2 * tl_id + 1);                              \
+        cudaLaunchKernelEx(&cfg_a, k_dp_classify<G, true>, a, u, items, count, ctr, rounds, ta);        \
+        cudaLaunchKernelEx(&cfg_b, k_dp_rounds<G, true>, a, u, ctr, (const int2 *)rounds, tb);          \
     } else {                                                                                            \
-        k_dp_classify<G, false><<<grid_a, kStepThreads, 0, st>>>(a, u, items, count, ctr, rounds, 2 * tl_id);             \
-        k_dp_rounds<G, false><<<grid_b, kStepThreads, 0, st>>>(a, u, ctr, rounds, 2 * tl_id + 1);                             \
+        cudaLaunchKernelEx(&cfg_a, k_dp_classify<G, false>, a, u, items, count, ctr, rounds, ta);       \
+        cudaLaunchKernelEx(&cfg_b, k_dp_rounds<G, false>, a, u, ctr, (const int2 *)rounds, tb);         \
     }
     if (group == 0) { GBMW_STEP(0) }
     else if (group == 1) { GBMW_STEP(1) }
