@@ -1031,12 +1031,15 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
                     const Chunk &cc = b->chunks.back();
                     std::vector<unsigned long long> tl(4096 * 2);
                     cudaMemcpy(tl.data(), al.k2_tl, tl.size() * 8, cudaMemcpyDeviceToHost);
+                    std::vector<unsigned long long> ctrs((size_t)(cc.Umax + 1) * kNumGroups * 3);
+                    cudaMemcpy(ctrs.data(), al.counters, ctrs.size() * 8, cudaMemcpyDeviceToHost);
                     unsigned long long t0 = ~0ull;
                     for (size_t l = 0; l < 2 * cc.slists.size(); ++l) t0 = std::min(t0, tl[2 * l]);
                     for (size_t l = 0; l < cc.slists.size(); ++l)
-                        fprintf(stderr, "TL u=%d g=%d a=[%.1f, %.1f] b=[%.1f, %.1f] us\n", cc.slists[l].u, cc.slist_group[l],
-                                (tl[4 * l] - t0) / 1e3, (tl[4 * l + 1] - t0) / 1e3, (tl[4 * l + 2] - t0) / 1e3,
-                                (tl[4 * l + 3] - t0) / 1e3);
+                        fprintf(stderr, "TL u=%d g=%d a=[%.1f, %.1f] b=[%.1f, %.1f] us rounds=%llu\n", cc.slists[l].u,
+                                cc.slist_group[l], (tl[4 * l] - t0) / 1e3, (tl[4 * l + 1] - t0) / 1e3,
+                                (tl[4 * l + 2] - t0) / 1e3, (tl[4 * l + 3] - t0) / 1e3,
+                                ctrs[((size_t)cc.slists[l].u * kNumGroups + cc.slist_group[l]) * 3 + 1]);
                 }
             }
             fprintf(stderr, "K2 tiles by entries (bin: <2^b entries): ");

@@ -278,12 +278,19 @@ __device__ __forceinline__ int classify_tile(const ChunkArgs &a, TileCtx &t, uin
     return n;
 }
 
-// Evaluation rounds of a tile with n entries, kRoundE entries per round: round 0 takes entries
-// [0, kRoundE) (a segment of 32 / next_pow2(entries) lanes each), round r >= 1 re-evaluates
-// entry (kRoundE - 1) r (the previous one, for the comparison) and takes the kRoundE - 1
-// after it (32 / kRoundE lanes per entry: short dependent-load chains per round).
-constexpr int kRoundE = 8;
-__device__ __forceinline__ int tile_rounds(int n) { return n <= kRoundE ? 1 : 1 + (n - 2) / (kRoundE - 1); }
+// Evaluation rounds of a tile with n entries, E entries per round: round 0 takes entries
+// [0, E) (a segment of 32 / next_pow2(entries) lanes each), round r >= 1 re-evaluates entry
+// (E - 1) r (the previous one, for the comparison) and takes the E - 1 after it, 32 / E
+// lanes per entry.  Tiles with up to kLightE entries are one round (in K2a); heavier tiles
+// use 8-entry rounds (short dependent-load chains, many warps), very dense ones 32-entry
+// rounds (a lane per row: fewest instructions per entry).
+constexpr int kLightE = 8;
+constexpr int kDenseN = 256;
+__device__ __forceinline__ int round_entries(int n) { return n <= kLightE ? kLightE : (n < kDenseN ? 8 : 32); }
+__device__ __forceinline__ int tile_rounds(int n) {
+    const int E = round_entries(n);
+    return n <= E ? 1 : 1 + (n - 2) / (E - 1);
+}
 
 // Phase B, one round of one tile by one warp: evaluate its entries, compare each with the
 // previous entry (unchanged columns keep change bit 0), store (t, f, argmin) of the
@@ -293,15 +300,16 @@ __device__ __forceinline__ void eval_round(const ChunkArgs &a, const TileCtx &t,
     const int K = GUARD ? t.K : KT;
     const int n_e = t.n_e, n = t.n_ent;
     int L, j0, nr;                                       // lanes per entry, first entry, entries
+    const int E = round_entries(n);
     if (r == 0) {
-        nr = n < kRoundE ? n : kRoundE;
+        nr = n < E ? n : E;
         L = 32;
         while (L > 1 && (32 / L) < nr) L >>= 1;
         j0 = 0;
     } else {
-        L = 32 / kRoundE;
-        j0 = (kRoundE - 1) * r;                          // = (first new entry) - 1
-        nr = min(kRoundE, n - j0);
+        L = 32 / E;
+        j0 = (E - 1) * r;                                // = (first new entry) - 1
+        nr = min(E, n - j0);
     }
     const int seg = lane / L, l = lane - seg * L;
     const int j = j0 + seg;
@@ -548,10 +556,10 @@ __global__ void __launch_bounds__(kStepThreads, GROUP <= 1 ? 3 : 1)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     TileCtx &t = s_t[warp];
     const int64_t total = (int64_t)*(volatile unsigned long long *)(ctr + 1);
+    // first round: the warp's global index (no atomic); later ones from the counter
+    const int64_t n_warps = (int64_t)gridDim.x * kK2Warps;
+    int64_t R = (int64_t)blockIdx.x * kK2Warps + warp;
     while (true) {
-        int64_t R = 0;
-        if (lane == 0) R = (int64_t)atomicAdd(ctr + 2, 1ull);
-        R = __shfl_sync(0xffffffffu, R, 0);
         if (R >= total) break;
         const int2 rr = rlist[R];
         const int64_t slot = rr.x;
@@ -579,6 +587,10 @@ __global__ void __launch_bounds__(kStepThreads, GROUP <= 1 ? 3 : 1)
 #undef GBMW_K2_FIN
         }
         __syncwarp();
+        if (n_warps >= total) break;
+        int64_t nx = 0;
+        if (lane == 0) nx = n_warps + (int64_t)atomicAdd(ctr + 2, 1ull);
+        R = __shfl_sync(0xffffffffu, nx, 0);
     }
     __syncthreads();
     tl_mark(a.k2_tl, tl_id, true);
