@@ -82,7 +82,7 @@ def main():
     PROF.mkdir(exist_ok=True)
     agg, total = launches(tag)
     (PROF / f"{tag}_launches.json").write_text(json.dumps({"total_us": total, "kernels": agg}, indent=1))
-    k2 = {k: v for k, v in agg.items() if "k_dp_step" in k}
+    k2 = {k: v for k, v in agg.items() if "k_dp_" in k}
     n = sum(v["launches"] for v in k2.values())
     b = sum(v["dram_bytes"] for v in k2.values())
     if n:
