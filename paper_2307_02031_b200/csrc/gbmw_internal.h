@@ -25,7 +25,7 @@ constexpr int kStepThreads = 256;    // threads per K2 CTA
 constexpr int kStepRows = 2048;      // rows per K2 tile (64 groups of 32)
 constexpr int kK2SlotEntries = 1024; // entries of one 1024-row K2 tile (anchor + breakpoints)
 constexpr int kK2RoundsPerSlot = 33; // evaluation rounds of a tile with 1024 entries
-constexpr int kK2HeavyBytes = 32;    // HeavyTile record
+constexpr int kK2HeavyBytes = 256;   // HeavyTile record (tile context + group entry offsets)
 
 // change-bit words per class column of n_e rows (one spare word for 2-word window reads)
 #if defined(__CUDACC__)

@@ -48,14 +48,16 @@ struct TileCtx {
     int64_t rm_prev, rm_cur;                // row maps of B_{u-1} and B_u (offsets into a.rmap)
     uint16_t *erow;                         // row of each entry, relative to the tile's first row
     uint16_t *echg;                         // bit kk: column kk changes at the entry's row
+    const uint16_t *goff;                   // heavy tiles: first entry of each 32-row group (33), or null
 };
 
-// Heavy tile deferred to K2b (one per tile slot).
-struct HeavyTile {
-    int32_t q, tile, n_ent, first_bp;
-    int32_t rounds, done, pad_[2];
+// Heavy tile deferred to K2b (one per tile slot): its context, so K2b reads one record.
+struct alignas(16) HeavyTile {
+    TileCtx t;
+    int32_t rounds, done;
+    uint16_t goff[33];                      // first entry of group g; goff[32] = n_ent
 };
-static_assert(sizeof(HeavyTile) == kK2HeavyBytes, "HeavyTile size");
+static_assert(sizeof(HeavyTile) <= kK2HeavyBytes, "HeavyTile size");
 
 __device__ __forceinline__ void load_tile_ctx(const ChunkArgs &a, int u, int q, int tile, TileCtx &t) {
     const DevProblem &p = a.probs[q];
@@ -178,7 +180,8 @@ __device__ __forceinline__ unsigned window_segments(unsigned long long v, int x0
 // the tile's entries in row order; its first live row is always an entry (the anchor of
 // the row map).  Returns the entry count.
 template <bool FIRST>
-__device__ __forceinline__ int classify_tile(const ChunkArgs &a, TileCtx &t, uint16_t *alist, int u, int lane) {
+__device__ __forceinline__ int classify_tile(const ChunkArgs &a, TileCtx &t, uint16_t *alist, uint16_t *goff, int u,
+                                             int lane) {
     const int lo = t.lo, hi = t.hi, S = t.S, lo_prev = t.lo_prev;
     const int r_base = t.r_base;
     // sources whose window [r_base - w, r_base + 1023 - w] holds a change
@@ -266,6 +269,7 @@ __device__ __forceinline__ int classify_tile(const ChunkArgs &a, TileCtx &t, uin
         if (lane >= off) incl += v;
     }
     int at = incl - cnt;
+    if (goff) { goff[g] = (uint16_t)at; if (g == 31) goff[32] = (uint16_t)incl; }
     unsigned m = seg;
     while (m) {
         const int x = __ffs(m) - 1;
@@ -358,11 +362,16 @@ __device__ __forceinline__ void finish_tile(const ChunkArgs &a, const TileCtx &t
     const bool dead = r1 < lo || r0 > hi;
     auto erow = [&](int j) { return GLOBAL ? (int)__ldcg(t.erow + j) : (int)t.erow[j]; };
     auto echg = [&](int j) { return GLOBAL ? (unsigned)__ldcg(t.echg + j) : (unsigned)t.echg[j]; };
-    // entries of group g: binary search of the first entry with row >= 32 g
+    // entries of group g: recorded offsets (heavy tiles), else binary search of the first
+    // entry with row >= 32 g
     int b0 = 0, b1 = n;
-    while (b0 < b1) {
-        const int mid = (b0 + b1) >> 1;
-        if (erow(mid) < 32 * g) b0 = mid + 1; else b1 = mid;
+    if (t.goff) {
+        b0 = __ldcg(t.goff + g);
+    } else {
+        while (b0 < b1) {
+            const int mid = (b0 + b1) >> 1;
+            if (erow(mid) < 32 * g) b0 = mid + 1; else b1 = mid;
+        }
     }
     int last = -1;                                       // last stored row of the group
     unsigned sbits = 0u;
@@ -490,6 +499,7 @@ __global__ void __launch_bounds__(kStepThreads, GROUP <= 1 ? 3 : 1)
     __shared__ uint16_t s_erow[kK2Warps][kWarpRows];
     __shared__ uint16_t s_echg[kK2Warps][kWarpRows];
     __shared__ uint16_t s_alist[kK2Warps][kMaxStrats];
+    __shared__ uint16_t s_goff[kK2Warps][34];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     TileCtx &t = s_t[warp];
     const int64_t n_items = *count;
@@ -504,11 +514,11 @@ __global__ void __launch_bounds__(kStepThreads, GROUP <= 1 ? 3 : 1)
         if (lane == 0) {
             if (item.x != q_prev) load_tile_ctx(a, u, item.x, item.y, t);
             t.r_base = item.y * kWarpRows;
-            t.erow = s_erow[warp]; t.echg = s_echg[warp];
+            t.erow = s_erow[warp]; t.echg = s_echg[warp]; t.goff = nullptr;
         }
         q_prev = item.x;
         __syncwarp();
-        const int n = classify_tile<FIRST>(a, t, s_alist[warp], u, lane);
+        const int n = classify_tile<FIRST>(a, t, s_alist[warp], s_goff[warp], u, lane);
         const int K = t.K;
         stat_rows += (unsigned long long)n * (unsigned long long)K;
         const int rounds = tile_rounds(n);
@@ -526,11 +536,16 @@ __global__ void __launch_bounds__(kStepThreads, GROUP <= 1 ? 3 : 1)
             uint16_t *ge = a.k2_erow + slot * kK2SlotEntries;
             for (int j = lane; j < n; j += 32) ge[j] = s_erow[warp][j];
             unsigned long long base = 0;
+            HeavyTile *hr = reinterpret_cast<HeavyTile *>(a.k2_heavy) + slot;
+            for (int g = lane; g < 33; g += 32) hr->goff[g] = s_goff[warp][g];
+            __threadfence();                             // entries and offsets before the round list
+            __syncwarp();
             if (lane == 0) {
-                HeavyTile h;
-                h.q = item.x; h.tile = item.y; h.n_ent = n; h.first_bp = t.first_bp;
-                h.rounds = rounds; h.done = 0; h.pad_[0] = h.pad_[1] = 0;
-                reinterpret_cast<HeavyTile *>(a.k2_heavy)[slot] = h;
+                TileCtx c = t;
+                c.erow = ge; c.echg = a.k2_echg + slot * kK2SlotEntries; c.goff = hr->goff;
+                hr->t = c;
+                hr->rounds = rounds; hr->done = 0;
+                __threadfence();
                 base = atomicAdd(ctr + 1, (unsigned long long)rounds);
             }
             base = __shfl_sync(0xffffffffu, base, 0);
@@ -564,11 +579,11 @@ __global__ void __launch_bounds__(kStepThreads, GROUP <= 1 ? 3 : 1)
         const int2 rr = rlist[R];
         const int64_t slot = rr.x;
         HeavyTile *ht = reinterpret_cast<HeavyTile *>(a.k2_heavy) + slot;
-        if (lane == 0) {
-            load_tile_ctx(a, u, ht->q, ht->tile, t);
-            t.n_ent = ht->n_ent; t.first_bp = ht->first_bp;
-            t.erow = a.k2_erow + slot * kK2SlotEntries;
-            t.echg = a.k2_echg + slot * kK2SlotEntries;
+        {                                                // the tile's context: one record, 8 B per lane
+            static_assert(sizeof(TileCtx) % 8 == 0 && sizeof(TileCtx) <= 256, "TileCtx copy");
+            const unsigned long long *src = reinterpret_cast<const unsigned long long *>(&ht->t);
+            unsigned long long *dst = reinterpret_cast<unsigned long long *>(&t);
+            if (lane < (int)(sizeof(TileCtx) / 8)) dst[lane] = __ldcg(src + lane);
         }
         __syncwarp();
         const int K = t.K;
