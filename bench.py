@@ -168,7 +168,7 @@ def cpu_sample(L, S, E, P, T, seconds, threads):
     problems whose estimated single-core time sums to ~seconds * threads."""
     rng = np.random.default_rng(20261017)
     order = rng.permutation(len(P))
-    budget = seconds * threads * 2.5e8          # ~2.5e8 transitions/s per core (oracle, measured)
+    budget = seconds * threads * 1.25e8         # ~1.25e8 transitions/s per core (oracle on the GPU box, measured)
     pick, acc = [], 0.0
     for i in order:
         if T[i] > budget * 0.25:                 # skip single searches larger than a quarter sample
