@@ -136,6 +136,10 @@ struct gbmw_batch {
     std::vector<Chunk> chunks;
     std::map<std::tuple<int32_t, int32_t, int64_t>, std::unique_ptr<StratInfo>> strat_cache;
     std::map<std::tuple<int32_t, int32_t, int>, std::unique_ptr<UnitInfo>> unit_cache;
+    const StratInfo *strat_last = nullptr;   // last lookups (consecutive problems usually share them)
+    std::tuple<int32_t, int32_t, int64_t> strat_last_key{};
+    const UnitInfo *unit_last = nullptr;
+    std::tuple<int32_t, int32_t, int> unit_last_key{};
     int64_t total_plan = 0, total_frontier = 0;
     // device arena: inputs | chunk descriptor blocks | outputs
     void *arena = nullptr;
@@ -357,8 +361,9 @@ namespace {
 // usable strategies + classes of one strategy list at one micro-batch (dpsearch.py:42-43)
 const StratInfo *strat_info(gbmw_batch &b, const gbmw_problem &P) {
     auto key = std::make_tuple(P.strat_begin, P.n_strats, P.micro_batch);
+    if (b.strat_last && b.strat_last_key == key) return b.strat_last;   // consecutive problems share it
     auto it = b.strat_cache.find(key);
-    if (it != b.strat_cache.end()) return it->second.get();
+    if (it != b.strat_cache.end()) { b.strat_last = it->second.get(); b.strat_last_key = key; return b.strat_last; }
     auto si = std::make_unique<StratInfo>();
     for (int i = 0; i < P.n_strats && si->status == GBMW_OK; ++i) {
         const gbmw_strategy &s = b.strats[P.strat_begin + i];
@@ -385,8 +390,9 @@ const StratInfo *strat_info(gbmw_batch &b, const gbmw_problem &P) {
 const UnitInfo *unit_info(gbmw_batch &b, const gbmw_problem &P) {
     const bool fuse = (P.flags & GBMW_FUSE) != 0;
     auto key = std::make_tuple(P.layer_begin, P.n_layers, (int)fuse);
+    if (b.unit_last && b.unit_last_key == key) return b.unit_last;
     auto it = b.unit_cache.find(key);
-    if (it != b.unit_cache.end()) return it->second.get();
+    if (it != b.unit_cache.end()) { b.unit_last = it->second.get(); b.unit_last_key = key; return b.unit_last; }
     auto ui = std::make_unique<UnitInfo>();
     for (int i = 0; i < P.n_layers; ++i) {
         const int gl = P.layer_begin + i;
@@ -606,12 +612,17 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
     double td[6] = {0, 0, 0, 0, 0, 0};
     for (Chunk &c : b->chunks) {
         double tq = now_ms();
-        std::stable_sort(c.probs.begin(), c.probs.end(), [&](int x, int y) {
-            const int gx = problem_group(b->hp[x].K, b->problems[x].flags, b->hp[x].U);
-            const int gy = problem_group(b->hp[y].K, b->problems[y].flags, b->hp[y].U);
-            if (gx != gy) return gx < gy;
-            return b->hp[x].U > b->hp[y].U;
-        });
+        {
+            // (group ascending, U descending, input order): one precomputed key per problem
+            std::vector<std::pair<int64_t, int>> keys(c.probs.size());
+            for (size_t i = 0; i < c.probs.size(); ++i) {
+                const int x = c.probs[i];
+                const int g = problem_group(b->hp[x].K, b->problems[x].flags, b->hp[x].U);
+                keys[i] = {((int64_t)g << 40) | ((int64_t)(kMaxUnits - b->hp[x].U) << 28) | (int64_t)i, x};
+            }
+            std::sort(keys.begin(), keys.end());
+            for (size_t i = 0; i < keys.size(); ++i) c.probs[i] = keys[i].second;
+        }
         td[0] += now_ms() - tq; tq = now_ms();
         std::vector<DevProblem> dps;
         std::vector<int64_t> cellp{0}, rp{0}, stepp{0};
