@@ -322,7 +322,7 @@ extern "C" int gbmw_ctx_create(int32_t device, uint64_t workspace_bytes, gbmw_ct
     {
         int lo_pri = 0, hi_pri = 0;                      // the main stream carries the deep band of group 0
         cudaDeviceGetStreamPriorityRange(&lo_pri, &hi_pri);
-        ce = cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, hi_pri);
+        ce = cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, hi_pri < lo_pri ? hi_pri + 1 : hi_pri);
     }
     if (ce != cudaSuccess) {
         delete c;
@@ -941,6 +941,8 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
                 // deep bands (the critical path: one launch per unit) get the higher priority
                 int lo_pri = 0, hi_pri = 0;
                 cudaDeviceGetStreamPriorityRange(&lo_pri, &hi_pri);
+                // deep bands above shallow ones; among deep bands the wider classes (their
+                // steps are the longest) above the main stream's K <= 4 band
                 const int pri = (g < kStepVGroups && g % kBands == 0) ? hi_pri : lo_pri;
                 if (cudaStreamCreateWithPriority(&ctx->aux[g], cudaStreamNonBlocking, pri) != cudaSuccess ||
                     cudaEventCreateWithFlags(&ctx->join[g], cudaEventDisableTiming) != cudaSuccess)
