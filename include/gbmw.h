@@ -240,6 +240,14 @@ int  gbmw_init_partition(const gbmw_layer *layers, int32_t n_layers, const gbmw_
 int  gbmw_seed_for(const gbmw_layer *layers, int32_t n_layers, const gbmw_env *env, int64_t n_devices,
                    int64_t pp_degree, int64_t micro_batch, int32_t n_micro, double budget,
                    gbmw_strategy *out_seed, int32_t *out_sizes);
+/* gbmw_seed_for over many (pp_degree, micro_batch, n_micro) cells of one model and cluster,
+ * on up to n_threads host threads (the seed partitions galvatron_base computes for every
+ * (batch, degree) cell of a batch window, planner.py:250-253).  out_sizes: n_cells rows of
+ * max_stages int32, row i holds pp_degree[i] stage sizes. */
+int  gbmw_seed_partitions(const gbmw_layer *layers, int32_t n_layers, const gbmw_env *env, int64_t n_devices,
+                          int32_t n_cells, const int64_t *pp_degree, const int64_t *micro_batch,
+                          const int32_t *n_micro, double budget, int32_t max_stages, int32_t n_threads,
+                          int32_t *out_sizes);
 /* CPython >= 3.12 built-in sum() of floats (Neumaier), as the reference folds sums. */
 double gbmw_py_sum(const double *x, int32_t n);
 const char *gbmw_planner_last_error(void);

@@ -11,6 +11,8 @@
 #include <cstring>
 #include <string>
 #include <vector>
+#include <thread>
+#include <atomic>
 
 #include "../../include/gbmw.h"
 #include "costmodel.cuh"
@@ -98,7 +100,9 @@ int partition_costs(const gbmw_layer *layers, const gbmw_strategy *strats, const
 
 // balance.py:62-77 balance_degrees -> alpha_t or alpha_m
 int balance_alpha(const StageCostOut *sc, int n, bool memory, double *alpha) {
-    std::vector<double> t(n), m(n);
+    thread_local std::vector<double> t, m;              // reused: called for every hill-climb move
+    t.resize(n);
+    m.resize(n);
     double tmax = 0.0, mmax = 0.0;
     for (int i = 0; i < n; ++i) {
         t[i] = sc[i].t;
@@ -230,7 +234,7 @@ int init_partition(const gbmw_layer *layers, int n_layers, const gbmw_strategy *
     int rc = tab.build(layers, n_layers, seeds, S, env, micro, n_micro);
     if (rc) return rc;
     std::vector<int32_t> best = greedy_split(w, S);
-    std::vector<StageCostOut> sc(S), cand_sc(S);
+    std::vector<StageCostOut> sc(S);
     tab.costs(best, sc.data());
     double best_score;
     if ((rc = balance_alpha(sc.data(), S, memory, &best_score))) return rc;
@@ -245,11 +249,14 @@ int init_partition(const gbmw_layer *layers, int n_layers, const gbmw_strategy *
             for (int dir = 0; dir < 2; ++dir) {
                 if (dir == 0 ? best[b] <= 1 : best[b + 1] <= 1) continue;
                 const int mid = starts[b] + best[b] + (dir == 0 ? -1 : 1);   // new boundary
-                cand_sc = sc;
-                cand_sc[b] = tab.stage(starts[b], mid, b + 1);
-                cand_sc[b + 1] = tab.stage(mid, starts[b + 1] + best[b + 1], b + 2);
+                const StageCostOut keep0 = sc[b], keep1 = sc[b + 1];            // re-cost the two stages in place
+                sc[b] = tab.stage(starts[b], mid, b + 1);
+                sc[b + 1] = tab.stage(mid, starts[b + 1] + best[b + 1], b + 2);
                 double s;
-                if ((rc = balance_alpha(cand_sc.data(), S, memory, &s))) return rc;
+                rc = balance_alpha(sc.data(), S, memory, &s);
+                sc[b] = keep0;
+                sc[b + 1] = keep1;
+                if (rc) return rc;
                 if (s > round_score + 1e-15) {
                     round_best = best;
                     if (dir == 0) { round_best[b] -= 1; round_best[b + 1] += 1; }
@@ -363,3 +370,44 @@ extern "C" int gbmw_seed_for(const gbmw_layer *layers, int32_t n_layers, const g
 }
 
 extern "C" double gbmw_py_sum(const double *x, int32_t n) { return py_sum(x, n); }
+
+// gbmw_seed_for for many (pp_degree, micro_batch, n_micro) cells of one model and cluster,
+// host threads over the cells (galvatron_base seeds every (batch, degree) cell of a batch
+// window this way, planner.py:250-253).  out_sizes: n_cells x max_stages, row i holds
+// pp_degree[i] stage sizes.  Returns the first failing cell's status (its message in
+// gbmw_planner_last_error of the calling thread).
+extern "C" int gbmw_seed_partitions(const gbmw_layer *layers, int32_t n_layers, const gbmw_env *env,
+                                    int64_t n_devices, int32_t n_cells, const int64_t *pp_degree,
+                                    const int64_t *micro_batch, const int32_t *n_micro, double budget,
+                                    int32_t max_stages, int32_t n_threads, int32_t *out_sizes) {
+    if (!layers || !env || !pp_degree || !micro_batch || !n_micro || !out_sizes || n_cells < 0 || max_stages < 1)
+        return perr(GBMW_EINVAL, "bad arguments");
+    for (int i = 0; i < n_cells; ++i)
+        if (pp_degree[i] < 1 || pp_degree[i] > max_stages) return perr(GBMW_EINVAL, "pp_degree out of range");
+    std::atomic<int> next{0}, first_bad{n_cells};
+    std::vector<int> codes(n_cells, GBMW_OK);
+    std::vector<std::string> msgs(n_cells);
+    auto work = [&]() {
+        while (true) {
+            const int i = next.fetch_add(1);
+            if (i >= n_cells) return;
+            gbmw_strategy seed;
+            const int rc = gbmw_seed_for(layers, n_layers, env, n_devices, pp_degree[i], micro_batch[i], n_micro[i],
+                                         budget, &seed, out_sizes + (size_t)i * max_stages);
+            if (rc) {
+                codes[i] = rc;
+                msgs[i] = g_perr;
+                int cur = first_bad.load();
+                while (i < cur && !first_bad.compare_exchange_weak(cur, i)) {}
+            }
+        }
+    };
+    const int nt = std::max(1, std::min<int>(n_threads, n_cells));
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nt; ++t) pool.emplace_back(work);
+    work();
+    for (auto &th : pool) th.join();
+    const int bad = first_bad.load();
+    if (bad < n_cells) return perr(codes[bad], msgs[bad]);
+    return GBMW_OK;
+}

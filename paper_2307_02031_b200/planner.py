@@ -27,6 +27,7 @@ from .balance import (
     bi_objective_optimize,
     init_partition_memory_balanced,
     partition_layers,
+    seed_partitions,
 )
 from .costs import EvalContext, StageCost, layer_memory, pipeline_cost, stage_cost
 from .dpsearch import StageProblem, dp_search_batch
@@ -300,13 +301,11 @@ def _base_cells_window(model, ctx, batches, opts):
     the seed partitions of all (batch, degree) pairs are computed concurrently."""
     cluster = ctx.cluster
     pairs = [(b, p) for b in batches for p in candidate_pp_degrees(cluster.n_devices) if p <= model.num_layers]
-
-    def seed(bp):
-        b, p = bp
+    cells = []
+    for b, p in pairs:
         m = init_microbatch_num(b, p, opts.microbatch_cap_factor, opts.min_micro_size)
-        return _seed_and_partition(model, ctx, cluster.n_devices, p, b // m, m)[1]
-
-    parts = list(_executor().map(seed, pairs)) if len(pairs) > 1 else [seed(bp) for bp in pairs]
+        cells.append((p, b // m, m))
+    parts = seed_partitions(model, ctx, cluster.n_devices, cells)     # one native call, host threads
     out = {b: [] for b in batches}
     for (b, p), part in zip(pairs, parts):
         out[b].append((p, part, (cluster.mem_budget_bytes, partition_layers(model, part), cluster.n_devices, b, p)))
@@ -317,17 +316,33 @@ def _base_cells(model, ctx, batch, opts):
     return _base_cells_window(model, ctx, [batch], opts)[0]
 
 
+_window_pool = None
+
+
+def _window_executor():
+    """One host thread that prepares the next batch window (its seed partitions) while the
+    current window's searches run on the device (the ctypes calls release the GIL)."""
+    global _window_pool
+    if _window_pool is None:
+        from concurrent.futures import ThreadPoolExecutor
+        _window_pool = ThreadPoolExecutor(max_workers=1)
+    return _window_pool
+
+
 def galvatron_base(model, cluster, profile, opts: PlannerOptions = PlannerOptions()) -> Plan:
     """Algorithm 1: raise the batch until no pipeline degree fits (planner.py:231-277)."""
     ctx = EvalContext(model=model, cluster=cluster, profile=profile)
     best: Plan | None = None
     batches = list(range(opts.batch_step, opts.max_batch + 1, opts.batch_step)) if opts.batch_step > 0 else []
     window = max(1, opts.batch_window)
-    pos = 0
-    while pos < len(batches):
-        chunk = batches[pos:pos + window]
-        pos += len(chunk)
-        per_batch = _base_cells_window(model, ctx, chunk, opts)
+    chunks = [batches[i:i + window] for i in range(0, len(batches), window)]
+    nxt = _window_executor().submit(_base_cells_window, model, ctx, chunks[0], opts) if chunks else None
+    for ci, chunk in enumerate(chunks):
+        per_batch = nxt.result()
+        # speculative: the next window's seeds overlap this window's device pass (unused if
+        # the stop rule ends the sweep here)
+        nxt = _window_executor().submit(_base_cells_window, model, ctx, chunks[ci + 1], opts) \
+            if ci + 1 < len(chunks) else None
         flat = [c[2] for cells in per_batch for c in cells]
         outcomes = galvatron_search_batch(flat, ctx, opts)
         k = 0
