@@ -116,6 +116,70 @@ int balance_alpha(const StageCostOut *sc, int n, bool memory, double *alpha) {
     return GBMW_OK;
 }
 
+// balance_alpha of a partition that differs from the current one only in stages b, b+1
+// (a hill-climb move), with the current partition's Neumaier prefix states and prefix /
+// suffix maxima cached: the sums resume at b with exactly py_sum's operations, so the
+// result is bit-identical to balance_alpha on the whole moved partition.
+struct AlphaCache {
+    int n = 0;
+    std::vector<double> ft, ct, fm, cm, pmt, pmm, smt, smm;   // state after element i; max of [0, i] / [i, n)
+
+    void build(const StageCostOut *sc, int n_) {
+        n = n_;
+        ft.resize(n); ct.resize(n); fm.resize(n); cm.resize(n);
+        pmt.resize(n); pmm.resize(n); smt.resize(n + 1); smm.resize(n + 1);
+        double f1 = sc[0].t, c1 = 0.0, f2 = sc[0].peak, c2 = 0.0;
+        ft[0] = f1; ct[0] = c1; fm[0] = f2; cm[0] = c2;
+        for (int i = 1; i < n; ++i) {
+            step(f1, c1, sc[i].t);
+            step(f2, c2, sc[i].peak);
+            ft[i] = f1; ct[i] = c1; fm[i] = f2; cm[i] = c2;
+        }
+        pmt[0] = sc[0].t; pmm[0] = sc[0].peak;
+        for (int i = 1; i < n; ++i) {
+            pmt[i] = sc[i].t > pmt[i - 1] ? sc[i].t : pmt[i - 1];
+            pmm[i] = sc[i].peak > pmm[i - 1] ? sc[i].peak : pmm[i - 1];
+        }
+        smt[n] = -INFINITY; smm[n] = -INFINITY;
+        for (int i = n - 1; i >= 0; --i) {
+            smt[i] = sc[i].t > smt[i + 1] ? sc[i].t : smt[i + 1];
+            smm[i] = sc[i].peak > smm[i + 1] ? sc[i].peak : smm[i + 1];
+        }
+    }
+
+    static void step(double &f, double &c, double x) {           // py_sum's loop body
+        const double t = f + x;
+        if (std::fabs(f) >= std::fabs(x)) c += (f - t) + x;
+        else c += (x - t) + f;
+        f = t;
+    }
+    static double finish(double f, double c) { return (c != 0.0 && std::isfinite(c)) ? f + c : f; }
+
+    // sc: the current partition's costs; n0, n1: the new costs of stages b, b + 1
+    int move_alpha(const StageCostOut *sc, int b, const StageCostOut &n0, const StageCostOut &n1, bool memory,
+                   double *alpha) const {
+        double f1, c1, f2, c2;
+        if (b == 0) { f1 = n0.t; c1 = 0.0; f2 = n0.peak; c2 = 0.0; }
+        else {
+            f1 = ft[b - 1]; c1 = ct[b - 1]; f2 = fm[b - 1]; c2 = cm[b - 1];
+            step(f1, c1, n0.t); step(f2, c2, n0.peak);
+        }
+        step(f1, c1, n1.t); step(f2, c2, n1.peak);
+        for (int i = b + 2; i < n; ++i) { step(f1, c1, sc[i].t); step(f2, c2, sc[i].peak); }
+        const double tt = finish(f1, c1), tm = finish(f2, c2);
+        double tmax = b > 0 ? pmt[b - 1] : n0.t, mmax = b > 0 ? pmm[b - 1] : n0.peak;
+        if (n0.t > tmax) tmax = n0.t;
+        if (n0.peak > mmax) mmax = n0.peak;
+        if (n1.t > tmax) tmax = n1.t;
+        if (n1.peak > mmax) mmax = n1.peak;
+        if (smt[b + 2] > tmax) tmax = smt[b + 2];
+        if (smm[b + 2] > mmax) mmax = smm[b + 2];
+        if (tt <= 0 || tm <= 0) return perr(GBMW_EINVAL, "stage totals must be positive to define balance degrees");
+        *alpha = memory ? 1.0 - mmax / tm : 1.0 - tmax / tt;
+        return GBMW_OK;
+    }
+};
+
 // balance.py:122-139 _greedy_split
 std::vector<int32_t> greedy_split(const std::vector<double> &w, int S) {
     const int n = (int)w.size();
@@ -240,23 +304,21 @@ int init_partition(const gbmw_layer *layers, int n_layers, const gbmw_strategy *
     if ((rc = balance_alpha(sc.data(), S, memory, &best_score))) return rc;
     // balance.py:160-177 _hill_climb, max_rounds = 2 L; neighbour order of _neighbor_moves
     std::vector<int32_t> starts(S);
+    AlphaCache ac;
     for (int round = 0; round < 2 * n_layers; ++round) {
         bool found = false;
         std::vector<int32_t> round_best;
         double round_score = best_score;
         for (int s = 0, a = 0; s < S; ++s) { starts[s] = a; a += best[s]; }
+        ac.build(sc.data(), S);
         for (int b = 0; b + 1 < S; ++b) {
             for (int dir = 0; dir < 2; ++dir) {
                 if (dir == 0 ? best[b] <= 1 : best[b + 1] <= 1) continue;
                 const int mid = starts[b] + best[b] + (dir == 0 ? -1 : 1);   // new boundary
-                const StageCostOut keep0 = sc[b], keep1 = sc[b + 1];            // re-cost the two stages in place
-                sc[b] = tab.stage(starts[b], mid, b + 1);
-                sc[b + 1] = tab.stage(mid, starts[b + 1] + best[b + 1], b + 2);
+                const StageCostOut n0 = tab.stage(starts[b], mid, b + 1);       // the two re-costed stages
+                const StageCostOut n1 = tab.stage(mid, starts[b + 1] + best[b + 1], b + 2);
                 double s;
-                rc = balance_alpha(sc.data(), S, memory, &s);
-                sc[b] = keep0;
-                sc[b + 1] = keep1;
-                if (rc) return rc;
+                if ((rc = ac.move_alpha(sc.data(), b, n0, n1, memory, &s))) return rc;
                 if (s > round_score + 1e-15) {
                     round_best = best;
                     if (dir == 0) { round_best[b] -= 1; round_best[b + 1] += 1; }
