@@ -74,10 +74,20 @@ def balance_degrees(stage_costs: Sequence[StageCost]) -> BalanceReport:
                          stage_times=times, stage_mems=mems)
 
 
+class StageLayers(list):
+    """The per-stage layer lists of a partition of ``model.layers`` (a plain list of
+    lists), remembering the slices so the batched search needs no identity check."""
+    __slots__ = ("model", "ranges")
+
+
 def partition_layers(model, partition: PipelinePartition) -> list[list]:
     if partition.num_layers != model.num_layers:
         raise ValueError(f"partition covers {partition.num_layers} layers, model has {model.num_layers}")
-    return [list(model.layers[a:b]) for a, b in partition.boundaries()]
+    bounds = partition.boundaries()
+    out = StageLayers(list(model.layers[a:b]) for a, b in bounds)
+    out.model = model
+    out.ranges = [(a, b - a) for a, b in bounds]
+    return out
 
 
 def seed_strategy(n_devices: int, pp_degree: int, use_sdp: bool = False) -> ParallelStrategy:

@@ -73,6 +73,20 @@ def _check(p: StageProblem):
     return n_buckets, strats, None
 
 
+_strat_arrays: dict = {}
+
+
+def _strategies_array_cached(strategies, strat_list):
+    """Strategy records of an immutable strategy set, built once per set object."""
+    hit = _strat_arrays.get(id(strategies))
+    if hit is None or hit[0] is not strategies:
+        if len(_strat_arrays) > 256:
+            _strat_arrays.clear()
+        hit = (strategies, _native.strategies_array(strat_list))
+        _strat_arrays[id(strategies)] = hit
+    return hit[1]
+
+
 class _Marshal:
     """Deduplicating builder of the flat layer / strategy / env tables of a batch."""
 
@@ -99,7 +113,7 @@ class _Marshal:
         hit = self.strat_ranges.get(key)
         if hit is None or hit[1] is not strategies:
             hit = (len(self.strats), strategies)
-            self.strats.append(_native.strategies_array(strat_list))
+            self.strats.append(_strategies_array_cached(strategies, strat_list))
             self.strat_ranges[key] = hit
         return hit[0]
 

@@ -104,6 +104,12 @@ def _sset(n_devices: int, pp_degree: int):
 
 def _stage_ranges(model, stages):
     """(start, length) of each stage if the stages are consecutive slices of model.layers."""
+    if getattr(stages, "model", None) is model and getattr(stages, "ranges", None) is not None:
+        # from partition_layers(model, ...), unmodified: the slices are known
+        ls = model.layers
+        if len(stages) == len(stages.ranges) and all(
+                len(st) == n and st[0] is ls[a] and st[-1] is ls[a + n - 1] for st, (a, n) in zip(stages, stages.ranges)):
+            return stages.ranges
     layers = model.layers
     index = _layer_index(model)
     out = []
