@@ -34,6 +34,37 @@ def test_partitions_match_reference():
             assert got == c[key], (c["model"], c["P"], key)
 
 
+def test_batched_seed_partitions_match_reference():
+    """gbmw_seed_partitions (one native call over host threads for many cells) gives the
+    reference's memory-balanced seed partitions, cell by cell and thread-count independent."""
+    by_model = {}
+    for c in load("partitions.json"):
+        by_model.setdefault((c["model"], c["budget"]), []).append(c)
+    for (name, budget), cases in by_model.items():
+        ctx = W.config(name, budget)
+        cells = [(c["P"], c["micro"], c["n_micro"]) for c in cases]
+        for threads in (1, 7):
+            parts = B.seed_partitions(ctx.model, ctx, ctx.cluster.n_devices, cells, n_threads=threads)
+            assert [list(p.stage_sizes) for p in parts] == [c["p_m"] for c in cases], (name, threads)
+
+
+def test_batched_seed_partitions_equal_single_cells():
+    """Across every pipeline degree and many batch sizes of the benchmark models."""
+    from paper_2307_02031_b200.planner import init_microbatch_num
+    from paper_2307_02031_b200.strategies import candidate_pp_degrees
+    for name in ("bert", "t5", "swin", "vit", "gpt"):
+        ctx = W.config(name)
+        cells = []
+        for b in (8, 24, 64, 200, 512):
+            for p in candidate_pp_degrees(ctx.cluster.n_devices):
+                if p <= ctx.model.num_layers:
+                    m = init_microbatch_num(b, p)
+                    cells.append((p, b // m, m))
+        parts = B.seed_partitions(ctx.model, ctx, ctx.cluster.n_devices, cells)
+        single = [B._seed_and_partition(ctx.model, ctx, ctx.cluster.n_devices, *c)[1] for c in cells]
+        assert parts == single, name
+
+
 def test_py_sum_matches_cpython():
     """gbmw_py_sum == CPython's built-in sum() (Neumaier since 3.12) bit for bit."""
     rng = random.Random(5)
