@@ -568,6 +568,8 @@ __global__ void __launch_bounds__(kStepThreads, GROUP <= 1 ? 3 : 1)
     pdl_wait();
     tl_mark(a.k2_tl, tl_id, false);
     __shared__ TileCtx s_t[kK2Warps];
+    __shared__ uint16_t s_erow[kK2Warps][kWarpRows];
+    __shared__ uint16_t s_echg[kK2Warps][kWarpRows];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     TileCtx &t = s_t[warp];
     const int64_t total = (int64_t)*(volatile unsigned long long *)(ctr + 1);
@@ -597,7 +599,17 @@ __global__ void __launch_bounds__(kStepThreads, GROUP <= 1 ? 3 : 1)
         last = __shfl_sync(0xffffffffu, last, 0);
         if (last) {
             __threadfence();
-#define GBMW_K2_FIN(KT, G) finish_tile<KT, G, true>(a, t, u, lane)
+            // the tile's entries into shared memory with coalesced loads (all independent),
+            // then the finish reads them there instead of chasing them in global memory
+            const int n = t.n_ent;
+            for (int j = lane; j < n; j += 32) {
+                s_erow[warp][j] = __ldcg(t.erow + j);
+                s_echg[warp][j] = __ldcg(t.echg + j);
+            }
+            __syncwarp();
+            if (lane == 0) { t.erow = s_erow[warp]; t.echg = s_echg[warp]; t.goff = nullptr; }
+            __syncwarp();
+#define GBMW_K2_FIN(KT, G) finish_tile<KT, G, false>(a, t, u, lane)
             GBMW_K2_DISPATCH(GBMW_K2_FIN)
 #undef GBMW_K2_FIN
         }
