@@ -24,7 +24,7 @@ constexpr int kMaxStrats = 512;      // smem staging of per-strategy constants
 constexpr int kStepThreads = 256;    // threads per K2 CTA
 constexpr int kStepRows = 2048;      // rows per K2 tile (64 groups of 32)
 constexpr int kK2SlotEntries = 1024; // entries of one 1024-row K2 tile (anchor + breakpoints)
-constexpr int kK2RoundsPerSlot = 33; // evaluation rounds of a tile with 1024 entries
+constexpr int kK2RoundsPerSlot = 40; // >= the most evaluation rounds of one tile (37, at 255 entries; static_assert in gbmw_step.cu)
 constexpr int kK2HeavyBytes = 256;   // HeavyTile record (tile context + group entry offsets)
 
 // change-bit words per class column of n_e rows (one spare word for 2-word window reads)

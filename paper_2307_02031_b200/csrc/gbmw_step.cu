@@ -291,10 +291,17 @@ __device__ __forceinline__ int classify_tile(const ChunkArgs &a, TileCtx &t, uin
 constexpr int kLightE = 8;
 constexpr int kDenseN = 256;
 __device__ __forceinline__ int round_entries(int n) { return n <= kLightE ? kLightE : (n < kDenseN ? 8 : 32); }
-__device__ __forceinline__ int tile_rounds(int n) {
-    const int E = round_entries(n);
-    return n <= E ? 1 : 1 + (n - 2) / (E - 1);
+__host__ __device__ constexpr int round_entries_c(int n) { return n <= kLightE ? kLightE : (n < kDenseN ? 8 : 32); }
+__host__ __device__ constexpr int tile_rounds_c(int n) {
+    return n <= round_entries_c(n) ? 1 : 1 + (n - 2) / (round_entries_c(n) - 1);
 }
+__device__ __forceinline__ int tile_rounds(int n) { return tile_rounds_c(n); }
+constexpr int max_tile_rounds() {
+    int m = 0;
+    for (int n = 1; n <= kWarpRows; ++n) m = tile_rounds_c(n) > m ? tile_rounds_c(n) : m;
+    return m;
+}
+static_assert(max_tile_rounds() <= kK2RoundsPerSlot, "round list capacity per tile slot");
 
 // Phase B, one round of one tile by one warp: evaluate its entries, compare each with the
 // previous entry (unchanged columns keep change bit 0), store (t, f, argmin) of the
