@@ -490,7 +490,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 // debug timeline: slot 2 * id = earliest CTA start, 2 * id + 1 = latest CTA end
 __device__ __forceinline__ void tl_mark(unsigned long long *tl, int id, bool end) {
-    if (!tl || threadIdx.x != 0) return;
+    if (!tl || threadIdx.x != 0 || id >= 4096) return;          // debug buffer: 4096 launches
     if (end) atomicMax(tl + 2 * id + 1, gtimer()); else atomicMin(tl + 2 * id, gtimer());
 }
 
