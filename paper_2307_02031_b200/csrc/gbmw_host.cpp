@@ -1047,8 +1047,9 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
                     std::vector<unsigned long long> ctrs((size_t)(cc.Umax + 1) * kNumGroups * 3);
                     cudaMemcpy(ctrs.data(), al.counters, ctrs.size() * 8, cudaMemcpyDeviceToHost);
                     unsigned long long t0 = ~0ull;
-                    for (size_t l = 0; l < 2 * cc.slists.size(); ++l) t0 = std::min(t0, tl[2 * l]);
-                    for (size_t l = 0; l < cc.slists.size(); ++l)
+                    const size_t nl = std::min<size_t>(cc.slists.size(), 2048);
+                    for (size_t l = 0; l < 2 * nl; ++l) t0 = std::min(t0, tl[2 * l]);
+                    for (size_t l = 0; l < nl; ++l)
                         fprintf(stderr, "TL u=%d g=%d a=[%.1f, %.1f] b=[%.1f, %.1f] us rounds=%llu\n", cc.slists[l].u,
                                 cc.slist_group[l], (tl[4 * l] - t0) / 1e3, (tl[4 * l + 1] - t0) / 1e3,
                                 (tl[4 * l + 2] - t0) / 1e3, (tl[4 * l + 3] - t0) / 1e3,
