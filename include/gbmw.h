@@ -248,6 +248,11 @@ int  gbmw_seed_partitions(const gbmw_layer *layers, int32_t n_layers, const gbmw
                           int32_t n_cells, const int64_t *pp_degree, const int64_t *micro_batch,
                           const int32_t *n_micro, double budget, int32_t max_stages, int32_t n_threads,
                           int32_t *out_sizes);
+/* The same on the device of ctx: one warp per cell. */
+int  gbmw_seed_partitions_device(gbmw_ctx *ctx, const gbmw_layer *layers, int32_t n_layers, const gbmw_env *env,
+                                 int64_t n_devices, int32_t n_cells, const int64_t *pp_degree,
+                                 const int64_t *micro_batch, const int32_t *n_micro, double budget,
+                                 int32_t max_stages, int32_t *out_sizes);
 /* CPython >= 3.12 built-in sum() of floats (Neumaier), as the reference folds sums. */
 double gbmw_py_sum(const double *x, int32_t n);
 const char *gbmw_planner_last_error(void);

@@ -182,10 +182,12 @@ def _seed_and_partition(model, ctx, n_devices, pp_degree, micro_batch, n_micro):
     return [s] * model.num_layers, PipelinePartition(tuple(int(x) for x in sizes))
 
 
-def seed_partitions(model, ctx, n_devices, cells, n_threads: int | None = None) -> list[PipelinePartition]:
+def seed_partitions(model, ctx, n_devices, cells, n_threads: int | None = None,
+                    device=None) -> list[PipelinePartition]:
     """The memory-balanced partition of the ``_seed_for`` strategy (balance.py:471-488,
-    planner.py:250-253) for many ``(pp_degree, micro_batch, n_micro)`` cells at once:
-    one native call, host threads over the cells (gbmw_seed_partitions)."""
+    planner.py:250-253) for many ``(pp_degree, micro_batch, n_micro)`` cells at once: one
+    native call, on the GPU of ``device`` (a ``_native.Context``: a warp per cell,
+    gbmw_seed_partitions_device) or on host threads (gbmw_seed_partitions)."""
     import os
     n = len(cells)
     if n == 0:
@@ -196,13 +198,22 @@ def seed_partitions(model, ctx, n_devices, cells, n_threads: int | None = None) 
     width = int(pp.max())
     sizes = np.zeros((n, width), dtype=np.int32)
     layers = _layers(model, ctx.profile)
-    threads = n_threads or max(1, min(32, len(os.sched_getaffinity(0))))
-    rc = _native.lib().gbmw_seed_partitions(_native.ptr(layers), len(layers), _native.ptr(_env(ctx)), int(n_devices),
-                                            n, _native.ptr(pp), _native.ptr(micro), _native.ptr(nm),
-                                            float(ctx.cluster.mem_budget_bytes), width, int(threads),
-                                            _native.ptr(sizes))
-    if rc != _native.OK:
-        _planner_error(rc)
+    env = _env(ctx)
+    budget = float(ctx.cluster.mem_budget_bytes)
+    if device is not None:
+        with device.lock:
+            rc = _native.lib().gbmw_seed_partitions_device(
+                device.handle, _native.ptr(layers), len(layers), _native.ptr(env), int(n_devices), n, _native.ptr(pp),
+                _native.ptr(micro), _native.ptr(nm), budget, width, _native.ptr(sizes))
+            if rc != _native.OK:
+                _native.raise_status(rc, device.error())
+    else:
+        threads = n_threads or max(1, min(32, len(os.sched_getaffinity(0))))
+        rc = _native.lib().gbmw_seed_partitions(_native.ptr(layers), len(layers), _native.ptr(env), int(n_devices),
+                                                n, _native.ptr(pp), _native.ptr(micro), _native.ptr(nm), budget,
+                                                width, int(threads), _native.ptr(sizes))
+        if rc != _native.OK:
+            _planner_error(rc)
     return [PipelinePartition(tuple(int(x) for x in sizes[i, :int(pp[i])])) for i in range(n)]
 
 

@@ -122,6 +122,8 @@ struct gbmw_ctx {
     // grow-only pinned staging buffer for uploads
     void *pinned = nullptr;
     std::vector<char> blob;                  // descriptor staging, reused across batches (no page faults)
+    void *seed_buf = nullptr;                // gbmw_seed_partitions_device buffers (grow-only)
+    size_t seed_cap = 0;
     size_t pinned_cap = 0;
     gbmw_timing last{};
     std::string err;
@@ -350,6 +352,7 @@ extern "C" int gbmw_ctx_destroy(gbmw_ctx *ctx) {
         if (ctx->join[g]) cudaEventDestroy(ctx->join[g]);
     }
     if (ctx->fork) cudaEventDestroy(ctx->fork);
+    if (ctx->seed_buf) cudaFree(ctx->seed_buf);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
     return GBMW_OK;
@@ -1141,6 +1144,69 @@ extern "C" int gbmw_batch_timing(const gbmw_batch *b, gbmw_timing *out) {
 extern "C" int gbmw_ctx_last_timing(const gbmw_ctx *ctx, gbmw_timing *out) {
     if (!ctx || !out) return set_err(nullptr, GBMW_EINVAL, "null ctx/out");
     *out = ctx->last;
+    return GBMW_OK;
+}
+
+// gbmw_seed_partitions on the device (csrc/gbmw_seed.cu): one warp per
+// cell, the hill climb's moves across the lanes.  Same contract as the host function.
+extern "C" int gbmw_seed_partitions_device(gbmw_ctx *ctx, const gbmw_layer *layers, int32_t n_layers,
+                                           const gbmw_env *env, int64_t n_devices, int32_t n_cells,
+                                           const int64_t *pp_degree, const int64_t *micro_batch,
+                                           const int32_t *n_micro, double budget, int32_t max_stages,
+                                           int32_t *out_sizes) {
+    if (!ctx || !layers || !env || !pp_degree || !micro_batch || !n_micro || !out_sizes || n_cells < 0 ||
+        max_stages < 1 || n_layers < 1)
+        return set_err(ctx ? &ctx->err : nullptr, GBMW_EINVAL, "bad arguments");
+    if (n_cells == 0) return GBMW_OK;
+    cudaSetDevice(ctx->device);
+    cudaStream_t st = ctx->stream;
+    const size_t b_layers = (size_t)n_layers * sizeof(gbmw_layer), b_env = sizeof(gbmw_env);
+    const size_t b_cells = (size_t)n_cells * (8 + 8 + 4), b_out = (size_t)n_cells * ((size_t)max_stages + 1) * 4;
+    const size_t b_scr = (size_t)n_cells * n_layers * 8;
+    size_t o = 0;
+    const size_t o_layers = o; o = align_up(o + b_layers);
+    const size_t o_env = o; o = align_up(o + b_env);
+    const size_t o_pp = o; o = align_up(o + (size_t)n_cells * 8);
+    const size_t o_mb = o; o = align_up(o + (size_t)n_cells * 8);
+    const size_t o_nm = o; o = align_up(o + (size_t)n_cells * 4);
+    const size_t up = o;
+    const size_t o_out = o; o = align_up(o + b_out);
+    const size_t o_scr = o; o = align_up(o + b_scr);
+    (void)b_cells;
+    if (ctx->seed_cap < o) {
+        if (ctx->seed_buf) cudaFree(ctx->seed_buf);
+        ctx->seed_buf = nullptr;
+        ctx->seed_cap = 0;
+        if (cudaMalloc(&ctx->seed_buf, o + o / 4) != cudaSuccess)
+            return set_err(&ctx->err, GBMW_ENOMEM, "cudaMalloc(seed partitions)");
+        ctx->seed_cap = o + o / 4;
+    }
+    std::vector<char> host(up);
+    std::memcpy(host.data() + o_layers, layers, b_layers);
+    std::memcpy(host.data() + o_env, env, b_env);
+    std::memcpy(host.data() + o_pp, pp_degree, (size_t)n_cells * 8);
+    std::memcpy(host.data() + o_mb, micro_batch, (size_t)n_cells * 8);
+    std::memcpy(host.data() + o_nm, n_micro, (size_t)n_cells * 4);
+    char *dev = (char *)ctx->seed_buf;
+    cudaError_t ce = cudaMemcpyAsync(dev, host.data(), up, cudaMemcpyHostToDevice, st);
+    int rc = (ce == cudaSuccess)
+                 ? launch_seed_partitions((const gbmw_layer *)(dev + o_layers), n_layers, (const gbmw_env *)(dev + o_env),
+                                          n_devices, n_cells, (const int64_t *)(dev + o_pp),
+                                          (const int64_t *)(dev + o_mb), (const int32_t *)(dev + o_nm), budget,
+                                          max_stages, (double *)(dev + o_scr), (int32_t *)(dev + o_out),
+                                          (int32_t *)(dev + o_out) + (size_t)n_cells * max_stages, st)
+                 : (int)ce;
+    if (rc) return cuda_fail(ctx, rc, "seed partitions launch");
+    std::vector<int32_t> out((size_t)n_cells * (max_stages + 1));
+    ce = cudaMemcpyAsync(out.data(), dev + o_out, out.size() * 4, cudaMemcpyDeviceToHost, st);
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
+    if (ce != cudaSuccess) return cuda_fail(ctx, (int)ce, "seed partitions");
+    const int32_t *status = out.data() + (size_t)n_cells * max_stages;
+    for (int i = 0; i < n_cells; ++i)
+        if (status[i])
+            return set_err(&ctx->err, status[i], "seed partition of cell " + std::to_string(i) + " failed (status " +
+                                                     std::to_string(status[i]) + ")");
+    std::memcpy(out_sizes, out.data(), (size_t)n_cells * max_stages * 4);
     return GBMW_OK;
 }
 

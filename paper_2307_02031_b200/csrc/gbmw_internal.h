@@ -219,5 +219,8 @@ int launch_sweep(const ChunkArgs &a, void *stream);
 int launch_approx_step(const ChunkArgs &a, int u, int64_t tile_base, int64_t n_tiles, unsigned long long *counter,
                        void *stream);
 int launch_finalize(const ChunkArgs &a, void *stream);
+int launch_seed_partitions(const gbmw_layer *layers, int32_t L, const gbmw_env *env, int64_t n_devices, int32_t n_cells,
+                           const int64_t *pp, const int64_t *micro, const int32_t *n_micro, double budget,
+                           int32_t max_stages, double *scratch, int32_t *out_sizes, int32_t *out_status, void *stream);
 
 }  // namespace gbmw

@@ -311,7 +311,10 @@ def _base_cells_window(model, ctx, batches, opts):
     for b, p in pairs:
         m = init_microbatch_num(b, p, opts.microbatch_cap_factor, opts.min_micro_size)
         cells.append((p, b // m, m))
-    parts = seed_partitions(model, ctx, cluster.n_devices, cells)     # one native call, host threads
+    # one native call over host threads: the hill climb is a chain of dependent fp64 folds per
+    # cell, faster on host cores than on a warp (gbmw_seed_partitions_device: bit-identical,
+    # ~3x slower on the GPT-3-96 windows)
+    parts = seed_partitions(model, ctx, cluster.n_devices, cells)
     out = {b: [] for b in batches}
     for (b, p), part in zip(pairs, parts):
         out[b].append((p, part, (cluster.mem_budget_bytes, partition_layers(model, part), cluster.n_devices, b, p)))
