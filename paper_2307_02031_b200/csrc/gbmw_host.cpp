@@ -690,9 +690,11 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
                 for (int u = 0; u < b->hp[c.probs[x]].U && u <= c.Umax; ++u) c.n_active[g][u]++;
         }
         td[2] += now_ms() - tq; tq = now_ms();
-        std::vector<int32_t> stepmap(stepp.back());
+        // K2 tile -> problem map: only the collapsed-DP step (K2c) still walks 2048-row tiles
+        std::vector<int32_t> stepmap(c.n_approx > 0 ? stepp.back() : 0);
         for (int x = 0; x < np; ++x) {
-            for (int64_t t = stepp[x]; t < stepp[x + 1]; ++t) stepmap[t] = x;
+            if (c.n_approx > 0)
+                for (int64_t t = stepp[x]; t < stepp[x + 1]; ++t) stepmap[t] = x;
             // every row of frontier / collapsed-DP problems is swept (K3r)
             if (b->problems[c.probs[x]].flags & (GBMW_FRONTIER | GBMW_APPROX))
                 for (int t = 0; t < dps[x].n_sweep_tiles; ++t) aux.push_back(make_int2(x, t));
