@@ -45,3 +45,17 @@ def test_sweep10k_sample_vs_oracle(gpu):
         assert res["feasible"][i] == ores["feasible"][a], int(i)
         n = int(P["n_layers"][i])
         assert np.array_equal(plans[offs[i]:offs[i] + n], oplans[ooffs[a]:ooffs[a] + n]), int(i)
+
+
+@pytest.mark.parametrize("gran_mib", [64, 16])
+def test_sweep10k_coarse_all_vs_oracle(gpu, gran_mib):
+    """Every one of the 10,000 searches at coarser buckets, bit-exact against the oracle."""
+    L, S, E, P, T = W.sweep_arrays(W.sweep_cells(10_000), granularity_bytes=gran_mib << 20)
+    rc, msg, res, plans, _ = run_native_batch(L, S, E, P, None)
+    assert rc == 0, msg
+    ores, oplans, _, _ = O.search_many(L, S, E, P)
+    for f in ("time_s", "e_fwd", "stage_time", "stage_ns", "stage_peak"):
+        assert np.array_equal(res[f].view(np.int64), ores[f].view(np.int64)), f
+    assert np.array_equal(res["feasible"], ores["feasible"])
+    n = int(np.clip(P["n_layers"], 0, None).sum())
+    assert np.array_equal(plans[:n], oplans[:n])
