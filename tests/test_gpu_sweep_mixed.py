@@ -47,7 +47,7 @@ def test_sweep10k_sample_vs_oracle(gpu):
         assert np.array_equal(plans[offs[i]:offs[i] + n], oplans[ooffs[a]:ooffs[a] + n]), int(i)
 
 
-@pytest.mark.parametrize("gran_mib", [64, 16])
+@pytest.mark.parametrize("gran_mib", [64, 16, 4])
 def test_sweep10k_coarse_all_vs_oracle(gpu, gran_mib):
     """Every one of the 10,000 searches at coarser buckets, bit-exact against the oracle."""
     L, S, E, P, T = W.sweep_arrays(W.sweep_cells(10_000), granularity_bytes=gran_mib << 20)
