@@ -977,6 +977,11 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
             const int g = c.slist_group[s];
             const int64_t ub = (s + 1 < c.slists.size() ? c.slists[s + 1].base : c.n_items) - sl.base;   // item bound
             int2 *rounds = a.k2_rounds + 2 * c.step_prefix[c.group_lo[g]] * kK2RoundsPerSlot;
+            if (sl.u == 1) {                             // first step: segments of the first unit's weights
+                if ((rc = launch_dp_first(a, sl.lo, sl.n, gs[g]))) return cuda_fail(ctx, rc, "K2 first launch");
+                c.launches += 1;
+                continue;
+            }
             if ((rc = launch_dp_step(a, g / kBands, sl.u, a.step_items + sl.base, a.step_count + s, ub,
                                      a.counters + ((size_t)sl.u * kNumGroups + g) * 3, rounds, (int)s, gs[g])))
                 return cuda_fail(ctx, rc, "K2 launch");

@@ -215,6 +215,7 @@ int launch_cost_tables(const ChunkArgs &a, int64_t n_cells, int64_t n_r, void *s
 int launch_step_lists(const ChunkArgs &a, void *stream);
 int launch_dp_step(const ChunkArgs &a, int group, int u, const int4 *items, const int64_t *count, int64_t max_items,
                    unsigned long long *counters3, int2 *rounds, int tl_id, void *stream);
+int launch_dp_first(const ChunkArgs &a, int p_lo, int p_n, void *stream);
 int launch_sweep(const ChunkArgs &a, void *stream);
 int launch_approx_step(const ChunkArgs &a, int u, int64_t tile_base, int64_t n_tiles, unsigned long long *counter,
                        void *stream);

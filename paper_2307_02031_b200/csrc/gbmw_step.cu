@@ -632,6 +632,138 @@ __global__ void __launch_bounds__(kStepThreads, GROUP <= 1 ? 3 : 1)
 }
 #undef GBMW_K2_DISPATCH
 
+// K2 for the first layer step (u = 1), one CTA per problem.  T_0[e, i] = time_c[0, i] for
+// e >= w_0i (dpsearch.py:255-259), so B_1 is piecewise constant with breakpoints only at the
+// distinct first-unit weights: B_1 is evaluated once per segment (the same lexmin as every
+// other step, T1 tie-break), stored at the segment starts where some column changes, and
+// the per-group outputs (change bits, summaries, row map) are written directly — no tiles,
+// no anchors.
+constexpr int kFirstThreads = 256;
+constexpr int kFirstMaxSeg = kMaxStrats + 1;
+
+__global__ void __launch_bounds__(kFirstThreads) k_dp_first(ChunkArgs a, int p_lo, int p_n) {
+    __shared__ int s_start[kFirstMaxSeg];                // segment start rows, ascending
+    __shared__ uint32_t s_chg[kFirstMaxSeg];             // bit k: column k changes at the start
+    __shared__ int s_stored[kFirstMaxSeg];               // stored rows, ascending
+    __shared__ double s_t[kFirstMaxSeg], s_f[kFirstMaxSeg];
+    __shared__ int s_key[kFirstMaxSeg];
+    __shared__ int s_m, s_ns;
+    const int q = p_lo + (int)blockIdx.x;
+    if ((int)blockIdx.x >= p_n) return;
+    const DevProblem &p = a.probs[q];
+    const int u = 1;
+    const int lo = a.unit_lo[p.ustate_off + u], hi = a.unit_hi[p.ustate_off + u];
+    if (hi < lo) return;
+    const int S = a.nuniq[p.ustate_off + 0], K = p.K;
+    const Cell *cell = a.ucell + p.cell_off;             // distinct sources of unit 0
+    const int32_t *idx = a.uniq + p.cell_off;
+    const double *R = a.rcls + p.r_off + (int64_t)u * K * K;
+    const int n_e = (int)(p.n_b + 1);
+    const int tid = threadIdx.x;
+    // segment starts: the distinct weights in [lo, hi] (lo is the smallest weight), ascending
+    __shared__ unsigned char s_first[kMaxStrats];       // source n holds the first occurrence of its weight
+    for (int n = tid; n < S; n += blockDim.x) {
+        const int w = cell[n].w;
+        bool first = w >= lo && w <= hi;
+        for (int j = 0; j < n && first; ++j) if (cell[j].w == w) first = false;
+        s_first[n] = first ? 1 : 0;
+    }
+    __syncthreads();
+    for (int n = tid; n < S; n += blockDim.x) {
+        if (!s_first[n]) continue;
+        const int w = cell[n].w;
+        int pos = 0;
+        for (int j = 0; j < S; ++j) pos += (s_first[j] && cell[j].w < w) ? 1 : 0;
+        s_start[pos] = w;
+    }
+    if (tid == 0) {
+        int m = 0;
+        for (int n = 0; n < S; ++n) m += s_first[n];
+        s_m = m;
+    }
+    __syncthreads();
+    const int m = s_m;
+    for (int j = tid; j < m; j += blockDim.x) s_chg[j] = (j == 0) ? ((K >= 32) ? 0xffffffffu : ((1u << K) - 1u)) : 0u;
+    __syncthreads();
+    // per column: B_1 at every segment start, then the change bits against the previous segment
+    for (int k = 0; k < K; ++k) {
+        for (int j = tid; j < m; j += blockDim.x) {
+            const int e = s_start[j];
+            double bt = GBMW_STEP_INF, bf = GBMW_STEP_INF;
+            int bk = 0x7fffffff;
+            for (int n = 0; n < S; ++n) {                // ascending source order (T1)
+                const Cell c = cell[n];
+                if (c.w > e) continue;
+                const double cand = c.c + R[c.k * K + k];
+                if (lex3_less(cand, c.ef, 2 * n, bt, bf, bk)) { bt = cand; bf = c.ef; bk = 2 * n; }
+            }
+            s_t[j] = bt; s_f[j] = bf; s_key[j] = bk;
+        }
+        __syncthreads();
+        for (int j = tid + 1; j < m; j += blockDim.x)
+            if (!(s_t[j] == s_t[j - 1] && s_f[j] == s_f[j - 1] && s_key[j] == s_key[j - 1])) s_chg[j] |= 1u << k;
+        __syncthreads();
+    }
+    if (tid == 0) {
+        int ns = 0;
+        for (int j = 0; j < m; ++j) if (j == 0 || s_chg[j]) s_stored[ns++] = s_start[j];
+        s_ns = ns;
+    }
+    __syncthreads();
+    const int ns = s_ns;
+    // (t, f, argmin) of every column at the stored rows
+    TFCell *bout = a.TF[u & 1] + p.b_off;
+    uint16_t *pout = a.par + p.par_off + (int64_t)(u - 1) * K * n_e;
+    for (int k = 0; k < K; ++k) {
+        for (int j = tid; j < m; j += blockDim.x) {
+            if (!(j == 0 || s_chg[j])) continue;
+            const int e = s_start[j];
+            double bt = GBMW_STEP_INF, bf = GBMW_STEP_INF;
+            int bk = 0x7fffffff;
+            for (int n = 0; n < S; ++n) {
+                const Cell c = cell[n];
+                if (c.w > e) continue;
+                const double cand = c.c + R[c.k * K + k];
+                if (lex3_less(cand, c.ef, 2 * n, bt, bf, bk)) { bt = cand; bf = c.ef; bk = 2 * n; }
+            }
+            reinterpret_cast<double2 *>(bout)[(int64_t)k * n_e + e] = make_double2(bt, bf);
+            pout[(int64_t)k * n_e + e] = (uint16_t)idx[bk >> 1];
+        }
+    }
+    // per 32-row group of the live rows: change-bit words, row map; per tile: summaries
+    const int nw = (int)flag_words(n_e), nsw = (int)sum_words(n_e);
+    uint32_t *fout = a.chg[u & 1] + p.flag_off;
+    uint32_t *sout = fout + (int64_t)K * nw;
+    int2 *rmo = a.rmap + p.rmap_off;                     // unit u = 1: row map index 0
+    const int lane = tid & 31, warp = tid >> 5;
+    for (int tile = lo / kWarpRows + warp; tile <= hi / kWarpRows; tile += blockDim.x / 32) {
+        const int r0 = tile * kWarpRows + 32 * lane, r1 = r0 + 31;
+        const bool dead = r1 < lo || r0 > hi;
+        int j0 = 0, j1 = m;                              // first segment start >= r0
+        while (j0 < j1) { const int mid = (j0 + j1) >> 1; if (s_start[mid] < r0) j0 = mid + 1; else j1 = mid; }
+        int s0 = 0, s1 = ns;                             // first stored row >= r0
+        while (s0 < s1) { const int mid = (s0 + s1) >> 1; if (s_stored[mid] < r0) s0 = mid + 1; else s1 = mid; }
+        const int before = s0 > 0 ? s_stored[s0 - 1] : -1;
+        unsigned sbits = 0u;
+        for (int x = s0; x < ns && s_stored[x] <= r1; ++x) sbits |= 1u << (s_stored[x] - r0);
+        for (int k = 0; k < K; ++k) {
+            uint32_t wd = 0u;
+            for (int j = j0; j < m && s_start[j] <= r1; ++j) wd |= ((s_chg[j] >> k) & 1u) << (s_start[j] - r0);
+            if (!dead) fout[(int64_t)k * nw + (r0 >> 5)] = wd;
+            const unsigned sm = __ballot_sync(0xffffffffu, wd != 0u);
+            if (lane == 0) sout[(int64_t)k * nsw + tile] = sm;
+        }
+        if (!dead) rmo[r0 >> 5] = make_int2((int)sbits, before);
+    }
+    if (tid == 0) atomicAdd(a.computed_cells, (unsigned long long)m * (unsigned long long)K);
+}
+
+int launch_dp_first(const ChunkArgs &a, int p_lo, int p_n, void *stream) {
+    if (p_n <= 0) return 0;
+    k_dp_first<<<p_n, kFirstThreads, 0, (cudaStream_t)stream>>>(a, p_lo, p_n);
+    return (int)cudaGetLastError();
+}
+
 int launch_dp_step(const ChunkArgs &a, int group, int u, const int4 *items, const int64_t *count, int64_t n_items,
                    unsigned long long *ctr, int2 *rounds, int tl_id, void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
