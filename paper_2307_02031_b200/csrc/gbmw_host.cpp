@@ -17,7 +17,9 @@
 #include <chrono>
 #include <map>
 #include <memory>
+#include <thread>
 #include <tuple>
+#include <unordered_map>
 
 static double now_ms() {
     return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
@@ -69,6 +71,17 @@ struct UnitInfo {
     int64_t max_bnd = 0, max_int = 0;
 };
 
+// hash of the (begin, count, micro-batch / fuse) record keys
+struct Key3Hash {
+    template <class A, class B, class C>
+    size_t operator()(const std::tuple<A, B, C> &k) const {
+        uint64_t h = (uint64_t)(uint32_t)std::get<0>(k) * 0x9E3779B97F4A7C15ull;
+        h ^= ((uint64_t)(uint32_t)std::get<1>(k) + 0x632BE59BD9B4E019ull) * 0xC2B2AE3D27D4EB4Full;
+        h ^= ((uint64_t)std::get<2>(k) + 0x165667B19E3779F9ull) * 0x94D049BB133111EBull;
+        return (size_t)(h ^ (h >> 29));
+    }
+};
+
 struct HostProb {
     int status = GBMW_OK;
     bool gpu = false;              // has device work
@@ -80,6 +93,7 @@ struct HostProb {
     // workspace footprint (elements)
     int64_t n_cells = 0, n_r = 0, n_bcells = 0, n_par = 0, n_tiles = 0, n_step_tiles = 0, n_flagw = 0, n_rmap = 0;
     size_t ws_bytes = 0;
+    bool head_ok = false;          // argument checks passed, strategy / unit records resolved
 };
 
 struct Chunk {
@@ -136,8 +150,8 @@ struct gbmw_batch {
     std::vector<gbmw_problem> problems;
     std::vector<HostProb> hp;
     std::vector<Chunk> chunks;
-    std::map<std::tuple<int32_t, int32_t, int64_t>, std::unique_ptr<StratInfo>> strat_cache;
-    std::map<std::tuple<int32_t, int32_t, int>, std::unique_ptr<UnitInfo>> unit_cache;
+    std::unordered_map<std::tuple<int32_t, int32_t, int64_t>, std::unique_ptr<StratInfo>, Key3Hash> strat_cache;
+    std::unordered_map<std::tuple<int32_t, int32_t, int>, std::unique_ptr<UnitInfo>, Key3Hash> unit_cache;
     const StratInfo *strat_last = nullptr;   // last lookups (consecutive problems usually share them)
     std::tuple<int32_t, int32_t, int64_t> strat_last_key{};
     const UnitInfo *unit_last = nullptr;
@@ -449,6 +463,18 @@ void prepare_problem(gbmw_batch &b, int pi, std::string *err) {
     const UnitInfo *ui = unit_info(b, P);
     if (ui->status) return fail(ui->status, ui->err);
     h.ui = ui;
+    h.head_ok = true;
+}
+
+// the rest of the checks and the sizes: reads only the problem and its (immutable) strategy
+// and unit records, so problems run in parallel
+void prepare_problem_tail(gbmw_batch &b, int pi, std::string *err) {
+    const gbmw_problem &P = b.problems[pi];
+    HostProb &h = b.hp[pi];
+    if (!h.head_ok) return;
+    auto fail = [&](int code, const std::string &msg) { h.status = code; set_err(err, code, msg); };
+    const StratInfo *si = h.si;
+    const UnitInfo *ui = h.ui;
     // layer_memory range checks (costs.py:207-210), raised on the first table cell
     if (P.stage_index < 1 || P.stage_index > si->min_pp)
         for (int32_t gi : si->cand) {
@@ -558,10 +584,27 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
     b->hp.resize(n_problems);
     int first_err = GBMW_OK;
     std::string first_msg;
-    for (int64_t i = 0; i < n_problems; ++i) {
-        std::string msg;
-        prepare_problem(*b, (int)i, &msg);
-        if (b->hp[i].status != GBMW_OK && first_err == GBMW_OK) { first_err = b->hp[i].status; first_msg = msg; }
+    double t_head = 0.0;
+    {
+        // checks and shared strategy / unit records in input order, then the per-problem
+        // rest on host threads; the first failing problem (in input order) names the error
+        std::vector<std::string> msgs(n_problems);
+        for (int64_t i = 0; i < n_problems; ++i) prepare_problem(*b, (int)i, &msgs[i]);
+        t_head = now_ms();
+        const int nt = n_problems >= 4096 ? (int)std::min<unsigned>(8u, std::max(1u, std::thread::hardware_concurrency())) : 1;
+        auto tail = [&](int t) {
+            for (int64_t i = t; i < n_problems; i += nt) prepare_problem_tail(*b, (int)i, &msgs[i]);
+        };
+        if (nt > 1) {
+            std::vector<std::thread> pool;
+            for (int t = 1; t < nt; ++t) pool.emplace_back(tail, t);
+            tail(0);
+            for (auto &th : pool) th.join();
+        } else {
+            tail(0);
+        }
+        for (int64_t i = 0; i < n_problems; ++i)
+            if (b->hp[i].status != GBMW_OK) { first_err = b->hp[i].status; first_msg = msgs[i]; break; }
     }
     const double t_probs = now_ms();
     // output offsets
@@ -616,15 +659,20 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
     for (Chunk &c : b->chunks) {
         double tq = now_ms();
         {
-            // (group ascending, U descending, input order): one precomputed key per problem
-            std::vector<std::pair<int64_t, int>> keys(c.probs.size());
+            // (group ascending, U descending, input order): a stable counting sort on the
+            // bucket g * (kMaxUnits + 1) + (kMaxUnits - U)
+            const size_t nb = (size_t)kNumGroups * (kMaxUnits + 1);
+            std::vector<int32_t> bucket(c.probs.size()), start(nb + 1, 0);
             for (size_t i = 0; i < c.probs.size(); ++i) {
                 const int x = c.probs[i];
                 const int g = problem_group(b->hp[x].K, b->problems[x].flags, b->hp[x].U);
-                keys[i] = {((int64_t)g << 40) | ((int64_t)(kMaxUnits - b->hp[x].U) << 28) | (int64_t)i, x};
+                bucket[i] = g * (kMaxUnits + 1) + (kMaxUnits - std::min(b->hp[x].U, kMaxUnits));
+                start[bucket[i] + 1]++;
             }
-            std::sort(keys.begin(), keys.end());
-            for (size_t i = 0; i < keys.size(); ++i) c.probs[i] = keys[i].second;
+            for (size_t k = 0; k < nb; ++k) start[k + 1] += start[k];
+            std::vector<int> sorted(c.probs.size());
+            for (size_t i = 0; i < c.probs.size(); ++i) sorted[start[bucket[i]]++] = c.probs[i];
+            c.probs.swap(sorted);
         }
         td[0] += now_ms() - tq; tq = now_ms();
         std::vector<DevProblem> dps;
@@ -633,8 +681,12 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
         cellp.reserve(c.probs.size() + 1); rp.reserve(c.probs.size() + 1); stepp.reserve(c.probs.size() + 1);
         std::vector<int2> aux;
         std::vector<int32_t> cand, ccls, clsd, clst, uf, uc;
-        std::map<const StratInfo *, std::pair<int32_t, int32_t>> soff;
-        std::map<const UnitInfo *, int32_t> uoff;
+        std::unordered_map<const StratInfo *, std::pair<int32_t, int32_t>> soff;
+        std::unordered_map<const UnitInfo *, int32_t> uoff;
+        const StratInfo *last_si = nullptr;
+        const UnitInfo *last_ui = nullptr;
+        std::pair<int32_t, int32_t> last_soff{0, 0};
+        int32_t last_uoff = 0;
         for (int pi : c.probs) {
             const HostProb &h = b->hp[pi];
             const gbmw_problem &P = b->problems[pi];
@@ -645,21 +697,27 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
             d.n_b = h.n_b; d.micro = P.micro_batch; d.gran = P.granularity_bytes; d.budget = P.budget_bytes;
             d.cell_off = c.n_cells; d.r_off = c.n_r; d.b_off = c.n_bcells; d.par_off = c.n_par; d.tile_off = c.n_tiles;
             d.plan_off = h.plan_off; d.frontier_off = h.frontier_off;
-            auto sit = soff.find(h.si);
-            if (sit == soff.end()) {
-                sit = soff.emplace(h.si, std::make_pair((int32_t)cand.size(), (int32_t)clsd.size())).first;
-                cand.insert(cand.end(), h.si->cand.begin(), h.si->cand.end());
-                ccls.insert(ccls.end(), h.si->cand_cls.begin(), h.si->cand_cls.end());
-                clsd.insert(clsd.end(), h.si->cls_d.begin(), h.si->cls_d.end());
-                clst.insert(clst.end(), h.si->cls_t.begin(), h.si->cls_t.end());
+            if (h.si != last_si) {                      // sorted problems share records in runs
+                auto sit = soff.find(h.si);
+                if (sit == soff.end()) {
+                    sit = soff.emplace(h.si, std::make_pair((int32_t)cand.size(), (int32_t)clsd.size())).first;
+                    cand.insert(cand.end(), h.si->cand.begin(), h.si->cand.end());
+                    ccls.insert(ccls.end(), h.si->cand_cls.begin(), h.si->cand_cls.end());
+                    clsd.insert(clsd.end(), h.si->cls_d.begin(), h.si->cls_d.end());
+                    clst.insert(clst.end(), h.si->cls_t.begin(), h.si->cls_t.end());
+                }
+                last_si = h.si; last_soff = sit->second;
             }
-            auto uit = uoff.find(h.ui);
-            if (uit == uoff.end()) {
-                uit = uoff.emplace(h.ui, (int32_t)uf.size()).first;
-                uf.insert(uf.end(), h.ui->unit_first.begin(), h.ui->unit_first.end());
-                uc.insert(uc.end(), h.ui->unit_count.begin(), h.ui->unit_count.end());
+            if (h.ui != last_ui) {
+                auto uit = uoff.find(h.ui);
+                if (uit == uoff.end()) {
+                    uit = uoff.emplace(h.ui, (int32_t)uf.size()).first;
+                    uf.insert(uf.end(), h.ui->unit_first.begin(), h.ui->unit_first.end());
+                    uc.insert(uc.end(), h.ui->unit_count.begin(), h.ui->unit_count.end());
+                }
+                last_ui = h.ui; last_uoff = uit->second;
             }
-            d.cand_off = sit->second.first; d.class_off = sit->second.second; d.unit_off = uit->second;
+            d.cand_off = last_soff.first; d.class_off = last_soff.second; d.unit_off = last_uoff;
             d.ustate_off = (int32_t)c.n_units;
             d.flag_off = c.n_flagw;
             d.rmap_off = c.n_rmap;
@@ -738,7 +796,8 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
     }
     const double t_prep = now_ms();
     if (getenv("GBMW_K2_HIST") && getenv("GBMW_K2_HIST")[0] == '1')
-        fprintf(stderr, "create: problems %.3f ms, chunking %.3f ms, descriptors %.3f ms (sort %.3f loop %.3f groups %.3f "
+        fprintf(stderr, "create: head %.3f ms, ", t_head - t_start),
+        fprintf(stderr, "problems %.3f ms, chunking %.3f ms, descriptors %.3f ms (sort %.3f loop %.3f groups %.3f "
                 "stepmap %.3f puts %.3f)\n", t_probs - t_start, t_chunks - t_probs, t_prep - t_chunks, td[0], td[1], td[2],
                 td[3], td[4]);
     // arena: inputs | descriptor blob | outputs
