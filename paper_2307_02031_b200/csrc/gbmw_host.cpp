@@ -111,6 +111,7 @@ struct Chunk {
     int64_t n_aux = 0;
     std::vector<StepList> slists;  // K2 launches (unit, group), in launch order
     std::vector<int> slist_group;
+    std::vector<char> slist_second;   // u = 2 list run by the candidate-row kernel (K2s)
     int64_t n_items = 0;           // K2 items (active problems) over all launches
     size_t small_bytes = 0;
     size_t ws_bytes = 0;
@@ -775,7 +776,8 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
         c.o_stepmap = put(blob, stepmap.data(), stepmap.size()) - base;
         c.o_aux = put(blob, aux.data(), aux.size()) - base;
         // K2 launches: items bounded by all tiles of the active problems
-        c.slists.clear(); c.slist_group.clear(); c.n_items = 0;
+        c.slists.clear(); c.slist_group.clear(); c.slist_second.clear(); c.n_items = 0;
+        static const bool no_second = getenv("GBMW_NO_SECOND") && getenv("GBMW_NO_SECOND")[0] == '1';
         for (int u = 1; u < c.Umax; ++u)
             for (int g = 0; g < kStepVGroups; ++g) {
                 const int lo = c.group_lo[g], na = c.n_active[g][u];
@@ -784,6 +786,12 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
                 sl.u = u; sl.lo = lo; sl.n = na; sl.pad_ = 0; sl.base = c.n_items;
                 c.slists.push_back(sl);
                 c.slist_group.push_back(g);
+                bool second = u == 2 && !no_second;
+                for (int x = lo; x < lo + na && second; ++x) {
+                    const HostProb &hx = b->hp[c.probs[x]];
+                    second = hx.S <= kSecondMaxS && hx.n_b + 1 <= kSecondMaxRows;
+                }
+                c.slist_second.push_back(second ? 1 : 0);
                 // items of >= 1 warp tile: a problem's warp tiles number at most 2 * (its
                 // 2048-row tiles)
                 c.n_items += 2 * (c.step_prefix[lo + na] - c.step_prefix[lo]);
@@ -1038,6 +1046,11 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
             int2 *rounds = a.k2_rounds + 2 * c.step_prefix[c.group_lo[g]] * kK2RoundsPerSlot;
             if (sl.u == 1) {                             // first step: segments of the first unit's weights
                 if ((rc = launch_dp_first(a, sl.lo, sl.n, gs[g]))) return cuda_fail(ctx, rc, "K2 first launch");
+                c.launches += 1;
+                continue;
+            }
+            if (c.slist_second[s]) {                     // second step: candidate rows of few-source problems
+                if ((rc = launch_dp_second(a, g / kBands, sl.lo, sl.n, gs[g]))) return cuda_fail(ctx, rc, "K2 second launch");
                 c.launches += 1;
                 continue;
             }

@@ -216,6 +216,11 @@ int launch_step_lists(const ChunkArgs &a, void *stream);
 int launch_dp_step(const ChunkArgs &a, int group, int u, const int4 *items, const int64_t *count, int64_t max_items,
                    unsigned long long *counters3, int2 *rounds, int tl_id, void *stream);
 int launch_dp_first(const ChunkArgs &a, int p_lo, int p_n, void *stream);
+// u = 2 on candidate rows, for problems with S <= kSecondMaxS distinct strategies and
+// n_e <= kSecondMaxRows rows (gbmw_step.cu)
+constexpr int kSecondMaxS = 60;
+constexpr int64_t kSecondMaxRows = 131072;
+int launch_dp_second(const ChunkArgs &a, int group, int p_lo, int p_n, void *stream);
 int launch_sweep(const ChunkArgs &a, void *stream);
 int launch_approx_step(const ChunkArgs &a, int u, int64_t tile_base, int64_t n_tiles, unsigned long long *counter,
                        void *stream);

@@ -630,7 +630,6 @@ __global__ void __launch_bounds__(kStepThreads, GROUP <= 1 ? 3 : 1)
     tl_mark(a.k2_tl, tl_id, true);
     pdl_trigger();
 }
-#undef GBMW_K2_DISPATCH
 
 // K2 for the first layer step (u = 1), one CTA per problem.  T_0[e, i] = time_c[0, i] for
 // e >= w_0i (dpsearch.py:255-259), so B_1 is piecewise constant with breakpoints only at the
@@ -761,6 +760,301 @@ __global__ void __launch_bounds__(kFirstThreads) k_dp_first(ChunkArgs a, int p_l
 int launch_dp_first(const ChunkArgs &a, int p_lo, int p_n, void *stream) {
     if (p_n <= 0) return 0;
     k_dp_first<<<p_n, kFirstThreads, 0, (cudaStream_t)stream>>>(a, p_lo, p_n);
+    return (int)cudaGetLastError();
+}
+
+// K2 for the second layer step (u = 2), one CTA per problem, for problems with few
+// distinct sources (S <= kSecondMaxS) and few rows (n_e <= kSecondMaxRows).  B_1 changes at
+// a handful of rows (K2f), so the rows of B_2 where some source's input changes are the
+// sums y + w_i over the change rows y of B_1 in column cls(i) and the unit-1 weights w_i:
+// at most (S + 1) S of them.  They are collected in a shared-memory bitmap, evaluated in
+// row order by the same lexmin as every step (eval_row, T1 tie-break, path-aware keys),
+// compared with the previous candidate (exact change bits: no tile anchors), and the row
+// map / change words / summaries written per group as K2 writes them.
+constexpr int kSecondThreads = 256;
+constexpr int kSecondMaxX = 4096;                        // candidate rows
+constexpr int kSecondMaxY = 128;                         // change rows of B_1
+constexpr int kSecondChunk = 64;                         // candidates per evaluation pass
+constexpr int kSecondL = 8;                              // lanes per candidate
+struct SecondSmem {
+    int x[kSecondMaxX];                                  // candidate rows, ascending
+    union {
+        uint32_t bits[kSecondMaxX];                      // candidate bitmap over [L_2, L_2 + 32 * 4096)
+        int last[kSecondMaxX];                           // last stored row at or before candidate j
+    };
+    uint16_t mask[kSecondMaxX];                          // change bits of candidate j
+    int y[kSecondMaxY];
+    uint32_t ymask[kSecondMaxY];
+    double rt[(kSecondChunk + 1) * kMaxClasses], rf[(kSecondChunk + 1) * kMaxClasses];
+    int rk[(kSecondChunk + 1) * kMaxClasses];
+    int scan[40];
+    TileCtx t;
+};
+
+// exclusive prefix sum over the block (blockDim.x == kSecondThreads); *total = sum
+__device__ __forceinline__ int second_scan(int v, int *tmp, int *total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int incl = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const int o = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += o;
+    }
+    if (lane == 31) tmp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        const int nw = kSecondThreads / 32;
+        int w = lane < nw ? tmp[lane] : 0;
+        int wi = w;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int o = __shfl_up_sync(0xffffffffu, wi, off);
+            if (lane >= off) wi += o;
+        }
+        if (lane < nw) tmp[lane] = wi - w;
+        if (lane == nw - 1) tmp[32] = wi;
+    }
+    __syncthreads();
+    const int r = incl - v + tmp[warp];
+    *total = tmp[32];
+    __syncthreads();
+    return r;
+}
+
+// exclusive prefix max over the block (identity -1)
+__device__ __forceinline__ int second_scan_max(int v, int *tmp) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int incl = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const int o = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl = max(incl, o);
+    }
+    if (lane == 31) tmp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        const int nw = kSecondThreads / 32;
+        const int w = lane < nw ? tmp[lane] : -1;
+        int wi = w;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int o = __shfl_up_sync(0xffffffffu, wi, off);
+            if (lane >= off) wi = max(wi, o);
+        }
+        const int ex = __shfl_up_sync(0xffffffffu, wi, 1);
+        if (lane < nw) tmp[lane] = lane == 0 ? -1 : ex;
+    }
+    __syncthreads();
+    const int ex_lane = __shfl_up_sync(0xffffffffu, incl, 1);
+    const int r = max(tmp[warp], lane == 0 ? -1 : ex_lane);
+    __syncthreads();
+    return r;
+}
+
+// evaluate candidates [c0, c0 + nc) into result slots 1..nc (slot 0: the previous candidate)
+template <int KT, bool GUARD>
+__device__ __forceinline__ void second_eval(const ChunkArgs &a, SecondSmem &sm, int c0, int nc) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int per_warp = 32 / kSecondL;
+    const int seg = lane / kSecondL, l = lane - seg * kSecondL;
+    for (int j0 = warp * per_warp; j0 < nc; j0 += (kSecondThreads / 32) * per_warp) {
+        const int j = j0 + seg;
+        const int e = j < nc ? sm.x[c0 + j] : -1;
+        double bt[KT], bf[KT];
+        int bk[KT];
+        eval_row<KT, false, GUARD>(a, sm.t, 2, e, kSecondL, l, bt, bf, bk);
+        if (j < nc && l == 0) {
+#pragma unroll
+            for (int kk = 0; kk < KT; ++kk) {
+                if (GUARD && kk >= sm.t.K) break;
+                sm.rt[(j + 1) * kMaxClasses + kk] = bt[kk];
+                sm.rf[(j + 1) * kMaxClasses + kk] = bf[kk];
+                sm.rk[(j + 1) * kMaxClasses + kk] = bk[kk];
+            }
+        }
+    }
+}
+
+template <int GROUP>
+__global__ void __launch_bounds__(kSecondThreads, GROUP <= 1 ? 3 : 1) k_dp_second(ChunkArgs a, int p_lo, int p_n) {
+    extern __shared__ __align__(16) unsigned char second_raw[];
+    SecondSmem &sm = *reinterpret_cast<SecondSmem *>(second_raw);
+    const int q = p_lo + (int)blockIdx.x;
+    if ((int)blockIdx.x >= p_n) return;
+    const int u = 2, tid = threadIdx.x;
+    if (tid == 0) load_tile_ctx(a, u, q, 0, sm.t);
+    __syncthreads();
+    const TileCtx &t = sm.t;
+    const int lo = t.lo, hi = t.hi, lo1 = t.lo_prev, K = t.K, S = t.S, n_e = t.n_e;
+    if (hi < lo) return;
+    const DevProblem &p = a.probs[q];
+    const int hi1 = a.unit_hi[p.ustate_off + 1];
+    const int64_t ng = rmap_groups(n_e);
+    const uint32_t *fin = a.chg[(u - 1) & 1] + t.f_off;
+    const uint32_t allk = (K >= 32) ? 0xffffffffu : ((1u << K) - 1u);
+    // 1. change rows of B_1: its stored rows (row map of unit 1) and their change columns
+    {
+        const int g0 = lo1 >> 5, g1 = hi1 >> 5, G = g1 - g0 + 1;
+        const int per = (G + kSecondThreads - 1) / kSecondThreads;
+        const int ga = g0 + tid * per, gb = min(g0 + (tid + 1) * per, g1 + 1);
+        int cnt = 0;
+        for (int g = ga; g < gb; ++g) cnt += __popc((unsigned)__ldg(a.rmap + t.rm_prev + g).x);
+        int total = 0;
+        int at = second_scan(cnt, sm.scan, &total);
+        for (int g = ga; g < gb; ++g) {
+            unsigned b = (unsigned)__ldg(a.rmap + t.rm_prev + g).x;
+            while (b) {
+                const int x = __ffs(b) - 1;
+                b &= b - 1u;
+                const int y = 32 * g + x;
+                uint32_t m = 0u;
+                for (int k = 0; k < K; ++k) m |= ((__ldg(fin + (int64_t)k * t.nw + (y >> 5)) >> x) & 1u) << k;
+                if (y == lo1) m = allk;                  // the first finite row: every column
+                if (at < kSecondMaxY) { sm.y[at] = y; sm.ymask[at] = m; }
+                ++at;
+            }
+        }
+        if (tid == 0) sm.scan[36] = total;
+        __syncthreads();
+    }
+    const int ny = min(sm.scan[36], kSecondMaxY);
+    // 2. candidate bitmap over [lo, hi]
+    const int nbits = hi - lo + 1, nwd = (nbits + 31) >> 5;
+    for (int w = tid; w < nwd; w += kSecondThreads) sm.bits[w] = 0u;
+    __syncthreads();
+    if (tid == 0) atomicOr(&sm.bits[0], 1u);                // the first live row (the anchor)
+    for (int pi = tid; pi < ny * S; pi += kSecondThreads) {
+        const int jy = pi / S, i = pi - jy * S;
+        const Cell c = t.cell[i];
+        if (!((sm.ymask[jy] >> c.k) & 1u)) continue;
+        const int x = sm.y[jy] + c.w;
+        if (x < lo || x > hi) continue;
+        atomicOr(&sm.bits[(x - lo) >> 5], 1u << ((x - lo) & 31));
+    }
+    __syncthreads();
+    // 3. candidates in row order
+    int nx = 0;
+    {
+        const int per = (nwd + kSecondThreads - 1) / kSecondThreads;
+        const int wa = tid * per, wb = min((tid + 1) * per, nwd);
+        int cnt = 0;
+        for (int w = wa; w < wb; ++w) cnt += __popc(sm.bits[w]);
+        int at = second_scan(cnt, sm.scan, &nx);
+        for (int w = wa; w < wb; ++w) {
+            unsigned b = sm.bits[w];
+            while (b) {
+                const int x = __ffs(b) - 1;
+                b &= b - 1u;
+                if (at < kSecondMaxX) sm.x[at] = lo + 32 * w + x;
+                ++at;
+            }
+        }
+        __syncthreads();
+    }
+    nx = min(nx, kSecondMaxX);                           // host bound: (S + 1) S <= kSecondMaxX
+    // 4. evaluation in chunks, change bits against the previous candidate, stored rows out
+    TFCell *bout = a.TF[u & 1] + t.b_off;
+    uint16_t *pout = a.par + t.par_off + (int64_t)(u - 1) * K * n_e;
+    for (int c0 = 0; c0 < nx; c0 += kSecondChunk) {
+        const int nc = min(kSecondChunk, nx - c0);
+#define GBMW_K2S_EVAL(KT, G) second_eval<KT, G>(a, sm, c0, nc)
+        GBMW_K2_DISPATCH(GBMW_K2S_EVAL)
+#undef GBMW_K2S_EVAL
+        __syncthreads();
+        for (int j = tid; j < nc; j += kSecondThreads) {
+            uint32_t chg = 0u;
+            const int s1 = (j + 1) * kMaxClasses, s0 = j * kMaxClasses;
+            for (int kk = 0; kk < K; ++kk) {
+                const bool same = sm.rt[s1 + kk] == sm.rt[s0 + kk] && sm.rf[s1 + kk] == sm.rf[s0 + kk] &&
+                                  (sm.rk[s1 + kk] >> 1) == (sm.rk[s0 + kk] >> 1) && !(sm.rk[s1 + kk] & 1);
+                chg |= same ? 0u : (1u << kk);
+            }
+            if (c0 + j == 0) chg = allk;
+            sm.mask[c0 + j] = (uint16_t)chg;
+        }
+        for (int jk = tid; jk < nc * K; jk += kSecondThreads) {
+            const int j = jk / K, kk = jk - j * K;
+            const int s1 = (j + 1) * kMaxClasses;
+            // stored: the anchor and every candidate where some column changes (mask of j
+            // is recomputed here from the same slots, so no barrier is needed)
+            uint32_t chg = 0u;
+            for (int k2 = 0; k2 < K; ++k2) {
+                const int s0 = j * kMaxClasses;
+                const bool same = sm.rt[s1 + k2] == sm.rt[s0 + k2] && sm.rf[s1 + k2] == sm.rf[s0 + k2] &&
+                                  (sm.rk[s1 + k2] >> 1) == (sm.rk[s0 + k2] >> 1) && !(sm.rk[s1 + k2] & 1);
+                chg |= same ? 0u : 1u;
+            }
+            if (c0 + j == 0 || chg) {
+                const int e = sm.x[c0 + j];
+                reinterpret_cast<double2 *>(bout)[(int64_t)kk * n_e + e] = make_double2(sm.rt[s1 + kk], sm.rf[s1 + kk]);
+                pout[(int64_t)kk * n_e + e] = (uint16_t)t.idx[sm.rk[s1 + kk] >> 1];
+            }
+        }
+        __syncthreads();
+        for (int kk = tid; kk < K; kk += kSecondThreads) {   // carry the last candidate to slot 0
+            sm.rt[kk] = sm.rt[nc * kMaxClasses + kk];
+            sm.rf[kk] = sm.rf[nc * kMaxClasses + kk];
+            sm.rk[kk] = sm.rk[nc * kMaxClasses + kk];
+        }
+        __syncthreads();
+    }
+    // 5. last stored row at or before each candidate (the bitmap is dead: reuse as `last`)
+    {
+        const int per = (nx + kSecondThreads - 1) / kSecondThreads;
+        const int ja = tid * per, jb = min((tid + 1) * per, nx);
+        int loc = -1;
+        for (int j = ja; j < jb; ++j) if (j == 0 || sm.mask[j]) loc = sm.x[j];
+        int run = second_scan_max(loc, sm.scan);
+        for (int j = ja; j < jb; ++j) {
+            if (j == 0 || sm.mask[j]) run = sm.x[j];
+            sm.last[j] = run;
+        }
+        __syncthreads();
+    }
+    // 6. per 32-row group of the live rows: change words, row map; per tile: summaries
+    const int nw = t.nw, nsw = (int)sum_words(n_e);
+    uint32_t *fout = a.chg[u & 1] + t.f_off;
+    uint32_t *sout = fout + (int64_t)K * nw;
+    int2 *rmo = a.rmap + t.rm_cur;
+    const int lane = tid & 31, warp = tid >> 5;
+    for (int tile = lo / kWarpRows + warp; tile <= hi / kWarpRows; tile += kSecondThreads / 32) {
+        const int r0 = tile * kWarpRows + 32 * lane, r1 = r0 + 31;
+        const bool dead = r1 < lo || r0 > hi;
+        int j0 = 0, j1 = nx;                             // first candidate >= r0
+        while (j0 < j1) { const int mid = (j0 + j1) >> 1; if (sm.x[mid] < r0) j0 = mid + 1; else j1 = mid; }
+        const int before = j0 > 0 ? sm.last[j0 - 1] : -1;
+        unsigned sbits = 0u;
+        for (int j = j0; j < nx && sm.x[j] <= r1; ++j)
+            if (j == 0 || sm.mask[j]) sbits |= 1u << (sm.x[j] - r0);
+        for (int k = 0; k < K; ++k) {
+            uint32_t wd = 0u;
+            for (int j = j0; j < nx && sm.x[j] <= r1; ++j) wd |= ((uint32_t)(sm.mask[j] >> k) & 1u) << (sm.x[j] - r0);
+            if (!dead) fout[(int64_t)k * nw + (r0 >> 5)] = wd;
+            const unsigned smk = __ballot_sync(0xffffffffu, wd != 0u);
+            if (lane == 0) sout[(int64_t)k * nsw + tile] = smk;
+        }
+        if (!dead) rmo[r0 >> 5] = make_int2((int)sbits, before);
+    }
+    if (tid == 0) atomicAdd(a.computed_cells, (unsigned long long)nx * (unsigned long long)K);
+    (void)ng;
+}
+
+#undef GBMW_K2_DISPATCH
+
+int launch_dp_second(const ChunkArgs &a, int group, int p_lo, int p_n, void *stream) {
+    if (p_n <= 0) return 0;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_dp_second<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SecondSmem));
+        cudaFuncSetAttribute(k_dp_second<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SecondSmem));
+        cudaFuncSetAttribute(k_dp_second<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SecondSmem));
+        attr = true;
+    }
+    const size_t sb = sizeof(SecondSmem);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (group == 0) k_dp_second<0><<<p_n, kSecondThreads, sb, st>>>(a, p_lo, p_n);
+    else if (group == 1) k_dp_second<1><<<p_n, kSecondThreads, sb, st>>>(a, p_lo, p_n);
+    else k_dp_second<2><<<p_n, kSecondThreads, sb, st>>>(a, p_lo, p_n);
     return (int)cudaGetLastError();
 }
 
