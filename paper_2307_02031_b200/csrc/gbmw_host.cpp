@@ -1177,15 +1177,30 @@ extern "C" int gbmw_batch_fetch(gbmw_ctx *ctx, gbmw_batch *b, gbmw_result *resul
     cudaSetDevice(ctx->device);
     cudaStream_t st = ctx->stream;
     const size_t np = b->problems.size();
-    std::vector<gbmw_result> dev_res(np);
+    // results | plans | frontier are contiguous in the arena: one copy through the
+    // context's pinned staging buffer, then out to the caller's arrays
+    const size_t lo = b->o_results;
+    const size_t hi = (frontier && b->total_frontier) ? b->o_frontier + (size_t)b->total_frontier * sizeof(double)
+                                                      : b->o_plans + (size_t)b->total_plan * sizeof(int32_t);
+    const size_t nbytes = hi > lo ? hi - lo : 0;
+    if (ctx->pinned_cap < nbytes) {
+        if (ctx->pinned) cudaFreeHost(ctx->pinned);
+        ctx->pinned = nullptr;
+        ctx->pinned_cap = 0;
+        const size_t cap = std::max<size_t>(nbytes + nbytes / 4, 1u << 20);
+        if (cudaHostAlloc(&ctx->pinned, cap, cudaHostAllocDefault) == cudaSuccess) ctx->pinned_cap = cap;
+    }
+    std::vector<char> fallback;
+    char *host = (char *)ctx->pinned;
+    if (!host) { fallback.resize(nbytes); host = fallback.data(); }
     cudaError_t ce = cudaSuccess;
-    if (np) ce = cudaMemcpyAsync(dev_res.data(), (char *)b->arena + b->o_results, np * sizeof(gbmw_result), cudaMemcpyDeviceToHost, st);
-    if (ce == cudaSuccess && plans && b->total_plan)
-        ce = cudaMemcpyAsync(plans, (char *)b->arena + b->o_plans, b->total_plan * sizeof(int32_t), cudaMemcpyDeviceToHost, st);
-    if (ce == cudaSuccess && frontier && b->total_frontier)
-        ce = cudaMemcpyAsync(frontier, (char *)b->arena + b->o_frontier, b->total_frontier * sizeof(double), cudaMemcpyDeviceToHost, st);
+    if (nbytes) ce = cudaMemcpyAsync(host, (char *)b->arena + lo, nbytes, cudaMemcpyDeviceToHost, st);
     if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
     if (ce != cudaSuccess) return cuda_fail(ctx, (int)ce, "fetch");
+    const gbmw_result *dev_res = reinterpret_cast<const gbmw_result *>(host);
+    if (plans && b->total_plan) std::memcpy(plans, host + (b->o_plans - lo), (size_t)b->total_plan * sizeof(int32_t));
+    if (frontier && b->total_frontier)
+        std::memcpy(frontier, host + (b->o_frontier - lo), (size_t)b->total_frontier * sizeof(double));
     b->timing.d2h_bytes = (double)(np * sizeof(gbmw_result)) + (plans ? (double)b->total_plan * 4.0 : 0.0) +
                           (frontier ? (double)b->total_frontier * 8.0 : 0.0);
     int first = GBMW_OK;
