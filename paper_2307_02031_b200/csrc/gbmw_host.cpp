@@ -991,7 +991,7 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
         cudaMemsetAsync(a.bup, 0, c.probs.size() * 8, st);
         cudaMemsetAsync(a.counters, 0, (size_t)(c.Umax + 1) * kNumGroups * 3 * 8, st);
         if ((rc = launch_cost_tables(a, c.n_cells, c.n_r, st))) return cuda_fail(ctx, rc, "K1 launch");
-        c.launches += (c.n_cells > 0) + (c.n_r > 0) + (c.n_units > 0);
+        c.launches += (c.n_cells > 0) + (c.n_r > 0) + 2 * (c.n_units > 0 && !c.probs.empty());
         cudaEventRecord(c.ev[1], st);
         if (tables_only) continue;
         if (!c.slists.empty()) {

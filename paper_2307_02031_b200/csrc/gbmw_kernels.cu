@@ -94,63 +94,75 @@ __global__ void k_cost_r(ChunkArgs a, int64_t n_r) {
 // time_c, ef_true) at unit u produce identical (T, F) in every row of the unit-u
 // table, hence identical candidates for every target; with ties resolved to the
 // first index (T1) the later one can never be an argmin.  K2 relaxes only the
-// first of each group.  One block per problem, one warp per unit.
+// first of each group.  A warp per (problem, unit).
 //
 // The same pass derives the live row range of every class table B_u: with
 // wmin_v = min_i weight[v][i], T_u is +inf below m_u = sum_{v<=u} wmin_v, so
 // B_u[e'] (built from T_{u-1}[e']) is +inf for e' < L_u = m_{u-1}; and B_u is only
 // ever read at rows e - w_uj <= n_b - wmin_u = H_u.  Rows outside [L_u, H_u] are
 // neither computed nor read (readers treat them as +inf, which they are).
+// A warp per (problem, unit) over the whole chunk, so a deep problem's units run on many SMs
+// at once; the unit's wmin is parked in unit_hi until k_unit_ranges turns it into [L_u, H_u].
 __global__ void k_dedupe(ChunkArgs a) {
-    const DevProblem &p = a.probs[blockIdx.x];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-    __shared__ int s_wmin[kMaxUnits];
-    for (int u = warp; u < p.U; u += nwarps) {
-        const Cell *cells = a.cells + p.cell_off + (int64_t)u * p.S;
-        int32_t *uniq = a.uniq + p.cell_off + (int64_t)u * p.S;
-        int count = 0;
-        int wmin = 0x7fffffff;
-        for (int base = 0; base < p.S; base += 32) {
-            const int i = base + lane;
-            bool keep = false;
-            if (i < p.S) {
-                const Cell ci = cells[i];
-                wmin = min(wmin, ci.w);
-                keep = true;
-                for (int j = 0; j < i; ++j) {
-                    const Cell cj = cells[j];
-                    if (cj.w == ci.w && cj.k == ci.k && cj.c == ci.c && cj.ef == ci.ef) { keep = false; break; }
-                }
-            }
-            const unsigned m = __ballot_sync(0xffffffffu, keep);
-            if (keep) {
-                const int slot = count + __popc(m & ((1u << lane) - 1u));
-                uniq[slot] = i;
-                a.ucell[p.cell_off + (int64_t)u * p.S + slot] = cells[i];
-            }
-            count += __popc(m);
-        }
-        for (int off = 16; off > 0; off >>= 1) wmin = min(wmin, __shfl_xor_sync(0xffffffffu, wmin, off));
-        if (lane == 0) {
-            a.nuniq[p.ustate_off + u] = count;
-            s_wmin[u] = wmin;
-        }
+    const int lane = threadIdx.x & 31;
+    const int64_t gu = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (gu >= a.n_units) return;
+    int qa = 0, qb = a.n_probs - 1;                      // problem holding global unit gu
+    while (qa < qb) {
+        const int mid = (qa + qb + 1) >> 1;
+        if (a.probs[mid].ustate_off <= gu) qa = mid; else qb = mid - 1;
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const int64_t top = p.n_b + 1;
-        int64_t acc = 0;
-        unsigned long long live = 0;
-        for (int u = 0; u < p.U; ++u) {
-            const int64_t lo = acc < top ? acc : top, hi = p.n_b - s_wmin[u];
-            a.unit_lo[p.ustate_off + u] = (int32_t)lo;                          // L_u = m_{u-1}
-            a.unit_hi[p.ustate_off + u] = (int32_t)hi;                          // H_u
-            if (u >= 1 && hi >= lo) live += (unsigned long long)(hi - lo + 1);
-            acc += s_wmin[u];
+    const DevProblem &p = a.probs[qa];
+    const int u = (int)(gu - p.ustate_off);
+    const Cell *cells = a.cells + p.cell_off + (int64_t)u * p.S;
+    int32_t *uniq = a.uniq + p.cell_off + (int64_t)u * p.S;
+    int count = 0;
+    int wmin = 0x7fffffff;
+    for (int base = 0; base < p.S; base += 32) {
+        const int i = base + lane;
+        bool keep = false;
+        if (i < p.S) {
+            const Cell ci = cells[i];
+            wmin = min(wmin, ci.w);
+            keep = true;
+            for (int j = 0; j < i; ++j) {
+                const Cell cj = cells[j];
+                if (cj.w == ci.w && cj.k == ci.k && cj.c == ci.c && cj.ef == ci.ef) { keep = false; break; }
+            }
         }
-        // live class cells written by K2 (algorithmic-bytes accounting)
-        if (!(p.flags & GBMW_APPROX)) atomicAdd(a.live_cells, live * (unsigned long long)p.K);
+        const unsigned m = __ballot_sync(0xffffffffu, keep);
+        if (keep) {
+            const int slot = count + __popc(m & ((1u << lane) - 1u));
+            uniq[slot] = i;
+            a.ucell[p.cell_off + (int64_t)u * p.S + slot] = cells[i];
+        }
+        count += __popc(m);
     }
+    for (int off = 16; off > 0; off >>= 1) wmin = min(wmin, __shfl_xor_sync(0xffffffffu, wmin, off));
+    if (lane == 0) {
+        a.nuniq[p.ustate_off + u] = count;
+        a.unit_hi[p.ustate_off + u] = wmin;
+    }
+}
+
+// Live row ranges of every unit, a thread per problem (reads the wmins k_dedupe parked).
+__global__ void k_unit_ranges(ChunkArgs a) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= a.n_probs) return;
+    const DevProblem &p = a.probs[q];
+    const int64_t top = p.n_b + 1;
+    int64_t acc = 0;
+    unsigned long long live = 0;
+    for (int u = 0; u < p.U; ++u) {
+        const int wmin = a.unit_hi[p.ustate_off + u];
+        const int64_t lo = acc < top ? acc : top, hi = p.n_b - wmin;
+        a.unit_lo[p.ustate_off + u] = (int32_t)lo;                          // L_u = m_{u-1}
+        a.unit_hi[p.ustate_off + u] = (int32_t)hi;                          // H_u
+        if (u >= 1 && hi >= lo) live += (unsigned long long)(hi - lo + 1);
+        acc += wmin;
+    }
+    // live class cells written by K2 (algorithmic-bytes accounting)
+    if (!(p.flags & GBMW_APPROX)) atomicAdd(a.live_cells, live * (unsigned long long)p.K);
 }
 
 // K2 (the min-plus layer step) lives in gbmw_step.cu.
@@ -936,7 +948,10 @@ int launch_cost_tables(const ChunkArgs &a, int64_t n_cells, int64_t n_r, void *s
     cudaStream_t st = (cudaStream_t)stream;
     if (n_cells > 0) k_cost_cells<<<blocks_for(n_cells, 128), 128, 0, st>>>(a, n_cells);
     if (n_r > 0) k_cost_r<<<blocks_for(n_r, 128), 128, 0, st>>>(a, n_r);
-    if (a.n_units > 0 && a.n_probs > 0) k_dedupe<<<a.n_probs, 128, 0, st>>>(a);
+    if (a.n_units > 0 && a.n_probs > 0) {
+        k_dedupe<<<blocks_for(a.n_units * 32, 128), 128, 0, st>>>(a);
+        k_unit_ranges<<<blocks_for(a.n_probs, 128), 128, 0, st>>>(a);
+    }
     return (int)cudaGetLastError();
 }
 
