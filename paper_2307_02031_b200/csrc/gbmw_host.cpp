@@ -782,19 +782,19 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
             for (int g = 0; g < kStepVGroups; ++g) {
                 const int lo = c.group_lo[g], na = c.n_active[g][u];
                 if (na == 0) continue;
-                StepList sl;
-                sl.u = u; sl.lo = lo; sl.n = na; sl.pad_ = 0; sl.base = c.n_items;
-                c.slists.push_back(sl);
-                c.slist_group.push_back(g);
                 bool second = u == 2 && !no_second;
                 for (int x = lo; x < lo + na && second; ++x) {
                     const HostProb &hx = b->hp[c.probs[x]];
                     second = hx.S <= kSecondMaxS && hx.n_b + 1 <= kSecondMaxRows;
                 }
+                StepList sl;
+                sl.u = u; sl.lo = lo; sl.n = na; sl.no_items = (u == 1 || second) ? 1 : 0; sl.base = c.n_items;
+                c.slists.push_back(sl);
+                c.slist_group.push_back(g);
                 c.slist_second.push_back(second ? 1 : 0);
                 // items of >= 1 warp tile: a problem's warp tiles number at most 2 * (its
                 // 2048-row tiles)
-                c.n_items += 2 * (c.step_prefix[lo + na] - c.step_prefix[lo]);
+                if (!sl.no_items) c.n_items += 2 * (c.step_prefix[lo + na] - c.step_prefix[lo]);
             }
         c.o_slists = put(blob, c.slists.data(), c.slists.size()) - base;
         td[4] += now_ms() - tq; tq = now_ms();

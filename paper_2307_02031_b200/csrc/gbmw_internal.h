@@ -148,7 +148,7 @@ struct SweepPartial {
 // k_step_lists writes the ones with live rows as (problem, first warp tile, last warp tile)
 // items at items[base ...] (rows [L_u, H_u] only) and the item count to step_count[index].
 struct StepList {
-    int32_t u, lo, n, pad_;
+    int32_t u, lo, n, no_items;   // no_items: the step runs without tile items (K2f / K2s)
     int64_t base;
 };
 

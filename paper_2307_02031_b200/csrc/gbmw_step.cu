@@ -427,6 +427,10 @@ __global__ void __launch_bounds__(1024) k_step_lists(ChunkArgs a) {
     __shared__ int s_part[1024];
     const StepList sl = a.step_lists[blockIdx.x];
     const int tid = threadIdx.x;
+    if (sl.no_items) {                                   // run by K2f / K2s
+        if (tid == 0) a.step_count[blockIdx.x] = 0;
+        return;
+    }
     const int per = (sl.n + 1023) / 1024;
     const int x0 = sl.lo + min(sl.n, tid * per), x1 = sl.lo + min(sl.n, tid * per + per);
     int cnt = 0;
