@@ -868,66 +868,126 @@ int launch_approx_step(const ChunkArgs &a, int u, int64_t tile_base, int64_t n_t
 }
 
 // ---------------------------------------------------------------- K4: finalize
-__global__ void k_finalize(ChunkArgs a) {
-    const int q = blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= a.n_probs) return;
-    const DevProblem &p = a.probs[q];
-    const SweepPartial safe = a.best[q];
-    double bt = safe.t;
-    int64_t be = safe.e;
-    int bj = safe.j;
-    for (int t = a.ufirst[q]; t < p.n_sweep_tiles; ++t) {       // unsafe (or collapsed-DP) tiles
-        const SweepPartial sp = a.partials[p.tile_off + t];
-        if (cand_better(sp.t, sp.e, bt, be)) { bt = sp.t; be = sp.e; bj = sp.j; }
+// One layer's stage-cost terms (costs.py:322-352): t + rc and t_ns + rc, rc the transform
+// cost from the previous layer's strategy (0 for the first layer).
+__device__ __forceinline__ void layer_terms(const ChunkArgs &a, const DevProblem &p, const gbmw_env &env, int l,
+                                            int gs, int gs_prev, double *ta, double *tb) {
+    const gbmw_strategy s = a.strats[gs];
+    const StratDeg d = strat_degrees(s);
+    const gbmw_layer L = a.layers[p.layer_begin + l];
+    double t, t_ns;
+    layer_times(L, s, d, p.micro, env, &t, &t_ns);
+    double rc = 0.0;
+    if (l > 0) {
+        const StratDeg dp = strat_degrees(a.strats[gs_prev]);
+        rc = transform_cost(L.bnd_bytes_per_sample, dp.data, dp.tp, d.data, d.tp, p.micro, env.intra_island_bw);
     }
+    *ta = t + rc;
+    *tb = t_ns + rc;
+}
+
+// K4: a warp per problem.  Lane 0 reduces the sweep partials, walks the argmin path and
+// folds E_all (serial chains); the layers' plan entries and stage-cost terms are computed
+// by all lanes, and lane 0 sums the terms in layer order (the reference's float order).
+constexpr int kFinWarps = 4;
+constexpr int kFinLayers = 256;
+__global__ void __launch_bounds__(32 * kFinWarps) k_finalize(ChunkArgs a) {
+    __shared__ uint16_t s_path[kFinWarps][kMaxUnits];
+    __shared__ int32_t s_gs[kFinWarps][kFinLayers];
+    __shared__ double s_ta[kFinWarps][kFinLayers], s_tb[kFinWarps][kFinLayers];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int q = blockIdx.x * kFinWarps + warp;
+    if (q >= a.n_probs) return;                          // warp-uniform
+    const DevProblem &p = a.probs[q];
+    uint16_t *path = s_path[warp];
     gbmw_result res;
+    double bt = GBMW_INF, e_all = 0.0;
+    int64_t be = -1;
+    if (lane == 0) {
+        const SweepPartial safe = a.best[q];
+        bt = safe.t;
+        be = safe.e;
+        int bj = safe.j;
+        for (int t = a.ufirst[q]; t < p.n_sweep_tiles; ++t) {   // unsafe (or collapsed-DP) tiles
+            const SweepPartial sp = a.partials[p.tile_off + t];
+            if (cand_better(sp.t, sp.e, bt, be)) { bt = sp.t; be = sp.e; bj = sp.j; }
+        }
+        if (be >= 0) {
+            if (p.flags & GBMW_APPROX) approx_reconstruct(a, p, be, path);
+            else backtrack(a, p, be, bj, path);
+            e_all = plan_e_all(a, p, path);
+        }
+    }
+    be = __shfl_sync(0xffffffffu, be, 0);
+    int32_t *plan = a.plans + p.plan_off;
+    if (be < 0) {
+        for (int l = lane; l < p.n_layers; l += 32) plan[l] = -1;
+        if (lane == 0) {
+            res.frontier_offset = -1;
+            res.status = GBMW_OK;
+            res.stage_time_s = 0.0; res.stage_time_no_sync_s = 0.0; res.stage_peak_mem_bytes = 0.0;
+            res.time_s = GBMW_INF; res.e_fwd_used = 0.0; res.feasible = 0;
+            a.results[p.result_index] = res;
+        }
+        return;
+    }
+    const gbmw_env env = a.envs[p.env_index];
+    const bool cost = (p.flags & GBMW_STAGE_COST) != 0;
+    const bool wide = p.n_layers <= kFinLayers;         // layer terms by all lanes
+    __syncwarp();
+    if (lane == 0 && wide) {                             // expand units to layers (dpsearch.py:230-234)
+        int l = 0;
+        for (int u = 0; u < p.U; ++u) {
+            const int gs = a.cand_strat[p.cand_off + path[u]];
+            const int cnt = a.unit_count[p.unit_off + u];
+            for (int r = 0; r < cnt; ++r, ++l) s_gs[warp][l] = gs;
+        }
+    }
+    __syncwarp();
+    double time_s = 0.0, no_sync = 0.0;
+    int32_t first_pp = 1;
+    if (wide) {
+        for (int l = lane; l < p.n_layers; l += 32) {
+            const int gs = s_gs[warp][l];
+            plan[l] = gs - p.strat_begin;
+            if (cost) layer_terms(a, p, env, l, gs, l > 0 ? s_gs[warp][l - 1] : gs, &s_ta[warp][l], &s_tb[warp][l]);
+        }
+        __syncwarp();
+        if (lane == 0) {
+            first_pp = a.strats[s_gs[warp][0]].pp_degree;
+            if (cost)
+                for (int l = 0; l < p.n_layers; ++l) {
+                    time_s = time_s + s_ta[warp][l];
+                    no_sync = no_sync + s_tb[warp][l];
+                }
+        }
+    } else if (lane == 0) {                              // long stages: lane 0 alone
+        int l = 0, gs_prev = 0;
+        for (int u = 0; u < p.U; ++u) {
+            const int gs = a.cand_strat[p.cand_off + path[u]];
+            const int cnt = a.unit_count[p.unit_off + u];
+            for (int r = 0; r < cnt; ++r, ++l) {
+                plan[l] = gs - p.strat_begin;
+                if (cost) {
+                    double ta, tb;
+                    layer_terms(a, p, env, l, gs, gs_prev, &ta, &tb);
+                    time_s = time_s + ta;
+                    no_sync = no_sync + tb;
+                }
+                if (l == 0) first_pp = a.strats[gs].pp_degree;
+                gs_prev = gs;
+            }
+        }
+    }
+    if (lane != 0) return;
     res.frontier_offset = -1;
     res.status = GBMW_OK;
     res.stage_time_s = 0.0; res.stage_time_no_sync_s = 0.0; res.stage_peak_mem_bytes = 0.0;
-    int32_t *plan = a.plans + p.plan_off;
-    if (be < 0) {
-        res.time_s = GBMW_INF; res.e_fwd_used = 0.0; res.feasible = 0;
-        for (int l = 0; l < p.n_layers; ++l) plan[l] = -1;
-        a.results[p.result_index] = res;
-        return;
-    }
-    uint16_t path[kMaxUnits];
-    if (p.flags & GBMW_APPROX) approx_reconstruct(a, p, be, path);
-    else backtrack(a, p, be, bj, path);
-    const double e_all = plan_e_all(a, p, path);
     res.time_s = bt;
     res.e_fwd_used = (double)(be * p.gran);
     res.feasible = 1;
     if (!(e_all <= p.budget)) res.status = GBMW_EINTERNAL;   // dpsearch.py:220
-    // expand units to layers (dpsearch.py:230-234) and cost the stage (costs.py:322-352)
-    const gbmw_env env = a.envs[p.env_index];
-    double time_s = 0.0, no_sync = 0.0;
-    int l = 0;
-    int prev_d = 0, prev_t = 0;
-    int32_t first_pp = 1;
-    for (int u = 0; u < p.U; ++u) {
-        const int cand = path[u];
-        const int gs = a.cand_strat[p.cand_off + cand];
-        const gbmw_strategy s = a.strats[gs];
-        const StratDeg d = strat_degrees(s);
-        const int cnt = a.unit_count[p.unit_off + u];
-        for (int r = 0; r < cnt; ++r, ++l) {
-            plan[l] = gs - p.strat_begin;
-            if (p.flags & GBMW_STAGE_COST) {
-                const gbmw_layer L = a.layers[p.layer_begin + l];
-                double t, t_ns;
-                layer_times(L, s, d, p.micro, env, &t, &t_ns);
-                const double rc = (l == 0) ? 0.0
-                    : transform_cost(L.bnd_bytes_per_sample, prev_d, prev_t, d.data, d.tp,
-                                     p.micro, env.intra_island_bw);
-                time_s = time_s + (t + rc);
-                no_sync = no_sync + (t_ns + rc);
-            }
-            if (l == 0) first_pp = s.pp_degree;
-            prev_d = d.data; prev_t = d.tp;
-        }
-    }
-    if (p.flags & GBMW_STAGE_COST) {
+    if (cost) {
         if (p.stage_index > 1) {
             const double p2p = stage_p2p_time(a.layers[p.layer_begin].bnd_bytes_per_sample,
                                               p.micro, first_pp, env);
@@ -977,7 +1037,7 @@ int launch_sweep(const ChunkArgs &a, void *stream) {
 
 int launch_finalize(const ChunkArgs &a, void *stream) {
     if (a.n_probs <= 0) return 0;
-    k_finalize<<<blocks_for(a.n_probs, 64), 64, 0, (cudaStream_t)stream>>>(a);
+    k_finalize<<<blocks_for(a.n_probs, kFinWarps), 32 * kFinWarps, 0, (cudaStream_t)stream>>>(a);
     return (int)cudaGetLastError();
 }
 
