@@ -644,15 +644,26 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
             uint16_t path[kMaxUnits];
             double ct = 0.0, cf = 0.0;
             int cj = -1;
+            double qt = GBMW_INF, qf = GBMW_INF;                // the candidate after the next one, from
+            int qj = -1;                                        // the same scan (consumed without a rescan)
             while (true) {
                 double nt = GBMW_INF, nf = GBMW_INF;            // next candidate in (T, F, j) order
                 int nj = -1;
-                for (int j = 0; j < S; ++j) {
-                    double T, F;
-                    row_value(r, e_val, j, T, F);
-                    if (!(T < GBMW_INF)) continue;
-                    if (cj >= 0 && !lex_less(ct, cf, cj, T, F, j)) continue;
-                    if (nj < 0 || lex_less(T, F, j, nt, nf, nj)) { nt = T; nf = F; nj = j; }
+                if (qj >= 0) {
+                    nt = qt; nf = qf; nj = qj; qj = -1;
+                } else {
+                    for (int j = 0; j < S; ++j) {
+                        double T, F;
+                        row_value(r, e_val, j, T, F);
+                        if (!(T < GBMW_INF)) continue;
+                        if (cj >= 0 && !lex_less(ct, cf, cj, T, F, j)) continue;
+                        if (nj < 0 || lex_less(T, F, j, nt, nf, nj)) {
+                            qt = nt; qf = nf; qj = nj;
+                            nt = T; nf = F; nj = j;
+                        } else if (qj < 0 || lex_less(T, F, j, qt, qf, qj)) {
+                            qt = T; qf = F; qj = j;
+                        }
+                    }
                 }
                 if (nj < 0) break;
                 {
