@@ -893,7 +893,6 @@ __global__ void __launch_bounds__(kSecondThreads, GROUP <= 1 ? 3 : 1) k_dp_secon
     if (hi < lo) return;
     const DevProblem &p = a.probs[q];
     const int hi1 = a.unit_hi[p.ustate_off + 1];
-    const int64_t ng = rmap_groups(n_e);
     const uint32_t *fin = a.chg[(u - 1) & 1] + t.f_off;
     const uint32_t allk = (K >= 32) ? 0xffffffffu : ((1u << K) - 1u);
     // 1. change rows of B_1: its stored rows (row map of unit 1) and their change columns
@@ -1040,7 +1039,6 @@ __global__ void __launch_bounds__(kSecondThreads, GROUP <= 1 ? 3 : 1) k_dp_secon
         if (!dead) rmo[r0 >> 5] = make_int2((int)sbits, before);
     }
     if (tid == 0) atomicAdd(a.computed_cells, (unsigned long long)nx * (unsigned long long)K);
-    (void)ng;
 }
 
 #undef GBMW_K2_DISPATCH
