@@ -126,6 +126,8 @@ struct gbmw_ctx {
     cudaStream_t stream = nullptr;
     cudaStream_t aux[kNumGroups] = {nullptr};   // K2 groups 1.. run concurrently with group 0
     cudaEvent_t fork = nullptr, join[kNumGroups] = {nullptr};
+    cudaStream_t list_stream = nullptr;           // K2l, concurrent with the first steps (K2f / K2s)
+    cudaEvent_t list_done = nullptr;
     cudaEvent_t gspan[kNumGroups][2] = {{nullptr}};   // debug (GBMW_K2_HIST): per-stream K2 span
     uint64_t workspace_limit = 0;
     void *ws = nullptr;
@@ -367,6 +369,8 @@ extern "C" int gbmw_ctx_destroy(gbmw_ctx *ctx) {
         if (ctx->join[g]) cudaEventDestroy(ctx->join[g]);
     }
     if (ctx->fork) cudaEventDestroy(ctx->fork);
+    if (ctx->list_stream) cudaStreamDestroy(ctx->list_stream);
+    if (ctx->list_done) cudaEventDestroy(ctx->list_done);
     if (ctx->seed_buf) cudaFree(ctx->seed_buf);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
@@ -994,9 +998,26 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
         c.launches += (c.n_cells > 0) + (c.n_r > 0) + 2 * (c.n_units > 0 && !c.probs.empty());
         cudaEventRecord(c.ev[1], st);
         if (tables_only) continue;
+        // K2l on its own stream from the fork: the bands' first steps (K2f, K2s) need no
+        // items, so the list kernel runs beside them; a band waits for it before its first
+        // tiled step
+        bool lists = false;
         if (!c.slists.empty()) {
-            if ((rc = launch_step_lists(a, st))) return cuda_fail(ctx, rc, "K2 list launch");
+            if (!ctx->list_stream) {
+                int lo_pri = 0, hi_pri = 0;
+                cudaDeviceGetStreamPriorityRange(&lo_pri, &hi_pri);
+                if (cudaStreamCreateWithPriority(&ctx->list_stream, cudaStreamNonBlocking, hi_pri) != cudaSuccess ||
+                    cudaEventCreateWithFlags(&ctx->list_done, cudaEventDisableTiming) != cudaSuccess)
+                    return cuda_fail(ctx, (int)cudaGetLastError(), "list stream");
+            }
+            if (!ctx->fork && cudaEventCreateWithFlags(&ctx->fork, cudaEventDisableTiming) != cudaSuccess)
+                return cuda_fail(ctx, (int)cudaGetLastError(), "fork event");
+            cudaEventRecord(ctx->fork, st);
+            cudaStreamWaitEvent(ctx->list_stream, ctx->fork, 0);
+            if ((rc = launch_step_lists(a, ctx->list_stream))) return cuda_fail(ctx, rc, "K2 list launch");
+            cudaEventRecord(ctx->list_done, ctx->list_stream);
             c.launches += 1;
+            lists = true;
         }
         // the class-count groups (and the collapsed-DP problems) are independent problems:
         // group 0 on the main stream, the others on their own streams, joined before K3
@@ -1022,7 +1043,8 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
             }
             if (!ctx->fork && cudaEventCreateWithFlags(&ctx->fork, cudaEventDisableTiming) != cudaSuccess)
                 return cuda_fail(ctx, (int)cudaGetLastError(), "fork event");
-            if (!forked) { cudaEventRecord(ctx->fork, st); forked = true; }
+            if (!forked && !lists) cudaEventRecord(ctx->fork, st);
+            forked = true;
             cudaStreamWaitEvent(ctx->aux[g], ctx->fork, 0);
             gs[g] = ctx->aux[g];
         }
@@ -1039,9 +1061,14 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
                 if (!ctx->gspan[g][0]) { cudaEventCreate(&ctx->gspan[g][0]); cudaEventCreate(&ctx->gspan[g][1]); }
                 cudaEventRecord(ctx->gspan[g][0], gs[g]);
             }
+        bool have_items[kNumGroups] = {false};
         for (size_t s = 0; s < c.slists.size(); ++s) {
             const StepList &sl = c.slists[s];
             const int g = c.slist_group[s];
+            if (!sl.no_items && !have_items[g]) {        // first tiled step of this stream
+                cudaStreamWaitEvent(gs[g], ctx->list_done, 0);
+                have_items[g] = true;
+            }
             const int64_t ub = (s + 1 < c.slists.size() ? c.slists[s + 1].base : c.n_items) - sl.base;   // item bound
             int2 *rounds = a.k2_rounds + 2 * c.step_prefix[c.group_lo[g]] * kK2RoundsPerSlot;
             if (sl.u == 1) {                             // first step: segments of the first unit's weights
@@ -1077,6 +1104,7 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
             cudaEventRecord(ctx->join[g], gs[g]);
             cudaStreamWaitEvent(st, ctx->join[g], 0);
         }
+        if (lists) cudaStreamWaitEvent(st, ctx->list_done, 0);
         cudaEventRecord(c.ev[2], st);
         if ((rc = launch_sweep(a, st))) return cuda_fail(ctx, rc, "K3 launch");
         cudaEventRecord(c.ev[3], st);
