@@ -297,3 +297,41 @@ def test_max_buckets_one_million(gpu):
     assert r.feasible
     e_all, _ = memory_footprint(layers, list(r.strategies), 8, 1, 1, 4.0)
     assert e_all <= budget
+
+
+def _wide_class_problems(rng, n_dev, count, max_strats):
+    """Stage searches with 9-10 (data, tp) classes (the K > 8 kernels): 256 / 512 devices,
+    P = 1, a random subset of at most `max_strats` strategies that keeps every class."""
+    from paper_2307_02031_b200.costs import EvalContext
+    from paper_2307_02031_b200.specs import ClusterSpec, CostProfile, LayerSpec, ModelSpec
+    from paper_2307_02031_b200.strategies import StrategySet
+    pool = list(prune_dp_sdp(enumerate_strategies(n_dev, 1)))
+    by_cls = {}
+    for i, s in enumerate(pool):
+        by_cls.setdefault((s.data_degree, s.tp_degree), []).append(i)
+    probs = []
+    for _ in range(count):
+        keep = {rng.choice(v) for v in by_cls.values()}          # one of every class
+        rest = [i for i in range(len(pool)) if i not in keep]
+        extra = rng.randint(0, max(0, min(max_strats, len(pool)) - len(keep)))
+        chosen = sorted(keep | set(rng.sample(rest, extra)))
+        sset = StrategySet(n_dev, tuple(pool[i] for i in chosen))
+        nl = rng.choice((3, 6, 12, 20, 24))
+        layers = [LayerSpec(i, rng.choice("ab"), 16 * rng.randint(1, 8), 16 * rng.randint(1, 4),
+                            16 * rng.randint(0, 8), rng.uniform(0.001, 0.05)) for i in range(nl)]
+        cl = ClusterSpec(n_dev, 1, n_dev, rng.choice((0.5, 1.0, 2.0)), rng.choice((0.25, 0.5)), rng.choice((1.0, 1.3)))
+        ctx = EvalContext(ModelSpec("w", tuple(layers), 4.0), cl, CostProfile())
+        gran = rng.choice((16, 32, 64))
+        budget = float(gran * rng.randint(20, 3000))
+        probs.append(StageProblem(layers, budget, sset, n_dev, gran, ctx, stage_index=1, n_micro=rng.randint(1, 4),
+                                  fuse_identical=rng.random() < 0.3, collect_frontier=rng.random() < 0.3))
+    return probs
+
+
+@pytest.mark.parametrize("n_dev,max_strats", [(256, 60), (512, 70)])
+def test_wide_class_counts_vs_oracle(gpu, n_dev, max_strats):
+    """K = 9-10 classes: the K > 8 instantiations of K2a / K2b and (with <= 60 strategies)
+    the second-step kernel K2s, bit-exact against the oracle."""
+    probs = _wide_class_problems(random.Random(n_dev), n_dev, 24, max_strats)
+    res = _compare_with_oracle(probs)
+    assert int(res["feasible"].sum()) > 0
