@@ -748,9 +748,14 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
             c.group_lo[g] = s;
             while (s < np && problem_group(b->hp[c.probs[s]].K, b->problems[c.probs[s]].flags, b->hp[c.probs[s]].U) == g) ++s;
             c.group_lo[g + 1] = s;
+            // problems with U > u, from a histogram of U (suffix sums)
             c.n_active[g].assign(c.Umax + 1, 0);
-            for (int x = c.group_lo[g]; x < s; ++x)
-                for (int u = 0; u < b->hp[c.probs[x]].U && u <= c.Umax; ++u) c.n_active[g][u]++;
+            std::vector<int> hist(c.Umax + 2, 0);
+            for (int x = c.group_lo[g]; x < s; ++x) hist[std::min(b->hp[c.probs[x]].U, c.Umax + 1)]++;
+            for (int u = c.Umax, above = hist[c.Umax + 1]; u >= 0; --u) {
+                c.n_active[g][u] = above;                // problems with U > u
+                above += hist[u];
+            }
         }
         td[2] += now_ms() - tq; tq = now_ms();
         // K2 tile -> problem map: only the collapsed-DP step (K2c) still walks 2048-row tiles
