@@ -17,7 +17,6 @@
 #include <chrono>
 #include <map>
 #include <memory>
-#include <thread>
 #include <tuple>
 #include <unordered_map>
 
@@ -591,23 +590,15 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
     std::string first_msg;
     double t_head = 0.0;
     {
-        // checks and shared strategy / unit records in input order, then the per-problem
-        // rest on host threads; the first failing problem (in input order) names the error
+        // argument checks, shared strategy / unit records, sizes; the first failing problem
+        // (in input order) names the error.  Serial: host threads lost more to spawning and
+        // cache-line traffic on the problem records than they saved (measured, v78)
         std::vector<std::string> msgs(n_problems);
-        for (int64_t i = 0; i < n_problems; ++i) prepare_problem(*b, (int)i, &msgs[i]);
-        t_head = now_ms();
-        const int nt = n_problems >= 4096 ? (int)std::min<unsigned>(8u, std::max(1u, std::thread::hardware_concurrency())) : 1;
-        auto tail = [&](int t) {
-            for (int64_t i = t; i < n_problems; i += nt) prepare_problem_tail(*b, (int)i, &msgs[i]);
-        };
-        if (nt > 1) {
-            std::vector<std::thread> pool;
-            for (int t = 1; t < nt; ++t) pool.emplace_back(tail, t);
-            tail(0);
-            for (auto &th : pool) th.join();
-        } else {
-            tail(0);
+        for (int64_t i = 0; i < n_problems; ++i) {
+            prepare_problem(*b, (int)i, &msgs[i]);
+            prepare_problem_tail(*b, (int)i, &msgs[i]);
         }
+        t_head = now_ms();
         for (int64_t i = 0; i < n_problems; ++i)
             if (b->hp[i].status != GBMW_OK) { first_err = b->hp[i].status; first_msg = msgs[i]; break; }
     }
