@@ -880,7 +880,7 @@ __device__ __forceinline__ void second_eval(const ChunkArgs &a, SecondSmem &sm, 
 }
 
 template <int GROUP>
-__global__ void __launch_bounds__(kSecondThreads, GROUP <= 1 ? 3 : 1) k_dp_second(ChunkArgs a, int p_lo, int p_n) {
+__global__ void __launch_bounds__(kSecondThreads, GROUP <= 1 ? 2 : 1) k_dp_second(ChunkArgs a, int p_lo, int p_n) {
     extern __shared__ __align__(16) unsigned char second_raw[];
     SecondSmem &sm = *reinterpret_cast<SecondSmem *>(second_raw);
     const int q = p_lo + (int)blockIdx.x;
