@@ -255,6 +255,12 @@ int  gbmw_seed_partitions_device(gbmw_ctx *ctx, const gbmw_layer *layers, int32_
                                  int32_t max_stages, int32_t *out_sizes);
 /* CPython >= 3.12 built-in sum() of floats (Neumaier), as the reference folds sums. */
 double gbmw_py_sum(const double *x, int32_t n);
+/* Select the host interpreter's sum() semantics for every planner fold (gbmw_py_sum, the
+ * balance degrees of balance.py:62-77 in the partition hill climb): 1 = CPython >= 3.12
+ * (Neumaier-compensated, the default), 0 = CPython <= 3.11 (left-to-right addition).
+ * gbmw_seed_partitions_device supports only 1 (GBMW_ENOTSUP otherwise). */
+int gbmw_set_sum_semantics(int32_t neumaier);
+int gbmw_sum_semantics(void);
 const char *gbmw_planner_last_error(void);
 
 #ifdef __cplusplus

@@ -9,6 +9,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import sys
 import threading
 from pathlib import Path
 
@@ -66,6 +67,7 @@ EXPORTS = (
     "gbmw_transform_cost", "gbmw_comm_breakdown", "gbmw_cost_tables", "gbmw_search_batch", "gbmw_batch_create",
     "gbmw_batch_run", "gbmw_batch_fetch", "gbmw_batch_timing", "gbmw_ctx_last_timing", "gbmw_batch_destroy",
     "gbmw_partition_costs", "gbmw_init_partition", "gbmw_seed_for", "gbmw_seed_partitions", "gbmw_seed_partitions_device", "gbmw_py_sum", "gbmw_planner_last_error",
+    "gbmw_set_sum_semantics", "gbmw_sum_semantics",
 )
 
 _lib = None
@@ -115,14 +117,20 @@ def lib() -> ctypes.CDLL:
             L.gbmw_py_sum.argtypes = [vp, i32]
             L.gbmw_py_sum.restype = ctypes.c_double
             L.gbmw_planner_last_error.restype = ctypes.c_char_p
+            L.gbmw_set_sum_semantics.argtypes = [i32]
             for name in EXPORTS:
                 getattr(L, name).restype = getattr(L, name).restype or ctypes.c_int
+            # the planner's folds follow this interpreter's built-in sum(): Neumaier-compensated
+            # since CPython 3.12, plain left-to-right before (the reference's balance.py:62-77,125)
+            L.gbmw_set_sum_semantics(1 if sys.version_info >= (3, 12) else 0)
             _lib = L
     return _lib
 
 
 def ptr(a: np.ndarray | None):
-    return None if a is None else ctypes.c_void_p(a.ctypes.data)
+    """Address of ``a`` for a ctypes call; the returned pointer object holds a reference to
+    the array, so a temporary passed inline stays alive for the duration of the call."""
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
 
 
 def global_error() -> str:

@@ -131,8 +131,9 @@ def evaluate_partition(model, partition: PipelinePartition, per_layer_strategies
     strats = _native.strategies_array(list(per_layer_strategies))
     out = np.zeros(3 * len(sizes), dtype=np.float64)
     layers = _layers(model, ctx.profile)
+    env = _env(ctx)
     rc = _native.lib().gbmw_partition_costs(_native.ptr(layers), len(layers), _native.ptr(strats),
-                                            _native.ptr(sizes), len(sizes), _native.ptr(_env(ctx)),
+                                            _native.ptr(sizes), len(sizes), _native.ptr(env),
                                             int(micro_batch), int(n_micro), _native.ptr(out))
     if rc != _native.OK:
         _planner_error(rc)
@@ -147,8 +148,9 @@ def _init_partition(model, num_stages, seed_strategies, micro_batch, n_micro, ct
     strats = _native.strategies_array(list(seed_strategies))
     out = np.zeros(num_stages, dtype=np.int32)
     layers = _layers(model, ctx.profile)
+    env = _env(ctx)
     rc = _native.lib().gbmw_init_partition(_native.ptr(layers), len(layers), _native.ptr(strats), int(num_stages),
-                                           _native.ptr(_env(ctx)), int(micro_batch), int(n_micro),
+                                           _native.ptr(env), int(micro_batch), int(n_micro),
                                            0 if objective == "memory" else 1, _native.ptr(out))
     if rc != _native.OK:
         _planner_error(rc)
@@ -170,7 +172,8 @@ def _seed_and_partition(model, ctx, n_devices, pp_degree, micro_batch, n_micro):
     seed = np.zeros(1, dtype=_native.STRATEGY_DT)
     sizes = np.zeros(pp_degree, dtype=np.int32)
     layers = _layers(model, ctx.profile)
-    rc = _native.lib().gbmw_seed_for(_native.ptr(layers), len(layers), _native.ptr(_env(ctx)), int(n_devices),
+    env = _env(ctx)
+    rc = _native.lib().gbmw_seed_for(_native.ptr(layers), len(layers), _native.ptr(env), int(n_devices),
                                      int(pp_degree), int(micro_batch), int(n_micro),
                                      float(ctx.cluster.mem_budget_bytes), _native.ptr(seed), _native.ptr(sizes))
     if rc != _native.OK:

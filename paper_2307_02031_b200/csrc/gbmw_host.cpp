@@ -1275,6 +1275,8 @@ extern "C" int gbmw_seed_partitions_device(gbmw_ctx *ctx, const gbmw_layer *laye
     if (!ctx || !layers || !env || !pp_degree || !micro_batch || !n_micro || !out_sizes || n_cells < 0 ||
         max_stages < 1 || n_layers < 1)
         return set_err(ctx ? &ctx->err : nullptr, GBMW_EINVAL, "bad arguments");
+    if (!gbmw_sum_semantics())
+        return set_err(&ctx->err, GBMW_ENOTSUP, "device seed partitions implement CPython >= 3.12 sum() only");
     if (n_cells == 0) return GBMW_OK;
     cudaSetDevice(ctx->device);
     cudaStream_t st = ctx->stream;

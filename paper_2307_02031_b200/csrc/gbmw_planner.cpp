@@ -28,11 +28,21 @@ int perr(int code, const std::string &m) {
     return code;
 }
 
+// Which sum() the host interpreter runs: 1 = CPython >= 3.12 (Neumaier-compensated),
+// 0 = CPython <= 3.11 (plain left-to-right addition).  Set once at import by the Python
+// package (gbmw_set_sum_semantics) from sys.version_info.
+std::atomic<int> g_neumaier{1};
+
 // CPython >= 3.12 sum() of a float sequence with start 0 (int): the first item is
-// taken as is (0 + x == x), the rest are Neumaier-compensated.
+// taken as is (0 + x == x), the rest are Neumaier-compensated.  Under the <= 3.11
+// semantics the loop is plain addition (the compensation term stays 0).
 double py_sum(const double *x, int n) {
     if (n <= 0) return 0.0;
     double f = x[0], c = 0.0;
+    if (!g_neumaier.load(std::memory_order_relaxed)) {
+        for (int i = 1; i < n; ++i) f = f + x[i];
+        return f;
+    }
     for (int i = 1; i < n; ++i) {
         const double t = f + x[i];
         if (std::fabs(f) >= std::fabs(x[i])) c += (f - t) + x[i];
@@ -148,6 +158,7 @@ struct AlphaCache {
     }
 
     static void step(double &f, double &c, double x) {           // py_sum's loop body
+        if (!g_neumaier.load(std::memory_order_relaxed)) { f = f + x; return; }
         const double t = f + x;
         if (std::fabs(f) >= std::fabs(x)) c += (f - t) + x;
         else c += (x - t) + f;
@@ -432,6 +443,13 @@ extern "C" int gbmw_seed_for(const gbmw_layer *layers, int32_t n_layers, const g
 }
 
 extern "C" double gbmw_py_sum(const double *x, int32_t n) { return py_sum(x, n); }
+
+extern "C" int gbmw_set_sum_semantics(int32_t neumaier) {
+    g_neumaier.store(neumaier ? 1 : 0);
+    return GBMW_OK;
+}
+
+extern "C" int gbmw_sum_semantics(void) { return g_neumaier.load(); }
 
 // gbmw_seed_for for many (pp_degree, micro_batch, n_micro) cells of one model and cluster,
 // host threads over the cells (galvatron_base seeds every (batch, degree) cell of a batch

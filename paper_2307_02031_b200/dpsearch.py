@@ -76,8 +76,18 @@ def _check(p: StageProblem):
 _strat_arrays: dict = {}
 
 
+def _frozen(strategies) -> bool:
+    """True for containers whose contents cannot change under the same object: a tuple, or a
+    StrategySet (frozen dataclass) holding a tuple (parapilot's and ours)."""
+    return isinstance(strategies, tuple) or isinstance(getattr(strategies, "strategies", None), tuple)
+
+
 def _strategies_array_cached(strategies, strat_list):
-    """Strategy records of an immutable strategy set, built once per set object."""
+    """Strategy records of an immutable strategy set, built once per set object.  Mutable
+    containers (a list the caller may change between calls) are re-read every call, as the
+    reference re-reads them (dpsearch.py:42-43)."""
+    if not _frozen(strategies):
+        return _native.strategies_array(strat_list)
     hit = _strat_arrays.get(id(strategies))
     if hit is None or hit[0] is not strategies:
         if len(_strat_arrays) > 256:
@@ -109,7 +119,8 @@ class _Marshal:
         return hit
 
     def strat_range(self, strategies, strat_list) -> int:
-        key = id(strategies)
+        # a mutable container is keyed on its elements as they are now
+        key = id(strategies) if _frozen(strategies) else tuple(id(x) for x in strat_list)
         hit = self.strat_ranges.get(key)
         if hit is None or hit[1] is not strategies:
             hit = (len(self.strats), strategies)

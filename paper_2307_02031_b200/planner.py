@@ -136,9 +136,25 @@ def _layer_index(model):
     return hit[1]
 
 
-def _search_slices(cells, ctx, opts):
+class FailedOutcome:
+    """A cell whose search raised inside the native pass (a speculative window's cell): the
+    exception is raised only if the reference's sequential order reaches the cell."""
+
+    cost = INF
+
+    def __init__(self, code: int, msg: str, n_micro: int):
+        self.code, self.msg, self.n_micro = code, msg, n_micro
+
+    def raise_(self):
+        from . import _native
+        _native.raise_status(self.code, self.msg)
+
+
+def _search_slices(cells, ctx, opts, defer_errors=False):
     """galvatron_search for cells whose stages are slices of ctx.model: one flat problem
-    table over a single copy of the model's layers, no per-stage Python objects."""
+    table over a single copy of the model's layers, no per-stage Python objects.  With
+    ``defer_errors`` a cell whose stage search fails yields a ``FailedOutcome`` instead of
+    raising for the whole batch."""
     from . import _native
     from .dpsearch import MAX_BUCKETS, _Marshal, run_native_batch
     gran = opts.granularity_bytes
@@ -148,6 +164,7 @@ def _search_slices(cells, ctx, opts):
     flags = _native.STAGE_COST | (_native.FUSE if opts.fuse_identical else 0) | \
         (_native.APPROX if opts.approx_prev else 0)
     rows, metas = [], []
+    rc = _native.OK
     for budget, ranges, n_devices, batch, pp in cells:
         m = init_microbatch_num(batch, pp, opts.microbatch_cap_factor, opts.min_micro_size)
         micro = batch // m
@@ -178,9 +195,21 @@ def _search_slices(cells, ctx, opts):
         rc, msg, res, plans, _ = run_native_batch(layers, strats_arr, envs, probs)
         if rc != _native.OK:
             bad = np.flatnonzero(res["status"] != 0)
-            _native.raise_status(int(res["status"][bad[0]]) if len(bad) else rc, msg)
+            if not (defer_errors and len(bad)):
+                _native.raise_status(int(res["status"][bad[0]]) if len(bad) else rc, msg)
+            first_bad = int(bad[0])
         plan_off = np.concatenate(([0], np.cumsum(probs["n_layers"])))
     for m, r0, r1, strats in metas:
+        if r0 is not None and rc != _native.OK:
+            st = res["status"][r0:r1]
+            k = np.flatnonzero(st != 0)
+            # the reference raises inside the first failing stage's dp_search, after the stages
+            # before it were searched; a stage that is infeasible earlier ends the cell first
+            if len(k) and res["feasible"][r0:r0 + int(k[0])].all():
+                code = int(st[k[0]])
+                out.append(FailedOutcome(code, msg if r0 + int(k[0]) == first_bad else
+                                         f"stage search failed (status {code})", m))
+                continue
         if r0 is None or not res["feasible"][r0:r1].all():      # first infeasible stage (planner.py:159-160)
             out.append(SearchOutcome(cost=INF, strategies=None, stage_costs=None, n_micro=m))
             continue
@@ -192,8 +221,13 @@ def _search_slices(cells, ctx, opts):
     return out
 
 
-def galvatron_search_batch(cells: Sequence[tuple], ctx: EvalContext, opts: PlannerOptions = PlannerOptions()):
-    """Many ``galvatron_search(budget, stages, n_devices, batch, pp_degree)`` calls, one device pass."""
+def galvatron_search_batch(cells: Sequence[tuple], ctx: EvalContext, opts: PlannerOptions = PlannerOptions(),
+                           defer_errors: bool = False):
+    """Many ``galvatron_search(budget, stages, n_devices, batch, pp_degree)`` calls, one device pass.
+
+    With ``defer_errors`` (the speculative drivers) a failing cell comes back as a
+    ``FailedOutcome`` whose ``raise_()`` the caller invokes when its sequential order reaches
+    it; otherwise the first failing cell raises for the whole batch."""
     sliced = []
     for budget, stages, n_devices, batch, pp in cells:
         ranges = _stage_ranges(ctx.model, stages)
@@ -201,7 +235,7 @@ def galvatron_search_batch(cells: Sequence[tuple], ctx: EvalContext, opts: Plann
             break
         sliced.append((budget, ranges, n_devices, batch, pp))
     else:
-        return _search_slices(sliced, ctx, opts)
+        return _search_slices(sliced, ctx, opts, defer_errors)
     problems, spans, metas = [], [], []
     for budget, stages, n_devices, batch, pp in cells:
         m = init_microbatch_num(batch, pp, opts.microbatch_cap_factor, opts.min_micro_size)
@@ -314,7 +348,20 @@ def _base_cells_window(model, ctx, batches, opts):
     # one native call over host threads: the hill climb is a chain of dependent fp64 folds per
     # cell, as fast on host cores as on a warp (gbmw_seed_partitions_device: bit-identical,
     # 6.8 vs 5.2 ms for a GPT-3-96 window) and it overlaps the device pass
-    parts = seed_partitions(model, ctx, cluster.n_devices, cells)
+    try:
+        parts = seed_partitions(model, ctx, cluster.n_devices, cells)
+    except Exception:
+        if len(batches) == 1:
+            raise
+        # a batch size of the window failed: seed per batch size, so that the error surfaces
+        # only when the sequential sweep reaches that batch size (the reference's order)
+        per = []
+        for b in batches:
+            try:
+                per.append(_base_cells_window(model, ctx, [b], opts)[0])
+            except Exception as e:          # re-raised by galvatron_base if it gets here
+                per.append(e)
+        return per
     out = {b: [] for b in batches}
     for (b, p), part in zip(pairs, parts):
         out[b].append((p, part, (cluster.mem_budget_bytes, partition_layers(model, part), cluster.n_devices, b, p)))
@@ -338,6 +385,16 @@ def _window_executor():
     return _window_pool
 
 
+def _drain(fut):
+    """Stop the speculative next-window preparation before the driver returns: cancel it if
+    it has not started, else wait for it (its result is discarded)."""
+    if fut is not None and not fut.cancel():
+        try:
+            fut.result()
+        except Exception:
+            pass
+
+
 def galvatron_base(model, cluster, profile, opts: PlannerOptions = PlannerOptions()) -> Plan:
     """Algorithm 1: raise the batch until no pipeline degree fits (planner.py:231-277)."""
     ctx = EvalContext(model=model, cluster=cluster, profile=profile)
@@ -352,17 +409,31 @@ def galvatron_base(model, cluster, profile, opts: PlannerOptions = PlannerOption
         # the stop rule ends the sweep here)
         nxt = _window_executor().submit(_base_cells_window, model, ctx, chunks[ci + 1], opts) \
             if ci + 1 < len(chunks) else None
-        flat = [c[2] for cells in per_batch for c in cells]
-        outcomes = galvatron_search_batch(flat, ctx, opts)
+        failed = next((i for i, cells in enumerate(per_batch) if isinstance(cells, Exception)), None)
+        if failed is not None:          # the searches stop before the batch size whose seeding failed
+            chunk, per_batch = chunk[:failed + 1], per_batch[:failed + 1]
+        flat = [c[2] for cells in per_batch if not isinstance(cells, Exception) for c in cells]
+        try:
+            outcomes = galvatron_search_batch(flat, ctx, opts, defer_errors=True)
+        except BaseException:
+            _drain(nxt)
+            raise
         k = 0
         for batch, cells in zip(chunk, per_batch):
+            if isinstance(cells, Exception):
+                _drain(nxt)
+                raise cells
             cell_best = None
             for p, part, _ in cells:
                 outcome = outcomes[k]
                 k += 1
+                if isinstance(outcome, FailedOutcome):   # the reference's call raises here
+                    _drain(nxt)
+                    outcome.raise_()
                 if outcome.cost < INF and (cell_best is None or outcome.cost < cell_best[0]):
                     cell_best = (outcome.cost, p, part, outcome)
             if cell_best is None:
+                _drain(nxt)
                 if best is None:
                     raise InfeasiblePlanError(f"no feasible plan at the smallest batch size {batch}",
                                               diagnostics=_infeasibility_diagnostics(model, ctx, batch, opts))

@@ -82,3 +82,53 @@ def test_layer_memory_errors():
     from paper_2307_02031_b200.errors import DivisibilityError
     with pytest.raises(DivisibilityError):
         C.layer_memory(layer, s, 3, 1, 1, 4.0)
+
+
+def test_sum_semantics_follow_the_interpreter():
+    """The planner's folds use this interpreter's sum(): Neumaier since CPython 3.12, plain
+    left-to-right before.  Both modes are selectable and reproduce the matching Python fold."""
+    import sys
+    L = _native.lib()
+    assert L.gbmw_sum_semantics() == (1 if sys.version_info >= (3, 12) else 0)
+    x = np.array([1e16, 1.0, -1e16, 3.0, 0.1, 0.2], dtype=np.float64)
+    naive = 0
+    for v in x.tolist():
+        naive = naive + v
+    saved = L.gbmw_sum_semantics()
+    try:
+        L.gbmw_set_sum_semantics(0)
+        assert L.gbmw_py_sum(_native.ptr(x), len(x)).hex() == float(naive).hex()
+        L.gbmw_set_sum_semantics(1)
+        got = L.gbmw_py_sum(_native.ptr(x), len(x))
+        if sys.version_info >= (3, 12):
+            assert got.hex() == sum(x.tolist()).hex()
+        assert got != naive                      # the compensated sum keeps the 1.0
+    finally:
+        L.gbmw_set_sum_semantics(saved)
+
+
+def test_ptr_keeps_temporaries_alive():
+    """_native.ptr of a temporary holds the array until the pointer object is dropped."""
+    import gc
+    p = _native.ptr(np.full(8, 7.0))
+    gc.collect()
+    junk = [np.zeros(8) for _ in range(64)]     # would reuse a freed 64-byte buffer
+    assert ctypes.cast(p, ctypes.POINTER(ctypes.c_double))[3] == 7.0
+    del junk
+
+
+def test_mutable_strategy_lists_are_not_cached_by_identity():
+    from paper_2307_02031_b200 import dpsearch as D
+    sset = ST.enumerate_pruned(8, 1)
+    assert D._frozen(sset) and D._frozen(tuple(sset))
+    lst = list(sset)
+    assert not D._frozen(lst)
+    a = D._strategies_array_cached(lst, lst)
+    lst.reverse()
+    b = D._strategies_array_cached(lst, lst)
+    assert len(a) == len(b) and not np.array_equal(a, b)
+    m = D._Marshal()
+    r0 = m.strat_range(lst, list(lst))
+    lst.pop()
+    r1 = m.strat_range(lst, list(lst))
+    assert r0 != r1 and len(m.strats[r1]) == len(lst)
