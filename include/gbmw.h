@@ -19,6 +19,8 @@
  *                            (costs.py:322-352) of each returned plan
  *   gbmw_batch_*          <- the same, split into prepare / run / fetch so the device
  *                            part can be timed with inputs resident in HBM
+ *   gbmw_brute_force      <- planner.brute_force_oracle (planner.py:344-449), the
+ *                            exhaustive (P, partition, assignment, m) scan, on the device
  *
  * Conventions: all functions return int status (0 = GBMW_OK, < 0 = error);
  * no C++ exception crosses the ABI; the message of the last failure is
@@ -262,6 +264,32 @@ double gbmw_py_sum(const double *x, int32_t n);
 int gbmw_set_sum_semantics(int32_t neumaier);
 int gbmw_sum_semantics(void);
 const char *gbmw_planner_last_error(void);
+
+/* ---- exhaustive oracle (planner.py:344-449) ---- */
+
+/* OracleResult (planner.py:344-351) + scan statistics. */
+typedef struct gbmw_oracle_result {
+    double  cost;              /* +inf when nothing is feasible */
+    int32_t feasible;
+    int32_t pp_degree;
+    int32_t n_micro;
+    int32_t n_stages;          /* entries of out_partition in use */
+    double  combos;            /* (partition, assignment) pairs scanned over all cells */
+    double  device_ms;         /* device time of the scan (CUDA events on the ctx stream) */
+} gbmw_oracle_result;
+
+/* brute_force_oracle(model, cluster, profile, batch) on the device of ctx: the minimum of
+ * pipeline_cost over every power-of-two pipeline degree P <= n_layers, micro-batch count m
+ * dividing batch, ordered partition of the layers into P stages and assignment of the
+ * usable strategies of prune_dp_sdp(enumerate_strategies(N, P)) to the layers, first
+ * minimum in the reference's loop order.  budget_bytes = ClusterSpec.mem_budget_bytes.
+ * out_partition[n_layers]: stage sizes (n_stages used); out_choice[n_layers]: per layer the
+ * index into the pruned strategy set of pp_degree.  max_combos caps the scan (0: 2^44);
+ * larger scans return GBMW_ENOTSUP, as do more than 24 layers.  The reference's own
+ * size guards (max_layers / max_devices) are applied by the Python wrapper. */
+int gbmw_brute_force(gbmw_ctx *ctx, const gbmw_layer *layers, int32_t n_layers, const gbmw_env *env,
+                     int64_t batch, double budget_bytes, double max_combos,
+                     int32_t *out_partition, int32_t *out_choice, gbmw_oracle_result *out);
 
 #ifdef __cplusplus
 }

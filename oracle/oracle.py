@@ -48,6 +48,8 @@ def lib():
         L.or_layer_memory.argtypes = [vp, vp, i64, ctypes.c_int, ctypes.c_int, ctypes.c_double, vp]
         L.or_transform.argtypes = [vp, vp, vp, i64, vp]
         L.or_transform.restype = ctypes.c_double
+        L.or_brute_force.argtypes = [vp, ctypes.c_int, vp, i64, ctypes.c_double, ctypes.c_int, vp, vp, vp]
+        L.or_brute_force.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -89,3 +91,18 @@ def cell(layer_rec, strat_rec, env_rec, micro, stage, n_micro):
     L.or_layer_memory(_p(layer_rec), _p(strat_rec), int(micro), int(stage), int(n_micro),
                       float(env_rec["ms"][0] if env_rec.shape else env_rec["ms"]), m)
     return (t.value, tns.value, m[0], m[1], m[2])
+
+
+def brute_force(layers, env, batch: int, budget: float, neumaier: bool = True):
+    """planner.brute_force_oracle restated (or_brute_force): (cost, feasible, P, m, partition, choice)."""
+    L = len(layers)
+    part = np.zeros(max(L, 1), dtype=np.int32)
+    choice = np.full(max(L, 1), -1, dtype=np.int32)
+    out = np.zeros(5, dtype=np.float64)
+    rc = lib().or_brute_force(_p(layers), L, _p(env), int(batch), float(budget), int(neumaier), _p(part),
+                              _p(choice), _p(out))
+    if rc != 0:
+        raise ValueError("or_brute_force: bad input")
+    n_st = int(out[4])
+    return (float(out[0]), bool(out[1]), int(out[2]), int(out[3]), tuple(int(x) for x in part[:n_st]),
+            tuple(int(x) for x in choice[:L]) if out[1] else ())

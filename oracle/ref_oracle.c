@@ -19,6 +19,9 @@
  *                       numpy min/argmax tie semantics, ranked sweep with per-candidate
  *                       reconstruct and E_all check (memory_footprint costs.py:289-319)
  *   or_stage_cost       costs.py:322-352
+ *   or_brute_force      planner.py:354-449 (_compositions, brute_force_oracle): every
+ *                       (P, m, partition, assignment) in the reference's loop order,
+ *                       pipeline_cost costs.py:355-362 with CPython's sum()
  *
  * It deliberately does NOT use the device formulation (class reduction, parallel
  * sweep): it is the reference's own sequential algorithm, so agreement with the
@@ -554,4 +557,123 @@ int or_search_many(const gbmw_layer *layers, const gbmw_strategy *strats, const 
     free(plan_off);
     free(front_off);
     return used;
+}
+
+/* ------------------------------------------------------------------ brute_force_oracle */
+/* CPython builtin sum() of floats from the int 0: Neumaier-compensated since 3.12
+ * (neumaier = 1), plain left-to-right before. */
+static double or_py_sum(const double *x, int n, int neumaier) {
+    if (n <= 0) return 0.0;
+    double f = 0.0 + x[0], c = 0.0;
+    for (int i = 1; i < n; ++i) {
+        if (!neumaier) { f = f + x[i]; continue; }
+        double t = f + x[i];
+        if (fabs(f) >= fabs(x[i])) c += (f - t) + x[i];
+        else c += (x[i] - t) + f;
+        f = t;
+    }
+    if (neumaier && c != 0.0 && isfinite(c)) f += c;
+    return f;
+}
+
+/* next ordered split of n layers into p nonempty stages after `sz` (planner.py:354-361:
+ * heads ascending, recursively); returns 0 when `sz` was the last one */
+static int next_composition(int *sz, int p) {
+    /* lexicographic successor among compositions with the same sum and part count */
+    for (int i = p - 2; i >= 0; --i) {
+        int rest = 0;
+        for (int k = i + 1; k < p; ++k) rest += sz[k];
+        if (rest - 1 >= p - 1 - i) {            /* head i can grow by one */
+            sz[i] += 1;
+            rest -= 1;
+            for (int k = i + 1; k < p - 1; ++k) { sz[k] = 1; rest -= 1; }
+            sz[p - 1] = rest;
+            return 1;
+        }
+    }
+    return 0;
+}
+
+/* planner.py:364-449.  out_partition / out_choice: n_layers entries (choice = index into
+ * prune_dp_sdp(enumerate_strategies(N, P))).  out[0] = cost (+inf if none), out[1] =
+ * feasible, out[2] = P, out[3] = m, out[4] = stages.  Returns 0, or -1 on bad input. */
+int or_brute_force(const gbmw_layer *layers, int n_layers, const gbmw_env *env, int64_t batch, double budget,
+                   int neumaier, int32_t *out_partition, int32_t *out_choice, double out[5]) {
+    out[0] = INFINITY; out[1] = 0; out[2] = 0; out[3] = 0; out[4] = 0;
+    if (n_layers < 1 || n_layers > 24 || batch < 1) return -1;
+    const int L = n_layers;
+    gbmw_strategy sset[512];
+    for (int64_t P = 1; P <= env->n_devices; P *= 2) {
+        if (P > L) continue;
+        int ns = or_enumerate(env->n_devices, P, 1, sset, 512);
+        if (ns < 0) return -1;
+        for (int64_t m = 1; m <= batch; ++m) {
+            if (batch % m) continue;
+            int64_t micro = batch / m;
+            int cand[512], S = 0;
+            for (int i = 0; i < ns; ++i)
+                if (micro % data_deg(&sset[i]) == 0) cand[S++] = i;
+            if (!S) continue;
+            double *lt = malloc(sizeof(double) * L * S * 5);
+            double *lns = lt + L * S, *of = lt + 2 * L * S, *ob = lt + 3 * L * S, *oms = lt + 4 * L * S;
+            for (int l = 0; l < L; ++l)
+                for (int j = 0; j < S; ++j) {
+                    double mm[3];
+                    or_layer_times(&layers[l], &sset[cand[j]], micro, env, &lt[l * S + j], &lns[l * S + j]);
+                    or_layer_memory(&layers[l], &sset[cand[j]], micro, 1, 1, env->ms_bytes_per_param_byte, mm);
+                    of[l * S + j] = mm[0]; ob[l * S + j] = mm[1]; oms[l * S + j] = mm[2];
+                }
+            int sz[24];
+            for (int k = 0; k < P - 1; ++k) sz[k] = 1;
+            sz[P - 1] = L - (int)(P - 1);
+            do {
+                int choice[24] = {0};
+                for (;;) {                              /* itertools.product, last digit fastest */
+                    double st_t[24] = {0}, st_ns[24] = {0};
+                    int feasible = 1, start = 0;
+                    for (int si = 0; si < P && feasible; ++si) {
+                        const int stage_idx = si + 1;
+                        int64_t stash = P - stage_idx + 1;
+                        if (m < stash) stash = m;
+                        double t = 0.0, t_ns = 0.0, prefix_f = 0.0, peak = 0.0, total_ms = 0.0;
+                        const gbmw_strategy *prev = NULL;
+                        for (int li = start; li < start + sz[si]; ++li) {
+                            const gbmw_strategy *s = &sset[cand[choice[li]]];
+                            const int x = li * S + choice[li];
+                            double r = or_transform(&layers[li], prev, s, micro, env);
+                            t += lt[x] + r;
+                            t_ns += lns[x] + r;
+                            prefix_f += of[x] * (double)stash;
+                            peak = pymax(peak, prefix_f + ob[x]);
+                            total_ms += oms[x];
+                            prev = s;
+                        }
+                        if (stage_idx > 1) {
+                            double p2p = or_p2p(&layers[start], micro, (int)P, env);
+                            t += p2p;
+                            t_ns += p2p;
+                        }
+                        if (peak + total_ms > budget) feasible = 0;
+                        st_t[si] = t; st_ns[si] = t_ns;
+                        start += sz[si];
+                    }
+                    if (feasible) {
+                        double steady = st_ns[0];
+                        for (int si = 1; si < P; ++si) steady = pymax(steady, st_ns[si]);
+                        double cost = (double)(m - 1) * steady + or_py_sum(st_t, (int)P, neumaier);
+                        if (cost < out[0]) {
+                            out[0] = cost; out[1] = 1; out[2] = (double)P; out[3] = (double)m; out[4] = (double)P;
+                            for (int k = 0; k < P; ++k) out_partition[k] = sz[k];
+                            for (int l = 0; l < L; ++l) out_choice[l] = cand[choice[l]];
+                        }
+                    }
+                    int l = L - 1;
+                    while (l >= 0 && ++choice[l] == S) choice[l--] = 0;
+                    if (l < 0) break;
+                }
+            } while (next_composition(sz, (int)P));
+            free(lt);
+        }
+    }
+    return 0;
 }

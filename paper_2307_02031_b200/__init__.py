@@ -60,8 +60,10 @@ from .balance import (
 )
 from .planner import (
     GalvatronSearch,
+    OracleResult,
     Plan,
     PlannerOptions,
+    brute_force_oracle,
     evaluate_plan_document,
     galvatron_base,
     galvatron_search,
@@ -74,10 +76,10 @@ __version__ = "0.1.0"
 
 __all__ = [
     "BalanceReport", "ClusterSpec", "CostProfile", "DivisibilityError", "DpResult", "EvalContext",
-    "GalvatronSearch", "InfeasiblePlanError", "LayerCost", "LayerSpec", "ModelSpec", "NativeError",
+    "GalvatronSearch", "InfeasiblePlanError", "OracleResult", "LayerCost", "LayerSpec", "ModelSpec", "NativeError",
     "ParallelStrategy", "PipelinePartition", "Plan", "PlannerOptions", "SearchOutcome", "SpecError", "StageCost",
     "StageProblem", "StrategySet", "UnsupportedDeviceCountError", "adjust_partition", "backward_peak_bound",
-    "balance_degrees", "bi_objective_optimize", "build_decision_trees", "candidate_pp_degrees", "comm_time",
+    "balance_degrees", "bi_objective_optimize", "brute_force_oracle", "build_decision_trees", "candidate_pp_degrees", "comm_time",
     "compute_time", "count_strategies", "dp_search", "dp_search_batch", "enumerate_strategies",
     "evaluate_partition", "evaluate_plan_document", "galvatron_base", "galvatron_search",
     "galvatron_search_batch", "init_microbatch_num", "init_partition_memory_balanced",

@@ -61,13 +61,20 @@ class Timing(ctypes.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class OracleRecord(ctypes.Structure):
+    """gbmw_oracle_result (gbmw.h)."""
+    _fields_ = [("cost", ctypes.c_double), ("feasible", ctypes.c_int32), ("pp_degree", ctypes.c_int32),
+                ("n_micro", ctypes.c_int32), ("n_stages", ctypes.c_int32), ("combos", ctypes.c_double),
+                ("device_ms", ctypes.c_double)]
+
+
 EXPORTS = (
     "gbmw_version", "gbmw_abi_version", "gbmw_limits", "gbmw_ctx_create", "gbmw_ctx_destroy",
     "gbmw_last_error", "gbmw_last_error_global", "gbmw_ctx_stream", "gbmw_enumerate", "gbmw_layer_cost",
     "gbmw_transform_cost", "gbmw_comm_breakdown", "gbmw_cost_tables", "gbmw_search_batch", "gbmw_batch_create",
     "gbmw_batch_run", "gbmw_batch_fetch", "gbmw_batch_timing", "gbmw_ctx_last_timing", "gbmw_batch_destroy",
     "gbmw_partition_costs", "gbmw_init_partition", "gbmw_seed_for", "gbmw_seed_partitions", "gbmw_seed_partitions_device", "gbmw_py_sum", "gbmw_planner_last_error",
-    "gbmw_set_sum_semantics", "gbmw_sum_semantics",
+    "gbmw_set_sum_semantics", "gbmw_sum_semantics", "gbmw_brute_force",
 )
 
 _lib = None
@@ -118,6 +125,8 @@ def lib() -> ctypes.CDLL:
             L.gbmw_py_sum.restype = ctypes.c_double
             L.gbmw_planner_last_error.restype = ctypes.c_char_p
             L.gbmw_set_sum_semantics.argtypes = [i32]
+            L.gbmw_brute_force.argtypes = [vp, vp, i32, vp, i64, ctypes.c_double, ctypes.c_double, vp, vp,
+                                           ctypes.POINTER(OracleRecord)]
             for name in EXPORTS:
                 getattr(L, name).restype = getattr(L, name).restype or ctypes.c_int
             # the planner's folds follow this interpreter's built-in sum(): Neumaier-compensated

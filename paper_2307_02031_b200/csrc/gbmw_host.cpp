@@ -1389,3 +1389,199 @@ extern "C" int gbmw_cost_tables(gbmw_ctx *ctx, const gbmw_layer *layers, int64_t
     gbmw_batch_destroy(b);
     return rc;
 }
+
+// ----------------------------------------------------------------------------- brute-force oracle
+// planner.brute_force_oracle (planner.py:364-449) on the device (gbmw_brute.cu).  The host
+// walks the reference's loops — candidate_pp_degrees (strategies.py:213-219), P <= L, the
+// divisors m of the batch in ascending order, the usable strategies of the pruned set —
+// builds each cell's per-(layer, strategy) tables with the shared cost model and its
+// compositions in _compositions order (planner.py:354-361); the device scans every
+// (partition, assignment) of all cells; the host then keeps the first cell whose minimum
+// is strictly below the running best (planner.py:437).
+namespace {
+void compositions(int total, int parts, int start, uint32_t mask, std::vector<uint32_t> &out) {
+    // ordered splits of layers [start, start + total) into `parts` nonempty stages, heads
+    // ascending (the recursion order of planner.py:354-361); bit l marks a stage start
+    mask |= 1u << start;
+    if (parts == 1) { out.push_back(mask); return; }
+    for (int head = 1; head <= total - parts + 1; ++head)
+        compositions(total - head, parts - 1, start + head, mask, out);
+}
+}  // namespace
+
+extern "C" int gbmw_brute_force(gbmw_ctx *ctx, const gbmw_layer *layers, int32_t n_layers, const gbmw_env *env,
+                                int64_t batch, double budget_bytes, double max_combos, int32_t *out_partition,
+                                int32_t *out_choice, gbmw_oracle_result *out) {
+    if (!ctx || !layers || !env || !out || !out_partition || !out_choice)
+        return set_err(ctx ? &ctx->err : nullptr, GBMW_EINVAL, "null argument");
+    std::string *err = &ctx->err;
+    if (n_layers < 1) return set_err(err, GBMW_EEMPTY, "model must contain at least one layer");
+    if (n_layers > kBruteMaxLayers)
+        return set_err(err, GBMW_ENOTSUP, "brute force limited to " + std::to_string(kBruteMaxLayers) + " layers");
+    if (batch < 1) return set_err(err, GBMW_EMICRO, "batch must be >= 1, got " + std::to_string(batch));
+    if (!(budget_bytes >= 0.0) || budget_bytes >= kTwo53)
+        return set_err(err, GBMW_ERANGE, "budget_bytes must lie in [0, 2^53)");
+    if (!is_pow2(env->n_devices))
+        return set_err(err, GBMW_EINVAL, "device count must be a power of two, got " + std::to_string(env->n_devices));
+    for (int l = 0; l < n_layers; ++l) {
+        int rc = check_layer(layers[l], err);
+        if (rc) return rc;
+        if (!prod_exact(layers[l].bnd_bytes_per_sample, batch) || !prod_exact(layers[l].int_bytes_per_sample, batch) ||
+            !prod_exact(layers[l].bnd_bytes_per_sample * batch, std::max<int64_t>(1, std::min<int64_t>(env->n_devices, batch))))
+            return set_err(err, GBMW_ERANGE, "byte products of a layer reach 2^53; fp64 would not be exact");
+    }
+    const double cap = max_combos > 0.0 ? max_combos : 17592186044416.0;   // 2^44 assignments
+    const int L = n_layers;
+    struct CellHost {
+        int P, m;
+        std::vector<int32_t> cand;      // usable positions in the pruned strategy set
+    };
+    std::vector<CellHost> ch;
+    std::vector<BruteCell> cells;
+    std::vector<double> tab;
+    std::vector<uint32_t> comps;
+    double total = 0.0;
+    int64_t parts = 0;
+    for (int64_t P = 1; P <= env->n_devices; P *= 2) {
+        if (P > L) continue;
+        int32_t ns = 0;
+        int rc = gbmw_enumerate(env->n_devices, P, 1, nullptr, 0, &ns);
+        if (rc) return set_err(err, rc, g_err);
+        std::vector<gbmw_strategy> sset(ns);
+        gbmw_enumerate(env->n_devices, P, 1, sset.data(), ns, &ns);
+        const int64_t comp_off = (int64_t)comps.size();
+        compositions(L, (int)P, 0, 0u, comps);
+        const int64_t n_comp = (int64_t)comps.size() - comp_off;
+        for (int64_t m = 1; m <= batch; ++m) {
+            if (batch % m) continue;
+            const int64_t micro = batch / m;
+            CellHost c{(int)P, (int)m, {}};
+            std::vector<StratDeg> deg;
+            for (int i = 0; i < ns; ++i) {
+                const StratDeg d = strat_degrees(sset[i]);
+                if (micro % d.data == 0) { c.cand.push_back(i); deg.push_back(d); }
+            }
+            if (c.cand.empty()) continue;
+            const int S = (int)c.cand.size();
+            double spow = 1.0;
+            for (int l = 0; l < L - 1; ++l) spow *= S;
+            const double combos = (double)n_comp * spow * S;
+            total += combos;
+            if (total > cap)
+                return set_err(err, GBMW_ENOTSUP, "brute force over " + std::to_string(total) +
+                                                      "+ assignments exceeds the limit of " + std::to_string(cap));
+            BruteCell bc{};
+            bc.S = S; bc.L = L; bc.P = (int)P; bc.n_micro = (int)m;
+            bc.n_comp = n_comp; bc.spow = (int64_t)spow; bc.n_items = n_comp * bc.spow;
+            bc.comp_off = comp_off;
+            bc.tab_off = (int64_t)tab.size();
+            bc.budget = budget_bytes;
+            const int64_t LS = (int64_t)L * S;
+            tab.resize(tab.size() + 5 * LS + L + LS * S);
+            double *T = tab.data() + bc.tab_off;
+            for (int l = 0; l < L; ++l) {
+                for (int j = 0; j < S; ++j) {
+                    const gbmw_strategy &s = sset[c.cand[j]];
+                    double t, tns;
+                    layer_times(layers[l], s, deg[j], micro, *env, &t, &tns);
+                    const Mem mem = layer_memory(layers[l], deg[j], micro, 1, 1, env->ms_bytes_per_param_byte);
+                    T[0 * LS + l * S + j] = t;
+                    T[1 * LS + l * S + j] = tns;
+                    T[2 * LS + l * S + j] = mem.o_f;
+                    T[3 * LS + l * S + j] = mem.o_b;
+                    T[4 * LS + l * S + j] = mem.o_ms;
+                    for (int a = 0; a < S; ++a)
+                        T[5 * LS + L + ((int64_t)l * S + a) * S + j] =
+                            transform_cost(layers[l].bnd_bytes_per_sample, deg[a].data, deg[a].tp, deg[j].data,
+                                           deg[j].tp, micro, env->intra_island_bw);
+                }
+                T[5 * LS + l] = stage_p2p_time(layers[l].bnd_bytes_per_sample, micro, (int32_t)P, *env);
+            }
+            bc.tab_len = 5 * LS + L + LS * S;
+            bc.smem_doubles = bc.tab_len * 8 <= 200 * 1024 ? (int32_t)bc.tab_len : 0;
+            bc.n_parts = brute_blocks(bc.n_items);
+            bc.part_off = parts;
+            parts += bc.n_parts;
+            cells.push_back(bc);
+            ch.push_back(std::move(c));
+        }
+    }
+    out->cost = INFINITY;
+    out->feasible = 0;
+    out->pp_degree = out->n_micro = out->n_stages = 0;
+    out->combos = total;
+    out->device_ms = 0.0;
+    for (int l = 0; l < L; ++l) { out_partition[l] = 0; out_choice[l] = -1; }
+    const int nc = (int)cells.size();
+    if (nc == 0) return GBMW_OK;
+    cudaSetDevice(ctx->device);
+    cudaStream_t st = ctx->stream;
+    const size_t b_cells = (size_t)nc * sizeof(BruteCell), b_tab = tab.size() * 8, b_comp = comps.size() * 4;
+    const size_t b_part = (size_t)parts * sizeof(BrutePartial), b_out = (size_t)nc * sizeof(BrutePartial);
+    size_t o = 0;
+    const size_t o_cells = o; o = align_up(o + b_cells);
+    const size_t o_tab = o; o = align_up(o + b_tab);
+    const size_t o_comp = o; o = align_up(o + b_comp);
+    const size_t up = o;
+    const size_t o_part = o; o = align_up(o + b_part);
+    const size_t o_out = o; o = align_up(o + b_out);
+    char *dev = nullptr;
+    if (cudaMalloc(&dev, o) != cudaSuccess) return set_err(err, GBMW_ENOMEM, "cudaMalloc(brute force)");
+    std::vector<char> host(up);
+    std::memcpy(host.data() + o_cells, cells.data(), b_cells);
+    std::memcpy(host.data() + o_tab, tab.data(), b_tab);
+    std::memcpy(host.data() + o_comp, comps.data(), b_comp);
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaError_t ce = cudaMemcpyAsync(dev, host.data(), up, cudaMemcpyHostToDevice, st);
+    int rc = (int)ce;
+    if (rc == 0) cudaEventRecord(e0, st);
+    const int neu = gbmw_sum_semantics();
+    for (int i = 0; i < nc && rc == 0; ++i)
+        rc = launch_brute_cell(cells[i], (const BruteCell *)(dev + o_cells), (const double *)(dev + o_tab),
+                               (const uint32_t *)(dev + o_comp), (BrutePartial *)(dev + o_part), i, neu, st);
+    if (rc == 0)
+        rc = launch_brute_reduce((const BruteCell *)(dev + o_cells), nc, (const BrutePartial *)(dev + o_part),
+                                 (BrutePartial *)(dev + o_out), st);
+    if (rc == 0) cudaEventRecord(e1, st);
+    std::vector<BrutePartial> res(nc);
+    if (rc == 0) rc = (int)cudaMemcpyAsync(res.data(), dev + o_out, b_out, cudaMemcpyDeviceToHost, st);
+    if (rc == 0) rc = (int)cudaStreamSynchronize(st);
+    float ms = 0.f;
+    if (rc == 0) cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(dev);
+    if (rc) return cuda_fail(ctx, rc, "brute force");
+    out->device_ms = ms;
+    // strict `<` over the cells in the reference's loop order (planner.py:437)
+    int best = -1;
+    double best_cost = INFINITY;
+    for (int i = 0; i < nc; ++i) {
+        if (res[i].index < 0 || res[i].cost_bits == ~0ull) continue;
+        double c;
+        std::memcpy(&c, &res[i].cost_bits, 8);
+        if (c < best_cost) { best_cost = c; best = i; }
+    }
+    if (best < 0) return GBMW_OK;
+    const BruteCell &bc = cells[best];
+    int64_t idx = res[best].index;
+    const int64_t ci = idx / (bc.spow * bc.S);
+    int64_t digits = idx - ci * bc.spow * bc.S;
+    for (int l = L - 1; l >= 0; --l) {
+        const int64_t q = digits / bc.S;
+        out_choice[l] = ch[best].cand[(int)(digits - q * bc.S)];
+        digits = q;
+    }
+    const uint32_t mask = comps[bc.comp_off + ci];
+    int ns = 0, start = 0;
+    for (int l = 1; l <= L; ++l)
+        if (l == L || ((mask >> l) & 1u)) { out_partition[ns++] = l - start; start = l; }
+    out->cost = best_cost;
+    out->feasible = 1;
+    out->pp_degree = bc.P;
+    out->n_micro = bc.n_micro;
+    out->n_stages = ns;
+    return GBMW_OK;
+}

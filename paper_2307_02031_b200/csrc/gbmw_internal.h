@@ -225,6 +225,33 @@ int launch_sweep(const ChunkArgs &a, void *stream);
 int launch_approx_step(const ChunkArgs &a, int u, int64_t tile_base, int64_t n_tiles, unsigned long long *counter,
                        void *stream);
 int launch_finalize(const ChunkArgs &a, void *stream);
+// ---- exhaustive planner oracle (gbmw_brute.cu, planner.py:364-449)
+constexpr int kBruteMaxLayers = 24;          // layers of the model (digits held in registers)
+// One (pipeline degree, micro-batch count) cell: its tables start at tab_off in the
+// double table — lt, lns, of, ob, oms [L][S] (per layer, usable strategy; memory at
+// stage 1 / n_micro 1), p2p [L] (stage_p2p_time of a stage starting at layer l),
+// R [L][S][S] (transform_cost at layer l from strategy a to b) — and its compositions at
+// comp_off (bit l: layer l starts a stage).
+struct BruteCell {
+    int32_t S, L, P, n_micro;
+    int64_t n_comp, spow;         // compositions; S^(L-1)
+    int64_t n_items;              // n_comp * spow threads' worth of work
+    int64_t tab_off, tab_len, comp_off;
+    int64_t part_off;             // first block partial
+    int32_t n_parts;              // blocks of the cell's launch
+    int32_t smem_doubles;         // tables staged in shared memory (0: read from global)
+    double budget;
+};
+struct BrutePartial {
+    unsigned long long cost_bits;
+    long long index;              // ci * S^L + digits (layer 0 most significant)
+};
+int brute_blocks(int64_t n_items);
+int launch_brute_cell(const BruteCell &host_cell, const BruteCell *cells, const double *tab, const uint32_t *comps,
+                      BrutePartial *partials, int cell_index, int neumaier, void *stream);
+int launch_brute_reduce(const BruteCell *cells, int n_cells, const BrutePartial *partials, BrutePartial *out,
+                        void *stream);
+
 int launch_seed_partitions(const gbmw_layer *layers, int32_t L, const gbmw_env *env, int64_t n_devices, int32_t n_cells,
                            const int64_t *pp, const int64_t *micro, const int32_t *n_micro, double budget,
                            int32_t max_stages, double *scratch, int32_t *out_sizes, int32_t *out_status, void *stream);

@@ -11,6 +11,7 @@ planner.py:241-277), so the returned plan is the one the reference returns.
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 from functools import lru_cache
 from typing import Any, Sequence
@@ -489,8 +490,61 @@ def evaluate_plan_document(doc: dict, model, cluster, profile) -> float:
     return pipeline_cost(costs, m)
 
 
+@dataclass(frozen=True)
+class OracleResult:
+    feasible: bool
+    cost: float
+    pp_degree: int = 0
+    partition: tuple[int, ...] = ()
+    n_micro: int = 0
+    strategies: tuple[ParallelStrategy, ...] = ()
+
+
+# statistics of the last brute_force_oracle scan (assignments, device ms), for tests / tools
+last_oracle_stats: dict = {}
+
+
+def brute_force_oracle(model, cluster, profile, batch: int, max_layers: int = 4, max_devices: int = 4,
+                       max_assignments: int = 0) -> OracleResult:
+    """Exhaustive minimum over (P, partition, per-layer strategies, m) (planner.py:364-449).
+
+    Same guards, loop order and first-minimum rule as the reference; the scan itself runs
+    on the device (gbmw_brute_force, csrc/gbmw_brute.cu), so the guards can be raised far
+    beyond the reference's 4 layers / 4 devices.  ``max_assignments`` (not in the
+    reference) caps the scan; 0 = the library's default (2^44)."""
+    from . import _native
+
+    if model.num_layers > max_layers:
+        raise ValueError(f"oracle limited to {max_layers} layers, got {model.num_layers}")
+    if cluster.n_devices > max_devices:
+        raise ValueError(f"oracle limited to {max_devices} devices, got {cluster.n_devices}")
+    ctx = EvalContext(model=model, cluster=cluster, profile=profile)
+    layers = _native.layers_array(list(model.layers), profile, {})
+    env = np.array([_native.env_record(ctx)], dtype=_native.ENV_DT)
+    L = len(layers)
+    part = np.zeros(max(L, 1), dtype=np.int32)
+    choice = np.zeros(max(L, 1), dtype=np.int32)
+    rec = _native.OracleRecord()
+    nctx = _native.default_context()
+    with nctx.lock:
+        rc = _native.lib().gbmw_brute_force(nctx.handle, _native.ptr(layers), L, _native.ptr(env), int(batch),
+                                            float(cluster.mem_budget_bytes), float(max_assignments),
+                                            _native.ptr(part), _native.ptr(choice), ctypes.byref(rec))
+        msg = nctx.error() if rc else ""
+    _native.raise_status(rc, msg)
+    last_oracle_stats.clear()
+    last_oracle_stats.update(assignments=rec.combos, device_ms=rec.device_ms)
+    if not rec.feasible:
+        return OracleResult(feasible=False, cost=INF)
+    sset = enumerate_pruned(cluster.n_devices, rec.pp_degree).strategies
+    return OracleResult(feasible=True, cost=rec.cost, pp_degree=rec.pp_degree,
+                        partition=tuple(int(x) for x in part[:rec.n_stages]), n_micro=rec.n_micro,
+                        strategies=tuple(sset[int(c)] for c in choice[:L]))
+
+
 __all__ = [
-    "DEFAULT_GRANULARITY_BYTES", "GalvatronSearch", "Plan", "PlannerOptions", "bi_objective_optimize",
+    "DEFAULT_GRANULARITY_BYTES", "GalvatronSearch", "OracleResult", "Plan", "PlannerOptions", "bi_objective_optimize",
+    "brute_force_oracle",
     "evaluate_plan_document", "galvatron_base", "galvatron_search", "galvatron_search_batch",
     "init_microbatch_num", "init_partition_memory_balanced", "plan_full", "PipelinePartition",
 ]

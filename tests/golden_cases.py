@@ -85,3 +85,17 @@ def check_case(case, res, plan, frontier_vals):
         if "frontier" in out:
             assert [float(v).hex() for v in frontier_vals] == out["frontier"], name
         assert frontier_digest(frontier_vals) == out["frontier_digest"], name
+
+
+def brute_objects(case):
+    """(model, cluster, profile) package objects of a brute.json case."""
+    from paper_2307_02031_b200.specs import load_cluster_spec, load_cost_profile, load_model_spec
+    model = load_model_spec(case["model"])
+    return model, load_cluster_spec(case["cluster"]), load_cost_profile(case["profile"], model)
+
+
+def brute_records(model, cluster, profile):
+    """(layers, env) records of a brute-force instance, as both libgbmw and the oracle take them."""
+    ctx = EvalContext(model, cluster, profile)
+    return (_native.layers_array(list(model.layers), profile, {}),
+            np.array([_native.env_record(ctx)], dtype=_native.ENV_DT))

@@ -56,3 +56,33 @@ def test_dp_search_matches_reference(fixture):
             front_off += nb
         check_case(c, res[i], plans[plan_off:plan_off + nl], fv)
         plan_off += nl
+
+
+def test_brute_force_matches_reference():
+    """or_brute_force (planner.py:364-449 restated) on the 200 golden instances."""
+    from golden_cases import brute_objects, brute_records
+    from paper_2307_02031_b200.strategies import enumerate_pruned
+    for c in load("brute.json")["cases"]:
+        model, cluster, profile = brute_objects(c)
+        layers, env = brute_records(model, cluster, profile)
+        cost, feas, P, m, part, choice = O.brute_force(layers, env, c["batch"], cluster.mem_budget_bytes)
+        out = c["out"]
+        assert feas == out["feasible"] and cost.hex() == out["cost"], (c["name"], cost.hex(), out)
+        if feas:
+            sset = enumerate_pruned(cluster.n_devices, P).strategies
+            assert (P, m, list(part)) == (out["pp_degree"], out["n_micro"], out["partition"]), c["name"]
+            assert [sset[j].to_string() for j in choice] == out["strategies"], c["name"]
+
+
+def test_brute_force_guards():
+    """The reference's size guards (planner.py:377-380) raise before any device work."""
+    from golden_cases import brute_objects
+    from paper_2307_02031_b200 import brute_force_oracle
+    c = next(c for c in load("brute.json")["cases"] if len(c["model"]["layers"]) == 5)
+    model, cluster, profile = brute_objects(c)
+    with pytest.raises(ValueError, match="oracle limited to 4 layers, got 5"):
+        brute_force_oracle(model, cluster, profile, c["batch"])
+    c = next(c for c in load("brute.json")["cases"] if c["cluster"]["n_devices"] == 8)
+    model, cluster, profile = brute_objects(c)
+    with pytest.raises(ValueError, match="oracle limited to 4 devices, got 8"):
+        brute_force_oracle(model, cluster, profile, c["batch"], max_layers=8)
