@@ -1163,9 +1163,11 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
                 }
             }
             fprintf(stderr, "K2 tiles by entries (bin: <2^b entries): ");
-            for (int i = 0; i < 32; ++i)
+            for (int i = 0; i < 31; ++i)
                 if (h[i]) fprintf(stderr, "[%d] %llu tiles %llu ent  ", i, h[i], h[32 + i]);
-            fprintf(stderr, "\n");
+            fprintf(stderr, "\nK2 incremental chunks sent to full evaluation: %llu\n", h[63]);
+            fprintf(stderr, "K2 incremental: chunks %llu, entries %llu, sum of max |G| %llu, candidates %llu, finite %llu\n",
+                    h[48], h[52], h[49], h[50], h[51]);
             // per launch: items, tiles (first chunk)
             const Chunk &c0 = b->chunks[0];
             const Chunk &cl = b->chunks.back();

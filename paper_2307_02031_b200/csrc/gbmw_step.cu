@@ -220,7 +220,9 @@ __device__ __forceinline__ int classify_tile(const ChunkArgs &a, TileCtx &t, uin
     const bool whole = r0 >= lo && r1 <= hi;
     const int f0 = r_base > lo ? r_base : lo;            // first live row of the tile (<= hi)
     unsigned seg = 0u;
-    if (whole) {
+    // breakpoints of the group from its sources' change bits; a partial group (straddling
+    // L_u or H_u) keeps only its live rows
+    if (!dead) {
         const uint32_t *fin = a.chg[(u - 1) & 1] + t.f_off;
         for (int n0 = 0; n0 < na; n0 += kClassifyIB) {
             uint32_t w0[kClassifyIB], w1[kClassifyIB];
@@ -254,9 +256,10 @@ __device__ __forceinline__ int classify_tile(const ChunkArgs &a, TileCtx &t, uin
                 }
             }
         }
-    } else if (!dead) {                                  // partial group: every live row
-        const int a0 = lo > r0 ? lo - r0 : 0, a1 = hi < r1 ? hi - r0 : 31;
-        seg = (0xffffffffu >> (31 - a1)) & ~((1u << a0) - 1u);
+        if (!whole) {
+            const int a0 = lo > r0 ? lo - r0 : 0, a1 = hi < r1 ? hi - r0 : 31;
+            seg &= (0xffffffffu >> (31 - a1)) & ~((1u << a0) - 1u);
+        }
     }
     // the anchor: change bits exact unless it is a breakpoint itself
     const bool fbp = __shfl_sync(0xffffffffu, (seg >> ((f0 - r_base) & 31)) & 1u, (f0 - r_base) >> 5) != 0u;
