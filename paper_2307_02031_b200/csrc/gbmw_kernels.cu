@@ -174,6 +174,7 @@ struct RowCtx {
     const TFCell *bin;
     const int2 *rm;      // row map of B_{U-1} (B is stored only at its stored rows)
     const int2 *rms;     // the same map staged in shared memory, or nullptr
+    int32_t K;           // classes: B is row-major, K (t, f) cells per row
     int64_t n_e;
     int64_t lo;        // rows of B_{U-1} below L_{U-1} are +inf (never written)
     bool init;
@@ -185,7 +186,7 @@ __device__ __forceinline__ void row_value(const RowCtx &r, int64_t e, int j, dou
     if (r.init) { T = r.c[j]; F = r.ef[j]; return; }
     const int x = (int)(e - w);
     const int row = r.rms ? stored_row(r.rms[x >> 5], x) : stored_row(r.rm, x);
-    const int64_t src = (int64_t)r.k[j] * r.n_e + row;
+    const int64_t src = (int64_t)row * r.K + r.k[j];
     const double2 v = __ldg(reinterpret_cast<const double2 *>(r.bin + src));
     T = v.x + r.c[j];
     F = v.y + r.ef[j];
@@ -204,7 +205,7 @@ __device__ __forceinline__ void backtrack(const ChunkArgs &a, const DevProblem &
         const Cell c = cells[(int64_t)u * S + j];
         e -= c.w;
         const int er = stored_row(a.rmap + p.rmap_off + (int64_t)(u - 1) * ng, (int)e);
-        j = par[((int64_t)(u - 1) * K + c.k) * n_e + er];
+        j = par[((int64_t)(u - 1) * n_e + er) * K + c.k];
         path[u - 1] = (uint16_t)j;
     }
 }
@@ -226,7 +227,7 @@ __device__ __forceinline__ void backtrack_wk(const ChunkArgs &a, const DevProble
         const int x = (int)e;
         const int er = (u == U - 1 && rms) ? stored_row(rms[x >> 5], x)
                                            : stored_row(a.rmap + p.rmap_off + (int64_t)(u - 1) * ng, x);
-        j = par[((int64_t)(u - 1) * K + (int)(c & 15u)) * n_e + er];
+        j = par[((int64_t)(u - 1) * n_e + er) * K + (int)(c & 15u)];
         path[u - 1] = (uint16_t)j;
     }
 }
@@ -404,7 +405,7 @@ __global__ void k_sweep_safe(ChunkArgs a) {
                     T = c.c; F = c.ef;
                 } else {
                     const double2 v = __ldg(reinterpret_cast<const double2 *>(
-                        bin + (int64_t)c.k * n_e + stored_row(rm, (int)(e_s - c.w))));
+                        bin + (int64_t)stored_row(rm, (int)(e_s - c.w)) * p.K + c.k));
                     T = v.x + c.c;
                     F = v.y + c.ef;
                 }
@@ -588,6 +589,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
         r.init = (last == 0);
         r.lo = (last == 0) ? 0 : a.unit_lo[p.ustate_off + last];
         r.bin = a.TF[last & 1] + p.b_off;
+        r.K = p.K;
         r.rm = a.rmap + p.rmap_off + (int64_t)(last >= 1 ? last - 1 : 0) * rmap_groups(p.n_b + 1);
         r.rms = (rmap_groups(p.n_b + 1) <= kSweepRmap) ? sRM : nullptr;
         unsigned long long *bound = a.bound + 2 * q;
@@ -780,6 +782,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_rows(ChunkArgs a) {
     r.init = (last == 0);
     r.lo = (last == 0) ? 0 : a.unit_lo[p.ustate_off + last];
     r.bin = a.TF[last & 1] + p.b_off;
+    r.K = p.K;
     r.rm = a.rmap + p.rmap_off + (int64_t)(last >= 1 ? last - 1 : 0) * rmap_groups(p.n_b + 1);
     r.rms = nullptr;
     if (e <= p.n_b) {

@@ -129,7 +129,7 @@ __device__ __forceinline__ void eval_row(const ChunkArgs &a, const SH &sh, int u
                 T[b] = c.c; F[b] = c.ef;
             } else {
                 const int row = stored_row(m[b], src_[b]);
-                const double2 v = __ldg(reinterpret_cast<const double2 *>(bin + (int64_t)k_[b] * n_e + row));
+                const double2 v = __ldg(reinterpret_cast<const double2 *>(bin + (int64_t)row * sh.K + k_[b]));
                 T[b] = v.x + c.c;
                 F[b] = v.y + c.ef;
                 key[b] |= (int)((cw[b] >> (src_[b] & 31)) & 1u);
@@ -348,12 +348,13 @@ __device__ __forceinline__ void eval_round(const ChunkArgs &a, const TileCtx &t,
     if (out) {
         if (j == 0 || chg) {
             TFCell *bout = a.TF[u & 1] + t.b_off;
-            uint16_t *pout = a.par + t.par_off + (int64_t)(u - 1) * K * n_e;
+            uint16_t *pout = a.par + t.par_off + ((int64_t)(u - 1) * n_e + e) * K;
+            double2 *brow = reinterpret_cast<double2 *>(bout) + (int64_t)e * K;
 #pragma unroll
             for (int kk = 0; kk < KT; ++kk) {
                 if (GUARD && kk >= K) break;
-                reinterpret_cast<double2 *>(bout)[(int64_t)kk * n_e + e] = make_double2(bt[kk], bf[kk]);
-                pout[(int64_t)kk * n_e + e] = (uint16_t)t.idx[bk[kk] >> 1];
+                brow[kk] = make_double2(bt[kk], bf[kk]);
+                pout[kk] = (uint16_t)t.idx[bk[kk] >> 1];
             }
         }
         t.echg[j] = (uint16_t)chg;
@@ -719,7 +720,7 @@ __global__ void __launch_bounds__(kFirstThreads) k_dp_first(ChunkArgs a, int p_l
     const int ns = s_ns;
     // (t, f, argmin) of every column at the stored rows
     TFCell *bout = a.TF[u & 1] + p.b_off;
-    uint16_t *pout = a.par + p.par_off + (int64_t)(u - 1) * K * n_e;
+    uint16_t *pout = a.par + p.par_off + (int64_t)(u - 1) * K * n_e;   // rows of K argmins
     for (int k = 0; k < K; ++k) {
         for (int j = tid; j < m; j += blockDim.x) {
             if (!(j == 0 || s_chg[j])) continue;
@@ -732,8 +733,8 @@ __global__ void __launch_bounds__(kFirstThreads) k_dp_first(ChunkArgs a, int p_l
                 const double cand = c.c + R[c.k * K + k];
                 if (lex3_less(cand, c.ef, 2 * n, bt, bf, bk)) { bt = cand; bf = c.ef; bk = 2 * n; }
             }
-            reinterpret_cast<double2 *>(bout)[(int64_t)k * n_e + e] = make_double2(bt, bf);
-            pout[(int64_t)k * n_e + e] = (uint16_t)idx[bk >> 1];
+            reinterpret_cast<double2 *>(bout)[(int64_t)e * K + k] = make_double2(bt, bf);
+            pout[(int64_t)e * K + k] = (uint16_t)idx[bk >> 1];
         }
     }
     // per 32-row group of the live rows: change-bit words, row map; per tile: summaries
@@ -992,8 +993,8 @@ __global__ void __launch_bounds__(kSecondThreads, GROUP <= 1 ? 2 : 1) k_dp_secon
             }
             if (c0 + j == 0 || chg) {
                 const int e = sm.x[c0 + j];
-                reinterpret_cast<double2 *>(bout)[(int64_t)kk * n_e + e] = make_double2(sm.rt[s1 + kk], sm.rf[s1 + kk]);
-                pout[(int64_t)kk * n_e + e] = (uint16_t)t.idx[sm.rk[s1 + kk] >> 1];
+                reinterpret_cast<double2 *>(bout)[(int64_t)e * K + kk] = make_double2(sm.rt[s1 + kk], sm.rf[s1 + kk]);
+                pout[(int64_t)e * K + kk] = (uint16_t)t.idx[sm.rk[s1 + kk] >> 1];
             }
         }
         __syncthreads();
