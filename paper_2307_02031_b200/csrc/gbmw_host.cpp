@@ -1165,9 +1165,8 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
             fprintf(stderr, "K2 tiles by entries (bin: <2^b entries): ");
             for (int i = 0; i < 31; ++i)
                 if (h[i]) fprintf(stderr, "[%d] %llu tiles %llu ent  ", i, h[i], h[32 + i]);
-            fprintf(stderr, "\nK2 incremental chunks sent to full evaluation: %llu\n", h[63]);
-            fprintf(stderr, "K2 incremental: chunks %llu, entries %llu, sum of max |G| %llu, candidates %llu, finite %llu\n",
-                    h[48], h[52], h[49], h[50], h[51]);
+            fprintf(stderr, "\nK3b items %llu, skipped by flag %llu, restagings %llu, pruned by t0 %llu\n", h[56], h[57],
+                    h[58], h[59]);
             // per launch: items, tiles (first chunk)
             const Chunk &c0 = b->chunks[0];
             const Chunk &cl = b->chunks.back();

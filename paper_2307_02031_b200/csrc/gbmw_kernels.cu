@@ -547,6 +547,10 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
                 s_q = q; s_tile = tile;
                 // a higher tile of q was pruned: this one cannot win either (t0 is monotone)
                 s_skip = *(volatile int32_t *)(a.upruned + q);
+                if (a.k2_hist) {                                  // debug: items, flag-skipped items
+                    atomicAdd(a.k2_hist + 56, 1ull);
+                    if (s_skip) atomicAdd(a.k2_hist + 57, 1ull);
+                }
                 if (s_skip) {
                     SweepPartial none;
                     none.t = GBMW_INF; none.e = -1; none.j = 0; none.pad_ = 0;
@@ -562,6 +566,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
         const int S = p.S;
         const int last = p.U - 1;
         if (q != q_prev) {
+            if (a.k2_hist && threadIdx.x == 0) atomicAdd(a.k2_hist + 58, 1ull);   // debug: restaging
             const Cell *lc = a.cells + p.cell_off + (int64_t)last * S;
             const CellMem *lm = a.cmem + p.cell_off + (int64_t)last * S;
             for (int i = threadIdx.x; i < S; i += blockDim.x) {
@@ -583,6 +588,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
             q_prev = q;
         }
         const double safe_limit = safe_limit_of(a, p, q);
+        const double b_up = __longlong_as_double((long long)a.bup[q]);
         RowCtx r;
         r.w = sW; r.k = sK; r.c = sC; r.ef = sE;
         r.n_e = p.n_b + 1;
@@ -614,6 +620,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
         }
         __syncthreads();
         if (s_skip) {
+            if (a.k2_hist && threadIdx.x == 0) atomicAdd(a.k2_hist + 59, 1ull);   // debug: pruned by t0
             if (threadIdx.x == 0) {
                 SweepPartial none;
                 none.t = GBMW_INF; none.e = -1; none.j = 0; none.pad_ = 0;
@@ -675,6 +682,13 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
                     if (nt > bt || (nt == bt && e < be)) break;            // cannot win
                 }
                 ++n_cands;
+                // E_all <= sum(O_f) + max O_b + sum(O_ms) <= F + b_up: a candidate under the
+                // budget by more than the rounding of both sums fits without the walk
+                if ((nf + b_up) * (1.0 + 1e-9) <= p.budget) {
+                    mt = nt; me = e; mj = nj;
+                    bound_offer(bound, nt, e);
+                    break;
+                }
                 // E_all >= sum(O_f) + sum(O_ms) + O_b(last layer) = F + O_b(last unit, nj): a
                 // candidate over the budget by more than the rounding of both sums cannot fit
                 if ((nf + sOB[nj]) * (1.0 - 1e-9) > p.budget) {
