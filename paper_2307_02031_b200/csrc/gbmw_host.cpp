@@ -143,6 +143,7 @@ struct gbmw_ctx {
     size_t pinned_cap = 0;
     gbmw_timing last{};
     std::string err;
+    gbmw_batch *spare = nullptr;             // a destroyed batch kept for its host buffers (no page faults)
 };
 
 struct gbmw_batch {
@@ -372,6 +373,7 @@ extern "C" int gbmw_ctx_destroy(gbmw_ctx *ctx) {
     if (ctx->list_done) cudaEventDestroy(ctx->list_done);
     if (ctx->seed_buf) cudaFree(ctx->seed_buf);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx->spare;
     delete ctx;
     return GBMW_OK;
 }
@@ -580,7 +582,8 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
     if (n_problems < 0 || n_layers < 0 || n_strategies < 0 || n_envs < 0)
         return set_err(&ctx->err, GBMW_EINVAL, "negative array length");
     const double t_start = now_ms();
-    gbmw_batch *b = new gbmw_batch();
+    gbmw_batch *b = ctx->spare ? ctx->spare : new gbmw_batch();   // reuse the host buffers of the last batch
+    ctx->spare = nullptr;
     b->layers.assign(layers, layers + n_layers);
     b->strats.assign(strategies, strategies + n_strategies);
     b->envs.assign(envs, envs + n_envs);
@@ -1338,7 +1341,22 @@ extern "C" int gbmw_batch_destroy(gbmw_batch *b) {
             if (e) cudaEventDestroy(e);
     if (b->ctx_arena) b->ctx->arena_busy = false;
     else if (b->arena) cudaFree(b->arena);
-    delete b;
+    gbmw_ctx *ctx = b->ctx;
+    if (ctx && !ctx->spare) {
+        // keep the batch's host vectors (their capacity) for the next gbmw_batch_create on
+        // this context: a 10k-search batch otherwise page-faults ~2 MB of fresh buffers
+        b->layers.clear(); b->strats.clear(); b->envs.clear(); b->problems.clear(); b->hp.clear();
+        b->chunks.clear(); b->strat_cache.clear(); b->unit_cache.clear();
+        b->strat_last = nullptr; b->unit_last = nullptr;
+        b->strat_last_key = {}; b->unit_last_key = {};
+        b->total_plan = b->total_frontier = 0;
+        b->arena = nullptr; b->arena_size = 0;
+        b->o_layers = b->o_strats = b->o_envs = b->o_results = b->o_plans = b->o_frontier = b->o_stats = 0;
+        b->max_ws = 0; b->timing = gbmw_timing{}; b->ran = false; b->ctx = nullptr; b->ctx_arena = false;
+        ctx->spare = b;
+    } else {
+        delete b;
+    }
     return GBMW_OK;
 }
 
