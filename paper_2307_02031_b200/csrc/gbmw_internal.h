@@ -193,7 +193,7 @@ struct ChunkArgs {
     SweepPartial *best;           // per problem: best safe bucket (K3a)
     unsigned long long *bound;    // per problem, 16 B: running best {bits of t, e + 1} of the sweep (K3a, K3b)
     int32_t *ufirst;              // per problem: first sweep tile holding unsafe rows
-    int32_t *upruned;             // per problem: an unsafe tile was pruned (every lower tile is too)
+    int32_t *upruned;             // per problem: 1 + the highest pruned unsafe tile (every lower tile is pruned too), 0: none
     int32_t *usorted;             // problems with unsafe tiles, by unsafe tile count descending
     int64_t *uprefix;             // kMaxSweepRanks + 1: K3b items before rank r (rank = tile from the top)
     unsigned long long *ucounter; // K3b work counter

@@ -518,6 +518,7 @@ __global__ void __launch_bounds__(1024) k_sweep_scan(ChunkArgs a) {
 // keep the larger e).  Persistent CTAs take (problem, tile) items from the
 // compact list K3a/K3scan built, highest buckets of a problem first (they carry the
 // lowest times, so the bound tightens soonest).
+constexpr int kSweepBatch = 4;
 __global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
     __shared__ int32_t sW[kMaxStrats];
     __shared__ int32_t sK[kMaxStrats];
@@ -529,37 +530,80 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
     __shared__ double sOB[kMaxStrats];                  // O_b of one layer of the last unit
     __shared__ uint32_t sWK[kSweepWK];                  // weight << 4 | class per (unit, strategy)
     __shared__ int2 sRM[kSweepRmap];                    // row map of B_{U-1}, when it fits
-    __shared__ long long s_next;
     __shared__ int s_skip, s_q, s_tile;
+    // items are taken kSweepBatch at a time by warp 0 (one counter atomic, the slot searches
+    // in parallel); items already pruned are retired right there, the rest queue in shared
+    // memory and the CTA works through them one by one (a small batch keeps the rank-major
+    // order, so the top tiles still tighten the bounds before the tiles below them run)
+    __shared__ int s_iq[32], s_it[32];
+    __shared__ int s_nq, s_qi, s_done;
+    __shared__ long long s_last;                        // the counter value of this CTA's last take
     const long long total = a.uprefix[kMaxSweepRanks];
     const int lane = threadIdx.x & 31;
     int q_prev = -1;
     unsigned long long n_rows = 0, n_cands = 0, n_checks = 0;
+    if (threadIdx.x == 0) { s_nq = 0; s_qi = 0; s_done = 0; s_last = 0; }
     while (true) {
         __syncthreads();
-        if (threadIdx.x == 0) {
-            const long long g = (long long)atomicAdd(a.ucounter, 1ull);
-            s_next = g;
-            if (g < total) {
-                const int rank = find_slot(a.uprefix, kMaxSweepRanks, g);
-                const int q = a.usorted[g - a.uprefix[rank]];
-                const int tile = a.probs[q].n_sweep_tiles - 1 - rank;
-                s_q = q; s_tile = tile;
-                // a higher tile of q was pruned: this one cannot win either (t0 is monotone)
-                s_skip = *(volatile int32_t *)(a.upruned + q);
-                if (a.k2_hist) {                                  // debug: items, flag-skipped items
-                    atomicAdd(a.k2_hist + 56, 1ull);
-                    if (s_skip) atomicAdd(a.k2_hist + 57, 1ull);
+        if (threadIdx.x < 32) {
+            while (s_qi >= s_nq && !s_done) {               // warp-uniform: shared state after __syncwarp
+                // batches while many items remain; single items in the tail (the deep
+                // problems' low tiles), where every CTA should take one
+                const int B = (total - s_last > (long long)kSweepBatch * 4 * gridDim.x) ? kSweepBatch : 1;
+                unsigned long long base = 0;
+                if (lane == 0) base = atomicAdd(a.ucounter, (unsigned long long)B);
+                base = __shfl_sync(0xffffffffu, base, 0);
+                if (lane == 0) s_last = (long long)base;
+                if ((long long)base >= total) {
+                    if (lane == 0) s_done = 1;
+                    __syncwarp();
+                    break;
                 }
+                const long long g = (long long)base + lane;
+                int q = 0, tile = 0;
+                bool keep = false;
+                if (lane < B && g < total) {
+                    const int rank = find_slot(a.uprefix, kMaxSweepRanks, g);
+                    q = a.usorted[g - a.uprefix[rank]];
+                    tile = a.probs[q].n_sweep_tiles - 1 - rank;
+                    // a higher tile of q was pruned: this one cannot win either (t0 is monotone)
+                    const bool skip = tile < *(volatile int32_t *)(a.upruned + q);
+                    if (a.k2_hist) {                                  // debug: items, flag-skipped items
+                        atomicAdd(a.k2_hist + 56, 1ull);
+                        if (skip) atomicAdd(a.k2_hist + 57, 1ull);
+                    }
+                    if (skip) {
+                        SweepPartial none;
+                        none.t = GBMW_INF; none.e = -1; none.j = 0; none.pad_ = 0;
+                        a.partials[a.probs[q].tile_off + tile] = none;
+                    } else {
+                        keep = true;
+                    }
+                }
+                const unsigned m = __ballot_sync(0xffffffffu, keep);
+                if (keep) {
+                    const int at = __popc(m & ((1u << lane) - 1u));
+                    s_iq[at] = q; s_it[at] = tile;
+                }
+                if (lane == 0) { s_nq = __popc(m); s_qi = 0; }
+                __syncwarp();
+            }
+            if (lane == 0 && s_qi < s_nq) {
+                const int k = s_qi++;
+                s_q = s_iq[k]; s_tile = s_it[k];
+                // re-check: the flag may have been set since the item was taken
+                s_skip = s_tile < *(volatile int32_t *)(a.upruned + s_q) ? 1 : 0;
                 if (s_skip) {
                     SweepPartial none;
                     none.t = GBMW_INF; none.e = -1; none.j = 0; none.pad_ = 0;
-                    a.partials[a.probs[q].tile_off + tile] = none;
+                    a.partials[a.probs[s_q].tile_off + s_tile] = none;
                 }
+            } else if (lane == 0) {
+                s_skip = -1;                                  // drained and no items left
             }
         }
         __syncthreads();
-        if (s_next >= total) break;
+        if (s_skip < 0) break;
         if (s_skip) continue;
         const int q = s_q, tile = s_tile;
         const DevProblem &p = a.probs[q];
@@ -625,7 +669,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
                 SweepPartial none;
                 none.t = GBMW_INF; none.e = -1; none.j = 0; none.pad_ = 0;
                 a.partials[p.tile_off + tile] = none;
-                a.upruned[q] = 1;
+                atomicMax(a.upruned + q, tile + 1);   // every tile below this one is pruned too
             }
             continue;
         }

@@ -1,6 +1,6 @@
 """Device time of the 10k sweep split by depth: all searches, the deep ones only (units > 16)
 and the rest, each as its own batch (median of 5 runs):
-python tools/split_probe.py  (GPU box)."""
+python tools/split_probe.py [all]  (GPU box; "all": the whole sweep only)."""
 import statistics
 import sys
 
@@ -32,6 +32,8 @@ def run(mask, name):
 
 import numpy as np   # noqa: E402
 run(np.ones(len(P), bool), "all")
+if len(sys.argv) > 1 and sys.argv[1] == "all":
+    sys.exit(0)
 run(deep, "deep>16")
 run(~deep, "shallow")
 run(gpt1, "gpt P=1")
