@@ -13,6 +13,7 @@ from __future__ import annotations
 
 import ctypes
 import logging
+from collections.abc import Sequence as _AbcSequence
 from dataclasses import dataclass, field
 from typing import Callable, Sequence
 
@@ -74,20 +75,48 @@ def balance_degrees(stage_costs: Sequence[StageCost]) -> BalanceReport:
                          stage_times=times, stage_mems=mems)
 
 
-class StageLayers(list):
-    """The per-stage layer lists of a partition of ``model.layers`` (a plain list of
-    lists), remembering the slices so the batched search needs no identity check."""
-    __slots__ = ("model", "ranges")
+class StageLayers(_AbcSequence):
+    """The per-stage layer lists of a partition of ``model.layers`` (balance.py's
+    ``partition_layers`` result): an immutable sequence of lists, built on first access.
+    The batched search only needs the slices (``ranges``), so the drivers, which partition
+    thousands of (batch, degree) cells per window, never copy the layers."""
+    __slots__ = ("model", "ranges", "_lists")
+
+    def __init__(self, model, ranges):
+        self.model = model
+        self.ranges = ranges
+        self._lists = None
+
+    def _materialize(self):
+        if self._lists is None:
+            ls = self.model.layers
+            self._lists = [list(ls[a:a + n]) for a, n in self.ranges]
+        return self._lists
+
+    def __len__(self):
+        return len(self.ranges)
+
+    def __getitem__(self, i):
+        return self._materialize()[i]
+
+    def __iter__(self):
+        return iter(self._materialize())
+
+    def __eq__(self, other):
+        return list(self) == list(other) if isinstance(other, (list, tuple, StageLayers)) else NotImplemented
+
+    def __repr__(self):
+        return repr(self._materialize())
 
 
-def partition_layers(model, partition: PipelinePartition) -> list[list]:
+def partition_layers(model, partition: PipelinePartition) -> Sequence[list]:
     if partition.num_layers != model.num_layers:
         raise ValueError(f"partition covers {partition.num_layers} layers, model has {model.num_layers}")
-    bounds = partition.boundaries()
-    out = StageLayers(list(model.layers[a:b]) for a, b in bounds)
-    out.model = model
-    out.ranges = [(a, b - a) for a, b in bounds]
-    return out
+    ranges, a = [], 0
+    for n in partition.stage_sizes:
+        ranges.append((a, n))
+        a += n
+    return StageLayers(model, ranges)
 
 
 def seed_strategy(n_devices: int, pp_degree: int, use_sdp: bool = False) -> ParallelStrategy:

@@ -27,6 +27,7 @@ from .balance import (
     bi_objective_multi,
     bi_objective_optimize,
     init_partition_memory_balanced,
+    StageLayers,
     partition_layers,
     seed_partitions,
 )
@@ -105,12 +106,8 @@ def _sset(n_devices: int, pp_degree: int):
 
 def _stage_ranges(model, stages):
     """(start, length) of each stage if the stages are consecutive slices of model.layers."""
-    if getattr(stages, "model", None) is model and getattr(stages, "ranges", None) is not None:
-        # from partition_layers(model, ...), unmodified: the slices are known
-        ls = model.layers
-        if len(stages) == len(stages.ranges) and all(
-                len(st) == n and st[0] is ls[a] and st[-1] is ls[a + n - 1] for st, (a, n) in zip(stages, stages.ranges)):
-            return stages.ranges
+    if isinstance(stages, StageLayers) and stages.model is model:
+        return stages.ranges                    # from partition_layers(model, ...): immutable slices
     layers = model.layers
     index = _layer_index(model)
     out = []
