@@ -148,6 +148,15 @@ class FailedOutcome:
         _native.raise_status(self.code, self.msg)
 
 
+@lru_cache(maxsize=4096)
+def _cell_setup(n_devices: int, pp: int, batch: int, cap_factor: int, min_micro: int):
+    """(n_micro, micro-batch, strategy set, any strategy usable) of a (N, P, B) cell."""
+    m = init_microbatch_num(batch, pp, cap_factor, min_micro)
+    micro = batch // m
+    sset = _sset(n_devices, pp)
+    return m, micro, sset, any(micro % s.data_degree == 0 for s in sset.strategies)
+
+
 def _search_slices(cells, ctx, opts, defer_errors=False):
     """galvatron_search for cells whose stages are slices of ctx.model: one flat problem
     table over a single copy of the model's layers, no per-stage Python objects.  With
@@ -161,12 +170,13 @@ def _search_slices(cells, ctx, opts, defer_errors=False):
     env = mar.env(ctx)
     flags = _native.STAGE_COST | (_native.FUSE if opts.fuse_identical else 0) | \
         (_native.APPROX if opts.approx_prev else 0)
-    rows, metas = [], []
+    # per searched cell: its stages' (start, length) and the cell-level fields of its rows
+    starts, lens, cell_rows, cell_vals = [], [], [], []
+    metas = []
+    n_rows = 0
     rc = _native.OK
     for budget, ranges, n_devices, batch, pp in cells:
-        m = init_microbatch_num(batch, pp, opts.microbatch_cap_factor, opts.min_micro_size)
-        micro = batch // m
-        sset = _sset(n_devices, pp)
+        m, micro, sset, usable = _cell_setup(n_devices, pp, batch, opts.microbatch_cap_factor, opts.min_micro_size)
         strats = sset.strategies
         if gran <= 0:
             raise ValueError(f"granularity_bytes must be positive, got {gran}")
@@ -176,46 +186,70 @@ def _search_slices(cells, ctx, opts, defer_errors=False):
         if nb > MAX_BUCKETS:
             raise ValueError(f"budget/granularity yields {nb} buckets (> {MAX_BUCKETS}); "
                              f"increase the memory granularity")
-        if nb == 0 or not any(micro % s.data_degree == 0 for s in strats):
+        if nb == 0 or not usable:
             metas.append((m, None, None, strats))
             continue
-        sb = mar.strat_range(sset, list(strats))
-        r0 = len(rows)
-        for idx, (start, n) in enumerate(ranges, start=1):
-            rows.append((base + start, n, sb, len(strats), env, idx, m, flags, micro, gran, float(budget), nb))
-        metas.append((m, r0, len(rows), strats))
+        sb = mar.strat_range(sset, strats)
+        k = len(ranges)
+        for a, n in ranges:
+            starts.append(a)
+            lens.append(n)
+        cell_rows.append(k)
+        cell_vals.append((sb, len(strats), m, micro, float(budget), nb))
+        metas.append((m, n_rows, n_rows + k, strats))
+        n_rows += k
     out = []
-    if rows:
+    if n_rows:
         layers, loffs, strats_arr, soffs, envs = mar.finish()
-        probs = np.array(rows, dtype=_native.PROBLEM_DT)
-        probs["layer_begin"] += loffs[0]
-        probs["strat_begin"] = [soffs[r] for r in probs["strat_begin"]]
+        probs = np.zeros(n_rows, dtype=_native.PROBLEM_DT)
+        reps = np.asarray(cell_rows, dtype=np.int64)
+        cv = list(zip(*cell_vals))
+        probs["layer_begin"] = np.asarray(starts, dtype=np.int64) + (base + loffs[0])
+        probs["n_layers"] = lens
+        probs["strat_begin"] = np.repeat(np.asarray([soffs[x] for x in cv[0]], dtype=np.int64), reps)
+        probs["n_strats"] = np.repeat(np.asarray(cv[1], dtype=np.int64), reps)
+        probs["env_index"] = env
+        # stage_index = 1 .. P within each cell
+        first = np.repeat(np.cumsum(reps) - reps, reps)
+        probs["stage_index"] = np.arange(n_rows, dtype=np.int64) - first + 1
+        probs["n_micro"] = np.repeat(np.asarray(cv[2], dtype=np.int64), reps)
+        probs["flags"] = flags
+        probs["micro"] = np.repeat(np.asarray(cv[3], dtype=np.int64), reps)
+        probs["gran"] = gran
+        probs["budget"] = np.repeat(np.asarray(cv[4], dtype=np.float64), reps)
+        probs["n_buckets"] = np.repeat(np.asarray(cv[5], dtype=np.int64), reps)
         rc, msg, res, plans, _ = run_native_batch(layers, strats_arr, envs, probs)
         if rc != _native.OK:
             bad = np.flatnonzero(res["status"] != 0)
             if not (defer_errors and len(bad)):
                 _native.raise_status(int(res["status"][bad[0]]) if len(bad) else rc, msg)
             first_bad = int(bad[0])
-        plan_off = np.concatenate(([0], np.cumsum(probs["n_layers"])))
+        plan_off = np.concatenate(([0], np.cumsum(probs["n_layers"]))).tolist()
+        feas = res["feasible"].tolist()
+        st_t, st_ns, st_pk = res["stage_time"].tolist(), res["stage_ns"].tolist(), res["stage_peak"].tolist()
+        status = res["status"]
+        plan_l = plans.tolist()
     for m, r0, r1, strats in metas:
         if r0 is not None and rc != _native.OK:
-            st = res["status"][r0:r1]
+            st = status[r0:r1]
             k = np.flatnonzero(st != 0)
             # the reference raises inside the first failing stage's dp_search, after the stages
             # before it were searched; a stage that is infeasible earlier ends the cell first
-            if len(k) and res["feasible"][r0:r0 + int(k[0])].all():
+            if len(k) and all(feas[r0:r0 + int(k[0])]):
                 code = int(st[k[0]])
                 out.append(FailedOutcome(code, msg if r0 + int(k[0]) == first_bad else
                                          f"stage search failed (status {code})", m))
                 continue
-        if r0 is None or not res["feasible"][r0:r1].all():      # first infeasible stage (planner.py:159-160)
+        if r0 is None or not all(feas[r0:r1]):                  # first infeasible stage (planner.py:159-160)
             out.append(SearchOutcome(cost=INF, strategies=None, stage_costs=None, n_micro=m))
             continue
-        idx = plans[plan_off[r0]:plan_off[r1]]
-        costs = tuple(StageCost(float(a), float(b), float(c)) for a, b, c in
-                      zip(res["stage_time"][r0:r1], res["stage_ns"][r0:r1], res["stage_peak"][r0:r1]))
-        out.append(SearchOutcome(cost=pipeline_cost(costs, m), strategies=tuple(strats[j] for j in idx),
-                                 stage_costs=costs, n_micro=m))
+        ts, ns = st_t[r0:r1], st_ns[r0:r1]
+        costs = tuple(map(StageCost, ts, ns, st_pk[r0:r1]))
+        idx = plan_l[plan_off[r0]:plan_off[r1]]
+        # pipeline_cost (costs.py:355-362) on the same floats in the same order
+        cost = (m - 1) * max(ns) + sum(ts)
+        out.append(SearchOutcome(cost=cost, strategies=tuple([strats[j] for j in idx]), stage_costs=costs,
+                                 n_micro=m))
     return out
 
 
