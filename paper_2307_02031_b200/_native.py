@@ -203,11 +203,24 @@ def strategy_record(s) -> tuple:
     return (int(s.pp_degree), len(levels), par, deg, 1 if s.ckpt else 0)
 
 
+_records: dict = {}
+
+
 def strategies_array(strats) -> np.ndarray:
-    out = np.zeros(len(strats), dtype=STRATEGY_DT)
-    for i, s in enumerate(strats):
-        out[i] = strategy_record(s)
-    return out
+    """STRATEGY_DT records of a strategy sequence.  A strategy's record is built once per
+    object (strategies are frozen dataclasses; the cached entry keeps the object alive, so
+    its id cannot be reused while cached)."""
+    recs = []
+    cache = _records
+    for s in strats:
+        hit = cache.get(id(s))
+        if hit is None or hit[0] is not s:
+            if len(cache) > 8192:
+                cache.clear()
+            hit = (s, strategy_record(s))
+            cache[id(s)] = hit
+        recs.append(hit[1])
+    return np.array(recs, dtype=STRATEGY_DT) if recs else np.zeros(0, dtype=STRATEGY_DT)
 
 
 def _i64(v, what):

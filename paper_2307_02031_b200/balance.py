@@ -240,7 +240,8 @@ def seed_partitions(model, ctx, n_devices, cells, n_threads: int | None = None,
             if rc != _native.OK:
                 _native.raise_status(rc, device.error())
     else:
-        threads = n_threads or max(1, min(32, len(os.sched_getaffinity(0))))
+        # leave cores to the main thread (batch creation, launches) that runs beside the seeding
+        threads = n_threads or max(1, min(16, len(os.sched_getaffinity(0)) // 2))
         rc = _native.lib().gbmw_seed_partitions(_native.ptr(layers), len(layers), _native.ptr(env), int(n_devices),
                                                 n, _native.ptr(pp), _native.ptr(micro), _native.ptr(nm), budget,
                                                 width, int(threads), _native.ptr(sizes))
@@ -347,19 +348,33 @@ def _run_trajectories(model, ctx, trajs: list[_Trajectory], search, microbatch_p
     """Advance all trajectories in lockstep rounds; searches of a round share one device pass."""
     cluster = ctx.cluster
     n_dev, budget, L = cluster.n_devices, cluster.mem_budget_bytes, model.num_layers
+
+    def setup(t):
+        n_micro_seed = microbatch_policy(t.batch, t.pp)
+        micro_seed = t.batch // n_micro_seed
+        # _seed_for (balance.py:471-488) already balances the chosen seed's memory: that is p0
+        seed_list, p0 = _seed_and_partition(model, ctx, n_dev, t.pp, micro_seed, n_micro_seed)
+        p_time = init_partition_time_balanced(model, t.pp, seed_list, micro_seed, n_micro_seed, ctx)
+        mem_ref = max(sc.peak_mem_bytes for sc in
+                      evaluate_partition(model, p_time, seed_list, micro_seed, n_micro_seed, ctx))
+        return mem_ref, p0
+
+    multi = [t for t in trajs if not t.single]
+    # independent per trajectory, native hill climbs (the GIL is released): on host threads
+    if len(multi) > 1:
+        from concurrent.futures import ThreadPoolExecutor
+        import os
+        with ThreadPoolExecutor(max_workers=max(1, min(len(multi), len(os.sched_getaffinity(0)) // 2))) as ex:
+            setups = list(ex.map(setup, multi))
+    else:
+        setups = [setup(t) for t in multi]
+    for t, (mem_ref, p0) in zip(multi, setups):
+        t.mem_ref = mem_ref
+        t.queue = [p0]
+        t.visited = {p0.stage_sizes}
     for t in trajs:
         if t.single:
             t.queue = [PipelinePartition((L,))]
-            continue
-        n_micro_seed = microbatch_policy(t.batch, t.pp)
-        micro_seed = t.batch // n_micro_seed
-        seed_list = _seed_for(model, ctx, n_dev, t.pp, micro_seed, n_micro_seed)
-        p_time = init_partition_time_balanced(model, t.pp, seed_list, micro_seed, n_micro_seed, ctx)
-        t.mem_ref = max(sc.peak_mem_bytes for sc in
-                        evaluate_partition(model, p_time, seed_list, micro_seed, n_micro_seed, ctx))
-        p0 = init_partition_memory_balanced(model, t.pp, seed_list, micro_seed, n_micro_seed, ctx)
-        t.queue = [p0]
-        t.visited = {p0.stage_sizes}
     batched = getattr(search, "batch", None)
     while True:
         active = [t for t in trajs if t.queue and (t.single and t.iterations == 0 or

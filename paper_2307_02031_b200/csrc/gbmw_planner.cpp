@@ -166,6 +166,30 @@ struct AlphaCache {
     }
     static double finish(double f, double c) { return (c != 0.0 && std::isfinite(c)) ? f + c : f; }
 
+    // The objective's exact total of the current partition (py_sum of its stage values).
+    double total(bool memory) const { return memory ? finish(fm[n - 1], cm[n - 1]) : finish(ft[n - 1], ct[n - 1]); }
+
+    // Can the move (stages b, b + 1 -> n0, n1) beat `thresh`?  A bound, no exact fold: the
+    // move's total is approximated from the current exact total; the approximation, the
+    // exact py_sum of the moved partition and the current total all lie within a few ulps
+    // of the true sums, so |alpha_approx - alpha| <= err below (with a wide margin), and a
+    // move whose approximate alpha plus err does not exceed `thresh` cannot be accepted.
+    bool may_beat(const StageCostOut *sc, int b, const StageCostOut &n0, const StageCostOut &n1, bool memory,
+                  double cur_total, double thresh) const {
+        const double x0 = memory ? n0.peak : n0.t, x1 = memory ? n1.peak : n1.t;
+        const double o0 = memory ? sc[b].peak : sc[b].t, o1 = memory ? sc[b + 1].peak : sc[b + 1].t;
+        double mx = b > 0 ? (memory ? pmm[b - 1] : pmt[b - 1]) : x0;
+        if (x0 > mx) mx = x0;
+        if (x1 > mx) mx = x1;
+        const double suf = memory ? smm[b + 2] : smt[b + 2];
+        if (suf > mx) mx = suf;
+        const double apx = ((cur_total - o0) - o1) + x0 + x1;
+        if (!(mx > 0.0) || !(apx > 0.0) || !std::isfinite(apx)) return true;     // let the exact path decide
+        const double eps = 2.220446049250313e-16;
+        const double err = 64.0 * eps * (cur_total + apx + x0 + x1) / apx + 8.0 * eps;
+        return (1.0 - mx / apx) + err > thresh;
+    }
+
     // sc: the current partition's costs; n0, n1: the new costs of stages b, b + 1
     int move_alpha(const StageCostOut *sc, int b, const StageCostOut &n0, const StageCostOut &n1, bool memory,
                    double *alpha) const {
@@ -242,11 +266,20 @@ struct PartitionTables {
                                       env.intra_island_bw);
             }
             p2p[l] = stage_p2p_time(layers[l].bnd_bytes_per_sample, micro, s.pp_degree, env);
+            // layer_memory at every stage index: only the 1F1B stash differs, so the
+            // stage-independent factor is formed once, with layer_memory's own operations
+            const Mem m1 = layer_memory(layers[l], d, micro, 1, n_micro, env.ms_bytes_per_param_byte);
+            ob[l] = m1.o_b;
+            oms[l] = m1.o_ms;
+            const int64_t samples = micro / d.data;
+            const int64_t bnd_mb = layers[l].bnd_bytes_per_sample * samples;
+            const double frac = layers[l].tp_act_replication_fraction;
+            const double ips = (double)layers[l].int_bytes_per_sample * (frac + ((1.0 - frac) / (double)d.tp));
+            const double x = (double)bnd_mb + ips * (double)samples;
             for (int st = 1; st <= S; ++st) {
-                const Mem m = layer_memory(layers[l], d, micro, st, n_micro, env.ms_bytes_per_param_byte);
-                of[(size_t)l * S + (st - 1)] = m.o_f;
-                ob[l] = m.o_b;
-                oms[l] = m.o_ms;
+                int64_t stash = (int64_t)d.pp - st + 1;
+                if ((int64_t)n_micro < stash) stash = n_micro;
+                of[(size_t)l * S + (st - 1)] = d.ckpt ? (double)(stash * bnd_mb) : (double)stash * x;
             }
         }
         return GBMW_OK;
@@ -322,6 +355,7 @@ int init_partition(const gbmw_layer *layers, int n_layers, const gbmw_strategy *
         double round_score = best_score;
         for (int s = 0, a = 0; s < S; ++s) { starts[s] = a; a += best[s]; }
         ac.build(sc.data(), S);
+        const double cur_total = ac.total(memory);
         for (int b = 0; b + 1 < S; ++b) {
             for (int dir = 0; dir < 2; ++dir) {
                 if (dir == 0 ? best[b] <= 1 : best[b + 1] <= 1) continue;
@@ -329,6 +363,7 @@ int init_partition(const gbmw_layer *layers, int n_layers, const gbmw_strategy *
                 const StageCostOut n0 = tab.stage(starts[b], mid, b + 1);       // the two re-costed stages
                 const StageCostOut n1 = tab.stage(mid, starts[b + 1] + best[b + 1], b + 2);
                 double s;
+                if (!ac.may_beat(sc.data(), b, n0, n1, memory, cur_total, round_score + 1e-15)) continue;
                 if ((rc = ac.move_alpha(sc.data(), b, n0, n1, memory, &s))) return rc;
                 if (s > round_score + 1e-15) {
                     round_best = best;
@@ -431,14 +466,9 @@ extern "C" int gbmw_seed_for(const gbmw_layer *layers, int32_t n_layers, const g
             return GBMW_OK;
         }
     }
+    // nothing fits: the last candidate, whose memory-balanced partition the loop just computed
     *out_seed = usable.back();
-    if (out_sizes) {
-        for (auto &x : seeds) x = usable.back();
-        const int rc = init_partition(layers, n_layers, seeds.data(), (int)pp_degree, *env, micro_batch, n_micro, true,
-                                      sizes);
-        if (rc) return rc;
-        std::memcpy(out_sizes, sizes.data(), sizeof(int32_t) * pp_degree);
-    }
+    if (out_sizes) std::memcpy(out_sizes, sizes.data(), sizeof(int32_t) * pp_degree);
     return GBMW_OK;
 }
 

@@ -433,7 +433,11 @@ def galvatron_base(model, cluster, profile, opts: PlannerOptions = PlannerOption
     best: Plan | None = None
     batches = list(range(opts.batch_step, opts.max_batch + 1, opts.batch_step)) if opts.batch_step > 0 else []
     window = max(1, opts.batch_window)
-    chunks = [batches[i:i + window] for i in range(0, len(batches), window)]
+    # a short first window where seeding is expensive (pipeline degrees >= 16: long hill
+    # climbs): the first window's seeding is the only one not hidden behind a device pass
+    first = max(1, window // 4) if min(cluster.n_devices, model.num_layers) >= 16 else window
+    chunks = [batches[:first]] + [batches[i:i + window] for i in range(first, len(batches), window)] \
+        if batches else []
     nxt = _window_executor().submit(_base_cells_window, model, ctx, chunks[0], opts) if chunks else None
     for ci, chunk in enumerate(chunks):
         per_batch = nxt.result()
