@@ -32,7 +32,7 @@ namespace gbmw {
 #define GBMW_STEP_INF __longlong_as_double(0x7ff0000000000000LL)
 
 constexpr int kClassifyIB = 8;              // window checks per thread in flight
-constexpr int kStepIB = 4;                  // sources per lane in flight (lane-per-row evaluation)
+constexpr int kStepIB = 2;                  // sources per lane in flight (lane-per-row evaluation)
 constexpr int kWarpRows = 1024;             // rows per warp tile: 32 groups of 32
 constexpr int kK2Warps = kStepThreads / 32;
 
