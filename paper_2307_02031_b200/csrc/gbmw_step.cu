@@ -97,19 +97,22 @@ __device__ __forceinline__ void eval_row(const ChunkArgs &a, const SH &sh, int u
                                          double *bt, double *bf, int *bk) {
     const int S = sh.S, K = GUARD ? sh.K : KT;
     const int n_e = sh.n_e, lo_prev = FIRST ? 0 : sh.lo_prev;
+    // sources in flight per lane: as many as the register budget holds without spilling an
+    // in-flight load (a spilled load result serialises the loads)
+    constexpr int IB = (KT <= 4) ? kStepIB : 1;
     const TFCell *bin = a.TF[(u - 1) & 1] + sh.b_off;
     const int2 *rm = a.rmap + sh.rm_prev;
     const uint32_t *fin = a.chg[(u - 1) & 1] + sh.f_off;
 #pragma unroll
     for (int kk = 0; kk < KT; ++kk) { bt[kk] = GBMW_STEP_INF; bf[kk] = GBMW_STEP_INF; bk[kk] = 0x7fffffff; }
-    for (int i0 = l; i0 < S; i0 += kStepIB * L) {
-        double T[kStepIB], F[kStepIB];
-        int key[kStepIB], src_[kStepIB], k_[kStepIB];
-        bool ok[kStepIB];
-        int2 m[kStepIB];
-        uint32_t cw[kStepIB];
+    for (int i0 = l; i0 < S; i0 += IB * L) {
+        double T[IB], F[IB];
+        int key[IB], src_[IB], k_[IB];
+        bool ok[IB];
+        int2 m[IB];
+        uint32_t cw[IB];
 #pragma unroll
-        for (int b = 0; b < kStepIB; ++b) {
+        for (int b = 0; b < IB; ++b) {
             const int i = i0 + b * L;
             const Cell c = sh.cell[i < S ? i : 0];
             const int src = e - c.w;
@@ -122,7 +125,7 @@ __device__ __forceinline__ void eval_row(const ChunkArgs &a, const SH &sh, int u
             }
         }
 #pragma unroll
-        for (int b = 0; b < kStepIB; ++b) {
+        for (int b = 0; b < IB; ++b) {
             if (!ok[b]) continue;
             const Cell c = sh.cell[i0 + b * L];
             if (FIRST) {                       // init row, dpsearch.py:255-259
@@ -136,7 +139,7 @@ __device__ __forceinline__ void eval_row(const ChunkArgs &a, const SH &sh, int u
             }
         }
 #pragma unroll
-        for (int b = 0; b < kStepIB; ++b) {
+        for (int b = 0; b < IB; ++b) {
             if (i0 + b * L >= S) break;
             const double *rrow = sh.r + k_[b] * K;
 #pragma unroll
