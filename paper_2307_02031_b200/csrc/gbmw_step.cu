@@ -556,18 +556,17 @@ __global__ void __launch_bounds__(kStepThreads, GROUP <= 1 ? 3 : 1)
             unsigned long long base = 0;
             HeavyTile *hr = reinterpret_cast<HeavyTile *>(a.k2_heavy) + slot;
             for (int g = lane; g < 33; g += 32) hr->goff[g] = s_goff[warp][g];
-            __threadfence();                             // entries and offsets before the round list
+            // no fences: K2b reads the records, entries and round list only after this grid has
+            // completed (griddepcontrol.wait), which makes all of its writes visible
             __syncwarp();
             if (lane == 0) {
                 TileCtx c = t;
                 c.erow = ge; c.echg = a.k2_echg + slot * kK2SlotEntries; c.goff = hr->goff;
                 hr->t = c;
                 hr->rounds = rounds; hr->done = 0;
-                __threadfence();
                 base = atomicAdd(ctr + 1, (unsigned long long)rounds);
             }
             base = __shfl_sync(0xffffffffu, base, 0);
-            __threadfence();
             for (int r = lane; r < rounds; r += 32) rlist[base + r] = make_int2((int)slot, r);
         }
         __syncwarp();
