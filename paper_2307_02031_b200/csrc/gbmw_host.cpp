@@ -112,6 +112,7 @@ struct Chunk {
     std::vector<int> slist_group;
     std::vector<char> slist_second;   // u = 2 list run by the candidate-row kernel (K2s)
     int64_t n_items = 0;           // K2 items (active problems) over all launches
+    int64_t n_ctx = 0;             // per-(launch, problem) step contexts
     size_t small_bytes = 0;
     size_t ws_bytes = 0;
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -528,7 +529,7 @@ size_t put(std::vector<char> &blob, const T *src, size_t n) {
 
 // chunk workspace layout (byte offsets from ws base)
 struct WsLayout {
-    size_t cells, cmem, rcls, bup, items, scount, tf0, tf1, chg0, chg1, rmap, par, parts, bestp, bound, ufirst, upruned, usorted, uprefix, uctr,
+    size_t cells, cmem, rcls, bup, items, sctx, scount, tf0, tf1, chg0, chg1, rmap, par, parts, bestp, bound, ufirst, upruned, usorted, uprefix, uctr,
         uniq, ucell, nuniq,
         ulo, uhi, ctr, k2e, k2c, k2h, k2r, total;
 };
@@ -540,6 +541,7 @@ WsLayout ws_layout(const Chunk &c) {
     w.rcls = o; o = align_up(o + c.n_r * 8);
     w.bup = o; o = align_up(o + c.probs.size() * 8);
     w.items = o; o = align_up(o + c.n_items * sizeof(int4));
+    w.sctx = o; o = align_up(o + (size_t)c.n_ctx * kStepCtxBytes);
     w.scount = o; o = align_up(o + c.slists.size() * 8);
     w.tf0 = o; o = align_up(o + c.n_bcells * sizeof(TFCell));
     w.tf1 = o; o = align_up(o + c.n_bcells * sizeof(TFCell));
@@ -779,7 +781,7 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
         c.o_stepmap = put(blob, stepmap.data(), stepmap.size()) - base;
         c.o_aux = put(blob, aux.data(), aux.size()) - base;
         // K2 launches: items bounded by all tiles of the active problems
-        c.slists.clear(); c.slist_group.clear(); c.slist_second.clear(); c.n_items = 0;
+        c.slists.clear(); c.slist_group.clear(); c.slist_second.clear(); c.n_items = 0; c.n_ctx = 0;
         static const bool no_second = getenv("GBMW_NO_SECOND") && getenv("GBMW_NO_SECOND")[0] == '1';
         for (int u = 1; u < c.Umax; ++u)
             for (int g = 0; g < kStepVGroups; ++g) {
@@ -792,6 +794,8 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
                 }
                 StepList sl;
                 sl.u = u; sl.lo = lo; sl.n = na; sl.no_items = (u == 1 || second) ? 1 : 0; sl.base = c.n_items;
+                sl.ctx_base = c.n_ctx;
+                if (!sl.no_items) c.n_ctx += na;
                 c.slists.push_back(sl);
                 c.slist_group.push_back(g);
                 c.slist_second.push_back(second ? 1 : 0);
@@ -928,6 +932,7 @@ ChunkArgs chunk_args(gbmw_batch *b, const Chunk &c, char *ws, size_t chunk_index
     a.rcls = (double *)(ws + w.rcls);
     a.bup = (unsigned long long *)(ws + w.bup);
     a.step_items = (int4 *)(ws + w.items);
+    a.step_ctx = (void *)(ws + w.sctx);
     a.step_count = (int64_t *)(ws + w.scount);
     a.TF[0] = (TFCell *)(ws + w.tf0);
     a.TF[1] = (TFCell *)(ws + w.tf1);

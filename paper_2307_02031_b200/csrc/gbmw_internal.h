@@ -150,7 +150,9 @@ struct SweepPartial {
 struct StepList {
     int32_t u, lo, n, no_items;   // no_items: the step runs without tile items (K2f / K2s)
     int64_t base;
+    int64_t ctx_base;             // first of the launch's per-problem step contexts (k_step_lists)
 };
+constexpr int kStepCtxBytes = 256;   // one step context (TileCtx, gbmw_step.cu) per (launch, problem)
 
 // Everything a chunk's kernels read or write (device pointers).
 struct ChunkArgs {
@@ -167,7 +169,8 @@ struct ChunkArgs {
     const int2 *aux_map;          // K3r tiles: (problem, tile) of frontier / collapsed-DP problems
     const StepList *step_lists;   // K2 launches of the chunk
     int32_t n_step_lists;
-    int4 *step_items;             // (problem, first tile, last tile) items of every K2 launch
+    int4 *step_items;             // (problem, first tile, last tile, step context) items of every K2 launch
+    void *step_ctx;               // per (launch, problem): its step context, written by k_step_lists
     int64_t *step_count;          // per K2 launch: number of items
     int64_t n_aux;
     const int32_t *cand_strat;    // global strategy index

@@ -58,6 +58,7 @@ struct alignas(16) HeavyTile {
     uint16_t goff[33];                      // first entry of group g; goff[32] = n_ent
 };
 static_assert(sizeof(HeavyTile) <= kK2HeavyBytes, "HeavyTile size");
+static_assert(sizeof(TileCtx) <= kStepCtxBytes && sizeof(TileCtx) % 8 == 0, "step context size");
 
 __device__ __forceinline__ void load_tile_ctx(const ChunkArgs &a, int u, int q, int tile, TileCtx &t) {
     const DevProblem &p = a.probs[q];
@@ -459,7 +460,13 @@ __global__ void __launch_bounds__(1024) k_step_lists(ChunkArgs a) {
         const DevProblem &p = a.probs[x];
         const int lo = a.unit_lo[p.ustate_off + sl.u], hi = a.unit_hi[p.ustate_off + sl.u];
         if (hi < lo) continue;
-        for (int t = lo / kWarpRows; t <= hi / kWarpRows; ++t) a.step_items[at++] = make_int4(x, t, t, 0);
+        // the step context of (problem, unit): K2a copies it in one round trip
+        const int64_t ci = sl.ctx_base + (x - sl.lo);
+        TileCtx c;
+        load_tile_ctx(a, sl.u, x, 0, c);
+        c.erow = nullptr; c.echg = nullptr; c.goff = nullptr; c.n_ent = 0; c.first_bp = 0;
+        *(reinterpret_cast<TileCtx *>(reinterpret_cast<char *>(a.step_ctx) + ci * kStepCtxBytes)) = c;
+        for (int t = lo / kWarpRows; t <= hi / kWarpRows; ++t) a.step_items[at++] = make_int4(x, t, t, (int)ci);
     }
     if (tid == 1023) a.step_count[blockIdx.x] = s_part[1023];
 }
@@ -529,8 +536,14 @@ __global__ void __launch_bounds__(kStepThreads, GROUP <= 1 ? 3 : 1)
         const int64_t it = (int64_t)blockIdx.x * kK2Warps + warp;
         if (it >= n_items) break;
         const int4 item = __ldg(items + it);
+        if (item.x != q_prev) {                          // the step context: one record, 8 B per lane
+            const unsigned long long *src = reinterpret_cast<const unsigned long long *>(
+                reinterpret_cast<const char *>(a.step_ctx) + (int64_t)item.w * kStepCtxBytes);
+            unsigned long long *dst = reinterpret_cast<unsigned long long *>(&t);
+            if (lane < (int)(sizeof(TileCtx) / 8)) dst[lane] = __ldg(src + lane);
+            __syncwarp();
+        }
         if (lane == 0) {
-            if (item.x != q_prev) load_tile_ctx(a, u, item.x, item.y, t);
             t.r_base = item.y * kWarpRows;
             t.erow = s_erow[warp]; t.echg = s_echg[warp]; t.goff = nullptr;
         }
