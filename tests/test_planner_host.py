@@ -98,3 +98,19 @@ def test_balance_degrees_reference_formula():
     costs = [StageCost(1.0, 1.0, 4.0), StageCost(3.0, 3.0, 4.0)]
     r = B.balance_degrees(costs)
     assert r.alpha_t == 1.0 - 3.0 / 4.0 and r.alpha_m == 0.5
+
+
+def test_partition_layers_is_a_lazy_sequence_of_slices():
+    """partition_layers (balance.py) returns the stages' layer lists; here built on access,
+    with the slices the batched search uses, and equal to the eager lists."""
+    from paper_2307_02031_b200 import workloads as W
+    from paper_2307_02031_b200.balance import PipelinePartition, StageLayers, partition_layers
+    from paper_2307_02031_b200.planner import _stage_ranges
+    model = W.config("bert").model
+    sl = partition_layers(model, PipelinePartition((5, 20, 7)))
+    assert isinstance(sl, StageLayers) and sl.ranges == [(0, 5), (5, 20), (25, 7)]
+    eager = [list(model.layers[0:5]), list(model.layers[5:25]), list(model.layers[25:32])]
+    assert len(sl) == 3 and sl == eager and [len(x) for x in sl] == [5, 20, 7]
+    assert all(a is b for a, b in zip(sl[1], eager[1]))
+    assert _stage_ranges(model, sl) == [(0, 5), (5, 20), (25, 7)]
+    assert _stage_ranges(model, eager) == [(0, 5), (5, 20), (25, 7)]
