@@ -19,6 +19,7 @@
 #include <memory>
 #include <tuple>
 #include <unordered_map>
+#include <unordered_set>
 
 static double now_ms() {
     return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
@@ -60,6 +61,7 @@ struct StratInfo {
     int status = GBMW_OK;
     std::string err;
     int32_t min_pp = 0, max_pp = 0;
+    int32_t cand_off = 0, class_off = 0;   // into the batch's concatenated candidate / class arrays
 };
 
 // Per (layer range, fusion flag): units and byte maxima for the 2^53 checks.
@@ -68,6 +70,7 @@ struct UnitInfo {
     int status = GBMW_OK;
     std::string err;
     int64_t max_bnd = 0, max_int = 0;
+    int32_t unit_off = 0;               // into the batch's concatenated unit arrays
 };
 
 // hash of the (begin, count, micro-batch / fuse) record keys
@@ -92,8 +95,10 @@ struct HostProb {
     // workspace footprint (elements)
     int64_t n_cells = 0, n_r = 0, n_bcells = 0, n_par = 0, n_tiles = 0, n_step_tiles = 0, n_flagw = 0, n_rmap = 0;
     size_t ws_bytes = 0;
-    bool head_ok = false;          // argument checks passed, strategy / unit records resolved
 };
+
+using StratKey = std::tuple<int32_t, int32_t, int64_t>;
+using UnitKey = std::tuple<int32_t, int32_t, int>;
 
 struct Chunk {
     std::vector<int> probs;        // host problem indices, sorted by (K group, U descending)
@@ -138,7 +143,6 @@ struct gbmw_ctx {
     bool arena_busy = false;
     // grow-only pinned staging buffer for uploads
     void *pinned = nullptr;
-    std::vector<char> blob;                  // descriptor staging, reused across batches (no page faults)
     void *seed_buf = nullptr;                // gbmw_seed_partitions_device buffers (grow-only)
     size_t seed_cap = 0;
     size_t pinned_cap = 0;
@@ -154,12 +158,16 @@ struct gbmw_batch {
     std::vector<gbmw_problem> problems;
     std::vector<HostProb> hp;
     std::vector<Chunk> chunks;
-    std::unordered_map<std::tuple<int32_t, int32_t, int64_t>, std::unique_ptr<StratInfo>, Key3Hash> strat_cache;
-    std::unordered_map<std::tuple<int32_t, int32_t, int>, std::unique_ptr<UnitInfo>, Key3Hash> unit_cache;
-    const StratInfo *strat_last = nullptr;   // last lookups (consecutive problems usually share them)
-    std::tuple<int32_t, int32_t, int64_t> strat_last_key{};
-    const UnitInfo *unit_last = nullptr;
-    std::tuple<int32_t, int32_t, int> unit_last_key{};
+    // one record per key, in first-appearance order (built in parallel once the keys are
+    // known), and their arrays concatenated (each chunk's descriptor block holds a copy)
+    std::vector<std::pair<StratKey, std::unique_ptr<StratInfo>>> strat_recs;
+    std::vector<std::pair<UnitKey, std::unique_ptr<UnitInfo>>> unit_recs;
+    // key -> record index, direct-indexed by strategy-list / layer-range start (touched slots
+    // are cleared on reuse)
+    std::vector<std::vector<std::pair<std::pair<int32_t, int64_t>, int32_t>>> strat_at;
+    std::vector<std::vector<std::pair<int32_t, int32_t>>> unit_at;
+    std::vector<int32_t> srec, urec;         // per problem: its records (-1: none)
+    std::vector<int32_t> g_cand, g_ccls, g_clsd, g_clst, g_uf, g_uc;
     int64_t total_plan = 0, total_frontier = 0;
     // device arena: inputs | chunk descriptor blocks | outputs
     void *arena = nullptr;
@@ -383,69 +391,57 @@ extern "C" int gbmw_ctx_destroy(gbmw_ctx *ctx) {
 namespace {
 
 // usable strategies + classes of one strategy list at one micro-batch (dpsearch.py:42-43)
-const StratInfo *strat_info(gbmw_batch &b, const gbmw_problem &P) {
-    auto key = std::make_tuple(P.strat_begin, P.n_strats, P.micro_batch);
-    if (b.strat_last && b.strat_last_key == key) return b.strat_last;   // consecutive problems share it
-    auto it = b.strat_cache.find(key);
-    if (it != b.strat_cache.end()) { b.strat_last = it->second.get(); b.strat_last_key = key; return b.strat_last; }
-    auto si = std::make_unique<StratInfo>();
-    for (int i = 0; i < P.n_strats && si->status == GBMW_OK; ++i) {
-        const gbmw_strategy &s = b.strats[P.strat_begin + i];
-        const int rc = check_strategy(s, &si->err);
-        if (rc) { si->status = rc; break; }
+void build_strat(const gbmw_batch &b, const StratKey &key, StratInfo &si) {
+    const int32_t begin = std::get<0>(key), n = std::get<1>(key);
+    const int64_t micro = std::get<2>(key);
+    for (int i = 0; i < n && si.status == GBMW_OK; ++i) {
+        const gbmw_strategy &s = b.strats[begin + i];
+        const int rc = check_strategy(s, &si.err);
+        if (rc) { si.status = rc; break; }
         const StratDeg d = strat_degrees(s);
-        if (P.micro_batch % d.data != 0) continue;
-        const int gi = P.strat_begin + i;
-        si->cand.push_back(gi);
-        si->min_pp = si->cand.size() == 1 ? s.pp_degree : std::min(si->min_pp, s.pp_degree);
-        si->max_pp = si->cand.size() == 1 ? s.pp_degree : std::max(si->max_pp, s.pp_degree);
+        if (micro % d.data != 0) continue;
+        si.cand.push_back(begin + i);
+        si.min_pp = si.cand.size() == 1 ? s.pp_degree : std::min(si.min_pp, s.pp_degree);
+        si.max_pp = si.cand.size() == 1 ? s.pp_degree : std::max(si.max_pp, s.pp_degree);
         int k = -1;                                   // (data, tp) classes in first-appearance order
-        for (int c = 0; c < (int)si->cls_d.size(); ++c)
-            if (si->cls_d[c] == d.data && si->cls_t[c] == d.tp) { k = c; break; }
-        if (k < 0) { k = (int)si->cls_d.size(); si->cls_d.push_back(d.data); si->cls_t.push_back(d.tp); }
-        si->cand_cls.push_back(k);
+        for (int c = 0; c < (int)si.cls_d.size(); ++c)
+            if (si.cls_d[c] == d.data && si.cls_t[c] == d.tp) { k = c; break; }
+        if (k < 0) { k = (int)si.cls_d.size(); si.cls_d.push_back(d.data); si.cls_t.push_back(d.tp); }
+        si.cand_cls.push_back(k);
     }
-    const StratInfo *out = si.get();
-    b.strat_cache.emplace(key, std::move(si));
-    return out;
 }
 
 // units of one stage (dpsearch.py:71-86): fusion key (kind, param, bnd, int, raw fwd_time, frac)
-const UnitInfo *unit_info(gbmw_batch &b, const gbmw_problem &P) {
-    const bool fuse = (P.flags & GBMW_FUSE) != 0;
-    auto key = std::make_tuple(P.layer_begin, P.n_layers, (int)fuse);
-    if (b.unit_last && b.unit_last_key == key) return b.unit_last;
-    auto it = b.unit_cache.find(key);
-    if (it != b.unit_cache.end()) { b.unit_last = it->second.get(); b.unit_last_key = key; return b.unit_last; }
-    auto ui = std::make_unique<UnitInfo>();
-    for (int i = 0; i < P.n_layers; ++i) {
-        const int gl = P.layer_begin + i;
+void build_unit(const gbmw_batch &b, const UnitKey &key, UnitInfo &ui) {
+    const int32_t begin = std::get<0>(key), n = std::get<1>(key);
+    const bool fuse = std::get<2>(key) != 0;
+    for (int i = 0; i < n; ++i) {
+        const int gl = begin + i;
         const gbmw_layer &B = b.layers[gl];
-        const int rc = check_layer(B, &ui->err);
-        if (rc) { ui->status = rc; break; }
-        ui->max_bnd = std::max(ui->max_bnd, B.bnd_bytes_per_sample);
-        ui->max_int = std::max(ui->max_int, B.int_bytes_per_sample);
-        if (fuse && !ui->unit_first.empty()) {
-            const gbmw_layer &A = b.layers[ui->unit_first.back()];
+        const int rc = check_layer(B, &ui.err);
+        if (rc) { ui.status = rc; break; }
+        ui.max_bnd = std::max(ui.max_bnd, B.bnd_bytes_per_sample);
+        ui.max_int = std::max(ui.max_int, B.int_bytes_per_sample);
+        if (fuse && !ui.unit_first.empty()) {
+            const gbmw_layer &A = b.layers[ui.unit_first.back()];
             if (A.kind_id == B.kind_id && A.param_bytes == B.param_bytes &&
                 A.bnd_bytes_per_sample == B.bnd_bytes_per_sample && A.int_bytes_per_sample == B.int_bytes_per_sample &&
                 A.fwd_time_raw == B.fwd_time_raw && A.tp_act_replication_fraction == B.tp_act_replication_fraction) {
-                ui->unit_count.back() += 1;
+                ui.unit_count.back() += 1;
                 continue;
             }
         }
-        ui->unit_first.push_back(gl);
-        ui->unit_count.push_back(1);
+        ui.unit_first.push_back(gl);
+        ui.unit_count.push_back(1);
     }
-    const UnitInfo *out = ui.get();
-    b.unit_cache.emplace(key, std::move(ui));
-    return out;
 }
 
-// dp_search argument checks and host bookkeeping (dpsearch.py:103-125)
+// dp_search argument checks and host bookkeeping (dpsearch.py:103-125), on the records the
+// key pass assigned
 void prepare_problem(gbmw_batch &b, int pi, std::string *err) {
     const gbmw_problem &P = b.problems[pi];
     HostProb &h = b.hp[pi];
+    h = HostProb();
     auto fail = [&](int code, const std::string &msg) { h.status = code; set_err(err, code, msg); };
     if (P.granularity_bytes <= 0) return fail(GBMW_EINVAL_GRAN, "granularity_bytes must be positive, got " + std::to_string(P.granularity_bytes));
     if (!(P.budget_bytes >= 0.0)) return fail(GBMW_EINVAL_BUDGET, "budget_bytes must be non-negative");
@@ -462,26 +458,14 @@ void prepare_problem(gbmw_batch &b, int pi, std::string *err) {
     if (P.env_index < 0 || P.env_index >= (int)b.envs.size()) return fail(GBMW_EINVAL, "problem env index out of bounds");
     if (P.budget_bytes >= kTwo53) return fail(GBMW_ERANGE, "budget_bytes must be < 2^53");
     h.n_b = P.n_buckets;
-    const StratInfo *si = strat_info(b, P);
+    const StratInfo *si = b.strat_recs[b.srec[pi]].second.get();   // assigned: both ranges are valid
     if (si->status) return fail(si->status, si->err);
     h.si = si;
     h.S = (int)si->cand.size();
     if (h.S == 0 || h.n_b == 0) return;    // infeasible, dpsearch.py:119-121
-    const UnitInfo *ui = unit_info(b, P);
+    const UnitInfo *ui = b.unit_recs[b.urec[pi]].second.get();
     if (ui->status) return fail(ui->status, ui->err);
     h.ui = ui;
-    h.head_ok = true;
-}
-
-// the rest of the checks and the sizes: reads only the problem and its (immutable) strategy
-// and unit records, so problems run in parallel
-void prepare_problem_tail(gbmw_batch &b, int pi, std::string *err) {
-    const gbmw_problem &P = b.problems[pi];
-    HostProb &h = b.hp[pi];
-    if (!h.head_ok) return;
-    auto fail = [&](int code, const std::string &msg) { h.status = code; set_err(err, code, msg); };
-    const StratInfo *si = h.si;
-    const UnitInfo *ui = h.ui;
     // layer_memory range checks (costs.py:207-210), raised on the first table cell
     if (P.stage_index < 1 || P.stage_index > si->min_pp)
         for (int32_t gi : si->cand) {
@@ -517,14 +501,6 @@ void prepare_problem_tail(gbmw_batch &b, int pi, std::string *err) {
                  (size_t)h.n_rmap * 8 + (size_t)(h.U > 1 ? h.U - 1 : 0) * 24 +
                  (size_t)h.n_step_tiles * 2 * (kK2SlotEntries * 4 + kK2HeavyBytes + kK2RoundsPerSlot * 8);
     h.gpu = true;
-}
-
-template <class T>
-size_t put(std::vector<char> &blob, const T *src, size_t n) {
-    const size_t off = align_up(blob.size(), 16);
-    blob.resize(off);
-    if (n) blob.insert(blob.end(), reinterpret_cast<const char *>(src), reinterpret_cast<const char *>(src + n));
-    return off;
 }
 
 // chunk workspace layout (byte offsets from ws base)
@@ -590,19 +566,93 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
     b->strats.assign(strategies, strategies + n_strategies);
     b->envs.assign(envs, envs + n_envs);
     b->problems.assign(problems, problems + n_problems);
-    b->hp.resize(n_problems);
+    if (b->hp.size() != (size_t)n_problems) b->hp.resize(n_problems);   // each record is reset below
     int first_err = GBMW_OK;
     std::string first_msg;
-    double t_head = 0.0;
+    double t_head = 0.0, th[3] = {0, 0, 0};
     {
-        // argument checks, shared strategy / unit records, sizes; the first failing problem
-        // (in input order) names the error.  Serial: host threads lost more to spawning and
-        // cache-line traffic on the problem records than they saved (measured, v78)
+        // argument checks, strategy / unit records, sizes; the first failing problem (in input
+        // order) names the error
         std::vector<std::string> msgs(n_problems);
-        for (int64_t i = 0; i < n_problems; ++i) {
-            prepare_problem(*b, (int)i, &msgs[i]);
-            prepare_problem_tail(*b, (int)i, &msgs[i]);
+        th[0] = now_ms();
+        // record keys of every problem whose ranges are valid, deduplicated in first-appearance
+        // order through the direct indexes (serial: ~10 ns a problem)
+        b->strat_recs.clear();
+        b->unit_recs.clear();
+        if (b->strat_at.size() < (size_t)n_strategies + 1) b->strat_at.resize(n_strategies + 1);
+        if (b->unit_at.size() < (size_t)n_layers + 1) b->unit_at.resize(n_layers + 1);
+        b->srec.assign(n_problems, -1);
+        b->urec.assign(n_problems, -1);
+        {
+            int32_t ls = -1, lu = -1;
+            StratKey lsk{};
+            UnitKey luk{};
+            for (int64_t i = 0; i < n_problems; ++i) {
+                const gbmw_problem &P = b->problems[i];
+                if (P.strat_begin >= 0 && P.n_strats >= 0 && (int64_t)P.strat_begin + P.n_strats <= n_strategies &&
+                    P.micro_batch >= 1) {
+                    const StratKey k = std::make_tuple(P.strat_begin, P.n_strats, P.micro_batch);
+                    if (ls < 0 || k != lsk) {
+                        auto &slot = b->strat_at[P.strat_begin];
+                        ls = -1;
+                        for (const auto &e : slot)
+                            if (e.first.first == P.n_strats && e.first.second == P.micro_batch) { ls = e.second; break; }
+                        if (ls < 0) {
+                            ls = (int32_t)b->strat_recs.size();
+                            slot.push_back({{P.n_strats, P.micro_batch}, ls});
+                            b->strat_recs.emplace_back(k, nullptr);
+                        }
+                        lsk = k;
+                    }
+                    b->srec[i] = ls;
+                }
+                if (P.layer_begin >= 0 && P.n_layers > 0 && (int64_t)P.layer_begin + P.n_layers <= n_layers) {
+                    const UnitKey k = std::make_tuple(P.layer_begin, P.n_layers, (P.flags & GBMW_FUSE) ? 1 : 0);
+                    if (lu < 0 || k != luk) {
+                        auto &slot = b->unit_at[P.layer_begin];
+                        const int32_t k2 = P.n_layers * 2 + std::get<2>(k);
+                        lu = -1;
+                        for (const auto &e : slot)
+                            if (e.first == k2) { lu = e.second; break; }
+                        if (lu < 0) {
+                            lu = (int32_t)b->unit_recs.size();
+                            slot.push_back({k2, lu});
+                            b->unit_recs.emplace_back(k, nullptr);
+                        }
+                        luk = k;
+                    }
+                    b->urec[i] = lu;
+                }
+            }
+            for (const auto &r : b->strat_recs) b->strat_at[std::get<0>(r.first)].clear();   // for the next batch
+            for (const auto &r : b->unit_recs) b->unit_at[std::get<0>(r.first)].clear();
         }
+        th[1] = now_ms();
+        // the records, and the concatenated arrays the descriptors point into
+        b->g_cand.clear(); b->g_ccls.clear(); b->g_clsd.clear(); b->g_clst.clear(); b->g_uf.clear(); b->g_uc.clear();
+        for (auto &e : b->strat_recs) {
+            e.second.reset(new StratInfo());
+            StratInfo &si = *e.second;
+            build_strat(*b, e.first, si);
+            if (si.status != GBMW_OK) continue;
+            si.cand_off = (int32_t)b->g_cand.size();
+            si.class_off = (int32_t)b->g_clsd.size();
+            b->g_cand.insert(b->g_cand.end(), si.cand.begin(), si.cand.end());
+            b->g_ccls.insert(b->g_ccls.end(), si.cand_cls.begin(), si.cand_cls.end());
+            b->g_clsd.insert(b->g_clsd.end(), si.cls_d.begin(), si.cls_d.end());
+            b->g_clst.insert(b->g_clst.end(), si.cls_t.begin(), si.cls_t.end());
+        }
+        for (auto &e : b->unit_recs) {
+            e.second.reset(new UnitInfo());
+            UnitInfo &ui = *e.second;
+            build_unit(*b, e.first, ui);
+            if (ui.status != GBMW_OK) continue;
+            ui.unit_off = (int32_t)b->g_uf.size();
+            b->g_uf.insert(b->g_uf.end(), ui.unit_first.begin(), ui.unit_first.end());
+            b->g_uc.insert(b->g_uc.end(), ui.unit_count.begin(), ui.unit_count.end());
+        }
+        th[2] = now_ms();
+        for (int64_t i = 0; i < n_problems; ++i) prepare_problem(*b, (int)i, &msgs[i]);
         t_head = now_ms();
         for (int64_t i = 0; i < n_problems; ++i)
             if (b->hp[i].status != GBMW_OK) { first_err = b->hp[i].status; first_msg = msgs[i]; break; }
@@ -644,142 +694,61 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
     }
     flush();
     const double t_chunks = now_ms();
-    // per-chunk descriptors
-    std::vector<char> &blob = ctx->blob;
-    blob.clear();
-    {
-        size_t est = 0;                                  // one allocation for the descriptor blob
-        for (const Chunk &c : b->chunks) {
-            int64_t st = 0;
-            for (int pi : c.probs) st += b->hp[pi].n_step_tiles;
-            est += c.probs.size() * (sizeof(DevProblem) + 3 * 8 + 64) + (size_t)st * 4 + 64 * 1024;
-        }
-        blob.reserve(est);
-    }
-    double td[6] = {0, 0, 0, 0, 0, 0};
+    // per-chunk descriptor layout: problem order, groups, totals
+    double td[4] = {0, 0, 0, 0};
+    size_t blob_size = 0;
     for (Chunk &c : b->chunks) {
         double tq = now_ms();
+        const int np = (int)c.probs.size();
         {
             // (group ascending, U descending, input order): a stable counting sort on the
-            // bucket g * (kMaxUnits + 1) + (kMaxUnits - U)
-            const size_t nb = (size_t)kNumGroups * (kMaxUnits + 1);
-            std::vector<int32_t> bucket(c.probs.size()), start(nb + 1, 0);
-            for (size_t i = 0; i < c.probs.size(); ++i) {
-                const int x = c.probs[i];
-                const int g = problem_group(b->hp[x].K, b->problems[x].flags, b->hp[x].U);
-                bucket[i] = g * (kMaxUnits + 1) + (kMaxUnits - std::min(b->hp[x].U, kMaxUnits));
+            // bucket g * (kMaxUnits + 1) + (kMaxUnits - U); groups and the per-unit active
+            // counts follow from the bucket histogram
+            constexpr int nu = kMaxUnits + 1;
+            const size_t nb = (size_t)kNumGroups * nu;
+            std::vector<int32_t> bucket(np), start(nb + 1, 0);
+            for (int i = 0; i < np; ++i) {
+                const HostProb &h = b->hp[c.probs[i]];
+                const int g = problem_group(h.K, b->problems[c.probs[i]].flags, h.U);
+                bucket[i] = g * nu + (kMaxUnits - h.U);             // U <= kMaxUnits (checked)
                 start[bucket[i] + 1]++;
             }
+            c.Umax = 0;
+            for (size_t k = 0; k < nb; ++k)
+                if (start[k + 1]) c.Umax = std::max(c.Umax, kMaxUnits - (int)(k % nu));
             for (size_t k = 0; k < nb; ++k) start[k + 1] += start[k];
-            std::vector<int> sorted(c.probs.size());
-            for (size_t i = 0; i < c.probs.size(); ++i) sorted[start[bucket[i]]++] = c.probs[i];
+            for (int g = 0; g < kNumGroups; ++g) {
+                c.group_lo[g] = start[(size_t)g * nu];
+                c.group_lo[g + 1] = start[(size_t)(g + 1) * nu];
+                c.n_active[g].assign(c.Umax + 1, 0);      // problems of the group with U > u
+                for (int u = c.Umax, above = 0; u >= 0; --u) {
+                    c.n_active[g][u] = above;
+                    const size_t k = (size_t)g * nu + (kMaxUnits - u);
+                    above += start[k + 1] - start[k];
+                }
+            }
+            std::vector<int> sorted(np);
+            for (int i = 0; i < np; ++i) sorted[start[bucket[i]]++] = c.probs[i];
             c.probs.swap(sorted);
         }
+        c.step_prefix.resize(np + 1);
+        c.step_prefix[0] = 0;
+        for (int x = 0; x < np; ++x) c.step_prefix[x + 1] = c.step_prefix[x] + b->hp[c.probs[x]].n_step_tiles;
         td[0] += now_ms() - tq; tq = now_ms();
-        std::vector<DevProblem> dps;
-        std::vector<int64_t> cellp{0}, rp{0}, stepp{0};
-        dps.reserve(c.probs.size());
-        cellp.reserve(c.probs.size() + 1); rp.reserve(c.probs.size() + 1); stepp.reserve(c.probs.size() + 1);
-        std::vector<int2> aux;
-        std::vector<int32_t> cand, ccls, clsd, clst, uf, uc;
-        std::unordered_map<const StratInfo *, std::pair<int32_t, int32_t>> soff;
-        std::unordered_map<const UnitInfo *, int32_t> uoff;
-        const StratInfo *last_si = nullptr;
-        const UnitInfo *last_ui = nullptr;
-        std::pair<int32_t, int32_t> last_soff{0, 0};
-        int32_t last_uoff = 0;
-        for (int pi : c.probs) {
-            const HostProb &h = b->hp[pi];
-            const gbmw_problem &P = b->problems[pi];
-            DevProblem d;
-            std::memset(&d, 0, sizeof(d));
-            d.U = h.U; d.S = h.S; d.K = h.K; d.flags = P.flags;
-            d.n_layers = P.n_layers; d.stage_index = P.stage_index; d.n_micro = P.n_micro; d.env_index = P.env_index;
-            d.n_b = h.n_b; d.micro = P.micro_batch; d.gran = P.granularity_bytes; d.budget = P.budget_bytes;
-            d.cell_off = c.n_cells; d.r_off = c.n_r; d.b_off = c.n_bcells; d.par_off = c.n_par; d.tile_off = c.n_tiles;
-            d.plan_off = h.plan_off; d.frontier_off = h.frontier_off;
-            if (h.si != last_si) {                      // sorted problems share records in runs
-                auto sit = soff.find(h.si);
-                if (sit == soff.end()) {
-                    sit = soff.emplace(h.si, std::make_pair((int32_t)cand.size(), (int32_t)clsd.size())).first;
-                    cand.insert(cand.end(), h.si->cand.begin(), h.si->cand.end());
-                    ccls.insert(ccls.end(), h.si->cand_cls.begin(), h.si->cand_cls.end());
-                    clsd.insert(clsd.end(), h.si->cls_d.begin(), h.si->cls_d.end());
-                    clst.insert(clst.end(), h.si->cls_t.begin(), h.si->cls_t.end());
-                }
-                last_si = h.si; last_soff = sit->second;
-            }
-            if (h.ui != last_ui) {
-                auto uit = uoff.find(h.ui);
-                if (uit == uoff.end()) {
-                    uit = uoff.emplace(h.ui, (int32_t)uf.size()).first;
-                    uf.insert(uf.end(), h.ui->unit_first.begin(), h.ui->unit_first.end());
-                    uc.insert(uc.end(), h.ui->unit_count.begin(), h.ui->unit_count.end());
-                }
-                last_ui = h.ui; last_uoff = uit->second;
-            }
-            d.cand_off = last_soff.first; d.class_off = last_soff.second; d.unit_off = last_uoff;
-            d.ustate_off = (int32_t)c.n_units;
-            d.flag_off = c.n_flagw;
-            d.rmap_off = c.n_rmap;
-            d.layer_begin = P.layer_begin; d.strat_begin = P.strat_begin; d.result_index = pi;
-            d.n_sweep_tiles = (int32_t)h.n_tiles;
-            dps.push_back(d);
+        // the chunk's totals (the block layout needs them before the descriptors are written)
+        c.n_cells = c.n_r = c.n_bcells = c.n_par = c.n_tiles = c.n_units = c.n_flagw = c.n_rmap = c.n_aux = 0;
+        c.n_approx = 0;
+        c.max_k = 1;
+        for (int x = 0; x < np; ++x) {
+            const HostProb &h = b->hp[c.probs[x]];
+            const int flags = b->problems[c.probs[x]].flags;
             c.n_cells += h.n_cells; c.n_r += h.n_r; c.n_bcells += h.n_bcells; c.n_par += h.n_par; c.n_tiles += h.n_tiles;
-            cellp.push_back(c.n_cells); rp.push_back(c.n_r);
-            stepp.push_back(stepp.back() + h.n_step_tiles);
-            c.n_units += h.U;
-            c.n_flagw += h.n_flagw;
-            c.n_rmap += h.n_rmap;
-            c.Umax = std::max(c.Umax, h.U);
-            if (P.flags & GBMW_APPROX) c.n_approx++;
+            c.n_units += h.U; c.n_flagw += h.n_flagw; c.n_rmap += h.n_rmap;
+            if (flags & (GBMW_FRONTIER | GBMW_APPROX)) c.n_aux += h.n_tiles;   // every row swept (K3r)
+            if (flags & GBMW_APPROX) c.n_approx++;
             c.max_k = std::max(c.max_k, h.K);
         }
         td[1] += now_ms() - tq; tq = now_ms();
-        c.step_prefix = stepp;
-        // groups are contiguous in sorted order; within a group U is descending, so
-        // the problems still active at unit u are a prefix of the group
-        const int np = (int)c.probs.size();
-        for (int g = 0, s = 0; g < kNumGroups; ++g) {
-            c.group_lo[g] = s;
-            while (s < np && problem_group(b->hp[c.probs[s]].K, b->problems[c.probs[s]].flags, b->hp[c.probs[s]].U) == g) ++s;
-            c.group_lo[g + 1] = s;
-            // problems with U > u, from a histogram of U (suffix sums)
-            c.n_active[g].assign(c.Umax + 1, 0);
-            std::vector<int> hist(c.Umax + 2, 0);
-            for (int x = c.group_lo[g]; x < s; ++x) hist[std::min(b->hp[c.probs[x]].U, c.Umax + 1)]++;
-            for (int u = c.Umax, above = hist[c.Umax + 1]; u >= 0; --u) {
-                c.n_active[g][u] = above;                // problems with U > u
-                above += hist[u];
-            }
-        }
-        td[2] += now_ms() - tq; tq = now_ms();
-        // K2 tile -> problem map: only the collapsed-DP step (K2c) still walks 2048-row tiles
-        std::vector<int32_t> stepmap(c.n_approx > 0 ? stepp.back() : 0);
-        for (int x = 0; x < np; ++x) {
-            if (c.n_approx > 0)
-                for (int64_t t = stepp[x]; t < stepp[x + 1]; ++t) stepmap[t] = x;
-            // every row of frontier / collapsed-DP problems is swept (K3r)
-            if (b->problems[c.probs[x]].flags & (GBMW_FRONTIER | GBMW_APPROX))
-                for (int t = 0; t < dps[x].n_sweep_tiles; ++t) aux.push_back(make_int2(x, t));
-        }
-        c.n_aux = (int64_t)aux.size();
-        td[3] += now_ms() - tq; tq = now_ms();
-        const size_t base = align_up(blob.size(), 256);
-        blob.resize(base);
-        c.small_off = base;
-        c.o_probs = put(blob, dps.data(), dps.size()) - base;
-        c.o_cellp = put(blob, cellp.data(), cellp.size()) - base;
-        c.o_rp = put(blob, rp.data(), rp.size()) - base;
-        c.o_stepp = put(blob, stepp.data(), stepp.size()) - base;
-        c.o_cand = put(blob, cand.data(), cand.size()) - base;
-        c.o_ccls = put(blob, ccls.data(), ccls.size()) - base;
-        c.o_clsd = put(blob, clsd.data(), clsd.size()) - base;
-        c.o_clst = put(blob, clst.data(), clst.size()) - base;
-        c.o_uf = put(blob, uf.data(), uf.size()) - base;
-        c.o_uc = put(blob, uc.data(), uc.size()) - base;
-        c.o_stepmap = put(blob, stepmap.data(), stepmap.size()) - base;
-        c.o_aux = put(blob, aux.data(), aux.size()) - base;
         // K2 launches: items bounded by all tiles of the active problems
         c.slists.clear(); c.slist_group.clear(); c.slist_second.clear(); c.n_items = 0; c.n_ctx = 0;
         static const bool no_second = getenv("GBMW_NO_SECOND") && getenv("GBMW_NO_SECOND")[0] == '1';
@@ -803,30 +772,112 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
                 // 2048-row tiles)
                 if (!sl.no_items) c.n_items += 2 * (c.step_prefix[lo + na] - c.step_prefix[lo]);
             }
-        c.o_slists = put(blob, c.slists.data(), c.slists.size()) - base;
-        td[4] += now_ms() - tq; tq = now_ms();
-        c.small_bytes = blob.size() - base;
+        // the chunk's descriptor block (16-byte aligned arrays), 256-byte aligned in the blob
+        size_t o = 0;
+        auto lay = [&](size_t bytes) { o = align_up(o, 16); const size_t at = o; o += bytes; return at; };
+        c.o_probs = lay((size_t)np * sizeof(DevProblem));
+        c.o_cellp = lay((size_t)(np + 1) * 8);
+        c.o_rp = lay((size_t)(np + 1) * 8);
+        c.o_stepp = lay((size_t)(np + 1) * 8);
+        c.o_cand = lay(b->g_cand.size() * 4);
+        c.o_ccls = lay(b->g_ccls.size() * 4);
+        c.o_clsd = lay(b->g_clsd.size() * 4);
+        c.o_clst = lay(b->g_clst.size() * 4);
+        c.o_uf = lay(b->g_uf.size() * 4);
+        c.o_uc = lay(b->g_uc.size() * 4);
+        c.o_stepmap = lay(c.n_approx > 0 ? (size_t)c.step_prefix[np] * 4 : 0);
+        c.o_aux = lay((size_t)c.n_aux * sizeof(int2));
+        c.o_slists = lay(c.slists.size() * sizeof(StepList));
+        c.small_bytes = o;
+        c.small_off = align_up(blob_size, 256);
+        blob_size = c.small_off + c.small_bytes;
         c.ws_bytes = ws_layout(c).total;
         b->max_ws = std::max(b->max_ws, c.ws_bytes);
+        td[2] += now_ms() - tq;
     }
-    const double t_prep = now_ms();
-    if (getenv("GBMW_K2_HIST") && getenv("GBMW_K2_HIST")[0] == '1')
-        fprintf(stderr, "create: head %.3f ms, ", t_head - t_start),
-        fprintf(stderr, "problems %.3f ms, chunking %.3f ms, descriptors %.3f ms (sort %.3f loop %.3f groups %.3f "
-                "stepmap %.3f puts %.3f)\n", t_probs - t_start, t_chunks - t_probs, t_prep - t_chunks, td[0], td[1], td[2],
-                td[3], td[4]);
-    // arena: inputs | descriptor blob | outputs
+    // arena: inputs | descriptor blocks | outputs
     size_t o = 0;
     b->o_layers = o; o = align_up(o + b->layers.size() * sizeof(gbmw_layer));
     b->o_strats = o; o = align_up(o + b->strats.size() * sizeof(gbmw_strategy));
     b->o_envs = o; o = align_up(o + b->envs.size() * sizeof(gbmw_env));
-    const size_t o_blob = o; o = align_up(o + blob.size());
+    const size_t o_blob = o; o = align_up(o + blob_size);
     b->o_results = o; o = align_up(o + b->problems.size() * sizeof(gbmw_result));
     b->o_plans = o; o = align_up(o + (size_t)b->total_plan * sizeof(int32_t));
     b->o_frontier = o; o = align_up(o + (size_t)b->total_frontier * sizeof(double));
     b->o_stats = o; o = align_up(o + (5 * (b->chunks.size() + 1) + 64) * 8);
     b->arena_size = std::max<size_t>(o, 256);
     for (Chunk &c : b->chunks) c.small_off += o_blob;
+    // the input part of the arena is staged in pinned memory: descriptors are written there directly
+    const size_t up = o_blob + blob_size;
+    if (ctx->pinned_cap < up) {
+        if (ctx->pinned) cudaFreeHost(ctx->pinned);
+        ctx->pinned = nullptr;
+        ctx->pinned_cap = 0;
+        const size_t cap = std::max<size_t>(up + up / 4, 1u << 20);
+        if (cudaHostAlloc(&ctx->pinned, cap, cudaHostAllocDefault) == cudaSuccess) ctx->pinned_cap = cap;
+    }
+    std::vector<char> fallback;
+    char *host = (char *)ctx->pinned;
+    if (!host) { fallback.resize(up); host = fallback.data(); }
+    const double t_fill = now_ms();
+    if (!b->layers.empty()) std::memcpy(host + b->o_layers, b->layers.data(), b->layers.size() * sizeof(gbmw_layer));
+    if (!b->strats.empty()) std::memcpy(host + b->o_strats, b->strats.data(), b->strats.size() * sizeof(gbmw_strategy));
+    if (!b->envs.empty()) std::memcpy(host + b->o_envs, b->envs.data(), b->envs.size() * sizeof(gbmw_env));
+    for (Chunk &c : b->chunks) {
+        // the descriptors, written in place
+        char *blk = host + c.small_off;
+        const int np = (int)c.probs.size();
+        auto cpy = [&](size_t off, const std::vector<int32_t> &v) { if (!v.empty()) std::memcpy(blk + off, v.data(), v.size() * 4); };
+        cpy(c.o_cand, b->g_cand); cpy(c.o_ccls, b->g_ccls); cpy(c.o_clsd, b->g_clsd); cpy(c.o_clst, b->g_clst);
+        cpy(c.o_uf, b->g_uf); cpy(c.o_uc, b->g_uc);
+        std::memcpy(blk + c.o_stepp, c.step_prefix.data(), (size_t)(np + 1) * 8);
+        if (!c.slists.empty()) std::memcpy(blk + c.o_slists, c.slists.data(), c.slists.size() * sizeof(StepList));
+        DevProblem *dps = (DevProblem *)(blk + c.o_probs);
+        int64_t *cellp = (int64_t *)(blk + c.o_cellp), *rp = (int64_t *)(blk + c.o_rp);
+        int32_t *stepmap = (int32_t *)(blk + c.o_stepmap);
+        int2 *aux = (int2 *)(blk + c.o_aux);
+        cellp[0] = 0;
+        rp[0] = 0;
+        const bool map_steps = c.n_approx > 0;        // K2 tile -> problem map of the collapsed-DP step (K2c)
+        {
+            int64_t s[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};   // cells r bcells par tiles units flagw rmap aux
+            for (int x = 0; x < np; ++x) {
+                const int pi = c.probs[x];
+                const HostProb &h = b->hp[pi];
+                const gbmw_problem &P = b->problems[pi];
+                DevProblem d;
+                std::memset(&d, 0, sizeof(d));
+                d.U = h.U; d.S = h.S; d.K = h.K; d.flags = P.flags;
+                d.n_layers = P.n_layers; d.stage_index = P.stage_index; d.n_micro = P.n_micro; d.env_index = P.env_index;
+                d.n_b = h.n_b; d.micro = P.micro_batch; d.gran = P.granularity_bytes; d.budget = P.budget_bytes;
+                d.cell_off = s[0]; d.r_off = s[1]; d.b_off = s[2]; d.par_off = s[3]; d.tile_off = s[4];
+                d.plan_off = h.plan_off; d.frontier_off = h.frontier_off;
+                d.cand_off = h.si->cand_off; d.class_off = h.si->class_off; d.unit_off = h.ui->unit_off;
+                d.ustate_off = (int32_t)s[5];
+                d.flag_off = s[6];
+                d.rmap_off = s[7];
+                d.layer_begin = P.layer_begin; d.strat_begin = P.strat_begin; d.result_index = pi;
+                d.n_sweep_tiles = (int32_t)h.n_tiles;
+                std::memcpy(dps + x, &d, sizeof(d));
+                s[0] += h.n_cells; s[1] += h.n_r; s[2] += h.n_bcells; s[3] += h.n_par; s[4] += h.n_tiles;
+                s[5] += h.U; s[6] += h.n_flagw; s[7] += h.n_rmap;
+                cellp[x + 1] = s[0];
+                rp[x + 1] = s[1];
+                if (map_steps)
+                    for (int64_t q = c.step_prefix[x]; q < c.step_prefix[x + 1]; ++q) stepmap[q] = x;
+                if (P.flags & (GBMW_FRONTIER | GBMW_APPROX))
+                    for (int q = 0; q < d.n_sweep_tiles; ++q) aux[s[8]++] = make_int2(x, q);
+            }
+        }
+    }
+    const double t_prep = now_ms();
+    td[3] = t_prep - t_fill;
+    static const bool host_timing = getenv("GBMW_HOST_TIMING") && getenv("GBMW_HOST_TIMING")[0] == '1';
+    if (host_timing)
+        fprintf(stderr, "create: problems %.3f ms (inputs %.3f keys %.3f records %.3f checks+sizes %.3f), "
+                "chunking %.3f ms, descriptors %.3f ms (sort %.3f sums %.3f layout %.3f fill %.3f)\n",
+                t_probs - t_start, th[0] - t_start, th[1] - th[0], th[2] - th[1], t_head - th[2], t_chunks - t_probs,
+                t_prep - t_chunks, td[0], td[1], td[2], td[3]);
     cudaSetDevice(ctx->device);
     b->ctx = ctx;
     cudaError_t ce = cudaSuccess;
@@ -851,22 +902,7 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
         delete b;
         return set_err(&ctx->err, GBMW_ENOMEM, std::string("cudaMalloc(arena): ") + cudaGetErrorString(ce));
     }
-    // one staged upload of the input part of the arena, through pinned memory
-    const size_t up = o_blob + blob.size();
-    if (ctx->pinned_cap < up) {
-        if (ctx->pinned) cudaFreeHost(ctx->pinned);
-        ctx->pinned = nullptr;
-        ctx->pinned_cap = 0;
-        const size_t cap = std::max<size_t>(up + up / 4, 1u << 20);
-        if (cudaHostAlloc(&ctx->pinned, cap, cudaHostAllocDefault) == cudaSuccess) ctx->pinned_cap = cap;
-    }
-    std::vector<char> fallback;
-    char *host = (char *)ctx->pinned;
-    if (!host) { fallback.resize(up); host = fallback.data(); }
-    if (!b->layers.empty()) std::memcpy(host + b->o_layers, b->layers.data(), b->layers.size() * sizeof(gbmw_layer));
-    if (!b->strats.empty()) std::memcpy(host + b->o_strats, b->strats.data(), b->strats.size() * sizeof(gbmw_strategy));
-    if (!b->envs.empty()) std::memcpy(host + b->o_envs, b->envs.data(), b->envs.size() * sizeof(gbmw_env));
-    if (!blob.empty()) std::memcpy(host + o_blob, blob.data(), blob.size());
+    // one upload of the input part of the arena
     ce = cudaMemcpyAsync(b->arena, host, up, cudaMemcpyHostToDevice, ctx->stream);
     if (ce == cudaSuccess) ce = cudaStreamSynchronize(ctx->stream);
     b->timing.h2d_bytes = (double)up;
@@ -1350,10 +1386,9 @@ extern "C" int gbmw_batch_destroy(gbmw_batch *b) {
     if (ctx && !ctx->spare) {
         // keep the batch's host vectors (their capacity) for the next gbmw_batch_create on
         // this context: a 10k-search batch otherwise page-faults ~2 MB of fresh buffers
-        b->layers.clear(); b->strats.clear(); b->envs.clear(); b->problems.clear(); b->hp.clear();
-        b->chunks.clear(); b->strat_cache.clear(); b->unit_cache.clear();
-        b->strat_last = nullptr; b->unit_last = nullptr;
-        b->strat_last_key = {}; b->unit_last_key = {};
+        b->layers.clear(); b->strats.clear(); b->envs.clear(); b->problems.clear();   // hp keeps its records
+        b->chunks.clear();
+        b->strat_recs.clear(); b->unit_recs.clear();
         b->total_plan = b->total_frontier = 0;
         b->arena = nullptr; b->arena_size = 0;
         b->o_layers = b->o_strats = b->o_envs = b->o_results = b->o_plans = b->o_frontier = b->o_stats = 0;
