@@ -207,20 +207,20 @@ _records: dict = {}
 
 
 def strategies_array(strats) -> np.ndarray:
-    """STRATEGY_DT records of a strategy sequence.  A strategy's record is built once per
-    object (strategies are frozen dataclasses; the cached entry keeps the object alive, so
-    its id cannot be reused while cached)."""
-    recs = []
+    """STRATEGY_DT records of a strategy sequence.  A strategy's record bytes are built once
+    per object (strategies are frozen dataclasses; the cached entry keeps the object alive, so
+    its id cannot be reused while cached) and the array is one join of them."""
+    parts = []
     cache = _records
     for s in strats:
         hit = cache.get(id(s))
         if hit is None or hit[0] is not s:
             if len(cache) > 8192:
                 cache.clear()
-            hit = (s, strategy_record(s))
+            hit = (s, np.array([strategy_record(s)], dtype=STRATEGY_DT).tobytes())
             cache[id(s)] = hit
-        recs.append(hit[1])
-    return np.array(recs, dtype=STRATEGY_DT) if recs else np.zeros(0, dtype=STRATEGY_DT)
+        parts.append(hit[1])
+    return np.frombuffer(bytearray(b"".join(parts)), dtype=STRATEGY_DT)
 
 
 def _i64(v, what):

@@ -118,6 +118,13 @@ class _Marshal:
             self.layer_ranges[key] = hit
         return hit
 
+    def layer_table(self, arr) -> int:
+        """Append a prebuilt LAYER_DT table (its kind ids its own: only for a batch whose
+        layers all come from this one table)."""
+        assert not self.layers, "a prebuilt layer table must be the batch's only one"
+        self.layers.append(arr)
+        return 0
+
     def strat_range(self, strategies, strat_list) -> int:
         # a mutable container is keyed on its elements as they are now
         key = id(strategies) if _frozen(strategies) else tuple(id(x) for x in strat_list)

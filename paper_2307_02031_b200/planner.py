@@ -12,8 +12,10 @@ planner.py:241-277), so the returned plan is the one the reference returns.
 from __future__ import annotations
 
 import ctypes
+import gc
+import sys
 from dataclasses import dataclass
-from functools import lru_cache
+from functools import lru_cache, wraps
 from typing import Any, Sequence
 
 import numpy as np
@@ -34,6 +36,7 @@ from .balance import (
 from .costs import EvalContext, StageCost, layer_memory, pipeline_cost, stage_cost
 from .dpsearch import StageProblem, dp_search_batch
 from .errors import InfeasiblePlanError
+from .specs import CostProfile
 from .strategies import (
     ParallelStrategy,
     candidate_pp_degrees,
@@ -157,16 +160,43 @@ def _cell_setup(n_devices: int, pp: int, batch: int, cap_factor: int, min_micro:
     return m, micro, sset, any(micro % s.data_degree == 0 for s in sset.strategies)
 
 
-def _search_slices(cells, ctx, opts, defer_errors=False):
-    """galvatron_search for cells whose stages are slices of ctx.model: one flat problem
-    table over a single copy of the model's layers, no per-stage Python objects.  With
-    ``defer_errors`` a cell whose stage search fails yields a ``FailedOutcome`` instead of
-    raising for the whole batch."""
+_layer_tables: dict = {}
+
+
+def _model_layer_table(ctx):
+    """LAYER_DT table of ctx.model's layers under ctx.profile, built once per EvalContext
+    object (a planner driver runs many batches on one).  Model, cluster and profile are frozen
+    dataclasses except the profile's override mapping, which is compared on every call, so a
+    changed override is re-read as the reference re-reads it."""
     from . import _native
-    from .dpsearch import MAX_BUCKETS, _Marshal, run_native_batch
+    prof = ctx.profile
+    ov = getattr(prof, "layer_overrides", None)
+    if not isinstance(prof, CostProfile) or not isinstance(ov, dict) or not isinstance(ctx.model.layers, tuple):
+        return _native.layers_array(list(ctx.model.layers), prof, {})
+    hit = _layer_tables.get(id(ctx))
+    if hit is None or hit[0] is not ctx or hit[1] != ov:
+        if len(_layer_tables) > 64:
+            _layer_tables.clear()
+        hit = (ctx, dict(ov), _native.layers_array(list(ctx.model.layers), prof, {}))
+        _layer_tables[id(ctx)] = hit
+    return hit[2]
+
+
+class _SlicedBatch:
+    """The flat problem table of a window of sliced cells (built by ``_slices_prepare``), its
+    native results once run (``_slices_native``), turned into outcomes by ``_slices_finish``."""
+    __slots__ = ("metas", "tables", "probs")
+
+    def __init__(self, metas, tables, probs):
+        self.metas, self.tables, self.probs = metas, tables, probs
+
+
+def _slices_prepare(cells, ctx, opts) -> _SlicedBatch:
+    from . import _native
+    from .dpsearch import MAX_BUCKETS, _Marshal
     gran = opts.granularity_bytes
     mar = _Marshal()
-    base = mar.layer_range(list(ctx.model.layers), ctx.profile)
+    base = mar.layer_table(_model_layer_table(ctx))
     env = mar.env(ctx)
     flags = _native.STAGE_COST | (_native.FUSE if opts.fuse_identical else 0) | \
         (_native.APPROX if opts.approx_prev else 0)
@@ -174,7 +204,6 @@ def _search_slices(cells, ctx, opts, defer_errors=False):
     starts, lens, cell_rows, cell_vals = [], [], [], []
     metas = []
     n_rows = 0
-    rc = _native.OK
     for budget, ranges, n_devices, batch, pp in cells:
         m, micro, sset, usable = _cell_setup(n_devices, pp, batch, opts.microbatch_cap_factor, opts.min_micro_size)
         strats = sset.strategies
@@ -198,38 +227,55 @@ def _search_slices(cells, ctx, opts, defer_errors=False):
         cell_vals.append((sb, len(strats), m, micro, float(budget), nb))
         metas.append((m, n_rows, n_rows + k, strats))
         n_rows += k
+    if not n_rows:
+        return _SlicedBatch(metas, None, None)
+    layers, loffs, strats_arr, soffs, envs = mar.finish()
+    probs = np.zeros(n_rows, dtype=_native.PROBLEM_DT)
+    reps = np.asarray(cell_rows, dtype=np.int64)
+    cv = list(zip(*cell_vals))
+    probs["layer_begin"] = np.asarray(starts, dtype=np.int64) + (base + loffs[0])
+    probs["n_layers"] = lens
+    probs["strat_begin"] = np.repeat(np.asarray([soffs[x] for x in cv[0]], dtype=np.int64), reps)
+    probs["n_strats"] = np.repeat(np.asarray(cv[1], dtype=np.int64), reps)
+    probs["env_index"] = env
+    # stage_index = 1 .. P within each cell
+    first = np.repeat(np.cumsum(reps) - reps, reps)
+    probs["stage_index"] = np.arange(n_rows, dtype=np.int64) - first + 1
+    probs["n_micro"] = np.repeat(np.asarray(cv[2], dtype=np.int64), reps)
+    probs["flags"] = flags
+    probs["micro"] = np.repeat(np.asarray(cv[3], dtype=np.int64), reps)
+    probs["gran"] = gran
+    probs["budget"] = np.repeat(np.asarray(cv[4], dtype=np.float64), reps)
+    probs["n_buckets"] = np.repeat(np.asarray(cv[5], dtype=np.int64), reps)
+    return _SlicedBatch(metas, (layers, strats_arr, envs), probs)
+
+
+def _slices_native(sb: _SlicedBatch):
+    """The device pass of a prepared window (blocking; the ctypes call releases the GIL)."""
+    from .dpsearch import run_native_batch
+    if sb.tables is None:
+        return None
+    layers, strats_arr, envs = sb.tables
+    return run_native_batch(layers, strats_arr, envs, sb.probs)
+
+
+def _slices_finish(sb: _SlicedBatch, native, defer_errors=False):
+    from . import _native
     out = []
-    if n_rows:
-        layers, loffs, strats_arr, soffs, envs = mar.finish()
-        probs = np.zeros(n_rows, dtype=_native.PROBLEM_DT)
-        reps = np.asarray(cell_rows, dtype=np.int64)
-        cv = list(zip(*cell_vals))
-        probs["layer_begin"] = np.asarray(starts, dtype=np.int64) + (base + loffs[0])
-        probs["n_layers"] = lens
-        probs["strat_begin"] = np.repeat(np.asarray([soffs[x] for x in cv[0]], dtype=np.int64), reps)
-        probs["n_strats"] = np.repeat(np.asarray(cv[1], dtype=np.int64), reps)
-        probs["env_index"] = env
-        # stage_index = 1 .. P within each cell
-        first = np.repeat(np.cumsum(reps) - reps, reps)
-        probs["stage_index"] = np.arange(n_rows, dtype=np.int64) - first + 1
-        probs["n_micro"] = np.repeat(np.asarray(cv[2], dtype=np.int64), reps)
-        probs["flags"] = flags
-        probs["micro"] = np.repeat(np.asarray(cv[3], dtype=np.int64), reps)
-        probs["gran"] = gran
-        probs["budget"] = np.repeat(np.asarray(cv[4], dtype=np.float64), reps)
-        probs["n_buckets"] = np.repeat(np.asarray(cv[5], dtype=np.int64), reps)
-        rc, msg, res, plans, _ = run_native_batch(layers, strats_arr, envs, probs)
+    rc = _native.OK
+    if native is not None:
+        rc, msg, res, plans, _ = native
         if rc != _native.OK:
             bad = np.flatnonzero(res["status"] != 0)
             if not (defer_errors and len(bad)):
                 _native.raise_status(int(res["status"][bad[0]]) if len(bad) else rc, msg)
             first_bad = int(bad[0])
-        plan_off = np.concatenate(([0], np.cumsum(probs["n_layers"]))).tolist()
+        plan_off = np.concatenate(([0], np.cumsum(sb.probs["n_layers"]))).tolist()
         feas = res["feasible"].tolist()
         st_t, st_ns, st_pk = res["stage_time"].tolist(), res["stage_ns"].tolist(), res["stage_peak"].tolist()
         status = res["status"]
         plan_l = plans.tolist()
-    for m, r0, r1, strats in metas:
+    for m, r0, r1, strats in sb.metas:
         if r0 is not None and rc != _native.OK:
             st = status[r0:r1]
             k = np.flatnonzero(st != 0)
@@ -253,6 +299,27 @@ def _search_slices(cells, ctx, opts, defer_errors=False):
     return out
 
 
+def _search_slices(cells, ctx, opts, defer_errors=False):
+    """galvatron_search for cells whose stages are slices of ctx.model: one flat problem
+    table over a single copy of the model's layers, no per-stage Python objects.  With
+    ``defer_errors`` a cell whose stage search fails yields a ``FailedOutcome`` instead of
+    raising for the whole batch."""
+    sb = _slices_prepare(cells, ctx, opts)
+    return _slices_finish(sb, _slices_native(sb), defer_errors)
+
+
+def _sliced_cells(cells, ctx):
+    """(budget, stage ranges, N, B, P) of every cell, or None if a stage is not a slice of
+    ctx.model."""
+    sliced = []
+    for budget, stages, n_devices, batch, pp in cells:
+        ranges = _stage_ranges(ctx.model, stages)
+        if ranges is None:
+            return None
+        sliced.append((budget, ranges, n_devices, batch, pp))
+    return sliced
+
+
 def galvatron_search_batch(cells: Sequence[tuple], ctx: EvalContext, opts: PlannerOptions = PlannerOptions(),
                            defer_errors: bool = False):
     """Many ``galvatron_search(budget, stages, n_devices, batch, pp_degree)`` calls, one device pass.
@@ -260,13 +327,8 @@ def galvatron_search_batch(cells: Sequence[tuple], ctx: EvalContext, opts: Plann
     With ``defer_errors`` (the speculative drivers) a failing cell comes back as a
     ``FailedOutcome`` whose ``raise_()`` the caller invokes when its sequential order reaches
     it; otherwise the first failing cell raises for the whole batch."""
-    sliced = []
-    for budget, stages, n_devices, batch, pp in cells:
-        ranges = _stage_ranges(ctx.model, stages)
-        if ranges is None:
-            break
-        sliced.append((budget, ranges, n_devices, batch, pp))
-    else:
+    sliced = _sliced_cells(cells, ctx)
+    if sliced is not None:
         return _search_slices(sliced, ctx, opts, defer_errors)
     problems, spans, metas = [], [], []
     for budget, stages, n_devices, batch, pp in cells:
@@ -417,6 +479,19 @@ def _window_executor():
     return _window_pool
 
 
+_search_pool = None
+
+
+def _search_executor():
+    """One host thread that runs the device passes of galvatron_base's windows, so that the
+    next window's pass runs while the current window's outcomes are read."""
+    global _search_pool
+    if _search_pool is None:
+        from concurrent.futures import ThreadPoolExecutor
+        _search_pool = ThreadPoolExecutor(max_workers=1)
+    return _search_pool
+
+
 def _drain(fut):
     """Stop the speculative next-window preparation before the driver returns: cancel it if
     it has not started, else wait for it (its result is discarded)."""
@@ -427,6 +502,30 @@ def _drain(fut):
             pass
 
 
+def _gc_paused(fn):
+    """Run a planner driver with the automatic cyclic collector off and a short GIL switch
+    interval (both restored after).  The searches allocate acyclic objects that reference
+    counting frees, while a full collection of a large process (one that imported torch) holds
+    the GIL for tens of milliseconds: measured, a 34 ms gen-2 pass stalled a 70 ms GPT-3-96
+    plan_full.  The driver's helper threads (seeding, device passes) each need the GIL only
+    briefly between native calls; at the default 5 ms interval they wait for the main thread's
+    Python to block first (profiles/README.md)."""
+    @wraps(fn)
+    def run(*args, **kwargs):
+        was = gc.isenabled()
+        interval = sys.getswitchinterval()
+        gc.disable()
+        sys.setswitchinterval(min(interval, 1e-4))
+        try:
+            return fn(*args, **kwargs)
+        finally:
+            sys.setswitchinterval(interval)
+            if was:
+                gc.enable()
+    return run
+
+
+@_gc_paused
 def galvatron_base(model, cluster, profile, opts: PlannerOptions = PlannerOptions()) -> Plan:
     """Algorithm 1: raise the batch until no pipeline degree fits (planner.py:231-277)."""
     ctx = EvalContext(model=model, cluster=cluster, profile=profile)
@@ -438,38 +537,71 @@ def galvatron_base(model, cluster, profile, opts: PlannerOptions = PlannerOption
     first = max(1, window // 4) if min(cluster.n_devices, model.num_layers) >= 16 else window
     chunks = [batches[:first]] + [batches[i:i + window] for i in range(first, len(batches), window)] \
         if batches else []
-    nxt = _window_executor().submit(_base_cells_window, model, ctx, chunks[0], opts) if chunks else None
-    for ci, chunk in enumerate(chunks):
-        per_batch = nxt.result()
-        # speculative: the next window's seeds overlap this window's device pass (unused if
-        # the stop rule ends the sweep here)
-        nxt = _window_executor().submit(_base_cells_window, model, ctx, chunks[ci + 1], opts) \
-            if ci + 1 < len(chunks) else None
-        failed = next((i for i, cells in enumerate(per_batch) if isinstance(cells, Exception)), None)
-        if failed is not None:          # the searches stop before the batch size whose seeding failed
-            chunk, per_batch = chunk[:failed + 1], per_batch[:failed + 1]
-        flat = [c[2] for cells in per_batch if not isinstance(cells, Exception) for c in cells]
+    if not chunks:
+        return best
+    wex, sex = _window_executor(), _search_executor()
+    seeds = {i: wex.submit(_base_cells_window, model, ctx, chunks[i], opts) for i in range(min(2, len(chunks)))}
+
+    def launch(ci):
+        """Window ci: its cells (its seeds), its problem table, and its device pass queued on
+        the search thread.  An error is kept until the sweep reaches the window."""
+        chunk = chunks[ci]
         try:
-            outcomes = galvatron_search_batch(flat, ctx, opts, defer_errors=True)
+            per_batch = seeds.pop(ci).result()
+            failed = next((i for i, cells in enumerate(per_batch) if isinstance(cells, Exception)), None)
+            if failed is not None:      # the searches stop before the batch size whose seeding failed
+                chunk, per_batch = chunk[:failed + 1], per_batch[:failed + 1]
+            flat = [c[2] for cells in per_batch if not isinstance(cells, Exception) for c in cells]
+            sliced = _sliced_cells(flat, ctx)
+            if sliced is None:
+                return chunk, per_batch, None, sex.submit(galvatron_search_batch, flat, ctx, opts, True), None
+            sb = _slices_prepare(sliced, ctx, opts)
+            return chunk, per_batch, sb, sex.submit(_slices_native, sb), None
+        except Exception as e:
+            return chunk, None, None, None, e
+
+    def stop():
+        # the speculative work past the stopping window: queued seeds and searches are
+        # cancelled; a started device pass finishes on the search thread (its result unused);
+        # a started seeding is waited for (it would compete for the host cores)
+        for f in seeds.values():
+            _drain(f)
+        if nxt is not None and nxt[3] is not None:
+            nxt[3].cancel()
+
+    cur = launch(0)
+    nxt = None
+    for ci in range(len(chunks)):
+        if ci + 2 < len(chunks):
+            seeds[ci + 2] = wex.submit(_base_cells_window, model, ctx, chunks[ci + 2], opts)
+        # speculative: the next window's table is built while this window's pass runs and its
+        # pass queued behind it, so that this window's outcomes are read while it runs
+        nxt = launch(ci + 1) if ci + 1 < len(chunks) else None
+        chunk, per_batch, sb, fut, err = cur
+        try:
+            if err is not None:
+                raise err
+            raw = fut.result()
+            outcomes = _slices_finish(sb, raw, defer_errors=True) if sb is not None else raw
         except BaseException:
-            _drain(nxt)
+            stop()
             raise
         k = 0
         for batch, cells in zip(chunk, per_batch):
             if isinstance(cells, Exception):
-                _drain(nxt)
+                stop()
                 raise cells
             cell_best = None
             for p, part, _ in cells:
                 outcome = outcomes[k]
                 k += 1
                 if isinstance(outcome, FailedOutcome):   # the reference's call raises here
-                    _drain(nxt)
+                    stop()
                     outcome.raise_()
                 if outcome.cost < INF and (cell_best is None or outcome.cost < cell_best[0]):
                     cell_best = (outcome.cost, p, part, outcome)
             if cell_best is None:
-                _drain(nxt)
+                stop()
                 if best is None:
                     raise InfeasiblePlanError(f"no feasible plan at the smallest batch size {batch}",
                                               diagnostics=_infeasibility_diagnostics(model, ctx, batch, opts))
@@ -478,9 +610,11 @@ def galvatron_base(model, cluster, profile, opts: PlannerOptions = PlannerOption
             plan = _assemble_plan(model, batch, p, part, outcome)
             if best is None or plan.predicted_throughput > best.predicted_throughput:
                 best = plan
+        cur = nxt
     return best
 
 
+@_gc_paused
 def plan_full(model, cluster, profile, opts: PlannerOptions = PlannerOptions()) -> Plan:
     """Algorithm 1, then (with bi_objective) Algorithm 2 around its batch size (planner.py:280-321)."""
     base = galvatron_base(model, cluster, profile, opts)
