@@ -357,7 +357,7 @@ def main():
     value = total_T / (step_ms / 1e3)
 
     # ---- e2e: public C-ABI call from host buffers (+ NCCL argmin), per step
-    e2e_ms, h2d, d2h = [], 0, 0
+    e2e_ms, call_ms, h2d, d2h = [], [], 0, 0
     winner = None
     n_e2e = args.e2e_steps if args.e2e_steps > 0 else args.steps
     for k in range(1 + n_e2e):                      # call 0: untimed warm-up of the host path
@@ -367,11 +367,13 @@ def main():
         t0 = time.perf_counter()
         rc, msg, r, pl, _ = run_native_batch(L, S, E, Pm, ctx)
         assert rc == 0, msg
+        t1 = time.perf_counter()
         # global argmin over feasible searches (min time, then lowest search index): one NCCL all-gather
         best = global_winner(r["time_s"], r["feasible"], mine, device="cuda")
         torch.cuda.synchronize()
         if k > 0:
             e2e_ms.append((time.perf_counter() - t0) * 1e3)
+            call_ms.append((t1 - t0) * 1e3)
         winner = best
         h2d = int(L.nbytes + S.nbytes + E.nbytes + Pm.nbytes)
         d2h = int(r.nbytes + 4 * int(Pm["n_layers"].sum()))
@@ -393,7 +395,9 @@ def main():
     t4 = time.perf_counter()
     breakdown = {"create_ms": (t1 - t0) * 1e3, "host_prep_ms": tb["prep_ms"], "upload_ms": tb["upload_ms"],
                  "run_ms": (t2 - t1) * 1e3, "device_ms": tb["total_ms"], "fetch_ms": (t3 - t2) * 1e3,
-                 "destroy_ms": (t4 - t3) * 1e3}
+                 "destroy_ms": (t4 - t3) * 1e3,
+                 "search_call_ms_mean": float(np.mean(call_ms)) if call_ms else None,
+                 "winner_ms_mean": float(np.mean(np.array(e2e_ms) - np.array(call_ms))) if call_ms else None}
 
     if rank == 0:
         hbm, kind = peaks()

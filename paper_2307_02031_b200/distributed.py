@@ -30,8 +30,16 @@ def local_winner(times: np.ndarray, feasible: np.ndarray, global_index: np.ndarr
     t = np.where(np.asarray(feasible) != 0, np.asarray(times, dtype=np.float64), np.inf)
     if len(t) == 0:
         return np.array([np.float64(np.inf).view(np.int64), np.iinfo(np.int64).max], dtype=np.int64)
-    best = np.lexsort((np.asarray(global_index), t))[0]
-    return np.array([np.float64(t[best]).view(np.int64), int(global_index[best])], dtype=np.int64)
+    # the first of lexsort((index, t)) in O(n): the least time (NaN after everything), then
+    # the least index among its ties
+    gi = np.asarray(global_index)
+    ok = ~np.isnan(t)
+    pool = np.flatnonzero(ok) if ok.any() else np.arange(len(t))
+    tp = t[pool]
+    m = tp.min()
+    cand = pool if np.isnan(m) else pool[tp == m]
+    best = cand[np.argmin(gi[cand])]
+    return np.array([np.float64(t[best]).view(np.int64), int(gi[best])], dtype=np.int64)
 
 
 def reduce_winners(records: np.ndarray) -> tuple[float, int]:
@@ -47,12 +55,10 @@ def global_winner(times, feasible, global_index, device=None):
     import torch.distributed as dist
 
     rec = torch.from_numpy(local_winner(times, feasible, global_index))
+    if not (dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1):
+        return reduce_winners(rec.numpy())          # one rank: nothing to exchange
     if device is not None:
         rec = rec.to(device)
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
-        out = torch.empty(dist.get_world_size() * 2, dtype=torch.int64, device=rec.device)
-        dist.all_gather_into_tensor(out, rec)
-        recs = out.cpu().numpy()
-    else:
-        recs = rec.cpu().numpy()
-    return reduce_winners(recs)
+    out = torch.empty(dist.get_world_size() * 2, dtype=torch.int64, device=rec.device)
+    dist.all_gather_into_tensor(out, rec)
+    return reduce_winners(out.cpu().numpy())
