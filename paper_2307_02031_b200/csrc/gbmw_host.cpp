@@ -167,6 +167,8 @@ struct gbmw_batch {
     std::vector<std::vector<std::pair<std::pair<int32_t, int64_t>, int32_t>>> strat_at;
     std::vector<std::vector<std::pair<int32_t, int32_t>>> unit_at;
     std::vector<int32_t> srec, urec;         // per problem: its records (-1: none)
+    std::vector<int32_t> host_fix;           // problems whose result entry the host writes (no device
+                                             // work, or a frontier offset), ascending
     std::vector<int32_t> g_cand, g_ccls, g_clsd, g_clst, g_uf, g_uc;
     int64_t total_plan = 0, total_frontier = 0;
     // device arena: inputs | chunk descriptor blocks | outputs
@@ -678,16 +680,19 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
         cur = Chunk();
         cur_bytes = 0;
     };
+    b->host_fix.clear();
     for (int64_t i = 0; i < n_problems; ++i) {
         HostProb &h = b->hp[i];
-        if (!h.gpu) continue;
+        if (!h.gpu) { b->host_fix.push_back((int32_t)i); continue; }
         const size_t need = h.ws_bytes + 16 * 256;
         if (need > limit) {
             h.status = GBMW_ENOMEM;
             h.gpu = false;
+            b->host_fix.push_back((int32_t)i);
             if (first_err == GBMW_OK) { first_err = GBMW_ENOMEM; first_msg = "one stage search needs more workspace than the context limit"; }
             continue;
         }
+        if (h.frontier_off >= 0) b->host_fix.push_back((int32_t)i);
         if (cur_bytes + need > limit) flush();
         cur.probs.push_back((int)i);
         cur_bytes += need;
@@ -1272,25 +1277,36 @@ extern "C" int gbmw_batch_fetch(gbmw_ctx *ctx, gbmw_batch *b, gbmw_result *resul
         std::memcpy(frontier, host + (b->o_frontier - lo), (size_t)b->total_frontier * sizeof(double));
     b->timing.d2h_bytes = (double)(np * sizeof(gbmw_result)) + (plans ? (double)b->total_plan * 4.0 : 0.0) +
                           (frontier ? (double)b->total_frontier * 8.0 : 0.0);
-    int first = GBMW_OK;
-    for (size_t i = 0; i < np; ++i) {
+    // the device's entries in one copy, then the host's (problems without device work, and
+    // frontier offsets); the first failing status in problem order
+    auto host_entry = [&](size_t i, gbmw_result &r) {
         const HostProb &h = b->hp[i];
-        gbmw_result r;
         if (h.gpu) {
             r = dev_res[i];
             r.frontier_offset = h.frontier_off;
-        } else {
-            std::memset(&r, 0, sizeof(r));
-            r.time_s = INFINITY;
-            r.e_fwd_used = 0.0;
-            r.feasible = 0;
-            r.status = h.status;
-            r.frontier_offset = -1;
-            if (plans)
-                for (int l = 0; l < std::max<int32_t>(0, b->problems[i].n_layers); ++l) plans[h.plan_off + l] = -1;
+            return;
         }
-        if (r.status != GBMW_OK && first == GBMW_OK) first = r.status;
-        if (results) results[i] = r;
+        std::memset(&r, 0, sizeof(r));
+        r.time_s = INFINITY;
+        r.e_fwd_used = 0.0;
+        r.feasible = 0;
+        r.status = h.status;
+        r.frontier_offset = -1;
+        if (plans)
+            for (int l = 0; l < std::max<int32_t>(0, b->problems[i].n_layers); ++l) plans[h.plan_off + l] = -1;
+    };
+    int first = GBMW_OK;
+    if (results) {
+        if (np) std::memcpy(results, dev_res, np * sizeof(gbmw_result));
+        for (int32_t i : b->host_fix) host_entry((size_t)i, results[i]);
+        for (size_t i = 0; i < np && first == GBMW_OK; ++i)
+            if (results[i].status != GBMW_OK) first = results[i].status;
+    } else {
+        for (size_t i = 0; i < np; ++i) {
+            gbmw_result r;
+            host_entry(i, r);
+            if (r.status != GBMW_OK && first == GBMW_OK) first = r.status;
+        }
     }
     if (first == GBMW_EINTERNAL) set_err(&ctx->err, first, "dp_search produced a plan exceeding the memory budget");
     b->timing.fetch_ms = now_ms() - t0;
