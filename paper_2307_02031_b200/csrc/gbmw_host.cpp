@@ -167,6 +167,8 @@ struct gbmw_batch {
     std::vector<std::vector<std::pair<std::pair<int32_t, int64_t>, int32_t>>> strat_at;
     std::vector<std::vector<std::pair<int32_t, int32_t>>> unit_at;
     std::vector<int32_t> srec, urec;         // per problem: its records (-1: none)
+    std::vector<int32_t> strat_ok;           // per strategy: check_strategy status
+    std::vector<StratDeg> strat_deg;         // per strategy: its degrees (valid where strat_ok is OK)
     std::vector<int32_t> host_fix;           // problems whose result entry the host writes (no device
                                              // work, or a frontier offset), ascending
     std::vector<int32_t> g_cand, g_ccls, g_clsd, g_clst, g_uf, g_uc;
@@ -277,14 +279,19 @@ extern "C" int gbmw_enumerate(int64_t n_devices, int64_t pp_degree, int32_t prun
 
 // ----------------------------------------------------------------------------- scalar costs
 namespace {
-int check_strategy(const gbmw_strategy &s, std::string *err) {
-    if (s.n_levels < 0 || s.n_levels > 3) return set_err(err, GBMW_EINVAL, "strategy has more than 3 levels");
-    if (s.pp_degree < 1) return set_err(err, GBMW_EINVAL, "strategy pipeline degree must be >= 1");
+// the first malformed field of a strategy record, or null
+const char *strategy_defect(const gbmw_strategy &s) {
+    if (s.n_levels < 0 || s.n_levels > 3) return "strategy has more than 3 levels";
+    if (s.pp_degree < 1) return "strategy pipeline degree must be >= 1";
     for (int l = 0; l < s.n_levels; ++l) {
-        if (s.paradigm[l] < 0 || s.paradigm[l] > 2) return set_err(err, GBMW_EINVAL, "strategy has an unknown paradigm");
-        if (s.degree[l] < 1) return set_err(err, GBMW_EINVAL, "strategy level degree must be >= 1");
+        if (s.paradigm[l] < 0 || s.paradigm[l] > 2) return "strategy has an unknown paradigm";
+        if (s.degree[l] < 1) return "strategy level degree must be >= 1";
     }
-    return GBMW_OK;
+    return nullptr;
+}
+int check_strategy(const gbmw_strategy &s, std::string *err) {
+    const char *d = strategy_defect(s);
+    return d ? set_err(err, GBMW_EINVAL, d) : GBMW_OK;
 }
 int check_layer(const gbmw_layer &L, std::string *err) {
     if (L.param_bytes < 0 || L.param_bytes >= kTwo53i || L.bnd_bytes_per_sample < 0 ||
@@ -398,9 +405,11 @@ void build_strat(const gbmw_batch &b, const StratKey &key, StratInfo &si) {
     const int64_t micro = std::get<2>(key);
     for (int i = 0; i < n && si.status == GBMW_OK; ++i) {
         const gbmw_strategy &s = b.strats[begin + i];
-        const int rc = check_strategy(s, &si.err);
-        if (rc) { si.status = rc; break; }
-        const StratDeg d = strat_degrees(s);
+        if (b.strat_ok[begin + i] != GBMW_OK) {       // the message is rebuilt only on failure
+            si.status = check_strategy(s, &si.err);
+            break;
+        }
+        const StratDeg &d = b.strat_deg[begin + i];
         if (micro % d.data != 0) continue;
         si.cand.push_back(begin + i);
         si.min_pp = si.cand.size() == 1 ? s.pp_degree : std::min(si.min_pp, s.pp_degree);
@@ -630,6 +639,13 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
             for (const auto &r : b->unit_recs) b->unit_at[std::get<0>(r.first)].clear();
         }
         th[1] = now_ms();
+        // per-strategy checks and degrees, once (records of one list at many micro-batches share them)
+        b->strat_ok.resize(n_strategies);
+        b->strat_deg.resize(n_strategies);
+        for (int64_t i = 0; i < n_strategies; ++i) {
+            b->strat_ok[i] = strategy_defect(b->strats[i]) ? GBMW_EINVAL : GBMW_OK;
+            if (b->strat_ok[i] == GBMW_OK) b->strat_deg[i] = strat_degrees(b->strats[i]);
+        }
         // the records, and the concatenated arrays the descriptors point into
         b->g_cand.clear(); b->g_ccls.clear(); b->g_clsd.clear(); b->g_clst.clear(); b->g_uf.clear(); b->g_uc.clear();
         for (auto &e : b->strat_recs) {
