@@ -106,6 +106,44 @@ __device__ __forceinline__ void eval_row(const ChunkArgs &a, const SH &sh, int u
     const uint32_t *fin = a.chg[(u - 1) & 1] + sh.f_off;
 #pragma unroll
     for (int kk = 0; kk < KT; ++kk) { bt[kk] = GBMW_STEP_INF; bf[kk] = GBMW_STEP_INF; bk[kk] = 0x7fffffff; }
+    if constexpr (IB == 1 && !FIRST) {
+        // one source's value in flight, the next source's row-map and change-bit words
+        // fetched while it arrives: the chain per source is one load, not two
+        int i = l;
+        Cell c = sh.cell[i < S ? i : 0];
+        int src = e - c.w;
+        bool ok = i < S && e >= 0 && src >= lo_prev;
+        int2 m = make_int2(0, 0);
+        uint32_t cw = 0u;
+        if (ok) { m = __ldg(rm + (src >> 5)); cw = __ldg(fin + (int64_t)c.k * sh.nw + (src >> 5)); }
+        for (; i < S; i += L) {
+            double2 v = make_double2(GBMW_STEP_INF, GBMW_STEP_INF);
+            if (ok) v = __ldg(reinterpret_cast<const double2 *>(bin + (int64_t)stored_row(m, src) * sh.K + c.k));
+            const int in = i + L;
+            const Cell cn = sh.cell[in < S ? in : 0];
+            const int srcn = e - cn.w;
+            const bool okn = in < S && e >= 0 && srcn >= lo_prev;
+            int2 mn = make_int2(0, 0);
+            uint32_t cwn = 0u;
+            if (okn) { mn = __ldg(rm + (srcn >> 5)); cwn = __ldg(fin + (int64_t)cn.k * sh.nw + (srcn >> 5)); }
+            if (ok) {
+                const double T = v.x + c.c, F = v.y + c.ef;
+                const int key = 2 * i | (int)((cw >> (src & 31)) & 1u);
+                const double *rrow = sh.r + c.k * K;
+#pragma unroll
+                for (int kk = 0; kk < KT; ++kk) {
+                    if (!GUARD || kk < K) {
+                        const double cand = T + rrow[kk];
+                        const bool better = lex3_less(cand, F, key, bt[kk], bf[kk], bk[kk]);
+                        bt[kk] = better ? cand : bt[kk];
+                        bf[kk] = better ? F : bf[kk];
+                        bk[kk] = better ? key : bk[kk];
+                    }
+                }
+            }
+            c = cn; src = srcn; ok = okn; m = mn; cw = cwn;
+        }
+    } else
     for (int i0 = l; i0 < S; i0 += IB * L) {
         double T[IB], F[IB];
         int key[IB], src_[IB], k_[IB];
