@@ -106,30 +106,48 @@ __device__ __forceinline__ void eval_row(const ChunkArgs &a, const SH &sh, int u
     const uint32_t *fin = a.chg[(u - 1) & 1] + sh.f_off;
 #pragma unroll
     for (int kk = 0; kk < KT; ++kk) { bt[kk] = GBMW_STEP_INF; bf[kk] = GBMW_STEP_INF; bk[kk] = 0x7fffffff; }
-    if constexpr (IB == 1 && !FIRST) {
-        // one source's value in flight, the next source's row-map and change-bit words
-        // fetched while it arrives: the chain per source is one load, not two
-        int i = l;
-        Cell c = sh.cell[i < S ? i : 0];
-        int src = e - c.w;
-        bool ok = i < S && e >= 0 && src >= lo_prev;
-        int2 m = make_int2(0, 0);
-        uint32_t cw = 0u;
-        if (ok) { m = __ldg(rm + (src >> 5)); cw = __ldg(fin + (int64_t)c.k * sh.nw + (src >> 5)); }
-        for (; i < S; i += L) {
-            double2 v = make_double2(GBMW_STEP_INF, GBMW_STEP_INF);
-            if (ok) v = __ldg(reinterpret_cast<const double2 *>(bin + (int64_t)stored_row(m, src) * sh.K + c.k));
-            const int in = i + L;
-            const Cell cn = sh.cell[in < S ? in : 0];
-            const int srcn = e - cn.w;
-            const bool okn = in < S && e >= 0 && srcn >= lo_prev;
-            int2 mn = make_int2(0, 0);
-            uint32_t cwn = 0u;
-            if (okn) { mn = __ldg(rm + (srcn >> 5)); cwn = __ldg(fin + (int64_t)cn.k * sh.nw + (srcn >> 5)); }
-            if (ok) {
-                const double T = v.x + c.c, F = v.y + c.ef;
-                const int key = 2 * i | (int)((cw >> (src & 31)) & 1u);
-                const double *rrow = sh.r + c.k * K;
+    if constexpr (!FIRST) {
+        // IB sources' values in flight, the next IB sources' row-map and change-bit words
+        // fetched while they arrive: the chain per group of sources is one load, not two
+        int src[IB], k_[IB];
+        bool ok[IB];
+        int2 m[IB];
+        uint32_t cw[IB];
+        auto fetch = [&](int i0, int *srcx, int *kx, bool *okx, int2 *mx, uint32_t *cwx) {
+#pragma unroll
+            for (int b = 0; b < IB; ++b) {
+                const int i = i0 + b * L;
+                const Cell c = sh.cell[i < S ? i : 0];
+                srcx[b] = e - c.w; kx[b] = c.k;
+                okx[b] = i < S && e >= 0 && srcx[b] >= lo_prev;
+                mx[b] = make_int2(0, 0); cwx[b] = 0u;
+                if (okx[b]) {
+                    mx[b] = __ldg(rm + (srcx[b] >> 5));
+                    cwx[b] = __ldg(fin + (int64_t)c.k * sh.nw + (srcx[b] >> 5));
+                }
+            }
+        };
+        fetch(l, src, k_, ok, m, cw);
+        for (int i0 = l; i0 < S; i0 += IB * L) {
+            double2 v[IB];
+#pragma unroll
+            for (int b = 0; b < IB; ++b) {
+                v[b] = make_double2(GBMW_STEP_INF, GBMW_STEP_INF);
+                if (ok[b]) v[b] = __ldg(reinterpret_cast<const double2 *>(bin + (int64_t)stored_row(m[b], src[b]) * sh.K + k_[b]));
+            }
+            int srcn[IB], kn[IB];
+            bool okn[IB];
+            int2 mn[IB];
+            uint32_t cwn[IB];
+            fetch(i0 + IB * L, srcn, kn, okn, mn, cwn);
+#pragma unroll
+            for (int b = 0; b < IB; ++b) {
+                if (!ok[b]) continue;
+                const int i = i0 + b * L;
+                const Cell c = sh.cell[i];
+                const double T = v[b].x + c.c, F = v[b].y + c.ef;
+                const int key = 2 * i | (int)((cw[b] >> (src[b] & 31)) & 1u);
+                const double *rrow = sh.r + k_[b] * K;
 #pragma unroll
                 for (int kk = 0; kk < KT; ++kk) {
                     if (!GUARD || kk < K) {
@@ -141,7 +159,8 @@ __device__ __forceinline__ void eval_row(const ChunkArgs &a, const SH &sh, int u
                     }
                 }
             }
-            c = cn; src = srcn; ok = okn; m = mn; cw = cwn;
+#pragma unroll
+            for (int b = 0; b < IB; ++b) { src[b] = srcn[b]; k_[b] = kn[b]; ok[b] = okn[b]; m[b] = mn[b]; cw[b] = cwn[b]; }
         }
     } else
     for (int i0 = l; i0 < S; i0 += IB * L) {
