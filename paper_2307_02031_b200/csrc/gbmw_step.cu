@@ -32,7 +32,17 @@ namespace gbmw {
 #define GBMW_STEP_INF __longlong_as_double(0x7ff0000000000000LL)
 
 constexpr int kClassifyIB = 8;              // window checks per thread in flight
-constexpr int kStepIB = 2;                  // sources per lane in flight (lane-per-row evaluation)
+#ifndef GBMW_STEP_IB
+#define GBMW_STEP_IB 2
+#endif
+#ifndef GBMW_STEP_IB_WIDE
+#define GBMW_STEP_IB_WIDE 1
+#endif
+#ifndef GBMW_KEEP_CELL                      // 1: keep each source's (c, ef) in registers from its index
+#define GBMW_KEEP_CELL 0                    // fetch (measured: 10k sweep +0.5 %, GPT-3-96 P=1 K2 -3 %)
+#endif
+constexpr int kStepIB = GBMW_STEP_IB;       // sources per lane in flight (lane-per-row evaluation), K <= 4
+constexpr int kStepIBWide = GBMW_STEP_IB_WIDE;   // the same for K >= 5
 constexpr int kWarpRows = 1024;             // rows per warp tile: 32 groups of 32
 constexpr int kK2Warps = kStepThreads / 32;
 
@@ -100,7 +110,7 @@ __device__ __forceinline__ void eval_row(const ChunkArgs &a, const SH &sh, int u
     const int n_e = sh.n_e, lo_prev = FIRST ? 0 : sh.lo_prev;
     // sources in flight per lane: as many as the register budget holds without spilling an
     // in-flight load (a spilled load result serialises the loads)
-    constexpr int IB = (KT <= 4) ? kStepIB : 1;
+    constexpr int IB = (KT <= 4) ? kStepIB : kStepIBWide;
     const TFCell *bin = a.TF[(u - 1) & 1] + sh.b_off;
     const int2 *rm = a.rmap + sh.rm_prev;
     const uint32_t *fin = a.chg[(u - 1) & 1] + sh.f_off;
@@ -113,11 +123,13 @@ __device__ __forceinline__ void eval_row(const ChunkArgs &a, const SH &sh, int u
         bool ok[IB];
         int2 m[IB];
         uint32_t cw[IB];
-        auto fetch = [&](int i0, int *srcx, int *kx, bool *okx, int2 *mx, uint32_t *cwx) {
+        double cc[IB], cf[IB];
+        auto fetch = [&](int i0, int *srcx, int *kx, bool *okx, int2 *mx, uint32_t *cwx, double *ccx, double *cfx) {
 #pragma unroll
             for (int b = 0; b < IB; ++b) {
                 const int i = i0 + b * L;
                 const Cell c = sh.cell[i < S ? i : 0];
+                if (GBMW_KEEP_CELL) { ccx[b] = c.c; cfx[b] = c.ef; }
                 srcx[b] = e - c.w; kx[b] = c.k;
                 okx[b] = i < S && e >= 0 && srcx[b] >= lo_prev;
                 mx[b] = make_int2(0, 0); cwx[b] = 0u;
@@ -127,7 +139,7 @@ __device__ __forceinline__ void eval_row(const ChunkArgs &a, const SH &sh, int u
                 }
             }
         };
-        fetch(l, src, k_, ok, m, cw);
+        fetch(l, src, k_, ok, m, cw, cc, cf);
         for (int i0 = l; i0 < S; i0 += IB * L) {
             double2 v[IB];
 #pragma unroll
@@ -139,13 +151,16 @@ __device__ __forceinline__ void eval_row(const ChunkArgs &a, const SH &sh, int u
             bool okn[IB];
             int2 mn[IB];
             uint32_t cwn[IB];
-            fetch(i0 + IB * L, srcn, kn, okn, mn, cwn);
+            double ccn[IB], cfn[IB];
+            fetch(i0 + IB * L, srcn, kn, okn, mn, cwn, ccn, cfn);
 #pragma unroll
             for (int b = 0; b < IB; ++b) {
                 if (!ok[b]) continue;
                 const int i = i0 + b * L;
-                const Cell c = sh.cell[i];
-                const double T = v[b].x + c.c, F = v[b].y + c.ef;
+                double c_c, c_ef;
+                if (GBMW_KEEP_CELL) { c_c = cc[b]; c_ef = cf[b]; }
+                else { const Cell c = sh.cell[i]; c_c = c.c; c_ef = c.ef; }
+                const double T = v[b].x + c_c, F = v[b].y + c_ef;
                 const int key = 2 * i | (int)((cw[b] >> (src[b] & 31)) & 1u);
                 const double *rrow = sh.r + k_[b] * K;
 #pragma unroll
@@ -160,7 +175,10 @@ __device__ __forceinline__ void eval_row(const ChunkArgs &a, const SH &sh, int u
                 }
             }
 #pragma unroll
-            for (int b = 0; b < IB; ++b) { src[b] = srcn[b]; k_[b] = kn[b]; ok[b] = okn[b]; m[b] = mn[b]; cw[b] = cwn[b]; }
+            for (int b = 0; b < IB; ++b) {
+                src[b] = srcn[b]; k_[b] = kn[b]; ok[b] = okn[b]; m[b] = mn[b]; cw[b] = cwn[b];
+                if (GBMW_KEEP_CELL) { cc[b] = ccn[b]; cf[b] = cfn[b]; }
+            }
         }
     } else
     for (int i0 = l; i0 < S; i0 += IB * L) {
