@@ -169,8 +169,10 @@ class Context:
 
     def close(self):
         if self.handle:
-            lib().gbmw_ctx_destroy(self.handle)
-            self.handle = None
+            with self.lock:                 # after a call in progress on another thread (e.g. the
+                if self.handle:             # planner's speculative device pass)
+                    lib().gbmw_ctx_destroy(self.handle)
+                    self.handle = None
 
     def __del__(self):
         try:

@@ -14,6 +14,7 @@ from __future__ import annotations
 import ctypes
 import gc
 import sys
+import threading
 from dataclasses import dataclass
 from functools import lru_cache, wraps
 from typing import Any, Sequence
@@ -502,6 +503,11 @@ def _drain(fut):
             pass
 
 
+_host_lock = threading.Lock()
+_host_depth = 0
+_host_saved = (True, 0.005)
+
+
 def _gc_paused(fn):
     """Run a planner driver with the automatic cyclic collector off and a short GIL switch
     interval (both restored after).  The searches allocate acyclic objects that reference
@@ -512,16 +518,22 @@ def _gc_paused(fn):
     Python to block first (profiles/README.md)."""
     @wraps(fn)
     def run(*args, **kwargs):
-        was = gc.isenabled()
-        interval = sys.getswitchinterval()
-        gc.disable()
-        sys.setswitchinterval(min(interval, 1e-4))
+        global _host_depth, _host_saved
+        with _host_lock:                    # the outermost driver call (over all threads) saves and restores
+            if _host_depth == 0:
+                _host_saved = (gc.isenabled(), sys.getswitchinterval())
+                gc.disable()
+                sys.setswitchinterval(min(_host_saved[1], 1e-4))
+            _host_depth += 1
         try:
             return fn(*args, **kwargs)
         finally:
-            sys.setswitchinterval(interval)
-            if was:
-                gc.enable()
+            with _host_lock:
+                _host_depth -= 1
+                if _host_depth == 0:
+                    sys.setswitchinterval(_host_saved[1])
+                    if _host_saved[0]:
+                        gc.enable()
     return run
 
 

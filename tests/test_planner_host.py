@@ -114,3 +114,38 @@ def test_partition_layers_is_a_lazy_sequence_of_slices():
     assert all(a is b for a, b in zip(sl[1], eager[1]))
     assert _stage_ranges(model, sl) == [(0, 5), (5, 20), (25, 7)]
     assert _stage_ranges(model, eager) == [(0, 5), (5, 20), (25, 7)]
+
+
+def test_gc_pause_restores_process_state_across_threads():
+    """The drivers' collector pause and GIL switch interval are process-wide: overlapping
+    driver calls on several threads restore the caller's settings when the last one ends."""
+    import gc
+    import sys
+    import threading
+    import time
+    from paper_2307_02031_b200.planner import _gc_paused
+
+    gc.enable()
+    before = sys.getswitchinterval()
+    inside = []
+
+    @_gc_paused
+    def driver(delay):
+        inside.append((gc.isenabled(), sys.getswitchinterval()))
+        time.sleep(delay)
+
+    ts = [threading.Thread(target=driver, args=(d,)) for d in (0.05, 0.01, 0.03)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert all(not en and iv <= 1e-4 for en, iv in inside)
+    assert gc.isenabled() and sys.getswitchinterval() == before
+    gc.disable()
+
+    @_gc_paused
+    def nested():
+        return gc.isenabled()
+
+    assert nested() is False and not gc.isenabled()      # a caller's own disabled GC stays disabled
+    gc.enable()
