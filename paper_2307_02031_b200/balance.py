@@ -20,7 +20,7 @@ from typing import Callable, Sequence
 import numpy as np
 
 from . import _native
-from .costs import StageCost
+from .costs import EvalContext, StageCost
 from .strategies import DP, SDP, TP, ParallelStrategy
 
 logger = logging.getLogger(__name__)
@@ -131,19 +131,36 @@ _layer_cache: dict = {}
 
 
 def _layers(model, profile) -> np.ndarray:
+    """LAYER_DT table of a model under a profile, cached per (model, profile) object pair; the
+    profile's override mapping (the one mutable part) is compared on every call."""
     key = (id(model), id(profile))
+    ov = getattr(profile, "layer_overrides", None)
+    snap = dict(ov) if isinstance(ov, dict) else None
     hit = _layer_cache.get(key)
-    if hit is None or hit[0] is not model or hit[1] is not profile:
+    if hit is None or hit[0] is not model or hit[1] is not profile or hit[2] != snap:
         arr = _native.layers_array(model.layers, profile, {})
         if len(_layer_cache) > 64:
             _layer_cache.clear()
-        hit = (model, profile, arr)
+        hit = (model, profile, snap, arr)
         _layer_cache[key] = hit
-    return hit[2]
+    return hit[3]
+
+
+_env_cache: dict = {}
 
 
 def _env(ctx) -> np.ndarray:
-    return np.array([_native.env_record(ctx)], dtype=_native.ENV_DT)
+    """ENV_DT record of an EvalContext, built once per context object (its cluster, profile
+    and model are frozen dataclasses, so the record cannot change under the same object)."""
+    if not isinstance(ctx, EvalContext):         # a duck-typed context may change: re-read it
+        return np.array([_native.env_record(ctx)], dtype=_native.ENV_DT)
+    hit = _env_cache.get(id(ctx))
+    if hit is None or hit[0] is not ctx:
+        if len(_env_cache) > 64:
+            _env_cache.clear()
+        hit = (ctx, np.array([_native.env_record(ctx)], dtype=_native.ENV_DT))
+        _env_cache[id(ctx)] = hit
+    return hit[1]
 
 
 def _planner_error(rc: int):
@@ -157,16 +174,18 @@ def evaluate_partition(model, partition: PipelinePartition, per_layer_strategies
     if len(per_layer_strategies) != model.num_layers:
         raise ValueError("need one strategy per model layer")
     sizes = np.array(partition.stage_sizes, dtype=np.int32)
-    strats = _native.strategies_array(list(per_layer_strategies))
+    strats = _native.strategies_array(per_layer_strategies)
     out = np.zeros(3 * len(sizes), dtype=np.float64)
     layers = _layers(model, ctx.profile)
     env = _env(ctx)
-    rc = _native.lib().gbmw_partition_costs(_native.ptr(layers), len(layers), _native.ptr(strats),
-                                            _native.ptr(sizes), len(sizes), _native.ptr(env),
-                                            int(micro_batch), int(n_micro), _native.ptr(out))
+    # raw addresses: every array is bound to a local for the duration of the call
+    rc = _native.lib().gbmw_partition_costs(layers.ctypes.data, len(layers), strats.ctypes.data,
+                                            sizes.ctypes.data, len(sizes), env.ctypes.data,
+                                            int(micro_batch), int(n_micro), out.ctypes.data)
     if rc != _native.OK:
         _planner_error(rc)
-    return [StageCost(float(out[3 * s]), float(out[3 * s + 1]), float(out[3 * s + 2])) for s in range(len(sizes))]
+    o = out.tolist()
+    return [StageCost(o[3 * s], o[3 * s + 1], o[3 * s + 2]) for s in range(len(sizes))]
 
 
 def _init_partition(model, num_stages, seed_strategies, micro_batch, n_micro, ctx, objective) -> PipelinePartition:
