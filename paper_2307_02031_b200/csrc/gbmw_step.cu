@@ -370,7 +370,10 @@ __device__ __forceinline__ int classify_tile(const ChunkArgs &a, TileCtx &t, uin
 // lanes per entry.  Tiles with up to kLightE entries are one round (in K2a); heavier tiles
 // use 8-entry rounds (short dependent-load chains, many warps), very dense ones 32-entry
 // rounds (a lane per row: fewest instructions per entry).
-constexpr int kLightE = 8;
+#ifndef GBMW_LIGHT_E
+#define GBMW_LIGHT_E 8
+#endif
+constexpr int kLightE = GBMW_LIGHT_E;
 constexpr int kDenseN = 256;
 __device__ __forceinline__ int round_entries(int n) { return n <= kLightE ? kLightE : (n < kDenseN ? 8 : 32); }
 __host__ __device__ constexpr int round_entries_c(int n) { return n <= kLightE ? kLightE : (n < kDenseN ? 8 : 32); }
