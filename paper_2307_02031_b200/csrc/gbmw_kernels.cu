@@ -210,6 +210,58 @@ __device__ __forceinline__ void backtrack(const ChunkArgs &a, const DevProblem &
     }
 }
 
+// The same walk by a whole warp (K4): lane s holds strategy s's (weight, class) of the next
+// units, fetched ahead, and the row-map word at the row each strategy would step to, so the
+// argmin load of a unit goes out with the next unit's row-map loads beside it: the chain per
+// unit is one global load instead of three (cell, row map, argmin).  S <= 64.
+__device__ __forceinline__ void backtrack_warp(const ChunkArgs &a, const DevProblem &p, int64_t e, int j,
+                                               uint16_t *path, int lane) {
+    const int U = p.U, S = p.S, K = p.K;
+    const int64_t n_e = p.n_b + 1;
+    const Cell *cells = a.cells + p.cell_off;
+    const uint16_t *par = a.par + p.par_off;
+    const int2 *rmb = a.rmap + p.rmap_off;
+    const int64_t ng = rmap_groups(n_e);
+    constexpr unsigned full = 0xffffffffu;
+    int wc[2], kc[2], wn[2], kn[2];                      // units u and u - 1, strategies lane, lane + 32
+    int2 m[2];                                           // row map of unit u - 1 at e - w_u(s)
+    auto cell_wk = [&](int u, int b, int *w, int *k) {
+        const int s = lane + 32 * b;
+        if (u >= 1 && s < S) { const Cell c = cells[(int64_t)u * S + s]; w[b] = c.w; k[b] = c.k; }
+        else { w[b] = 0; k[b] = 0; }
+    };
+    auto rm_at = [&](int u, int64_t e_u, int b, const int *w) {
+        const int s = lane + 32 * b;
+        const int64_t x = e_u - w[b];
+        return (u >= 1 && s < S && x >= 0) ? __ldg(rmb + (int64_t)(u - 1) * ng + (x >> 5)) : make_int2(0, 0);
+    };
+    if (lane == 0) path[U - 1] = (uint16_t)j;
+#pragma unroll
+    for (int b = 0; b < 2; ++b) { cell_wk(U - 1, b, wc, kc); cell_wk(U - 2, b, wn, kn); }
+#pragma unroll
+    for (int b = 0; b < 2; ++b) m[b] = rm_at(U - 1, e, b, wc);
+    for (int u = U - 1; u >= 1; --u) {
+        int wnn[2], knn[2];                              // unit u - 2, fetched two units ahead
+#pragma unroll
+        for (int b = 0; b < 2; ++b) cell_wk(u - 2, b, wnn, knn);
+        const int src = j & 31, hb = j >> 5;
+        const int w = __shfl_sync(full, hb ? wc[1] : wc[0], src);
+        const int k = __shfl_sync(full, hb ? kc[1] : kc[0], src);
+        const int mx = __shfl_sync(full, hb ? m[1].x : m[0].x, src);
+        const int my = __shfl_sync(full, hb ? m[1].y : m[0].y, src);
+        e -= w;
+        const int er = stored_row(make_int2(mx, my), (int)e);
+        const int jn = par[((int64_t)(u - 1) * n_e + er) * K + k];
+#pragma unroll
+        for (int b = 0; b < 2; ++b) m[b] = rm_at(u - 1, e, b, wn);
+        j = jn;
+        if (lane == 0) path[u - 1] = (uint16_t)j;
+#pragma unroll
+        for (int b = 0; b < 2; ++b) { wc[b] = wn[b]; kc[b] = kn[b]; wn[b] = wnn[b]; kn[b] = knn[b]; }
+    }
+    __syncwarp();
+}
+
 // Same walk with (weight, class) of every (unit, strategy) staged in shared memory, packed
 // as weight << 4 | class (weight <= n_b + 1 < 2^27): the chain per unit is then one global
 // load (the argmin) after the row-map entry.  rms: row map of the last unit in shared
@@ -975,6 +1027,7 @@ __global__ void __launch_bounds__(32 * kFinWarps) k_finalize(ChunkArgs a) {
     gbmw_result res;
     double bt = GBMW_INF, e_all = 0.0;
     int64_t be = -1;
+    int sj = 0;
     if (lane == 0) {
         const SweepPartial safe = a.best[q];
         bt = safe.t;
@@ -984,13 +1037,15 @@ __global__ void __launch_bounds__(32 * kFinWarps) k_finalize(ChunkArgs a) {
             const SweepPartial sp = a.partials[p.tile_off + t];
             if (cand_better(sp.t, sp.e, bt, be)) { bt = sp.t; be = sp.e; bj = sp.j; }
         }
-        if (be >= 0) {
-            if (p.flags & GBMW_APPROX) approx_reconstruct(a, p, be, path);
-            else backtrack(a, p, be, bj, path);
-            e_all = plan_e_all(a, p, path);
-        }
+        if (be >= 0 && (p.flags & GBMW_APPROX)) approx_reconstruct(a, p, be, path);
+        if (be >= 0 && !(p.flags & GBMW_APPROX) && p.S > 64) backtrack(a, p, be, bj, path);
+        sj = bj;
     }
     be = __shfl_sync(0xffffffffu, be, 0);
+    if (be >= 0 && !(p.flags & GBMW_APPROX) && p.S <= 64)
+        backtrack_warp(a, p, be, __shfl_sync(0xffffffffu, sj, 0), path, lane);
+    __syncwarp();
+    if (lane == 0 && be >= 0) e_all = plan_e_all(a, p, path);
     int32_t *plan = a.plans + p.plan_off;
     if (be < 0) {
         for (int l = lane; l < p.n_layers; l += 32) plan[l] = -1;
