@@ -146,23 +146,39 @@ __global__ void k_dedupe(ChunkArgs a) {
 }
 
 // Live row ranges of every unit, a thread per problem (reads the wmins k_dedupe parked).
+// A warp per problem: L_u is the exclusive prefix sum of the units' least weights (capped at
+// n_b + 1), so 32 units at a time go through one load and a warp scan instead of a chain of
+// dependent loads and stores over the units.
 __global__ void k_unit_ranges(ChunkArgs a) {
-    const int q = blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= a.n_probs) return;
+    const int q = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
+    if (q >= a.n_probs) return;                          // warp-uniform
     const DevProblem &p = a.probs[q];
     const int64_t top = p.n_b + 1;
-    int64_t acc = 0;
+    int64_t carry = 0;                                   // sum of the least weights of the units before
     unsigned long long live = 0;
-    for (int u = 0; u < p.U; ++u) {
-        const int wmin = a.unit_hi[p.ustate_off + u];
-        const int64_t lo = acc < top ? acc : top, hi = p.n_b - wmin;
-        a.unit_lo[p.ustate_off + u] = (int32_t)lo;                          // L_u = m_{u-1}
-        a.unit_hi[p.ustate_off + u] = (int32_t)hi;                          // H_u
-        if (u >= 1 && hi >= lo) live += (unsigned long long)(hi - lo + 1);
-        acc += wmin;
+    for (int u0 = 0; u0 < p.U; u0 += 32) {
+        const int u = u0 + lane;
+        const int wmin = u < p.U ? a.unit_hi[p.ustate_off + u] : 0;
+        int64_t incl = wmin;                             // inclusive scan over the lanes
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int64_t v = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= off) incl += v;
+        }
+        const int64_t acc = carry + incl - wmin;         // exclusive: units before u
+        if (u < p.U) {
+            const int64_t lo = acc < top ? acc : top, hi = p.n_b - wmin;
+            a.unit_lo[p.ustate_off + u] = (int32_t)lo;                      // L_u = m_{u-1}
+            a.unit_hi[p.ustate_off + u] = (int32_t)hi;                      // H_u
+            if (u >= 1 && hi >= lo) live += (unsigned long long)(hi - lo + 1);
+        }
+        carry += __shfl_sync(0xffffffffu, incl, 31);
     }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) live += __shfl_xor_sync(0xffffffffu, live, off);
     // live class cells written by K2 (algorithmic-bytes accounting)
-    if (!(p.flags & GBMW_APPROX)) atomicAdd(a.live_cells, live * (unsigned long long)p.K);
+    if (lane == 0 && !(p.flags & GBMW_APPROX)) atomicAdd(a.live_cells, live * (unsigned long long)p.K);
 }
 
 // K2 (the min-plus layer step) lives in gbmw_step.cu.
@@ -1137,7 +1153,7 @@ int launch_cost_tables(const ChunkArgs &a, int64_t n_cells, int64_t n_r, void *s
     if (n_r > 0) k_cost_r<<<blocks_for(n_r, 128), 128, 0, st>>>(a, n_r);
     if (a.n_units > 0 && a.n_probs > 0) {
         k_dedupe<<<blocks_for(a.n_units * 32, 128), 128, 0, st>>>(a);
-        k_unit_ranges<<<blocks_for(a.n_probs, 128), 128, 0, st>>>(a);
+        k_unit_ranges<<<blocks_for((int64_t)a.n_probs * 32, 128), 128, 0, st>>>(a);
     }
     return (int)cudaGetLastError();
 }
