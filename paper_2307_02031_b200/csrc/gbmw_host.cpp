@@ -111,7 +111,8 @@ struct Chunk {
     size_t small_off = 0;          // byte offset of this chunk's descriptor block in the arena
     // offsets inside the descriptor block
     size_t o_probs, o_cellp, o_rp, o_stepp, o_cand, o_ccls, o_clsd, o_clst, o_uf, o_uc;
-    size_t o_stepmap, o_aux, o_slists;
+    size_t o_stepmap, o_aux, o_slists, o_cellc, o_rc, o_unitc;
+    int64_t n_cellc = 0, n_rc = 0, n_unitc = 0;
     int64_t n_aux = 0;
     std::vector<StepList> slists;  // K2 launches (unit, group), in launch order
     std::vector<int> slist_group;
@@ -809,6 +810,12 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
         c.o_stepmap = lay(c.n_approx > 0 ? (size_t)c.step_prefix[np] * 4 : 0);
         c.o_aux = lay((size_t)c.n_aux * sizeof(int2));
         c.o_slists = lay(c.slists.size() * sizeof(StepList));
+        c.n_cellc = (c.n_cells + (1 << kCoarseShift) - 1) >> kCoarseShift;
+        c.n_rc = (c.n_r + (1 << kCoarseShift) - 1) >> kCoarseShift;
+        c.n_unitc = (c.n_units + (1 << kUnitCoarseShift) - 1) >> kUnitCoarseShift;
+        c.o_cellc = lay((size_t)c.n_cellc * 4);
+        c.o_rc = lay((size_t)c.n_rc * 4);
+        c.o_unitc = lay((size_t)c.n_unitc * 4);
         c.small_bytes = o;
         c.small_off = align_up(blob_size, 256);
         blob_size = c.small_off + c.small_bytes;
@@ -857,6 +864,12 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
         int64_t *cellp = (int64_t *)(blk + c.o_cellp), *rp = (int64_t *)(blk + c.o_rp);
         int32_t *stepmap = (int32_t *)(blk + c.o_stepmap);
         int2 *aux = (int2 *)(blk + c.o_aux);
+        int32_t *cellc = (int32_t *)(blk + c.o_cellc), *rc = (int32_t *)(blk + c.o_rc), *unitc = (int32_t *)(blk + c.o_unitc);
+        // the coarse entries whose position falls in [first, first + n): problem x
+        auto coarse = [](int32_t *map, int shift, int64_t first, int64_t n, int x) {
+            const int64_t step = (int64_t)1 << shift;
+            for (int64_t b = (first + step - 1) >> shift; (b << shift) < first + n; ++b) map[b] = x;
+        };
         cellp[0] = 0;
         rp[0] = 0;
         const bool map_steps = c.n_approx > 0;        // K2 tile -> problem map of the collapsed-DP step (K2c)
@@ -880,6 +893,9 @@ extern "C" int gbmw_batch_create(gbmw_ctx *ctx, const gbmw_layer *layers, int64_
                 d.layer_begin = P.layer_begin; d.strat_begin = P.strat_begin; d.result_index = pi;
                 d.n_sweep_tiles = (int32_t)h.n_tiles;
                 std::memcpy(dps + x, &d, sizeof(d));
+                coarse(cellc, kCoarseShift, s[0], h.n_cells, x);
+                coarse(rc, kCoarseShift, s[1], h.n_r, x);
+                coarse(unitc, kUnitCoarseShift, s[5], h.U, x);
                 s[0] += h.n_cells; s[1] += h.n_r; s[2] += h.n_bcells; s[3] += h.n_par; s[4] += h.n_tiles;
                 s[5] += h.U; s[6] += h.n_flagw; s[7] += h.n_rmap;
                 cellp[x + 1] = s[0];
@@ -979,6 +995,10 @@ ChunkArgs chunk_args(gbmw_batch *b, const Chunk &c, char *ws, size_t chunk_index
     a.unit_first = (const int32_t *)(sm + c.o_uf);
     a.unit_count = (const int32_t *)(sm + c.o_uc);
     a.step_map = (const int32_t *)(sm + c.o_stepmap);
+    a.cell_coarse = (const int32_t *)(sm + c.o_cellc);
+    a.r_coarse = (const int32_t *)(sm + c.o_rc);
+    a.unit_coarse = (const int32_t *)(sm + c.o_unitc);
+    a.n_cell_coarse = c.n_cellc; a.n_r_coarse = c.n_rc; a.n_unit_coarse = c.n_unitc;
     a.aux_map = (const int2 *)(sm + c.o_aux);
     a.step_lists = (const StepList *)(sm + c.o_slists);
     a.n_step_lists = (int32_t)c.slists.size();

@@ -20,6 +20,8 @@ namespace gbmw {
 
 constexpr int kMaxUnits = 1024;      // backtrack path held in local memory
 constexpr int kMaxClasses = 16;
+constexpr int kCoarseShift = 10;     // K1 coarse maps: one entry per 1024 cells / R entries
+constexpr int kUnitCoarseShift = 6;  // and per 64 units
 constexpr int kMaxStrats = 512;      // smem staging of per-strategy constants
 constexpr int kStepThreads = 256;    // threads per K2 CTA
 constexpr int kStepRows = 2048;      // rows per K2 tile (64 groups of 32)
@@ -166,6 +168,10 @@ struct ChunkArgs {
     const int64_t *r_prefix;      // n_probs + 1
     const int64_t *step_tiles;    // n_probs + 1, tiles of ceil(n_e / kStepRows)
     const int32_t *step_map;      // K2 tile -> problem (sorted position)
+    // coarse position maps for the K1 index searches: the problem holding cell / R entry
+    // b << kCoarseShift, and global unit b << kUnitCoarseShift (sorted positions)
+    const int32_t *cell_coarse, *r_coarse, *unit_coarse;
+    int64_t n_cell_coarse, n_r_coarse, n_unit_coarse;
     const int2 *aux_map;          // K3r tiles: (problem, tile) of frontier / collapsed-DP problems
     const StepList *step_lists;   // K2 launches of the chunk
     int32_t n_step_lists;

@@ -31,6 +31,19 @@ __device__ __forceinline__ int find_slot(const int64_t *prefix, int n, int64_t x
     return lo;
 }
 
+// The same search started from a coarse map: the slot holds position x is between the slots
+// holding coarse entries x >> shift and (x >> shift) + 1, usually the same one.
+__device__ __forceinline__ int find_slot_coarse(const int64_t *prefix, int n, int64_t x, const int32_t *coarse,
+                                                int64_t n_coarse, int shift) {
+    const int64_t b = x >> shift;
+    int lo = __ldg(coarse + b), hi = b + 1 < n_coarse ? __ldg(coarse + b + 1) : n - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (prefix[mid] <= x) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
 // Python's `int <= float` is exact; e_fwd = e * gran is an int.
 __device__ __forceinline__ bool int_le_double(int64_t x, double y) {
     if (y != y) return false;
@@ -43,7 +56,7 @@ __device__ __forceinline__ bool int_le_double(int64_t x, double y) {
 __global__ void k_cost_cells(ChunkArgs a, int64_t n_cells) {
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= n_cells) return;
-    const int q = find_slot(a.cell_prefix, a.n_probs, idx);
+    const int q = find_slot_coarse(a.cell_prefix, a.n_probs, idx, a.cell_coarse, a.n_cell_coarse, kCoarseShift);
     const DevProblem &p = a.probs[q];
     const int64_t local = idx - a.cell_prefix[q];
     const int u = (int)(local / p.S);
@@ -76,7 +89,7 @@ __global__ void k_cost_cells(ChunkArgs a, int64_t n_cells) {
 __global__ void k_cost_r(ChunkArgs a, int64_t n_r) {
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= n_r) return;
-    const int q = find_slot(a.r_prefix, a.n_probs, idx);
+    const int q = find_slot_coarse(a.r_prefix, a.n_probs, idx, a.r_coarse, a.n_r_coarse, kCoarseShift);
     const DevProblem &p = a.probs[q];
     const int64_t local = idx - a.r_prefix[q];
     const int KK = p.K * p.K;
@@ -107,7 +120,8 @@ __global__ void k_dedupe(ChunkArgs a) {
     const int lane = threadIdx.x & 31;
     const int64_t gu = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (gu >= a.n_units) return;
-    int qa = 0, qb = a.n_probs - 1;                      // problem holding global unit gu
+    const int64_t cb = gu >> kUnitCoarseShift;           // problem holding global unit gu
+    int qa = __ldg(a.unit_coarse + cb), qb = cb + 1 < a.n_unit_coarse ? __ldg(a.unit_coarse + cb + 1) : a.n_probs - 1;
     while (qa < qb) {
         const int mid = (qa + qb + 1) >> 1;
         if (a.probs[mid].ustate_off <= gu) qa = mid; else qb = mid - 1;
