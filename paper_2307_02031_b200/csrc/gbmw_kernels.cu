@@ -54,8 +54,10 @@ __device__ __forceinline__ bool int_le_double(int64_t x, double y) {
 
 // ---------------------------------------------------------------- K1: cost tables
 __global__ void k_cost_cells(ChunkArgs a, int64_t n_cells) {
-    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= n_cells) return;
+    const int64_t idx0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool valid = idx0 < n_cells;
+    if (__all_sync(0xffffffffu, !valid)) return;         // whole warps only: the b_up max below is warp-wide
+    const int64_t idx = valid ? idx0 : n_cells - 1;       // past the end: a duplicate of the last cell
     const int q = find_slot_coarse(a.cell_prefix, a.n_probs, idx, a.cell_coarse, a.n_cell_coarse, kCoarseShift);
     const DevProblem &p = a.probs[q];
     const int64_t local = idx - a.cell_prefix[q];
@@ -77,13 +79,25 @@ __global__ void k_cost_cells(ChunkArgs a, int64_t n_cells) {
     if (w < 0) w = 0;                            // dpsearch.py:145
     c.w = (int32_t)w;
     c.k = a.cand_cls[p.cand_off + i];
-    a.cells[p.cell_off + local] = c;
-    CellMem cm;
-    cm.o_f = m.o_f; cm.o_b = m.o_b; cm.o_ms = m.o_ms;
-    a.cmem[p.cell_off + local] = cm;
+    if (valid) {
+        a.cells[p.cell_off + local] = c;
+        CellMem cm;
+        cm.o_f = m.o_f; cm.o_b = m.o_b; cm.o_ms = m.o_ms;
+        a.cmem[p.cell_off + local] = cm;
+    }
     // b_up = max O_b over (unit, strategy)  (dpsearch.py:162); O_b >= 0 so the bit
-    // pattern orders like the value
-    atomicMax(&a.bup[q], (unsigned long long)__double_as_longlong(m.o_b));
+    // pattern orders like the value.  Consecutive lanes hold consecutive cells, so a
+    // problem's lanes are a contiguous run: a segmented max, then one atomic per run.
+    const int lane = threadIdx.x & 31;
+    unsigned long long v = (unsigned long long)__double_as_longlong(m.o_b);
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const unsigned long long ov = __shfl_down_sync(0xffffffffu, v, off);
+        const int oq = __shfl_down_sync(0xffffffffu, q, off);
+        if (lane + off < 32 && oq == q && ov > v) v = ov;
+    }
+    const int pq = __shfl_up_sync(0xffffffffu, q, 1);
+    if (valid && (lane == 0 || pq != q)) atomicMax(&a.bup[q], v);
 }
 
 __global__ void k_cost_r(ChunkArgs a, int64_t n_r) {
