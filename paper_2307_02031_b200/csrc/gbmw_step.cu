@@ -662,8 +662,17 @@ __global__ void __launch_bounds__(kStepThreads, GROUP <= 1 ? 3 : 1)
         }
         __syncwarp();
     }
-    if (lane == 0 && stat_rows) atomicAdd(a.computed_cells, stat_rows);
+    // the statistics counter is one address for the whole pass: one atomic per CTA, not per
+    // warp (same-address atomics serialise in L2 and the grid completes only after them)
+    __shared__ unsigned long long s_stat[kK2Warps];
+    if (lane == 0) s_stat[warp] = stat_rows;
     __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long tot = 0;
+#pragma unroll
+        for (int w = 0; w < kK2Warps; ++w) tot += s_stat[w];
+        if (tot) atomicAdd(a.computed_cells, tot);
+    }
     tl_mark(a.k2_tl, tl_id, true);
     pdl_trigger();
 }
