@@ -854,10 +854,19 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
         n_cands += __shfl_xor_sync(0xffffffffu, n_cands, off);
         n_checks += __shfl_xor_sync(0xffffffffu, n_checks, off);
     }
-    if (lane == 0 && n_rows) {
-        atomicAdd(a.sweep_stats, n_rows);
-        atomicAdd(a.sweep_stats + 1, n_cands);
-        atomicAdd(a.sweep_stats + 2, n_checks);
+    // three statistics counters for the whole pass: one atomic each per CTA, not per warp
+    // (same-address atomics serialise in L2 and the grid completes only after them); the
+    // tile loop above is CTA-uniform, so every thread gets here
+    __shared__ unsigned long long s_st[kSweepThreads / 32][3];
+    if (lane == 0) {
+        const int wid = threadIdx.x >> 5;
+        s_st[wid][0] = n_rows; s_st[wid][1] = n_cands; s_st[wid][2] = n_checks;
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+        unsigned long long tot = 0;
+        for (int w = 0; w < kSweepThreads / 32; ++w) tot += s_st[w][threadIdx.x];
+        if (tot) atomicAdd(a.sweep_stats + threadIdx.x, tot);
     }
 }
 
