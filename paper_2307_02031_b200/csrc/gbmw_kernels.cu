@@ -117,11 +117,15 @@ __global__ void k_cost_r(ChunkArgs a, int64_t n_r) {
         a.class_d[p.class_off + kb], a.class_t[p.class_off + kb], p.micro, env.intra_island_bw);
 }
 
-// Source-side de-duplication (exact): two strategies with identical (weight, class,
-// time_c, ef_true) at unit u produce identical (T, F) in every row of the unit-u
-// table, hence identical candidates for every target; with ties resolved to the
-// first index (T1) the later one can never be an argmin.  K2 relaxes only the
-// first of each group.  A warp per (problem, unit).
+// Source-side pruning by dominance (exact): strategies j < i with the same weight and
+// class at unit u read the same row and column of B_u, so in every row
+// T_j = v.t + c_j and F_j = v.f + ef_j against T_i = v.t + c_i and F_i = v.f + ef_i.
+// fp addition is monotone, so c_j <= c_i and ef_j <= ef_i give T_j <= T_i, F_j <= F_i
+// (and the same for every target after + R[cls, k]); with ties resolved to the first
+// index (T1), i can never be an argmin.  This covers the identical cells (the exact
+// duplicates) and, e.g., 38 -> 26 sources per GPT-3-96 P = 1 unit.  K2 relaxes only
+// the surviving sources; the sweep's rank-0 candidate (K3a, K3r) is never a dominated
+// one either, and K3b walks every strategy.  A warp per (problem, unit).
 //
 // The same pass derives the live row range of every class table B_u: with
 // wmin_v = min_i weight[v][i], T_u is +inf below m_u = sum_{v<=u} wmin_v, so
@@ -155,7 +159,7 @@ __global__ void k_dedupe(ChunkArgs a) {
             keep = true;
             for (int j = 0; j < i; ++j) {
                 const Cell cj = cells[j];
-                if (cj.w == ci.w && cj.k == ci.k && cj.c == ci.c && cj.ef == ci.ef) { keep = false; break; }
+                if (cj.w == ci.w && cj.k == ci.k && cj.c <= ci.c && cj.ef <= ci.ef) { keep = false; break; }
             }
         }
         const unsigned m = __ballot_sync(0xffffffffu, keep);
