@@ -133,6 +133,8 @@ struct gbmw_ctx {
     cudaStream_t aux[kNumGroups] = {nullptr};   // K2 groups 1.. run concurrently with group 0
     cudaEvent_t fork = nullptr, join[kNumGroups] = {nullptr};
     cudaStream_t list_stream = nullptr;           // K2l, concurrent with the first steps (K2f / K2s)
+    cudaStream_t tstream = nullptr;               // timing: waits for every group's K2 (ev[2])
+    cudaEvent_t k2done[kNumGroups] = {nullptr};
     cudaEvent_t list_done = nullptr;
     cudaEvent_t gspan[kNumGroups][2] = {{nullptr}};   // debug (GBMW_K2_HIST): per-stream K2 span
     uint64_t workspace_limit = 0;
@@ -389,6 +391,9 @@ extern "C" int gbmw_ctx_destroy(gbmw_ctx *ctx) {
     }
     if (ctx->fork) cudaEventDestroy(ctx->fork);
     if (ctx->list_stream) cudaStreamDestroy(ctx->list_stream);
+    if (ctx->tstream) cudaStreamDestroy(ctx->tstream);
+    for (auto &e : ctx->k2done)
+        if (e) cudaEventDestroy(e);
     if (ctx->list_done) cudaEventDestroy(ctx->list_done);
     if (ctx->seed_buf) cudaFree(ctx->seed_buf);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -543,8 +548,8 @@ WsLayout ws_layout(const Chunk &c) {
     w.ufirst = o; o = align_up(o + c.probs.size() * 4);
     w.upruned = o; o = align_up(o + c.probs.size() * 4);
     w.usorted = o; o = align_up(o + c.probs.size() * 4);
-    w.uprefix = o; o = align_up(o + (kMaxSweepRanks + 1) * 8);
-    w.uctr = o; o = align_up(o + 8);
+    w.uprefix = o; o = align_up(o + (size_t)kNumGroups * (kMaxSweepRanks + 1) * 8);   // one per group sweep
+    w.uctr = o; o = align_up(o + (size_t)kNumGroups * 8);
     w.uniq = o; o = align_up(o + c.n_cells * 4);
     w.ucell = o; o = align_up(o + c.n_cells * sizeof(Cell));
     w.nuniq = o; o = align_up(o + c.n_units * 4);
@@ -1054,6 +1059,19 @@ ChunkArgs chunk_args(gbmw_batch *b, const Chunk &c, char *ws, size_t chunk_index
     return a;
 }
 
+// The sweep / finalize view of one group's problems [lo, lo + n): per-problem arrays offset
+// to the group, its own K3b work-list prefix and counter (groups sweep concurrently).
+ChunkArgs group_view(const ChunkArgs &a, int lo, int n, int g) {
+    ChunkArgs s = a;
+    s.probs += lo; s.n_probs = n;
+    s.bup += lo; s.best += lo; s.bound += 2 * (int64_t)lo;
+    s.ufirst += lo; s.upruned += lo; s.usorted += lo;
+    s.uprefix += (int64_t)g * (kMaxSweepRanks + 1);
+    s.ucounter += g;
+    s.n_aux = 0;
+    return s;
+}
+
 int cuda_fail(gbmw_ctx *ctx, int rc, const char *what) {
     return set_err(&ctx->err, GBMW_ECUDA, std::string(what) + ": " + cudaGetErrorString((cudaError_t)rc));
 }
@@ -1180,18 +1198,58 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
         if (k2_spans)
             for (int g = 0; g < kNumGroups; ++g)
                 if (used[g] || g == 0) cudaEventRecord(ctx->gspan[g][1], gs[g]);
+        // Without K3r tiles (frontier requests, collapsed-DP problems) every group sweeps and
+        // finalises its own problems on its own stream right after its last layer step, so
+        // the shallow groups' K3/K4 run while the deep groups are still in K2.  ev[2] marks
+        // the end of K2 on every stream (a timing stream waits for all of them).
+        static const bool no_group_sweep = getenv("GBMW_SWEEP_PER_GROUP") && getenv("GBMW_SWEEP_PER_GROUP")[0] == '0';
+        // shallow groups' K3b at 3 CTAs per SM (occupancy allows 4): the deep groups' layer
+        // steps keep SM slots (measured on the 10k sweep: 2 per SM 7.53-7.67 ms, 3 per SM 7.44-7.51,
+        // 4 per SM 8.04-8.08, one sweep after every group's K2 7.70-7.75)
+        static const int group_ctas = getenv("GBMW_SWEEP_GROUP_CTAS") ? atoi(getenv("GBMW_SWEEP_GROUP_CTAS")) : 3;
+        static const int group_min = getenv("GBMW_SWEEP_GROUP_MIN") ? atoi(getenv("GBMW_SWEEP_GROUP_MIN")) : 2000;
+        const bool per_group = c.n_aux == 0 && (int64_t)c.probs.size() >= group_min && !no_group_sweep;
+        if (per_group) {
+            if (!ctx->tstream) {
+                if (cudaStreamCreateWithFlags(&ctx->tstream, cudaStreamNonBlocking) != cudaSuccess)
+                    return cuda_fail(ctx, (int)cudaGetLastError(), "timing stream");
+                for (auto &e : ctx->k2done)
+                    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
+                        return cuda_fail(ctx, (int)cudaGetLastError(), "K2 done events");
+            }
+            for (int g = 0; g < kNumGroups; ++g) {
+                if (g != 0 && gs[g] == st) continue;
+                cudaEventRecord(ctx->k2done[g], gs[g]);
+                cudaStreamWaitEvent(ctx->tstream, ctx->k2done[g], 0);
+            }
+            if (lists) cudaStreamWaitEvent(ctx->tstream, ctx->list_done, 0);
+            cudaEventRecord(c.ev[2], ctx->tstream);
+            for (int g = 0; g < kNumGroups; ++g) {
+                const int lo = c.group_lo[g], n = c.group_lo[g + 1] - lo;
+                if (n <= 0) continue;
+                const ChunkArgs sub = group_view(a, lo, n, g);
+                if ((rc = launch_sweep(sub, gs[g], (g < kStepVGroups && g % kBands == 1) ? group_ctas : 0))) return cuda_fail(ctx, rc, "K3 launch");
+                if ((rc = launch_finalize(sub, gs[g]))) return cuda_fail(ctx, rc, "K4 launch");
+                c.launches += 4;
+            }
+        }
         for (int g = 1; g < kNumGroups; ++g) {
             if (gs[g] == st) continue;
             cudaEventRecord(ctx->join[g], gs[g]);
             cudaStreamWaitEvent(st, ctx->join[g], 0);
         }
         if (lists) cudaStreamWaitEvent(st, ctx->list_done, 0);
-        cudaEventRecord(c.ev[2], st);
-        if ((rc = launch_sweep(a, st))) return cuda_fail(ctx, rc, "K3 launch");
-        cudaEventRecord(c.ev[3], st);
-        if ((rc = launch_finalize(a, st))) return cuda_fail(ctx, rc, "K4 launch");
-        c.launches += 4 + (c.n_aux > 0);
-        cudaEventRecord(c.ev[4], st);
+        if (per_group) {
+            cudaEventRecord(c.ev[3], st);                // sweep_ms: K3 + K4 past the end of K2
+            cudaEventRecord(c.ev[4], st);
+        } else {
+            cudaEventRecord(c.ev[2], st);
+            if ((rc = launch_sweep(a, st))) return cuda_fail(ctx, rc, "K3 launch");
+            cudaEventRecord(c.ev[3], st);
+            if ((rc = launch_finalize(a, st))) return cuda_fail(ctx, rc, "K4 launch");
+            c.launches += 4 + (c.n_aux > 0);
+            cudaEventRecord(c.ev[4], st);
+        }
     }
     cudaError_t ce = cudaStreamSynchronize(st);
     if (ce != cudaSuccess) return cuda_fail(ctx, (int)ce, "search kernels");

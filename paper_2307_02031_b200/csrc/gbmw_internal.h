@@ -230,7 +230,7 @@ int launch_dp_first(const ChunkArgs &a, int p_lo, int p_n, void *stream);
 constexpr int kSecondMaxS = 60;
 constexpr int64_t kSecondMaxRows = 131072;
 int launch_dp_second(const ChunkArgs &a, int group, int p_lo, int p_n, void *stream);
-int launch_sweep(const ChunkArgs &a, void *stream);
+int launch_sweep(const ChunkArgs &a, void *stream, int ctas_per_sm = 0);   // K3b's persistent grid (0: occupancy)
 int launch_approx_step(const ChunkArgs &a, int u, int64_t tile_base, int64_t n_tiles, unsigned long long *counter,
                        void *stream);
 int launch_finalize(const ChunkArgs &a, void *stream);

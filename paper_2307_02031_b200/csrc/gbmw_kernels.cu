@@ -1199,23 +1199,25 @@ int launch_cost_tables(const ChunkArgs &a, int64_t n_cells, int64_t n_r, void *s
     return (int)cudaGetLastError();
 }
 
-int launch_sweep(const ChunkArgs &a, void *stream) {
+int launch_sweep(const ChunkArgs &a, void *stream, int ctas_per_sm) {
     if (a.n_probs <= 0) return 0;
     cudaStream_t st = (cudaStream_t)stream;
     k_sweep_safe<<<blocks_for(a.n_probs, 4), 128, 0, st>>>(a);
     if (a.n_aux > 0) k_sweep_rows<<<(unsigned)a.n_aux, kSweepThreads, 0, st>>>(a);
     k_sweep_scan<<<1, 1024, 0, st>>>(a);
-    static int grid[64] = {0};
+    static int occ_of[64] = {0}, sms_of[64] = {0};
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 0 || dev >= 64) dev = 0;
-    if (!grid[dev]) {
+    if (!occ_of[dev]) {
         int occ = 0, sms = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sweep_unsafe, kSweepThreads, 0);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        grid[dev] = (occ > 0 ? occ : 1) * (sms > 0 ? sms : 148);
+        sms_of[dev] = sms > 0 ? sms : 148;
+        occ_of[dev] = occ > 0 ? occ : 1;
     }
-    k_sweep_unsafe<<<grid[dev], kSweepThreads, 0, st>>>(a);
+    const int per_sm = (ctas_per_sm > 0 && ctas_per_sm < occ_of[dev]) ? ctas_per_sm : occ_of[dev];
+    k_sweep_unsafe<<<per_sm * sms_of[dev], kSweepThreads, 0, st>>>(a);
     return (int)cudaGetLastError();
 }
 

@@ -10,7 +10,7 @@ for line in open(f"gpurun_out/bench_{tag}.log"):
               "e2e ms", round(d["e2e"]["ms_per_step"], 3), "clocks", d["clocks"]["sm_mhz"])
 for w in ["gpt96", "gpt96-bmw", "swin-bmw", "vit-bmw", "bert", "t5-16"]:
     try:
-        d = json.load(open(f"gpurun_out/fs_{w}.json"))
+        d = json.load(open(f"gpurun_out/fs_{w}{sys.argv[2] if len(sys.argv) > 2 else ''}.json"))
         print(w, round(d["ms_per_step"], 2), "device", round(d.get("device_ms", 0), 2))
     except Exception as ex:  # noqa: BLE001
         print(w, "?", ex)
