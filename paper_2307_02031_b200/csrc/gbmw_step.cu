@@ -24,6 +24,7 @@
 // (cand, F, i), first i) is the reference's for every row.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "gbmw_internal.h"
 
@@ -459,7 +460,7 @@ __device__ __forceinline__ void finish_tile(const ChunkArgs &a, const TileCtx &t
     // entry with row >= 32 g
     int b0 = 0, b1 = n;
     if (t.goff) {
-        b0 = __ldcg(t.goff + g);
+        b0 = GLOBAL ? (int)__ldcg(t.goff + g) : (int)t.goff[g];
     } else {
         while (b0 < b1) {
             const int mid = (b0 + b1) >> 1;
@@ -737,6 +738,63 @@ __global__ void __launch_bounds__(kStepThreads, GROUP <= 1 ? 3 : 1)
         R = __shfl_sync(0xffffffffu, nx, 0);
     }
     __syncthreads();
+    tl_mark(a.k2_tl, tl_id, true);
+    pdl_trigger();
+}
+
+// K2t: both halves of a layer step in one kernel, a CTA per tile, for launches with few
+// tiles (the deep bands' tail, where the step chain, not the throughput, bounds the pass):
+// warp 0 classifies the tile into shared memory, the CTA's warps share its rounds, warp 0
+// finishes it.  No hand-off through global memory and no second kernel per step.
+constexpr int kTileThreads = 128;
+constexpr int kTileWarps = kTileThreads / 32;
+
+template <int GROUP, bool FIRST>
+__global__ void __launch_bounds__(kTileThreads)
+    k_dp_tile(ChunkArgs a, int u, const int4 *items, const int64_t *count, int tl_id) {
+    pdl_wait();
+    tl_mark(a.k2_tl, tl_id, false);
+    __shared__ TileCtx s_t;
+    __shared__ uint16_t s_erow[kWarpRows];
+    __shared__ uint16_t s_echg[kWarpRows];
+    __shared__ uint16_t s_alist[kMaxStrats];
+    __shared__ uint16_t s_goff[34];
+    __shared__ int s_n;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    TileCtx &t = s_t;
+    const int64_t it = blockIdx.x;
+    if (it < *count) {                                   // CTA-uniform
+        if (warp == 0) {
+            const int4 item = __ldg(items + it);
+            const unsigned long long *src = reinterpret_cast<const unsigned long long *>(
+                reinterpret_cast<const char *>(a.step_ctx) + (int64_t)item.w * kStepCtxBytes);
+            unsigned long long *dst = reinterpret_cast<unsigned long long *>(&t);
+            if (lane < (int)(sizeof(TileCtx) / 8)) dst[lane] = __ldg(src + lane);
+            __syncwarp();
+            if (lane == 0) {
+                t.r_base = item.y * kWarpRows;
+                t.erow = s_erow; t.echg = s_echg; t.goff = nullptr;
+            }
+            __syncwarp();
+            const int n = classify_tile<FIRST>(a, t, s_alist, s_goff, u, lane);
+            if (lane == 0) { s_n = n; t.goff = s_goff; }
+        }
+        __syncthreads();
+        const int n = s_n, K = t.K;
+        const int rounds = tile_rounds(n);
+        for (int r = warp; r < rounds; r += kTileWarps) {
+#define GBMW_K2_EVAL(KT, G) eval_round<KT, FIRST, G>(a, t, u, r, lane)
+            GBMW_K2_DISPATCH(GBMW_K2_EVAL)
+#undef GBMW_K2_EVAL
+        }
+        __syncthreads();
+        if (warp == 0) {
+#define GBMW_K2_FIN(KT, G) finish_tile<KT, G, false>(a, t, u, lane)
+            GBMW_K2_DISPATCH(GBMW_K2_FIN)
+#undef GBMW_K2_FIN
+            if (lane == 0 && n) atomicAdd(a.computed_cells, (unsigned long long)n * (unsigned long long)K);
+        }
+    }
     tl_mark(a.k2_tl, tl_id, true);
     pdl_trigger();
 }
@@ -1201,6 +1259,23 @@ int launch_dp_step(const ChunkArgs &a, int group, int u, const int4 *items, cons
     cfg_a.attrs = attr; cfg_a.numAttrs = 1;
     cfg_b = cfg_a; cfg_b.gridDim = dim3(grid_b);
     const int ta = 2 * tl_id, tb = 2 * tl_id + 1;
+    // few tiles: one fused kernel, a CTA per tile (GBMW_TILE_FUSED_MAX: the item bound up to
+    // which it is used; 0 disables it).  Measured bounds 0 / 2048 / 3072 / 4096: 10k sweep
+    // 7.52-7.58 / 7.34-7.48 / 7.72-7.75 / 7.76 ms; device time of the full searches at 2048:
+    // gpt96 23.3 -> 21.1 ms, swin-bmw 38.5 -> 31.5 ms, vit-bmw 29.5 -> 23.8 ms
+    static const int64_t fused_max = getenv("GBMW_TILE_FUSED_MAX") ? atoll(getenv("GBMW_TILE_FUSED_MAX")) : 2048;
+    if (n_items <= fused_max) {
+        cudaLaunchConfig_t cfg_t = cfg_a;
+        cfg_t.gridDim = dim3((unsigned)n_items); cfg_t.blockDim = dim3(kTileThreads);
+#define GBMW_TILE(G)                                                                                    \
+        if (fi) cudaLaunchKernelEx(&cfg_t, k_dp_tile<G, true>, a, u, items, count, ta);                  \
+        else cudaLaunchKernelEx(&cfg_t, k_dp_tile<G, false>, a, u, items, count, ta);
+        if (group == 0) { GBMW_TILE(0) }
+        else if (group == 1) { GBMW_TILE(1) }
+        else { GBMW_TILE(2) }
+#undef GBMW_TILE
+        return (int)cudaGetLastError();
+    }
 #define GBMW_STEP(G)                                                                                    \
     if (fi) {                                                                                           \
         cudaLaunchKernelEx(&cfg_a, k_dp_classify<G, true>, a, u, items, count, ctr, rounds, ta);        \
