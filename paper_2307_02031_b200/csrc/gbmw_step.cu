@@ -746,11 +746,8 @@ __global__ void __launch_bounds__(kStepThreads, GROUP <= 1 ? 3 : 1)
 // tiles (the deep bands' tail, where the step chain, not the throughput, bounds the pass):
 // warp 0 classifies the tile into shared memory, the CTA's warps share its rounds, warp 0
 // finishes it.  No hand-off through global memory and no second kernel per step.
-constexpr int kTileThreads = 128;
-constexpr int kTileWarps = kTileThreads / 32;
-
-template <int GROUP, bool FIRST>
-__global__ void __launch_bounds__(kTileThreads)
+template <int GROUP, bool FIRST, int kTileWarps>
+__global__ void __launch_bounds__(32 * kTileWarps)
     k_dp_tile(ChunkArgs a, int u, const int4 *items, const int64_t *count, int tl_id) {
     pdl_wait();
     tl_mark(a.k2_tl, tl_id, false);
@@ -1264,12 +1261,20 @@ int launch_dp_step(const ChunkArgs &a, int group, int u, const int4 *items, cons
     // 7.52-7.58 / 7.34-7.48 / 7.72-7.75 / 7.76 ms; device time of the full searches at 2048:
     // gpt96 23.3 -> 21.1 ms, swin-bmw 38.5 -> 31.5 ms, vit-bmw 29.5 -> 23.8 ms
     static const int64_t fused_max = getenv("GBMW_TILE_FUSED_MAX") ? atoll(getenv("GBMW_TILE_FUSED_MAX")) : 2048;
+    // eight warps per tile CTA up to this item bound, four above it
+    static const int64_t wide_max = getenv("GBMW_TILE_WIDE_MAX") ? atoll(getenv("GBMW_TILE_WIDE_MAX")) : 1024;
     if (n_items <= fused_max) {
         cudaLaunchConfig_t cfg_t = cfg_a;
-        cfg_t.gridDim = dim3((unsigned)n_items); cfg_t.blockDim = dim3(kTileThreads);
+        const bool wide = n_items <= wide_max;
+        cfg_t.gridDim = dim3((unsigned)n_items); cfg_t.blockDim = dim3(wide ? 256 : 128);
 #define GBMW_TILE(G)                                                                                    \
-        if (fi) cudaLaunchKernelEx(&cfg_t, k_dp_tile<G, true>, a, u, items, count, ta);                  \
-        else cudaLaunchKernelEx(&cfg_t, k_dp_tile<G, false>, a, u, items, count, ta);
+        if (wide) {                                                                                     \
+            if (fi) cudaLaunchKernelEx(&cfg_t, k_dp_tile<G, true, 8>, a, u, items, count, ta);           \
+            else cudaLaunchKernelEx(&cfg_t, k_dp_tile<G, false, 8>, a, u, items, count, ta);             \
+        } else {                                                                                        \
+            if (fi) cudaLaunchKernelEx(&cfg_t, k_dp_tile<G, true, 4>, a, u, items, count, ta);           \
+            else cudaLaunchKernelEx(&cfg_t, k_dp_tile<G, false, 4>, a, u, items, count, ta);             \
+        }
         if (group == 0) { GBMW_TILE(0) }
         else if (group == 1) { GBMW_TILE(1) }
         else { GBMW_TILE(2) }
