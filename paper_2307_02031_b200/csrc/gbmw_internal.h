@@ -48,7 +48,7 @@ __host__ __device__
 #endif
 inline int64_t rmap_groups(int64_t n_e) { return (n_e + 31) / 32; }
 constexpr int kSweepThreads = 256;   // rows per K3 tile
-constexpr int kSweepWK = 4096;       // (unit, strategy) pairs staged in shared memory by K3b
+constexpr int kSweepWK = 4608;       // (unit, strategy) pairs staged in shared memory by K3b (GPT-3-96 P = 1: 96 x 46)
 constexpr int kSweepRmap = 1536;     // row-map entries of B_{U-1} staged in shared memory by K3b (n_e <= 49152)
 constexpr int kMaxSweepRanks = 4096; // >= sweep tiles of one problem: ceil(GBMW_MAX_BUCKETS / kSweepThreads)
 
