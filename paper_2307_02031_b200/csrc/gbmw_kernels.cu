@@ -332,18 +332,32 @@ __device__ __forceinline__ void backtrack_wk(const ChunkArgs &a, const DevProble
     }
 }
 
-// E_all of the expanded plan in layer order (costs.py:307-318).
+#ifndef GBMW_EALL_B_K3
+#define GBMW_EALL_B_K3 1                     // units in flight in K3b's E_all folds (2: 64-register cap spills, measured equal)
+#endif
+// E_all of the expanded plan in layer order (costs.py:307-318).  The units' memory terms
+// are fetched B at a time (independent loads in flight together), then folded in order.
+template <int B = 4>
 __device__ __forceinline__ double plan_e_all(const ChunkArgs &a, const DevProblem &p, const uint16_t *path) {
     double total_ms = 0.0, prefix_f = 0.0, peak = 0.0;
     const CellMem *cm = a.cmem + p.cell_off;
-    for (int u = 0; u < p.U; ++u) {
-        const CellMem m = cm[(int64_t)u * p.S + path[u]];
-        const int cnt = a.unit_count[p.unit_off + u];
-        for (int r = 0; r < cnt; ++r) {
-            total_ms = total_ms + m.o_ms;
-            prefix_f = prefix_f + m.o_f;
-            peak = py_max(peak, prefix_f + m.o_b);
+    const int32_t *uc = a.unit_count + p.unit_off;
+    for (int u0 = 0; u0 < p.U; u0 += B) {
+        CellMem m[B];
+        int cnt[B];
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+            const int u = u0 + b;
+            cnt[b] = 0;
+            if (u < p.U) { m[b] = cm[(int64_t)u * p.S + path[u]]; cnt[b] = uc[u]; }
         }
+#pragma unroll
+        for (int b = 0; b < B; ++b)
+            for (int r = 0; r < cnt[b]; ++r) {
+                total_ms = total_ms + m[b].o_ms;
+                prefix_f = prefix_f + m[b].o_f;
+                peak = py_max(peak, prefix_f + m[b].o_b);
+            }
     }
     return peak + total_ms;
 }
@@ -619,7 +633,7 @@ __global__ void __launch_bounds__(1024) k_sweep_scan(ChunkArgs a) {
 // compact list K3a/K3scan built, highest buckets of a problem first (they carry the
 // lowest times, so the bound tightens soonest).
 constexpr int kSweepBatch = 4;
-__global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
+__global__ void __launch_bounds__(kSweepThreads, 4) k_sweep_unsafe(ChunkArgs a) {
     __shared__ int32_t sW[kMaxStrats];
     __shared__ int32_t sK[kMaxStrats];
     __shared__ double sC[kMaxStrats];
@@ -842,7 +856,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
                 ++n_checks;
                 if (wk_smem) backtrack_wk(a, p, e, nj, path, sWK, r.rms);
                 else backtrack(a, p, e, nj, path);
-                if (plan_e_all(a, p, path) <= p.budget) {
+                if (plan_e_all<GBMW_EALL_B_K3>(a, p, path) <= p.budget) {
                     mt = nt; me = e; mj = nj;
                     bound_offer(bound, nt, e);
                     break;
@@ -917,7 +931,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_rows(ChunkArgs a) {
                 if (!fits) {
                     uint16_t path[kMaxUnits];
                     approx_reconstruct(a, p, e, path);
-                    fits = plan_e_all(a, p, path) <= p.budget;
+                    fits = plan_e_all<GBMW_EALL_B_K3>(a, p, path) <= p.budget;
                 }
                 if (fits) { mt = t; me = e; }
             }
@@ -1102,7 +1116,7 @@ __global__ void __launch_bounds__(32 * kFinWarps) k_finalize(ChunkArgs a) {
     if (be >= 0 && !(p.flags & GBMW_APPROX) && p.S <= 64)
         backtrack_warp(a, p, be, __shfl_sync(0xffffffffu, sj, 0), path, lane);
     __syncwarp();
-    if (lane == 0 && be >= 0) e_all = plan_e_all(a, p, path);
+    if (lane == 0 && be >= 0) e_all = plan_e_all<8>(a, p, path);
     int32_t *plan = a.plans + p.plan_off;
     if (be < 0) {
         for (int l = lane; l < p.n_layers; l += 32) plan[l] = -1;
@@ -1119,12 +1133,20 @@ __global__ void __launch_bounds__(32 * kFinWarps) k_finalize(ChunkArgs a) {
     const bool cost = (p.flags & GBMW_STAGE_COST) != 0;
     const bool wide = p.n_layers <= kFinLayers;         // layer terms by all lanes
     __syncwarp();
-    if (lane == 0 && wide) {                             // expand units to layers (dpsearch.py:230-234)
-        int l = 0;
-        for (int u = 0; u < p.U; ++u) {
-            const int gs = a.cand_strat[p.cand_off + path[u]];
-            const int cnt = a.unit_count[p.unit_off + u];
-            for (int r = 0; r < cnt; ++r, ++l) s_gs[warp][l] = gs;
+    if (wide) {                                          // expand units to layers (dpsearch.py:230-234)
+        int base = 0;                                    // lane u: unit u0 + u at its layer offset
+        for (int u0 = 0; u0 < p.U; u0 += 32) {
+            const int u = u0 + lane;
+            int gs = 0, cnt = 0;
+            if (u < p.U) { gs = a.cand_strat[p.cand_off + path[u]]; cnt = a.unit_count[p.unit_off + u]; }
+            int incl = cnt;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, incl, off);
+                if (lane >= off) incl += v;
+            }
+            for (int r = 0, l = base + incl - cnt; r < cnt; ++r, ++l) s_gs[warp][l] = gs;
+            base += __shfl_sync(0xffffffffu, incl, 31);
         }
     }
     __syncwarp();
