@@ -342,6 +342,18 @@ __device__ __forceinline__ double plan_e_all(const ChunkArgs &a, const DevProble
     double total_ms = 0.0, prefix_f = 0.0, peak = 0.0;
     const CellMem *cm = a.cmem + p.cell_off;
     const int32_t *uc = a.unit_count + p.unit_off;
+    if constexpr (B == 1) {
+        for (int u = 0; u < p.U; ++u) {
+            const CellMem m = cm[(int64_t)u * p.S + path[u]];
+            const int cnt = uc[u];
+            for (int r = 0; r < cnt; ++r) {
+                total_ms = total_ms + m.o_ms;
+                prefix_f = prefix_f + m.o_f;
+                peak = py_max(peak, prefix_f + m.o_b);
+            }
+        }
+        return peak + total_ms;
+    }
     for (int u0 = 0; u0 < p.U; u0 += B) {
         CellMem m[B];
         int cnt[B];
@@ -633,7 +645,7 @@ __global__ void __launch_bounds__(1024) k_sweep_scan(ChunkArgs a) {
 // compact list K3a/K3scan built, highest buckets of a problem first (they carry the
 // lowest times, so the bound tightens soonest).
 constexpr int kSweepBatch = 4;
-__global__ void __launch_bounds__(kSweepThreads, 4) k_sweep_unsafe(ChunkArgs a) {
+__global__ void __launch_bounds__(kSweepThreads) k_sweep_unsafe(ChunkArgs a) {
     __shared__ int32_t sW[kMaxStrats];
     __shared__ int32_t sK[kMaxStrats];
     __shared__ double sC[kMaxStrats];
