@@ -793,6 +793,8 @@ __global__ void __launch_bounds__(32 * kTileWarps)
         }
     }
     tl_mark(a.k2_tl, tl_id, true);
+    tl_mark(a.k2_tl, tl_id + 1, false);                  // debug timeline: an empty second half
+    tl_mark(a.k2_tl, tl_id + 1, true);
     pdl_trigger();
 }
 
@@ -1263,7 +1265,9 @@ int launch_dp_step(const ChunkArgs &a, int group, int u, const int4 *items, cons
     static const int64_t fused_max = getenv("GBMW_TILE_FUSED_MAX") ? atoll(getenv("GBMW_TILE_FUSED_MAX")) : 2048;
     // eight warps per tile CTA up to this item bound, four above it
     static const int64_t wide_max = getenv("GBMW_TILE_WIDE_MAX") ? atoll(getenv("GBMW_TILE_WIDE_MAX")) : 1024;
-    if (n_items <= fused_max) {
+    // class-count groups (bit g) that use it
+    static const int fused_groups = getenv("GBMW_TILE_FUSED_GROUPS") ? atoi(getenv("GBMW_TILE_FUSED_GROUPS")) : 7;
+    if (n_items <= fused_max && ((fused_groups >> group) & 1)) {
         cudaLaunchConfig_t cfg_t = cfg_a;
         const bool wide = n_items <= wide_max;
         cfg_t.gridDim = dim3((unsigned)n_items); cfg_t.blockDim = dim3(wide ? 256 : 128);
