@@ -419,7 +419,7 @@ def main():
             "wall_ms_per_step": float(allst[:, 2].max()),
             "phase_ms": {"dp_k2": float(np.mean(dp_ms)), "sweep_k3": float(np.mean(sweep_ms)),
                          "total": my_ms},
-            "roofline": {"kernel": "k_dp_classify + k_dp_rounds (K2)", "bound": "hbm", "achieved": achieved, "peak": hbm,
+            "roofline": {"kernel": "K2: k_dp_classify + k_dp_rounds, k_dp_tile (few-tile steps), k_dp_first, k_dp_second", "bound": "hbm", "achieved": achieved, "peak": hbm,
                          "peak_kind": kind, "unit": "GB/s", "frac": achieved / hbm,
                          "traffic": (tr or {}).get("bytes_per_launch") if tr else None,
                          "algorithmic_bytes_per_launch": alg / n_k2,
