@@ -60,7 +60,8 @@ class PlannerOptions:
     batch_radius: int = 16
     fuse_identical: bool = False
     approx_prev: bool = False
-    batch_window: int = 16          # batch sizes evaluated per device pass by galvatron_base
+    batch_window: int = 0           # batch sizes per device pass of galvatron_base (0: 16 for
+                                    # large clusters / deep models, else 32)
 
 
 @dataclass(frozen=True)
@@ -543,10 +544,15 @@ def galvatron_base(model, cluster, profile, opts: PlannerOptions = PlannerOption
     ctx = EvalContext(model=model, cluster=cluster, profile=profile)
     best: Plan | None = None
     batches = list(range(opts.batch_step, opts.max_batch + 1, opts.batch_step)) if opts.batch_step > 0 else []
-    window = max(1, opts.batch_window)
-    # a short first window where seeding is expensive (pipeline degrees >= 16: long hill
-    # climbs): the first window's seeding is the only one not hidden behind a device pass
-    first = max(1, window // 4) if min(cluster.n_devices, model.num_layers) >= 16 else window
+    # where seeding is expensive (pipeline degrees >= 16: long hill climbs) windows of 16 batch
+    # sizes and a short first window (its seeding is the only one not hidden behind a device
+    # pass); elsewhere a window's pass is bound by its deepest search's layer-step chain, not
+    # its width, so 32 batch sizes per pass halve the round trips (measured in
+    # profiles/README.md: swin-bmw 47.7 -> 38.3 ms, vit-bmw 38.8 -> 31.9 ms; gpt96 24.8 -> 31.1
+    # ms with 32, hence 16 there)
+    large = min(cluster.n_devices, model.num_layers) >= 16
+    window = max(1, opts.batch_window) if opts.batch_window > 0 else (16 if large else 32)
+    first = max(1, window // 4) if large else window
     chunks = [batches[:first]] + [batches[i:i + window] for i in range(first, len(batches), window)] \
         if batches else []
     if not chunks:

@@ -58,7 +58,7 @@ def test_algorithm1_window_independent(gpu):
     """The speculative batch window must not change the plan."""
     c = _drivers()["base"][0]
     ctx = W.config(c["model"], c["budget"])
-    for window in (1, 5):
+    for window in (1, 5, 32, 0):
         plan = galvatron_base(ctx.model, ctx.cluster, ctx.profile, PlannerOptions(batch_window=window))
         assert _plan(plan) == c["plan"]
 
