@@ -1180,10 +1180,11 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
                 c.launches += 1;
                 continue;
             }
+            int nk = 0;
             if ((rc = launch_dp_step(a, g / kBands, sl.u, a.step_items + sl.base, a.step_count + s, ub,
-                                     a.counters + ((size_t)sl.u * kNumGroups + g) * 3, rounds, (int)s, gs[g])))
+                                     a.counters + ((size_t)sl.u * kNumGroups + g) * 3, rounds, (int)s, gs[g], &nk)))
                 return cuda_fail(ctx, rc, "K2 launch");
-            c.launches += 1;
+            c.launches += nk;
         }
         // approx_prev problems: collapsed-state layer steps, unit 0 included
         for (int u = 0; u < c.Umax; ++u) {

@@ -223,7 +223,7 @@ struct ChunkArgs {
 int launch_cost_tables(const ChunkArgs &a, int64_t n_cells, int64_t n_r, void *stream);
 int launch_step_lists(const ChunkArgs &a, void *stream);
 int launch_dp_step(const ChunkArgs &a, int group, int u, const int4 *items, const int64_t *count, int64_t max_items,
-                   unsigned long long *counters3, int2 *rounds, int tl_id, void *stream);
+                   unsigned long long *counters3, int2 *rounds, int tl_id, void *stream, int *n_kernels);
 int launch_dp_first(const ChunkArgs &a, int p_lo, int p_n, void *stream);
 // u = 2 on candidate rows, for problems with S <= kSecondMaxS distinct strategies and
 // n_e <= kSecondMaxRows rows (gbmw_step.cu)

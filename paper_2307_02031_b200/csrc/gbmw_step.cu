@@ -1224,8 +1224,9 @@ int launch_dp_second(const ChunkArgs &a, int group, int p_lo, int p_n, void *str
 }
 
 int launch_dp_step(const ChunkArgs &a, int group, int u, const int4 *items, const int64_t *count, int64_t n_items,
-                   unsigned long long *ctr, int2 *rounds, int tl_id, void *stream) {
+                   unsigned long long *ctr, int2 *rounds, int tl_id, void *stream, int *n_kernels) {
     cudaStream_t st = (cudaStream_t)stream;
+    *n_kernels = 0;
     if (n_items <= 0) return 0;
     static int sms = 0;
     static int occ[kStepGroups][2][2] = {{{0}}};
@@ -1283,6 +1284,7 @@ int launch_dp_step(const ChunkArgs &a, int group, int u, const int4 *items, cons
         else if (group == 1) { GBMW_TILE(1) }
         else { GBMW_TILE(2) }
 #undef GBMW_TILE
+        *n_kernels = 1;
         return (int)cudaGetLastError();
     }
 #define GBMW_STEP(G)                                                                                    \
@@ -1298,6 +1300,7 @@ int launch_dp_step(const ChunkArgs &a, int group, int u, const int4 *items, cons
     else { GBMW_STEP(2) }
 #undef GBMW_STEP
 #undef GBMW_PREP
+    *n_kernels = 2;
     return (int)cudaGetLastError();
 }
 
