@@ -250,6 +250,13 @@ int  gbmw_seed_partitions(const gbmw_layer *layers, int32_t n_layers, const gbmw
                           int32_t n_cells, const int64_t *pp_degree, const int64_t *micro_batch,
                           const int32_t *n_micro, double budget, int32_t max_stages, int32_t n_threads,
                           int32_t *out_sizes);
+/* Algorithm 2's trajectory set-up (balance.py:366-384 as _run_trajectories runs it) for many
+ * (pp_degree, micro_batch, n_micro) cells, on up to n_threads host threads: the _seed_for
+ * strategy's memory-balanced partition p0 (out_p0, rows of max_stages int32) and mem_ref, the
+ * largest stage peak of the seed's time-balanced partition (out_mem_ref, one per cell). */
+int  gbmw_bmw_setup(const gbmw_layer *layers, int32_t n_layers, const gbmw_env *env, int64_t n_devices,
+                    int32_t n_cells, const int64_t *pp_degree, const int64_t *micro_batch, const int32_t *n_micro,
+                    double budget, int32_t max_stages, int32_t n_threads, int32_t *out_p0, double *out_mem_ref);
 /* The same on the device of ctx: one warp per cell. */
 int  gbmw_seed_partitions_device(gbmw_ctx *ctx, const gbmw_layer *layers, int32_t n_layers, const gbmw_env *env,
                                  int64_t n_devices, int32_t n_cells, const int64_t *pp_degree,

@@ -20,6 +20,7 @@ from typing import Callable, Sequence
 import numpy as np
 
 from . import _native
+from . import dpsearch as _dps
 from .costs import EvalContext, StageCost
 from .strategies import DP, SDP, TP, ParallelStrategy
 
@@ -174,7 +175,9 @@ def evaluate_partition(model, partition: PipelinePartition, per_layer_strategies
     if len(per_layer_strategies) != model.num_layers:
         raise ValueError("need one strategy per model layer")
     sizes = np.array(partition.stage_sizes, dtype=np.int32)
-    strats = _native.strategies_array(per_layer_strategies)
+    strats = _dps.plan_records(per_layer_strategies)    # a searched plan: records by index
+    if strats is None:
+        strats = _native.strategies_array(per_layer_strategies)
     out = np.zeros(3 * len(sizes), dtype=np.float64)
     layers = _layers(model, ctx.profile)
     env = _env(ctx)
@@ -368,29 +371,30 @@ def _run_trajectories(model, ctx, trajs: list[_Trajectory], search, microbatch_p
     cluster = ctx.cluster
     n_dev, budget, L = cluster.n_devices, cluster.mem_budget_bytes, model.num_layers
 
-    def setup(t):
-        n_micro_seed = microbatch_policy(t.batch, t.pp)
-        micro_seed = t.batch // n_micro_seed
-        # _seed_for (balance.py:471-488) already balances the chosen seed's memory: that is p0
-        seed_list, p0 = _seed_and_partition(model, ctx, n_dev, t.pp, micro_seed, n_micro_seed)
-        p_time = init_partition_time_balanced(model, t.pp, seed_list, micro_seed, n_micro_seed, ctx)
-        mem_ref = max(sc.peak_mem_bytes for sc in
-                      evaluate_partition(model, p_time, seed_list, micro_seed, n_micro_seed, ctx))
-        return mem_ref, p0
-
     multi = [t for t in trajs if not t.single]
-    # independent per trajectory, native hill climbs (the GIL is released): on host threads
-    if len(multi) > 1:
-        from concurrent.futures import ThreadPoolExecutor
+    # every trajectory's set-up (_seed_for, its memory-balanced p0, the time-balanced p_t and
+    # mem_ref = max stage peak of p_t) in one native call over host threads
+    if multi:
         import os
-        with ThreadPoolExecutor(max_workers=max(1, min(len(multi), len(os.sched_getaffinity(0)) // 2))) as ex:
-            setups = list(ex.map(setup, multi))
-    else:
-        setups = [setup(t) for t in multi]
-    for t, (mem_ref, p0) in zip(multi, setups):
-        t.mem_ref = mem_ref
-        t.queue = [p0]
-        t.visited = {p0.stage_sizes}
+        pp = np.array([t.pp for t in multi], dtype=np.int64)
+        nm = np.array([microbatch_policy(t.batch, t.pp) for t in multi], dtype=np.int32)
+        micro = np.array([t.batch // int(m) for t, m in zip(multi, nm)], dtype=np.int64)
+        width = int(pp.max())
+        p0s = np.zeros((len(multi), width), dtype=np.int32)
+        mem_refs = np.zeros(len(multi), dtype=np.float64)
+        layers = _layers(model, ctx.profile)
+        env = _env(ctx)
+        threads = max(1, min(len(multi), len(os.sched_getaffinity(0)) // 2))
+        rc = _native.lib().gbmw_bmw_setup(layers.ctypes.data, len(layers), env.ctypes.data, int(n_dev), len(multi),
+                                          pp.ctypes.data, micro.ctypes.data, nm.ctypes.data, float(budget), width,
+                                          threads, p0s.ctypes.data, mem_refs.ctypes.data)
+        if rc != _native.OK:
+            _planner_error(rc)
+        for i, t in enumerate(multi):
+            p0 = PipelinePartition(tuple(p0s[i, :t.pp].tolist()))
+            t.mem_ref = float(mem_refs[i])
+            t.queue = [p0]
+            t.visited = {p0.stage_sizes}
     for t in trajs:
         if t.single:
             t.queue = [PipelinePartition((L,))]

@@ -521,3 +521,63 @@ extern "C" int gbmw_seed_partitions(const gbmw_layer *layers, int32_t n_layers, 
     if (bad < n_cells) return perr(codes[bad], msgs[bad]);
     return GBMW_OK;
 }
+
+// The set-up of Algorithm 2's trajectories (balance.py:366-384 as _run_trajectories runs it):
+// per (pp_degree, micro_batch, n_micro) cell the _seed_for strategy and its memory-balanced
+// partition p0 (the trajectory's first partition), the time-balanced partition p_t of the
+// same uniform seed list, and mem_ref = max stage peak of p_t (evaluate_partition), on up to
+// n_threads host threads.  out_p0: n_cells rows of max_stages int32.  Errors: the first
+// failing cell's, as the sequential set-up would raise it.
+extern "C" int gbmw_bmw_setup(const gbmw_layer *layers, int32_t n_layers, const gbmw_env *env, int64_t n_devices,
+                              int32_t n_cells, const int64_t *pp_degree, const int64_t *micro_batch,
+                              const int32_t *n_micro, double budget, int32_t max_stages, int32_t n_threads,
+                              int32_t *out_p0, double *out_mem_ref) {
+    if (!layers || !env || !pp_degree || !micro_batch || !n_micro || !out_p0 || !out_mem_ref || n_cells < 0 ||
+        max_stages < 1 || n_layers < 1)
+        return perr(GBMW_EINVAL, "bad arguments");
+    for (int i = 0; i < n_cells; ++i)
+        if (pp_degree[i] < 1 || pp_degree[i] > max_stages || pp_degree[i] > n_layers)
+            return perr(GBMW_EINVAL, "pp_degree out of range");
+    std::atomic<int> next{0}, first_bad{n_cells};
+    std::vector<int> codes(n_cells, GBMW_OK);
+    std::vector<std::string> msgs(n_cells);
+    auto work = [&]() {
+        std::vector<gbmw_strategy> per_layer((size_t)n_layers);
+        std::vector<int32_t> pt((size_t)max_stages);
+        std::vector<double> costs(3 * (size_t)max_stages);
+        while (true) {
+            const int i = next.fetch_add(1);
+            if (i >= n_cells) return;
+            const int P = (int)pp_degree[i];
+            gbmw_strategy seed;
+            int rc = gbmw_seed_for(layers, n_layers, env, n_devices, P, micro_batch[i], n_micro[i], budget, &seed,
+                                   out_p0 + (size_t)i * max_stages);
+            if (!rc) {
+                std::fill(per_layer.begin(), per_layer.end(), seed);
+                rc = gbmw_init_partition(layers, n_layers, per_layer.data(), P, env, micro_batch[i], n_micro[i], 1,
+                                         pt.data());
+            }
+            if (!rc)
+                rc = gbmw_partition_costs(layers, n_layers, per_layer.data(), pt.data(), P, env, micro_batch[i],
+                                          n_micro[i], costs.data());
+            if (!rc) {
+                double m = costs[2];                     // max(sc.peak_mem_bytes for sc in ...)
+                for (int s = 1; s < P; ++s) m = costs[3 * s + 2] > m ? costs[3 * s + 2] : m;
+                out_mem_ref[i] = m;
+            } else {
+                codes[i] = rc;
+                msgs[i] = g_perr;
+                int cur = first_bad.load();
+                while (i < cur && !first_bad.compare_exchange_weak(cur, i)) {}
+            }
+        }
+    };
+    const int nt = std::max(1, std::min<int>(n_threads, n_cells));
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nt; ++t) pool.emplace_back(work);
+    work();
+    for (auto &th : pool) th.join();
+    const int bad = first_bad.load();
+    if (bad < n_cells) return perr(codes[bad], msgs[bad]);
+    return GBMW_OK;
+}

@@ -97,6 +97,27 @@ def _strategies_array_cached(strategies, strat_list):
     return hit[1]
 
 
+# per-layer strategy tuples of the plans the searches returned -> (the tuple, its strategy
+# table, indices into it): evaluate_partition gathers their C records from the table's cached
+# records instead of rebuilding them object by object (Algorithm 2 re-costs every plan)
+_plan_records: dict = {}
+
+
+def plan_records_register(plan: tuple, strats: tuple, idx: list):
+    if len(_plan_records) > 4096:
+        _plan_records.clear()
+    _plan_records[id(plan)] = (plan, strats, idx)
+
+
+def plan_records(per_layer_strategies):
+    """STRATEGY_DT records of a plan tuple registered by a search, or None."""
+    hit = _plan_records.get(id(per_layer_strategies))
+    if hit is None or hit[0] is not per_layer_strategies:
+        return None
+    _, strats, idx = hit
+    return _strategies_array_cached(strats, strats)[np.asarray(idx, dtype=np.intp)]
+
+
 class _Marshal:
     """Deduplicating builder of the flat layer / strategy / env tables of a batch."""
 

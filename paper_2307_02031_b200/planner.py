@@ -21,6 +21,7 @@ from typing import Any, Sequence
 
 import numpy as np
 
+from . import dpsearch as _dps
 from .balance import (
     BalanceReport,
     PipelinePartition,
@@ -296,8 +297,9 @@ def _slices_finish(sb: _SlicedBatch, native, defer_errors=False):
         idx = plan_l[plan_off[r0]:plan_off[r1]]
         # pipeline_cost (costs.py:355-362) on the same floats in the same order
         cost = (m - 1) * max(ns) + sum(ts)
-        out.append(SearchOutcome(cost=cost, strategies=tuple([strats[j] for j in idx]), stage_costs=costs,
-                                 n_micro=m))
+        plan = tuple([strats[j] for j in idx])
+        _dps.plan_records_register(plan, strats, idx)
+        out.append(SearchOutcome(cost=cost, strategies=plan, stage_costs=costs, n_micro=m))
     return out
 
 

@@ -149,3 +149,53 @@ def test_gc_pause_restores_process_state_across_threads():
 
     assert nested() is False and not gc.isenabled()      # a caller's own disabled GC stays disabled
     gc.enable()
+
+
+def test_plan_records_gather_equals_rebuilt_records():
+    """evaluate_partition's records of a searched plan (gathered from the strategy table by
+    index) are byte-identical to the records rebuilt from the strategy objects, and an
+    unregistered or different sequence is not served from the registry."""
+    from paper_2307_02031_b200 import _native, dpsearch
+    from paper_2307_02031_b200.strategies import enumerate_pruned
+    strats = tuple(enumerate_pruned(64, 4))
+    idx = [(7 * i) % len(strats) for i in range(24)]
+    plan = tuple(strats[j] for j in idx)
+    assert dpsearch.plan_records(plan) is None
+    dpsearch.plan_records_register(plan, strats, idx)
+    got = dpsearch.plan_records(plan)
+    assert got.tobytes() == _native.strategies_array(list(plan)).tobytes()
+    assert dpsearch.plan_records(tuple(plan)[:-1]) is None
+    assert dpsearch.plan_records(list(plan)) is None
+
+
+def test_bmw_setup_native_equals_sequential_setup():
+    """gbmw_bmw_setup (Algorithm 2's trajectory set-up on host threads) against the
+    sequential composition of the single-cell calls it replaces: _seed_for's memory-balanced
+    p0, and mem_ref = max stage peak of the seed's time-balanced partition."""
+    import os
+    from paper_2307_02031_b200.balance import (_env, _layers, _seed_and_partition, default_microbatch_policy,
+                                               evaluate_partition, init_partition_time_balanced)
+    from paper_2307_02031_b200.strategies import candidate_pp_degrees
+    for name in ("gpt", "swin", "vit", "t5"):
+        ctx = W.config(name)
+        model, cl = ctx.model, ctx.cluster
+        cells = [(p, b) for p in candidate_pp_degrees(cl.n_devices) if 2 <= p <= model.num_layers
+                 for b in (8, 24, 64, 136)]
+        pp = np.array([p for p, _ in cells], dtype=np.int64)
+        nm = np.array([default_microbatch_policy(b, p) for p, b in cells], dtype=np.int32)
+        micro = np.array([b // int(m) for (_, b), m in zip(cells, nm)], dtype=np.int64)
+        width = int(pp.max())
+        p0s = np.zeros((len(cells), width), dtype=np.int32)
+        refs = np.zeros(len(cells))
+        layers, env = _layers(model, ctx.profile), _env(ctx)
+        rc = _native.lib().gbmw_bmw_setup(layers.ctypes.data, len(layers), env.ctypes.data, cl.n_devices, len(cells),
+                                          pp.ctypes.data, micro.ctypes.data, nm.ctypes.data,
+                                          float(cl.mem_budget_bytes), width, min(4, os.cpu_count() or 1),
+                                          p0s.ctypes.data, refs.ctypes.data)
+        assert rc == _native.OK
+        for i, (p, b) in enumerate(cells):
+            seed, p0 = _seed_and_partition(model, ctx, cl.n_devices, p, int(micro[i]), int(nm[i]))
+            assert tuple(p0s[i, :p].tolist()) == p0.stage_sizes
+            pt = init_partition_time_balanced(model, p, seed, int(micro[i]), int(nm[i]), ctx)
+            ref = max(sc.peak_mem_bytes for sc in evaluate_partition(model, pt, seed, int(micro[i]), int(nm[i]), ctx))
+            assert refs[i] == ref
