@@ -233,6 +233,14 @@ int  gbmw_batch_destroy(gbmw_batch *batch);
 int  gbmw_partition_costs(const gbmw_layer *layers, int32_t n_layers, const gbmw_strategy *per_layer,
                           const int32_t *sizes, int32_t n_stages, const gbmw_env *env,
                           int64_t micro_batch, int32_t n_micro, double *out);
+/* gbmw_partition_costs for n_items (partition, per-layer strategies, micro-batch) items on up to
+ * n_threads host threads (the adjusted partitions of one Algorithm-2 round, balance.py:420-424):
+ * per_layer n_items x n_layers records, sizes n_items x max_stages (n_stages[i] used),
+ * out n_items x 3 * max_stages. */
+int  gbmw_partition_costs_batch(const gbmw_layer *layers, int32_t n_layers, const gbmw_strategy *per_layer,
+                                const int32_t *sizes, const int32_t *n_stages, int32_t max_stages,
+                                const gbmw_env *env, const int64_t *micro_batch, const int32_t *n_micro,
+                                int32_t n_items, int32_t n_threads, double *out);
 /* _init_partition (balance.py:180-236): objective 0 = memory-balanced, 1 = time-balanced. */
 int  gbmw_init_partition(const gbmw_layer *layers, int32_t n_layers, const gbmw_strategy *per_layer,
                          int32_t n_stages, const gbmw_env *env, int64_t micro_batch, int32_t n_micro,

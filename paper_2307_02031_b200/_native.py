@@ -73,7 +73,7 @@ EXPORTS = (
     "gbmw_last_error", "gbmw_last_error_global", "gbmw_ctx_stream", "gbmw_enumerate", "gbmw_layer_cost",
     "gbmw_transform_cost", "gbmw_comm_breakdown", "gbmw_cost_tables", "gbmw_search_batch", "gbmw_batch_create",
     "gbmw_batch_run", "gbmw_batch_fetch", "gbmw_batch_timing", "gbmw_ctx_last_timing", "gbmw_batch_destroy",
-    "gbmw_partition_costs", "gbmw_init_partition", "gbmw_seed_for", "gbmw_seed_partitions", "gbmw_seed_partitions_device", "gbmw_bmw_setup", "gbmw_py_sum", "gbmw_planner_last_error",
+    "gbmw_partition_costs", "gbmw_init_partition", "gbmw_seed_for", "gbmw_seed_partitions", "gbmw_seed_partitions_device", "gbmw_bmw_setup", "gbmw_partition_costs_batch", "gbmw_py_sum", "gbmw_planner_last_error",
     "gbmw_set_sum_semantics", "gbmw_sum_semantics", "gbmw_brute_force",
 )
 
@@ -122,6 +122,7 @@ def lib() -> ctypes.CDLL:
             L.gbmw_seed_partitions.argtypes = [vp, i32, vp, i64, i32, vp, vp, vp, ctypes.c_double, i32, i32, vp]
             L.gbmw_seed_partitions_device.argtypes = [vp, vp, i32, vp, i64, i32, vp, vp, vp, ctypes.c_double, i32, vp]
             L.gbmw_bmw_setup.argtypes = [vp, i32, vp, i64, i32, vp, vp, vp, ctypes.c_double, i32, i32, vp, vp]
+            L.gbmw_partition_costs_batch.argtypes = [vp, i32, vp, vp, vp, i32, vp, vp, vp, i32, i32, vp]
             L.gbmw_py_sum.argtypes = [vp, i32]
             L.gbmw_py_sum.restype = ctypes.c_double
             L.gbmw_planner_last_error.restype = ctypes.c_char_p

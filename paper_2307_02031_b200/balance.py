@@ -410,6 +410,9 @@ def _run_trajectories(model, ctx, trajs: list[_Trajectory], search, microbatch_p
             parts.append(t.queue.pop(0))
         calls = [(budget, partition_layers(model, p), n_dev, t.batch, t.pp) for t, p in zip(active, parts)]
         outcomes = batched(calls) if batched is not None else [search(*c) for c in calls]
+        # pass 1: each trajectory's statistics and adjusted partition; the adjusted partitions
+        # of the round are then costed in one native call (independent per trajectory)
+        pending = []
         for t, part, outcome in zip(active, parts, outcomes):
             record = {"batch_size": t.batch, "pp_degree": t.pp, "partition": list(part.stage_sizes),
                       "iteration": t.iterations, "cost": outcome.cost, "accepted": False, "proposed": None}
@@ -420,18 +423,60 @@ def _run_trajectories(model, ctx, trajs: list[_Trajectory], search, microbatch_p
             if t.single:
                 t.events.append((part, outcome, record, True))
                 continue
-            c_max_prev = max(report.stage_times)
             adjusted = adjust_partition(part, outcome.stage_costs)
             if adjusted.stage_sizes != part.stage_sizes:
-                micro = t.batch // outcome.n_micro
-                costs_adj = evaluate_partition(model, adjusted, outcome.strategies, micro, outcome.n_micro, ctx)
-                ok = validate_partition(adjusted, costs_adj, c_max_prev, budget, t.mem_ref)
-                record["proposed"] = list(adjusted.stage_sizes)
-                record["accepted"] = bool(ok and adjusted.stage_sizes not in t.visited)
-                if ok and adjusted.stage_sizes not in t.visited:
-                    t.visited.add(adjusted.stage_sizes)
-                    t.queue.append(adjusted)
+                pending.append((t, adjusted, outcome, record, max(report.stage_times)))
             t.events.append((part, outcome, record, True))
+        # pass 2: validation in trajectory order (balance.py:420-431)
+        for (t, adjusted, outcome, record, c_max_prev), costs_adj in zip(pending, _costs_batch(model, ctx, pending)):
+            ok = validate_partition(adjusted, costs_adj, c_max_prev, budget, t.mem_ref)
+            record["proposed"] = list(adjusted.stage_sizes)
+            record["accepted"] = bool(ok and adjusted.stage_sizes not in t.visited)
+            if ok and adjusted.stage_sizes not in t.visited:
+                t.visited.add(adjusted.stage_sizes)
+                t.queue.append(adjusted)
+
+
+def _costs_batch(model, ctx, pending) -> list[list[StageCost]]:
+    """evaluate_partition of every (trajectory, adjusted partition, outcome) of a round in one
+    native call (gbmw_partition_costs_batch)."""
+    n = len(pending)
+    if n == 0:
+        return []
+    if n == 1:
+        t, adjusted, outcome, _, _ = pending[0]
+        return [evaluate_partition(model, adjusted, outcome.strategies, t.batch // outcome.n_micro,
+                                   outcome.n_micro, ctx)]
+    L = model.num_layers
+    recs = []
+    for t, adjusted, outcome, _, _ in pending:
+        if len(outcome.strategies) != L:
+            raise ValueError("need one strategy per model layer")
+        r = _dps.plan_records(outcome.strategies)
+        recs.append(r if r is not None else _native.strategies_array(outcome.strategies))
+    per_layer = np.concatenate(recs)
+    width = max(len(a.stage_sizes) for _, a, _, _, _ in pending)
+    sizes = np.zeros((n, width), dtype=np.int32)
+    n_st = np.zeros(n, dtype=np.int32)
+    for i, (_, a, _, _, _) in enumerate(pending):
+        sizes[i, :len(a.stage_sizes)] = a.stage_sizes
+        n_st[i] = len(a.stage_sizes)
+    micro = np.array([t.batch // o.n_micro for t, _, o, _, _ in pending], dtype=np.int64)
+    nm = np.array([o.n_micro for _, _, o, _, _ in pending], dtype=np.int32)
+    out = np.zeros((n, 3 * width), dtype=np.float64)
+    layers = _layers(model, ctx.profile)
+    env = _env(ctx)
+    # one thread: a round has a few dozen items of ~15 us each; spawning threads per round
+    # cost more than it saved (measured: swin-bmw Algorithm 2 host time 5.0 -> 6.3 ms)
+    threads = 1
+    rc = _native.lib().gbmw_partition_costs_batch(layers.ctypes.data, len(layers), per_layer.ctypes.data,
+                                                  sizes.ctypes.data, n_st.ctypes.data, width, env.ctypes.data,
+                                                  micro.ctypes.data, nm.ctypes.data, n, threads, out.ctypes.data)
+    if rc != _native.OK:
+        _planner_error(rc)
+    o = out.tolist()
+    return [[StageCost(o[i][3 * s], o[i][3 * s + 1], o[i][3 * s + 2]) for s in range(int(n_st[i]))]
+            for i in range(n)]
 
 
 def _replay(result: BiObjectiveResult, trajs: list[_Trajectory]):

@@ -522,6 +522,48 @@ extern "C" int gbmw_seed_partitions(const gbmw_layer *layers, int32_t n_layers, 
     return GBMW_OK;
 }
 
+// gbmw_partition_costs for many (partition, per-layer strategies, micro-batch) items at once
+// (Algorithm 2 re-costs the adjusted partition of every trajectory of a round,
+// balance.py:420-424), on up to n_threads host threads.  per_layer: n_items rows of n_layers
+// records; sizes: n_items rows of max_stages int32 (n_stages[i] used); out: n_items rows of
+// 3 * max_stages doubles.  Errors: the first failing item's.
+extern "C" int gbmw_partition_costs_batch(const gbmw_layer *layers, int32_t n_layers, const gbmw_strategy *per_layer,
+                                          const int32_t *sizes, const int32_t *n_stages, int32_t max_stages,
+                                          const gbmw_env *env, const int64_t *micro_batch, const int32_t *n_micro,
+                                          int32_t n_items, int32_t n_threads, double *out) {
+    if (!layers || !per_layer || !sizes || !n_stages || !env || !micro_batch || !n_micro || !out || n_items < 0 ||
+        max_stages < 1 || n_layers < 1)
+        return perr(GBMW_EINVAL, "bad arguments");
+    std::atomic<int> next{0}, first_bad{n_items};
+    std::vector<int> codes(n_items, GBMW_OK);
+    std::vector<std::string> msgs(n_items);
+    auto work = [&]() {
+        while (true) {
+            const int i = next.fetch_add(1);
+            if (i >= n_items) return;
+            const int rc = (n_stages[i] < 1 || n_stages[i] > max_stages)
+                               ? perr(GBMW_EINVAL, "bad arguments")
+                               : gbmw_partition_costs(layers, n_layers, per_layer + (size_t)i * n_layers,
+                                                      sizes + (size_t)i * max_stages, n_stages[i], env,
+                                                      micro_batch[i], n_micro[i], out + (size_t)i * 3 * max_stages);
+            if (rc) {
+                codes[i] = rc;
+                msgs[i] = g_perr;
+                int cur = first_bad.load();
+                while (i < cur && !first_bad.compare_exchange_weak(cur, i)) {}
+            }
+        }
+    };
+    const int nt = std::max(1, std::min<int>(n_threads, n_items));
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nt; ++t) pool.emplace_back(work);
+    work();
+    for (auto &th : pool) th.join();
+    const int bad = first_bad.load();
+    if (bad < n_items) return perr(codes[bad], msgs[bad]);
+    return GBMW_OK;
+}
+
 // The set-up of Algorithm 2's trajectories (balance.py:366-384 as _run_trajectories runs it):
 // per (pp_degree, micro_batch, n_micro) cell the _seed_for strategy and its memory-balanced
 // partition p0 (the trajectory's first partition), the time-balanced partition p_t of the
