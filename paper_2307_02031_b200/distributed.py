@@ -33,6 +33,11 @@ def local_winner(times: np.ndarray, feasible: np.ndarray, global_index: np.ndarr
     # the first of lexsort((index, t)) in O(n): the least time (NaN after everything), then
     # the least index among its ties
     gi = np.asarray(global_index)
+    m = t.min()
+    if not np.isnan(m):                  # no NaN anywhere (the usual case): one pass for the ties
+        cand = np.flatnonzero(t == m)
+        best = cand[0] if len(cand) == 1 else cand[np.argmin(gi[cand])]
+        return np.array([np.float64(t[best]).view(np.int64), int(gi[best])], dtype=np.int64)
     ok = ~np.isnan(t)
     pool = np.flatnonzero(ok) if ok.any() else np.arange(len(t))
     tp = t[pool]
