@@ -1135,7 +1135,7 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
                 cudaDeviceGetStreamPriorityRange(&lo_pri, &hi_pri);
                 // deep bands above shallow ones; among deep bands the wider classes (their
                 // steps are the longest) above the main stream's K <= 4 band
-                const int pri = (g < kStepVGroups && g % kBands == 0) ? hi_pri : lo_pri;
+                const int pri = (g < kStepVGroups && !shallow_group(g)) ? hi_pri : lo_pri;
                 if (cudaStreamCreateWithPriority(&ctx->aux[g], cudaStreamNonBlocking, pri) != cudaSuccess ||
                     cudaEventCreateWithFlags(&ctx->join[g], cudaEventDisableTiming) != cudaSuccess)
                     return cuda_fail(ctx, (int)cudaGetLastError(), "aux stream");
@@ -1229,7 +1229,7 @@ int run_chunks(gbmw_ctx *ctx, gbmw_batch *b, bool tables_only) {
                 const int lo = c.group_lo[g], n = c.group_lo[g + 1] - lo;
                 if (n <= 0) continue;
                 const ChunkArgs sub = group_view(a, lo, n, g);
-                if ((rc = launch_sweep(sub, gs[g], (g < kStepVGroups && g % kBands == 1) ? group_ctas : 0))) return cuda_fail(ctx, rc, "K3 launch");
+                if ((rc = launch_sweep(sub, gs[g], shallow_group(g) ? group_ctas : 0))) return cuda_fail(ctx, rc, "K3 launch");
                 if ((rc = launch_finalize(sub, gs[g]))) return cuda_fail(ctx, rc, "K4 launch");
                 c.launches += 4;
             }

@@ -59,14 +59,23 @@ inline int step_group(int K) { return K <= 4 ? 0 : (K <= 8 ? 1 : 2); }
 // Each class-count group is split into bands by depth (deep problems first); every band
 // has its own K2 launches on its own stream, so the many short launches of deep problems
 // overlap the few wide launches of shallow ones.
-constexpr int kBands = 2;
-constexpr int kDeepUnits = 16;       // band 0: more units than this
+#ifndef GBMW_BANDS
+#define GBMW_BANDS 2
+#endif
+constexpr int kBands = GBMW_BANDS;   // 2: deep / shallow; 3: very deep / deep / shallow
+constexpr int kDeepUnits = 16;       // the deep bands: more units than this
+constexpr int kVeryDeepUnits = 48;   // with 3 bands, band 0: more units than this
 constexpr int kStepVGroups = kStepGroups * kBands;
 // problems with approx_prev (collapsed state, dpsearch.py:306-375) form their own group
 constexpr int kApproxGroup = kStepVGroups;
 constexpr int kNumGroups = kStepVGroups + 1;
+inline int problem_band(int U) {
+    if (kBands == 2) return U > kDeepUnits ? 0 : 1;
+    return U > kVeryDeepUnits ? 0 : (U > kDeepUnits ? 1 : 2);
+}
+inline bool shallow_group(int g) { return g < kStepVGroups && g % kBands == kBands - 1; }
 inline int problem_group(int K, int flags, int U) {
-    return (flags & GBMW_APPROX) ? kApproxGroup : step_group(K) * kBands + (U > kDeepUnits ? 0 : 1);
+    return (flags & GBMW_APPROX) ? kApproxGroup : step_group(K) * kBands + problem_band(U);
 }
 
 struct Cell {
