@@ -104,14 +104,14 @@ __device__ __forceinline__ bool lex3_less(double t1, double f1, int k1, double t
 // segment leaves the result in each of its lanes.  e < 0: no row (+inf).
 // key = 2 * argmin position + (1 if the argmin's source row is a change point of its
 // column of B_{u-1}: the path behind the argmin changes there).
-template <int KT, bool FIRST, bool GUARD, class SH>
+template <int KT, bool FIRST, bool GUARD, class SH, int IBW = 0>
 __device__ __forceinline__ void eval_row(const ChunkArgs &a, const SH &sh, int u, int e, int L, int l,
                                          double *bt, double *bf, int *bk) {
     const int S = sh.S, K = GUARD ? sh.K : KT;
     const int n_e = sh.n_e, lo_prev = FIRST ? 0 : sh.lo_prev;
     // sources in flight per lane: as many as the register budget holds without spilling an
     // in-flight load (a spilled load result serialises the loads)
-    constexpr int IB = (KT <= 4) ? kStepIB : kStepIBWide;
+    constexpr int IB = (KT <= 4) ? kStepIB : (IBW > 0 ? IBW : kStepIBWide);
     const TFCell *bin = a.TF[(u - 1) & 1] + sh.b_off;
     const int2 *rm = a.rmap + sh.rm_prev;
     const uint32_t *fin = a.chg[(u - 1) & 1] + sh.f_off;
@@ -392,7 +392,7 @@ static_assert(max_tile_rounds() <= kK2RoundsPerSlot, "round list capacity per ti
 // Phase B, one round of one tile by one warp: evaluate its entries, compare each with the
 // previous entry (unchanged columns keep change bit 0), store (t, f, argmin) of the
 // entries where some column changes and of the tile's first entry (the anchor).
-template <int KT, bool FIRST, bool GUARD>
+template <int KT, bool FIRST, bool GUARD, int IBW = 0>
 __device__ __forceinline__ void eval_round(const ChunkArgs &a, const TileCtx &t, int u, int r, int lane) {
     const int K = GUARD ? t.K : KT;
     const int n_e = t.n_e, n = t.n_ent;
@@ -414,7 +414,7 @@ __device__ __forceinline__ void eval_round(const ChunkArgs &a, const TileCtx &t,
     const int e = have ? t.r_base + (int)t.erow[j] : -1;
     double bt[KT], bf[KT];
     int bk[KT];
-    eval_row<KT, FIRST, GUARD>(a, t, u, e, L, l, bt, bf, bk);
+    eval_row<KT, FIRST, GUARD, TileCtx, IBW>(a, t, u, e, L, l, bt, bf, bk);
     unsigned chg = 0u;
 #pragma unroll
     for (int kk = 0; kk < KT; ++kk) {
@@ -746,6 +746,11 @@ __global__ void __launch_bounds__(kStepThreads, GROUP <= 1 ? 3 : 1)
 // tiles (the deep bands' tail, where the step chain, not the throughput, bounds the pass):
 // warp 0 classifies the tile into shared memory, the CTA's warps share its rounds, warp 0
 // finishes it.  No hand-off through global memory and no second kernel per step.
+#ifndef GBMW_TILE_IB_WIDE
+#define GBMW_TILE_IB_WIDE 1
+#endif
+constexpr int kTileIBWide = GBMW_TILE_IB_WIDE;   // K2t: sources in flight per lane for K >= 5 (2, 3: no spills, measured no faster)
+
 template <int GROUP, bool FIRST, int kTileWarps>
 __global__ void __launch_bounds__(32 * kTileWarps)
     k_dp_tile(ChunkArgs a, int u, const int4 *items, const int64_t *count, int tl_id) {
@@ -780,7 +785,7 @@ __global__ void __launch_bounds__(32 * kTileWarps)
         const int n = s_n, K = t.K;
         const int rounds = tile_rounds(n);
         for (int r = warp; r < rounds; r += kTileWarps) {
-#define GBMW_K2_EVAL(KT, G) eval_round<KT, FIRST, G>(a, t, u, r, lane)
+#define GBMW_K2_EVAL(KT, G) eval_round<KT, FIRST, G, kTileIBWide>(a, t, u, r, lane)
             GBMW_K2_DISPATCH(GBMW_K2_EVAL)
 #undef GBMW_K2_EVAL
         }
