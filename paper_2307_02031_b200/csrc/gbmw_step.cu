@@ -258,88 +258,103 @@ __device__ __forceinline__ unsigned window_segments(unsigned long long v, int x0
 // Phase A, one warp per tile: the breakpoints of its 32 groups (lane g = group g) from the
 // change bits of the sources whose window over the tile changes (change summaries), then
 // the tile's entries in row order; its first live row is always an entry (the anchor of
-// the row map).  Returns the entry count.
+// the row map).  In three steps so that K2t can spread the middle one over its warps:
+// (A1) the active sources, (A2) each group's breakpoints from a subset of them, (A3) the
+// entries from the groups' breakpoint masks.
+
+// A1: sources whose window [r_base - w, r_base + 1023 - w] holds a change, into alist
 template <bool FIRST>
-__device__ __forceinline__ int classify_tile(const ChunkArgs &a, TileCtx &t, uint16_t *alist, uint16_t *goff, int u,
-                                             int lane) {
-    const int lo = t.lo, hi = t.hi, S = t.S, lo_prev = t.lo_prev;
-    const int r_base = t.r_base;
-    // sources whose window [r_base - w, r_base + 1023 - w] holds a change
+__device__ __forceinline__ int active_sources(const ChunkArgs &a, const TileCtx &t, uint16_t *alist, int u, int lane) {
+    const int S = t.S, lo_prev = t.lo_prev, r_base = t.r_base;
     int na = 0;
-    {
-        const int ns = (int)sum_words(t.n_e);
-        const uint32_t *sum = a.chg[(u - 1) & 1] + t.f_off + (int64_t)t.K * t.nw;
-        for (int n0 = 0; n0 < S; n0 += 32) {
-            const int n = n0 + lane;
-            bool act = false;
-            if (n < S) {
-                const Cell c = t.cell[n];
-                const int A = r_base - c.w, B = A + kWarpRows - 1;
-                if (FIRST) {
-                    act = c.w >= r_base && c.w < r_base + kWarpRows;    // T_0[., i] turns finite at w_i
-                } else if (B >= lo_prev) {
-                    act = lo_prev >= A;                                 // the column's first finite row
-                    if (!act) {
-                        const int ga = A >> 5, gb = B >> 5;             // 32-row groups [ga, gb]
-                        const uint32_t *sk = sum + (int64_t)c.k * ns;
-                        const uint32_t w0 = __ldg(sk + (ga >> 5)), w1 = __ldg(sk + (gb >> 5));
-                        const uint32_t m0 = w0 & (0xffffffffu << (ga & 31));
-                        const uint32_t m1 = w1 & (0xffffffffu >> (31 - (gb & 31)));
-                        act = ((ga >> 5) == (gb >> 5)) ? (m0 & m1) != 0u : (m0 | m1) != 0u;
-                    }
+    const int ns = (int)sum_words(t.n_e);
+    const uint32_t *sum = a.chg[(u - 1) & 1] + t.f_off + (int64_t)t.K * t.nw;
+    for (int n0 = 0; n0 < S; n0 += 32) {
+        const int n = n0 + lane;
+        bool act = false;
+        if (n < S) {
+            const Cell c = t.cell[n];
+            const int A = r_base - c.w, B = A + kWarpRows - 1;
+            if (FIRST) {
+                act = c.w >= r_base && c.w < r_base + kWarpRows;    // T_0[., i] turns finite at w_i
+            } else if (B >= lo_prev) {
+                act = lo_prev >= A;                                 // the column's first finite row
+                if (!act) {
+                    const int ga = A >> 5, gb = B >> 5;             // 32-row groups [ga, gb]
+                    const uint32_t *sk = sum + (int64_t)c.k * ns;
+                    const uint32_t w0 = __ldg(sk + (ga >> 5)), w1 = __ldg(sk + (gb >> 5));
+                    const uint32_t m0 = w0 & (0xffffffffu << (ga & 31));
+                    const uint32_t m1 = w1 & (0xffffffffu >> (31 - (gb & 31)));
+                    act = ((ga >> 5) == (gb >> 5)) ? (m0 & m1) != 0u : (m0 | m1) != 0u;
                 }
             }
-            const unsigned bal = __ballot_sync(0xffffffffu, act);
-            if (act) alist[na + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)n;
-            na += __popc(bal);
         }
-        __syncwarp();
+        const unsigned bal = __ballot_sync(0xffffffffu, act);
+        if (act) alist[na + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)n;
+        na += __popc(bal);
     }
+    __syncwarp();
+    return na;
+}
+
+// A2: breakpoints of group g = lane from the active sources of batches b0, b0 + bstep, ...
+// (kClassifyIB sources a batch)
+template <bool FIRST>
+__device__ __forceinline__ unsigned group_segs(const ChunkArgs &a, const TileCtx &t, const uint16_t *alist, int na,
+                                               int b0, int bstep, int u, int lane) {
+    const int lo_prev = t.lo_prev;
+    const int r0 = t.r_base + 32 * lane, r1 = r0 + 31;
+    unsigned seg = 0u;
+    if (r1 < t.lo || r0 > t.hi) return seg;              // dead group
+    const uint32_t *fin = a.chg[(u - 1) & 1] + t.f_off;
+    for (int n0 = b0 * kClassifyIB; n0 < na; n0 += bstep * kClassifyIB) {
+        uint32_t w0[kClassifyIB], w1[kClassifyIB];
+        int xs_[kClassifyIB];
+        bool ld[kClassifyIB];
+#pragma unroll
+        for (int b = 0; b < kClassifyIB; ++b) {
+            const int n = n0 + b;
+            const Cell c = t.cell[n < na ? alist[n] : 0];
+            const int xs = r0 - c.w;
+            xs_[b] = xs; w0[b] = 0u; w1[b] = 0u;
+            ld[b] = n < na && (FIRST || xs + 31 >= lo_prev);
+            if (!FIRST && ld[b]) {
+                const int xl = xs < 0 ? 0 : xs;
+                const uint32_t *fl = fin + (int64_t)c.k * t.nw + (xl >> 5);
+                w0[b] = __ldg(fl); w1[b] = __ldg(fl + 1);
+            }
+        }
+#pragma unroll
+        for (int b = 0; b < kClassifyIB; ++b) {
+            if (!ld[b]) continue;
+            const int xs = xs_[b];
+            if (FIRST) {
+                const int j = -xs;                       // T_0[e, i] is finite from e = w_i on
+                seg |= (j >= 0 && j <= 31) ? (1u << j) : 0u;
+            } else {
+                const int xl = xs < 0 ? 0 : xs;
+                const unsigned long long v =
+                    ((unsigned long long)w1[b] << 32 | (unsigned long long)w0[b]) >> (xl & 31);
+                seg |= window_segments((xs < 0) ? (v << (-xs)) : v, xs, lo_prev);
+            }
+        }
+    }
+    return seg;
+}
+
+// A3: a partial group (straddling L_u or H_u) keeps only its live rows; the anchor; the
+// entries in row order.  Returns the entry count.
+__device__ __forceinline__ int tile_entries(TileCtx &t, uint16_t *goff, unsigned seg, int lane) {
+    const int lo = t.lo, hi = t.hi, r_base = t.r_base;
     const int g = lane, r0 = r_base + 32 * g, r1 = r0 + 31;
     const bool dead = r1 < lo || r0 > hi;
     const bool whole = r0 >= lo && r1 <= hi;
     const int f0 = r_base > lo ? r_base : lo;            // first live row of the tile (<= hi)
-    unsigned seg = 0u;
-    // breakpoints of the group from its sources' change bits; a partial group (straddling
-    // L_u or H_u) keeps only its live rows
-    if (!dead) {
-        const uint32_t *fin = a.chg[(u - 1) & 1] + t.f_off;
-        for (int n0 = 0; n0 < na; n0 += kClassifyIB) {
-            uint32_t w0[kClassifyIB], w1[kClassifyIB];
-            int xs_[kClassifyIB];
-            bool ld[kClassifyIB];
-#pragma unroll
-            for (int b = 0; b < kClassifyIB; ++b) {
-                const int n = n0 + b;
-                const Cell c = t.cell[n < na ? alist[n] : 0];
-                const int xs = r0 - c.w;
-                xs_[b] = xs; w0[b] = 0u; w1[b] = 0u;
-                ld[b] = n < na && (FIRST || xs + 31 >= lo_prev);
-                if (!FIRST && ld[b]) {
-                    const int xl = xs < 0 ? 0 : xs;
-                    const uint32_t *fl = fin + (int64_t)c.k * t.nw + (xl >> 5);
-                    w0[b] = __ldg(fl); w1[b] = __ldg(fl + 1);
-                }
-            }
-#pragma unroll
-            for (int b = 0; b < kClassifyIB; ++b) {
-                if (!ld[b]) continue;
-                const int xs = xs_[b];
-                if (FIRST) {
-                    const int j = -xs;                   // T_0[e, i] is finite from e = w_i on
-                    seg |= (j >= 0 && j <= 31) ? (1u << j) : 0u;
-                } else {
-                    const int xl = xs < 0 ? 0 : xs;
-                    const unsigned long long v =
-                        ((unsigned long long)w1[b] << 32 | (unsigned long long)w0[b]) >> (xl & 31);
-                    seg |= window_segments((xs < 0) ? (v << (-xs)) : v, xs, lo_prev);
-                }
-            }
-        }
-        if (!whole) {
-            const int a0 = lo > r0 ? lo - r0 : 0, a1 = hi < r1 ? hi - r0 : 31;
-            seg &= (0xffffffffu >> (31 - a1)) & ~((1u << a0) - 1u);
-        }
+    if (dead) {
+        seg = 0u;
+    } else if (!whole) {
+        const int a0 = lo > r0 ? lo - r0 : 0, a1 = hi < r1 ? hi - r0 : 31;
+        seg &= (0xffffffffu >> (31 - a1)) & ~((1u << a0) - 1u);
     }
     // the anchor: change bits exact unless it is a breakpoint itself
     const bool fbp = __shfl_sync(0xffffffffu, (seg >> ((f0 - r_base) & 31)) & 1u, (f0 - r_base) >> 5) != 0u;
@@ -363,6 +378,13 @@ __device__ __forceinline__ int classify_tile(const ChunkArgs &a, TileCtx &t, uin
     if (lane == 0) { t.n_ent = n; t.first_bp = (f0 == lo || fbp) ? 1 : 0; }
     __syncwarp();
     return n;
+}
+
+template <bool FIRST>
+__device__ __forceinline__ int classify_tile(const ChunkArgs &a, TileCtx &t, uint16_t *alist, uint16_t *goff, int u,
+                                             int lane) {
+    const int na = active_sources<FIRST>(a, t, alist, u, lane);
+    return tile_entries(t, goff, group_segs<FIRST>(a, t, alist, na, 0, 1, u, lane), lane);
 }
 
 // Evaluation rounds of a tile with n entries, E entries per round: round 0 takes entries
@@ -761,7 +783,8 @@ __global__ void __launch_bounds__(32 * kTileWarps)
     __shared__ uint16_t s_echg[kWarpRows];
     __shared__ uint16_t s_alist[kMaxStrats];
     __shared__ uint16_t s_goff[34];
-    __shared__ int s_n;
+    __shared__ unsigned s_seg[32];
+    __shared__ int s_n, s_na;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     TileCtx &t = s_t;
     const int64_t it = blockIdx.x;
@@ -778,7 +801,17 @@ __global__ void __launch_bounds__(32 * kTileWarps)
                 t.erow = s_erow; t.echg = s_echg; t.goff = nullptr;
             }
             __syncwarp();
-            const int n = classify_tile<FIRST>(a, t, s_alist, s_goff, u, lane);
+            const int na = active_sources<FIRST>(a, t, s_alist, u, lane);
+            if (lane == 0) s_na = na;
+            s_seg[lane] = 0u;
+        }
+        __syncthreads();
+        // the groups' breakpoints: the warps take the active sources' batches in turn
+        const unsigned sg = group_segs<FIRST>(a, t, s_alist, s_na, warp, kTileWarps, u, lane);
+        if (sg) atomicOr(&s_seg[lane], sg);
+        __syncthreads();
+        if (warp == 0) {
+            const int n = tile_entries(t, s_goff, s_seg[lane], lane);
             if (lane == 0) { s_n = n; t.goff = s_goff; }
         }
         __syncthreads();
