@@ -1111,15 +1111,30 @@ __global__ void __launch_bounds__(32 * kFinWarps) k_finalize(ChunkArgs a) {
     double bt = GBMW_INF, e_all = 0.0;
     int64_t be = -1;
     int sj = 0;
-    if (lane == 0) {
+    {
+        // the best of the safe bucket and the unsafe (or collapsed-DP) tiles' partials: the
+        // lanes take the tiles in turn, then a butterfly.  "better" (smaller t, ties to the
+        // larger e) is a strict total order on the candidates (their e are distinct; the empty
+        // ones are (inf, -1, 0) alike), so the result is the sequential fold's
         const SweepPartial safe = a.best[q];
         bt = safe.t;
         be = safe.e;
         int bj = safe.j;
-        for (int t = a.ufirst[q]; t < p.n_sweep_tiles; ++t) {   // unsafe (or collapsed-DP) tiles
+        for (int t = a.ufirst[q] + lane; t < p.n_sweep_tiles; t += 32) {
             const SweepPartial sp = a.partials[p.tile_off + t];
             if (cand_better(sp.t, sp.e, bt, be)) { bt = sp.t; be = sp.e; bj = sp.j; }
         }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const double ot = __shfl_xor_sync(0xffffffffu, bt, off);
+            const long long oe = __shfl_xor_sync(0xffffffffu, (long long)be, off);
+            const int oj = __shfl_xor_sync(0xffffffffu, bj, off);
+            if (cand_better(ot, oe, bt, be)) { bt = ot; be = oe; bj = oj; }
+        }
+        sj = bj;
+    }
+    if (lane == 0) {
+        const int bj = sj;
         if (be >= 0 && (p.flags & GBMW_APPROX)) approx_reconstruct(a, p, be, path);
         if (be >= 0 && !(p.flags & GBMW_APPROX) && p.S > 64) backtrack(a, p, be, bj, path);
         sj = bj;
